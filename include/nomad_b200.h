@@ -1,0 +1,231 @@
+/*
+ * nomad_b200.h — C-ABI of the B200-native NOMAD Projection engine
+ * (libnomad_b200.so, sm_100a). Plain pointers and sizes only.
+ *
+ * The reference (/root/reference/proj/include/nomad) is a header-only C++20
+ * library of free functions; it has no FFI layer. Each entry point below
+ * replaces one reference function (cited as file:line) with the same
+ * argument meaning; the C++ shim include/nomad_b200/nomad_b200.hpp re-exposes
+ * the reference signatures on top of this ABI, and the Python package
+ * paper_2505_15511_b200 binds it with ctypes.
+ *
+ * Conventions
+ *  - Return value: 0 on success, else 1 + ErrorKind in the reference's enum
+ *    order (error.hpp:25-36): 1 Io, 2 Dimension, 3 Validation, 4 Schema,
+ *    5 Parameter, 6 Config, 7 Degenerate, 8 Divergence, 9 Size, 10 Internal.
+ *    CUDA / NCCL failures map to Internal. nomad_b200_last_error() returns the
+ *    message (thread-local), e.g. the divergence text of optimizer.hpp:222-225.
+ *  - Buffers carry a location flag: NOMAD_B200_HOST (pageable or pinned host
+ *    memory) or NOMAD_B200_DEVICE (memory on the context's device, e.g. a
+ *    torch CUDA tensor). Device inputs are used in place (no copy).
+ *  - Calls are blocking and synchronous w.r.t. the caller (results are ready
+ *    on return). A context is not thread-safe; distinct contexts are
+ *    independent. No host threads are spawned per epoch.
+ *  - There is no CPU fallback: every numeric stage runs in sm_100a kernels.
+ */
+#ifndef NOMAD_B200_H_
+#define NOMAD_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NOMAD_B200_ABI_VERSION 1
+
+enum nomad_b200_status {
+  NOMAD_B200_OK = 0,
+  NOMAD_B200_ERR_IO = 1,
+  NOMAD_B200_ERR_DIMENSION = 2,
+  NOMAD_B200_ERR_VALIDATION = 3,
+  NOMAD_B200_ERR_SCHEMA = 4,
+  NOMAD_B200_ERR_PARAMETER = 5,
+  NOMAD_B200_ERR_CONFIG = 6,
+  NOMAD_B200_ERR_DEGENERATE = 7,
+  NOMAD_B200_ERR_DIVERGENCE = 8,
+  NOMAD_B200_ERR_SIZE = 9,
+  NOMAD_B200_ERR_INTERNAL = 10
+};
+
+enum nomad_b200_location { NOMAD_B200_HOST = 0, NOMAD_B200_DEVICE = 1 };
+
+/* SGD execution mode of the epoch loop (optimizer.hpp:232-307). */
+enum nomad_b200_sgd_mode {
+  /* Deterministic replay: the reference's per-worker mt19937_64 draw stream
+   * (rng.hpp:42-84, optimizer.hpp:254-255, :284-285) scheduled into
+   * conflict-free wavefront levels; fp64 in the reference's op order, no FMA,
+   * non-atomic. Layouts are bit-identical to the reference. */
+  NOMAD_B200_SGD_REPLAY = 0,
+  /* Throughput mode: counter-based (Philox4x32-10) draws with the reference's
+   * distributions, thread-per-head, atomic fp64 scatter-add (Hogwild),
+   * bounded heads in flight per shard. Statistically equivalent. */
+  NOMAD_B200_SGD_HOGWILD = 1
+};
+
+/* kNN distance mode (knn.hpp:65-109). */
+enum nomad_b200_knn_mode {
+  /* fp32 FFMA direct-difference filter with a rigorous error bound, top-K'
+   * per row, fp64 j-sequential re-rank and certificate (else exhaustive fp64
+   * for that row): ids AND fp64 distances bit-identical to the reference. */
+  NOMAD_B200_KNN_EXACT = 0,
+  /* bf16 tcgen05 distance contraction (||a||^2+||b||^2-2ab), top-k; report
+   * recall@k against the exact mode. Distances returned are fp64 re-ranked. */
+  NOMAD_B200_KNN_BF16 = 1
+};
+
+typedef struct nomad_b200_ctx nomad_b200_ctx;
+typedef struct nomad_b200_trainer nomad_b200_trainer;
+
+/* VectorDataset (dataset.hpp:35-44): f32 row-major rows x dims. */
+typedef struct {
+  uint64_t rows;
+  uint64_t dims;
+  const float* data;
+  int32_t location;
+} nomad_b200_dataset_view;
+
+/* ClusterAssignment (kmeans.hpp:32-43). Caller-owned, sized from
+ * (rows, n_clusters, dims). centroids may be NULL on output if unwanted. */
+typedef struct {
+  uint64_t rows;
+  uint64_t n_clusters;
+  uint64_t dims;
+  uint32_t* assignment; /* rows */
+  double* centroids;    /* n_clusters * dims */
+  uint32_t* sizes;      /* n_clusters */
+  int32_t location;
+} nomad_b200_clusters;
+
+/* KnnGraph (knn.hpp:31-47), CSR: offsets rows+1; neighbors/distances sized
+ * rows*k by the caller (offsets[rows] entries are written). */
+typedef struct {
+  uint64_t rows;
+  uint64_t k;
+  uint32_t* offsets;
+  uint32_t* neighbors;
+  double* distances; /* may be NULL */
+  int32_t location;
+} nomad_b200_graph;
+
+/* TrainConfig (optimizer.hpp:45-82) plus engine-only fields. */
+typedef struct {
+  uint64_t epochs;           /* 200 */
+  uint64_t k;                /* 15 */
+  uint64_t negatives;        /* |M| = 5 */
+  uint64_t local_draws;      /* s = 5 */
+  uint64_t batch_size;       /* 1024 (a step divisor: step = lr / batch) */
+  uint64_t workers;          /* W logical workers (shards) */
+  uint64_t n_clusters;       /* 0: auto (optimizer.hpp:73-77) */
+  uint64_t seed;
+  double lr0;                /* 0: auto n/10 */
+  uint64_t kmeans_max_iters; /* 100 */
+  double kmeans_tol;         /* < 0: auto (default_kmeans_tol) */
+  int32_t approx_all_but_own;/* ApproxMode::AllButOwnCluster */
+  int32_t head_only;
+  /* engine-only */
+  int32_t sgd_mode;          /* nomad_b200_sgd_mode */
+  int32_t knn_mode;          /* nomad_b200_knn_mode */
+  uint32_t hogwild_cap;      /* heads in flight per shard <= shard/cap (0: 16) */
+  int32_t verbose;           /* per-epoch line to stderr (optimizer.hpp:455-462) */
+} nomad_b200_train_config;
+
+/* Fills *cfg with the reference defaults (optimizer.hpp:45-61), replay mode,
+ * exact kNN. */
+void nomad_b200_default_config(nomad_b200_train_config* cfg);
+
+/* ----------------------------------------------------------- context */
+int32_t nomad_b200_create(int32_t device, nomad_b200_ctx** out);
+int32_t nomad_b200_destroy(nomad_b200_ctx* ctx);
+const char* nomad_b200_last_error(void);
+/* Work is issued on this stream (a cudaStream_t); NULL = the context's own. */
+int32_t nomad_b200_set_stream(nomad_b200_ctx* ctx, void* cuda_stream);
+/* Number of kernels this context has launched so far (evidence counter). */
+uint64_t nomad_b200_kernel_launches(const nomad_b200_ctx* ctx);
+
+/* ------------------------------------------------ index build (L2) */
+/* kmeans.hpp:157-161 default_kmeans_tol */
+int32_t nomad_b200_default_kmeans_tol(nomad_b200_ctx* ctx,
+                                      const nomad_b200_dataset_view* data,
+                                      double* tol_out);
+/* kmeans.hpp:167-250 lsh_init. out->n_clusters = C. */
+int32_t nomad_b200_lsh_init(nomad_b200_ctx* ctx,
+                            const nomad_b200_dataset_view* data,
+                            uint64_t n_clusters, uint64_t seed,
+                            nomad_b200_clusters* out);
+/* kmeans.hpp:257-296 kmeans_em; inout holds the init and receives the result.
+ * qe_trace: NULL or max_iters doubles; iters_out: iterations run (nullable).*/
+int32_t nomad_b200_kmeans_em(nomad_b200_ctx* ctx,
+                             const nomad_b200_dataset_view* data,
+                             nomad_b200_clusters* inout, uint64_t max_iters,
+                             double tol, double* qe_trace, uint64_t* iters_out);
+/* knn.hpp:65-109 build_knn. clusters: assignment + sizes. */
+int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx,
+                             const nomad_b200_dataset_view* data,
+                             const nomad_b200_clusters* clusters, uint64_t k,
+                             int32_t knn_mode, nomad_b200_graph* out);
+
+/* --------------------------------------------- epoch loop (L3 + L4) */
+/* The setup half of fit() (optimizer.hpp:342-386): build_affinity,
+ * shard_clusters, make_noise_model, worker states, means of the init layout.
+ * graph: CSR; clusters: assignment + n_clusters (sizes recomputed).
+ * init_layout: rows x 2 f64 (e.g. pca_init). Multi-GPU: rank/world_size and
+ * a 128-byte ncclUniqueId (nccl_id may be NULL when world_size == 1). Every
+ * rank passes the full index; rank r trains workers
+ * [r*W/world, (r+1)*W/world) (W % world_size == 0). */
+int32_t nomad_b200_trainer_create(nomad_b200_ctx* ctx,
+                                  const nomad_b200_graph* graph,
+                                  const nomad_b200_clusters* clusters,
+                                  const double* init_layout,
+                                  int32_t init_location,
+                                  const nomad_b200_train_config* cfg,
+                                  int32_t rank, int32_t world_size,
+                                  const void* nccl_id,
+                                  nomad_b200_trainer** out);
+int32_t nomad_b200_trainer_destroy(nomad_b200_trainer* tr);
+/* Runs the next n_epochs epochs of the cfg->epochs schedule
+ * (optimizer.hpp:388-470): SGD epoch, means all-gather, mean loss.
+ * epoch_loss: NULL or n_epochs doubles. */
+int32_t nomad_b200_trainer_run(nomad_b200_trainer* tr, uint64_t n_epochs,
+                               double* epoch_loss);
+/* Current layout in ORIGINAL point order (rows x 2 f64). On a multi-GPU
+ * trainer only this rank's points are written (others untouched). */
+int32_t nomad_b200_trainer_layout(nomad_b200_trainer* tr, double* out,
+                                  int32_t location);
+/* Current all-gathered ClusterMeans snapshot (objective.hpp:65-73):
+ * means n_clusters x 2, counts n_clusters; either may be NULL. */
+int32_t nomad_b200_trainer_means(nomad_b200_trainer* tr, double* means,
+                                 uint32_t* counts);
+/* CommLog counters (optimizer.hpp:178-189): totals since creation. */
+int32_t nomad_b200_trainer_comm(nomad_b200_trainer* tr, uint64_t* epochs,
+                                uint64_t* messages, uint64_t* payload_doubles,
+                                uint64_t* payload_counts);
+/* Epochs completed and edge-updates applied (sum over heads of |N(h)|+s). */
+int32_t nomad_b200_trainer_progress(nomad_b200_trainer* tr,
+                                    uint64_t* epochs_done,
+                                    uint64_t* edge_updates);
+
+/* --------------------------------------------------- fit (L4) */
+/* optimizer.hpp:327-482 fit. init_layout: the PCA initialisation
+ * (pca.hpp:79, rows x 2; NULL = computed on the GPU by power iteration).
+ * layout_out: rows x 2 f64. Report pointers may be NULL. */
+int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                       const nomad_b200_train_config* cfg,
+                       const double* init_layout, double* layout_out,
+                       nomad_b200_clusters* clusters_out,
+                       nomad_b200_graph* graph_out, double* epoch_loss_out);
+
+/* ------------------------------------------- helpers (multi-GPU, data) */
+/* ncclGetUniqueId into 128 bytes (rank 0 calls it, then broadcasts). */
+int32_t nomad_b200_nccl_unique_id(void* out128);
+/* Synthetic Gaussian mixture on the device: centres
+ * ~N(0, spread^2), x_i = c_{i mod blobs} + N(0,1), Philox4x32-10 streams.
+ * out: rows*dims f32 on the device. */
+int32_t nomad_b200_generate_mixture(nomad_b200_ctx* ctx, uint64_t rows,
+                                    uint64_t dims, uint64_t blobs,
+                                    double spread, uint64_t seed, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NOMAD_B200_H_ */

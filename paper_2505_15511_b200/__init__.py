@@ -1,0 +1,10 @@
+"""B200-native NOMAD Projection engine (arxiv 2505.15511 hot path).
+
+Drop-in for the reference library's index build + epoch loop
+(/root/reference/proj/include/nomad): hand-written sm_100a kernels behind the
+C-ABI in include/nomad_b200.h (libnomad_b200.so), bound here with ctypes.
+"""
+from ._native import NomadError, build, lib, EXPORTED  # noqa: F401
+from .api import (ClusterAssignment, CommLog, Context, FitReport, KnnGraph,  # noqa: F401
+                  TrainConfig, Trainer, build_knn, default_kmeans_tol, fit,
+                  generate_mixture, kmeans_em, lsh_init, nccl_unique_id)

@@ -1,0 +1,392 @@
+"""Host-side mirror of the reference library's API for the NOMAD hot path.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/nomad (cited per function), backed by
+libnomad_b200.so. Arrays may be numpy arrays (host) or torch tensors (host or
+CUDA); CUDA tensors are used in place.
+
+    clusters = lsh_init(data, n_clusters, seed)              # kmeans.hpp:167
+    clusters = kmeans_em(data, clusters, 100, tol)           # kmeans.hpp:257
+    graph    = build_knn(data, clusters, k)                  # knn.hpp:65
+    layout   = fit(data, TrainConfig(...), init_layout=pca)  # optimizer.hpp:327
+    tr = Trainer(graph, clusters, init_layout, cfg); tr.run(E)   # epoch loop
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from ._native import NomadError, check, lib
+
+
+# ---------------------------------------------------------------- arrays
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _view(x, dtype):
+    """(pointer, location, keepalive) of a contiguous array of dtype."""
+    if _is_torch(x):
+        import torch
+        tdt = {np.float32: torch.float32, np.float64: torch.float64,
+               np.uint32: torch.int32, np.int32: torch.int32}[dtype]
+        if x.dtype != tdt and not (dtype == np.uint32 and x.dtype == torch.int32):
+            x = x.to(tdt)
+        x = x.contiguous()
+        return x.data_ptr(), (N.DEVICE if x.is_cuda else N.HOST), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data, N.HOST, a
+
+
+def _dataset(data):
+    p, loc, keep = _view(data, np.float32)
+    rows, dims = (int(data.shape[0]), int(data.shape[1]))
+    return N.DatasetView(rows, dims, p, loc), keep
+
+
+# ---------------------------------------------------------------- types
+
+@dataclass
+class ClusterAssignment:
+    """kmeans.hpp:32-43"""
+    assignment: np.ndarray
+    n_clusters: int
+    dims: int
+    centroids: np.ndarray
+    sizes: np.ndarray
+
+    def centroid(self, r: int) -> np.ndarray:
+        return self.centroids[r * self.dims:(r + 1) * self.dims]
+
+    def _view(self):
+        self.assignment = np.ascontiguousarray(self.assignment, np.uint32)
+        self.centroids = np.ascontiguousarray(self.centroids, np.float64).reshape(-1)
+        self.sizes = np.ascontiguousarray(self.sizes, np.uint32)
+        return N.ClustersView(len(self.assignment), self.n_clusters, self.dims,
+                              self.assignment.ctypes.data, self.centroids.ctypes.data,
+                              self.sizes.ctypes.data, N.HOST)
+
+
+@dataclass
+class KnnGraph:
+    """knn.hpp:31-47 (CSR, squared distances)."""
+    rows: int
+    k: int
+    offsets: np.ndarray
+    neighbors: np.ndarray
+    distances: np.ndarray
+
+    def neighbor_count(self, i: int) -> int:
+        return int(self.offsets[i + 1] - self.offsets[i])
+
+    def neighbors_of(self, i: int) -> np.ndarray:
+        return self.neighbors[self.offsets[i]:self.offsets[i + 1]]
+
+
+@dataclass
+class TrainConfig:
+    """optimizer.hpp:45-82 plus engine-only fields (sgd_mode, knn_mode, hogwild_cap)."""
+    epochs: int = 200
+    k: int = 15
+    negatives: int = 5
+    local_draws: int = 5
+    batch_size: int = 1024
+    workers: int = 1
+    n_clusters: int = 0
+    seed: int = 0
+    lr0: float = 0.0
+    kmeans_max_iters: int = 100
+    kmeans_tol: float = -1.0
+    approx: str = "remote"          # "remote" | "non-own-cluster"
+    head_only: bool = False
+    verbose: bool = False
+    sgd_mode: str = "replay"        # "replay" (bit-exact) | "hogwild" (throughput)
+    knn_mode: str = "exact"         # "exact" | "bf16"
+    hogwild_cap: int = 0
+
+    def validate(self) -> None:  # optimizer.hpp:63-71
+        if self.workers < 1:
+            raise NomadError("Parameter", "workers must be >= 1")
+        if self.k < 1:
+            raise NomadError("Parameter", "k must be >= 1")
+        if self.negatives < 1:
+            raise NomadError("Parameter", "negatives must be >= 1")
+        if self.local_draws < 1:
+            raise NomadError("Parameter", "local draws must be >= 1")
+        if self.batch_size < 1:
+            raise NomadError("Parameter", "batch size must be >= 1")
+        if self.n_clusters != 0 and self.n_clusters < self.workers:
+            raise NomadError("Parameter", "clusters must be >= workers")
+
+    def resolve_clusters(self, n: int) -> int:  # optimizer.hpp:73-77
+        if self.n_clusters != 0:
+            return min(self.n_clusters, n)
+        return min(n, max((n + 4095) // 4096, self.workers, 2))
+
+    def resolve_lr0(self, n: int) -> float:  # optimizer.hpp:79-81
+        return self.lr0 if self.lr0 > 0.0 else n / 10.0
+
+    def c_struct(self) -> N.TrainConfigC:
+        return N.TrainConfigC(
+            self.epochs, self.k, self.negatives, self.local_draws, self.batch_size,
+            self.workers, self.n_clusters, self.seed & (2**64 - 1), float(self.lr0),
+            self.kmeans_max_iters, float(self.kmeans_tol),
+            1 if self.approx == "non-own-cluster" else 0, 1 if self.head_only else 0,
+            {"replay": N.SGD_REPLAY, "hogwild": N.SGD_HOGWILD}[self.sgd_mode],
+            {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16}[self.knn_mode],
+            self.hogwild_cap, 1 if self.verbose else 0)
+
+
+# ---------------------------------------------------------------- context
+
+class Context:
+    """One CUDA device + stream; owns no data between calls."""
+
+    _default: dict = {}
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        check(lib().nomad_b200_create(device, C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def kernel_launches(self) -> int:
+        return int(lib().nomad_b200_kernel_launches(self.h))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        check(lib().nomad_b200_set_stream(self.h, stream_ptr))
+
+    def close(self) -> None:
+        if self.h:
+            lib().nomad_b200_destroy(self.h)
+            self.h = None
+
+
+def _ctx(ctx: Optional[Context]) -> Context:
+    return ctx if ctx is not None else Context.default()
+
+
+# ---------------------------------------------------------------- index
+
+def default_kmeans_tol(data, ctx: Optional[Context] = None) -> float:
+    """kmeans.hpp:157-161"""
+    dv, keep = _dataset(data)
+    out = C.c_double()
+    check(lib().nomad_b200_default_kmeans_tol(_ctx(ctx).h, C.byref(dv), C.byref(out)))
+    return out.value
+
+
+def lsh_init(data, n_clusters: int, seed: int, ctx: Optional[Context] = None) -> ClusterAssignment:
+    """kmeans.hpp:167-250"""
+    dv, keep = _dataset(data)
+    n, d = dv.rows, dv.dims
+    ca = ClusterAssignment(np.zeros(n, np.uint32), int(n_clusters), d,
+                           np.zeros(int(n_clusters) * d, np.float64),
+                           np.zeros(int(n_clusters), np.uint32))
+    v = ca._view()
+    check(lib().nomad_b200_lsh_init(_ctx(ctx).h, C.byref(dv), n_clusters, seed & (2**64 - 1),
+                                    C.byref(v)))
+    return ca
+
+
+def kmeans_em(data, init: ClusterAssignment, max_iters: int = 100, tol: float = 0.0,
+              qe_trace: Optional[list] = None, ctx: Optional[Context] = None) -> ClusterAssignment:
+    """kmeans.hpp:257-296 (init is taken by value, as the reference)."""
+    dv, keep = _dataset(data)
+    if len(init.assignment) != dv.rows or init.dims != dv.dims:
+        raise NomadError("Parameter", "init assignment does not match dataset")
+    ca = ClusterAssignment(np.array(init.assignment, np.uint32), init.n_clusters, init.dims,
+                           np.array(init.centroids, np.float64).reshape(-1),
+                           np.array(init.sizes, np.uint32))
+    v = ca._view()
+    trace = np.zeros(max(max_iters, 1), np.float64) if qe_trace is not None else None
+    iters = C.c_uint64()
+    check(lib().nomad_b200_kmeans_em(_ctx(ctx).h, C.byref(dv), C.byref(v), max_iters, tol,
+                                     trace.ctypes.data if trace is not None else None,
+                                     C.byref(iters)))
+    if qe_trace is not None:
+        qe_trace.clear()
+        qe_trace.extend(trace[: iters.value].tolist())
+    return ca
+
+
+def build_knn(data, clusters: ClusterAssignment, k: int, mode: str = "exact",
+              ctx: Optional[Context] = None) -> KnnGraph:
+    """knn.hpp:65-109"""
+    if k < 1:
+        raise NomadError("Parameter", "k must be >= 1")
+    dv, keep = _dataset(data)
+    n = dv.rows
+    v = clusters._view()
+    off = np.zeros(n + 1, np.uint32)
+    nb = np.zeros(max(n * k, 1), np.uint32)
+    di = np.zeros(max(n * k, 1), np.float64)
+    gv = N.GraphView(n, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
+    check(lib().nomad_b200_build_knn(_ctx(ctx).h, C.byref(dv), C.byref(v), k,
+                                     {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16}[mode],
+                                     C.byref(gv)))
+    m = int(off[n])
+    return KnnGraph(n, k, off, nb[:m], di[:m])
+
+
+# ---------------------------------------------------------------- training
+
+@dataclass
+class CommLog:
+    """optimizer.hpp:178-189 totals."""
+    epochs: int
+    messages: int
+    payload_doubles: int
+    payload_counts: int
+
+
+class Trainer:
+    """The epoch loop of fit() (optimizer.hpp:342-470) on the GPU.
+
+    graph: KnnGraph (or a dict of device tensors offsets/neighbors), clusters:
+    ClusterAssignment (assignment + n_clusters), init_layout: n x 2 f64.
+    Multi-GPU: rank/world_size and a 128-byte NCCL unique id.
+    """
+
+    def __init__(self, graph, clusters, init_layout, cfg: TrainConfig, rank: int = 0,
+                 world_size: int = 1, nccl_id: Optional[bytes] = None,
+                 ctx: Optional[Context] = None):
+        cfg.validate()
+        self.ctx = _ctx(ctx)
+        self.cfg = cfg
+        if isinstance(graph, KnnGraph):
+            n, k = graph.rows, graph.k
+            offs, nbrs = graph.offsets, graph.neighbors
+        else:
+            n, k = int(graph["rows"]), int(graph["k"])
+            offs, nbrs = graph["offsets"], graph["neighbors"]
+        po, lo, ko = _view(offs, np.uint32)
+        nbrs_nonempty = nbrs if len(nbrs) else np.zeros(1, np.uint32)
+        pn, ln, kn = _view(nbrs_nonempty, np.uint32)
+        if lo != ln:
+            raise NomadError("Parameter", "graph offsets/neighbors must share a location")
+        gv = N.GraphView(n, k, po, pn, None, lo)
+        if isinstance(clusters, ClusterAssignment):
+            asg, ncl = clusters.assignment, clusters.n_clusters
+        else:
+            asg, ncl = clusters["assignment"], int(clusters["n_clusters"])
+        pa, la, ka = _view(asg, np.uint32)
+        cv = N.ClustersView(n, ncl, 0, pa, None, None, la)
+        pl, ll, kl = _view(init_layout, np.float64)
+        self.n, self.n_clusters = n, ncl
+        self._keep = (ko, kn, ka, kl)
+        c = cfg.c_struct()
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        h = C.c_void_p()
+        check(lib().nomad_b200_trainer_create(self.ctx.h, C.byref(gv), C.byref(cv), pl, ll,
+                                              C.byref(c), rank, world_size, idbuf, C.byref(h)))
+        self.h = h
+
+    def run(self, n_epochs: int) -> np.ndarray:
+        out = np.zeros(max(n_epochs, 1), np.float64)
+        check(lib().nomad_b200_trainer_run(self.h, n_epochs, out.ctypes.data))
+        return out[:n_epochs]
+
+    def layout(self, out=None) -> np.ndarray:
+        if out is not None and _is_torch(out) and out.is_cuda:
+            check(lib().nomad_b200_trainer_layout(self.h, out.data_ptr(), N.DEVICE))
+            return out
+        arr = np.zeros((self.n, 2), np.float64) if out is None else out
+        check(lib().nomad_b200_trainer_layout(self.h, arr.ctypes.data, N.HOST))
+        return arr
+
+    def means(self):
+        m = np.zeros((self.n_clusters, 2), np.float64)
+        c = np.zeros(self.n_clusters, np.uint32)
+        check(lib().nomad_b200_trainer_means(self.h, m.ctypes.data, c.ctypes.data))
+        return m, c
+
+    def comm_log(self) -> CommLog:
+        v = [C.c_uint64() for _ in range(4)]
+        check(lib().nomad_b200_trainer_comm(self.h, *[C.byref(x) for x in v]))
+        return CommLog(*[x.value for x in v])
+
+    def progress(self):
+        e, u = C.c_uint64(), C.c_uint64()
+        check(lib().nomad_b200_trainer_progress(self.h, C.byref(e), C.byref(u)))
+        return e.value, u.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nomad_b200_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class FitReport:
+    """optimizer.hpp:312-321 (the parts the engine reports)."""
+    clusters: Optional[ClusterAssignment] = None
+    graph: Optional[KnnGraph] = None
+    epoch_mean_loss: list = field(default_factory=list)
+
+
+def fit(data, config: TrainConfig, init_layout=None, report: Optional[FitReport] = None,
+        ctx: Optional[Context] = None) -> np.ndarray:
+    """optimizer.hpp:327-482. init_layout: the PCA initialisation (n x 2)."""
+    config.validate()
+    dv, keep = _dataset(data)
+    n, d = dv.rows, dv.dims
+    ncl = config.resolve_clusters(n)
+    ca = ClusterAssignment(np.zeros(n, np.uint32), ncl, d, np.zeros(ncl * d, np.float64),
+                           np.zeros(ncl, np.uint32))
+    cv = ca._view()
+    k = config.k
+    off = np.zeros(n + 1, np.uint32)
+    nb = np.zeros(max(n * k, 1), np.uint32)
+    di = np.zeros(max(n * k, 1), np.float64)
+    gv = N.GraphView(n, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
+    out = np.zeros((n, 2), np.float64)
+    losses = np.zeros(max(config.epochs, 1), np.float64)
+    pl = None
+    if init_layout is not None:
+        il = np.ascontiguousarray(init_layout, np.float64)
+        pl = il.ctypes.data
+    c = config.c_struct()
+    check(lib().nomad_b200_fit(_ctx(ctx).h, C.byref(dv), C.byref(c), pl, out.ctypes.data,
+                               C.byref(cv), C.byref(gv), losses.ctypes.data))
+    if report is not None:
+        m = int(off[n])
+        report.clusters = ca
+        report.graph = KnnGraph(n, k, off, nb[:m], di[:m])
+        report.epoch_mean_loss = losses[: config.epochs].tolist()
+    return out
+
+
+def generate_mixture(rows: int, dims: int, blobs: int, spread: float = 10.0, seed: int = 42,
+                     out=None, ctx: Optional[Context] = None):
+    """Device synthetic Gaussian mixture into a CUDA float32 tensor (rows x dims)."""
+    import torch
+    cx = _ctx(ctx)
+    if out is None:
+        out = torch.empty((rows, dims), dtype=torch.float32, device=f"cuda:{cx.device}")
+    check(lib().nomad_b200_generate_mixture(cx.h, rows, dims, blobs, spread, seed,
+                                            out.data_ptr()))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().nomad_b200_nccl_unique_id(buf))
+    return buf.raw

@@ -1,0 +1,184 @@
+// Context, error plumbing, config defaults, NCCL id, device data generator.
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace nb {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+void bind_device(nomad_b200_ctx* c) { NB_CUDA(cudaSetDevice(c->device)); }
+
+void note_launch(nomad_b200_ctx* c, const char* name) {
+  ++c->launches;
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess)
+    fail(kInternal, std::string("launch of ") + name + " failed: " + cudaGetErrorString(e));
+}
+
+// SURVEY §8(d) synthetic mixture: centres ~ N(0, spread^2 I), x_i =
+// c_{i mod blobs} + N(0, I). Each thread emits 4 consecutive coordinates of
+// one row from one Philox block (Box-Muller on two pairs, fp32).
+__global__ void k_mixture_centres(float* centres, uint64_t count, float spread,
+                                  uint32_t s0, uint32_t s1) {
+  const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (q * 4 >= count) return;
+  const u32x4 r = philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0xC3u, 0u}, s0, s1);
+  const float u0 = ((r.x >> 8) + 1) * 0x1p-24f, v0 = (r.y >> 8) * 0x1p-24f;
+  const float u1 = ((r.z >> 8) + 1) * 0x1p-24f, v1 = (r.w >> 8) * 0x1p-24f;
+  const float a = sqrtf(-2.f * logf(u0)), b = sqrtf(-2.f * logf(u1));
+  float g[4];
+  sincospif(2.f * v0, &g[1], &g[0]);
+  sincospif(2.f * v1, &g[3], &g[2]);
+  g[0] *= a; g[1] *= a; g[2] *= b; g[3] *= b;
+  for (int t = 0; t < 4; ++t)
+    if (q * 4 + t < count) centres[q * 4 + t] = spread * g[t];
+}
+
+__global__ void k_mixture_points(float* out, const float* centres, uint64_t rows,
+                                 uint64_t dims, uint64_t blobs, uint32_t s0, uint32_t s1) {
+  const uint64_t total = rows * dims;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q * 4 < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const u32x4 r = philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0x9Au, 1u}, s0, s1);
+    const float u0 = ((r.x >> 8) + 1) * 0x1p-24f, v0 = (r.y >> 8) * 0x1p-24f;
+    const float u1 = ((r.z >> 8) + 1) * 0x1p-24f, v1 = (r.w >> 8) * 0x1p-24f;
+    const float a = sqrtf(-2.f * __logf(u0)), b = sqrtf(-2.f * __logf(u1));
+    float g[4];
+    sincospif(2.f * v0, &g[1], &g[0]);
+    sincospif(2.f * v1, &g[3], &g[2]);
+    g[0] *= a; g[1] *= a; g[2] *= b; g[3] *= b;
+    const uint64_t e0 = q * 4;
+    if ((dims & 3) == 0 && e0 + 3 < total) {
+      const uint64_t i = e0 / dims, j = e0 % dims;
+      const float4 c = *reinterpret_cast<const float4*>(centres + (i % blobs) * dims + j);
+      *reinterpret_cast<float4*>(out + e0) = make_float4(c.x + g[0], c.y + g[1], c.z + g[2], c.w + g[3]);
+    } else {
+      for (int t = 0; t < 4; ++t) {
+        const uint64_t e = e0 + t;
+        if (e >= total) break;
+        const uint64_t i = e / dims, j = e % dims;
+        out[e] = centres[(i % blobs) * dims + j] + g[t];
+      }
+    }
+  }
+}
+
+}  // namespace nb
+
+using namespace nb;
+
+extern "C" {
+
+const char* nomad_b200_last_error(void) { return g_last_error.c_str(); }
+
+void nomad_b200_default_config(nomad_b200_train_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->epochs = 200;
+  c->k = 15;
+  c->negatives = 5;
+  c->local_draws = 5;
+  c->batch_size = 1024;
+  c->workers = 1;
+  c->n_clusters = 0;
+  c->seed = 0;
+  c->lr0 = 0.0;
+  c->kmeans_max_iters = 100;
+  c->kmeans_tol = -1.0;
+  c->sgd_mode = NOMAD_B200_SGD_REPLAY;
+  c->knn_mode = NOMAD_B200_KNN_EXACT;
+  c->hogwild_cap = 0;
+}
+
+int32_t nomad_b200_create(int32_t device, nomad_b200_ctx** out) {
+  return guard([&] {
+    if (!out) fail(kParameter, "out is NULL");
+    int n = 0;
+    NB_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n)
+      fail(kParameter, "device " + std::to_string(device) + " out of range (" +
+                           std::to_string(n) + " visible)");
+    cudaDeviceProp prop;
+    NB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(kConfig, std::string("libnomad_b200 is built for sm_100a; device is ") +
+                        prop.name + " sm_" + std::to_string(prop.major) +
+                        std::to_string(prop.minor));
+    auto* c = new nomad_b200_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    NB_CUDA(cudaSetDevice(device));
+    NB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    *out = c;
+  });
+}
+
+int32_t nomad_b200_destroy(nomad_b200_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->own_stream && c->stream) {
+      cudaStreamSynchronize(c->stream);
+      cudaStreamDestroy(c->stream);
+    }
+    delete c;
+  });
+}
+
+int32_t nomad_b200_set_stream(nomad_b200_ctx* c, void* s) {
+  return guard([&] {
+    if (!c) fail(kParameter, "ctx is NULL");
+    bind_device(c);
+    if (c->own_stream && c->stream) {
+      NB_CUDA(cudaStreamSynchronize(c->stream));
+      NB_CUDA(cudaStreamDestroy(c->stream));
+    }
+    if (s) {
+      c->stream = static_cast<cudaStream_t>(s);
+      c->own_stream = false;
+    } else {
+      NB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+  });
+}
+
+uint64_t nomad_b200_kernel_launches(const nomad_b200_ctx* c) { return c ? c->launches : 0; }
+
+int32_t nomad_b200_nccl_unique_id(void* out128) {
+  return guard([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) fail(kInternal, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out128, &id, 128);
+  });
+}
+
+int32_t nomad_b200_generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
+                                    uint64_t blobs, double spread, uint64_t seed,
+                                    float* out) {
+  return guard([&] {
+    if (!c || !out) fail(kParameter, "NULL argument");
+    if (rows < 1 || dims < 1 || blobs < 1) fail(kParameter, "empty mixture shape");
+    bind_device(c);
+    DBuf<float> centres(blobs * dims + 4);
+    const uint32_t s0 = (uint32_t)seed, s1 = (uint32_t)(seed >> 32) ^ 0x5eedu;
+    const uint64_t cq = (blobs * dims + 3) / 4;
+    k_mixture_centres<<<(unsigned)((cq + 255) / 256), 256, 0, c->stream>>>(
+        centres.p, blobs * dims, (float)spread, s0, s1);
+    note_launch(c, "k_mixture_centres");
+    k_mixture_points<<<c->sm_count * 8, 256, 0, c->stream>>>(out, centres.p, rows, dims,
+                                                             blobs, s0, s1);
+    note_launch(c, "k_mixture_points");
+    NB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+}  // extern "C"

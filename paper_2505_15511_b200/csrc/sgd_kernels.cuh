@@ -1,0 +1,86 @@
+// Device side of the epoch loop: the SGD kernels (K8r replay, K8p hogwild) and
+// the cluster-means kernels (K9). Reference: optimizer.hpp:215-307 (worker
+// epoch, apply_update), objective.hpp:36-41/113-145/178-237 (Cauchy kernel,
+// noise terms, analytic gradient), optimizer.hpp:411-442 (means all-gather).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "philox.cuh"
+
+namespace nb {
+
+// Per logical worker (shard) on this rank. Points of worker w are the
+// contiguous local ids [pstart, pstart + npts), grouped by cluster (ascending
+// cluster id), ascending original id inside each cluster.
+struct WorkerDev {
+  uint32_t pstart, npts;      // local point range
+  uint32_t elig_off, n_elig;  // eligible heads (local ids) in elig[]
+  uint32_t rem_off, n_rem;    // remote cells R~ (RemoteClusters mode)
+  uint32_t draws;             // heads drawn this epoch (= n_elig)
+  uint32_t blk_start;         // first block of this worker (hogwild grid)
+  uint32_t nblk;              // blocks of this worker
+  uint32_t id;                // global worker id
+  double local_mass;          // optimizer.hpp:369-370
+};
+
+// A cluster owned by this rank: local ids [start, start + count).
+struct LocalCluster {
+  uint32_t start, count, gid, worker;  // worker = local worker index
+};
+
+struct SgdParams {
+  double2* pos;                 // local positions (f64 x, y)
+  const uint32_t* ell;          // local ids, kpad per row
+  const uint8_t* ncnt;          // neighbour count per row (nullptr: all == k)
+  const double* wtab;           // (k+1) x k inverse-rank weights, row = count
+  const uint32_t* elig;         // eligible heads, local ids, worker-major
+  const WorkerDev* workers;
+  const double2* means;         // all C cluster means (stale snapshot)
+  const uint32_t* remote_ids;   // concat per worker (global cluster ids)
+  const double* remote_probs;   // p(m in r), parallel
+  const uint32_t* cl_of;        // local cluster index per local point (AllButOwn)
+  const LocalCluster* lclusters;
+  const double* cell_probs;     // global C: size_r / n
+  double* loss_acc;             // per local worker
+  unsigned long long* edge_acc; // per local worker: sum of |N(h)| + s
+  unsigned long long* diverge;  // first offending key (replay: t * stride + u)
+  uint32_t n_workers, kpad, k, s, m_total, n_clusters;
+  int head_only, all_but_own;
+  double step;
+  uint64_t epoch;
+  uint32_t seed_lo, seed_hi;
+  // replay tape (level-ordered)
+  const uint32_t* tape_head;    // local id per draw (level order)
+  const uint32_t* tape_tails;   // s local ids per draw
+  const uint32_t* tape_t;       // sequential draw index t per draw
+  const uint32_t* lvl_off;      // per worker: level offsets into the tape
+  const uint32_t* wk_lvl_base;  // per worker: index of its first level in lvl_off
+  const uint32_t* wk_nlev;      // per worker: number of levels
+  double* loss_slot;            // per worker-draw loss, indexed by worker base + t
+  const uint32_t* wk_draw_base; // per worker: base into loss_slot
+};
+
+// Host launchers (sgd.cu).
+void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cudaStream_t st);
+void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
+                     double* out, cudaStream_t st);
+void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st);
+void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,
+                        cudaStream_t st);
+void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
+                        const uint32_t* chunk_off, uint32_t nchunks, double* sums,
+                        unsigned long long* diverge, cudaStream_t st);
+void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, double* slot,
+                           cudaStream_t st);
+void launch_means_unpack(const double* recv, const uint32_t* slot_gid, uint32_t nslots,
+                         double2* means, cudaStream_t st);
+void launch_build_ell(const uint32_t* offsets, const uint32_t* nbrs, const uint32_t* orig_of,
+                      const uint32_t* new_of, uint32_t n_loc, uint32_t kpad, uint32_t* ell,
+                      uint8_t* ncnt, unsigned long long* bad, cudaStream_t st);
+void launch_scatter_layout(const double2* pos, const uint32_t* orig_of, uint32_t n_loc,
+                           double2* out, cudaStream_t st);
+void launch_gather_layout(const double2* in, const uint32_t* orig_of, uint32_t n_loc,
+                          double2* pos, cudaStream_t st);
+
+}  // namespace nb

@@ -1,0 +1,144 @@
+"""Epoch loop parity on the B200: replay mode must be bit-identical to the
+oracle (the C restatement of optimizer.hpp:232-470, itself pinned to the
+reference in test_oracle.py); hogwild mode must match statistically."""
+import numpy as np
+import pytest
+
+from common import index_case
+
+pytestmark = pytest.mark.gpu
+
+
+def _trainer(nb, ctx, c, g, pca, **kw):
+    cfg = nb.TrainConfig(**kw)
+    return nb.Trainer(nb.KnnGraph(len(c.assignment), g.k, g.offsets, g.neighbors, g.distances),
+                      nb.ClusterAssignment(c.assignment, c.n_clusters, c.dims, c.centroids,
+                                           c.sizes), pca, cfg, ctx=ctx)
+
+
+def _oracle(port, c, g, pca, n_run, **kw):
+    from oracle import train_config
+    return port.train_epochs(c.assignment, c.n_clusters, g.offsets, g.neighbors, g.k,
+                             train_config(**kw), pca, 0, n_run)
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+def test_replay_bit_exact(port, ctx, workers):
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=10, workers=workers, seed=7)
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    loss = tr.run(6)
+    lay = tr.layout()
+    rl, rloss, rmeans, _ = _oracle(port, c, g, pca, 6, **kw)
+    assert np.array_equal(lay, rl)
+    # loss goes through CUDA's log (<= 1 ulp from glibc): relative 1e-13
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+    m, counts = tr.means()
+    assert np.array_equal(m, rmeans)
+    assert counts.tolist() == c.sizes.tolist()
+    log = tr.comm_log()
+    assert (log.epochs, log.messages) == (6, 6 * workers)
+    assert log.payload_doubles == 6 * 2 * 8 and log.payload_counts == 6 * 8
+
+
+def test_replay_resume_equals_single_run(port, ctx):
+    """run(2)+run(3) == run(5): worker RNG streams persist across calls."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=8, workers=2, seed=3)
+    a = _trainer(nb, ctx, c, g, pca, **kw)
+    a.run(2)
+    a.run(3)
+    b = _trainer(nb, ctx, c, g, pca, **kw)
+    b.run(5)
+    assert np.array_equal(a.layout(), b.layout())
+
+
+@pytest.mark.parametrize("mode", ["all_but_own", "head_only"])
+def test_replay_ablation_modes(port, ctx, mode):
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=10, workers=2, seed=11)
+    okw = dict(kw)
+    if mode == "all_but_own":
+        kw["approx"] = "non-own-cluster"
+        okw["approx_all_but_own"] = 1
+    else:
+        kw["head_only"] = True
+        okw["head_only"] = 1
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    loss = tr.run(4)
+    rl, rloss, _, _ = _oracle(port, c, g, pca, 4, **okw)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
+def test_replay_ragged_neighbor_lists(port, ctx):
+    """Clusters smaller than k+1 give short lists (knn.hpp:77-83)."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(600, 8, 40, 40, 15)
+    counts = np.diff(g.offsets)
+    assert counts.min() < 15  # the case is actually ragged
+    kw = dict(epochs=5, workers=4, seed=5)
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    loss = tr.run(5)
+    rl, rloss, _, _ = _oracle(port, c, g, pca, 5, **kw)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
+def test_divergence_error_matches_reference(port, ctx):
+    """optimizer.hpp:215-227: a huge lr0 diverges; same kind and message."""
+    import paper_2505_15511_b200 as nb
+    from oracle import OracleError
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=10, workers=1, seed=7, lr0=1e14)
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    with pytest.raises(nb.NomadError) as ei:
+        tr.run(3)
+    with pytest.raises(OracleError) as eo:
+        _oracle(port, c, g, pca, 3, **kw)
+    assert ei.value.kind == "Divergence" == eo.value.kind
+    assert ei.value.message == eo.value.msg
+
+
+def test_parameter_errors(ctx):
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    with pytest.raises(nb.NomadError) as e:
+        _trainer(nb, ctx, c, g, pca, epochs=10, workers=9)
+    assert e.value.kind == "Parameter"
+    tr = _trainer(nb, ctx, c, g, pca, epochs=2, workers=1)
+    tr.run(2)
+    with pytest.raises(nb.NomadError) as e:
+        tr.run(1)
+    assert e.value.kind == "Parameter"
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+def test_hogwild_statistical_parity(port, ctx, workers):
+    """Throughput mode: same loss trajectory as the reference within 5%."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=30, workers=workers, seed=7)
+    tr = _trainer(nb, ctx, c, g, pca, sgd_mode="hogwild", **kw)
+    loss = tr.run(30)
+    lay = tr.layout()
+    assert np.isfinite(lay).all()
+    _, rloss, _, _ = _oracle(port, c, g, pca, 30, **kw)
+    assert abs(loss[-5:].mean() - rloss[-5:].mean()) < 0.05 * rloss[-5:].mean()
+    e, edges = tr.progress()
+    assert e == 30 and edges == 30 * 3000 * 20
+
+
+def test_config_a_replay(port, ctx):
+    """BASELINE config A (20k x 64, k=15, single shard): 3 epochs bit-exact."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(20000, 64, 10, 5, 15)
+    kw = dict(epochs=200, workers=1, seed=7)
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    loss = tr.run(3)
+    rl, rloss, _, _ = _oracle(port, c, g, pca, 3, **kw)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
