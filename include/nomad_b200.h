@@ -200,6 +200,14 @@ int32_t nomad_b200_trainer_means(nomad_b200_trainer* tr, double* means,
 int32_t nomad_b200_trainer_comm(nomad_b200_trainer* tr, uint64_t* epochs,
                                 uint64_t* messages, uint64_t* payload_doubles,
                                 uint64_t* payload_counts);
+/* Replace the positions (rows x 2, ORIGINAL order) and re-gather the means
+ * snapshot (the layout handed to the epoch loop, optimizer.hpp:353/:384). */
+int32_t nomad_b200_trainer_set_layout(nomad_b200_trainer* tr, const double* layout,
+                                      int32_t location);
+/* Device time (CUDA events on the launching stream) accumulated over every
+ * epoch run so far: the SGD kernel, and the means + all-gather step. */
+int32_t nomad_b200_trainer_timing(nomad_b200_trainer* tr, double* sgd_ms,
+                                  double* means_ms, uint64_t* epochs);
 /* Epochs completed and edge-updates applied (sum over heads of |N(h)|+s). */
 int32_t nomad_b200_trainer_progress(nomad_b200_trainer* tr,
                                     uint64_t* epochs_done,

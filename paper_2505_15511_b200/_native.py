@@ -81,6 +81,9 @@ _SIGS = {
     "nomad_b200_trainer_layout": (C.c_int32, [_vp, _vp, C.c_int32]),
     "nomad_b200_trainer_means": (C.c_int32, [_vp, _vp, _vp]),
     "nomad_b200_trainer_comm": (C.c_int32, [_vp] + [C.POINTER(C.c_uint64)] * 4),
+    "nomad_b200_trainer_set_layout": (C.c_int32, [_vp, _vp, C.c_int32]),
+    "nomad_b200_trainer_timing": (C.c_int32, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                              C.POINTER(C.c_uint64)]),
     "nomad_b200_trainer_progress": (C.c_int32, [_vp] + [C.POINTER(C.c_uint64)] * 2),
     "nomad_b200_fit": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(TrainConfigC), _vp,
                                    _vp, C.POINTER(ClustersView), C.POINTER(GraphView), _vp]),

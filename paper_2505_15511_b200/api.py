@@ -317,6 +317,16 @@ class Trainer:
         check(lib().nomad_b200_trainer_comm(self.h, *[C.byref(x) for x in v]))
         return CommLog(*[x.value for x in v])
 
+    def set_layout(self, layout) -> None:
+        p, loc, keep = _view(layout, np.float64)
+        check(lib().nomad_b200_trainer_set_layout(self.h, p, loc))
+
+    def timing(self):
+        """(sgd_ms, means_ms, epochs): device time accumulated over all epochs run."""
+        a, b, e = C.c_double(), C.c_double(), C.c_uint64()
+        check(lib().nomad_b200_trainer_timing(self.h, C.byref(a), C.byref(b), C.byref(e)))
+        return a.value, b.value, e.value
+
     def progress(self):
         e, u = C.c_uint64(), C.c_uint64()
         check(lib().nomad_b200_trainer_progress(self.h, C.byref(e), C.byref(u)))

@@ -1,6 +1,8 @@
 // SGD epoch kernels and cluster-means kernels (see sgd_kernels.cuh).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "sgd_kernels.cuh"
 
@@ -191,7 +193,7 @@ __global__ void k_loss_seq(const double* slot, const uint32_t* base, const Worke
 // are fp64 atomic scatter-adds (RED.ADD.F64). Heads in flight per worker are
 // bounded by the grid share the host gives the worker (hogwild cap).
 template <int KMAX, int SMAX>
-__global__ void __launch_bounds__(256) k_sgd_hogwild(SgdParams P) {
+__global__ void __launch_bounds__(256, 2) k_sgd_hogwild(SgdParams P) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[8];
   uint32_t w = 0;
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(256) k_sgd_hogwild(SgdParams P) {
   unsigned long long edges = 0;
   for (uint32_t t = tid; t < W.draws; t += nthr) {
     // --- draws (1 + s) x 64 bits
-    uint64_t rnd[1 + SMAX + 1];
+    uint64_t rnd[2 * ((SMAX + 2) / 2)];
 #pragma unroll
     for (int c = 0; c < (SMAX + 2) / 2; ++c) {
       const u32x4 r = philox4x32_10(u32x4{t, W.id, (uint32_t)P.epoch, (uint32_t)c},
@@ -451,10 +453,25 @@ void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaS
       NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<nblocks, 256, smem, st>>>(P);
   };
-  if (P.kpad <= 16) go(k_sgd_hogwild<16, 8>);
+  if (P.kpad <= 16 && P.s == 5) go(k_sgd_hogwild<16, 5>);
+  else if (P.kpad <= 16) go(k_sgd_hogwild<16, 8>);
   else if (P.kpad <= 32) go(k_sgd_hogwild<32, 8>);
   else if (P.kpad <= 64) go(k_sgd_hogwild<64, 8>);
   else fail(kParameter, "throughput mode supports k <= 64");
+}
+
+uint32_t hogwild_resident_blocks(uint32_t kpad, uint32_t s, size_t smem, int sm_count) {
+  int per_sm = 0;
+  auto q = [&](auto kern) {
+    if (smem > 48 * 1024)
+      NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  };
+  if (kpad <= 16 && s == 5) q(k_sgd_hogwild<16, 5>);
+  else if (kpad <= 16) q(k_sgd_hogwild<16, 8>);
+  else if (kpad <= 32) q(k_sgd_hogwild<32, 8>);
+  else q(k_sgd_hogwild<64, 8>);
+  return (uint32_t)std::max(1, per_sm) * (uint32_t)sm_count;
 }
 
 void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,

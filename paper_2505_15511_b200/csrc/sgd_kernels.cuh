@@ -66,6 +66,7 @@ void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cuda
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
                      double* out, cudaStream_t st);
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st);
+uint32_t hogwild_resident_blocks(uint32_t kpad, uint32_t s, size_t smem, int sm_count);
 void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,
                         cudaStream_t st);
 void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,

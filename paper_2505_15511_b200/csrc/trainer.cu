@@ -100,12 +100,19 @@ struct nomad_b200_trainer {
   std::vector<uint32_t> draw_base_h;
 
   uint64_t epochs_done = 0, edge_updates = 0;
+  // device-side timing of the SGD kernel and the means+exchange step (CUDA
+  // events on the launching stream), accumulated over all epochs run.
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double sgd_ms = 0.0, means_ms = 0.0;
+  uint64_t timed_epochs = 0;
   uint64_t comm_epochs = 0, comm_msgs = 0, comm_doubles = 0, comm_counts = 0;
 
   cudaStream_t st() const { return ctx->stream; }
   void launched(const char* name) { note_launch(ctx, name); }
   ~nomad_b200_trainer() {
     if (comm) ncclCommDestroy(comm);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
   }
 
   void validate() {
@@ -390,10 +397,9 @@ struct nomad_b200_trainer {
 
   void plan_hogwild_grid() {
     const uint32_t cap = cfg.hogwild_cap ? cfg.hogwild_cap : 16;
-    // resident blocks of 256 threads: 1 per SM at <=255 regs (measured by
-    // occupancy API in the launcher is overkill here; 2 per SM is the
-    // register-file bound at 128 regs). Use 2 x SMs as the share budget.
-    const uint64_t budget = (uint64_t)ctx->sm_count * 2;
+    // The grid never exceeds what is resident at once (the kernel loops over
+    // its draws with a grid stride, so a second wave would only add a tail).
+    const uint64_t budget = hogwild_resident_blocks((uint32_t)kpad, (uint32_t)s, smem_hog, ctx->sm_count);
     uint64_t total = 0;
     for (auto& d : wk) total += d.draws;
     uint32_t blk = 0;
@@ -587,6 +593,8 @@ struct nomad_b200_trainer {
       const double step = lr / static_cast<double>(cfg.batch_size);
       SgdParams P = params(step, e);
       uint64_t edges = 0;
+      if (!ev[0])
+        for (auto& x : ev) NB_CUDA(cudaEventCreate(&x));
       if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
         build_tapes(0, th, tt, tid, loff, lbase, nlev, edges);
         upload(tape_head, th, S);
@@ -603,21 +611,26 @@ struct nomad_b200_trainer {
         P.wk_nlev = wk_nlev.p;
         P.loss_slot = loss_slot.p;
         P.wk_draw_base = wk_draw_base.p;
+        NB_CUDA(cudaEventRecord(ev[0], S));
         if (nwl) {
           launch_sgd_replay(P, nwl, smem_replay, S);
           launched("k_sgd_replay");
           launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
           launched("k_loss_seq");
         }
+        NB_CUDA(cudaEventRecord(ev[1], S));
       } else {
         NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
         NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
+        NB_CUDA(cudaEventRecord(ev[0], S));
         if (hog_blocks) {
           launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
           launched("k_sgd_hogwild");
         }
+        NB_CUDA(cudaEventRecord(ev[1], S));
       }
       compute_means_and_exchange();
+      NB_CUDA(cudaEventRecord(ev[2], S));
       // per-worker loss sums -> epoch mean (optimizer.hpp:444-451)
       const double* lsrc = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? wloss.p : loss_acc.p;
       if (nwl) NB_CUDA(cudaMemcpyAsync(wl_loss.data(), lsrc, nwl * 8, cudaMemcpyDeviceToHost, S));
@@ -630,6 +643,14 @@ struct nomad_b200_trainer {
                                 cudaMemcpyDeviceToHost, S));
       }
       check_divergence(e, cfg.sgd_mode == NOMAD_B200_SGD_REPLAY);  // syncs the stream
+      {
+        float a = 0.f, b = 0.f;
+        NB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        NB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        sgd_ms += a;
+        means_ms += b;
+        ++timed_epochs;
+      }
       if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD)
         for (uint32_t wl = 0; wl < nwl; ++wl) edges += wl_edges[wl];
       edge_updates += edges;
@@ -676,6 +697,26 @@ struct nomad_b200_trainer {
       for (double v : h) global_heads += (uint64_t)v;
     }
     return global_heads;
+  }
+
+  // Replace the positions (original order, n x 2) and re-gather the means
+  // snapshot, as if the epoch loop had been given this layout.
+  void set_layout(const double* in, int loc) {
+    cudaStream_t S = st();
+    const uint32_t n_loc = (uint32_t)orig_of.size();
+    DBuf<double> tmp;
+    const double* src = in;
+    if (loc != NOMAD_B200_DEVICE) {
+      tmp.alloc(2 * n);
+      NB_CUDA(cudaMemcpyAsync(tmp.p, in, n * 16, cudaMemcpyHostToDevice, S));
+      src = tmp.p;
+    }
+    if (n_loc) {
+      launch_gather_layout(reinterpret_cast<const double2*>(src), orig_of_d.p, n_loc, pos.p, S);
+      launched("k_gather_layout");
+    }
+    compute_means_and_exchange();
+    NB_CUDA(cudaStreamSynchronize(S));
   }
 
   void layout(double* out, int loc) {
@@ -769,6 +810,24 @@ int32_t nomad_b200_trainer_comm(nomad_b200_trainer* t, uint64_t* epochs, uint64_
     if (messages) *messages = t->comm_msgs;
     if (doubles) *doubles = t->comm_doubles;
     if (counts) *counts = t->comm_counts;
+  });
+}
+
+int32_t nomad_b200_trainer_set_layout(nomad_b200_trainer* t, const double* layout, int32_t loc) {
+  return guard([&] {
+    if (!t || !layout) fail(kParameter, "NULL argument");
+    bind_device(t->ctx);
+    t->set_layout(layout, loc);
+  });
+}
+
+int32_t nomad_b200_trainer_timing(nomad_b200_trainer* t, double* sgd_ms, double* means_ms,
+                                  uint64_t* epochs) {
+  return guard([&] {
+    if (!t) fail(kParameter, "trainer is NULL");
+    if (sgd_ms) *sgd_ms = t->sgd_ms;
+    if (means_ms) *means_ms = t->means_ms;
+    if (epochs) *epochs = t->timed_epochs;
   });
 }
 
