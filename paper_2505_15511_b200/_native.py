@@ -11,7 +11,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnomad_b200.so")
+LIB_PATH = os.environ.get("NOMAD_B200_LIB") or os.path.join(HERE, "libnomad_b200.so")
 
 KINDS = ["Io", "Dimension", "Validation", "Schema", "Parameter", "Config",
          "Degenerate", "Divergence", "Size", "Internal"]

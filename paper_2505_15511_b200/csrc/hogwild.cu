@@ -1,0 +1,402 @@
+// K8p: throughput-mode SGD epoch kernel (optimizer.hpp:232-307 semantics with
+// Hogwild-style concurrent heads).
+//
+// One group of G lanes per head (G = 4: 8 heads per warp). Draws come from
+// Philox4x32-10 keyed by (seed, epoch, worker, draw t): head ~ U(eligible_w),
+// tails ~ U(pool_w) — the distributions of optimizer.hpp:254-255 / :284-285.
+// Lane gl of a group owns neighbours [NPL*gl, NPL*gl+NPL) (one vector load of
+// the ELL row), tails gl, gl+G, ..., and remote cells gl, gl+G, ...; the
+// shared sums (mean field, sampled noise, bg sensitivity, head gradient) are
+// butterfly-reduced inside the group, which leaves bitwise-identical values
+// on every lane. The gradient is the reference's (objective.hpp:178-237)
+// with algebraic reuse: pull = 2 w q bg / (q + bg), and the mean push folded
+// into one sum. Updates are fp64 atomic scatter-adds (RED.ADD.F64).
+//
+// Scheduling: blocks pull fixed-size chunks of draws from a global counter;
+// chunks are numbered worker-major, so at any moment the GPU works on about
+// one shard and that shard's positions stay resident in L2. Shards are
+// disjoint and the means snapshot is read-only, so the order in which shards
+// run does not change the semantics (the reference runs them as independent
+// threads). Heads in flight <= grid threads / G (the hogwild cap).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "sgd_device.cuh"
+#include "sgd_kernels.cuh"
+
+// Tuning knobs (compile-time; the Makefile default is the measured best).
+#ifndef HOG_MINB
+#define HOG_MINB 3        // min resident blocks per SM (register cap)
+#endif
+#ifndef HOG_G16
+#define HOG_G16 4         // lanes per head when k <= 16
+#endif
+#ifndef HOG_ROUNDS
+#define HOG_ROUNDS 4      // rounds of 256/G heads per scheduled chunk
+#endif
+#ifndef HOG_CAS
+#define HOG_CAS 0         // 1: one 128-bit CAS per row instead of two RED.F64 (measured 1.9x slower)
+#endif
+#ifndef HOG_MF32
+#define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
+#endif
+
+namespace nb {
+
+template <int G>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Atomic x/y add on one 16-byte row with a single 128-bit compare-and-swap
+// (one L2 tag request instead of two RED.F64). `seen` returns the value the
+// row held; the add succeeded iff it equals `expect` bitwise.
+__device__ __forceinline__ double2 cas128(double2* p, double2 expect, double2 desired) {
+  unsigned long long r0, r1;
+  asm volatile(
+      "{\n\t.reg .b128 e, d, r;\n\t"
+      "mov.b128 e, {%2, %3};\n\t"
+      "mov.b128 d, {%4, %5};\n\t"
+      "atom.global.cas.b128 r, [%6], e, d;\n\t"
+      "mov.b128 {%0, %1}, r;\n\t}"
+      : "=l"(r0), "=l"(r1)
+      : "l"(__double_as_longlong(expect.x)), "l"(__double_as_longlong(expect.y)),
+        "l"(__double_as_longlong(desired.x)), "l"(__double_as_longlong(desired.y)), "l"(p)
+      : "memory");
+  return make_double2(__longlong_as_double(r0), __longlong_as_double(r1));
+}
+__device__ __forceinline__ bool same_bits(double2 a, double2 b) {
+  return __double_as_longlong(a.x) == __double_as_longlong(b.x) &&
+         __double_as_longlong(a.y) == __double_as_longlong(b.y);
+}
+// Finish a CAS-add whose first attempt returned `seen` for expected `old`.
+__device__ __forceinline__ void cas_add_finish(double2* p, double2 old, double2 seen, double ax,
+                                               double ay) {
+  while (!same_bits(seen, old)) {
+    old = seen;
+    seen = cas128(p, old, make_double2(old.x + ax, old.y + ay));
+  }
+}
+
+template <int NPL>
+__device__ __forceinline__ void load_ids(const uint32_t* p, uint32_t (&v)[NPL]) {
+  if constexpr (NPL == 4) {
+    const uint4 x = *reinterpret_cast<const uint4*>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else if constexpr (NPL == 2) {
+    const uint2 x = *reinterpret_cast<const uint2*>(p);
+    v[0] = x.x; v[1] = x.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < NPL; j += 4) {
+      const uint4 x = *reinterpret_cast<const uint4*>(p + j);
+      v[j] = x.x; v[j + 1] = x.y; v[j + 2] = x.z; v[j + 3] = x.w;
+    }
+  }
+}
+
+template <int G, int KMAX, int SMAX>
+__global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
+  constexpr int NPL = KMAX / G;            // neighbour slots per lane
+  constexpr int TPL = (SMAX + G - 1) / G;  // tail slots per lane
+  constexpr int GPB = 256 / G;             // heads per block per round
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[8];
+  __shared__ uint32_t s_chunk;
+  const uint32_t k = P.k, s = P.s, C = P.n_clusters;
+  const double M = (double)P.m_total;
+  const int gl = threadIdx.x % G;
+  const int grp = threadIdx.x / G;
+  const int g0 = (threadIdx.x & 31) & ~(G - 1);  // first lane of my group
+  double* wt = sm;
+  double* tab = sm + ((((k + 1) * k) + 1) & ~1u);
+  for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
+
+  uint32_t cur = 0xFFFFFFFFu;
+  WorkerDev W{};
+  uint32_t ncell = 0;
+  double sf_w = 0.0, loss_acc = 0.0, edge_acc = 0.0;
+  const double st = P.step;
+  const uint32_t nblk_draw = (s + 2) / 2;  // Philox blocks per head (2 draws each)
+
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = atomicAdd(P.chunk_counter, 1u);
+    __syncthreads();
+    const uint32_t c = s_chunk;
+    uint32_t w = 0;
+    if (c < P.total_chunks)
+      while (w + 1 < P.n_workers && c >= P.workers[w + 1].chunk0) ++w;
+    if (c >= P.total_chunks || w != cur) {  // block-uniform
+      if (cur != 0xFFFFFFFFu) {  // flush the previous shard's statistics
+        const double ls = block_sum(loss_acc, red);
+        const double es = block_sum(edge_acc, red);
+        if (threadIdx.x == 0) {
+          atomicAdd(&P.loss_acc[cur], ls);
+          atomicAdd(&P.edge_acc[cur], (unsigned long long)es);
+        }
+        loss_acc = 0.0;
+        edge_acc = 0.0;
+      }
+      if (c >= P.total_chunks) break;
+      cur = w;
+      W = P.workers[w];
+      ncell = P.all_but_own ? C : W.n_rem;
+      sf_w = M * W.local_mass / (double)s;
+      __syncthreads();
+      for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
+        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
+        const double p = P.all_but_own ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
+#if HOG_MF32
+        float* tf = reinterpret_cast<float*>(tab);
+        tf[3 * q] = (float)P.means[r].x;
+        tf[3 * q + 1] = (float)P.means[r].y;
+        tf[3 * q + 2] = (float)(M * p);
+#else
+        tab[3 * q] = P.means[r].x;
+        tab[3 * q + 1] = P.means[r].y;
+        tab[3 * q + 2] = M * p;
+#endif
+      }
+      __syncthreads();
+    }
+    const uint32_t t_base = (c - W.chunk0) * P.chunk_heads;
+    // chunk_heads is a multiple of GPB, so every warp runs the same number of
+    // rounds: all shuffles below are executed by full warps (inactive groups
+    // at the end of a shard run predicated off).
+    for (uint32_t j = grp; j < P.chunk_heads; j += GPB) {
+      const uint32_t t = t_base + j;
+      const bool act = t < W.draws;
+      // ---- draws: lane b of the group computes Philox block b = draws 2b, 2b+1
+      uint64_t dA = 0, dB = 0;
+      if (gl < (int)nblk_draw) {
+        const u32x4 r = philox4x32_10(u32x4{t, W.id, (uint32_t)P.epoch, (uint32_t)gl},
+                                      P.seed_lo, P.seed_hi);
+        dA = join64(r.x, r.y);
+        dB = join64(r.z, r.w);
+      }
+      const uint64_t d0 = __shfl_sync(0xffffffffu, dA, g0);
+      const uint32_t hidx = act ? bounded(d0, W.n_elig) : 0u;
+      const uint32_t head = (W.all_elig || !act) ? W.pstart + hidx : P.elig[W.elig_off + hidx];
+      uint32_t pool0 = W.pstart, pooln = W.npts, own_gid = 0xFFFFFFFFu;
+      double sf = sf_w;
+      if (P.all_but_own) {  // optimizer.hpp:264-277
+        const LocalCluster L = P.lclusters[P.cl_of[head]];
+        pool0 = L.start;
+        pooln = L.count;
+        own_gid = L.gid;
+        sf = M * P.cell_probs[L.gid] / (double)s;
+      }
+      // tails owned by this lane: q = gl + G m uses draw 1 + q
+      uint32_t tl[TPL];
+#pragma unroll
+      for (int m = 0; m < TPL; ++m) {
+        const int q = gl + G * m;
+        const int d = 1 + q;
+        const int src = g0 + (((d >> 1) < G) ? (d >> 1) : 0);
+        const uint64_t a = __shfl_sync(0xffffffffu, dA, src);
+        const uint64_t b = __shfl_sync(0xffffffffu, dB, src);
+        tl[m] = (act && q < (int)s) ? pool0 + bounded((d & 1) ? b : a, pooln) : head;
+      }
+      // ---- gathers (all issued before any use)
+      const uint32_t cnt = act ? (P.ncnt ? P.ncnt[head] : k) : 0u;
+      uint32_t nb[NPL];
+      load_ids<NPL>(P.ell + (size_t)head * P.kpad + NPL * gl, nb);
+      const double2 h = P.pos[head];
+      double2 pn[NPL], pt[TPL];
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? P.pos[nb[i]] : h;
+#pragma unroll
+      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? P.pos[tl[m]] : h;
+
+      // ---- mean field over this lane's cells: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
+      double s1 = 0.0, s2x = 0.0, s2y = 0.0;
+#if HOG_MF32
+      {
+        const float* tf = reinterpret_cast<const float*>(tab);
+        const float hx = (float)h.x, hy = (float)h.y;
+        float f1 = 0.f, fx = 0.f, fy = 0.f;
+        for (uint32_t q = gl; q < ncell; q += G) {
+          if (P.all_but_own && q == own_gid) continue;
+          const float dx = hx - tf[3 * q], dy = hy - tf[3 * q + 1];
+          const float qq = __frcp_rn(fmaf(dx, dx, fmaf(dy, dy, 1.f)));
+          const float pq = tf[3 * q + 2] * qq;
+          f1 += pq;
+          const float pq2 = pq * qq;
+          fx = fmaf(pq2, dx, fx);
+          fy = fmaf(pq2, dy, fy);
+        }
+        s1 = f1;
+        s2x = fx;
+        s2y = fy;
+      }
+#else
+      for (uint32_t q = gl; q < ncell; q += G) {
+        if (P.all_but_own && q == own_gid) continue;
+        const double dx = h.x - tab[3 * q], dy = h.y - tab[3 * q + 1];
+        const double qq = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
+        const double pq = tab[3 * q + 2] * qq;
+        s1 += pq;
+        const double pq2 = pq * qq;
+        s2x = fma(pq2, dx, s2x);
+        s2y = fma(pq2, dy, s2y);
+      }
+#endif
+      // ---- sampled negatives
+      double qn[TPL], qsum = 0.0;
+#pragma unroll
+      for (int m = 0; m < TPL; ++m) {
+        qn[m] = 0.0;
+        if (act && gl + G * m < (int)s) {
+          const double dx = h.x - pt[m].x, dy = h.y - pt[m].y;
+          qn[m] = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
+          qsum += qn[m];
+        }
+      }
+      s1 = gsum<G>(s1);
+      qsum = gsum<G>(qsum);
+      const double bg = fma(sf, qsum, s1);
+      // ---- attraction over this lane's neighbours; their updates go out now
+      const double* wrow = wt + cnt * k;
+      double gx = 0.0, gy = 0.0, bgs = 0.0;
+      float lf = 0.f;
+#if HOG_CAS
+      double2 dn[NPL], dt[TPL];
+#endif
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        const int jj = NPL * gl + i;
+        if (jj < (int)cnt) {
+          const double dx = h.x - pn[i].x, dy = h.y - pn[i].y;
+          const double q = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
+          const double inv = frcp(q + bg);
+          const double wj = wrow[jj];
+          lf -= (float)wj * __logf((float)(q * inv));
+          bgs = fma(wj, inv, bgs);
+          const double pull = 2.0 * wj * q * bg * inv;
+          gx = fma(pull, dx, gx);
+          gy = fma(pull, dy, gy);
+          if (!P.head_only) {
+            const double a = st * pull;
+#if HOG_CAS
+            dn[i] = make_double2(a * dx, a * dy);
+#else
+            atomicAdd(&P.pos[nb[i]].x, a * dx);
+            atomicAdd(&P.pos[nb[i]].y, a * dy);
+#endif
+          }
+        }
+      }
+      bgs = gsum<G>(bgs);
+      // ---- negative repulsion
+      const double c2 = 2.0 * bgs * sf;
+#pragma unroll
+      for (int m = 0; m < TPL; ++m) {
+        if (act && gl + G * m < (int)s) {
+          const double dx = h.x - pt[m].x, dy = h.y - pt[m].y;
+          const double push = c2 * qn[m] * qn[m];
+          gx = fma(-push, dx, gx);
+          gy = fma(-push, dy, gy);
+          if (!P.head_only) {
+            const double a = -st * push;
+#if HOG_CAS
+            dt[m] = make_double2(a * dx, a * dy);
+#else
+            atomicAdd(&P.pos[tl[m]].x, a * dx);
+            atomicAdd(&P.pos[tl[m]].y, a * dy);
+#endif
+          }
+        }
+      }
+      // ---- mean repulsion + head update (lane 0 of the group)
+      gx = gsum<G>(fma(-2.0 * bgs, s2x, gx));
+      gy = gsum<G>(fma(-2.0 * bgs, s2y, gy));
+#if HOG_CAS
+      // All of this lane's row updates go out back to back (independent
+      // ATOMG.CAS.128 in flight), then the rare failed ones are retried.
+      {
+        const bool upd = act && !P.head_only;
+        double2 sn[NPL], stt[TPL], sh = h;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i)
+          if (upd && NPL * gl + i < (int)cnt)
+            sn[i] = cas128(&P.pos[nb[i]], pn[i], make_double2(pn[i].x + dn[i].x, pn[i].y + dn[i].y));
+#pragma unroll
+        for (int m = 0; m < TPL; ++m)
+          if (upd && gl + G * m < (int)s)
+            stt[m] = cas128(&P.pos[tl[m]], pt[m], make_double2(pt[m].x + dt[m].x, pt[m].y + dt[m].y));
+        const double hx = -st * gx, hy = -st * gy;
+        if (act && gl == 0) sh = cas128(&P.pos[head], h, make_double2(h.x + hx, h.y + hy));
+#pragma unroll
+        for (int i = 0; i < NPL; ++i)
+          if (upd && NPL * gl + i < (int)cnt) cas_add_finish(&P.pos[nb[i]], pn[i], sn[i], dn[i].x, dn[i].y);
+#pragma unroll
+        for (int m = 0; m < TPL; ++m)
+          if (upd && gl + G * m < (int)s) cas_add_finish(&P.pos[tl[m]], pt[m], stt[m], dt[m].x, dt[m].y);
+        if (act && gl == 0) {
+          cas_add_finish(&P.pos[head], h, sh, hx, hy);
+          edge_acc += (double)(cnt + s);
+        }
+      }
+#else
+      if (act && gl == 0) {
+        atomicAdd(&P.pos[head].x, -st * gx);
+        atomicAdd(&P.pos[head].y, -st * gy);
+        edge_acc += (double)(cnt + s);
+      }
+#endif
+      loss_acc += (double)lf;
+    }
+  }
+}
+
+template <int G, int KMAX, int SMAX>
+static void hog_go(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st,
+                   int* per_sm) {
+  auto kern = k_sgd_hogwild<G, KMAX, SMAX>;
+  if (smem > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (per_sm) {
+    NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, 256, smem));
+    return;
+  }
+  kern<<<nblocks, 256, smem, st>>>(P);
+}
+
+static void hog_dispatch(const SgdParams& P, uint32_t kpad, uint32_t s, uint32_t nblocks,
+                         size_t smem, cudaStream_t st, int* per_sm) {
+  if (s > 15) fail(kParameter, "throughput mode supports local_draws <= 15");
+  if (kpad <= 16 && s <= 7) {
+    if (s <= 4) hog_go<HOG_G16, 16, 4>(P, nblocks, smem, st, per_sm);
+    else hog_go<HOG_G16, 16, 8>(P, nblocks, smem, st, per_sm);
+  } else if (kpad <= 16) {
+    hog_go<8, 16, 16>(P, nblocks, smem, st, per_sm);
+  } else if (kpad <= 32) {
+    hog_go<8, 32, 16>(P, nblocks, smem, st, per_sm);
+  } else if (kpad <= 64) {
+    hog_go<8, 64, 16>(P, nblocks, smem, st, per_sm);
+  } else {
+    fail(kParameter, "throughput mode supports k <= 64");
+  }
+}
+
+uint32_t hogwild_group_size(uint32_t kpad, uint32_t s) {
+  return (kpad <= 16 && s <= 7) ? HOG_G16 : 8;
+}
+uint32_t hogwild_chunk_rounds() { return HOG_ROUNDS; }
+
+void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st) {
+  hog_dispatch(P, P.kpad, P.s, nblocks, smem, st, nullptr);
+}
+
+uint32_t hogwild_resident_blocks(uint32_t kpad, uint32_t s, size_t smem, int sm_count) {
+  int per_sm = 0;
+  hog_dispatch(SgdParams{}, kpad, s, 0, smem, nullptr, &per_sm);
+  return (uint32_t)std::max(1, per_sm) * (uint32_t)sm_count;
+}
+
+}  // namespace nb

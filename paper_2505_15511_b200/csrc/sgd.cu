@@ -4,44 +4,10 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "sgd_device.cuh"
 #include "sgd_kernels.cuh"
 
 namespace nb {
-
-// ---------------------------------------------------------------- helpers
-
-// Exact Cauchy kernel, reference op order, no contraction (objective.hpp:36-41).
-__device__ __forceinline__ double cauchy_rn(double a0, double a1, double b0, double b1) {
-  const double dx = __dsub_rn(a0, b0), dy = __dsub_rn(a1, b1);
-  const double sq = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-  return __ddiv_rn(1.0, __dadd_rn(1.0, sq));
-}
-
-// Fast fp64 reciprocal for throughput mode: MUFU.RCP64H seed + one cubic
-// Newton correction (rel. error ~2^-69 before rounding => ~1 ulp).
-__device__ __forceinline__ double frcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);
-  return fma(r, fma(e, e, e), r);
-}
-
-// optimizer.hpp:220-221 divergence predicate.
-__device__ __forceinline__ bool diverged(double x, double y) {
-  return !isfinite(x) || !isfinite(y) || fabs(x) > 1e9 || fabs(y) > 1e9;
-}
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-  return s;  // valid on thread 0
-}
 
 // ------------------------------------------------------- K8r replay kernel
 //
@@ -182,161 +148,6 @@ __global__ void k_loss_seq(const double* slot, const uint32_t* base, const Worke
   out[w] = acc;
 }
 
-// ------------------------------------------------------ K8p hogwild kernel
-//
-// Throughput mode, thread per head. Draws come from Philox4x32-10 keyed by
-// (seed, epoch, worker, draw t): head ~ U(eligible_w), tails ~ U(pool_w)
-// exactly as optimizer.hpp:254-255/:284-285 define the distributions. All
-// (1 + k + s) rows are gathered up front (MLP), the gradient is the
-// reference's (objective.hpp:178-237) with algebraic reuse
-// (pull = 2 w q bg / (q + bg), mean push folded into one sum), and updates
-// are fp64 atomic scatter-adds (RED.ADD.F64). Heads in flight per worker are
-// bounded by the grid share the host gives the worker (hogwild cap).
-template <int KMAX, int SMAX>
-__global__ void __launch_bounds__(256, 2) k_sgd_hogwild(SgdParams P) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ double red[8];
-  uint32_t w = 0;
-  while (w + 1 < P.n_workers && blockIdx.x >= P.workers[w + 1].blk_start) ++w;
-  const WorkerDev W = P.workers[w];
-  const uint32_t k = P.k, s = P.s, C = P.n_clusters;
-  const double M = (double)P.m_total;
-  double* wt = sm;                              // (k+1)*k
-  double* tab = sm + (((k + 1) * k + 1) & ~1u);  // 3 per cell: mu.x, mu.y, M*p
-  const uint32_t ncell = P.all_but_own ? C : W.n_rem;
-  for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
-  for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
-    const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
-    const double p = P.all_but_own ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
-    tab[3 * q] = P.means[r].x;
-    tab[3 * q + 1] = P.means[r].y;
-    tab[3 * q + 2] = M * p;
-  }
-  __syncthreads();
-
-  const uint32_t nthr = W.nblk * blockDim.x;
-  const uint32_t tid = (blockIdx.x - W.blk_start) * blockDim.x + threadIdx.x;
-  const double sf_w = M * W.local_mass / (double)s;
-  const double st = P.step;
-  double loss_acc = 0.0;
-  unsigned long long edges = 0;
-  for (uint32_t t = tid; t < W.draws; t += nthr) {
-    // --- draws (1 + s) x 64 bits
-    uint64_t rnd[2 * ((SMAX + 2) / 2)];
-#pragma unroll
-    for (int c = 0; c < (SMAX + 2) / 2; ++c) {
-      const u32x4 r = philox4x32_10(u32x4{t, W.id, (uint32_t)P.epoch, (uint32_t)c},
-                                    P.seed_lo, P.seed_hi);
-      rnd[2 * c] = join64(r.x, r.y);
-      rnd[2 * c + 1] = join64(r.z, r.w);
-    }
-    const uint32_t head = P.elig[W.elig_off + bounded(rnd[0], W.n_elig)];
-    uint32_t pool0 = W.pstart, pooln = W.npts, own_gid = 0xFFFFFFFFu;
-    double sf = sf_w;
-    if (P.all_but_own) {
-      const LocalCluster L = P.lclusters[P.cl_of[head]];
-      pool0 = L.start;
-      pooln = L.count;
-      own_gid = L.gid;
-      sf = M * P.cell_probs[L.gid] / (double)s;
-    }
-    // --- gathers
-    const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
-    uint32_t nb[KMAX];
-    const uint32_t* row = P.ell + (size_t)head * P.kpad;
-#pragma unroll
-    for (int j = 0; j < KMAX; j += 4) {
-      const uint4 v = *reinterpret_cast<const uint4*>(row + j);
-      nb[j] = v.x; nb[j + 1] = v.y; nb[j + 2] = v.z; nb[j + 3] = v.w;
-    }
-    uint32_t tl[SMAX];
-#pragma unroll
-    for (int q = 0; q < SMAX; ++q) tl[q] = q < (int)s ? pool0 + bounded(rnd[1 + q], pooln) : 0;
-    const double2 h = P.pos[head];
-    double2 pn[KMAX], pt[SMAX];
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) pn[j] = j < (int)cnt ? P.pos[nb[j]] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < SMAX; ++q) pt[q] = q < (int)s ? P.pos[tl[q]] : make_double2(0.0, 0.0);
-
-    // --- mean field: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
-    double s1 = 0.0, s2x = 0.0, s2y = 0.0;
-    for (uint32_t q = 0; q < ncell; ++q) {
-      if (P.all_but_own && q == own_gid) continue;
-      const double dx = h.x - tab[3 * q], dy = h.y - tab[3 * q + 1];
-      const double qq = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
-      const double pq = tab[3 * q + 2] * qq;
-      s1 += pq;
-      const double pq2 = pq * qq;
-      s2x = fma(pq2, dx, s2x);
-      s2y = fma(pq2, dy, s2y);
-    }
-    // --- sampled negatives
-    double qn[SMAX], qsum = 0.0;
-#pragma unroll
-    for (int q = 0; q < SMAX; ++q) {
-      if (q < (int)s) {
-        const double dx = h.x - pt[q].x, dy = h.y - pt[q].y;
-        qn[q] = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
-        qsum += qn[q];
-      }
-    }
-    const double bg = fma(sf, qsum, s1);
-    // --- attraction; neighbour updates issued immediately
-    const double* wrow = wt + cnt * k;
-    double gx = 0.0, gy = 0.0, bgs = 0.0;
-    float lf = 0.f;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-      if (j < (int)cnt) {
-        const double dx = h.x - pn[j].x, dy = h.y - pn[j].y;
-        const double q = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
-        const double inv = frcp(q + bg);
-        const double wj = wrow[j];
-        lf -= (float)wj * __logf((float)(q * inv));
-        bgs = fma(wj, inv, bgs);
-        const double pull = 2.0 * wj * q * bg * inv;
-        gx = fma(pull, dx, gx);
-        gy = fma(pull, dy, gy);
-        if (!P.head_only) {
-          const double a = st * pull;
-          atomicAdd(&P.pos[nb[j]].x, a * dx);
-          atomicAdd(&P.pos[nb[j]].y, a * dy);
-        }
-      }
-    }
-    // --- negative repulsion
-    const double c2 = 2.0 * bgs * sf;
-#pragma unroll
-    for (int q = 0; q < SMAX; ++q) {
-      if (q < (int)s) {
-        const double dx = h.x - pt[q].x, dy = h.y - pt[q].y;
-        const double push = c2 * qn[q] * qn[q];
-        gx = fma(-push, dx, gx);
-        gy = fma(-push, dy, gy);
-        if (!P.head_only) {
-          const double a = -st * push;
-          atomicAdd(&P.pos[tl[q]].x, a * dx);
-          atomicAdd(&P.pos[tl[q]].y, a * dy);
-        }
-      }
-    }
-    // --- mean repulsion, then the head update
-    gx = fma(-2.0 * bgs, s2x, gx);
-    gy = fma(-2.0 * bgs, s2y, gy);
-    atomicAdd(&P.pos[head].x, -st * gx);
-    atomicAdd(&P.pos[head].y, -st * gy);
-    loss_acc += (double)lf;
-    edges += cnt + s;
-  }
-  const double ls = block_sum(loss_acc, red);
-  const double es = block_sum((double)edges, red);
-  if (threadIdx.x == 0) {
-    atomicAdd(&P.loss_acc[w], ls);
-    atomicAdd(&P.edge_acc[w], (unsigned long long)es);
-  }
-}
-
 // ------------------------------------------------------ K9 cluster means
 //
 // Exact: per local cluster and coordinate, a sequential sum over the
@@ -444,34 +255,6 @@ void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cuda
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
                      double* out, cudaStream_t st) {
   k_loss_seq<<<blocks_for(nw, 32), 32, 0, st>>>(slot, base, wk, nw, out);
-}
-
-void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st) {
-  if (P.s > 8) fail(kParameter, "throughput mode supports local_draws <= 8");
-  auto go = [&](auto kern) {
-    if (smem > 48 * 1024)
-      NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<nblocks, 256, smem, st>>>(P);
-  };
-  if (P.kpad <= 16 && P.s == 5) go(k_sgd_hogwild<16, 5>);
-  else if (P.kpad <= 16) go(k_sgd_hogwild<16, 8>);
-  else if (P.kpad <= 32) go(k_sgd_hogwild<32, 8>);
-  else if (P.kpad <= 64) go(k_sgd_hogwild<64, 8>);
-  else fail(kParameter, "throughput mode supports k <= 64");
-}
-
-uint32_t hogwild_resident_blocks(uint32_t kpad, uint32_t s, size_t smem, int sm_count) {
-  int per_sm = 0;
-  auto q = [&](auto kern) {
-    if (smem > 48 * 1024)
-      NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-  };
-  if (kpad <= 16 && s == 5) q(k_sgd_hogwild<16, 5>);
-  else if (kpad <= 16) q(k_sgd_hogwild<16, 8>);
-  else if (kpad <= 32) q(k_sgd_hogwild<32, 8>);
-  else q(k_sgd_hogwild<64, 8>);
-  return (uint32_t)std::max(1, per_sm) * (uint32_t)sm_count;
 }
 
 void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,

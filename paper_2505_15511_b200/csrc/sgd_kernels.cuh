@@ -18,8 +18,8 @@ struct WorkerDev {
   uint32_t elig_off, n_elig;  // eligible heads (local ids) in elig[]
   uint32_t rem_off, n_rem;    // remote cells R~ (RemoteClusters mode)
   uint32_t draws;             // heads drawn this epoch (= n_elig)
-  uint32_t blk_start;         // first block of this worker (hogwild grid)
-  uint32_t nblk;              // blocks of this worker
+  uint32_t chunk0;            // first hogwild chunk of this worker (worker-major)
+  uint32_t all_elig;          // eligible == all points (head = pstart + idx)
   uint32_t id;                // global worker id
   double local_mass;          // optimizer.hpp:369-370
 };
@@ -50,6 +50,9 @@ struct SgdParams {
   double step;
   uint64_t epoch;
   uint32_t seed_lo, seed_hi;
+  // hogwild dynamic schedule (chunks of chunk_heads draws, worker-major)
+  uint32_t* chunk_counter;
+  uint32_t total_chunks, chunk_heads;
   // replay tape (level-ordered)
   const uint32_t* tape_head;    // local id per draw (level order)
   const uint32_t* tape_tails;   // s local ids per draw
@@ -67,6 +70,8 @@ void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* 
                      double* out, cudaStream_t st);
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st);
 uint32_t hogwild_resident_blocks(uint32_t kpad, uint32_t s, size_t smem, int sm_count);
+uint32_t hogwild_group_size(uint32_t kpad, uint32_t s);
+uint32_t hogwild_chunk_rounds();
 void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,
                         cudaStream_t st);
 void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,

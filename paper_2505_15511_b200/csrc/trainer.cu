@@ -84,7 +84,8 @@ struct nomad_b200_trainer {
   std::vector<std::mt19937_64> rng;
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
-  uint32_t hog_blocks = 0;
+  uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0;
+  DBuf<uint32_t> chunk_counter;
 
   DBuf<double2> pos, means;
   DBuf<uint32_t> ell, elig, remote_ids, orig_of_d, cl_of, slot_gid, chunk_off;
@@ -396,24 +397,29 @@ struct nomad_b200_trainer {
   }
 
   void plan_hogwild_grid() {
+    // Heads in flight (grid threads / G) <= min shard size / cap (SURVEY
+    // Appendix C.6), and never more blocks than are resident at once (the
+    // kernel pulls chunks dynamically, so extra blocks would only idle).
     const uint32_t cap = cfg.hogwild_cap ? cfg.hogwild_cap : 16;
-    // The grid never exceeds what is resident at once (the kernel loops over
-    // its draws with a grid stride, so a second wave would only add a tail).
-    const uint64_t budget = hogwild_resident_blocks((uint32_t)kpad, (uint32_t)s, smem_hog, ctx->sm_count);
-    uint64_t total = 0;
-    for (auto& d : wk) total += d.draws;
-    uint32_t blk = 0;
+    const uint32_t G = hogwild_group_size((uint32_t)kpad, (uint32_t)s);
+    const uint64_t resident = hogwild_resident_blocks((uint32_t)kpad, (uint32_t)s, smem_hog, ctx->sm_count);
+    uint64_t min_pts = ~0ull;
+    for (auto& d : wk)
+      if (d.draws) min_pts = std::min<uint64_t>(min_pts, d.npts);
+    if (min_pts == ~0ull) min_pts = 1;
+    const uint64_t heads_per_block = 256 / G;
+    const uint64_t by_cap = std::max<uint64_t>(1, (min_pts / cap + heads_per_block - 1) / heads_per_block);
+    hog_blocks = (uint32_t)std::min<uint64_t>(resident, by_cap);
+    chunk_heads = (uint32_t)(heads_per_block * hogwild_chunk_rounds());
+    uint32_t c = 0;
     for (auto& d : wk) {
-      d.blk_start = blk;
-      if (d.draws == 0) { d.nblk = 0; continue; }
-      const uint64_t cap_thr = std::max<uint64_t>(32, d.npts / cap);
-      const uint64_t by_cap = (cap_thr + 255) / 256;
-      const uint64_t by_draws = (d.draws + 255) / 256;
-      const uint64_t share = std::max<uint64_t>(1, (budget * d.draws + total - 1) / std::max<uint64_t>(total, 1));
-      d.nblk = (uint32_t)std::max<uint64_t>(1, std::min({by_cap, by_draws, share}));
-      blk += d.nblk;
+      d.chunk0 = c;
+      d.all_elig = d.n_elig == d.npts ? 1u : 0u;
+      c += (d.draws + chunk_heads - 1) / chunk_heads;
     }
-    hog_blocks = blk;
+    total_chunks = c;
+    chunk_counter.alloc(1);
+    if (total_chunks == 0) hog_blocks = 0;
   }
 
   void compute_means_and_exchange() {
@@ -488,6 +494,9 @@ struct nomad_b200_trainer {
     const uint64_t sk = mix_seed(cfg.seed ^ 0x686f67776c64ull);
     P.seed_lo = (uint32_t)sk;
     P.seed_hi = (uint32_t)(sk >> 32);
+    P.chunk_counter = chunk_counter.p;
+    P.total_chunks = total_chunks;
+    P.chunk_heads = chunk_heads;
     return P;
   }
 
@@ -622,6 +631,7 @@ struct nomad_b200_trainer {
       } else {
         NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
         NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
+        NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
         NB_CUDA(cudaEventRecord(ev[0], S));
         if (hog_blocks) {
           launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
