@@ -159,6 +159,15 @@ int32_t nomad_b200_kmeans_em(nomad_b200_ctx* ctx,
                              const nomad_b200_dataset_view* data,
                              nomad_b200_clusters* inout, uint64_t max_iters,
                              double tol, double* qe_trace, uint64_t* iters_out);
+/* kmeans_em(data, init, max_iters, default_kmeans_tol(data)) as fit() calls
+ * it (optimizer.hpp:337-339). The tolerance is bracketed from a parallel
+ * sum and resolved exactly (sequential sum) only if a max_move falls inside
+ * the bracket, so the result equals the reference's. */
+int32_t nomad_b200_kmeans_em_default_tol(nomad_b200_ctx* ctx,
+                                         const nomad_b200_dataset_view* data,
+                                         nomad_b200_clusters* inout,
+                                         uint64_t max_iters, double* qe_trace,
+                                         uint64_t* iters_out);
 /* knn.hpp:65-109 build_knn. clusters: assignment + sizes. */
 int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx,
                              const nomad_b200_dataset_view* data,

@@ -71,6 +71,9 @@ _SIGS = {
     "nomad_b200_kmeans_em": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(ClustersView),
                                          C.c_uint64, C.c_double, _vp,
                                          C.POINTER(C.c_uint64)]),
+    "nomad_b200_kmeans_em_default_tol": (C.c_int32, [_vp, C.POINTER(DatasetView),
+                                                     C.POINTER(ClustersView), C.c_uint64, _vp,
+                                                     C.POINTER(C.c_uint64)]),
     "nomad_b200_build_knn": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(ClustersView),
                                          C.c_uint64, C.c_int32, C.POINTER(GraphView)]),
     "nomad_b200_trainer_create": (C.c_int32, [_vp, C.POINTER(GraphView), C.POINTER(ClustersView),

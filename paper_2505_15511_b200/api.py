@@ -221,6 +221,30 @@ def kmeans_em(data, init: ClusterAssignment, max_iters: int = 100, tol: float = 
     return ca
 
 
+def kmeans_em_default_tol(data, init: ClusterAssignment, max_iters: int = 100,
+                          qe_trace: Optional[list] = None,
+                          ctx: Optional[Context] = None) -> ClusterAssignment:
+    """kmeans_em(data, init, max_iters, default_kmeans_tol(data)) exactly as fit()
+    calls it (optimizer.hpp:337-339), without the sequential tolerance sum
+    unless a stop decision needs it."""
+    dv, keep = _dataset(data)
+    if len(init.assignment) != dv.rows or init.dims != dv.dims:
+        raise NomadError("Parameter", "init assignment does not match dataset")
+    ca = ClusterAssignment(np.array(init.assignment, np.uint32), init.n_clusters, init.dims,
+                           np.array(init.centroids, np.float64).reshape(-1),
+                           np.array(init.sizes, np.uint32))
+    v = ca._view()
+    trace = np.zeros(max(max_iters, 1), np.float64) if qe_trace is not None else None
+    iters = C.c_uint64()
+    check(lib().nomad_b200_kmeans_em_default_tol(_ctx(ctx).h, C.byref(dv), C.byref(v), max_iters,
+                                                 trace.ctypes.data if trace is not None else None,
+                                                 C.byref(iters)))
+    if qe_trace is not None:
+        qe_trace.clear()
+        qe_trace.extend(trace[: iters.value].tolist())
+    return ca
+
+
 def build_knn(data, clusters: ClusterAssignment, k: int, mode: str = "exact",
               ctx: Optional[Context] = None) -> KnnGraph:
     """knn.hpp:65-109"""

@@ -1,0 +1,152 @@
+// Stable grouping by label and exact sequential column means (see
+// index_common.cuh).
+#include <cub/cub.cuh>
+
+#include "index_common.cuh"
+
+namespace nb {
+
+namespace {
+
+constexpr uint32_t kChunk = 4096;
+
+// Per-chunk label histogram, label-major: hist[label * nchunks + chunk].
+__global__ void k_chunk_hist(const uint32_t* labels, uint64_t n, uint32_t L, uint32_t nchunks,
+                             uint32_t* hist) {
+  extern __shared__ uint32_t h[];
+  const bool use_smem = L <= 8192;
+  const uint64_t c = blockIdx.x;
+  const uint64_t b = c * kChunk, e = umin64(b + kChunk, n);
+  if (use_smem) {
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      const uint32_t l = labels[i];
+      if (l < L) atomicAdd(&h[l], 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) hist[(uint64_t)i * nchunks + c] = h[i];
+  } else {
+    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      const uint32_t l = labels[i];
+      if (l < L) atomicAdd(&hist[(uint64_t)l * nchunks + c], 1u);
+    }
+  }
+}
+
+// One warp per chunk walks its points in order; __match_any_sync ranks equal
+// labels inside each 32-point batch, so the scatter preserves id order.
+__global__ void k_chunk_scatter(const uint32_t* labels, uint64_t n, uint32_t L, uint32_t nchunks,
+                                uint32_t* cursor, uint32_t* members) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp >= nchunks) return;
+  const uint64_t b = (uint64_t)warp * kChunk, e = umin64(b + kChunk, n);
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint64_t base = b; base < e; base += 32) {
+    const uint64_t i = base + lane;
+    const uint32_t l = i < e ? labels[i] : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, l);
+    const uint32_t rank = __popc(peers & lt);
+    const bool leader = (peers >> lane) == 1u;  // highest lane of the group
+    uint32_t pos = 0;
+    if (l < L) pos = cursor[(uint64_t)l * nchunks + warp] + rank;
+    __syncwarp();
+    if (l < L && leader) cursor[(uint64_t)l * nchunks + warp] += __popc(peers);
+    __syncwarp();
+    if (l < L) members[pos] = (uint32_t)i;
+  }
+}
+
+__global__ void k_extract_offsets(const uint32_t* scanned, const uint32_t* hist, uint32_t L,
+                                  uint32_t nchunks, uint64_t* off) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < L) off[r] = scanned[(uint64_t)r * nchunks];
+  if (r == L - 1) {
+    const uint64_t last = (uint64_t)r * nchunks + nchunks - 1;
+    off[L] = (uint64_t)scanned[last] + hist[last];
+  }
+}
+
+// Warp per (segment, 32-column group); lanes own columns. Members are walked
+// in order with a 2-stage register pipeline of U rows to keep loads in flight
+// while the dependent fp64 adds retire (reference order, no reassociation).
+template <int U>
+__global__ void k_seq_colsum(const float* __restrict__ x, uint64_t d, const uint32_t* members,
+                             const uint64_t* seg_beg, const uint64_t* seg_cnt,
+                             const uint32_t* seg_row, uint32_t nseg, double* out) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t groups = (uint32_t)((d + 31) / 32);
+  if (gw >= (uint64_t)nseg * groups) return;
+  const uint32_t sidx = gw / groups;
+  const uint64_t j = (uint64_t)(gw % groups) * 32 + lane;
+  const uint64_t beg = seg_beg[sidx], cnt = seg_cnt[sidx];
+  if (cnt == 0) return;
+  const bool colok = j < d;
+  double acc = 0.0;
+  float a[U], b[U];
+  auto row = [&](uint64_t t) -> uint64_t { return members ? members[beg + t] : beg + t; };
+  uint64_t t = 0;
+  for (; t + 2 * U <= cnt; t += 2 * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = colok ? __ldg(x + row(t + u) * d + j) : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) b[u] = colok ? __ldg(x + row(t + U + u) * d + j) : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)a[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)b[u]);
+  }
+  for (; t < cnt; ++t) acc = __dadd_rn(acc, colok ? (double)__ldg(x + row(t) * d + j) : 0.0);
+  if (colok) out[(uint64_t)seg_row[sidx] * d + j] = __ddiv_rn(acc, (double)cnt);
+}
+
+}  // namespace
+
+void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uint32_t L,
+                    DBuf<uint32_t>& members, std::vector<uint64_t>& off) {
+  cudaStream_t S = ctx->stream;
+  const uint32_t nchunks = (uint32_t)((n + kChunk - 1) / kChunk);
+  const uint64_t H = (uint64_t)L * nchunks;
+  DBuf<uint32_t> hist(H), scanned(H);
+  NB_CUDA(cudaMemsetAsync(hist.p, 0, H * 4, S));
+  k_chunk_hist<<<nchunks, 256, L <= 8192 ? L * 4 : 0, S>>>(labels, n, L, nchunks, hist.p);
+  note_launch(ctx, "k_chunk_hist");
+  size_t tmp = 0;
+  NB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hist.p, scanned.p, (int64_t)H, S));
+  DBuf<uint8_t> tb(tmp + 1);
+  NB_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, tmp, hist.p, scanned.p, (int64_t)H, S));
+  note_launch(ctx, "cub_exclusive_sum");
+  DBuf<uint64_t> offd(L + 1);
+  k_extract_offsets<<<(L + 255) / 256, 256, 0, S>>>(scanned.p, hist.p, L, nchunks, offd.p);
+  note_launch(ctx, "k_extract_offsets");
+  off.assign(L + 1, 0);
+  NB_CUDA(cudaMemcpyAsync(off.data(), offd.p, (L + 1) * 8, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  members.alloc(std::max<uint64_t>(off[L], 1));
+  // scanned now serves as the per-(label, chunk) write cursor
+  k_chunk_scatter<<<(nchunks * 32 + 255) / 256, 256, 0, S>>>(labels, n, L, nchunks, scanned.p,
+                                                              members.p);
+  note_launch(ctx, "k_chunk_scatter");
+}
+
+void seq_column_means(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+                      const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
+                      const std::vector<uint32_t>& seg_ids, double* out) {
+  cudaStream_t S = ctx->stream;
+  const uint32_t nseg = (uint32_t)seg_ids.size();
+  if (!nseg) return;
+  DBuf<uint64_t> db(nseg), dc(nseg);
+  DBuf<uint32_t> dr(nseg);
+  NB_CUDA(cudaMemcpyAsync(db.p, beg.data(), nseg * 8, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(dc.p, cnt.data(), nseg * 8, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(dr.p, seg_ids.data(), nseg * 4, cudaMemcpyHostToDevice, S));
+  const uint64_t warps = (uint64_t)nseg * ((d + 31) / 32);
+  k_seq_colsum<32><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, S>>>(x, d, members, db.p, dc.p,
+                                                                       dr.p, nseg, out);
+  note_launch(ctx, "k_seq_colsum");
+  NB_CUDA(cudaStreamSynchronize(S));
+}
+
+}  // namespace nb

@@ -1,0 +1,88 @@
+// Shared pieces of the index build (k-means partitioner, kNN graph):
+// device-resident dataset views, the reference Rng on the host, stable
+// grouping of points by label, exact sequential column sums.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <random>
+#include <vector>
+
+#include "common.cuh"
+
+namespace nb {
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// The reference's Rng (rng.hpp:25-84): splitmix stream seeds, mt19937_64,
+// rejection-sampled bounded ints, 53-bit uniforms, Box-Muller with a cached
+// spare. Host-side (it seeds the LSH planes and the perturbation draws,
+// O(planes x d) values; libm gives the reference's bits on this image).
+struct HostRng {
+  std::mt19937_64 g;
+  double spare = 0.0;
+  bool have = false;
+  static uint64_t mix(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+  }
+  static uint64_t stream_seed(uint64_t base, uint64_t s) { return mix(base ^ mix(s)); }
+  explicit HostRng(uint64_t seed) : g(seed) {}
+  double uniform01() { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+  double gaussian() {
+    if (have) {
+      have = false;
+      return spare;
+    }
+    double u = uniform01();
+    while (u == 0.0) u = uniform01();
+    const double v = uniform01();
+    const double radius = std::sqrt(-2.0 * std::log(u));
+    const double angle = 6.283185307179586476925286766559 * v;
+    spare = radius * std::sin(angle);
+    have = true;
+    return radius * std::cos(angle);
+  }
+};
+
+// A dataset on the device (uploaded once per call when the caller passed
+// host memory).
+struct DevData {
+  const float* x = nullptr;
+  uint64_t n = 0, d = 0;
+  DBuf<float> owned;
+  void bind(const nomad_b200_dataset_view* v, cudaStream_t st) {
+    if (!v || !v->data) fail(kParameter, "dataset view is NULL");
+    n = v->rows;
+    d = v->dims;
+    if (n < 1 || d < 1) fail(kParameter, "empty dataset");
+    if (n >= 0xFFFFFFFFull) fail(kSize, "point ids are u32 (n < 2^32)");
+    if (v->location == NOMAD_B200_DEVICE) {
+      x = v->data;
+    } else {
+      owned.alloc(n * d);
+      NB_CUDA(cudaMemcpyAsync(owned.p, v->data, n * d * 4, cudaMemcpyHostToDevice, st));
+      x = owned.p;
+    }
+  }
+};
+
+// Stable grouping of [0, n) by label (labels >= L are dropped): members of
+// label r are written to members[off[r] .. off[r+1]) in ascending id order.
+// off (host) receives L + 1 offsets.
+void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uint32_t L,
+                    DBuf<uint32_t>& members, std::vector<uint64_t>& off);
+
+// out[seg_ids[s] * d + j] = (sum over members[beg[s] .. beg[s] + cnt[s]),
+// in order, of (double) x[m * d + j]) / cnt[s]  — the reference's sequential centroid /
+// mean accumulation (kmeans.hpp:75-104, :176-181, :218-226) bit for bit.
+// members == nullptr means the identity list. Segments with count 0 are
+// left untouched.
+void seq_column_means(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+                      const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
+                      const std::vector<uint32_t>& seg_ids, double* out);
+
+}  // namespace nb
