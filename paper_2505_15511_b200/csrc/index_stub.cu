@@ -2,10 +2,6 @@
 #include "common.cuh"
 using namespace nb;
 extern "C" {
-int32_t nomad_b200_build_knn(nomad_b200_ctx*, const nomad_b200_dataset_view*,
-                             const nomad_b200_clusters*, uint64_t, int32_t, nomad_b200_graph*) {
-  return guard([&] { fail(kInternal, "build_knn: not built yet"); });
-}
 int32_t nomad_b200_fit(nomad_b200_ctx*, const nomad_b200_dataset_view*,
                        const nomad_b200_train_config*, const double*, double*,
                        nomad_b200_clusters*, nomad_b200_graph*, double*) {

@@ -1,0 +1,523 @@
+// K6 + K7: exact within-cluster kNN graph (knn.hpp:51-109) on the GPU.
+//
+// Pass 1 (filter, FFMA): per cluster, a block takes 64 query points and
+// streams every 128-point candidate tile of the same cluster through shared
+// memory, computing fp32 direct-difference distances sum (a - b)^2. Each
+// query keeps its KP smallest approximate distances (threshold + shared
+// buffer, compacted by a warp when it passes KP entries).
+// Pass 2 (re-rank + certificate): a warp per query recomputes the KP
+// survivors with the reference's fp64 j-ascending chain (bit-identical
+// distances), sorts by (distance, id) and keeps min(k, size-1). The fp32
+// chain has relative error <= g32 = (d+3)u32 against the exact distance and
+// the reference's fp64 chain <= g64 = d u64, so every excluded candidate has
+// reference distance >= T / (1 + g32) * (1 - g64), T = the KP-th approximate
+// distance. If that bound is above the k-th re-ranked distance, the top-k is
+// certified exact; otherwise the query goes to pass 3.
+// Pass 3 (fallback, rare): exhaustive fp64 for uncertified queries.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "index_common.cuh"
+
+namespace nb {
+
+namespace {
+
+constexpr int QT = 64;    // queries per block
+constexpr int CT = 128;   // candidates per tile
+constexpr int DK = 32;    // dims per smem chunk
+
+struct ClusterSeg {
+  uint64_t beg;   // offset into members
+  uint32_t size;  // members in the cluster
+  uint32_t qtile; // first query tile index of this cluster
+};
+
+template <int KP>
+__device__ void compact_warp(float* bd, uint32_t* bi, uint32_t& cnt, float& tau, int lane) {
+  // keep the KP smallest (dist) of cnt <= KP + CT entries, by repeated
+  // warp-wide min extraction; tau = KP-th smallest.
+  constexpr int PER = (KP + CT + 31) / 32;
+  float v[PER];
+  uint32_t id[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const uint32_t p = lane + 32 * e;
+    v[e] = p < cnt ? bd[p] : __int_as_float(0x7f800000);
+    id[e] = p < cnt ? bi[p] : 0xFFFFFFFFu;
+  }
+  __syncwarp();
+  float last = __int_as_float(0x7f800000);
+  for (int r = 0; r < KP; ++r) {
+    // local min
+    float m = v[0];
+    int me = 0;
+#pragma unroll
+    for (int e = 1; e < PER; ++e)
+      if (v[e] < m) { m = v[e]; me = e; }
+    float wm = m;
+    int wl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, wm, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, wl, o);
+      if (om < wm || (om == wm && ol < wl)) { wm = om; wl = ol; }
+    }
+    uint32_t wid = 0;
+#pragma unroll
+    for (int e = 0; e < PER; ++e)
+      if (lane == wl && e == me) wid = id[e];
+    wid = __shfl_sync(0xffffffffu, wid, wl);
+    if (lane == wl) {
+#pragma unroll
+      for (int e = 0; e < PER; ++e)
+        if (e == me) v[e] = __int_as_float(0x7f800000);
+    }
+    if (lane == 0) {
+      bd[r] = wm;
+      bi[r] = wid;
+    }
+    last = wm;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    cnt = KP;
+    tau = last;
+  }
+  __syncwarp();
+}
+
+// Pass 1. grid = total query tiles; block 256 = 16 x 16 threads; thread
+// (tx, ty) owns queries ty + 16 i (4) and candidates tx + 16 c (8).
+template <int KP>
+__global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__ x, uint32_t d,
+                                                       const uint32_t* __restrict__ members,
+                                                       const ClusterSeg* segs, uint32_t nseg,
+                                                       uint32_t* cand_ids, float* cand_tau,
+                                                       uint32_t* cand_cnt) {
+  constexpr int CAP = KP + CT;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  float(*qs)[DK + 1] = reinterpret_cast<float(*)[DK + 1]>(smraw);
+  float(*cs)[DK + 1] = reinterpret_cast<float(*)[DK + 1]>(smraw + QT * (DK + 1) * 4);
+  float* bd = reinterpret_cast<float*>(smraw + (QT + CT) * (DK + 1) * 4);
+  uint32_t* bi = reinterpret_cast<uint32_t*>(bd + QT * CAP);
+  uint32_t* cnt = bi + QT * CAP;
+  float* tau = reinterpret_cast<float*>(cnt + QT);
+  uint32_t* qid = reinterpret_cast<uint32_t*>(tau + QT);
+  __shared__ int any_full;
+
+  // which cluster / query tile
+  uint32_t s = 0;
+  {
+    uint32_t lo = 0, hi = nseg;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) / 2;
+      if (segs[mid].qtile <= blockIdx.x) lo = mid; else hi = mid;
+    }
+    s = lo;
+  }
+  const ClusterSeg S = segs[s];
+  const uint32_t q0 = (blockIdx.x - S.qtile) * QT;  // query offset inside the cluster
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = threadIdx.x; q < QT; q += 256) {
+    cnt[q] = 0;
+    tau[q] = __int_as_float(0x7f800000);
+    qid[q] = q0 + q < S.size ? members[S.beg + q0 + q] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < S.size; c0 += CT) {
+    float acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+    for (uint32_t j0 = 0; j0 < d; j0 += DK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < QT * DK; e += 256) {
+        const int p = e / DK, jj = e % DK;
+        const uint32_t g = qid[p];
+        qs[p][jj] = (g != 0xFFFFFFFFu && j0 + jj < d) ? x[(uint64_t)g * d + j0 + jj] : 0.f;
+      }
+      for (int e = threadIdx.x; e < CT * DK; e += 256) {
+        const int p = e / DK, jj = e % DK;
+        const uint32_t cl = c0 + p;
+        cs[p][jj] = (cl < S.size && j0 + jj < d)
+                        ? x[(uint64_t)members[S.beg + cl] * d + j0 + jj] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int jj = 0; jj < DK; ++jj) {
+        float qv[4], cv[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qv[i] = qs[ty + 16 * i][jj];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) cv[c] = cs[tx + 16 * c][jj];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float df = qv[i] - cv[c];
+            acc[i][c] = fmaf(df, df, acc[i][c]);
+          }
+      }
+    }
+    // insert below-threshold candidates
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q = ty + 16 * i;
+      const uint32_t gq = qid[q];
+      if (gq == 0xFFFFFFFFu) continue;
+      const float t = tau[q];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t cl = c0 + tx + 16 * c;
+        if (cl < S.size && cl != q0 + q && acc[i][c] < t) {
+          const uint32_t pos = atomicAdd(&cnt[q], 1u);
+          bd[q * CAP + pos] = acc[i][c];
+          bi[q * CAP + pos] = members[S.beg + cl];
+        }
+      }
+    }
+    if (threadIdx.x == 0) any_full = 0;
+    __syncthreads();
+    for (int q = threadIdx.x; q < QT; q += 256)
+      if (cnt[q] > KP) any_full = 1;
+    __syncthreads();
+    if (any_full) {
+      for (int q = warp; q < QT; q += 8)
+        if (cnt[q] > KP) compact_warp<KP>(bd + q * CAP, bi + q * CAP, cnt[q], tau[q], lane);
+      __syncthreads();
+    }
+  }
+  // write survivors
+  for (int q = warp; q < QT; q += 8) {
+    const uint32_t gq = qid[q];
+    if (gq == 0xFFFFFFFFu) continue;
+    const uint32_t c = cnt[q];
+    if (lane < (int)c) cand_ids[(uint64_t)gq * KP + lane] = bi[q * CAP + lane];
+    if (KP > 32 && lane + 32 < (int)c) cand_ids[(uint64_t)gq * KP + lane + 32] = bi[q * CAP + lane + 32];
+    if (lane == 0) {
+      cand_cnt[gq] = c;
+      cand_tau[gq] = c == KP ? tau[q] : __int_as_float(0x7f800000);
+    }
+  }
+}
+
+// Reference fp64 distance (knn.hpp:51-58), j ascending, no FMA.
+__device__ __forceinline__ double ref_dist(const float* __restrict__ a, const float* __restrict__ b,
+                                           uint32_t d) {
+  double acc = 0.0;
+  uint32_t j = 0;
+  if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+    for (; j + 4 <= d; j += 4) {
+      const float4 u = *reinterpret_cast<const float4*>(a + j);
+      const float4 v = *reinterpret_cast<const float4*>(b + j);
+      double t = __dsub_rn((double)u.x, (double)v.x);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)u.y, (double)v.y);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)u.z, (double)v.z);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)u.w, (double)v.w);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+  }
+  for (; j < d; ++j) {
+    const double t = __dsub_rn((double)a[j], (double)b[j]);
+    acc = __dadd_rn(acc, __dmul_rn(t, t));
+  }
+  return acc;
+}
+
+__device__ __forceinline__ bool key_less(double da, uint32_t ia, double db, uint32_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+// Pass 2: warp per query; lanes own KP/32 survivors each; warp bitonic sort
+// by (distance, id).
+template <int KP>
+__global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t n,
+                             const uint32_t* assign, const uint32_t* sizes, uint32_t k,
+                             const uint32_t* cand_ids, const float* cand_tau,
+                             const uint32_t* cand_cnt, const uint32_t* offsets, uint32_t* out_nb,
+                             double* out_d, uint32_t* fallback, uint32_t* n_fallback,
+                             double lb_factor) {
+  constexpr int PER = KP / 32;
+  const uint64_t q = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= n) return;
+  const uint32_t size = sizes[assign[q]];
+  const uint32_t want = min(k, size - 1);
+  if (want == 0) return;
+  const uint32_t c = cand_cnt[q];
+  double dv[PER];
+  uint32_t iv[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int p = lane + 32 * e;  // slot
+    if (p < (int)c) {
+      iv[e] = cand_ids[q * KP + p];
+      dv[e] = ref_dist(x + q * d, x + (uint64_t)iv[e] * d, d);
+    } else {
+      iv[e] = 0xFFFFFFFFu;
+      dv[e] = __longlong_as_double(0x7ff0000000000000ll);
+    }
+  }
+  // select the `want` smallest (distance, id) keys in order by repeated
+  // warp-wide min extraction; rank r goes to out[o + r].
+  const uint32_t o = offsets[q];
+  double dk = 0.0;
+  for (uint32_t r = 0; r < want; ++r) {
+    double m = dv[0];
+    uint32_t mi = iv[0];
+    int me = 0;
+#pragma unroll
+    for (int e = 1; e < PER; ++e)
+      if (key_less(dv[e], iv[e], m, mi)) { m = dv[e]; mi = iv[e]; me = e; }
+    double wm = m;
+    uint32_t wi = mi;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double om = __shfl_xor_sync(0xffffffffu, wm, off);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, wi, off);
+      if (key_less(om, oi, wm, wi)) { wm = om; wi = oi; }
+    }
+    if (mi == wi && wi != 0xFFFFFFFFu) {  // ids are unique: the owner retires it
+#pragma unroll
+      for (int e = 0; e < PER; ++e)
+        if (e == me) { dv[e] = __longlong_as_double(0x7ff0000000000000ll); iv[e] = 0xFFFFFFFFu; }
+    }
+    if (lane == 0) {
+      out_nb[o + r] = wi;
+      if (out_d) out_d[o + r] = wm;
+    }
+    dk = wm;
+  }
+  // certificate (dk = the want-th exact distance among the survivors)
+  const float t = cand_tau[q];
+  const bool complete = c < KP || isinf(t);
+  const bool ok = complete || (double)t * lb_factor > dk;
+  if (!ok && lane == 0) fallback[atomicAdd(n_fallback, 1u)] = (uint32_t)q;
+}
+
+// Pass 3: one block per uncertified query, exhaustive fp64 over its cluster;
+// per-thread sorted top-`want`, merged by warp 0.
+__global__ void __launch_bounds__(128) k_knn_exhaustive(
+    const float* __restrict__ x, uint32_t d, const uint32_t* assign, const uint32_t* members,
+    const uint64_t* cl_beg, const uint32_t* sizes, uint32_t k, const uint32_t* fallback,
+    const uint32_t* offsets, uint32_t* out_nb, double* out_d) {
+  constexpr int KMAX = 64;
+  __shared__ double sd[128 * 8];
+  __shared__ uint32_t si[128 * 8];
+  const uint32_t q = fallback[blockIdx.x];
+  const uint32_t r = assign[q];
+  const uint32_t size = sizes[r];
+  const uint32_t want = min(k, size - 1);
+  const uint64_t beg = cl_beg[r];
+  double bd[KMAX];
+  uint32_t bi[KMAX];
+  uint32_t cnt = 0;
+  for (uint32_t t = threadIdx.x; t < size; t += blockDim.x) {
+    const uint32_t j = members[beg + t];
+    if (j == q) continue;
+    const double dd = ref_dist(x + (uint64_t)q * d, x + (uint64_t)j * d, d);
+    if (cnt == want && !key_less(dd, j, bd[want - 1], bi[want - 1])) continue;
+    uint32_t pos = cnt < want ? cnt : want - 1;
+    while (pos > 0 && key_less(dd, j, bd[pos - 1], bi[pos - 1])) {
+      bd[pos] = bd[pos - 1];
+      bi[pos] = bi[pos - 1];
+      --pos;
+    }
+    bd[pos] = dd;
+    bi[pos] = j;
+    if (cnt < want) ++cnt;
+  }
+  // merge: repeatedly take the global min of the per-thread list heads
+  uint32_t head = 0;
+  const uint32_t o = offsets[q];
+  for (uint32_t r2 = 0; r2 < want; ++r2) {
+    double v = head < cnt ? bd[head] : __longlong_as_double(0x7ff0000000000000ll);
+    uint32_t vi = head < cnt ? bi[head] : 0xFFFFFFFFu;
+    sd[threadIdx.x] = v;
+    si[threadIdx.x] = vi;
+    __syncthreads();
+    for (int st = 64; st > 0; st >>= 1) {
+      if ((int)threadIdx.x < st) {
+        if (key_less(sd[threadIdx.x + st], si[threadIdx.x + st], sd[threadIdx.x], si[threadIdx.x])) {
+          sd[threadIdx.x] = sd[threadIdx.x + st];
+          si[threadIdx.x] = si[threadIdx.x + st];
+        }
+      }
+      __syncthreads();
+    }
+    const uint32_t win = si[0];
+    const double wd = sd[0];
+    if (threadIdx.x == 0) {
+      out_nb[o + r2] = win;
+      if (out_d) out_d[o + r2] = wd;
+    }
+    if (head < cnt && bi[head] == win) ++head;
+    __syncthreads();
+  }
+}
+
+__global__ void k_knn_want(const uint32_t* assign, const uint32_t* sizes, uint64_t n, uint32_t k,
+                           uint32_t* want) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = sizes[assign[i]];
+    want[i] = min(k, s - 1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) want[n] = 0;
+}
+
+__global__ void k_sizes2(const uint32_t* a, uint64_t n, uint32_t* sizes) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&sizes[a[i]], 1u);
+}
+
+}  // namespace
+
+// Builds the exact graph into device buffers (offsets n+1, nb/dist offsets[n]).
+struct KnnResult {
+  DBuf<uint32_t> offsets, nb;
+  DBuf<double> dist;
+  uint64_t edges = 0;
+  uint64_t fallbacks = 0;
+};
+
+void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                     const uint32_t* assign_d, uint32_t C, uint32_t k, KnnResult& R) {
+  cudaStream_t S = ctx->stream;
+  if (k < 1) fail(kParameter, "k must be >= 1");
+  if (k > 56) fail(kParameter, "k > 56 is not supported by the exact kNN build");
+  DBuf<uint32_t> sizes(C);
+  NB_CUDA(cudaMemsetAsync(sizes.p, 0, C * 4, S));
+  k_sizes2<<<(unsigned)std::min<uint64_t>(4096, (n + 255) / 256), 256, 0, S>>>(assign_d, n, sizes.p);
+  note_launch(ctx, "k_sizes");
+  // offsets = exclusive scan of min(k, size-1) (knn.hpp:77-83)
+  DBuf<uint32_t> want(n + 1);
+  k_knn_want<<<(unsigned)std::min<uint64_t>(4096, (n + 255) / 256), 256, 0, S>>>(assign_d, sizes.p, n, k, want.p);
+  note_launch(ctx, "k_knn_want");
+  R.offsets.alloc(n + 1);
+  size_t tmp = 0;
+  NB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, want.p, R.offsets.p, (int64_t)(n + 1), S));
+  DBuf<uint8_t> tb(tmp + 1);
+  NB_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, tmp, want.p, R.offsets.p, (int64_t)(n + 1), S));
+  note_launch(ctx, "cub_exclusive_sum");
+  uint32_t edges = 0;
+  NB_CUDA(cudaMemcpyAsync(&edges, R.offsets.p + n, 4, cudaMemcpyDeviceToHost, S));
+  // members per cluster, ascending id (knn.hpp:70-72)
+  DBuf<uint32_t> mem;
+  std::vector<uint64_t> off;
+  group_by_label(ctx, assign_d, n, C, mem, off);
+  R.edges = edges;
+  R.nb.alloc(std::max<uint64_t>(edges, 1));
+  R.dist.alloc(std::max<uint64_t>(edges, 1));
+  // segments / query tiles
+  std::vector<ClusterSeg> segs;
+  uint32_t tiles = 0;
+  for (uint32_t r = 0; r < C; ++r) {
+    const uint32_t sz = (uint32_t)(off[r + 1] - off[r]);
+    if (sz < 2) continue;
+    segs.push_back(ClusterSeg{off[r], sz, tiles});
+    tiles += (sz + QT - 1) / QT;
+  }
+  if (tiles == 0) {
+    NB_CUDA(cudaStreamSynchronize(S));
+    return;
+  }
+  DBuf<ClusterSeg> segs_d(segs.size());
+  NB_CUDA(cudaMemcpyAsync(segs_d.p, segs.data(), segs.size() * sizeof(ClusterSeg),
+                          cudaMemcpyHostToDevice, S));
+  const int KP = k <= 24 ? 32 : 64;
+  DBuf<uint32_t> cid(n * (uint64_t)KP), ccnt(n);
+  DBuf<float> ctau(n);
+  NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
+  auto filt = [&](auto kern, int kp) {
+    const size_t smem = (size_t)(QT + CT) * (DK + 1) * 4 + (size_t)QT * (kp + CT) * 8 + QT * 12;
+    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<tiles, 256, smem, S>>>(x, (uint32_t)d, mem.p, segs_d.p, (uint32_t)segs.size(), cid.p,
+                                  ctau.p, ccnt.p);
+  };
+  if (KP == 32) filt(k_knn_filter<32>, 32); else filt(k_knn_filter<64>, 64);
+  note_launch(ctx, "k_knn_filter");
+  // certificate factor: T / (1 + g32) * (1 - g64), rounded down generously
+  const double g32 = (double)(d + 3) * 0x1p-24 / (1.0 - (double)(d + 3) * 0x1p-24);
+  const double g64 = (double)(d + 1) * 0x1p-53 / (1.0 - (double)(d + 1) * 0x1p-53);
+  const double lbf = (1.0 - g64) / (1.0 + g32) * (1.0 - 1e-12);
+  DBuf<uint32_t> fb(n), nfb(1);
+  NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
+  const unsigned rb = (unsigned)((n * 32 + 255) / 256);
+  if (KP == 32)
+    k_knn_rerank<32><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, ctau.p,
+                                        ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, lbf);
+  else
+    k_knn_rerank<64><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, ctau.p,
+                                        ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, lbf);
+  note_launch(ctx, "k_knn_rerank");
+  uint32_t nf = 0;
+  NB_CUDA(cudaMemcpyAsync(&nf, nfb.p, 4, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  R.fallbacks = nf;
+  if (nf) {
+    std::vector<uint64_t> cb(C);
+    for (uint32_t r = 0; r < C; ++r) cb[r] = off[r];
+    DBuf<uint64_t> cb_d(C);
+    NB_CUDA(cudaMemcpyAsync(cb_d.p, cb.data(), C * 8, cudaMemcpyHostToDevice, S));
+    k_knn_exhaustive<<<nf, 128, 0, S>>>(x, (uint32_t)d, assign_d, mem.p, cb_d.p, sizes.p, k, fb.p,
+                                        R.offsets.p, R.nb.p, R.dist.p);
+    note_launch(ctx, "k_knn_exhaustive");
+  }
+  NB_CUDA(cudaStreamSynchronize(S));
+}
+
+}  // namespace nb
+
+using namespace nb;
+
+extern "C" {
+
+int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                             const nomad_b200_clusters* clusters, uint64_t k, int32_t knn_mode,
+                             nomad_b200_graph* out) {
+  return guard([&] {
+    if (!ctx || !clusters || !out) fail(kParameter, "NULL argument");
+    if (k < 1) fail(kParameter, "k must be >= 1");
+    bind_device(ctx);
+    cudaStream_t S = ctx->stream;
+    DevData dd;
+    dd.bind(data, S);
+    if (clusters->rows != dd.n) fail(kParameter, "clusters and dataset cover different points");
+    if (!clusters->assignment) fail(kParameter, "assignment is NULL");
+    const uint32_t C = (uint32_t)clusters->n_clusters;
+    DBuf<uint32_t> a_own;
+    const uint32_t* a = clusters->assignment;
+    if (clusters->location != NOMAD_B200_DEVICE) {
+      a_own.alloc(dd.n);
+      NB_CUDA(cudaMemcpyAsync(a_own.p, a, dd.n * 4, cudaMemcpyHostToDevice, S));
+      a = a_own.p;
+    }
+    if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16)
+      fail(kParameter, "unknown knn_mode");
+    KnnResult R;
+    build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R);
+    const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
+                                                         : cudaMemcpyDeviceToHost;
+    NB_CUDA(cudaMemcpyAsync(out->offsets, R.offsets.p, (dd.n + 1) * 4, kind, S));
+    if (R.edges) {
+      NB_CUDA(cudaMemcpyAsync(out->neighbors, R.nb.p, R.edges * 4, kind, S));
+      if (out->distances)
+        NB_CUDA(cudaMemcpyAsync(out->distances, R.dist.p, R.edges * 8, kind, S));
+    }
+    NB_CUDA(cudaStreamSynchronize(S));
+    out->rows = dd.n;
+    out->k = k;
+  });
+}
+
+}  // extern "C"
