@@ -222,6 +222,12 @@ int32_t nomad_b200_trainer_progress(nomad_b200_trainer* tr,
                                     uint64_t* epochs_done,
                                     uint64_t* edge_updates);
 
+/* pca.hpp:79-218 pca_init on the GPU (tolerance parity: the covariance
+ * passes are tree-reduced fp64; the vector algebra, Rng stream, sign rule and
+ * rank-1 jitter follow the reference exactly). layout_out: rows x 2 f64. */
+int32_t nomad_b200_pca_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                            uint64_t seed, double* layout_out, int32_t location);
+
 /* --------------------------------------------------- fit (L4) */
 /* optimizer.hpp:327-482 fit. init_layout: the PCA initialisation
  * (pca.hpp:79, rows x 2; NULL = computed on the GPU by power iteration).
@@ -233,6 +239,14 @@ int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                        nomad_b200_graph* graph_out, double* epoch_loss_out);
 
 /* ------------------------------------------- helpers (multi-GPU, data) */
+/* Host-only: shard_clusters' LPT plan (optimizer.hpp:106-144) for `workers`
+ * logical workers mapped to `world` ranks in contiguous blocks, and the slot
+ * layout of the per-epoch means all-gather: slot_cluster[world * max_slots]
+ * holds the cluster id of each rank's slot (UINT32_MAX = padding; NULL to
+ * skip). cluster_to_worker: n_clusters entries. */
+int32_t nomad_b200_plan(uint64_t n, uint64_t n_clusters, const uint32_t* assignment,
+                        uint64_t workers, int32_t world, uint32_t* cluster_to_worker,
+                        uint32_t* slot_cluster, uint32_t* max_slots);
 /* ncclGetUniqueId into 128 bytes (rank 0 calls it, then broadcasts). */
 int32_t nomad_b200_nccl_unique_id(void* out128);
 /* Synthetic Gaussian mixture on the device: centres

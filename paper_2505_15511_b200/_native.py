@@ -88,8 +88,11 @@ _SIGS = {
     "nomad_b200_trainer_timing": (C.c_int32, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                               C.POINTER(C.c_uint64)]),
     "nomad_b200_trainer_progress": (C.c_int32, [_vp] + [C.POINTER(C.c_uint64)] * 2),
+    "nomad_b200_pca_init": (C.c_int32, [_vp, C.POINTER(DatasetView), C.c_uint64, _vp, C.c_int32]),
     "nomad_b200_fit": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(TrainConfigC), _vp,
                                    _vp, C.POINTER(ClustersView), C.POINTER(GraphView), _vp]),
+    "nomad_b200_plan": (C.c_int32, [C.c_uint64, C.c_uint64, _vp, C.c_uint64, C.c_int32, _vp, _vp,
+                                    C.POINTER(C.c_uint32)]),
     "nomad_b200_nccl_unique_id": (C.c_int32, [_vp]),
     "nomad_b200_generate_mixture": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
                                                 C.c_double, C.c_uint64, _vp]),

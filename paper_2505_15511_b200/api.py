@@ -408,6 +408,15 @@ def fit(data, config: TrainConfig, init_layout=None, report: Optional[FitReport]
     return out
 
 
+def pca_init(data, seed: int = 0, ctx: Optional[Context] = None) -> np.ndarray:
+    """pca.hpp:79-218 on the GPU (tolerance parity; see nomad_b200_pca_init)."""
+    dv, keep = _dataset(data)
+    out = np.zeros((dv.rows, 2), np.float64)
+    check(lib().nomad_b200_pca_init(_ctx(ctx).h, C.byref(dv), seed & (2**64 - 1),
+                                    out.ctypes.data, N.HOST))
+    return out
+
+
 def generate_mixture(rows: int, dims: int, blobs: int, spread: float = 10.0, seed: int = 42,
                      out=None, ctx: Optional[Context] = None):
     """Device synthetic Gaussian mixture into a CUDA float32 tensor (rows x dims)."""
@@ -424,3 +433,20 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().nomad_b200_nccl_unique_id(buf))
     return buf.raw
+
+
+def shard_plan(assignment, n_clusters: int, workers: int, world_size: int = 1):
+    """shard_clusters (optimizer.hpp:106-144) + the means all-gather slot layout.
+
+    Returns (cluster_to_worker[C], slot_cluster[world, max_slots]) where
+    slot_cluster[r, q] is the cluster whose mean rank r sends in slot q
+    (0xFFFFFFFF = padding). Host-only; identical to what the trainer uses."""
+    a = np.ascontiguousarray(assignment, np.uint32)
+    c2w = np.zeros(n_clusters, np.uint32)
+    ms = C.c_uint32()
+    check(lib().nomad_b200_plan(len(a), n_clusters, a.ctypes.data, workers, world_size,
+                                c2w.ctypes.data, None, C.byref(ms)))
+    slots = np.zeros(world_size * ms.value, np.uint32)
+    check(lib().nomad_b200_plan(len(a), n_clusters, a.ctypes.data, workers, world_size,
+                                c2w.ctypes.data, slots.ctypes.data, C.byref(ms)))
+    return c2w, slots.reshape(world_size, ms.value)

@@ -15,6 +15,7 @@
 #include <random>
 
 #include "common.cuh"
+#include "plan.cuh"
 #include "sgd_kernels.cuh"
 
 using namespace nb;
@@ -166,28 +167,10 @@ struct nomad_b200_trainer {
     for (uint64_t r = 0; r < C; ++r)
       if (sizes[r] == 0) fail(kInternal, "empty cluster in means gather");
 
-    // shard_clusters (optimizer.hpp:106-144): LPT
-    if (C < W)
-      fail(kParameter, "clusters must be >= workers (" + std::to_string(C) + " < " +
-                           std::to_string(W) + ")");
-    std::vector<uint32_t> order(C);
-    std::iota(order.begin(), order.end(), 0u);
-    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-      if (sizes[a] != sizes[b]) return sizes[a] > sizes[b];
-      return a < b;
-    });
-    c2w.assign(C, 0);
-    std::vector<uint64_t> load(W, 0);
-    std::vector<std::vector<uint32_t>> wclusters(W);
-    for (uint32_t c : order) {
-      uint32_t light = 0;
-      for (uint32_t w = 1; w < W; ++w)
-        if (load[w] < load[light]) light = w;
-      c2w[c] = light;
-      wclusters[light].push_back(c);
-      load[light] += sizes[c];
-    }
-    for (auto& v : wclusters) std::sort(v.begin(), v.end());
+    // shard_clusters (optimizer.hpp:106-144) + rank / slot layout (plan.cu)
+    ShardPlan plan = make_plan(sizes, W, world);
+    c2w = plan.c2w;
+    const auto& wclusters = plan.wclusters;
 
     nwl = W / world;
     w0 = rank * nwl;
@@ -348,16 +331,9 @@ struct nomad_b200_trainer {
       NB_CUDA(cudaStreamSynchronize(S));
     }
     // means exchange: fixed slots per rank, static slot -> cluster map
-    std::vector<uint32_t> per_rank(world, 0);
-    for (uint64_t r = 0; r < C; ++r) ++per_rank[c2w[r] / nwl];
-    max_slots = *std::max_element(per_rank.begin(), per_rank.end());
-    std::vector<uint32_t> sg((size_t)world * max_slots, 0xFFFFFFFFu);
-    for (int rk = 0; rk < world; ++rk) {
-      uint32_t q = 0;
-      for (uint32_t wl = 0; wl < nwl; ++wl)
-        for (uint32_t c : wclusters[rk * nwl + wl]) sg[(size_t)rk * max_slots + q++] = c;
-    }
-    upload(slot_gid, sg, S);
+    max_slots = plan.max_slots;
+    const std::vector<uint32_t>& sg = plan.slot_cluster;
+    upload(slot_gid, std::vector<uint32_t>(sg), S);
     slot.alloc(2 * (size_t)max_slots);
     NB_CUDA(cudaMemsetAsync(slot.p, 0, slot.bytes(), S));
     recv.alloc(2 * (size_t)world * max_slots);

@@ -1,0 +1,86 @@
+"""fit() end to end on the B200 (optimizer.hpp:327-482) against the
+reference / oracle, and the GPU PCA initialisation (pca.hpp:79-218)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _pipeline(O, x, C, W, epochs, seed):
+    from oracle import train_config
+    c = O.lsh_init(x, C, seed)
+    c = O.kmeans_em(x, c, 100, O.default_kmeans_tol(x))
+    g = O.build_knn(x, c, 15)
+    pca = O.pca_init(x, seed)
+    cfg = train_config(epochs=epochs, workers=W, seed=seed, n_clusters=C)
+    lay, loss, means, _ = O.train_epochs(c.assignment, C, g.offsets, g.neighbors, 15, cfg, pca)
+    return c, g, pca, lay, loss
+
+
+def test_fit_bit_exact_with_injected_pca(port, ctx):
+    """Replay-mode fit with the reference's PCA layout injected reproduces the
+    reference's fit bit for bit (clusters, graph, layout)."""
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(3000, 24, 8, 10.0, 17)
+    c, g, pca, lay, loss = _pipeline(port, x, 6, 3, 8, 5)
+    rep = nb.FitReport()
+    cfg = nb.TrainConfig(epochs=8, workers=3, seed=5, n_clusters=6)
+    out = nb.fit(x, cfg, init_layout=pca, report=rep, ctx=ctx)
+    assert np.array_equal(rep.clusters.assignment, c.assignment)
+    assert np.array_equal(rep.graph.neighbors, g.neighbors)
+    assert np.array_equal(rep.graph.distances, g.distances)
+    assert np.array_equal(out, lay)
+    np.testing.assert_allclose(rep.epoch_mean_loss, loss, rtol=1e-13, atol=0)
+
+
+def test_fit_epochs_zero_returns_init(port, ctx):
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(800, 10, 4, 10.0, 3)
+    pca = port.pca_init(x, 1)
+    out = nb.fit(x, nb.TrainConfig(epochs=0, workers=2, seed=1, n_clusters=4), init_layout=pca,
+                 ctx=ctx)
+    assert np.array_equal(out, pca)
+
+
+@pytest.mark.parametrize("n,d,blobs", [(3000, 24, 8), (2000, 200, 5)])
+def test_gpu_pca_tolerance(port, ctx, n, d, blobs):
+    """Tolerance parity: same sign convention, |delta| <= 1e-8 per coordinate
+    of the unit-SD columns (the power iteration's stop rule is 1e-30 on the
+    squared drift, so the remaining difference is summation order)."""
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(n, d, blobs, 10.0, 23)
+    ref = port.pca_init(x, 9)
+    got = nb.pca_init(x, 9, ctx=ctx)
+    assert np.max(np.abs(got - ref)) < 1e-8
+
+
+def test_gpu_pca_rank_one_jitter(port, ctx):
+    """Rank-1 data: second coordinate is the reference's seeded jitter."""
+    import paper_2505_15511_b200 as nb
+    t = np.linspace(-1, 1, 500)
+    x = np.ascontiguousarray(np.outer(t, np.arange(1, 9)).astype(np.float32))
+    ref = port.pca_init(x, 4)
+    got = nb.pca_init(x, 4, ctx=ctx)
+    assert np.array_equal(got[:, 1], ref[:, 1])
+    assert np.max(np.abs(got[:, 0] - ref[:, 0])) < 1e-9
+
+
+def test_gpu_pca_degenerate(ctx):
+    import paper_2505_15511_b200 as nb
+    with pytest.raises(nb.NomadError) as e:
+        nb.pca_init(np.ones((20, 3), np.float32), ctx=ctx)
+    assert e.value.kind == "Degenerate"
+
+
+def test_fit_with_gpu_pca_quality(port, ctx):
+    """Full GPU fit (GPU PCA, throughput SGD): loss trajectory tracks the
+    reference's within 5% after 40 epochs."""
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(4000, 32, 10, 10.0, 42)
+    *_, rloss = _pipeline(port, x, 5, 1, 40, 7)
+    rep = nb.FitReport()
+    out = nb.fit(x, nb.TrainConfig(epochs=40, workers=1, seed=7, n_clusters=5,
+                                   sgd_mode="hogwild"), report=rep, ctx=ctx)
+    assert np.isfinite(out).all()
+    l = np.array(rep.epoch_mean_loss)
+    assert abs(l[-5:].mean() - rloss[-5:].mean()) < 0.05 * rloss[-5:].mean()
