@@ -1,0 +1,52 @@
+// Reference-side integration check: the same program calls the reference's
+// own header-only functions (nomad::X) and the B200 engine through the shim
+// (nomad::b200::X) on identical inputs and compares.
+#include <cstdio>
+#include <cstring>
+
+#include "nomad/nomad.hpp"
+#include "nomad_b200/nomad_b200.hpp"
+
+int main() {
+  nomad::VectorDataset ds;
+  ds.rows = 2000;
+  ds.dims = 16;
+  nomad::Rng r(42);
+  std::vector<double> centres(5 * 16);
+  for (double& c : centres) c = 10.0 * r.gaussian();
+  for (std::size_t i = 0; i < ds.rows; ++i)
+    for (std::size_t j = 0; j < ds.dims; ++j)
+      ds.data.push_back(static_cast<float>(centres[(i % 5) * 16 + j] + r.gaussian()));
+  int bad = 0;
+  auto a = nomad::lsh_init(ds, 6, 3), b = nomad::b200::lsh_init(ds, 6, 3);
+  bad += a.assignment != b.assignment || a.centroids != b.centroids;
+  const double tol = nomad::default_kmeans_tol(ds);
+  bad += tol != nomad::b200::default_kmeans_tol(ds);
+  std::vector<double> qa, qb;
+  a = nomad::kmeans_em(ds, a, 100, tol, &qa);
+  b = nomad::b200::kmeans_em(ds, b, 100, tol, &qb);
+  bad += a.assignment != b.assignment || a.centroids != b.centroids || qa != qb;
+  auto ga = nomad::build_knn(ds, a, 15), gb = nomad::b200::build_knn(ds, b, 15);
+  bad += ga.neighbors != gb.neighbors || ga.distances != gb.distances || ga.offsets != gb.offsets;
+  nomad::TrainConfig cfg;
+  cfg.epochs = 20;
+  cfg.workers = 2;
+  cfg.n_clusters = 6;
+  cfg.seed = 3;
+  nomad::FitReport ra, rb;
+  auto la = nomad::fit(ds, cfg, &ra);
+  auto lb = nomad::b200::fit(ds, cfg, &rb);
+  bad += ra.clusters.assignment != rb.clusters.assignment;
+  bad += ra.graph.neighbors != rb.graph.neighbors;
+  const double l0 = ra.epoch_mean_loss.back(), l1 = rb.epoch_mean_loss.back();
+  bad += !(std::fabs(l0 - l1) < 0.05 * l0);
+  bad += rb.comm.epochs.size() != 20 || rb.comm.epochs[0].size() != 2;
+  try {
+    nomad::b200::lsh_init(ds, 1, 0);
+    ++bad;
+  } catch (const nomad::Error& e) {
+    bad += e.kind() != nomad::ErrorKind::Parameter;
+  }
+  std::printf("%s loss ref %.6f b200 %.6f\n", bad ? "FAIL" : "OK", l0, l1);
+  return bad ? 1 : 0;
+}
