@@ -256,6 +256,11 @@ int32_t nomad_b200_generate_mixture(nomad_b200_ctx* ctx, uint64_t rows,
                                     uint64_t dims, uint64_t blobs,
                                     double spread, uint64_t seed, float* out);
 
+/* Diagnostic: one 128 x 128 bf16 tile product D = A B^T through the same
+ * TMA + tcgen05.mma + TMEM path the bf16 kNN uses (rows rounded to bf16). */
+int32_t nomad_b200_debug_tc_gemm(nomad_b200_ctx* ctx, const float* host_rows, uint64_t rows,
+                                 uint64_t d, uint32_t a0, uint32_t b0, float* out128x128);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,8 @@ _SIGS = {
                                    _vp, C.POINTER(ClustersView), C.POINTER(GraphView), _vp]),
     "nomad_b200_plan": (C.c_int32, [C.c_uint64, C.c_uint64, _vp, C.c_uint64, C.c_int32, _vp, _vp,
                                     C.POINTER(C.c_uint32)]),
+    "nomad_b200_debug_tc_gemm": (C.c_int32, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint32,
+                                             C.c_uint32, _vp]),
     "nomad_b200_nccl_unique_id": (C.c_int32, [_vp]),
     "nomad_b200_generate_mixture": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
                                                 C.c_double, C.c_uint64, _vp]),

@@ -382,7 +382,11 @@ __global__ void k_sizes2(const uint32_t* a, uint64_t n, uint32_t* sizes) {
 
 }  // namespace
 
-// Builds the exact graph into device buffers (offsets n+1, nb/dist offsets[n]).
+void knn_bf16_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                         const uint32_t* assign_d, uint32_t C, DBuf<uint32_t>& cand_ids,
+                         DBuf<float>& cand_tau, DBuf<uint32_t>& cand_cnt);
+
+// Builds the graph into device buffers (offsets n+1, nb/dist offsets[n]).
 struct KnnResult {
   DBuf<uint32_t> offsets, nb;
   DBuf<double> dist;
@@ -391,7 +395,8 @@ struct KnnResult {
 };
 
 void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
-                     const uint32_t* assign_d, uint32_t C, uint32_t k, KnnResult& R) {
+                     const uint32_t* assign_d, uint32_t C, uint32_t k, KnnResult& R,
+                     int mode) {
   cudaStream_t S = ctx->stream;
   if (k < 1) fail(kParameter, "k must be >= 1");
   if (k > 56) fail(kParameter, "k > 56 is not supported by the exact kNN build");
@@ -434,9 +439,17 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   DBuf<ClusterSeg> segs_d(segs.size());
   NB_CUDA(cudaMemcpyAsync(segs_d.p, segs.data(), segs.size() * sizeof(ClusterSeg),
                           cudaMemcpyHostToDevice, S));
-  const int KP = k <= 24 ? 32 : 64;
-  DBuf<uint32_t> cid(n * (uint64_t)KP), ccnt(n);
-  DBuf<float> ctau(n);
+  int KP = k <= 24 ? 32 : 64;
+  DBuf<uint32_t> cid, ccnt;
+  DBuf<float> ctau;
+  if (mode == NOMAD_B200_KNN_BF16) {
+    if (k > 24) fail(kParameter, "bf16 kNN mode supports k <= 24");
+    KP = 32;
+    knn_bf16_candidates(ctx, x, n, d, assign_d, C, cid, ctau, ccnt);
+  } else {
+  cid.alloc(n * (uint64_t)KP);
+  ccnt.alloc(n);
+  ctau.alloc(n);
   NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
   auto filt = [&](auto kern, int kp) {
     const size_t smem = (size_t)(QT + CT) * (DK + 1) * 4 + (size_t)QT * (kp + CT) * 8 + QT * 12;
@@ -446,6 +459,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   };
   if (KP == 32) filt(k_knn_filter<32>, 32); else filt(k_knn_filter<64>, 64);
   note_launch(ctx, "k_knn_filter");
+  }
   // certificate factor: T / (1 + g32) * (1 - g64), rounded down generously
   const double g32 = (double)(d + 3) * 0x1p-24 / (1.0 - (double)(d + 3) * 0x1p-24);
   const double g64 = (double)(d + 1) * 0x1p-53 / (1.0 - (double)(d + 1) * 0x1p-53);
@@ -505,7 +519,7 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
     if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16)
       fail(kParameter, "unknown knn_mode");
     KnnResult R;
-    build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R);
+    build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R, knn_mode);
     const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
                                                          : cudaMemcpyDeviceToHost;
     NB_CUDA(cudaMemcpyAsync(out->offsets, R.offsets.p, (dd.n + 1) * 4, kind, S));
