@@ -25,11 +25,9 @@ namespace nb {
 namespace {
 
 constexpr int TM = 128;        // query rows per CTA (UMMA M)
-constexpr int TN = 128;        // candidate rows per tile (UMMA N)
+constexpr int TN = 128;        // tile width of the diagnostic GEMM
 constexpr int KC = 64;         // bf16 columns per stage (one 128B swizzle atom)
-constexpr int STAGES = 4;
 constexpr int KPF = 32;        // survivors per query
-constexpr int CAPF = 64;       // per-row buffer
 constexpr uint32_t STAGE_BYTES = (TM + TN) * KC * 2;  // 32 KB
 
 struct TcTile {
@@ -62,131 +60,179 @@ __global__ void k_tc_prep(const float* __restrict__ x, uint64_t d, uint64_t dpad
   if (lane == 0) norms[row] = acc;
 }
 
-__device__ void row_compact(float* bd, uint32_t* bi, int r, uint32_t& cnt, float& tau) {
-  // keep the KPF smallest of cnt entries (column-major row r), selection sort
-  for (int i = 0; i < KPF; ++i) {
-    int m = i;
-    float mv = bd[i * TM + r];
-    for (uint32_t e = i + 1; e < cnt; ++e) {
-      const float v = bd[e * TM + r];
-      if (v < mv) { mv = v; m = (int)e; }
-    }
-    if (m != i) {
-      const float tv = bd[i * TM + r];
-      const uint32_t ti = bi[i * TM + r];
-      bd[i * TM + r] = mv;
-      bi[i * TM + r] = bi[m * TM + r];
-      bd[m * TM + r] = tv;
-      bi[m * TM + r] = ti;
-    }
-  }
-  cnt = KPF;
-  tau = bd[(KPF - 1) * TM + r];
-}
+// v2, warp-specialised: warp 0 = TMA producer, warp 1 = MMA issuer (and TMEM
+// owner), warps 2..5 = epilogue (one query row per thread; TMEM lane quarter
+// = warp % 4). Candidate tiles are N2 = 256 wide; the fp32 accumulator is
+// double-buffered in TMEM (2 x 256 columns) so the epilogue of tile t
+// overlaps the MMAs of tile t+1. Each epilogue thread keeps its row's KPF
+// best (distance, index) in registers (sorted; insertion is a compare-swap
+// chain, rare after the first tiles).
+constexpr int TN2 = 256;
+constexpr int STAGES2 = 4;
+constexpr uint32_t STAGE2_BYTES = (TM + TN2) * KC * 2;  // 48 KB
 
-__global__ void __launch_bounds__(128, 1) k_knn_tc(const __grid_constant__ CUtensorMap tmap,
-                                                   const TcTile* __restrict__ tiles,
-                                                   const float* __restrict__ norms,
-                                                   const uint32_t* __restrict__ perm_pad,
-                                                   uint32_t kchunks, uint32_t* cand_ids,
-                                                   float* cand_tau, uint32_t* cand_cnt) {
+__global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUtensorMap tmap,
+                                                    const TcTile* __restrict__ tiles,
+                                                    const float* __restrict__ norms,
+                                                    const uint32_t* __restrict__ perm_pad,
+                                                    uint32_t kchunks, uint32_t* cand_ids,
+                                                    float* cand_tau, uint32_t* cand_cnt) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* base = smem + ((1024 - (tc::smem_u32(smem) & 1023)) & 1023);
-  uint8_t* stage_mem = base;                                  // STAGES x 32 KB
-  float* bd = reinterpret_cast<float*>(base + STAGES * STAGE_BYTES);  // CAPF x TM
-  uint32_t* bi = reinterpret_cast<uint32_t*>(bd + CAPF * TM);
-  uint64_t* full = reinterpret_cast<uint64_t*>(bi + CAPF * TM);
-  uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint8_t* stage_mem = base;
+  float* cn = reinterpret_cast<float*>(base + STAGES2 * STAGE2_BYTES);  // 2 x TN2 norms
+  uint64_t* full = reinterpret_cast<uint64_t*>(cn + 2 * TN2);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;  // 2
+  uint64_t* tempty = tfull + 2;       // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* spill = reinterpret_cast<float*>(tmem_slot + 4);  // 128 x 33 (epilogue scratch)
 
   const TcTile T = tiles[blockIdx.x];
-  const int r = threadIdx.x, warp = r >> 5;
-  if (warp == 0) tc::tmem_alloc(tmem_slot, TN);
-  if (r == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * TN2);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], 128);
+    }
     tc::fence_mbar_init();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-
-  const uint32_t q_local = T.qoff + r;  // my query inside the cluster
-  const bool qvalid = q_local < T.size;
-  const float qn = norms[T.row0 + r];
-  uint32_t cnt = 0;
-  float tau = __int_as_float(0x7f800000);
-  const uint32_t ntiles = (T.size + TN - 1) / TN;
+  const uint32_t ntiles = (T.size + TN2 - 1) / TN2;
   const uint32_t total = ntiles * kchunks;
-  const uint32_t idesc = tc::idesc_bf16(TM, TN);
-  uint32_t issued = 0;  // TMA loads issued (thread 0)
-  for (uint32_t ct = 0; ct < ntiles; ++ct) {
-    if (r == 0) {
-      for (uint32_t kc = 0; kc < kchunks; ++kc) {
-        const uint32_t it = ct * kchunks + kc;
-        // keep the TMA producer up to STAGES loads ahead of the MMA
-        while (issued < total && issued < it + STAGES) {
-          const uint32_t s = issued % STAGES;
-          if (issued >= STAGES) tc::mbar_wait(&empty[s], ((issued / STAGES) - 1) & 1);
-          const uint32_t ict = issued / kchunks, ikc = issued % kchunks;
-          uint8_t* sa = stage_mem + s * STAGE_BYTES;
-          tc::mbar_expect_tx(&full[s], STAGE_BYTES);
-          tc::tma_load_2d(sa, &tmap, &full[s], (int32_t)(ikc * KC), (int32_t)T.row0);
-          tc::tma_load_2d(sa + TM * KC * 2, &tmap, &full[s], (int32_t)(ikc * KC),
-                          (int32_t)(T.cbase + ict * TN));
-          ++issued;
-        }
-        const uint32_t s = it % STAGES;
-        tc::mbar_wait(&full[s], (it / STAGES) & 1);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (uint32_t it = 0; it < total; ++it) {
+        const uint32_t s = it % STAGES2;
+        if (it >= STAGES2) tc::mbar_wait(&empty[s], ((it / STAGES2) - 1) & 1);
+        const uint32_t ct = it / kchunks, kc = it % kchunks;
+        uint8_t* sa = stage_mem + s * STAGE2_BYTES;
+        tc::mbar_expect_tx(&full[s], STAGE2_BYTES);
+        tc::tma_load_2d(sa, &tmap, &full[s], (int32_t)(kc * KC), (int32_t)T.row0);
+        tc::tma_load_2d(sa + TM * KC * 2, &tmap, &full[s], (int32_t)(kc * KC),
+                        (int32_t)(T.cbase + ct * TN2));
+        tc::tma_load_2d(sa + (TM + 128) * KC * 2, &tmap, &full[s], (int32_t)(kc * KC),
+                        (int32_t)(T.cbase + ct * TN2 + 128));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = tc::idesc_bf16(TM, TN2);
+      for (uint32_t ct = 0; ct < ntiles; ++ct) {
+        const uint32_t b = ct & 1;
+        if (ct >= 2) tc::mbar_wait(&tempty[b], ((ct >> 1) - 1) & 1);
         tc::fence_after();
-        const uint32_t sa = tc::smem_u32(stage_mem + s * STAGE_BYTES);
-        const uint64_t da = tc::sdesc_k_sw128(sa), db = tc::sdesc_k_sw128(sa + TM * KC * 2);
+        const uint32_t acc = tmem + b * TN2;
+        for (uint32_t kc = 0; kc < kchunks; ++kc) {
+          const uint32_t it = ct * kchunks + kc, s = it % STAGES2;
+          tc::mbar_wait(&full[s], (it / STAGES2) & 1);
+          tc::fence_after();
+          const uint32_t sa = tc::smem_u32(stage_mem + s * STAGE2_BYTES);
+          const uint64_t da = tc::sdesc_k_sw128(sa), db = tc::sdesc_k_sw128(sa + TM * KC * 2);
 #pragma unroll
-        for (int k = 0; k < KC / 16; ++k)
-          tc::umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (kc | k) != 0);
-        tc::umma_commit(&empty[s]);
+          for (int k = 0; k < KC / 16; ++k)
+            tc::umma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (kc | k) != 0);
+          tc::umma_commit(&empty[s]);
+        }
+        tc::umma_commit(&tfull[b]);
       }
-      tc::umma_commit(done);
     }
-    __syncwarp();
-    tc::mbar_wait(done, ct & 1);
-    tc::fence_after();
-    // epilogue: my TMEM lane = my query row; 4 x 32 columns
-#pragma unroll 1
-    for (int cc = 0; cc < TN; cc += 32) {
-      float v[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + cc, v);
-      if (!qvalid) continue;
-      const uint32_t c0 = ct * TN + cc;  // cluster-local index of column 0
+  } else {
+    // ---- epilogue: row r <-> TMEM lane r
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
+    const uint32_t q_local = T.qoff + r;
+    const bool qvalid = q_local < T.size;
+    const float qn = norms[T.row0 + r];
+    float ld[KPF];
+    uint32_t li[KPF];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const uint32_t cl = c0 + j;
-        if (cl >= T.size || cl == q_local) continue;
-        const float dist = qn + norms[T.cbase + cl] - 2.f * v[j];
-        if (dist < tau) {
-          bd[cnt * TM + r] = dist;
-          bi[cnt * TM + r] = cl;
-          if (++cnt == CAPF) row_compact(bd, bi, r, cnt, tau);
+    for (int e = 0; e < KPF; ++e) {
+      ld[e] = __int_as_float(0x7f800000);
+      li[e] = 0xFFFFFFFFu;
+    }
+    float tau = ld[KPF - 1];
+    for (uint32_t ct = 0; ct < ntiles; ++ct) {
+      const uint32_t b = ct & 1;
+      float* cnb = cn + b * TN2;
+      // candidate norms of this tile (invalid columns -> +inf)
+      for (int j = et; j < TN2; j += 128) {
+        const uint32_t cl = ct * TN2 + j;
+        cnb[j] = cl < T.size ? norms[T.cbase + cl] : __int_as_float(0x7f800000);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      tc::mbar_wait(&tfull[b], (ct >> 1) & 1);
+      tc::fence_after();
+      const uint32_t acc = tmem + b * TN2 + ((uint32_t)(q4 * 32) << 16);
+#pragma unroll 1
+      for (int cc = 0; cc < TN2; cc += 32) {
+        float v[32];
+        tc::tmem_ld32(acc + cc, v);
+        if (!qvalid) continue;
+        // distances + below-threshold mask (straight-line); the rare
+        // insertions run afterwards from shared memory, one code copy.
+        uint32_t mask = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float dist = fmaf(-2.f, v[j], qn + cnb[cc + j]);
+          if (ct * TN2 + cc + j == q_local) dist = __int_as_float(0x7f800000);
+          v[j] = dist;
+          mask |= (dist < tau ? 1u : 0u) << j;
+        }
+        if (mask) {
+          float* row = spill + et * 33;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) row[j] = v[j];
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            float cd = row[j];
+            if (!(cd < tau)) continue;
+            uint32_t ci = ct * TN2 + cc + j;
+#pragma unroll
+            for (int e = 0; e < KPF; ++e) {
+              if (cd < ld[e]) {
+                const float td = ld[e];
+                const uint32_t ti = li[e];
+                ld[e] = cd;
+                li[e] = ci;
+                cd = td;
+                ci = ti;
+              }
+            }
+            tau = ld[KPF - 1];
+          }
         }
       }
+      tc::fence_before();
+      tc::mbar_arrive(&tempty[b]);
     }
-    tc::fence_before();
-    __syncthreads();
+    if (qvalid) {
+      const uint32_t gq = perm_pad[T.row0 + r];
+      uint32_t c = 0;
+#pragma unroll
+      for (int e = 0; e < KPF; ++e)
+        if (li[e] != 0xFFFFFFFFu) {
+          cand_ids[(uint64_t)gq * KPF + c] = perm_pad[T.cbase + li[e]];
+          ++c;
+        }
+      cand_cnt[gq] = c;
+      cand_tau[gq] = __int_as_float(0x7f800000);
+    }
   }
-  if (qvalid) {
-    if (cnt > KPF) row_compact(bd, bi, r, cnt, tau);
-    const uint32_t gq = perm_pad[T.row0 + r];
-    for (uint32_t e = 0; e < cnt; ++e) cand_ids[(uint64_t)gq * KPF + e] = perm_pad[T.cbase + bi[e * TM + r]];
-    cand_cnt[gq] = cnt;
-    cand_tau[gq] = __int_as_float(0x7f800000);
-  }
+  tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, TN);
+  if (warp == 1) tc::tmem_dealloc(tmem, 2 * TN2);
 }
 
 // Debug / unit path: D = A B^T for one 128 x 128 tile pair (rows a0, b0 of
@@ -264,9 +310,6 @@ CUtensorMap make_tmap(const __nv_bfloat16* xb, uint64_t rows, uint64_t dpad) {
   return m;
 }
 
-size_t knn_tc_smem() {
-  return 1024 + STAGES * STAGE_BYTES + (size_t)CAPF * TM * 8 + (2 * STAGES + 1) * 8 + 16;
-}
 
 }  // namespace
 
@@ -327,12 +370,13 @@ void knn_bf16_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64
   DBuf<TcTile> tiles_d(tiles.size());
   NB_CUDA(cudaMemcpyAsync(tiles_d.p, tiles.data(), tiles.size() * sizeof(TcTile),
                           cudaMemcpyHostToDevice, S));
-  const size_t smem = knn_tc_smem();
-  NB_CUDA(cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_knn_tc<<<(unsigned)tiles.size(), 128, smem, S>>>(tm, tiles_d.p, norms.p, perm_d.p,
-                                                      (uint32_t)(dpad / KC), cand_ids.p, cand_tau.p,
-                                                      cand_cnt.p);
-  note_launch(ctx, "k_knn_tc");
+  const size_t smem = 1024 + STAGES2 * STAGE2_BYTES + 2 * TN2 * 4 + (2 * STAGES2 + 4) * 8 + 16 +
+                      128 * 33 * 4;
+  NB_CUDA(cudaFuncSetAttribute(k_knn_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_knn_tc2<<<(unsigned)tiles.size(), 192, smem, S>>>(tm, tiles_d.p, norms.p, perm_d.p,
+                                                       (uint32_t)(dpad / KC), cand_ids.p,
+                                                       cand_tau.p, cand_cnt.p);
+  note_launch(ctx, "k_knn_tc2");
   NB_CUDA(cudaStreamSynchronize(S));
 }
 
