@@ -173,7 +173,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=list(CONFIGS), default="C")
     ap.add_argument("--sgd-mode", choices=["hogwild", "replay"], default="hogwild")
-    ap.add_argument("--graph", choices=["synthetic"], default="synthetic")
+    ap.add_argument("--graph", choices=["knn", "synthetic"], default="knn",
+                    help="knn: full GPU index build (lsh_init -> kmeans_em -> build_knn) on "
+                         "device-generated data; synthetic: random within-cluster graph")
+    ap.add_argument("--knn-mode", choices=["bf16", "exact"], default="bf16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=2)
     args = ap.parse_args()
@@ -197,10 +200,31 @@ def main():
         W = world * ((W + world - 1) // world)
     k = 15
     t0 = time.perf_counter()
-    a, offsets, nb, init = synthetic_index(n, ncl, k)
     ctx = nbx.Context(local)
     stream = torch.cuda.Stream(device=local)
     ctx.set_stream(stream.cuda_stream)
+    index = {}
+    if args.graph == "knn":
+        # the full hot-path index build on this GPU (identical on every rank:
+        # same seeds, deterministic kernels), then the dataset is released
+        x = nbx.generate_mixture(n, d, blobs, 10.0, 42, ctx=ctx)
+        torch.cuda.synchronize()
+        t_a = time.perf_counter()
+        c0 = nbx.lsh_init(x, ncl, 7, ctx=ctx)
+        t_b = time.perf_counter()
+        cl = nbx.kmeans_em_default_tol(x, c0, 100, ctx=ctx)
+        t_c = time.perf_counter()
+        g = nbx.build_knn(x, cl, k, mode=args.knn_mode, ctx=ctx)
+        t_d = time.perf_counter()
+        del x
+        torch.cuda.empty_cache()
+        a, offsets, nb = cl.assignment, g.offsets, g.neighbors
+        init = np.random.default_rng(1234).standard_normal((n, 2))
+        index = {"lsh_init_s": round(t_b - t_a, 3), "kmeans_em_s": round(t_c - t_b, 3),
+                 "build_knn_s": round(t_d - t_c, 3), "knn_mode": args.knn_mode,
+                 "cluster_sizes_min_max": [int(cl.sizes.min()), int(cl.sizes.max())]}
+    else:
+        a, offsets, nb, init = synthetic_index(n, ncl, k)
     nid = None
     if world > 1:
         obj = [nbx.nccl_unique_id() if rank == 0 else None]
@@ -304,8 +328,11 @@ def main():
                 "workload": f"{args.config}: {n} x {d} -> 2D, {ncl} clusters, W={W} logical "
                             f"shards, k={k}, s=5, |M|=5",
                 "sgd_mode": args.sgd_mode,
-                "graph": "random within-cluster k-regular graph, clusters = mixture components "
-                         "(GPU kNN build reported separately when enabled)",
+                "graph": ("GPU index build: lsh_init + kmeans_em (exact fp64) + build_knn "
+                          f"({args.knn_mode}) on device-generated data"
+                          if args.graph == "knn" else
+                          "random within-cluster k-regular graph, clusters = mixture components"),
+                "index": index,
                 "init": "N(0,1) layout", "parallelism": f"cluster-sharded dp{world}",
                 "l2": "inputs larger than L2 (positions 16n B + ELL 64n B > 126 MB)",
                 "setup_s": round(setup_s, 2), "final_loss": float(losses[-1])},
