@@ -68,38 +68,57 @@ __global__ void k_extract_offsets(const uint32_t* scanned, const uint32_t* hist,
   }
 }
 
-// Warp per (segment, 32-column group); lanes own columns. Members are walked
-// in order with a 2-stage register pipeline of U rows to keep loads in flight
-// while the dependent fp64 adds retire (reference order, no reassociation).
-template <int U>
-__global__ void k_seq_colsum(const float* __restrict__ x, uint64_t d, const uint32_t* members,
-                             const uint64_t* seg_beg, const uint64_t* seg_cnt,
-                             const uint32_t* seg_row, uint32_t nseg, double* out) {
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
+// Same sums, latency-hidden: a CTA per (segment, 32-column group). All 8
+// warps stream batches of BR rows (one 128-B row slice per warp instruction,
+// cp.async into a double buffer), while warp 0 walks the previous batch in
+// order (lanes = columns) with the dependent fp64 adds. Order and rounding
+// are exactly k_seq_colsum's (ascending member order, one add per row).
+template <int BR>
+__global__ void __launch_bounds__(256) k_seq_colsum2(const float* __restrict__ x, uint64_t d,
+                                                     const uint32_t* members,
+                                                     const uint64_t* seg_beg,
+                                                     const uint64_t* seg_cnt,
+                                                     const uint32_t* seg_row, uint32_t nseg,
+                                                     double* out) {
+  extern __shared__ float sbuf[];  // [2][BR][33]
   const uint32_t groups = (uint32_t)((d + 31) / 32);
-  if (gw >= (uint64_t)nseg * groups) return;
-  const uint32_t sidx = gw / groups;
-  const uint64_t j = (uint64_t)(gw % groups) * 32 + lane;
+  const uint32_t sidx = blockIdx.x / groups;
+  const uint64_t j0 = (uint64_t)(blockIdx.x % groups) * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t beg = seg_beg[sidx], cnt = seg_cnt[sidx];
   if (cnt == 0) return;
+  const uint64_t j = j0 + lane;
   const bool colok = j < d;
+  auto issue = [&](uint64_t b) {
+    const uint64_t r0 = b * BR;
+    float* dst = sbuf + (b & 1) * BR * 33;
+    for (int rr = warp; rr < BR; rr += 8) {
+      const uint64_t t = r0 + rr;
+      if (t < cnt && colok) {
+        const uint64_t row = members ? members[beg + t] : beg + t;
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + rr * 33 + lane);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(x + row * d + j)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const uint64_t nb = (cnt + BR - 1) / BR;
   double acc = 0.0;
-  float a[U], b[U];
-  auto row = [&](uint64_t t) -> uint64_t { return members ? members[beg + t] : beg + t; };
-  uint64_t t = 0;
-  for (; t + 2 * U <= cnt; t += 2 * U) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) a[u] = colok ? __ldg(x + row(t + u) * d + j) : 0.f;
-#pragma unroll
-    for (int u = 0; u < U; ++u) b[u] = colok ? __ldg(x + row(t + U + u) * d + j) : 0.f;
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)a[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, (double)b[u]);
+  issue(0);
+  for (uint64_t b = 0; b < nb; ++b) {
+    if (b + 1 < nb) issue(b + 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+      const float* src = sbuf + (b & 1) * BR * 33;
+      const int m = (int)umin64(BR, cnt - b * BR);
+      for (int r = 0; r < m; ++r) acc = __dadd_rn(acc, colok ? (double)src[r * 33 + lane] : 0.0);
+    }
+    __syncthreads();
   }
-  for (; t < cnt; ++t) acc = __dadd_rn(acc, colok ? (double)__ldg(x + row(t) * d + j) : 0.0);
-  if (colok) out[(uint64_t)seg_row[sidx] * d + j] = __ddiv_rn(acc, (double)cnt);
+  if (warp == 0 && colok) out[(uint64_t)seg_row[sidx] * d + j] = __ddiv_rn(acc, (double)cnt);
 }
 
 }  // namespace
@@ -142,10 +161,13 @@ void seq_column_means(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uin
   NB_CUDA(cudaMemcpyAsync(db.p, beg.data(), nseg * 8, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(dc.p, cnt.data(), nseg * 8, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(dr.p, seg_ids.data(), nseg * 4, cudaMemcpyHostToDevice, S));
-  const uint64_t warps = (uint64_t)nseg * ((d + 31) / 32);
-  k_seq_colsum<32><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, S>>>(x, d, members, db.p, dc.p,
-                                                                       dr.p, nseg, out);
-  note_launch(ctx, "k_seq_colsum");
+  const uint64_t ctas = (uint64_t)nseg * ((d + 31) / 32);
+  constexpr int BR = 256;
+  const size_t smem = 2 * BR * 33 * sizeof(float);
+  NB_CUDA(cudaFuncSetAttribute(k_seq_colsum2<BR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  k_seq_colsum2<BR><<<(unsigned)ctas, 256, smem, S>>>(x, d, members, db.p, dc.p, dr.p, nseg, out);
+  note_launch(ctx, "k_seq_colsum2");
   NB_CUDA(cudaStreamSynchronize(S));
 }
 
