@@ -135,6 +135,12 @@ class Oracle:
         if which == "reference":
             self._fit = fn("fit", C.c_int, [f32p, C.c_uint64, C.c_uint64, C.POINTER(TrainConfig),
                                            f64p, u32p, u64p, u32p, u32p, f64p, f64p, f64p, f64p])
+            self._np = fn("neighborhood_preservation", C.c_int,
+                          [f32p, C.c_uint64, C.c_uint64, f64p, C.c_uint64, C.c_uint64,
+                           C.c_uint64, f64p, f64p])
+            self._tri = fn("random_triplet_accuracy", C.c_int,
+                           [f32p, C.c_uint64, C.c_uint64, f64p, C.c_uint64, C.c_uint64, f64p,
+                            f64p])
             self._qe = None
         else:
             self._fit = None
@@ -305,6 +311,23 @@ class Oracle:
         return dict(layout=lay, assignment=a, n_clusters=ncl, offsets=off, neighbors=nb[:m],
                     distances=di[:m], pca=pca, epoch_loss=loss[: cfg.epochs],
                     final_means=means[:ncl])
+
+    # -- reference-only quality metrics (metrics.hpp) -----------------------
+    def neighborhood_preservation(self, x, layout, k=10, sample=0, seed=0):
+        x = np.ascontiguousarray(x, np.float32)
+        lay = np.ascontiguousarray(layout, np.float64)
+        v, se = np.zeros(1), np.zeros(1)
+        self._check(self._np(_p(x, C.c_float), x.shape[0], x.shape[1], _p(lay, C.c_double), k,
+                             sample, seed, _p(v, C.c_double), _p(se, C.c_double)))
+        return float(v[0]), float(se[0])
+
+    def random_triplet_accuracy(self, x, layout, count=100000, seed=0):
+        x = np.ascontiguousarray(x, np.float32)
+        lay = np.ascontiguousarray(layout, np.float64)
+        v, se = np.zeros(1), np.zeros(1)
+        self._check(self._tri(_p(x, C.c_float), x.shape[0], x.shape[1], _p(lay, C.c_double),
+                              count, seed, _p(v, C.c_double), _p(se, C.c_double)))
+        return float(v[0]), float(se[0])
 
     # -- port-only helpers --------------------------------------------------
     def quantization_error(self, x, clusters: Clusters) -> float:

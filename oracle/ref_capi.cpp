@@ -372,6 +372,36 @@ int ref_train_epochs(uint64_t n, uint64_t C, const uint32_t* assign,
   } catch (const nomad::Error& e) { return fail_code(e); }
 }
 
+// metrics.hpp:113-168 / :205-243 — the reference's own quality metrics, used
+// only as the checker of final-map quality parity (tests/test_quality_gpu.py).
+int ref_neighborhood_preservation(const float* data, uint64_t n, uint64_t d,
+                                  const double* layout, uint64_t k, uint64_t sample,
+                                  uint64_t seed, double* value, double* std_error) {
+  try {
+    nomad::LayoutMatrix l;
+    l.rows = n;
+    l.positions.assign(layout, layout + 2 * n);
+    auto r = nomad::neighborhood_preservation(make_ds(data, n, d), l, k, sample, seed);
+    *value = r.value;
+    *std_error = r.std_error;
+    return 0;
+  } catch (const nomad::Error& e) { return fail_code(e); }
+}
+
+int ref_random_triplet_accuracy(const float* data, uint64_t n, uint64_t d,
+                                const double* layout, uint64_t count, uint64_t seed,
+                                double* value, double* std_error) {
+  try {
+    nomad::LayoutMatrix l;
+    l.rows = n;
+    l.positions.assign(layout, layout + 2 * n);
+    auto r = nomad::random_triplet_accuracy(make_ds(data, n, d), l, count, seed);
+    *value = r.value;
+    *std_error = r.std_error;
+    return 0;
+  } catch (const nomad::Error& e) { return fail_code(e); }
+}
+
 // optimizer.hpp:327-482, the whole pipeline, with the FitReport pieces the
 // parity tests need. Pointers are nullable except layout.
 int ref_fit(const float* data, uint64_t n, uint64_t d, const ref_train_config* c,
