@@ -65,13 +65,17 @@ enum nomad_b200_sgd_mode {
 
 /* kNN distance mode (knn.hpp:65-109). */
 enum nomad_b200_knn_mode {
-  /* fp32 FFMA direct-difference filter with a rigorous error bound, top-K'
-   * per row, fp64 j-sequential re-rank and certificate (else exhaustive fp64
-   * for that row): ids AND fp64 distances bit-identical to the reference. */
+  /* Exact: an fp16 tcgen05 distance filter (top-64 per row) with a rigorous
+   * error bound, fp64 j-sequential re-rank and certificate, exhaustive fp64
+   * for any uncertified row: ids AND fp64 distances bit-identical to the
+   * reference. (k > 56 uses the FFMA filter below.) */
   NOMAD_B200_KNN_EXACT = 0,
   /* bf16 tcgen05 distance contraction (||a||^2+||b||^2-2ab), top-k; report
    * recall@k against the exact mode. Distances returned are fp64 re-ranked. */
-  NOMAD_B200_KNN_BF16 = 1
+  NOMAD_B200_KNN_BF16 = 1,
+  /* Exact with the fp32 FFMA direct-difference filter (relative error bound
+   * (d+3) u32) instead of the tensor cores; same certificate / fallback. */
+  NOMAD_B200_KNN_EXACT_FFMA = 2
 };
 
 typedef struct nomad_b200_ctx nomad_b200_ctx;
@@ -173,6 +177,11 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx,
                              const nomad_b200_dataset_view* data,
                              const nomad_b200_clusters* clusters, uint64_t k,
                              int32_t knn_mode, nomad_b200_graph* out);
+
+/* Statistics of the context's last build_knn: rows the tensor-core
+ * certificate did not settle, and rows resolved by the exhaustive fp64 pass. */
+int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
+                             uint64_t* exhaustive_rows);
 
 /* --------------------------------------------- epoch loop (L3 + L4) */
 /* The setup half of fit() (optimizer.hpp:342-386): build_affinity,

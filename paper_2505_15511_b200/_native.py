@@ -18,7 +18,7 @@ KINDS = ["Io", "Dimension", "Validation", "Schema", "Parameter", "Config",
 
 HOST, DEVICE = 0, 1
 SGD_REPLAY, SGD_HOGWILD = 0, 1
-KNN_EXACT, KNN_BF16 = 0, 1
+KNN_EXACT, KNN_BF16, KNN_EXACT_FFMA = 0, 1, 2
 
 
 class NomadError(RuntimeError):
@@ -76,6 +76,7 @@ _SIGS = {
                                                      C.POINTER(C.c_uint64)]),
     "nomad_b200_build_knn": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(ClustersView),
                                          C.c_uint64, C.c_int32, C.POINTER(GraphView)]),
+    "nomad_b200_knn_stats": (C.c_int32, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "nomad_b200_trainer_create": (C.c_int32, [_vp, C.POINTER(GraphView), C.POINTER(ClustersView),
                                               _vp, C.c_int32, C.POINTER(TrainConfigC),
                                               C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),

@@ -138,7 +138,7 @@ class TrainConfig:
             self.kmeans_max_iters, float(self.kmeans_tol),
             1 if self.approx == "non-own-cluster" else 0, 1 if self.head_only else 0,
             {"replay": N.SGD_REPLAY, "hogwild": N.SGD_HOGWILD}[self.sgd_mode],
-            {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16}[self.knn_mode],
+            {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[self.knn_mode],
             self.hogwild_cap, 1 if self.verbose else 0)
 
 
@@ -160,6 +160,12 @@ class Context:
         if device not in cls._default:
             cls._default[device] = Context(device)
         return cls._default[device]
+
+    def knn_stats(self):
+        """(tc_uncertified_rows, exhaustive_rows) of this context's last build_knn."""
+        a, b = C.c_uint64(), C.c_uint64()
+        check(lib().nomad_b200_knn_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def kernel_launches(self) -> int:
         return int(lib().nomad_b200_kernel_launches(self.h))
@@ -258,7 +264,7 @@ def build_knn(data, clusters: ClusterAssignment, k: int, mode: str = "exact",
     di = np.zeros(max(n * k, 1), np.float64)
     gv = N.GraphView(n, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
     check(lib().nomad_b200_build_knn(_ctx(ctx).h, C.byref(dv), C.byref(v), k,
-                                     {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16}[mode],
+                                     {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[mode],
                                      C.byref(gv)))
     m = int(off[n])
     return KnnGraph(n, k, off, nb[:m], di[:m])

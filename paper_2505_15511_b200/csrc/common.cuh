@@ -89,6 +89,8 @@ struct nomad_b200_ctx {
   bool own_stream = false;
   uint64_t launches = 0;
   int sm_count = 148;
+  // statistics of the last build_knn call
+  uint64_t knn_tc_uncertified = 0, knn_exhaustive = 0;
 };
 
 namespace nb {

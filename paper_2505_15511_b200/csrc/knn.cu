@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__
                                                        const uint32_t* __restrict__ members,
                                                        const ClusterSeg* segs, uint32_t nseg,
                                                        uint32_t* cand_ids, float* cand_tau,
-                                                       uint32_t* cand_cnt) {
+                                                       uint32_t* cand_cnt, double lbf) {
   constexpr int CAP = KP + CT;
   extern __shared__ __align__(16) unsigned char smraw[];
   float(*qs)[DK + 1] = reinterpret_cast<float(*)[DK + 1]>(smraw);
@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__
     if (KP > 32 && lane + 32 < (int)c) cand_ids[(uint64_t)gq * KP + lane + 32] = bi[q * CAP + lane + 32];
     if (lane == 0) {
       cand_cnt[gq] = c;
-      cand_tau[gq] = c == KP ? tau[q] : __int_as_float(0x7f800000);
+      // lower bound on every excluded candidate's reference distance
+      cand_tau[gq] = c == KP ? __double2float_rd((double)tau[q] * lbf) : __int_as_float(0x7f800000);
     }
   }
 }
@@ -382,16 +383,17 @@ __global__ void k_sizes2(const uint32_t* a, uint64_t n, uint32_t* sizes) {
 
 }  // namespace
 
-void knn_bf16_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
-                         const uint32_t* assign_d, uint32_t C, DBuf<uint32_t>& cand_ids,
-                         DBuf<float>& cand_tau, DBuf<uint32_t>& cand_cnt);
+void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                       const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
+                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out);
 
 // Builds the graph into device buffers (offsets n+1, nb/dist offsets[n]).
 struct KnnResult {
   DBuf<uint32_t> offsets, nb;
   DBuf<double> dist;
   uint64_t edges = 0;
-  uint64_t fallbacks = 0;
+  uint64_t fallbacks = 0;       // rows resolved by the exhaustive fp64 pass
+  uint64_t tc_uncertified = 0;  // rows the tensor-core certificate did not settle
 };
 
 void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
@@ -439,44 +441,85 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   DBuf<ClusterSeg> segs_d(segs.size());
   NB_CUDA(cudaMemcpyAsync(segs_d.p, segs.data(), segs.size() * sizeof(ClusterSeg),
                           cudaMemcpyHostToDevice, S));
-  int KP = k <= 24 ? 32 : 64;
-  DBuf<uint32_t> cid, ccnt;
-  DBuf<float> ctau;
-  if (mode == NOMAD_B200_KNN_BF16) {
-    if (k > 24) fail(kParameter, "bf16 kNN mode supports k <= 24");
-    KP = 32;
-    knn_bf16_candidates(ctx, x, n, d, assign_d, C, cid, ctau, ccnt);
-  } else {
-  cid.alloc(n * (uint64_t)KP);
-  ccnt.alloc(n);
-  ctau.alloc(n);
-  NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
-  auto filt = [&](auto kern, int kp) {
-    const size_t smem = (size_t)(QT + CT) * (DK + 1) * 4 + (size_t)QT * (kp + CT) * 8 + QT * 12;
-    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<tiles, 256, smem, S>>>(x, (uint32_t)d, mem.p, segs_d.p, (uint32_t)segs.size(), cid.p,
-                                  ctau.p, ccnt.p);
-  };
-  if (KP == 32) filt(k_knn_filter<32>, 32); else filt(k_knn_filter<64>, 64);
-  note_launch(ctx, "k_knn_filter");
-  }
-  // certificate factor: T / (1 + g32) * (1 - g64), rounded down generously
+  // FFMA filter certificate factor: T / (1 + g32) * (1 - g64), rounded down generously
   const double g32 = (double)(d + 3) * 0x1p-24 / (1.0 - (double)(d + 3) * 0x1p-24);
   const double g64 = (double)(d + 1) * 0x1p-53 / (1.0 - (double)(d + 1) * 0x1p-53);
-  const double lbf = (1.0 - g64) / (1.0 + g32) * (1.0 - 1e-12);
+  const double lbf_ffma = (1.0 - g64) / (1.0 + g32) * (1.0 - 1e-12);
+  int KP = k <= 24 ? 32 : 64;
+  DBuf<uint32_t> cid, ccnt;
+  DBuf<float> clb;  // per-row lower bound on every excluded reference distance
+  auto ffma_filter = [&](const std::vector<ClusterSeg>& sg, uint32_t ntiles, int kp) {
+    DBuf<ClusterSeg> sg_d(sg.size());
+    NB_CUDA(cudaMemcpyAsync(sg_d.p, sg.data(), sg.size() * sizeof(ClusterSeg),
+                            cudaMemcpyHostToDevice, S));
+    auto go = [&](auto kern) {
+      const size_t smem = (size_t)(QT + CT) * (DK + 1) * 4 + (size_t)QT * (kp + CT) * 8 + QT * 12;
+      NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<ntiles, 256, smem, S>>>(x, (uint32_t)d, mem.p, sg_d.p, (uint32_t)sg.size(), cid.p,
+                                     clb.p, ccnt.p, lbf_ffma);
+    };
+    if (kp == 32) go(k_knn_filter<32>); else go(k_knn_filter<64>);
+    note_launch(ctx, "k_knn_filter");
+    NB_CUDA(cudaStreamSynchronize(S));
+  };
   DBuf<uint32_t> fb(n), nfb(1);
-  NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
-  const unsigned rb = (unsigned)((n * 32 + 255) / 256);
-  if (KP == 32)
-    k_knn_rerank<32><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, ctau.p,
-                                        ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, lbf);
-  else
-    k_knn_rerank<64><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, ctau.p,
-                                        ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, lbf);
-  note_launch(ctx, "k_knn_rerank");
+  auto rerank = [&]() -> uint32_t {
+    NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
+    const unsigned rb = (unsigned)((n * 32 + 255) / 256);
+    if (KP == 32)
+      k_knn_rerank<32><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, clb.p,
+                                          ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
+    else
+      k_knn_rerank<64><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, clb.p,
+                                          ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
+    note_launch(ctx, "k_knn_rerank");
+    uint32_t nf = 0;
+    NB_CUDA(cudaMemcpyAsync(&nf, nfb.p, 4, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    return nf;
+  };
+
+  const bool tc = (mode == NOMAD_B200_KNN_BF16) || (mode == NOMAD_B200_KNN_EXACT && k <= 56);
   uint32_t nf = 0;
-  NB_CUDA(cudaMemcpyAsync(&nf, nfb.p, 4, cudaMemcpyDeviceToHost, S));
-  NB_CUDA(cudaStreamSynchronize(S));
+  if (tc) {
+    // stage 1: tensor-core filter (bf16 fast / fp16 certified)
+    if (mode == NOMAD_B200_KNN_BF16 && k > 24) fail(kParameter, "bf16 kNN mode supports k <= 24");
+    knn_tc_candidates(ctx, x, n, d, assign_d, C, mode == NOMAD_B200_KNN_EXACT, cid, clb, ccnt,
+                      &KP);
+    nf = rerank();
+    R.tc_uncertified = nf;
+    if (nf && mode == NOMAD_B200_KNN_EXACT) {
+      // stage 2: clusters where many rows failed the tensor-core certificate
+      // (large norms -> loose accumulation bound) get the FFMA filter, whose
+      // error is relative to the distance itself.
+      std::vector<uint32_t> fbh(nf), ah(n);
+      NB_CUDA(cudaMemcpy(fbh.data(), fb.p, nf * 4, cudaMemcpyDeviceToHost));
+      NB_CUDA(cudaMemcpy(ah.data(), assign_d, n * 4, cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> fail_per(C, 0);
+      for (uint32_t q : fbh) ++fail_per[ah[q]];
+      std::vector<ClusterSeg> sg;
+      uint32_t nt = 0;
+      for (uint32_t r = 0; r < C; ++r) {
+        const uint64_t sz = off[r + 1] - off[r];
+        if (sz < 2 || fail_per[r] == 0) continue;
+        if (fail_per[r] * 16 < sz) continue;  // few: the exhaustive pass is cheaper
+        sg.push_back(ClusterSeg{off[r], (uint32_t)sz, nt});
+        nt += (uint32_t)((sz + QT - 1) / QT);
+      }
+      if (nt) {
+        ffma_filter(sg, nt, KP);
+        nf = rerank();
+      }
+    }
+  } else {
+    cid.alloc(n * (uint64_t)KP);
+    ccnt.alloc(n);
+    clb.alloc(n);
+    NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
+    ffma_filter(segs, tiles, KP);
+    nf = rerank();
+  }
+  // stage 3: exhaustive fp64 for whatever is still uncertified
   R.fallbacks = nf;
   if (nf) {
     std::vector<uint64_t> cb(C);
@@ -516,10 +559,13 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
       NB_CUDA(cudaMemcpyAsync(a_own.p, a, dd.n * 4, cudaMemcpyHostToDevice, S));
       a = a_own.p;
     }
-    if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16)
+    if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16 &&
+        knn_mode != NOMAD_B200_KNN_EXACT_FFMA)
       fail(kParameter, "unknown knn_mode");
     KnnResult R;
     build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R, knn_mode);
+    ctx->knn_tc_uncertified = R.tc_uncertified;
+    ctx->knn_exhaustive = R.fallbacks;
     const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
                                                          : cudaMemcpyDeviceToHost;
     NB_CUDA(cudaMemcpyAsync(out->offsets, R.offsets.p, (dd.n + 1) * 4, kind, S));
@@ -531,6 +577,15 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
     NB_CUDA(cudaStreamSynchronize(S));
     out->rows = dd.n;
     out->k = k;
+  });
+}
+
+int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
+                             uint64_t* exhaustive_rows) {
+  return guard([&] {
+    if (!ctx) fail(kParameter, "NULL argument");
+    if (tc_uncertified) *tc_uncertified = ctx->knn_tc_uncertified;
+    if (exhaustive_rows) *exhaustive_rows = ctx->knn_exhaustive;
   });
 }
 

@@ -1,18 +1,29 @@
-// kNN fast mode on the 5th-gen tensor cores (knn.hpp:65-109 semantics, bf16
-// distances): per cluster, rows are centred on the cluster mean, rounded to
-// bf16 into a padded cluster-contiguous copy, and every (query tile,
-// candidate tile) product S = A B^T (128 x 128, K = d) runs on tcgen05.mma
-// with operands streamed by TMA into 128B-swizzled shared memory (4-stage
-// ring) and the fp32 accumulator in TMEM. The epilogue reads the accumulator
-// with tcgen05.ld (one thread per query row), forms ||a||^2 + ||b||^2 - 2ab
-// and keeps the KP smallest per row. The survivors are re-ranked with the
-// reference's exact fp64 distance (knn.cu), so reported distances are exact;
-// recall@k against the exact mode measures the bf16 selection.
+// kNN distance filter on the 5th-gen tensor cores (knn.hpp:65-109).
+//
+// Per cluster, rows are centred on the cluster mean (u = x - mu, fp64) and
+// rounded to 16 bits into a padded cluster-contiguous copy; every (query
+// tile, candidate tile) product S = U_q U_c^T (128 x 256, K = d) runs on
+// tcgen05.mma with operands streamed by TMA into 128B-swizzled shared memory
+// (4-stage ring) and the fp32 accumulator double-buffered in TMEM. Warp 0
+// issues TMA, warp 1 issues MMAs, warps 2-5 run the epilogue (tcgen05.ld, one
+// query row per thread, distance ||u_q||^2 + ||u_c||^2 - 2 S, register-
+// resident sorted top-KP with rolled insertion).
+//
+// Two uses:
+//  * fast mode (NOMAD_B200_KNN_BF16): bf16 operands, KP = 32 survivors,
+//    re-ranked in exact fp64 (knn.cu) — recall@k vs the exact mode is reported.
+//  * certified exact mode: fp16 operands (11-bit mantissa), KP = 64 survivors
+//    and a rigorous lower bound on the reference distance of every excluded
+//    candidate; the re-rank certifies the top-k or sends the row to the
+//    exhaustive fp64 fallback, so ids and distances are bit-identical to the
+//    reference.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "index_common.cuh"
@@ -20,28 +31,71 @@
 
 namespace nb {
 
-
-
 namespace {
 
-constexpr int TM = 128;        // query rows per CTA (UMMA M)
-constexpr int TN = 128;        // tile width of the diagnostic GEMM
-constexpr int KC = 64;         // bf16 columns per stage (one 128B swizzle atom)
-constexpr int KPF = 32;        // survivors per query
-constexpr uint32_t STAGE_BYTES = (TM + TN) * KC * 2;  // 32 KB
+constexpr int TM = 128;       // query rows per CTA (UMMA M)
+constexpr int TN = 128;       // tile width of the diagnostic GEMM
+constexpr int TN2 = 256;      // candidate rows per tile (UMMA N)
+constexpr int KC = 64;        // 16-bit columns per stage (one 128B swizzle atom)
+constexpr int STAGES2 = 4;
+constexpr uint32_t STAGE_BYTES = (TM + TN) * KC * 2;    // diagnostic GEMM
+constexpr uint32_t STAGE2_BYTES = (TM + TN2) * KC * 2;  // 48 KB
 
 struct TcTile {
   uint32_t row0;   // padded row of this query tile
   uint32_t cbase;  // padded row of the cluster's first member
   uint32_t size;   // cluster size
   uint32_t qoff;   // query offset inside the cluster
+  uint32_t cid;    // cluster id
 };
 
-// bf16(x - mean) into the padded cluster-contiguous copy, fp32 norms.
+// Error model of the certified filter (scaled units, see the host side):
+//   g_acc    relative error of S and of the norms: tcgen05 fp32 accumulation
+//            (taken as <= 2 ulp per addition over dpad additions), the fp32
+//            norm chains and the two final fp32 roundings, x1.5
+//   eps      componentwise relative rounding of u to fp16 (fp64 -> fp32 -> fp16)
+//   abs_norm fp16 subnormal absolute rounding, 2^-25 sqrt(dpad)
+struct CertParams {
+  float g_acc;
+  float eps;
+  float abs_norm;
+  float inv_s2;  // 1 / scale^2
+  float g64;     // reference fp64 chain relative error (2 (d + 1) u64)
+};
+
+template <bool FP16>
+__device__ __forceinline__ uint16_t to16(float v) {
+  if constexpr (FP16) return __half_as_ushort(__float2half_rn(v));
+  else return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+template <bool FP16>
+__device__ __forceinline__ float from16(uint16_t b) {
+  if constexpr (FP16) return __half2float(__ushort_as_half(b));
+  else return __bfloat162float(__ushort_as_bfloat16(b));
+}
+
+__global__ void k_tc_absmax(const float* __restrict__ x, uint64_t d, const uint32_t* perm_pad,
+                            const uint32_t* row_cl, const double* means, uint64_t rows_pad,
+                            unsigned int* amax_bits) {
+  const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows_pad) return;
+  const uint32_t id = perm_pad[row];
+  if (id == 0xFFFFFFFFu) return;
+  const double* mu = means + (uint64_t)row_cl[row] * d;
+  float m = 0.f;
+  for (uint64_t j = lane; j < d; j += 32)
+    m = fmaxf(m, fabsf((float)((double)x[(uint64_t)id * d + j] - mu[j])));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomicMax(amax_bits, __float_as_uint(m));
+}
+
+// 16-bit (scale * (x - mu)) into the padded copy; fp32 norms of the rounded rows.
+template <bool FP16>
 __global__ void k_tc_prep(const float* __restrict__ x, uint64_t d, uint64_t dpad,
                           const uint32_t* __restrict__ perm_pad, const uint32_t* __restrict__ row_cl,
-                          const double* __restrict__ means, uint64_t rows_pad,
-                          __nv_bfloat16* __restrict__ xb, float* __restrict__ norms) {
+                          const double* __restrict__ means, uint64_t rows_pad, float scale,
+                          uint16_t* __restrict__ xb, float* __restrict__ norms) {
   const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= rows_pad) return;
@@ -50,33 +104,25 @@ __global__ void k_tc_prep(const float* __restrict__ x, uint64_t d, uint64_t dpad
   float acc = 0.f;
   for (uint64_t j = lane; j < dpad; j += 32) {
     float v = 0.f;
-    if (id != 0xFFFFFFFFu && j < d) v = (float)((double)x[(uint64_t)id * d + j] - mu[j]);
-    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    if (id != 0xFFFFFFFFu && j < d) v = (float)((double)x[(uint64_t)id * d + j] - mu[j]) * scale;
+    const uint16_t b = to16<FP16>(v);
     xb[row * dpad + j] = b;
-    const float bf = __bfloat162float(b);
+    const float bf = from16<FP16>(b);
     acc = fmaf(bf, bf, acc);
   }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) norms[row] = acc;
 }
 
-// v2, warp-specialised: warp 0 = TMA producer, warp 1 = MMA issuer (and TMEM
-// owner), warps 2..5 = epilogue (one query row per thread; TMEM lane quarter
-// = warp % 4). Candidate tiles are N2 = 256 wide; the fp32 accumulator is
-// double-buffered in TMEM (2 x 256 columns) so the epilogue of tile t
-// overlaps the MMAs of tile t+1. Each epilogue thread keeps its row's KPF
-// best (distance, index) in registers (sorted; insertion is a compare-swap
-// chain, rare after the first tiles).
-constexpr int TN2 = 256;
-constexpr int STAGES2 = 4;
-constexpr uint32_t STAGE2_BYTES = (TM + TN2) * KC * 2;  // 48 KB
-
+template <int KP, bool CERT>
 __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUtensorMap tmap,
                                                     const TcTile* __restrict__ tiles,
                                                     const float* __restrict__ norms,
+                                                    const float* __restrict__ cl_maxnorm,
                                                     const uint32_t* __restrict__ perm_pad,
-                                                    uint32_t kchunks, uint32_t* cand_ids,
-                                                    float* cand_tau, uint32_t* cand_cnt) {
+                                                    uint32_t kchunks, uint32_t idesc,
+                                                    CertParams cp, uint32_t* cand_ids,
+                                                    float* cand_lb, uint32_t* cand_cnt) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* base = smem + ((1024 - (tc::smem_u32(smem) & 1023)) & 1023);
   uint8_t* stage_mem = base;
@@ -126,7 +172,6 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
-      const uint32_t idesc = tc::idesc_bf16(TM, TN2);
       for (uint32_t ct = 0; ct < ntiles; ++ct) {
         const uint32_t b = ct & 1;
         if (ct >= 2) tc::mbar_wait(&tempty[b], ((ct >> 1) - 1) & 1);
@@ -154,19 +199,18 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
     const uint32_t q_local = T.qoff + r;
     const bool qvalid = q_local < T.size;
     const float qn = norms[T.row0 + r];
-    float ld[KPF];
-    uint32_t li[KPF];
+    float ld[KP];
+    uint32_t li[KP];
 #pragma unroll
-    for (int e = 0; e < KPF; ++e) {
+    for (int e = 0; e < KP; ++e) {
       ld[e] = __int_as_float(0x7f800000);
       li[e] = 0xFFFFFFFFu;
     }
-    float tau = ld[KPF - 1];
+    float tau = ld[KP - 1];
     for (uint32_t ct = 0; ct < ntiles; ++ct) {
       const uint32_t b = ct & 1;
       float* cnb = cn + b * TN2;
-      // candidate norms of this tile (invalid columns -> +inf)
-      for (int j = et; j < TN2; j += 128) {
+      for (int j = et; j < TN2; j += 128) {  // candidate norms; invalid -> +inf
         const uint32_t cl = ct * TN2 + j;
         cnb[j] = cl < T.size ? norms[T.cbase + cl] : __int_as_float(0x7f800000);
       }
@@ -200,7 +244,7 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
             if (!(cd < tau)) continue;
             uint32_t ci = ct * TN2 + cc + j;
 #pragma unroll
-            for (int e = 0; e < KPF; ++e) {
+            for (int e = 0; e < KP; ++e) {
               if (cd < ld[e]) {
                 const float td = ld[e];
                 const uint32_t ti = li[e];
@@ -210,7 +254,7 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
                 ci = ti;
               }
             }
-            tau = ld[KPF - 1];
+            tau = ld[KP - 1];
           }
         }
       }
@@ -221,13 +265,30 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
       const uint32_t gq = perm_pad[T.row0 + r];
       uint32_t c = 0;
 #pragma unroll
-      for (int e = 0; e < KPF; ++e)
+      for (int e = 0; e < KP; ++e)
         if (li[e] != 0xFFFFFFFFu) {
-          cand_ids[(uint64_t)gq * KPF + c] = perm_pad[T.cbase + li[e]];
+          cand_ids[(uint64_t)gq * KP + c] = perm_pad[T.cbase + li[e]];
           ++c;
         }
       cand_cnt[gq] = c;
-      cand_tau[gq] = __int_as_float(0x7f800000);
+      float lb = __int_as_float(0x7f800000);  // complete list: nothing excluded
+      if (CERT && c == KP) {
+        // Every excluded candidate j has Dtilde_j >= T = tau (scaled units).
+        // With a = ||u_b,q||, s = ||u_b,q - u_b,j|| and ||u_b,j|| <= a + s:
+        //   T <= Dtilde_j <= s^2 + g (2a + s)^2
+        //   => s >= (-2ga + sqrt(4g^2a^2 + (1+g)(T - 4ga^2))) / (1+g)
+        // The rounding to 16 bits moves each vector by <= eps ||u|| + abs:
+        //   t = ||u_q - u_j|| >= (s - 2 eps a_true - 2 abs) / (1 + eps)
+        //   ref_j >= t^2 (1 - g64) / scale^2
+        // (double precision, rounded down at the end; no cluster-wide norm)
+        const double g = cp.g_acc, a = sqrt((double)qn) * (1.0 + 1e-6);
+        const double disc = 4.0 * g * g * a * a + (1.0 + g) * ((double)tau - 4.0 * g * a * a);
+        const double s = fmax((-2.0 * g * a + sqrt(fmax(disc, 0.0))) / (1.0 + g), 0.0);
+        const double eps = cp.eps, a_true = a / (1.0 - eps) + cp.abs_norm;
+        const double t = fmax((s - 2.0 * eps * a_true - 2.0 * cp.abs_norm) / (1.0 + eps), 0.0);
+        lb = __double2float_rd(t * t * cp.inv_s2 * (1.0 - cp.g64) * (1.0 - 1e-9));
+      }
+      cand_lb[gq] = lb;
     }
   }
   tc::fence_before();
@@ -236,10 +297,11 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
 }
 
 // Debug / unit path: D = A B^T for one 128 x 128 tile pair (rows a0, b0 of
-// the bf16 tensor), written to out[128][128].
+// the 16-bit tensor), written to out[128][128].
 __global__ void __launch_bounds__(128, 1) k_tc_gemm_tile(const __grid_constant__ CUtensorMap tmap,
                                                          uint32_t a0, uint32_t b0,
-                                                         uint32_t kchunks, float* out) {
+                                                         uint32_t kchunks, uint32_t idesc,
+                                                         float* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* base = smem + ((1024 - (tc::smem_u32(smem) & 1023)) & 1023);
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + STAGE_BYTES);
@@ -265,7 +327,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_gemm_tile(const __grid_constant__
       const uint32_t sa = tc::smem_u32(base);
       const uint64_t da = tc::sdesc_k_sw128(sa), db = tc::sdesc_k_sw128(sa + TM * KC * 2);
       for (int k = 0; k < KC / 16; ++k)
-        tc::umma_bf16(tmem, da + 2 * k, db + 2 * k, tc::idesc_bf16(TM, TN), (kc | k) != 0);
+        tc::umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (kc | k) != 0);
       tc::umma_commit(&bar[1]);
       tc::mbar_wait(&bar[1], kc & 1);
     }
@@ -295,33 +357,42 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-CUtensorMap make_tmap(const __nv_bfloat16* xb, uint64_t rows, uint64_t dpad) {
+CUtensorMap make_tmap(const uint16_t* xb, uint64_t rows, uint64_t dpad, bool fp16) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof m);
   const cuuint64_t gdim[2] = {dpad, rows};
   const cuuint64_t gstride[1] = {dpad * 2};
   const cuuint32_t box[2] = {KC, TM};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)xb, gdim, gstride,
-                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r = encode_fn()(
+      &m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)xb,
+      gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(kInternal, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
 }
 
+// kind::f16 instruction descriptor: fp32 D, A/B = bf16 (1) or fp16 (0).
+constexpr uint32_t idesc16(uint32_t M, uint32_t N, bool fp16) {
+  return (1u << 4) | ((fp16 ? 0u : 1u) << 7) | ((fp16 ? 0u : 1u) << 10) | ((N >> 3) << 17) |
+         ((M >> 4) << 24);
+}
 
 }  // namespace
 
-// Fast-mode candidate generation; fills cand_ids[n][32] / cand_cnt[n].
-void knn_bf16_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
-                         const uint32_t* assign_d, uint32_t C, DBuf<uint32_t>& cand_ids,
-                         DBuf<float>& cand_tau, DBuf<uint32_t>& cand_cnt) {
+// Candidate generation on the tensor cores. fp16 == certified exact filter
+// (KP = 64, cand_lb = rigorous lower bound on excluded reference distances);
+// otherwise the bf16 fast filter (KP = 32, cand_lb = +inf).
+void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                       const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
+                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out) {
   cudaStream_t S = ctx->stream;
+  const int KP = fp16 ? 64 : 32;
+  *kp_out = KP;
   DBuf<uint32_t> mem;
   std::vector<uint64_t> off;
   group_by_label(ctx, assign_d, n, C, mem, off);
-  // cluster means (centring for bf16)
+  // centring vectors: the clusters' exact means (any fixed vector is valid)
   DBuf<double> means((uint64_t)C * d);
   NB_CUDA(cudaMemsetAsync(means.p, 0, (uint64_t)C * d * 8, S));
   {
@@ -335,13 +406,13 @@ void knn_bf16_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64
       }
     seq_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
   }
-  // padded layout
+  // padded cluster-contiguous layout (tiles never straddle a cluster start)
   std::vector<uint32_t> mem_h(off[C]);
   NB_CUDA(cudaMemcpy(mem_h.data(), mem.p, off[C] * 4, cudaMemcpyDeviceToHost));
   std::vector<uint64_t> pstart(C + 1, 0);
   for (uint32_t r = 0; r < C; ++r) pstart[r + 1] = pstart[r] + (off[r + 1] - off[r] + TM - 1) / TM * TM;
   const uint64_t rows_pad = std::max<uint64_t>(pstart[C], TM);
-  if (rows_pad >= (1ull << 31)) fail(kSize, "bf16 kNN: too many rows for TMA coordinates");
+  if (rows_pad >= (1ull << 31)) fail(kSize, "tensor-core kNN: too many rows for TMA coordinates");
   std::vector<uint32_t> perm(rows_pad, 0xFFFFFFFFu), rcl(rows_pad, 0);
   std::vector<TcTile> tiles;
   for (uint32_t r = 0; r < C; ++r) {
@@ -350,53 +421,99 @@ void knn_bf16_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64
     for (uint64_t t = 0; t < sz; ++t) perm[pstart[r] + t] = mem_h[off[r] + t];
     if (sz < 2) continue;
     for (uint64_t q = 0; q < sz; q += TM)
-      tiles.push_back(TcTile{(uint32_t)(pstart[r] + q), (uint32_t)pstart[r], (uint32_t)sz, (uint32_t)q});
+      tiles.push_back(TcTile{(uint32_t)(pstart[r] + q), (uint32_t)pstart[r], (uint32_t)sz,
+                             (uint32_t)q, r});
   }
   const uint64_t dpad = (d + KC - 1) / KC * KC;
   DBuf<uint32_t> perm_d(rows_pad), rcl_d(rows_pad);
   NB_CUDA(cudaMemcpyAsync(perm_d.p, perm.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(rcl_d.p, rcl.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
-  DBuf<__nv_bfloat16> xb(rows_pad * dpad);
+  // power-of-two scale keeping |u| well inside the 16-bit range
+  DBuf<unsigned int> amax(1);
+  NB_CUDA(cudaMemsetAsync(amax.p, 0, 4, S));
+  const unsigned rb = (unsigned)((rows_pad * 32 + 255) / 256);
+  k_tc_absmax<<<rb, 256, 0, S>>>(x, d, perm_d.p, rcl_d.p, means.p, rows_pad, amax.p);
+  note_launch(ctx, "k_tc_absmax");
+  unsigned int ab = 0;
+  NB_CUDA(cudaMemcpyAsync(&ab, amax.p, 4, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  float amx;
+  std::memcpy(&amx, &ab, 4);
+  float scale = 1.f;
+  if (amx > 0.f && std::isfinite(amx)) {
+    const float target = 1024.f;  // max |scaled u|: squares and sums stay far from overflow
+    scale = std::ldexp(1.f, (int)std::floor(std::log2(target / amx)));
+  }
+  DBuf<uint16_t> xb(rows_pad * dpad);
   DBuf<float> norms(rows_pad);
-  k_tc_prep<<<(unsigned)((rows_pad * 32 + 255) / 256), 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p,
-                                                                     means.p, rows_pad, xb.p, norms.p);
+  if (fp16)
+    k_tc_prep<true><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means.p, rows_pad, scale,
+                                       xb.p, norms.p);
+  else
+    k_tc_prep<false><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means.p, rows_pad, scale,
+                                        xb.p, norms.p);
   note_launch(ctx, "k_tc_prep");
-  cand_ids.alloc(n * KPF);
-  cand_tau.alloc(n);
+  // per-cluster max ||u_b|| (scaled), for the certificate
+  std::vector<float> nh(rows_pad), cmax(C, 0.f);
+  NB_CUDA(cudaMemcpyAsync(nh.data(), norms.p, rows_pad * 4, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  for (uint64_t row = 0; row < rows_pad; ++row)
+    cmax[rcl[row]] = std::max(cmax[rcl[row]], std::sqrt(nh[row]) * 1.0001f);
+  DBuf<float> cmax_d(C);
+  NB_CUDA(cudaMemcpyAsync(cmax_d.p, cmax.data(), C * 4, cudaMemcpyHostToDevice, S));
+
+  cand_ids.alloc(n * (uint64_t)KP);
+  cand_lb.alloc(n);
   cand_cnt.alloc(n);
   NB_CUDA(cudaMemsetAsync(cand_cnt.p, 0, n * 4, S));
   if (tiles.empty()) return;
-  const CUtensorMap tm = make_tmap(xb.p, rows_pad, dpad);
+  const CUtensorMap tm = make_tmap(xb.p, rows_pad, dpad, fp16);
   DBuf<TcTile> tiles_d(tiles.size());
   NB_CUDA(cudaMemcpyAsync(tiles_d.p, tiles.data(), tiles.size() * sizeof(TcTile),
                           cudaMemcpyHostToDevice, S));
+  CertParams cp;
+  const double u32 = 0x1p-24;
+  cp.g_acc = (float)(((double)dpad * 2.0 * 2 * u32 + (double)(dpad / 32 + 6) * u32 + 4 * u32) *
+                     1.5);
+  cp.eps = (float)(0x1p-11 + u32 + 1e-12);
+  cp.abs_norm = (float)(0x1p-25 * std::sqrt((double)dpad));
+  cp.inv_s2 = 1.f / (scale * scale);
+  cp.g64 = (float)((double)(d + 1) * 0x1p-53 * 2);
   const size_t smem = 1024 + STAGES2 * STAGE2_BYTES + 2 * TN2 * 4 + (2 * STAGES2 + 4) * 8 + 16 +
                       128 * 33 * 4;
-  NB_CUDA(cudaFuncSetAttribute(k_knn_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_knn_tc2<<<(unsigned)tiles.size(), 192, smem, S>>>(tm, tiles_d.p, norms.p, perm_d.p,
-                                                       (uint32_t)(dpad / KC), cand_ids.p,
-                                                       cand_tau.p, cand_cnt.p);
+  auto go = [&](auto kern) {
+    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)tiles.size(), 192, smem, S>>>(tm, tiles_d.p, norms.p, cmax_d.p, perm_d.p,
+                                                   (uint32_t)(dpad / KC), idesc16(TM, TN2, fp16),
+                                                   cp, cand_ids.p, cand_lb.p, cand_cnt.p);
+  };
+  if (fp16) go(k_knn_tc2<64, true>);
+  else go(k_knn_tc2<32, false>);
   note_launch(ctx, "k_knn_tc2");
   NB_CUDA(cudaStreamSynchronize(S));
 }
 
-// Unit check of the tcgen05 path: rows of a (m x d) f32 host matrix are
-// rounded to bf16; returns D = A[a0:a0+128] B[b0:b0+128]^T (fp32, 128 x 128).
+// Unit check of the tcgen05 path: rows of a (rows x d) f32 host matrix are
+// rounded to bf16 / fp16; returns D = A[a0:a0+128] B[b0:b0+128]^T.
 void tc_gemm_tile_check(nomad_b200_ctx* ctx, const float* host, uint64_t rows, uint64_t d,
-                        uint32_t a0, uint32_t b0, float* out_host) {
+                        uint32_t a0, uint32_t b0, bool fp16, float* out_host) {
   cudaStream_t S = ctx->stream;
   const uint64_t dpad = (d + KC - 1) / KC * KC;
-  std::vector<__nv_bfloat16> hb(rows * dpad);
+  std::vector<uint16_t> hb(rows * dpad);
   for (uint64_t i = 0; i < rows; ++i)
-    for (uint64_t j = 0; j < dpad; ++j)
-      hb[i * dpad + j] = __float2bfloat16_rn(j < d ? host[i * d + j] : 0.f);
-  DBuf<__nv_bfloat16> xb(rows * dpad);
+    for (uint64_t j = 0; j < dpad; ++j) {
+      const float v = j < d ? host[i * d + j] : 0.f;
+      hb[i * dpad + j] = fp16 ? __half_as_ushort(__float2half_rn(v))
+                              : __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    }
+  DBuf<uint16_t> xb(rows * dpad);
   NB_CUDA(cudaMemcpy(xb.p, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
-  const CUtensorMap tm = make_tmap(xb.p, rows, dpad);
+  const CUtensorMap tm = make_tmap(xb.p, rows, dpad, fp16);
   DBuf<float> out(TM * TN);
   const size_t smem = 1024 + STAGE_BYTES + 64;
   NB_CUDA(cudaFuncSetAttribute(k_tc_gemm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_tc_gemm_tile<<<1, 128, smem, S>>>(tm, a0, b0, (uint32_t)(dpad / KC), out.p);
+  k_tc_gemm_tile<<<1, 128, smem, S>>>(tm, a0, b0, (uint32_t)(dpad / KC), idesc16(TM, TN, fp16),
+                                      out.p);
   note_launch(ctx, "k_tc_gemm_tile");
   NB_CUDA(cudaMemcpyAsync(out_host, out.p, TM * TN * 4, cudaMemcpyDeviceToHost, S));
   NB_CUDA(cudaStreamSynchronize(S));
@@ -409,8 +526,10 @@ extern "C" int32_t nomad_b200_debug_tc_gemm(nomad_b200_ctx* ctx, const float* ho
                                             float* out128x128) {
   return nb::guard([&] {
     if (!ctx || !host_rows || !out128x128) nb::fail(nb::kParameter, "NULL argument");
+    const bool fp16 = (a0 & 0x80000000u) != 0;  // high bit of a0 selects fp16 operands
+    a0 &= 0x7FFFFFFFu;
     if (rows < a0 + 128 || rows < b0 + 128) nb::fail(nb::kParameter, "tile out of range");
     nb::bind_device(ctx);
-    nb::tc_gemm_tile_check(ctx, host_rows, rows, d, a0, b0, out128x128);
+    nb::tc_gemm_tile_check(ctx, host_rows, rows, d, a0, b0, fp16, out128x128);
   });
 }

@@ -13,23 +13,28 @@ pytestmark = pytest.mark.gpu
 G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_goldens.json")))
 
 
-def _gpu_graph(nb, ctx, x, c, k):
+def _gpu_graph(nb, ctx, x, c, k, mode="exact"):
     ca = nb.ClusterAssignment(c.assignment, c.n_clusters, x.shape[1], c.centroids, c.sizes)
-    return nb.build_knn(x, ca, k, ctx=ctx)
+    return nb.build_knn(x, ca, k, mode=mode, ctx=ctx)
+
+MODES = ["exact", "exact_ffma"]  # tensor-core certified filter / FFMA certified filter
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("n,d,blobs,C,k", [(3000, 32, 10, 8, 15), (600, 8, 40, 40, 15),
-                                           (4000, 100, 5, 6, 7), (2500, 768, 8, 4, 15)])
-def test_knn_bit_exact(port, ctx, n, d, blobs, C, k):
+                                           (4000, 100, 5, 6, 7), (2500, 768, 8, 4, 15),
+                                           (3000, 50, 6, 5, 40)])
+def test_knn_bit_exact(port, ctx, n, d, blobs, C, k, mode):
     import paper_2505_15511_b200 as nb
     x, c, g, _ = index_case(n, d, blobs, C, k)
-    gg = _gpu_graph(nb, ctx, x, c, k)
+    gg = _gpu_graph(nb, ctx, x, c, k, mode)
     assert np.array_equal(gg.offsets, g.offsets)
     assert np.array_equal(gg.neighbors, g.neighbors)
     assert np.array_equal(gg.distances, g.distances)
 
 
-def test_knn_ties_and_singletons(port, ctx):
+@pytest.mark.parametrize("mode", MODES)
+def test_knn_ties_and_singletons(port, ctx, mode):
     """Exact duplicates make every k-th distance a tie at 0 (the certificate
     cannot hold, so the exhaustive fp64 path decides by id), plus clusters of
     size 1 (empty lists) and 2."""
@@ -42,14 +47,15 @@ def test_knn_ties_and_singletons(port, ctx):
     a[1] = a[2] = 4     # pair
     cl = Clusters(a, np.zeros(5), np.bincount(a, minlength=5).astype(np.uint32), 5, 12)
     g = port.build_knn(x, cl, 15)
-    gg = _gpu_graph(nb, ctx, x, cl, 15)
+    gg = _gpu_graph(nb, ctx, x, cl, 15, mode)
     assert np.array_equal(gg.offsets, g.offsets)
     assert np.array_equal(gg.neighbors, g.neighbors)
     assert np.array_equal(gg.distances, g.distances)
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("case", ["small_w4", "config_a_w1"])
-def test_knn_matches_reference_goldens(port, ctx, case):
+def test_knn_matches_reference_goldens(port, ctx, case, mode):
     """Whole GPU index build (lsh_init -> kmeans_em -> build_knn) vs the
     reference's outputs on the golden inputs."""
     import paper_2505_15511_b200 as nb
@@ -57,7 +63,7 @@ def test_knn_matches_reference_goldens(port, ctx, case):
     n, d, blobs, ncl, k = gc["shape"][:5]
     x = port.gaussian_mixture(n, d, blobs, 10.0, 42)
     c = nb.kmeans_em_default_tol(x, nb.lsh_init(x, ncl, 7, ctx=ctx), 100, ctx=ctx)
-    gg = nb.build_knn(x, c, k, ctx=ctx)
+    gg = nb.build_knn(x, c, k, mode=mode, ctx=ctx)
     assert sha(gg.offsets) == gc["knn_offsets"]
     assert sha(gg.neighbors) == gc["knn_neighbors"]
     assert sha(gg.distances) == gc["knn_distances"]

@@ -16,15 +16,17 @@ def _bf16(a):
     return r.view(np.float32)
 
 
+@pytest.mark.parametrize("fp16", [False, True])
 @pytest.mark.parametrize("d", [64, 192, 768, 100])
-def test_tc_tile_gemm_matches_numpy(ctx, d):
+def test_tc_tile_gemm_matches_numpy(ctx, d, fp16):
     import paper_2505_15511_b200 as nb
     rng = np.random.default_rng(d)
     x = rng.normal(size=(384, d)).astype(np.float32)
     out = np.zeros((128, 128), np.float32)
-    nb._native.check(nb.lib().nomad_b200_debug_tc_gemm(ctx.h, x.ctypes.data, 384, d, 0, 256,
+    a0 = 0x80000000 if fp16 else 0
+    nb._native.check(nb.lib().nomad_b200_debug_tc_gemm(ctx.h, x.ctypes.data, 384, d, a0, 256,
                                                        out.ctypes.data))
-    xb = _bf16(x).astype(np.float64)
+    xb = (x.astype(np.float16).astype(np.float64) if fp16 else _bf16(x).astype(np.float64))
     ref = xb[0:128] @ xb[256:384].T
     np.testing.assert_allclose(out, ref, rtol=1e-4, atol=1e-3 * np.sqrt(d))
 
