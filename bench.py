@@ -177,6 +177,7 @@ def main():
                     help="knn: full GPU index build (lsh_init -> kmeans_em -> build_knn) on "
                          "device-generated data; synthetic: random within-cluster graph")
     ap.add_argument("--knn-mode", choices=["bf16", "exact"], default="bf16")
+    ap.add_argument("--recall-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=2)
     args = ap.parse_args()
@@ -216,11 +217,16 @@ def main():
         t_c = time.perf_counter()
         g = nbx.build_knn(x, cl, k, mode=args.knn_mode, ctx=ctx)
         t_d = time.perf_counter()
+        # kNN recall@15 of the graph the epochs use, against exact fp64 lists
+        # recomputed exhaustively for a row sample (exact mode: 1.0 by construction)
+        recall = nbx.knn_recall(x, cl, g, sample=args.recall_sample, seed=11, ctx=ctx)
         del x
         torch.cuda.empty_cache()
         a, offsets, nb = cl.assignment, g.offsets, g.neighbors
         init = np.random.default_rng(1234).standard_normal((n, 2))
-        index = {"lsh_init_s": round(t_b - t_a, 3), "kmeans_em_s": round(t_c - t_b, 3),
+        index = {"knn_recall_at_15": {"value": recall, "sample_rows": args.recall_sample,
+                                      "mode": args.knn_mode, "vs": "exact fp64 (exhaustive)"},
+                 "lsh_init_s": round(t_b - t_a, 3), "kmeans_em_s": round(t_c - t_b, 3),
                  "build_knn_s": round(t_d - t_c, 3), "knn_mode": args.knn_mode,
                  "cluster_sizes_min_max": [int(cl.sizes.min()), int(cl.sizes.max())]}
     else:
@@ -343,6 +349,7 @@ def main():
                          "bytes_per_head": BYTES_PER_HEAD, "peak_source": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "knn_recall_at_15": index.get("knn_recall_at_15"),
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -178,6 +178,13 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx,
                              const nomad_b200_clusters* clusters, uint64_t k,
                              int32_t knn_mode, nomad_b200_graph* out);
 
+/* recall@k of `graph` against exact lists recomputed (exhaustive fp64) for
+ * `sample` rows drawn without replacement from the rows with a non-empty
+ * list (0 = all rows). */
+int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                              const nomad_b200_clusters* clusters,
+                              const nomad_b200_graph* graph, uint64_t sample, uint64_t seed,
+                              double* recall_out);
 /* Statistics of the context's last build_knn: rows the tensor-core
  * certificate did not settle, and rows resolved by the exhaustive fp64 pass. */
 int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,

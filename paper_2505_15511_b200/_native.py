@@ -76,6 +76,9 @@ _SIGS = {
                                                      C.POINTER(C.c_uint64)]),
     "nomad_b200_build_knn": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(ClustersView),
                                          C.c_uint64, C.c_int32, C.POINTER(GraphView)]),
+    "nomad_b200_knn_recall": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(ClustersView),
+                                          C.POINTER(GraphView), C.c_uint64, C.c_uint64,
+                                          C.POINTER(C.c_double)]),
     "nomad_b200_knn_stats": (C.c_int32, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "nomad_b200_trainer_create": (C.c_int32, [_vp, C.POINTER(GraphView), C.POINTER(ClustersView),
                                               _vp, C.c_int32, C.POINTER(TrainConfigC),

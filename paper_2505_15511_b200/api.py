@@ -270,6 +270,22 @@ def build_knn(data, clusters: ClusterAssignment, k: int, mode: str = "exact",
     return KnnGraph(n, k, off, nb[:m], di[:m])
 
 
+def knn_recall(data, clusters: ClusterAssignment, graph: KnnGraph, sample: int = 20000,
+               seed: int = 0, ctx: Optional[Context] = None) -> float:
+    """recall@k of `graph` vs exact lists recomputed in fp64 for `sample` rows."""
+    dv, keep = _dataset(data)
+    cv = clusters._view()
+    off = np.ascontiguousarray(graph.offsets, np.uint32)
+    nb_ = np.ascontiguousarray(graph.neighbors, np.uint32)
+    if nb_.size == 0:
+        nb_ = np.zeros(1, np.uint32)
+    gv = N.GraphView(graph.rows, graph.k, off.ctypes.data, nb_.ctypes.data, None, N.HOST)
+    out = C.c_double()
+    check(lib().nomad_b200_knn_recall(_ctx(ctx).h, C.byref(dv), C.byref(cv), C.byref(gv), sample,
+                                      seed, C.byref(out)))
+    return out.value
+
+
 # ---------------------------------------------------------------- training
 
 @dataclass

@@ -580,6 +580,84 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
   });
 }
 
+// recall@k of a graph against the exact lists of `sample` rows drawn without
+// replacement (splitmix order), each recomputed exhaustively in fp64.
+int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                              const nomad_b200_clusters* clusters,
+                              const nomad_b200_graph* graph, uint64_t sample, uint64_t seed,
+                              double* recall_out) {
+  return guard([&] {
+    if (!ctx || !clusters || !graph || !recall_out) fail(kParameter, "NULL argument");
+    bind_device(ctx);
+    cudaStream_t S = ctx->stream;
+    DevData dd;
+    dd.bind(data, S);
+    const uint64_t n = dd.n, k = graph->k;
+    const uint32_t C = (uint32_t)clusters->n_clusters;
+    if (graph->rows != n || clusters->rows != n) fail(kParameter, "row counts differ");
+    std::vector<uint32_t> a(n), off(n + 1);
+    const auto kind_a = clusters->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToHost
+                                                                : cudaMemcpyHostToHost;
+    const auto kind_g = graph->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToHost
+                                                             : cudaMemcpyHostToHost;
+    NB_CUDA(cudaMemcpy(a.data(), clusters->assignment, n * 4, kind_a));
+    NB_CUDA(cudaMemcpy(off.data(), graph->offsets, (n + 1) * 4, kind_g));
+    std::vector<uint32_t> nbh(off[n]);
+    if (off[n]) NB_CUDA(cudaMemcpy(nbh.data(), graph->neighbors, (size_t)off[n] * 4, kind_g));
+    // sample rows with a non-empty list
+    std::vector<uint32_t> rows;
+    {
+      std::vector<uint32_t> cand;
+      for (uint64_t i = 0; i < n; ++i)
+        if (off[i + 1] > off[i]) cand.push_back((uint32_t)i);
+      uint64_t st = seed ^ 0x7265636c6c21ull;
+      const uint64_t m = std::min<uint64_t>(sample ? sample : cand.size(), cand.size());
+      for (uint64_t t = 0; t < m; ++t) {  // partial Fisher-Yates
+        st += 0x9E3779B97F4A7C15ull;
+        uint64_t z = st;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const uint64_t j = t + z % (cand.size() - t);
+        std::swap(cand[t], cand[j]);
+      }
+      rows.assign(cand.begin(), cand.begin() + m);
+    }
+    if (rows.empty()) {
+      *recall_out = 1.0;
+      return;
+    }
+    DBuf<uint32_t> a_d(n), sizes(C), mem, rows_d(rows.size()), off_d(n + 1), nb2(off[n] + 1);
+    NB_CUDA(cudaMemcpyAsync(a_d.p, a.data(), n * 4, cudaMemcpyHostToDevice, S));
+    NB_CUDA(cudaMemcpyAsync(off_d.p, off.data(), (n + 1) * 4, cudaMemcpyHostToDevice, S));
+    NB_CUDA(cudaMemcpyAsync(rows_d.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, S));
+    NB_CUDA(cudaMemsetAsync(sizes.p, 0, C * 4, S));
+    k_sizes2<<<(unsigned)std::min<uint64_t>(4096, (n + 255) / 256), 256, 0, S>>>(a_d.p, n, sizes.p);
+    note_launch(ctx, "k_sizes");
+    std::vector<uint64_t> coff;
+    group_by_label(ctx, a_d.p, n, C, mem, coff);
+    std::vector<uint64_t> cb(coff.begin(), coff.end() - 1);
+    DBuf<uint64_t> cb_d(C);
+    NB_CUDA(cudaMemcpyAsync(cb_d.p, cb.data(), C * 8, cudaMemcpyHostToDevice, S));
+    k_knn_exhaustive<<<(unsigned)rows.size(), 128, 0, S>>>(dd.x, (uint32_t)dd.d, a_d.p, mem.p,
+                                                          cb_d.p, sizes.p, (uint32_t)k, rows_d.p,
+                                                          off_d.p, nb2.p, nullptr);
+    note_launch(ctx, "k_knn_exhaustive");
+    std::vector<uint32_t> ex(off[n]);
+    NB_CUDA(cudaMemcpyAsync(ex.data(), nb2.p, (size_t)off[n] * 4, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    uint64_t hits = 0, total = 0;
+    for (uint32_t q : rows) {
+      std::vector<uint32_t> e(ex.begin() + off[q], ex.begin() + off[q + 1]);
+      std::sort(e.begin(), e.end());
+      for (uint32_t t = off[q]; t < off[q + 1]; ++t)
+        hits += std::binary_search(e.begin(), e.end(), nbh[t]) ? 1 : 0;
+      total += off[q + 1] - off[q];
+    }
+    *recall_out = total ? (double)hits / (double)total : 1.0;
+  });
+}
+
 int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
                              uint64_t* exhaustive_rows) {
   return guard([&] {
