@@ -687,15 +687,16 @@ struct nomad_b200_trainer {
 
   // Replace the positions (original order, n x 2) and re-gather the means
   // snapshot, as if the epoch loop had been given this layout.
+  DBuf<double2> stage;  // n rows, original order (host <-> device staging)
+
   void set_layout(const double* in, int loc) {
     cudaStream_t S = st();
     const uint32_t n_loc = (uint32_t)orig_of.size();
-    DBuf<double> tmp;
     const double* src = in;
     if (loc != NOMAD_B200_DEVICE) {
-      tmp.alloc(2 * n);
-      NB_CUDA(cudaMemcpyAsync(tmp.p, in, n * 16, cudaMemcpyHostToDevice, S));
-      src = tmp.p;
+      if (stage.n != n) stage.alloc(n);
+      NB_CUDA(cudaMemcpyAsync(stage.p, in, n * 16, cudaMemcpyHostToDevice, S));
+      src = reinterpret_cast<const double*>(stage.p);
     }
     if (n_loc) {
       launch_gather_layout(reinterpret_cast<const double2*>(src), orig_of_d.p, n_loc, pos.p, S);
@@ -713,6 +714,16 @@ struct nomad_b200_trainer {
         launch_scatter_layout(pos.p, orig_of_d.p, n_loc, reinterpret_cast<double2*>(out), S);
         launched("k_scatter_layout");
       }
+      NB_CUDA(cudaStreamSynchronize(S));
+      return;
+    }
+    if (world == 1) {  // every row is local: scatter on the device, one D2H copy
+      if (stage.n != n) stage.alloc(n);
+      if (n_loc) {
+        launch_scatter_layout(pos.p, orig_of_d.p, n_loc, stage.p, S);
+        launched("k_scatter_layout");
+      }
+      NB_CUDA(cudaMemcpyAsync(out, stage.p, n * 16, cudaMemcpyDeviceToHost, S));
       NB_CUDA(cudaStreamSynchronize(S));
       return;
     }
