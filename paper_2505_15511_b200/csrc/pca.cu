@@ -1,11 +1,13 @@
-// PCA initialisation (pca.hpp:79-218) on the GPU, tolerance parity: the two
-// data passes of covariance_apply (pca.hpp:34-55) and the final projection
-// run as fp64 kernels (tree reductions, so low-order bits differ from the
-// reference's sequential sums); the d-dimensional vector algebra (deflation,
-// normalisation, drift test, 2x2 Rayleigh-Ritz, sign rule) stays on the host
-// in the reference's exact expression order, and the mean is the exact
-// sequential mean. The start vectors and the rank-1 jitter come from the
-// reference's own "pca" Rng stream.
+// PCA initialisation (pca.hpp:79-218) on the GPU, bit-exact: both data
+// passes of covariance_apply (pca.hpp:34-55) follow the reference's
+// summation order — t_i is a j-ascending chain per row (thread per row, rows
+// staged through shared memory), y_j an i-ascending chain per column
+// (cp.async-staged column chains) — with _rn intrinsics (no FMA); the
+// d-dimensional vector algebra (deflation, normalisation, drift test, 2x2
+// Rayleigh-Ritz, sign rule) runs on the host in the reference's expression
+// order; the projection, column means and variances are again sequential
+// chains. The start vectors and the rank-1 jitter come from the reference's
+// own "pca" Rng stream.
 #include <algorithm>
 #include <cmath>
 
@@ -15,57 +17,125 @@ namespace nb {
 
 namespace {
 
-// t_i = sum_j (x_ij - mean_j) v_j   (warp per row)
-__global__ void k_pca_rows(const float* __restrict__ x, uint64_t n, uint32_t d,
-                           const double* __restrict__ mean, const double* __restrict__ v,
-                           double* __restrict__ t) {
-  const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n) return;
-  const float* xr = x + row * d;
+// t_i = sum_{j ascending} ((double)x_ij - mean_j) * v_j   (pca.hpp:40-45)
+// thread per row; a 128-row x 32-column tile is staged through shared memory.
+__global__ void __launch_bounds__(128) k_pca_rows(const float* __restrict__ x, uint64_t n,
+                                                  uint32_t d, const double* __restrict__ mean,
+                                                  const double* __restrict__ v,
+                                                  double* __restrict__ t, double* __restrict__ t2,
+                                                  const double* __restrict__ v2) {
+  constexpr int TP = 128, DK = 32;
+  __shared__ float xs[TP][DK + 1];
+  __shared__ double ms[DK], vs[DK], vs2[DK];
+  const uint64_t p0 = (uint64_t)blockIdx.x * TP;
+  const uint64_t gp = p0 + threadIdx.x;
+  double acc = 0.0, acc2 = 0.0;
+  for (uint32_t j0 = 0; j0 < d; j0 += DK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < TP * DK; e += TP) {
+      const int p = e / DK, jj = e % DK;
+      const uint64_t q = p0 + p;
+      xs[p][jj] = (q < n && j0 + jj < d) ? x[q * d + j0 + jj] : 0.f;
+    }
+    if (threadIdx.x < DK && j0 + threadIdx.x < d) {
+      ms[threadIdx.x] = mean[j0 + threadIdx.x];
+      vs[threadIdx.x] = v[j0 + threadIdx.x];
+      if (v2) vs2[threadIdx.x] = v2[j0 + threadIdx.x];
+    }
+    __syncthreads();
+    const int jmax = min(DK, (int)(d - j0));
+    for (int jj = 0; jj < jmax; ++jj) {
+      const double c = __dsub_rn((double)xs[threadIdx.x][jj], ms[jj]);
+      acc = __dadd_rn(acc, __dmul_rn(c, vs[jj]));
+      if (v2) acc2 = __dadd_rn(acc2, __dmul_rn(c, vs2[jj]));
+    }
+  }
+  if (gp < n) {
+    t[gp * (t2 ? 2 : 1)] = acc;
+    if (t2) t2[gp * 2] = acc2;
+  }
+}
+
+// y_j = (sum_{i ascending} ((double)x_ij - mean_j) * t_i) / n   (pca.hpp:47-54)
+// CTA per 32-column group: 8 warps stream BR-row slices (cp.async, double
+// buffer) and t; warp 0 runs the 32 column chains in order.
+template <int BR>
+__global__ void __launch_bounds__(256) k_pca_cols(const float* __restrict__ x, uint64_t n,
+                                                  uint32_t d, const double* __restrict__ mean,
+                                                  const double* __restrict__ t,
+                                                  double* __restrict__ y) {
+  extern __shared__ float sbuf[];  // [2][BR][33]
+  __shared__ double ts[2][BR];
+  const uint64_t j0 = (uint64_t)blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t j = j0 + lane;
+  const bool colok = j < d;
+  auto issue = [&](uint64_t b) {
+    const uint64_t r0 = b * BR;
+    float* dst = sbuf + (b & 1) * BR * 33;
+    for (int rr = warp; rr < BR; rr += 8) {
+      const uint64_t row = r0 + rr;
+      if (row < n && colok) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + rr * 33 + lane);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(x + row * d + j)
+                     : "memory");
+      }
+    }
+    for (int rr = threadIdx.x; rr < BR; rr += 256)
+      if (r0 + rr < n) ts[b & 1][rr] = t[r0 + rr];
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const uint64_t nb = (n + BR - 1) / BR;
+  const double m = colok ? mean[j] : 0.0;
   double acc = 0.0;
-  for (uint32_t j = lane; j < d; j += 32) acc += ((double)xr[j] - mean[j]) * v[j];
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) t[row] = acc;
+  issue(0);
+  for (uint64_t b = 0; b < nb; ++b) {
+    if (b + 1 < nb) issue(b + 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (warp == 0 && colok) {
+      const float* src = sbuf + (b & 1) * BR * 33;
+      const double* tb = ts[b & 1];
+      const int mrows = (int)umin64(BR, n - b * BR);
+      for (int r = 0; r < mrows; ++r)
+        acc = __dadd_rn(acc, __dmul_rn(__dsub_rn((double)src[r * 33 + lane], m), tb[r]));
+    }
+    __syncthreads();
+  }
+  if (warp == 0 && colok) y[j] = __ddiv_rn(acc, (double)n);
 }
 
-// y_j += sum_{i in chunk} (x_ij - mean_j) t_i   (block per row chunk,
-// thread per column, one atomic per (block, column))
-__global__ void k_pca_cols(const float* __restrict__ x, uint64_t n, uint32_t d,
-                           const double* __restrict__ mean, const double* __restrict__ t,
-                           uint64_t rows_per_block, double* __restrict__ y) {
-  const uint64_t r0 = blockIdx.x * rows_per_block;
-  const uint64_t r1 = umin64(r0 + rows_per_block, n);
-  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) {
-    double acc = 0.0;
-    const double m = mean[j];
-    for (uint64_t i = r0; i < r1; ++i) acc += ((double)x[i * d + j] - m) * t[i];
-    atomicAdd(&y[j], acc);
+// Sequential chains over a strided column of the layout (pca.hpp:197-212):
+// mode 0: sum_i v_i; mode 1: sum_i (v_i - mu)^2. One adding thread; the
+// block stages the next tile.
+__global__ void k_seq_col(const double* lay, uint64_t n, int comp, int mode, double mu,
+                          double* out) {
+  constexpr int T = 2048;
+  __shared__ double buf[2][T];
+  double acc = 0.0;
+  int cur = 0;
+  for (uint64_t e = threadIdx.x; e < T && e < n; e += blockDim.x) buf[0][e] = lay[2 * e + comp];
+  __syncthreads();
+  for (uint64_t b = 0; b < n; b += T) {
+    const uint64_t nb = b + T;
+    for (uint64_t e = threadIdx.x; e < T && nb + e < n; e += blockDim.x)
+      buf[cur ^ 1][e] = lay[2 * (nb + e) + comp];
+    if (threadIdx.x == 0) {
+      const uint64_t m = umin64(T, n - b);
+      if (mode == 0) {
+        for (uint64_t e = 0; e < m; ++e) acc = __dadd_rn(acc, buf[cur][e]);
+      } else {
+        for (uint64_t e = 0; e < m; ++e) {
+          const double c = __dsub_rn(buf[cur][e], mu);
+          acc = __dadd_rn(acc, __dmul_rn(c, c));
+        }
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
   }
-}
-
-// layout_i = (sum_j (x_ij - mean_j) b0_j, sum_j (x_ij - mean_j) b1_j)
-__global__ void k_pca_project(const float* __restrict__ x, uint64_t n, uint32_t d,
-                              const double* __restrict__ mean, const double* __restrict__ b0,
-                              const double* __restrict__ b1, double* __restrict__ out) {
-  const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= n) return;
-  const float* xr = x + row * d;
-  double a0 = 0.0, a1 = 0.0;
-  for (uint32_t j = lane; j < d; j += 32) {
-    const double c = (double)xr[j] - mean[j];
-    a0 += c * b0[j];
-    a1 += c * b1[j];
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-  }
-  if (lane == 0) {
-    out[2 * row] = a0;
-    out[2 * row + 1] = a1;
-  }
+  if (threadIdx.x == 0) *out = acc;
 }
 
 // sums of (x - mean)^2 and x^2 over all entries; column sums / sq of layout
@@ -86,25 +156,6 @@ __global__ void k_pca_moments(const float* __restrict__ x, uint64_t N, uint32_t 
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&out2[0], v);
     atomicAdd(&out2[1], s);
-  }
-}
-
-__global__ void k_layout_stats(const double* lay, uint64_t n, int comp, double mu, double* out) {
-  double s = 0.0, q = 0.0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const double v = lay[2 * i + comp];
-    s += v;
-    const double c = v - mu;
-    q += c * c;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    q += __shfl_xor_sync(0xffffffffu, q, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&out[0], s);
-    atomicAdd(&out[1], q);
   }
 }
 
@@ -153,21 +204,21 @@ void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, u
   if (total_var <= 1e-18 * std::max(1.0, total_sq))
     fail(kDegenerate, "data has zero variance");
 
-  const unsigned rows_blocks = (unsigned)((n * 32 + 255) / 256);
-  const uint64_t rpb = std::max<uint64_t>(64, (n + ctx->sm_count * 16 - 1) / (ctx->sm_count * 16));
-  const unsigned col_blocks = (unsigned)((n + rpb - 1) / rpb);
+  const unsigned row_blocks = (unsigned)((n + 127) / 128);
+  constexpr int BR = 256;
+  const size_t col_smem = 2 * BR * 33 * sizeof(float);
+  NB_CUDA(cudaFuncSetAttribute(k_pca_cols<BR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)col_smem));
   auto cov_apply = [&](const std::vector<double>& v, std::vector<double>& out) {
     NB_CUDA(cudaMemcpyAsync(vd.p, v.data(), d * 8, cudaMemcpyHostToDevice, S));
-    k_pca_rows<<<rows_blocks, 256, 0, S>>>(x, n, (uint32_t)d, mean.p, vd.p, t.p);
+    k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, vd.p, t.p, nullptr, nullptr);
     note_launch(ctx, "k_pca_rows");
-    NB_CUDA(cudaMemsetAsync(yd.p, 0, d * 8, S));
-    k_pca_cols<<<col_blocks, std::min<unsigned>(256, ((unsigned)d + 31) / 32 * 32), 0, S>>>(
-        x, n, (uint32_t)d, mean.p, t.p, rpb, yd.p);
+    k_pca_cols<BR><<<(unsigned)((d + 31) / 32), 256, col_smem, S>>>(x, n, (uint32_t)d, mean.p,
+                                                                      t.p, yd.p);
     note_launch(ctx, "k_pca_cols");
     out.resize(d);
     NB_CUDA(cudaMemcpyAsync(out.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
-    for (double& o : out) o /= static_cast<double>(n);
   };
 
   std::vector<double> applied(d);
@@ -246,8 +297,10 @@ void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, u
   DBuf<double> b0(d), b1(d), st(2);
   NB_CUDA(cudaMemcpyAsync(b0.p, basis[0].data(), d * 8, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(b1.p, basis[1].data(), d * 8, cudaMemcpyHostToDevice, S));
-  k_pca_project<<<rows_blocks, 256, 0, S>>>(x, n, (uint32_t)d, mean.p, b0.p, b1.p, layout_out);
-  note_launch(ctx, "k_pca_project");
+  // layout_i[comp] = j-ascending chain (pca.hpp:199-204), both components in one pass
+  k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, b0.p, layout_out,
+                                        layout_out + 1, b1.p);
+  note_launch(ctx, "k_pca_rows");
   const bool rank_deficient = eigen[1] <= 1e-12 * std::max(eigen[0], 0.0);
   for (int comp = 0; comp < 2; ++comp) {  // pca.hpp:189-216
     if (comp == 1 && rank_deficient) {
@@ -260,18 +313,17 @@ void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, u
       NB_CUDA(cudaStreamSynchronize(S));
       break;
     }
-    double h[2];
-    NB_CUDA(cudaMemsetAsync(st.p, 0, 16, S));
-    k_layout_stats<<<ctx->sm_count * 4, 256, 0, S>>>(layout_out, n, comp, 0.0, st.p);
-    NB_CUDA(cudaMemcpyAsync(h, st.p, 16, cudaMemcpyDeviceToHost, S));
+    double h = 0.0;
+    k_seq_col<<<1, 256, 0, S>>>(layout_out, n, comp, 0, 0.0, st.p);
+    note_launch(ctx, "k_seq_col");
+    NB_CUDA(cudaMemcpyAsync(&h, st.p, 8, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
-    const double col_mean = h[0] / static_cast<double>(n);
-    NB_CUDA(cudaMemsetAsync(st.p, 0, 16, S));
-    k_layout_stats<<<ctx->sm_count * 4, 256, 0, S>>>(layout_out, n, comp, col_mean, st.p);
-    note_launch(ctx, "k_layout_stats");
-    NB_CUDA(cudaMemcpyAsync(h, st.p, 16, cudaMemcpyDeviceToHost, S));
+    const double col_mean = h / static_cast<double>(n);
+    k_seq_col<<<1, 256, 0, S>>>(layout_out, n, comp, 1, col_mean, st.p);
+    note_launch(ctx, "k_seq_col");
+    NB_CUDA(cudaMemcpyAsync(&h, st.p, 8, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
-    const double sd = std::sqrt(h[1] / static_cast<double>(n));
+    const double sd = std::sqrt(h / static_cast<double>(n));
     if (sd > 0.0) {
       k_layout_scale<<<ctx->sm_count * 4, 256, 0, S>>>(layout_out, n, comp, sd);
       note_launch(ctx, "k_layout_scale");
