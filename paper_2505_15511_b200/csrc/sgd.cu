@@ -169,7 +169,7 @@ __global__ void k_means_exact(const double2* pos, const LocalCluster* lc, uint32
 // with the divergence scan of every position (optimizer.hpp:220-221).
 __global__ void k_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl,
                               uint32_t chunk, const uint32_t* chunk_off, double* sums,
-                              unsigned long long* diverge) {
+                              unsigned long long* diverge, unsigned long long tag) {
   __shared__ double red[8];
   // find cluster for this block
   uint32_t c = 0;
@@ -180,7 +180,7 @@ __global__ void k_means_chunk(const double2* pos, const LocalCluster* lc, uint32
   double sx = 0.0, sy = 0.0;
   for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
     const double2 v = pos[i];
-    if (diverged(v.x, v.y)) atomicMin(diverge, (unsigned long long)i);
+    if (diverged(v.x, v.y)) atomicMin(diverge, (tag << 32) | (unsigned long long)i);
     sx += v.x;
     sy += v.y;
   }
@@ -264,8 +264,8 @@ void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl
 
 void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
                         const uint32_t* chunk_off, uint32_t nchunks, double* sums,
-                        unsigned long long* diverge, cudaStream_t st) {
-  k_means_chunk<<<nchunks, 256, 0, st>>>(pos, lc, ncl, chunk, chunk_off, sums, diverge);
+                        unsigned long long* diverge, unsigned long long tag, cudaStream_t st) {
+  k_means_chunk<<<nchunks, 256, 0, st>>>(pos, lc, ncl, chunk, chunk_off, sums, diverge, tag);
 }
 
 void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, double* slot,

@@ -76,7 +76,7 @@ void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl
                         cudaStream_t st);
 void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
                         const uint32_t* chunk_off, uint32_t nchunks, double* sums,
-                        unsigned long long* diverge, cudaStream_t st);
+                        unsigned long long* diverge, unsigned long long tag, cudaStream_t st);
 void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, double* slot,
                            cudaStream_t st);
 void launch_means_unpack(const double* recv, const uint32_t* slot_gid, uint32_t nslots,

@@ -398,6 +398,8 @@ struct nomad_b200_trainer {
     if (total_chunks == 0) hog_blocks = 0;
   }
 
+  unsigned long long div_tag = 0;  // run-relative epoch tag of divergence keys (hogwild)
+
   void compute_means_and_exchange() {
     cudaStream_t S = st();
     const uint32_t ncl = (uint32_t)lcl.size();
@@ -406,7 +408,8 @@ struct nomad_b200_trainer {
         launch_means_exact(pos.p, lcl_d.p, ncl, slot.p, S);
         launched("k_means_exact");
       } else {
-        launch_means_chunk(pos.p, lcl_d.p, ncl, chunk, chunk_off.p, nchunks, sums.p, diverge.p, S);
+        launch_means_chunk(pos.p, lcl_d.p, ncl, chunk, chunk_off.p, nchunks, sums.p, diverge.p,
+                           div_tag, S);
         launched("k_means_chunk");
         launch_means_finalize(sums.p, lcl_d.p, ncl, slot.p, S);
         launched("k_means_finalize");
@@ -555,7 +558,95 @@ struct nomad_b200_trainer {
   }
 
   // ---------------------------------------------------------------- run
+  // Throughput mode without per-epoch host round trips: every epoch's SGD
+  // kernel, means pass and all-gather are queued back to back; per-epoch
+  // loss / edge sums land in device arrays and are read (and, multi-rank,
+  // gathered) once at the end; divergence keys carry the epoch.
+  void run_async(uint64_t n_epochs, double* epoch_loss) {
+    cudaStream_t S = st();
+    if (epochs_done + n_epochs > cfg.epochs) fail(kParameter, "epoch out of range for schedule");
+    const uint64_t E = n_epochs, L = std::max<uint32_t>(nwl, 1);
+    DBuf<double> lossb(E * L);
+    DBuf<unsigned long long> edgeb(E * L);
+    NB_CUDA(cudaMemsetAsync(lossb.p, 0, lossb.bytes(), S));
+    NB_CUDA(cudaMemsetAsync(edgeb.p, 0, edgeb.bytes(), S));
+    std::vector<cudaEvent_t> evs(3 * E);
+    for (auto& x : evs) NB_CUDA(cudaEventCreate(&x));
+    const uint64_t e_first = epochs_done;
+    for (uint64_t it = 0; it < E; ++it) {
+      const uint64_t e = epochs_done;
+      const double lr = lr0 * (1.0 - static_cast<double>(e) / static_cast<double>(cfg.epochs));
+      const double step = lr / static_cast<double>(cfg.batch_size);
+      SgdParams P = params(step, e);
+      P.loss_acc = lossb.p + it * L;
+      P.edge_acc = edgeb.p + it * L;
+      NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
+      NB_CUDA(cudaEventRecord(evs[3 * it], S));
+      if (hog_blocks) {
+        launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
+        launched("k_sgd_hogwild");
+      }
+      NB_CUDA(cudaEventRecord(evs[3 * it + 1], S));
+      div_tag = it;
+      compute_means_and_exchange();
+      NB_CUDA(cudaEventRecord(evs[3 * it + 2], S));
+      ++comm_epochs;
+      comm_msgs += W;
+      comm_doubles += 2 * C;
+      comm_counts += C;
+      ++epochs_done;
+    }
+    div_tag = 0;
+    std::vector<double> lh(E * L);
+    std::vector<unsigned long long> eh(E * L);
+    NB_CUDA(cudaMemcpyAsync(lh.data(), lossb.p, E * L * 8, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaMemcpyAsync(eh.data(), edgeb.p, E * L * 8, cudaMemcpyDeviceToHost, S));
+    std::vector<double> all;
+    if (world > 1) {
+      DBuf<double> g((size_t)world * E * L);
+      NB_NCCL(ncclAllGather(lossb.p, g.p, E * L, ncclDouble, comm, S));
+      all.resize((size_t)world * E * L);
+      NB_CUDA(cudaMemcpyAsync(all.data(), g.p, all.size() * 8, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+    }
+    unsigned long long key = 0;
+    NB_CUDA(cudaMemcpyAsync(&key, diverge.p, 8, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    for (uint64_t it = 0; it < E; ++it) {
+      float a = 0.f, b = 0.f;
+      NB_CUDA(cudaEventElapsedTime(&a, evs[3 * it], evs[3 * it + 1]));
+      NB_CUDA(cudaEventElapsedTime(&b, evs[3 * it + 1], evs[3 * it + 2]));
+      sgd_ms += a;
+      means_ms += b;
+      ++timed_epochs;
+    }
+    for (auto& x : evs) cudaEventDestroy(x);
+    if (key != ~0ull) {
+      char m[200];
+      snprintf(m, sizeof m, "positions diverged at epoch %llu (point %u)",
+               (unsigned long long)(e_first + (key >> 32)), orig_of[(uint32_t)key]);
+      fail(kDivergence, m);
+    }
+    const uint64_t heads = world > 1 ? total_heads_global() : [&] {
+      uint64_t h = 0;
+      for (auto& d : wk) h += d.draws;
+      return h;
+    }();
+    for (uint64_t it = 0; it < E; ++it) {
+      double loss_sum = 0.0;  // worker order: rank-major, then local worker
+      if (world > 1) {
+        for (int r = 0; r < world; ++r)
+          for (uint32_t wl = 0; wl < nwl; ++wl) loss_sum += all[((size_t)r * E + it) * L + wl];
+      } else {
+        for (uint32_t wl = 0; wl < nwl; ++wl) loss_sum += lh[it * L + wl];
+      }
+      for (uint32_t wl = 0; wl < nwl; ++wl) edge_updates += eh[it * L + wl];
+      if (epoch_loss) epoch_loss[it] = heads > 0 ? loss_sum / static_cast<double>(heads) : 0.0;
+    }
+  }
+
   void run(uint64_t n_epochs, double* epoch_loss) {
+    if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD && !cfg.verbose) return run_async(n_epochs, epoch_loss);
     cudaStream_t S = st();
     if (draw_base_h.empty()) {
       draw_base_h.assign(nwl, 0);
