@@ -39,6 +39,9 @@
 #ifndef HOG_CAS
 #define HOG_CAS 0         // 1: one 128-bit CAS per row instead of two RED.F64 (measured 1.9x slower)
 #endif
+#ifndef HOG_PLAIN
+#define HOG_PLAIN 0       // 1: unsynchronised read-modify-write rows (the reference's Hogwild stores)
+#endif
 #ifndef HOG_MF32
 #define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
 #endif
@@ -284,6 +287,8 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
             const double a = st * pull;
 #if HOG_CAS
             dn[i] = make_double2(a * dx, a * dy);
+#elif HOG_PLAIN
+            P.pos[nb[i]] = make_double2(pn[i].x + a * dx, pn[i].y + a * dy);
 #else
             atomicAdd(&P.pos[nb[i]].x, a * dx);
             atomicAdd(&P.pos[nb[i]].y, a * dy);
@@ -305,6 +310,8 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
             const double a = -st * push;
 #if HOG_CAS
             dt[m] = make_double2(a * dx, a * dy);
+#elif HOG_PLAIN
+            P.pos[tl[m]] = make_double2(pt[m].x + a * dx, pt[m].y + a * dy);
 #else
             atomicAdd(&P.pos[tl[m]].x, a * dx);
             atomicAdd(&P.pos[tl[m]].y, a * dy);
@@ -341,6 +348,11 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           cas_add_finish(&P.pos[head], h, sh, hx, hy);
           edge_acc += (double)(cnt + s);
         }
+      }
+#elif HOG_PLAIN
+      if (act && gl == 0) {
+        P.pos[head] = make_double2(h.x - st * gx, h.y - st * gy);
+        edge_acc += (double)(cnt + s);
       }
 #else
       if (act && gl == 0) {
