@@ -190,6 +190,28 @@ int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
 int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
                              uint64_t* exhaustive_rows);
 
+/* ------------------------------------------- final-map quality metrics */
+/* metrics.hpp:113-168 neighborhood_preservation on the GPU. Same evaluated
+ * points (sample == 0 or >= rows: all; else partial Fisher-Yates on the
+ * reference stream stream_seed(seed, "np")), exact high-d neighbours by
+ * (reference fp64 distance, id), exact 2-D neighbours, overlaps accumulated
+ * in evaluation order: value and std_error are bit-identical to the
+ * reference's. layout: rows x 2 f64 at layout_location. 1 <= k <= 56,
+ * k < rows (else NOMAD_B200_ERR_PARAMETER). std_error may be NULL. */
+int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
+                                             const nomad_b200_dataset_view* high,
+                                             const double* layout, int32_t layout_location,
+                                             uint64_t k, uint64_t sample, uint64_t seed,
+                                             double* value, double* std_error);
+/* metrics.hpp:205-243 random_triplet_accuracy on the GPU: triplets drawn on
+ * the host from the reference stream stream_seed(seed, "tri"), distances and
+ * the agreement count on the device; bit-identical value / std_error. */
+int32_t nomad_b200_random_triplet_accuracy(nomad_b200_ctx* ctx,
+                                           const nomad_b200_dataset_view* high,
+                                           const double* layout, int32_t layout_location,
+                                           uint64_t n_triplets, uint64_t seed, double* value,
+                                           double* std_error);
+
 /* --------------------------------------------- epoch loop (L3 + L4) */
 /* The setup half of fit() (optimizer.hpp:342-386): build_affinity,
  * shard_clusters, make_noise_model, worker states, means of the init layout.

@@ -8,4 +8,5 @@ from ._native import NomadError, build, lib, EXPORTED  # noqa: F401
 from .api import (ClusterAssignment, CommLog, Context, FitReport, KnnGraph,  # noqa: F401
                   TrainConfig, Trainer, build_knn, default_kmeans_tol, fit,
                   kmeans_em_default_tol, knn_recall, pca_init, shard_plan,
-                  generate_mixture, kmeans_em, lsh_init, nccl_unique_id)
+                  generate_mixture, kmeans_em, lsh_init, nccl_unique_id,
+                  neighborhood_preservation, random_triplet_accuracy)

@@ -80,6 +80,14 @@ _SIGS = {
                                           C.POINTER(GraphView), C.c_uint64, C.c_uint64,
                                           C.POINTER(C.c_double)]),
     "nomad_b200_knn_stats": (C.c_int32, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "nomad_b200_neighborhood_preservation": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp, C.c_int32,
+                                                         C.c_uint64, C.c_uint64, C.c_uint64,
+                                                         C.POINTER(C.c_double),
+                                                         C.POINTER(C.c_double)]),
+    "nomad_b200_random_triplet_accuracy": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp, C.c_int32,
+                                                       C.c_uint64, C.c_uint64,
+                                                       C.POINTER(C.c_double),
+                                                       C.POINTER(C.c_double)]),
     "nomad_b200_trainer_create": (C.c_int32, [_vp, C.POINTER(GraphView), C.POINTER(ClustersView),
                                               _vp, C.c_int32, C.POINTER(TrainConfigC),
                                               C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),

@@ -286,6 +286,31 @@ def knn_recall(data, clusters: ClusterAssignment, graph: KnnGraph, sample: int =
     return out.value
 
 
+# ---------------------------------------------------------------- quality metrics
+
+def neighborhood_preservation(data, layout, k: int = 10, sample: int = 0, seed: int = 0,
+                              ctx: Optional[Context] = None):
+    """metrics.hpp:113-168 on the GPU -> (value, std_error), bit-identical to the
+    reference's (same sampled rows, exact high-d and 2-D neighbours)."""
+    dv, keep = _dataset(data)
+    lp, lloc, lkeep = _view(layout, np.float64)
+    v, se = C.c_double(), C.c_double()
+    check(lib().nomad_b200_neighborhood_preservation(_ctx(ctx).h, C.byref(dv), lp, lloc, k, sample,
+                                                     seed & (2**64 - 1), C.byref(v), C.byref(se)))
+    return v.value, se.value
+
+
+def random_triplet_accuracy(data, layout, count: int = 100000, seed: int = 0,
+                            ctx: Optional[Context] = None):
+    """metrics.hpp:205-243 on the GPU -> (value, std_error), bit-identical."""
+    dv, keep = _dataset(data)
+    lp, lloc, lkeep = _view(layout, np.float64)
+    v, se = C.c_double(), C.c_double()
+    check(lib().nomad_b200_random_triplet_accuracy(_ctx(ctx).h, C.byref(dv), lp, lloc, count,
+                                                   seed & (2**64 - 1), C.byref(v), C.byref(se)))
+    return v.value, se.value
+
+
 # ---------------------------------------------------------------- training
 
 @dataclass

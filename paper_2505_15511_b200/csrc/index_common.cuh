@@ -31,6 +31,13 @@ struct HostRng {
   }
   static uint64_t stream_seed(uint64_t base, uint64_t s) { return mix(base ^ mix(s)); }
   explicit HostRng(uint64_t seed) : g(seed) {}
+  // unbiased integer in [0, n): rejection on the top range (rng.hpp:49-55)
+  uint64_t uniform_index(uint64_t n) {
+    const uint64_t limit = n * (0xFFFFFFFFFFFFFFFFull / n);
+    uint64_t draw = g();
+    while (draw >= limit) draw = g();
+    return draw % n;
+  }
   double uniform01() { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
   double gaussian() {
     if (have) {
@@ -47,6 +54,36 @@ struct HostRng {
     return radius * std::cos(angle);
   }
 };
+
+// Reference fp64 distance (knn.hpp:51-58), j ascending, no FMA.
+__device__ __forceinline__ double ref_dist(const float* __restrict__ a, const float* __restrict__ b,
+                                           uint32_t d) {
+  double acc = 0.0;
+  uint32_t j = 0;
+  if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+    for (; j + 4 <= d; j += 4) {
+      const float4 u = *reinterpret_cast<const float4*>(a + j);
+      const float4 v = *reinterpret_cast<const float4*>(b + j);
+      double t = __dsub_rn((double)u.x, (double)v.x);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)u.y, (double)v.y);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)u.z, (double)v.z);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn((double)u.w, (double)v.w);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+  }
+  for (; j < d; ++j) {
+    const double t = __dsub_rn((double)a[j], (double)b[j]);
+    acc = __dadd_rn(acc, __dmul_rn(t, t));
+  }
+  return acc;
+}
+
+__device__ __forceinline__ bool key_less(double da, uint32_t ia, double db, uint32_t ib) {
+  return da < db || (da == db && ia < ib);
+}
 
 // A dataset on the device (uploaded once per call when the caller passed
 // host memory).
@@ -84,5 +121,11 @@ void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uin
 void seq_column_means(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
                       const std::vector<uint32_t>& seg_ids, double* out);
+
+// Exact global kNN of m sampled points (knn.cu): out_ids_d[v * k + r] = the
+// r-th smallest (reference fp64 distance, id) key of point qlist_d[v] among
+// all other points. 1 <= k <= 56, k < n.
+void knn_global_sample(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                       const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d);
 
 }  // namespace nb

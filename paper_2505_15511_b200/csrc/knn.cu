@@ -29,17 +29,11 @@ constexpr int QT = 64;    // queries per block
 constexpr int CT = 128;   // candidates per tile
 constexpr int DK = 32;    // dims per smem chunk
 
-struct ClusterSeg {
-  uint64_t beg;   // offset into members
-  uint32_t size;  // members in the cluster
-  uint32_t qtile; // first query tile index of this cluster
-};
-
-template <int KP>
+template <int KP, int CAP = KP + CT>
 __device__ void compact_warp(float* bd, uint32_t* bi, uint32_t& cnt, float& tau, int lane) {
-  // keep the KP smallest (dist) of cnt <= KP + CT entries, by repeated
+  // keep the KP smallest (dist) of cnt <= CAP entries, by repeated
   // warp-wide min extraction; tau = KP-th smallest.
-  constexpr int PER = (KP + CT + 31) / 32;
+  constexpr int PER = (CAP + 31) / 32;
   float v[PER];
   uint32_t id[PER];
 #pragma unroll
@@ -89,26 +83,68 @@ __device__ void compact_warp(float* bd, uint32_t* bi, uint32_t& cnt, float& tau,
   __syncwarp();
 }
 
-// Pass 1. grid = total query tiles; block 256 = 16 x 16 threads; thread
-// (tx, ty) owns queries ty + 16 i (4) and candidates tx + 16 c (8).
-template <int KP>
+// Pass 1 (FFMA filter). grid = query tiles of 64; block 256 = 16 x 16
+// threads; thread (tx, ty) owns queries ty + 16 i (4) and candidates
+// tx + 16 c (8) of each 128-candidate tile; distances are fp32 j-ascending
+// chains sum (a - b)^2.
+//  * the 32-dim chunks of the query and candidate tiles are double-buffered
+//    in shared memory by cp.async (16-byte pieces when rows are
+//    float4-addressable, else four 4-byte copies per piece), the next chunk
+//    in flight while the current one is consumed; each thread owns six fixed
+//    pieces per chunk, so the only per-tile address work is four row ids;
+//  * rows are stored unpadded with the 16-byte pieces XOR-swizzled by
+//    (row & 7), so the compute loop reads float4s (one LDS.128 feeds four
+//    dims) without bank conflicts;
+//  * queries come from their own list (the whole cluster, the rows a
+//    tensor-core certificate left open, or a metric's sample); self-pairs
+//    are excluded by id; members == nullptr means candidates are the rows
+//    [beg, beg + size) themselves;
+//  * insertions run in phases of 64 (KP = 32) or 32 (KP = 64) candidates per
+//    query, so the survivor buffers hold KP + 64 / KP + 32 entries and two
+//    CTAs fit per SM.
+struct FilterSeg {
+  uint64_t beg;    // candidates: members[beg, beg + size)
+  uint64_t qbeg;   // queries: qlist[qbeg, qbeg + qn)
+  uint32_t size;
+  uint32_t qn;
+  uint32_t qtile;  // first query tile of this segment
+  uint32_t part;   // candidate partition (slot-indexed output)
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+template <int KP, bool V4>
 __global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__ x, uint32_t d,
                                                        const uint32_t* __restrict__ members,
-                                                       const ClusterSeg* segs, uint32_t nseg,
-                                                       uint32_t* cand_ids, float* cand_tau,
-                                                       uint32_t* cand_cnt, double lbf) {
-  constexpr int CAP = KP + CT;
+                                                       const uint32_t* __restrict__ qlist,
+                                                       const FilterSeg* segs, uint32_t nseg,
+                                                       int by_slot /* 0: by point id; P: slot * P + part */,
+                                                       uint32_t* cand_ids,
+                                                       float* cand_tau, uint32_t* cand_cnt,
+                                                       double lbf) {
+  constexpr int NPH = KP <= 32 ? 2 : 4;    // insertion phases per tile
+  constexpr int CPP = 8 / NPH;             // candidates per thread per phase
+  constexpr int CAP = KP + CT / NPH;
+  constexpr int ROWS = QT + CT;           // rows per chunk buffer
+  constexpr int BUF = ROWS * DK;          // floats per chunk buffer
   extern __shared__ __align__(16) unsigned char smraw[];
-  float(*qs)[DK + 1] = reinterpret_cast<float(*)[DK + 1]>(smraw);
-  float(*cs)[DK + 1] = reinterpret_cast<float(*)[DK + 1]>(smraw + QT * (DK + 1) * 4);
-  float* bd = reinterpret_cast<float*>(smraw + (QT + CT) * (DK + 1) * 4);
+  float* tb = reinterpret_cast<float*>(smraw);  // 2 x BUF
+  float* bd = tb + 2 * BUF;
   uint32_t* bi = reinterpret_cast<uint32_t*>(bd + QT * CAP);
   uint32_t* cnt = bi + QT * CAP;
   float* tau = reinterpret_cast<float*>(cnt + QT);
   uint32_t* qid = reinterpret_cast<uint32_t*>(tau + QT);
   __shared__ int any_full;
 
-  // which cluster / query tile
   uint32_t s = 0;
   {
     uint32_t lo = 0, hi = nseg;
@@ -118,158 +154,186 @@ __global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__
     }
     s = lo;
   }
-  const ClusterSeg S = segs[s];
-  const uint32_t q0 = (blockIdx.x - S.qtile) * QT;  // query offset inside the cluster
+  const FilterSeg S = segs[s];
+  const uint32_t q0 = (blockIdx.x - S.qtile) * QT;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int q = threadIdx.x; q < QT; q += 256) {
     cnt[q] = 0;
     tau[q] = __int_as_float(0x7f800000);
-    qid[q] = q0 + q < S.size ? members[S.beg + q0 + q] : 0xFFFFFFFFu;
+    qid[q] = q0 + q < S.qn ? qlist[S.qbeg + q0 + q] : 0xFFFFFFFFu;
   }
-  __syncthreads();
+  // this thread's pieces: rows r_e = threadIdx.x / 8 + 32 e (e < 6; e < 2 are
+  // query rows), 16-byte piece pc = threadIdx.x & 7 of each row's chunk
+  const int pr = threadIdx.x >> 3, pc = threadIdx.x & 7;
+  const float* qrow[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const uint32_t qq = q0 + pr + 32 * e;
+    qrow[e] = qq < S.qn ? x + (uint64_t)qlist[S.qbeg + qq] * d : nullptr;
+  }
+  const float* crow[4];
+  auto load_crow = [&](uint32_t c0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t cl = c0 + pr + 32 * e;
+      crow[e] = cl < S.size ? x + (members ? (uint64_t)members[S.beg + cl] : S.beg + cl) * d
+                            : nullptr;
+    }
+  };
+  const uint32_t smem_tb = (uint32_t)__cvta_generic_to_shared(tb);
+  // piece (row, pc) of chunk j0 -> buffer b; swizzled slot pc ^ (row & 7)
+  auto issue = [&](int b, uint32_t j0) {
+    const uint32_t jb = j0 + 4 * pc;
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      const int row = pr + 32 * e;
+      const float* rp = e < 2 ? qrow[e] : crow[e - 2];
+      const uint32_t dst = smem_tb + (uint32_t)((b * BUF + row * DK + ((pc ^ (row & 7)) << 2)) * 4);
+      if constexpr (V4) {
+        const bool ok = rp != nullptr && jb < d;
+        cp_async16(dst, ok ? (const void*)(rp + jb) : (const void*)x, ok ? 16u : 0u);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = rp != nullptr && jb + u < d;
+          cp_async4(dst + 4 * u, ok ? (const void*)(rp + jb + u) : (const void*)x, ok ? 4u : 0u);
+        }
+      }
+    }
+  };
+  const uint32_t nchunk = (d + DK - 1) / DK;
+  load_crow(0);
+  issue(0, 0);
+  cp_async_commit();
+  uint32_t it = 0;  // global chunk counter (buffer = it & 1)
   for (uint32_t c0 = 0; c0 < S.size; c0 += CT) {
     float acc[4][8];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
-    for (uint32_t j0 = 0; j0 < d; j0 += DK) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < QT * DK; e += 256) {
-        const int p = e / DK, jj = e % DK;
-        const uint32_t g = qid[p];
-        qs[p][jj] = (g != 0xFFFFFFFFu && j0 + jj < d) ? x[(uint64_t)g * d + j0 + jj] : 0.f;
+    for (uint32_t ch = 0; ch < nchunk; ++ch, ++it) {
+      // prefetch the next chunk (next tile's first chunk at the end of a tile)
+      if (ch + 1 < nchunk) {
+        issue((it + 1) & 1, (ch + 1) * DK);
+      } else if (c0 + CT < S.size) {
+        load_crow(c0 + CT);
+        issue((it + 1) & 1, 0);
       }
-      for (int e = threadIdx.x; e < CT * DK; e += 256) {
-        const int p = e / DK, jj = e % DK;
-        const uint32_t cl = c0 + p;
-        cs[p][jj] = (cl < S.size && j0 + jj < d)
-                        ? x[(uint64_t)members[S.beg + cl] * d + j0 + jj] : 0.f;
-      }
+      cp_async_commit();
+      cp_async_wait1();
       __syncthreads();
-#pragma unroll 4
-      for (int jj = 0; jj < DK; ++jj) {
-        float qv[4], cv[8];
+      const float* Q = tb + (it & 1) * BUF;
+      const float* Cc = Q + QT * DK;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) qv[i] = qs[ty + 16 * i][jj];
+      for (int p = 0; p < DK / 4; ++p) {
+        float4 qv[4], cv[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) cv[c] = cs[tx + 16 * c][jj];
+        for (int i = 0; i < 4; ++i)
+          qv[i] = *reinterpret_cast<const float4*>(Q + (ty + 16 * i) * DK + ((p ^ (ty & 7)) << 2));
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          cv[c] = *reinterpret_cast<const float4*>(Cc + (tx + 16 * c) * DK + ((p ^ (tx & 7)) << 2));
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float df = qv[i] - cv[c];
+            float df = qv[i].x - cv[c].x;
+            acc[i][c] = fmaf(df, df, acc[i][c]);
+            df = qv[i].y - cv[c].y;
+            acc[i][c] = fmaf(df, df, acc[i][c]);
+            df = qv[i].z - cv[c].z;
+            acc[i][c] = fmaf(df, df, acc[i][c]);
+            df = qv[i].w - cv[c].w;
             acc[i][c] = fmaf(df, df, acc[i][c]);
           }
       }
-    }
-    // insert below-threshold candidates
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int q = ty + 16 * i;
-      const uint32_t gq = qid[q];
-      if (gq == 0xFFFFFFFFu) continue;
-      const float t = tau[q];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t cl = c0 + tx + 16 * c;
-        if (cl < S.size && cl != q0 + q && acc[i][c] < t) {
-          const uint32_t pos = atomicAdd(&cnt[q], 1u);
-          bd[q * CAP + pos] = acc[i][c];
-          bi[q * CAP + pos] = members[S.beg + cl];
-        }
-      }
-    }
-    if (threadIdx.x == 0) any_full = 0;
-    __syncthreads();
-    for (int q = threadIdx.x; q < QT; q += 256)
-      if (cnt[q] > KP) any_full = 1;
-    __syncthreads();
-    if (any_full) {
-      for (int q = warp; q < QT; q += 8)
-        if (cnt[q] > KP) compact_warp<KP>(bd + q * CAP, bi + q * CAP, cnt[q], tau[q], lane);
       __syncthreads();
     }
+    // insert below-threshold candidates, CT / NPH per query at a time
+#pragma unroll
+    for (int h = 0; h < NPH; ++h) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int q = ty + 16 * i;
+        const uint32_t gq = qid[q];
+        if (gq == 0xFFFFFFFFu) continue;
+        const float t = tau[q];
+#pragma unroll
+        for (int c = CPP * h; c < CPP * h + CPP; ++c) {
+          const uint32_t cl = c0 + tx + 16 * c;
+          if (cl < S.size && acc[i][c] < t) {
+            const uint32_t gid = members ? members[S.beg + cl] : (uint32_t)(S.beg + cl);
+            if (gid != gq) {
+              const uint32_t pos = atomicAdd(&cnt[q], 1u);
+              bd[q * CAP + pos] = acc[i][c];
+              bi[q * CAP + pos] = gid;
+            }
+          }
+        }
+      }
+      if (threadIdx.x == 0) any_full = 0;
+      __syncthreads();
+      for (int q = threadIdx.x; q < QT; q += 256)
+        if (cnt[q] > KP) any_full = 1;
+      __syncthreads();
+      if (any_full) {
+        for (int q = warp; q < QT; q += 8)
+          if (cnt[q] > KP) compact_warp<KP, CAP>(bd + q * CAP, bi + q * CAP, cnt[q], tau[q], lane);
+        __syncthreads();
+      }
+    }
   }
-  // write survivors
+  // survivors, indexed by point id (graph build) or by query slot (metrics)
   for (int q = warp; q < QT; q += 8) {
     const uint32_t gq = qid[q];
     if (gq == 0xFFFFFFFFu) continue;
+    const uint64_t o = by_slot ? (S.qbeg + q0 + q) * (uint64_t)by_slot + S.part : gq;
     const uint32_t c = cnt[q];
-    if (lane < (int)c) cand_ids[(uint64_t)gq * KP + lane] = bi[q * CAP + lane];
-    if (KP > 32 && lane + 32 < (int)c) cand_ids[(uint64_t)gq * KP + lane + 32] = bi[q * CAP + lane + 32];
+    if (lane < (int)c) cand_ids[o * KP + lane] = bi[q * CAP + lane];
+    if (KP > 32 && lane + 32 < (int)c) cand_ids[o * KP + lane + 32] = bi[q * CAP + lane + 32];
     if (lane == 0) {
-      cand_cnt[gq] = c;
-      // lower bound on every excluded candidate's reference distance
-      cand_tau[gq] = c == KP ? __double2float_rd((double)tau[q] * lbf) : __int_as_float(0x7f800000);
+      cand_cnt[o] = c;
+      cand_tau[o] = c == KP ? __double2float_rd((double)tau[q] * lbf) : __int_as_float(0x7f800000);
     }
   }
 }
 
-// Reference fp64 distance (knn.hpp:51-58), j ascending, no FMA.
-__device__ __forceinline__ double ref_dist(const float* __restrict__ a, const float* __restrict__ b,
-                                           uint32_t d) {
-  double acc = 0.0;
-  uint32_t j = 0;
-  if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
-    for (; j + 4 <= d; j += 4) {
-      const float4 u = *reinterpret_cast<const float4*>(a + j);
-      const float4 v = *reinterpret_cast<const float4*>(b + j);
-      double t = __dsub_rn((double)u.x, (double)v.x);
-      acc = __dadd_rn(acc, __dmul_rn(t, t));
-      t = __dsub_rn((double)u.y, (double)v.y);
-      acc = __dadd_rn(acc, __dmul_rn(t, t));
-      t = __dsub_rn((double)u.z, (double)v.z);
-      acc = __dadd_rn(acc, __dmul_rn(t, t));
-      t = __dsub_rn((double)u.w, (double)v.w);
-      acc = __dadd_rn(acc, __dmul_rn(t, t));
-    }
-  }
-  for (; j < d; ++j) {
-    const double t = __dsub_rn((double)a[j], (double)b[j]);
-    acc = __dadd_rn(acc, __dmul_rn(t, t));
-  }
-  return acc;
-}
-
-__device__ __forceinline__ bool key_less(double da, uint32_t ia, double db, uint32_t ib) {
-  return da < db || (da == db && ia < ib);
-}
-
-// Pass 2: warp per query; lanes own KP/32 survivors each; warp bitonic sort
-// by (distance, id).
+// Pass 2: warp per query slot; lanes own KP/32 survivors each; the `want`
+// smallest (distance, id) keys are extracted in order. Slot v is point
+// qlist[v] (qlist == nullptr: point v); want = min(k, size - 1) of its
+// cluster (assign/sizes) or `fixed_want` when nonzero; list position
+// offsets[point] or v * k when offsets == nullptr.
 template <int KP>
-__global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t n,
-                             const uint32_t* assign, const uint32_t* sizes, uint32_t k,
-                             const uint32_t* cand_ids, const float* cand_tau,
-                             const uint32_t* cand_cnt, const uint32_t* offsets, uint32_t* out_nb,
-                             double* out_d, uint32_t* fallback, uint32_t* n_fallback,
-                             double lb_factor) {
+__global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t nq,
+                             const uint32_t* qlist, const uint32_t* assign, const uint32_t* sizes,
+                             uint32_t k, uint32_t fixed_want, const uint32_t* cand_ids,
+                             const float* cand_tau, const uint32_t* cand_cnt,
+                             const uint32_t* offsets, uint32_t* out_nb, double* out_d,
+                             uint32_t* fallback, uint32_t* n_fallback, double lb_factor) {
   constexpr int PER = KP / 32;
-  const uint64_t q = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (q >= n) return;
-  const uint32_t size = sizes[assign[q]];
-  const uint32_t want = min(k, size - 1);
+  if (v >= nq) return;
+  const uint64_t q = qlist ? qlist[v] : v;
+  const uint32_t want = fixed_want ? fixed_want : min(k, sizes[assign[q]] - 1);
   if (want == 0) return;
-  const uint32_t c = cand_cnt[q];
+  const uint32_t c = cand_cnt[v];
   double dv[PER];
   uint32_t iv[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) {
     const int p = lane + 32 * e;  // slot
     if (p < (int)c) {
-      iv[e] = cand_ids[q * KP + p];
+      iv[e] = cand_ids[v * KP + p];
       dv[e] = ref_dist(x + q * d, x + (uint64_t)iv[e] * d, d);
     } else {
       iv[e] = 0xFFFFFFFFu;
       dv[e] = __longlong_as_double(0x7ff0000000000000ll);
     }
   }
-  // select the `want` smallest (distance, id) keys in order by repeated
-  // warp-wide min extraction; rank r goes to out[o + r].
-  const uint32_t o = offsets[q];
+  const uint64_t o = offsets ? (uint64_t)offsets[q] : v * k;
   double dk = 0.0;
   for (uint32_t r = 0; r < want; ++r) {
     double m = dv[0];
@@ -298,31 +362,38 @@ __global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t n
     dk = wm;
   }
   // certificate (dk = the want-th exact distance among the survivors)
-  const float t = cand_tau[q];
-  const bool complete = c < KP || isinf(t);
-  const bool ok = complete || (double)t * lb_factor > dk;
-  if (!ok && lane == 0) fallback[atomicAdd(n_fallback, 1u)] = (uint32_t)q;
+  const float t = cand_tau[v];
+  // (every filter writes +inf when its list holds all candidates)
+  const bool ok = isinf(t) || (double)t * lb_factor > dk;
+  if (!ok && lane == 0) fallback[atomicAdd(n_fallback, 1u)] = (uint32_t)v;
 }
 
-// Pass 3: one block per uncertified query, exhaustive fp64 over its cluster;
-// per-thread sorted top-`want`, merged by warp 0.
+// Pass 3: one block per uncertified slot, exhaustive fp64 over its cluster
+// (members[cl_beg[r] ..], or every point when members == nullptr); per-thread
+// sorted top-`want`, merged by a block reduction. Slot / want / offsets as in
+// pass 2.
 __global__ void __launch_bounds__(128) k_knn_exhaustive(
-    const float* __restrict__ x, uint32_t d, const uint32_t* assign, const uint32_t* members,
-    const uint64_t* cl_beg, const uint32_t* sizes, uint32_t k, const uint32_t* fallback,
+    const float* __restrict__ x, uint32_t d, uint64_t n_all, const uint32_t* qlist,
+    const uint32_t* assign, const uint32_t* members, const uint64_t* cl_beg,
+    const uint32_t* sizes, uint32_t k, uint32_t fixed_want, const uint32_t* fallback,
     const uint32_t* offsets, uint32_t* out_nb, double* out_d) {
   constexpr int KMAX = 64;
   __shared__ double sd[128 * 8];
   __shared__ uint32_t si[128 * 8];
-  const uint32_t q = fallback[blockIdx.x];
-  const uint32_t r = assign[q];
-  const uint32_t size = sizes[r];
-  const uint32_t want = min(k, size - 1);
-  const uint64_t beg = cl_beg[r];
+  const uint32_t v = fallback[blockIdx.x];
+  const uint32_t q = qlist ? qlist[v] : v;
+  uint64_t size = n_all, beg = 0;
+  if (members) {
+    const uint32_t r = assign[q];
+    size = sizes[r];
+    beg = cl_beg[r];
+  }
+  const uint32_t want = fixed_want ? fixed_want : (uint32_t)umin64(k, size - 1);
   double bd[KMAX];
   uint32_t bi[KMAX];
   uint32_t cnt = 0;
-  for (uint32_t t = threadIdx.x; t < size; t += blockDim.x) {
-    const uint32_t j = members[beg + t];
+  for (uint64_t t = threadIdx.x; t < size; t += blockDim.x) {
+    const uint32_t j = members ? members[beg + t] : (uint32_t)t;
     if (j == q) continue;
     const double dd = ref_dist(x + (uint64_t)q * d, x + (uint64_t)j * d, d);
     if (cnt == want && !key_less(dd, j, bd[want - 1], bi[want - 1])) continue;
@@ -338,11 +409,11 @@ __global__ void __launch_bounds__(128) k_knn_exhaustive(
   }
   // merge: repeatedly take the global min of the per-thread list heads
   uint32_t head = 0;
-  const uint32_t o = offsets[q];
+  const uint64_t o = offsets ? (uint64_t)offsets[q] : (uint64_t)v * k;
   for (uint32_t r2 = 0; r2 < want; ++r2) {
-    double v = head < cnt ? bd[head] : __longlong_as_double(0x7ff0000000000000ll);
+    double val = head < cnt ? bd[head] : __longlong_as_double(0x7ff0000000000000ll);
     uint32_t vi = head < cnt ? bi[head] : 0xFFFFFFFFu;
-    sd[threadIdx.x] = v;
+    sd[threadIdx.x] = val;
     si[threadIdx.x] = vi;
     __syncthreads();
     for (int st = 64; st > 0; st >>= 1) {
@@ -396,6 +467,64 @@ struct KnnResult {
   uint64_t tc_uncertified = 0;  // rows the tensor-core certificate did not settle
 };
 
+// Concatenate the P partition lists of each query slot (slot-major, KP per
+// partition) into one list of up to P * KP ids; the slot's bound is the
+// smallest partition bound (+inf partitions hold all their candidates).
+__global__ void k_merge_parts(uint32_t m, uint32_t P, uint32_t KP, const uint32_t* pid,
+                              const float* plb, const uint32_t* pcnt, uint32_t* cid, float* clb,
+                              uint32_t* ccnt) {
+  const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= m) return;
+  uint32_t c = 0;
+  float lb = __int_as_float(0x7f800000);
+  for (uint32_t p = 0; p < P; ++p) {
+    const uint64_t e = v * P + p;
+    const uint32_t cp = pcnt[e];
+    for (uint32_t i = lane; i < cp; i += 32) cid[v * P * KP + c + i] = pid[e * KP + i];
+    c += cp;
+    lb = fminf(lb, plb[e]);
+  }
+  if (lane == 0) {
+    ccnt[v] = c;
+    clb[v] = lb;
+  }
+}
+
+// FFMA certificate factor: every excluded candidate's reference distance is
+// >= T / (1 + g32) * (1 - g64), T = the KP-th fp32 distance, with
+// g32 = (d + 3) u32 for the fp32 chain and g64 = (d + 1) u64 for the
+// reference's fp64 chain; rounded down generously.
+double ffma_lb_factor(uint64_t d) {
+  const double g32 = (double)(d + 3) * 0x1p-24 / (1.0 - (double)(d + 3) * 0x1p-24);
+  const double g64 = (double)(d + 1) * 0x1p-53 / (1.0 - (double)(d + 1) * 0x1p-53);
+  return (1.0 - g64) / (1.0 + g32) * (1.0 - 1e-12);
+}
+
+// Launch the FFMA filter over `sg` (ntiles query tiles in total).
+void ffma_filter(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+                 const uint32_t* qlist, const std::vector<FilterSeg>& sg, uint32_t ntiles, int kp,
+                 int by_slot, uint32_t* cid, float* clb, uint32_t* ccnt) {
+  cudaStream_t S = ctx->stream;
+  DBuf<FilterSeg> sg_d(sg.size());
+  NB_CUDA(cudaMemcpyAsync(sg_d.p, sg.data(), sg.size() * sizeof(FilterSeg), cudaMemcpyHostToDevice, S));
+  const bool v4 = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const int cap = kp + CT / (kp <= 32 ? 2 : 4);
+  const size_t smem = (size_t)2 * (QT + CT) * DK * 4 + (size_t)QT * cap * 8 + QT * 12;
+  auto go = [&](auto kern) {
+    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<ntiles, 256, smem, S>>>(x, (uint32_t)d, members, qlist, sg_d.p, (uint32_t)sg.size(),
+                                   by_slot, cid, clb, ccnt, ffma_lb_factor(d));
+  };
+  if (kp == 32) {
+    if (v4) go(k_knn_filter<32, true>); else go(k_knn_filter<32, false>);
+  } else {
+    if (v4) go(k_knn_filter<64, true>); else go(k_knn_filter<64, false>);
+  }
+  note_launch(ctx, "k_knn_filter");
+  NB_CUDA(cudaStreamSynchronize(S));
+}
+
 void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
                      const uint32_t* assign_d, uint32_t C, uint32_t k, KnnResult& R,
                      int mode) {
@@ -425,53 +554,31 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   R.edges = edges;
   R.nb.alloc(std::max<uint64_t>(edges, 1));
   R.dist.alloc(std::max<uint64_t>(edges, 1));
-  // segments / query tiles
-  std::vector<ClusterSeg> segs;
+  // whole-cluster segments (queries = candidates = the cluster's members)
+  std::vector<FilterSeg> segs;
   uint32_t tiles = 0;
   for (uint32_t r = 0; r < C; ++r) {
     const uint32_t sz = (uint32_t)(off[r + 1] - off[r]);
     if (sz < 2) continue;
-    segs.push_back(ClusterSeg{off[r], sz, tiles});
+    segs.push_back(FilterSeg{off[r], off[r], sz, sz, tiles, 0});
     tiles += (sz + QT - 1) / QT;
   }
   if (tiles == 0) {
     NB_CUDA(cudaStreamSynchronize(S));
     return;
   }
-  DBuf<ClusterSeg> segs_d(segs.size());
-  NB_CUDA(cudaMemcpyAsync(segs_d.p, segs.data(), segs.size() * sizeof(ClusterSeg),
-                          cudaMemcpyHostToDevice, S));
-  // FFMA filter certificate factor: T / (1 + g32) * (1 - g64), rounded down generously
-  const double g32 = (double)(d + 3) * 0x1p-24 / (1.0 - (double)(d + 3) * 0x1p-24);
-  const double g64 = (double)(d + 1) * 0x1p-53 / (1.0 - (double)(d + 1) * 0x1p-53);
-  const double lbf_ffma = (1.0 - g64) / (1.0 + g32) * (1.0 - 1e-12);
   int KP = k <= 24 ? 32 : 64;
   DBuf<uint32_t> cid, ccnt;
   DBuf<float> clb;  // per-row lower bound on every excluded reference distance
-  auto ffma_filter = [&](const std::vector<ClusterSeg>& sg, uint32_t ntiles, int kp) {
-    DBuf<ClusterSeg> sg_d(sg.size());
-    NB_CUDA(cudaMemcpyAsync(sg_d.p, sg.data(), sg.size() * sizeof(ClusterSeg),
-                            cudaMemcpyHostToDevice, S));
-    auto go = [&](auto kern) {
-      const size_t smem = (size_t)(QT + CT) * (DK + 1) * 4 + (size_t)QT * (kp + CT) * 8 + QT * 12;
-      NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<ntiles, 256, smem, S>>>(x, (uint32_t)d, mem.p, sg_d.p, (uint32_t)sg.size(), cid.p,
-                                     clb.p, ccnt.p, lbf_ffma);
-    };
-    if (kp == 32) go(k_knn_filter<32>); else go(k_knn_filter<64>);
-    note_launch(ctx, "k_knn_filter");
-    NB_CUDA(cudaStreamSynchronize(S));
-  };
   DBuf<uint32_t> fb(n), nfb(1);
   auto rerank = [&]() -> uint32_t {
     NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
     const unsigned rb = (unsigned)((n * 32 + 255) / 256);
-    if (KP == 32)
-      k_knn_rerank<32><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, clb.p,
-                                          ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
-    else
-      k_knn_rerank<64><<<rb, 256, 0, S>>>(x, (uint32_t)d, n, assign_d, sizes.p, k, cid.p, clb.p,
-                                          ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
+    auto go = [&](auto kern) {
+      kern<<<rb, 256, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d, sizes.p, k, 0u, cid.p, clb.p,
+                              ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
+    };
+    if (KP == 32) go(k_knn_rerank<32>); else go(k_knn_rerank<64>);
     note_launch(ctx, "k_knn_rerank");
     uint32_t nf = 0;
     NB_CUDA(cudaMemcpyAsync(&nf, nfb.p, 4, cudaMemcpyDeviceToHost, S));
@@ -497,17 +604,28 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
       NB_CUDA(cudaMemcpy(ah.data(), assign_d, n * 4, cudaMemcpyDeviceToHost));
       std::vector<uint64_t> fail_per(C, 0);
       for (uint32_t q : fbh) ++fail_per[ah[q]];
-      std::vector<ClusterSeg> sg;
+      // only the open rows are re-filtered (against their whole cluster);
+      // clusters with a handful of open rows go straight to the exhaustive pass
+      std::vector<uint64_t> qoff(C + 1, 0);
+      for (uint32_t r = 0; r < C; ++r) qoff[r + 1] = qoff[r] + (fail_per[r] >= 16 ? fail_per[r] : 0);
+      std::vector<uint32_t> qh(qoff[C]);
+      std::vector<uint64_t> fill(qoff.begin(), qoff.end() - 1);
+      std::sort(fbh.begin(), fbh.end());
+      for (uint32_t q : fbh)
+        if (fail_per[ah[q]] >= 16) qh[fill[ah[q]]++] = q;
+      std::vector<FilterSeg> sg;
       uint32_t nt = 0;
       for (uint32_t r = 0; r < C; ++r) {
         const uint64_t sz = off[r + 1] - off[r];
-        if (sz < 2 || fail_per[r] == 0) continue;
-        if (fail_per[r] * 16 < sz) continue;  // few: the exhaustive pass is cheaper
-        sg.push_back(ClusterSeg{off[r], (uint32_t)sz, nt});
-        nt += (uint32_t)((sz + QT - 1) / QT);
+        const uint64_t qn = qoff[r + 1] - qoff[r];
+        if (sz < 2 || qn == 0) continue;
+        sg.push_back(FilterSeg{off[r], qoff[r], (uint32_t)sz, (uint32_t)qn, nt, 0});
+        nt += (uint32_t)((qn + QT - 1) / QT);
       }
       if (nt) {
-        ffma_filter(sg, nt, KP);
+        DBuf<uint32_t> ql(qh.size());
+        NB_CUDA(cudaMemcpyAsync(ql.p, qh.data(), qh.size() * 4, cudaMemcpyHostToDevice, S));
+        ffma_filter(ctx, x, d, mem.p, ql.p, sg, nt, KP, 0, cid.p, clb.p, ccnt.p);
         nf = rerank();
       }
     }
@@ -516,7 +634,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
     ccnt.alloc(n);
     clb.alloc(n);
     NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
-    ffma_filter(segs, tiles, KP);
+    ffma_filter(ctx, x, d, mem.p, mem.p, segs, tiles, KP, 0, cid.p, clb.p, ccnt.p);
     nf = rerank();
   }
   // stage 3: exhaustive fp64 for whatever is still uncertified
@@ -526,8 +644,63 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
     for (uint32_t r = 0; r < C; ++r) cb[r] = off[r];
     DBuf<uint64_t> cb_d(C);
     NB_CUDA(cudaMemcpyAsync(cb_d.p, cb.data(), C * 8, cudaMemcpyHostToDevice, S));
-    k_knn_exhaustive<<<nf, 128, 0, S>>>(x, (uint32_t)d, assign_d, mem.p, cb_d.p, sizes.p, k, fb.p,
-                                        R.offsets.p, R.nb.p, R.dist.p);
+    k_knn_exhaustive<<<nf, 128, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d, mem.p, cb_d.p,
+                                        sizes.p, k, 0u, fb.p, R.offsets.p, R.nb.p, R.dist.p);
+    note_launch(ctx, "k_knn_exhaustive");
+  }
+  NB_CUDA(cudaStreamSynchronize(S));
+}
+
+// Exact global kNN (over all n points, self excluded) of the m query points
+// qlist_d[0..m): out_ids_d[v * k ..] = the k smallest (reference fp64
+// distance, id) keys of point qlist_d[v], in that order (metrics.hpp:77-91
+// exact_knn_ids before its final id sort). FFMA certified filter over the
+// whole dataset -> fp64 re-rank -> exhaustive fp64 for uncertified slots.
+void knn_global_sample(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                       const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d) {
+  cudaStream_t S = ctx->stream;
+  if (k < 1 || k > 56) fail(kParameter, "GPU exact kNN supports 1 <= k <= 56");
+  if (k >= n) fail(kParameter, "k must be < n");
+  if (m == 0) return;
+  const uint32_t KP = k <= 24 ? 32 : 64;
+  // candidates split into P partitions so that the grid covers the GPU
+  const uint32_t nt = (m + QT - 1) / QT;
+  uint32_t P = 1;
+  while (P < 16 && nt * P < 2 * (uint32_t)ctx->sm_count && n / (2 * P) >= (uint64_t)CT) P *= 2;
+  DBuf<uint32_t> pid((uint64_t)m * P * KP), pcnt((uint64_t)m * P);
+  DBuf<float> plb((uint64_t)m * P);
+  std::vector<FilterSeg> sg;
+  for (uint32_t p = 0; p < P; ++p) {
+    const uint64_t lo = n * p / P, hi = n * (p + 1) / P;
+    sg.push_back(FilterSeg{lo, 0, (uint32_t)(hi - lo), m, nt * p, p});
+  }
+  ffma_filter(ctx, x, d, nullptr, qlist_d, sg, nt * P, (int)KP, (int)P, pid.p, plb.p, pcnt.p);
+  const uint32_t KPP = P * KP;
+  DBuf<uint32_t> cid((uint64_t)m * KPP), ccnt(m), fb(m), nfb(1);
+  DBuf<float> clb(m);
+  const unsigned rb = (unsigned)(((uint64_t)m * 32 + 255) / 256);
+  k_merge_parts<<<rb, 256, 0, S>>>(m, P, KP, pid.p, plb.p, pcnt.p, cid.p, clb.p, ccnt.p);
+  note_launch(ctx, "k_merge_parts");
+  NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
+  auto go = [&](auto kern) {
+    kern<<<rb, 256, 0, S>>>(x, (uint32_t)d, (uint64_t)m, qlist_d, nullptr, nullptr, k, k, cid.p,
+                            clb.p, ccnt.p, nullptr, out_ids_d, nullptr, fb.p, nfb.p, 1.0);
+  };
+  switch (KPP) {
+    case 32: go(k_knn_rerank<32>); break;
+    case 64: go(k_knn_rerank<64>); break;
+    case 128: go(k_knn_rerank<128>); break;
+    case 256: go(k_knn_rerank<256>); break;
+    case 512: go(k_knn_rerank<512>); break;
+    default: go(k_knn_rerank<1024>); break;
+  }
+  note_launch(ctx, "k_knn_rerank");
+  uint32_t nf = 0;
+  NB_CUDA(cudaMemcpyAsync(&nf, nfb.p, 4, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  if (nf) {
+    k_knn_exhaustive<<<nf, 128, 0, S>>>(x, (uint32_t)d, n, qlist_d, nullptr, nullptr, nullptr,
+                                        nullptr, k, k, fb.p, nullptr, out_ids_d, nullptr);
     note_launch(ctx, "k_knn_exhaustive");
   }
   NB_CUDA(cudaStreamSynchronize(S));
@@ -639,9 +812,9 @@ int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     std::vector<uint64_t> cb(coff.begin(), coff.end() - 1);
     DBuf<uint64_t> cb_d(C);
     NB_CUDA(cudaMemcpyAsync(cb_d.p, cb.data(), C * 8, cudaMemcpyHostToDevice, S));
-    k_knn_exhaustive<<<(unsigned)rows.size(), 128, 0, S>>>(dd.x, (uint32_t)dd.d, a_d.p, mem.p,
-                                                          cb_d.p, sizes.p, (uint32_t)k, rows_d.p,
-                                                          off_d.p, nb2.p, nullptr);
+    k_knn_exhaustive<<<(unsigned)rows.size(), 128, 0, S>>>(dd.x, (uint32_t)dd.d, n, nullptr, a_d.p,
+                                                          mem.p, cb_d.p, sizes.p, (uint32_t)k, 0u,
+                                                          rows_d.p, off_d.p, nb2.p, nullptr);
     note_launch(ctx, "k_knn_exhaustive");
     std::vector<uint32_t> ex(off[n]);
     NB_CUDA(cudaMemcpyAsync(ex.data(), nb2.p, (size_t)off[n] * 4, cudaMemcpyDeviceToHost, S));

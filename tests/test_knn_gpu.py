@@ -67,3 +67,24 @@ def test_knn_matches_reference_goldens(port, ctx, case, mode):
     assert sha(gg.offsets) == gc["knn_offsets"]
     assert sha(gg.neighbors) == gc["knn_neighbors"]
     assert sha(gg.distances) == gc["knn_distances"]
+
+
+@pytest.mark.parametrize("d", [64, 50])
+def test_knn_multiblob_clusters_open_rows(port, ctx, d):
+    """Clusters that merge far-apart blobs: large centred norms leave many rows
+    uncertified by the fp16 tensor-core filter; those rows (only) are
+    re-filtered by the FFMA kernel (d % 4 == 0: pipelined query-list form;
+    otherwise the scalar whole-cluster form) and the result is still
+    bit-identical to the oracle."""
+    import paper_2505_15511_b200 as nb
+    from oracle import Clusters
+    x = port.gaussian_mixture(8000, d, 24, 60.0, 3)
+    a = (np.arange(len(x)) % 2).astype(np.uint32)  # every cluster spans all blobs
+    cl = Clusters(a, np.zeros(2 * d), np.bincount(a, minlength=2).astype(np.uint32), 2, d)
+    g = port.build_knn(x, cl, 15)
+    gg = _gpu_graph(nb, ctx, x, cl, 15, "exact")
+    tc_open, _ = ctx.knn_stats()
+    assert tc_open > 0
+    assert np.array_equal(gg.offsets, g.offsets)
+    assert np.array_equal(gg.neighbors, g.neighbors)
+    assert np.array_equal(gg.distances, g.distances)

@@ -36,19 +36,39 @@ __global__ void k_rmw(double2* p, uint32_t n, uint32_t per) {
     double2 v = p[r]; v.x += 1e-9; v.y -= 1e-9; p[r] = v;
   }
 }
+// double-float rows {hi.x, hi.y, lo.x, lo.y}: one RED.F32x2 onto lo
+__global__ void k_red32x2(double2* p, uint32_t n, uint32_t per) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  float* f = reinterpret_cast<float*>(p);
+  for (uint32_t i = 0; i < per; ++i) {
+    uint32_t r = hsh(t * 7919u + i) % n;
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" :: "l"(f + 4 * (uint64_t)r + 2),
+                 "f"(1e-9f), "f"(-1e-9f) : "memory");
+  }
+}
+// one RED.F64 per row (x only): the per-instruction cost reference
+__global__ void k_red1(double2* p, uint32_t n, uint32_t per) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t i = 0; i < per; ++i) {
+    uint32_t r = hsh(t * 7919u + i) % n;
+    atomicAdd(&p[r].x, 1e-9);
+  }
+}
 int main() {
   const uint32_t n = 1250000;  // 20 MB of double2
   double2* p; cudaMalloc(&p, n * 16); cudaMemset(p, 0, n * 16);
   const uint32_t blocks = 148 * 8, threads = 256, per = 1400;  // ~424M row updates
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   float ms;
-  const char* names[3] = {"2xRED.F64", "UBLKRED16", "RMW(non-atomic)"};
-  for (int v = 0; v < 3; ++v) {
+  const char* names[5] = {"2xRED.F64", "UBLKRED16", "RMW(non-atomic)", "1xRED.F32x2", "1xRED.F64"};
+  for (int v = 0; v < 5; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (v == 0) k_red<<<blocks, threads>>>(p, n, per);
       if (v == 1) k_bulk<<<blocks, threads>>>(p, n, per);
       if (v == 2) k_rmw<<<blocks, threads>>>(p, n, per);
+      if (v == 3) k_red32x2<<<blocks, threads>>>(p, n, per);
+      if (v == 4) k_red1<<<blocks, threads>>>(p, n, per);
       cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
     }
     double upd = (double)blocks * threads * per;
