@@ -127,6 +127,10 @@ typedef struct {
   double kmeans_tol;         /* < 0: auto (default_kmeans_tol) */
   int32_t approx_all_but_own;/* ApproxMode::AllButOwnCluster */
   int32_t head_only;
+  uint64_t checkpoint_every;  /* fit(): layout CSV every N epochs (0: none), optimizer.hpp:463-469 */
+  const char* checkpoint_prefix;   /* "<prefix>.epoch<N>.csv" (NULL or "": none) */
+  const char* const* checkpoint_ids;    /* row ids (NULL: "0".."n-1", the raw loader's) */
+  const char* const* checkpoint_labels; /* label column (NULL: none) */
   /* engine-only */
   int32_t sgd_mode;          /* nomad_b200_sgd_mode */
   int32_t knn_mode;          /* nomad_b200_knn_mode */
@@ -275,6 +279,24 @@ int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                        const double* init_layout, double* layout_out,
                        nomad_b200_clusters* clusters_out,
                        nomad_b200_graph* graph_out, double* epoch_loss_out);
+
+/* ----------------------------------------------------------- data I/O */
+/* dataset.hpp:122-173 load_vectors_raw: little-endian f32 row-major file;
+ * rows or dims may be 0 (derived from the file size; both given = strict).
+ * Same checks and messages (Io / Parameter / Dimension / Validation: first
+ * non-finite value in row-major order). out == NULL: shape query only.
+ * out_location DEVICE streams the file through pinned buffers into device
+ * memory (ctx required; the finiteness scan runs on the GPU). */
+int32_t nomad_b200_load_vectors_raw(nomad_b200_ctx* ctx, const char* path, uint64_t rows,
+                                    uint64_t dims, float* out, int32_t out_location,
+                                    uint64_t* rows_out, uint64_t* dims_out);
+/* dataset.hpp:223-250 save_layout: `id,x,y[,label]`, %.17g, byte-identical
+ * to the reference (formatted on all host cores). layout: host rows x 2.
+ * ids NULL: "0".."rows-1"; labels NULL: no label column. */
+int32_t nomad_b200_save_layout_csv(const char* path, const double* layout, uint64_t rows,
+                                   const char* const* ids, const char* const* labels);
+/* Raw little-endian f64 rows x 2 (16 bytes per row, no header). */
+int32_t nomad_b200_save_layout_f64(const char* path, const double* layout, uint64_t rows);
 
 /* ------------------------------------------- helpers (multi-GPU, data) */
 /* Host-only: shard_clusters' LPT plan (optimizer.hpp:106-144) for `workers`

@@ -141,6 +141,10 @@ class Oracle:
             self._tri = fn("random_triplet_accuracy", C.c_int,
                            [f32p, C.c_uint64, C.c_uint64, f64p, C.c_uint64, C.c_uint64, f64p,
                             f64p])
+            self._save = fn("save_layout", C.c_int, [C.c_char_p, f64p, C.c_uint64, C.c_void_p,
+                                                     C.c_void_p])
+            self._loadraw = fn("load_vectors_raw", C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64,
+                                                             C.c_void_p, u64p, u64p])
             self._qe = None
         else:
             self._fit = None
@@ -320,6 +324,31 @@ class Oracle:
         self._check(self._np(_p(x, C.c_float), x.shape[0], x.shape[1], _p(lay, C.c_double), k,
                              sample, seed, _p(v, C.c_double), _p(se, C.c_double)))
         return float(v[0]), float(se[0])
+
+    def save_layout(self, layout, path, ids=None, labels=None):
+        """dataset.hpp:223-250 (reference library only)."""
+        lay = np.ascontiguousarray(layout, np.float64)
+        keep = []
+
+        def arr(xs):
+            if xs is None:
+                return None
+            bs = [str(v).encode() for v in xs]
+            a = (C.c_char_p * len(bs))(*bs)
+            keep.append((a, bs))
+            return C.cast(a, C.c_void_p)
+        self._check(self._save(path.encode(), _p(lay, C.c_double), lay.shape[0], arr(ids),
+                               arr(labels)))
+
+    def load_vectors_raw(self, path, rows=0, dims=0):
+        """dataset.hpp:122-173 (reference library only) -> f32 array."""
+        r, d = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        self._check(self._loadraw(path.encode(), rows, dims, None, _p(r, C.c_uint64),
+                                  _p(d, C.c_uint64)))
+        out = np.empty((int(r[0]), int(d[0])), np.float32)
+        self._check(self._loadraw(path.encode(), rows, dims, out.ctypes.data, _p(r, C.c_uint64),
+                                  _p(d, C.c_uint64)))
+        return out
 
     def random_triplet_accuracy(self, x, layout, count=100000, seed=0):
         x = np.ascontiguousarray(x, np.float32)

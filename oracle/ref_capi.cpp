@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -398,6 +399,38 @@ int ref_random_triplet_accuracy(const float* data, uint64_t n, uint64_t d,
     auto r = nomad::random_triplet_accuracy(make_ds(data, n, d), l, count, seed);
     *value = r.value;
     *std_error = r.std_error;
+    return 0;
+  } catch (const nomad::Error& e) { return fail_code(e); }
+}
+
+// dataset.hpp:223-250 save_layout (ids NULL: "0".."n-1"; labels NULL: none).
+int ref_save_layout(const char* path, const double* layout, uint64_t n, const char* const* ids,
+                    const char* const* labels) {
+  try {
+    nomad::LayoutMatrix l;
+    l.rows = n;
+    l.positions.assign(layout, layout + 2 * n);
+    std::vector<std::string> iv(n), lv;
+    for (uint64_t i = 0; i < n; ++i) iv[i] = ids ? std::string(ids[i]) : std::to_string(i);
+    if (labels)
+      for (uint64_t i = 0; i < n; ++i) lv.emplace_back(labels[i]);
+    nomad::save_layout(l, iv, lv, path);
+    return 0;
+  } catch (const nomad::Error& e) { return fail_code(e); }
+}
+
+// dataset.hpp:122-173 load_vectors_raw (rows / dims 0 = not given); out may
+// be NULL (shape only).
+int ref_load_vectors_raw(const char* path, uint64_t rows, uint64_t dims, float* out,
+                         uint64_t* rows_out, uint64_t* dims_out) {
+  try {
+    std::optional<std::size_t> r, d;
+    if (rows) r = rows;
+    if (dims) d = dims;
+    auto ds = nomad::load_vectors_raw(path, r, d);
+    *rows_out = ds.rows;
+    *dims_out = ds.dims;
+    if (out) std::memcpy(out, ds.data.data(), ds.data.size() * 4);
     return 0;
   } catch (const nomad::Error& e) { return fail_code(e); }
 }

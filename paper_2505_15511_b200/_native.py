@@ -52,7 +52,9 @@ class TrainConfigC(C.Structure):
                 ("workers", C.c_uint64), ("n_clusters", C.c_uint64), ("seed", C.c_uint64),
                 ("lr0", C.c_double), ("kmeans_max_iters", C.c_uint64),
                 ("kmeans_tol", C.c_double), ("approx_all_but_own", C.c_int32),
-                ("head_only", C.c_int32), ("sgd_mode", C.c_int32), ("knn_mode", C.c_int32),
+                ("head_only", C.c_int32), ("checkpoint_every", C.c_uint64),
+                ("checkpoint_prefix", C.c_char_p), ("checkpoint_ids", C.c_void_p),
+                ("checkpoint_labels", C.c_void_p), ("sgd_mode", C.c_int32), ("knn_mode", C.c_int32),
                 ("hogwild_cap", C.c_uint32), ("verbose", C.c_int32)]
 
 
@@ -108,6 +110,11 @@ _SIGS = {
     "nomad_b200_debug_tc_gemm": (C.c_int32, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint32,
                                              C.c_uint32, _vp]),
     "nomad_b200_nccl_unique_id": (C.c_int32, [_vp]),
+    "nomad_b200_load_vectors_raw": (C.c_int32, [_vp, C.c_char_p, C.c_uint64, C.c_uint64, _vp,
+                                                C.c_int32, C.POINTER(C.c_uint64),
+                                                C.POINTER(C.c_uint64)]),
+    "nomad_b200_save_layout_csv": (C.c_int32, [C.c_char_p, _vp, C.c_uint64, _vp, _vp]),
+    "nomad_b200_save_layout_f64": (C.c_int32, [C.c_char_p, _vp, C.c_uint64]),
     "nomad_b200_generate_mixture": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
                                                 C.c_double, C.c_uint64, _vp]),
 }

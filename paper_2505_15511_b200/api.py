@@ -108,6 +108,8 @@ class TrainConfig:
     sgd_mode: str = "replay"        # "replay" (bit-exact) | "hogwild" (throughput)
     knn_mode: str = "exact"         # "exact" | "bf16"
     hogwild_cap: int = 0
+    checkpoint_every: int = 0       # fit(): layout CSV every N epochs (optimizer.hpp:463-469)
+    checkpoint_prefix: str = ""     # "<prefix>.epoch<N>.csv"
 
     def validate(self) -> None:  # optimizer.hpp:63-71
         if self.workers < 1:
@@ -137,6 +139,7 @@ class TrainConfig:
             self.workers, self.n_clusters, self.seed & (2**64 - 1), float(self.lr0),
             self.kmeans_max_iters, float(self.kmeans_tol),
             1 if self.approx == "non-own-cluster" else 0, 1 if self.head_only else 0,
+            self.checkpoint_every, self.checkpoint_prefix.encode() or None, None, None,
             {"replay": N.SGD_REPLAY, "hogwild": N.SGD_HOGWILD}[self.sgd_mode],
             {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[self.knn_mode],
             self.hogwild_cap, 1 if self.verbose else 0)
@@ -284,6 +287,50 @@ def knn_recall(data, clusters: ClusterAssignment, graph: KnnGraph, sample: int =
     check(lib().nomad_b200_knn_recall(_ctx(ctx).h, C.byref(dv), C.byref(cv), C.byref(gv), sample,
                                       seed, C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------- data I/O
+
+def load_vectors_raw(path: str, rows: int = 0, dims: int = 0, device: bool = False,
+                     ctx: Optional[Context] = None):
+    """dataset.hpp:122-173 (raw little-endian f32). device=True streams the file
+    into a CUDA float32 tensor through pinned buffers; else a numpy array."""
+    r, d = C.c_uint64(), C.c_uint64()
+    h = _ctx(ctx).h if device else None
+    check(lib().nomad_b200_load_vectors_raw(h, path.encode(), rows, dims, None, N.HOST,
+                                            C.byref(r), C.byref(d)))
+    if device:
+        import torch
+        out = torch.empty((r.value, d.value), dtype=torch.float32, device=f"cuda:{_ctx(ctx).device}")
+        check(lib().nomad_b200_load_vectors_raw(h, path.encode(), rows, dims, out.data_ptr(),
+                                                N.DEVICE, None, None))
+        return out
+    out = np.empty((r.value, d.value), np.float32)
+    check(lib().nomad_b200_load_vectors_raw(None, path.encode(), rows, dims, out.ctypes.data,
+                                            N.HOST, None, None))
+    return out
+
+
+def _str_array(xs):
+    if xs is None:
+        return None, None
+    bs = [str(v).encode() for v in xs]
+    arr = (C.c_char_p * len(bs))(*bs)
+    return C.cast(arr, C.c_void_p), (arr, bs)
+
+
+def save_layout(layout, path: str, ids=None, labels=None) -> None:
+    """dataset.hpp:223-250: `id,x,y[,label]` CSV with %.17g (byte-identical)."""
+    lay = np.ascontiguousarray(layout, np.float64).reshape(-1, 2)
+    ip, ik = _str_array(ids)
+    lp, lk = _str_array(labels)
+    check(lib().nomad_b200_save_layout_csv(path.encode(), lay.ctypes.data, lay.shape[0], ip, lp))
+
+
+def save_layout_f64(layout, path: str) -> None:
+    """Raw little-endian f64 rows x 2."""
+    lay = np.ascontiguousarray(layout, np.float64).reshape(-1, 2)
+    check(lib().nomad_b200_save_layout_f64(path.encode(), lay.ctypes.data, lay.shape[0]))
 
 
 # ---------------------------------------------------------------- quality metrics

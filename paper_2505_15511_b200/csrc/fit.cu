@@ -76,9 +76,26 @@ extern "C" int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_
     chk(nomad_b200_trainer_create(ctx, &g, &cl, init.p, NOMAD_B200_DEVICE, cfg, 0, 1, nullptr,
                                   &tr));
     int32_t rc = 0;
-    if (cfg->epochs > 0) rc = nomad_b200_trainer_run(tr, cfg->epochs, epoch_loss_out);
+    // epochs in segments ending at the checkpoint epochs (optimizer.hpp:463-469)
+    const bool ckpt = cfg->checkpoint_every > 0 && cfg->checkpoint_prefix && *cfg->checkpoint_prefix;
+    std::string msg;
+    for (uint64_t e = 0; rc == 0 && e < cfg->epochs;) {
+      const uint64_t seg = ckpt ? std::min(cfg->checkpoint_every - e % cfg->checkpoint_every,
+                                           cfg->epochs - e)
+                                : cfg->epochs - e;
+      rc = nomad_b200_trainer_run(tr, seg, epoch_loss_out ? epoch_loss_out + e : nullptr);
+      e += seg;
+      if (rc == 0 && ckpt && e % cfg->checkpoint_every == 0) {
+        rc = nomad_b200_trainer_layout(tr, layout_out, NOMAD_B200_HOST);
+        if (rc == 0) {
+          const std::string path = std::string(cfg->checkpoint_prefix) + ".epoch" + std::to_string(e) + ".csv";
+          rc = nomad_b200_save_layout_csv(path.c_str(), layout_out, n, cfg->checkpoint_ids,
+                                          cfg->checkpoint_labels);
+        }
+      }
+    }
     if (rc == 0) rc = nomad_b200_trainer_layout(tr, layout_out, NOMAD_B200_HOST);
-    std::string msg = rc ? nomad_b200_last_error() : "";
+    if (rc) msg = nomad_b200_last_error();
     nomad_b200_trainer_destroy(tr);
     if (rc) throw Error(static_cast<Kind>(rc - 1), msg);
 

@@ -10,7 +10,8 @@
 // butterfly-reduced inside the group, which leaves bitwise-identical values
 // on every lane. The gradient is the reference's (objective.hpp:178-237)
 // with algebraic reuse: pull = 2 w q bg / (q + bg), and the mean push folded
-// into one sum. Updates are fp64 atomic scatter-adds (RED.ADD.F64).
+// into one sum; all arithmetic in fp64. Updates are atomic scatter-adds onto
+// double-float position rows (one RED.F32x2 per row, see ld_row/add_row).
 //
 // Scheduling: blocks pull fixed-size chunks of draws from a global counter;
 // chunks are numbered worker-major, so at any moment the GPU works on about
@@ -42,8 +43,15 @@
 #ifndef HOG_PLAIN
 #define HOG_PLAIN 0       // 1: unsynchronised read-modify-write rows (the reference's Hogwild stores)
 #endif
+#ifndef HOG_DF
+#define HOG_DF 1          // 1: double-float rows {hi, lo}, one RED.F32x2 per row update
+#endif
 #ifndef HOG_MF32
 #define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
+#endif
+
+#if HOG_DF && (HOG_CAS || HOG_PLAIN)
+#error "HOG_CAS / HOG_PLAIN operate on f64 rows: build them with -DHOG_DF=0"
 #endif
 
 namespace nb {
@@ -83,6 +91,31 @@ __device__ __forceinline__ void cas_add_finish(double2* p, double2 old, double2 
     old = seen;
     seen = cas128(p, old, make_double2(old.x + ax, old.y + ay));
   }
+}
+
+// Position rows. HOG_DF: 16-byte double-float rows {hi.x, hi.y, lo.x, lo.y},
+// value = hi + lo (exact in fp64), updates are one RED.F32x2 onto lo (the
+// per-request cost of RED.F32x2 equals one RED.F64, tools/micro/red_bench.cu,
+// so a row update costs half); the means pass renormalises every epoch.
+// Otherwise f64 rows and two RED.F64.
+__device__ __forceinline__ double2 ld_row(const double2* pos, uint32_t i) {
+#if HOG_DF
+  const float4 r = reinterpret_cast<const float4*>(pos)[i];
+  return make_double2((double)r.x + (double)r.z, (double)r.y + (double)r.w);
+#else
+  return pos[i];
+#endif
+}
+__device__ __forceinline__ void add_row(double2* pos, uint32_t i, double ax, double ay) {
+#if HOG_DF
+  float* lo = reinterpret_cast<float*>(pos + i) + 2;
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(lo), "f"(__double2float_rn(ax)),
+               "f"(__double2float_rn(ay))
+               : "memory");
+#else
+  atomicAdd(&pos[i].x, ax);
+  atomicAdd(&pos[i].y, ay);
+#endif
 }
 
 template <int NPL>
@@ -209,12 +242,12 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       const uint32_t cnt = act ? (P.ncnt ? P.ncnt[head] : k) : 0u;
       uint32_t nb[NPL];
       load_ids<NPL>(P.ell + (size_t)head * P.kpad + NPL * gl, nb);
-      const double2 h = P.pos[head];
+      const double2 h = ld_row(P.pos, head);
       double2 pn[NPL], pt[TPL];
 #pragma unroll
-      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? P.pos[nb[i]] : h;
+      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row(P.pos, nb[i]) : h;
 #pragma unroll
-      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? P.pos[tl[m]] : h;
+      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row(P.pos, tl[m]) : h;
 
       // ---- mean field over this lane's cells: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
       double s1 = 0.0, s2x = 0.0, s2y = 0.0;
@@ -290,8 +323,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #elif HOG_PLAIN
             P.pos[nb[i]] = make_double2(pn[i].x + a * dx, pn[i].y + a * dy);
 #else
-            atomicAdd(&P.pos[nb[i]].x, a * dx);
-            atomicAdd(&P.pos[nb[i]].y, a * dy);
+            add_row(P.pos, nb[i], a * dx, a * dy);
 #endif
           }
         }
@@ -313,8 +345,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #elif HOG_PLAIN
             P.pos[tl[m]] = make_double2(pt[m].x + a * dx, pt[m].y + a * dy);
 #else
-            atomicAdd(&P.pos[tl[m]].x, a * dx);
-            atomicAdd(&P.pos[tl[m]].y, a * dy);
+            add_row(P.pos, tl[m], a * dx, a * dy);
 #endif
           }
         }
@@ -356,8 +387,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       }
 #else
       if (act && gl == 0) {
-        atomicAdd(&P.pos[head].x, -st * gx);
-        atomicAdd(&P.pos[head].y, -st * gy);
+        add_row(P.pos, head, -st * gx, -st * gy);
         edge_acc += (double)(cnt + s);
       }
 #endif
@@ -400,6 +430,7 @@ uint32_t hogwild_group_size(uint32_t kpad, uint32_t s) {
   return (kpad <= 16 && s <= 7) ? HOG_G16 : 8;
 }
 uint32_t hogwild_chunk_rounds() { return HOG_ROUNDS; }
+bool hogwild_double_float() { return HOG_DF && !HOG_CAS && !HOG_PLAIN; }
 
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st) {
   hog_dispatch(P, P.kpad, P.s, nblocks, smem, st, nullptr);

@@ -167,7 +167,11 @@ __global__ void k_means_exact(const double2* pos, const LocalCluster* lc, uint32
 
 // Throughput: chunked tree reduction into per-cluster sums (atomics), fused
 // with the divergence scan of every position (optimizer.hpp:220-221).
-__global__ void k_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl,
+// DF: positions are double-float rows {hi.x, hi.y, lo.x, lo.y} (the
+// throughput kernel's atomic format); each row is read as hi + lo and
+// renormalised in place (hi = fl32(p), lo = fl32(p - hi)).
+template <bool DF>
+__global__ void k_means_chunk(double2* pos, const LocalCluster* lc, uint32_t ncl,
                               uint32_t chunk, const uint32_t* chunk_off, double* sums,
                               unsigned long long* diverge, unsigned long long tag) {
   __shared__ double red[8];
@@ -179,7 +183,16 @@ __global__ void k_means_chunk(const double2* pos, const LocalCluster* lc, uint32
   const uint32_t b1 = min(b0 + chunk, L.start + L.count);
   double sx = 0.0, sy = 0.0;
   for (uint32_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    const double2 v = pos[i];
+    double2 v;
+    if constexpr (DF) {
+      float4* r = reinterpret_cast<float4*>(pos) + i;
+      const float4 f = *r;
+      v = make_double2((double)f.x + (double)f.z, (double)f.y + (double)f.w);
+      const float hx = __double2float_rn(v.x), hy = __double2float_rn(v.y);
+      *r = make_float4(hx, hy, __double2float_rn(v.x - (double)hx), __double2float_rn(v.y - (double)hy));
+    } else {
+      v = pos[i];
+    }
     if (diverged(v.x, v.y)) atomicMin(diverge, (tag << 32) | (unsigned long long)i);
     sx += v.x;
     sy += v.y;
@@ -189,6 +202,21 @@ __global__ void k_means_chunk(const double2* pos, const LocalCluster* lc, uint32
   if (threadIdx.x == 0) {
     atomicAdd(&sums[2 * c], sx);
     atomicAdd(&sums[2 * c + 1], sy);
+  }
+}
+
+// In-place format change of the position rows: f64 (x, y) <-> double-float.
+__global__ void k_pos_df(double2* pos, uint32_t n, int to_df) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (to_df) {
+    const double2 v = pos[i];
+    const float hx = __double2float_rn(v.x), hy = __double2float_rn(v.y);
+    reinterpret_cast<float4*>(pos)[i] =
+        make_float4(hx, hy, __double2float_rn(v.x - (double)hx), __double2float_rn(v.y - (double)hy));
+  } else {
+    const float4 f = reinterpret_cast<const float4*>(pos)[i];
+    pos[i] = make_double2((double)f.x + (double)f.z, (double)f.y + (double)f.w);
   }
 }
 
@@ -262,10 +290,17 @@ void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl
   k_means_exact<<<blocks_for(2 * ncl, 64), 64, 0, st>>>(pos, lc, ncl, slot);
 }
 
-void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
+void launch_means_chunk(double2* pos, bool df, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
                         const uint32_t* chunk_off, uint32_t nchunks, double* sums,
                         unsigned long long* diverge, unsigned long long tag, cudaStream_t st) {
-  k_means_chunk<<<nchunks, 256, 0, st>>>(pos, lc, ncl, chunk, chunk_off, sums, diverge, tag);
+  if (df)
+    k_means_chunk<true><<<nchunks, 256, 0, st>>>(pos, lc, ncl, chunk, chunk_off, sums, diverge, tag);
+  else
+    k_means_chunk<false><<<nchunks, 256, 0, st>>>(pos, lc, ncl, chunk, chunk_off, sums, diverge, tag);
+}
+
+void launch_pos_df(double2* pos, uint32_t n, bool to_df, cudaStream_t st) {
+  if (n) k_pos_df<<<blocks_for(n, 256), 256, 0, st>>>(pos, n, to_df ? 1 : 0);
 }
 
 void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, double* slot,

@@ -30,7 +30,7 @@ struct LocalCluster {
 };
 
 struct SgdParams {
-  double2* pos;                 // local positions (f64 x, y)
+  double2* pos;                 // local positions (f64 x, y; hogwild: double-float rows)
   const uint32_t* ell;          // local ids, kpad per row
   const uint8_t* ncnt;          // neighbour count per row (nullptr: all == k)
   const double* wtab;           // (k+1) x k inverse-rank weights, row = count
@@ -74,9 +74,13 @@ uint32_t hogwild_group_size(uint32_t kpad, uint32_t s);
 uint32_t hogwild_chunk_rounds();
 void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,
                         cudaStream_t st);
-void launch_means_chunk(const double2* pos, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
+void launch_means_chunk(double2* pos, bool df, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,
                         const uint32_t* chunk_off, uint32_t nchunks, double* sums,
                         unsigned long long* diverge, unsigned long long tag, cudaStream_t st);
+// f64 rows <-> double-float rows {hi.x, hi.y, lo.x, lo.y}, in place.
+void launch_pos_df(double2* pos, uint32_t n, bool to_df, cudaStream_t st);
+// true when the throughput kernel keeps positions as double-float rows
+bool hogwild_double_float();
 void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, double* slot,
                            cudaStream_t st);
 void launch_means_unpack(const double* recv, const uint32_t* slot_gid, uint32_t nslots,

@@ -399,6 +399,15 @@ struct nomad_b200_trainer {
   }
 
   unsigned long long div_tag = 0;  // run-relative epoch tag of divergence keys (hogwild)
+  // The throughput kernel's position rows are double-float while a run is in
+  // progress (hogwild_double_float()); outside run() they are f64 again.
+  bool pos_is_df = false;
+  void pos_format(bool df) {
+    if (df == pos_is_df || !hogwild_double_float()) return;
+    launch_pos_df(pos.p, (uint32_t)orig_of.size(), df, st());
+    launched("k_pos_df");
+    pos_is_df = df;
+  }
 
   void compute_means_and_exchange() {
     cudaStream_t S = st();
@@ -408,8 +417,8 @@ struct nomad_b200_trainer {
         launch_means_exact(pos.p, lcl_d.p, ncl, slot.p, S);
         launched("k_means_exact");
       } else {
-        launch_means_chunk(pos.p, lcl_d.p, ncl, chunk, chunk_off.p, nchunks, sums.p, diverge.p,
-                           div_tag, S);
+        launch_means_chunk(pos.p, pos_is_df, lcl_d.p, ncl, chunk, chunk_off.p, nchunks, sums.p,
+                           diverge.p, div_tag, S);
         launched("k_means_chunk");
         launch_means_finalize(sums.p, lcl_d.p, ncl, slot.p, S);
         launched("k_means_finalize");
@@ -573,6 +582,7 @@ struct nomad_b200_trainer {
     std::vector<cudaEvent_t> evs(3 * E);
     for (auto& x : evs) NB_CUDA(cudaEventCreate(&x));
     const uint64_t e_first = epochs_done;
+    pos_format(true);
     for (uint64_t it = 0; it < E; ++it) {
       const uint64_t e = epochs_done;
       const double lr = lr0 * (1.0 - static_cast<double>(e) / static_cast<double>(cfg.epochs));
@@ -597,6 +607,7 @@ struct nomad_b200_trainer {
       ++epochs_done;
     }
     div_tag = 0;
+    pos_format(false);
     std::vector<double> lh(E * L);
     std::vector<unsigned long long> eh(E * L);
     NB_CUDA(cudaMemcpyAsync(lh.data(), lossb.p, E * L * 8, cudaMemcpyDeviceToHost, S));
@@ -699,6 +710,7 @@ struct nomad_b200_trainer {
         NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
         NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
         NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
+        pos_format(true);
         NB_CUDA(cudaEventRecord(ev[0], S));
         if (hog_blocks) {
           launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
@@ -707,6 +719,7 @@ struct nomad_b200_trainer {
         NB_CUDA(cudaEventRecord(ev[1], S));
       }
       compute_means_and_exchange();
+      pos_format(false);
       NB_CUDA(cudaEventRecord(ev[2], S));
       // per-worker loss sums -> epoch mean (optimizer.hpp:444-451)
       const double* lsrc = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? wloss.p : loss_acc.p;

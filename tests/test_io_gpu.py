@@ -1,0 +1,51 @@
+"""Device-side data I/O: the raw-f32 loader streaming into device memory
+(dataset.hpp:122-173, GPU finiteness scan) and fit() checkpoints
+(optimizer.hpp:463-469: `<prefix>.epoch<N>.csv` every N epochs)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_load_raw_to_device(ref, ctx, tmp_path):
+    import paper_2505_15511_b200 as nb
+    x = np.random.default_rng(2).normal(size=(20000, 300)).astype(np.float32)  # > 1 chunk
+    p = str(tmp_path / "x.f32")
+    x.tofile(p)
+    t = nb.load_vectors_raw(p, 0, 300, device=True, ctx=ctx)
+    assert t.is_cuda and tuple(t.shape) == (20000, 300)
+    assert np.array_equal(t.cpu().numpy().view(np.uint32), x.view(np.uint32))
+    x[12345, 17] = np.inf
+    x[19999, 0] = np.nan
+    x.tofile(p)
+    with pytest.raises(nb.NomadError) as e:
+        nb.load_vectors_raw(p, 20000, 300, device=True, ctx=ctx)
+    from oracle import OracleError
+    with pytest.raises(OracleError) as r:
+        ref.load_vectors_raw(p, 20000, 300)
+    assert e.value.kind == r.value.kind == "Validation"
+    assert e.value.message == r.value.msg
+
+
+def test_fit_checkpoints(port, ctx, tmp_path):
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(1500, 16, 4, 10.0, 3)
+    prefix = str(tmp_path / "run")
+    cfg = nb.TrainConfig(epochs=5, workers=2, n_clusters=4, seed=3, checkpoint_every=2,
+                         checkpoint_prefix=prefix)
+    y = nb.fit(x, cfg, ctx=ctx)
+    assert sorted(os.listdir(tmp_path)) == ["run.epoch2.csv", "run.epoch4.csv"]
+    # epoch-4 checkpoint = the replay trajectory after 4 of the 5 epochs
+    cfg4 = nb.TrainConfig(epochs=5, workers=2, n_clusters=4, seed=3)
+    c = nb.kmeans_em_default_tol(x, nb.lsh_init(x, 4, 3, ctx=ctx), 100, ctx=ctx)
+    g = nb.build_knn(x, c, 15, ctx=ctx)
+    tr = nb.Trainer(g, c, nb.pca_init(x, 3, ctx=ctx), cfg4, ctx=ctx)
+    tr.run(4)
+    ref_csv = str(tmp_path / "direct.csv")
+    nb.save_layout(tr.layout(), ref_csv)
+    tr.run(1)
+    assert np.array_equal(tr.layout(), y)
+    tr.close()
+    assert open(prefix + ".epoch4.csv", "rb").read() == open(ref_csv, "rb").read()
