@@ -339,6 +339,9 @@ def main():
                           if args.graph == "knn" else
                           "random within-cluster k-regular graph, clusters = mixture components"),
                 "index": index,
+                "positions": ("double-float rows (hi + lo f32, ~48-bit significand), "
+                              "fp64 gradient arithmetic, one RED.F32x2 per row update"
+                              if args.sgd_mode == "hogwild" else "f64 rows"),
                 "init": "N(0,1) layout", "parallelism": f"cluster-sharded dp{world}",
                 "l2": "inputs larger than L2 (positions 16n B + ELL 64n B > 126 MB)",
                 "setup_s": round(setup_s, 2), "final_loss": float(losses[-1])},

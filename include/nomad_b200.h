@@ -259,6 +259,12 @@ int32_t nomad_b200_trainer_set_layout(nomad_b200_trainer* tr, const double* layo
  * epoch run so far: the SGD kernel, and the means + all-gather step. */
 int32_t nomad_b200_trainer_timing(nomad_b200_trainer* tr, double* sgd_ms,
                                   double* means_ms, uint64_t* epochs);
+/* Continue the epoch schedule at `epoch` (resume: trainer_set_layout with a
+ * checkpoint written after `epoch` epochs, then seek). Throughput mode: any
+ * epoch (Philox draws are keyed by epoch); replay mode: forward only, the
+ * workers' mt19937_64 streams are advanced past the skipped draws, so the
+ * resumed run is bit-identical to an uninterrupted one. */
+int32_t nomad_b200_trainer_seek(nomad_b200_trainer* tr, uint64_t epoch);
 /* Epochs completed and edge-updates applied (sum over heads of |N(h)|+s). */
 int32_t nomad_b200_trainer_progress(nomad_b200_trainer* tr,
                                     uint64_t* epochs_done,

@@ -14,9 +14,14 @@
 //   build_knn           knn.hpp:65-66                 nomad::b200::build_knn
 //   pca_init            pca.hpp:79                    nomad::b200::pca_init
 //   fit                 optimizer.hpp:327-328         nomad::b200::fit
+//   neighborhood_preservation metrics.hpp:113         nomad::b200::neighborhood_preservation
+//   random_triplet_accuracy   metrics.hpp:205         nomad::b200::random_triplet_accuracy
+//   load_vectors_raw    dataset.hpp:122-125           nomad::b200::load_vectors_raw
+//   save_layout         dataset.hpp:223-226           nomad::b200::save_layout
 #pragma once
 
 #include <cstdint>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -94,6 +99,8 @@ inline nomad_b200_train_config cfg(const TrainConfig& c) {
   o.kmeans_tol = c.kmeans_tol;
   o.approx_all_but_own = c.approx == ApproxMode::AllButOwnCluster ? 1 : 0;
   o.head_only = c.head_only ? 1 : 0;
+  o.checkpoint_every = c.checkpoint_every;
+  o.checkpoint_prefix = c.checkpoint_prefix.c_str();  // valid while c lives
   o.verbose = c.verbose ? 1 : 0;
   o.sgd_mode = options().sgd_mode;
   o.knn_mode = options().knn_mode;
@@ -163,7 +170,7 @@ inline KnnGraph build_knn(const VectorDataset& data, const ClusterAssignment& cl
   return g;
 }
 
-/// pca.hpp:79-218 (GPU; tolerance parity)
+/// pca.hpp:79-218 (GPU; bit-identical)
 inline LayoutMatrix pca_init(const VectorDataset& data, std::uint64_t seed = 0) {
   LayoutMatrix l = LayoutMatrix::zeros(data.rows);
   const auto v = detail::view(data);
@@ -199,7 +206,13 @@ inline LayoutMatrix fit(const VectorDataset& data, const TrainConfig& config,
   auto cv = detail::cview(ca, n);
   nomad_b200_graph gv{n, config.k, g.offsets.data(), g.neighbors.data(), g.distances.data(),
                       NOMAD_B200_HOST};
-  const auto c = detail::cfg(config);
+  auto c = detail::cfg(config);
+  // checkpoint rows carry the dataset's ids / labels, as save_layout does
+  std::vector<const char*> idp, lbp;
+  for (const auto& s : data.ids) idp.push_back(s.c_str());
+  for (const auto& s : data.labels) lbp.push_back(s.c_str());
+  c.checkpoint_ids = idp.size() == n ? idp.data() : nullptr;
+  c.checkpoint_labels = lbp.size() == n ? lbp.data() : nullptr;
   detail::check(nomad_b200_fit(detail::ctx(), &v, &c, pca.positions.data(),
                                out.positions.data(), &cv, &gv, losses.data()));
   out.epoch = config.epochs;
@@ -225,6 +238,70 @@ inline LayoutMatrix fit(const VectorDataset& data, const TrainConfig& config,
     report->epoch_mean_loss.assign(losses.begin(), losses.begin() + config.epochs);
   }
   return out;
+}
+
+/// metrics.hpp:113-168 on the GPU (bit-identical value and std_error; k <= 56)
+inline MetricReport neighborhood_preservation(const VectorDataset& high, const LayoutMatrix& low,
+                                              std::size_t k, std::size_t sample = 0,
+                                              std::uint64_t seed = 0) {
+  if (low.rows != high.rows) fail(ErrorKind::Parameter, "vector and layout row counts differ");
+  MetricReport r;
+  r.metric = "np";
+  r.param = k;
+  r.sample = (sample == 0 || sample >= high.rows) ? 0 : sample;
+  r.seed = seed;
+  const auto v = detail::view(high);
+  detail::check(nomad_b200_neighborhood_preservation(detail::ctx(), &v, low.positions.data(),
+                                                     NOMAD_B200_HOST, k, sample, seed, &r.value,
+                                                     &r.std_error));
+  return r;
+}
+
+/// metrics.hpp:205-243 on the GPU (bit-identical)
+inline MetricReport random_triplet_accuracy(const VectorDataset& high, const LayoutMatrix& low,
+                                            std::size_t n_triplets, std::uint64_t seed = 0) {
+  if (low.rows != high.rows) fail(ErrorKind::Parameter, "vector and layout row counts differ");
+  MetricReport r;
+  r.metric = "triplet";
+  r.param = n_triplets;
+  r.seed = seed;
+  const auto v = detail::view(high);
+  detail::check(nomad_b200_random_triplet_accuracy(detail::ctx(), &v, low.positions.data(),
+                                                   NOMAD_B200_HOST, n_triplets, seed, &r.value,
+                                                   &r.std_error));
+  return r;
+}
+
+/// dataset.hpp:122-173 (host result; default ids)
+inline VectorDataset load_vectors_raw(const std::string& path, std::optional<std::size_t> rows,
+                                      std::optional<std::size_t> dims) {
+  std::uint64_t n = 0, d = 0;
+  detail::check(nomad_b200_load_vectors_raw(nullptr, path.c_str(), rows.value_or(0),
+                                            dims.value_or(0), nullptr, NOMAD_B200_HOST, &n, &d));
+  VectorDataset ds;
+  ds.rows = n;
+  ds.dims = d;
+  ds.data.resize(n * d);
+  detail::check(nomad_b200_load_vectors_raw(nullptr, path.c_str(), n, d, ds.data.data(),
+                                            NOMAD_B200_HOST, nullptr, nullptr));
+  ds.ids.resize(n);
+  for (std::size_t i = 0; i < n; ++i) ds.ids[i] = std::to_string(i);
+  return ds;
+}
+
+/// dataset.hpp:223-250 (byte-identical CSV, formatted on all host cores)
+inline void save_layout(const LayoutMatrix& layout, const std::vector<std::string>& ids,
+                        const std::vector<std::string>& labels, const std::string& path) {
+  if (ids.size() != layout.rows)
+    fail(ErrorKind::Parameter, "ids length " + std::to_string(ids.size()) + " != layout rows " +
+                                   std::to_string(layout.rows));
+  if (!labels.empty() && labels.size() != layout.rows)
+    fail(ErrorKind::Parameter, "labels length != layout rows");
+  std::vector<const char*> ip, lp;
+  for (const auto& x : ids) ip.push_back(x.c_str());
+  for (const auto& x : labels) lp.push_back(x.c_str());
+  detail::check(nomad_b200_save_layout_csv(path.c_str(), layout.positions.data(), layout.rows,
+                                           ip.data(), labels.empty() ? nullptr : lp.data()));
 }
 
 }  // namespace nomad::b200

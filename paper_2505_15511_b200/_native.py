@@ -110,6 +110,7 @@ _SIGS = {
     "nomad_b200_debug_tc_gemm": (C.c_int32, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint32,
                                              C.c_uint32, _vp]),
     "nomad_b200_nccl_unique_id": (C.c_int32, [_vp]),
+    "nomad_b200_trainer_seek": (C.c_int32, [_vp, C.c_uint64]),
     "nomad_b200_load_vectors_raw": (C.c_int32, [_vp, C.c_char_p, C.c_uint64, C.c_uint64, _vp,
                                                 C.c_int32, C.POINTER(C.c_uint64),
                                                 C.POINTER(C.c_uint64)]),

@@ -445,6 +445,10 @@ class Trainer:
         check(lib().nomad_b200_trainer_timing(self.h, C.byref(a), C.byref(b), C.byref(e)))
         return a.value, b.value, e.value
 
+    def seek(self, epoch: int) -> None:
+        """Continue the schedule at `epoch` (resume after set_layout(checkpoint))."""
+        check(lib().nomad_b200_trainer_seek(self.h, epoch))
+
     def progress(self):
         e, u = C.c_uint64(), C.c_uint64()
         check(lib().nomad_b200_trainer_progress(self.h, C.byref(e), C.byref(u)))

@@ -35,23 +35,16 @@
 #define HOG_G16 4         // lanes per head when k <= 16
 #endif
 #ifndef HOG_ROUNDS
-#define HOG_ROUNDS 4      // rounds of 256/G heads per scheduled chunk
+#define HOG_ROUNDS 8      // rounds of 256/G heads per scheduled chunk
 #endif
-#ifndef HOG_CAS
-#define HOG_CAS 0         // 1: one 128-bit CAS per row instead of two RED.F64 (measured 1.9x slower)
-#endif
-#ifndef HOG_PLAIN
-#define HOG_PLAIN 0       // 1: unsynchronised read-modify-write rows (the reference's Hogwild stores)
+#ifndef HOG_PF
+#define HOG_PF 1          // 1: next head's draws + neighbour ids issued before this head's math
 #endif
 #ifndef HOG_DF
 #define HOG_DF 1          // 1: double-float rows {hi, lo}, one RED.F32x2 per row update
 #endif
 #ifndef HOG_MF32
 #define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
-#endif
-
-#if HOG_DF && (HOG_CAS || HOG_PLAIN)
-#error "HOG_CAS / HOG_PLAIN operate on f64 rows: build them with -DHOG_DF=0"
 #endif
 
 namespace nb {
@@ -61,36 +54,6 @@ __device__ __forceinline__ double gsum(double v) {
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-// Atomic x/y add on one 16-byte row with a single 128-bit compare-and-swap
-// (one L2 tag request instead of two RED.F64). `seen` returns the value the
-// row held; the add succeeded iff it equals `expect` bitwise.
-__device__ __forceinline__ double2 cas128(double2* p, double2 expect, double2 desired) {
-  unsigned long long r0, r1;
-  asm volatile(
-      "{\n\t.reg .b128 e, d, r;\n\t"
-      "mov.b128 e, {%2, %3};\n\t"
-      "mov.b128 d, {%4, %5};\n\t"
-      "atom.global.cas.b128 r, [%6], e, d;\n\t"
-      "mov.b128 {%0, %1}, r;\n\t}"
-      : "=l"(r0), "=l"(r1)
-      : "l"(__double_as_longlong(expect.x)), "l"(__double_as_longlong(expect.y)),
-        "l"(__double_as_longlong(desired.x)), "l"(__double_as_longlong(desired.y)), "l"(p)
-      : "memory");
-  return make_double2(__longlong_as_double(r0), __longlong_as_double(r1));
-}
-__device__ __forceinline__ bool same_bits(double2 a, double2 b) {
-  return __double_as_longlong(a.x) == __double_as_longlong(b.x) &&
-         __double_as_longlong(a.y) == __double_as_longlong(b.y);
-}
-// Finish a CAS-add whose first attempt returned `seen` for expected `old`.
-__device__ __forceinline__ void cas_add_finish(double2* p, double2 old, double2 seen, double ax,
-                                               double ay) {
-  while (!same_bits(seen, old)) {
-    old = seen;
-    seen = cas128(p, old, make_double2(old.x + ax, old.y + ay));
-  }
 }
 
 // Position rows. HOG_DF: 16-byte double-float rows {hi.x, hi.y, lo.x, lo.y},
@@ -134,6 +97,15 @@ __device__ __forceinline__ void load_ids(const uint32_t* p, uint32_t (&v)[NPL]) 
     }
   }
 }
+
+// One head's draws: head, tails owned by this lane, this lane's neighbour ids.
+template <int NPL, int TPL>
+struct Draw {
+  uint32_t head, cnt, own_gid;
+  uint32_t tl[TPL], nb[NPL];
+  double sf;
+  bool act;
+};
 
 template <int G, int KMAX, int SMAX>
 __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
@@ -201,13 +173,14 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       __syncthreads();
     }
     const uint32_t t_base = (c - W.chunk0) * P.chunk_heads;
-    // chunk_heads is a multiple of GPB, so every warp runs the same number of
-    // rounds: all shuffles below are executed by full warps (inactive groups
-    // at the end of a shard run predicated off).
-    for (uint32_t j = grp; j < P.chunk_heads; j += GPB) {
-      const uint32_t t = t_base + j;
-      const bool act = t < W.draws;
-      // ---- draws: lane b of the group computes Philox block b = draws 2b, 2b+1
+    // draw(t): the Philox draws of head t (lane b of the group computes
+    // Philox block b = draws 2b, 2b+1), its tails, and the load of its
+    // neighbour ids (this lane's slice of the ELL row). Executed by full warps
+    // (shuffles): chunk_heads is a multiple of GPB, so every warp runs the
+    // same number of rounds; inactive groups at the end of a shard run
+    // predicated off.
+    auto draw = [&](uint32_t t, Draw<NPL, TPL>& D) {
+      D.act = t < W.draws;
       uint64_t dA = 0, dB = 0;
       if (gl < (int)nblk_draw) {
         const u32x4 r = philox4x32_10(u32x4{t, W.id, (uint32_t)P.epoch, (uint32_t)gl},
@@ -216,19 +189,19 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
         dB = join64(r.z, r.w);
       }
       const uint64_t d0 = __shfl_sync(0xffffffffu, dA, g0);
-      const uint32_t hidx = act ? bounded(d0, W.n_elig) : 0u;
-      const uint32_t head = (W.all_elig || !act) ? W.pstart + hidx : P.elig[W.elig_off + hidx];
-      uint32_t pool0 = W.pstart, pooln = W.npts, own_gid = 0xFFFFFFFFu;
-      double sf = sf_w;
+      const uint32_t hidx = D.act ? bounded(d0, W.n_elig) : 0u;
+      D.head = (W.all_elig || !D.act) ? W.pstart + hidx : P.elig[W.elig_off + hidx];
+      uint32_t pool0 = W.pstart, pooln = W.npts;
+      D.own_gid = 0xFFFFFFFFu;
+      D.sf = sf_w;
       if (P.all_but_own) {  // optimizer.hpp:264-277
-        const LocalCluster L = P.lclusters[P.cl_of[head]];
+        const LocalCluster L = P.lclusters[P.cl_of[D.head]];
         pool0 = L.start;
         pooln = L.count;
-        own_gid = L.gid;
-        sf = M * P.cell_probs[L.gid] / (double)s;
+        D.own_gid = L.gid;
+        D.sf = M * P.cell_probs[L.gid] / (double)s;
       }
       // tails owned by this lane: q = gl + G m uses draw 1 + q
-      uint32_t tl[TPL];
 #pragma unroll
       for (int m = 0; m < TPL; ++m) {
         const int q = gl + G * m;
@@ -236,18 +209,30 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
         const int src = g0 + (((d >> 1) < G) ? (d >> 1) : 0);
         const uint64_t a = __shfl_sync(0xffffffffu, dA, src);
         const uint64_t b = __shfl_sync(0xffffffffu, dB, src);
-        tl[m] = (act && q < (int)s) ? pool0 + bounded((d & 1) ? b : a, pooln) : head;
+        D.tl[m] = (D.act && q < (int)s) ? pool0 + bounded((d & 1) ? b : a, pooln) : D.head;
       }
+      D.cnt = D.act ? (P.ncnt ? P.ncnt[D.head] : k) : 0u;
+      load_ids<NPL>(P.ell + (size_t)D.head * P.kpad + NPL * gl, D.nb);
+    };
+    Draw<NPL, TPL> D;
+    draw(t_base + grp, D);
+    for (uint32_t j = grp; j < P.chunk_heads; j += GPB) {
+      const bool act = D.act;
+      const uint32_t head = D.head, cnt = D.cnt, own_gid = D.own_gid;
+      const double sf = D.sf;
       // ---- gathers (all issued before any use)
-      const uint32_t cnt = act ? (P.ncnt ? P.ncnt[head] : k) : 0u;
-      uint32_t nb[NPL];
-      load_ids<NPL>(P.ell + (size_t)head * P.kpad + NPL * gl, nb);
       const double2 h = ld_row(P.pos, head);
       double2 pn[NPL], pt[TPL];
 #pragma unroll
-      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row(P.pos, nb[i]) : h;
+      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row(P.pos, D.nb[i]) : h;
 #pragma unroll
-      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row(P.pos, tl[m]) : h;
+      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row(P.pos, D.tl[m]) : h;
+      const bool more = j + GPB < P.chunk_heads;  // warp-uniform
+#if HOG_PF
+      // next head's draws and neighbour ids in flight during this head's math
+      Draw<NPL, TPL> Dn;
+      if (more) draw(t_base + j + GPB, Dn);
+#endif
 
       // ---- mean field over this lane's cells: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
       double s1 = 0.0, s2x = 0.0, s2y = 0.0;
@@ -300,9 +285,6 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       const double* wrow = wt + cnt * k;
       double gx = 0.0, gy = 0.0, bgs = 0.0;
       float lf = 0.f;
-#if HOG_CAS
-      double2 dn[NPL], dt[TPL];
-#endif
 #pragma unroll
       for (int i = 0; i < NPL; ++i) {
         const int jj = NPL * gl + i;
@@ -318,13 +300,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           gy = fma(pull, dy, gy);
           if (!P.head_only) {
             const double a = st * pull;
-#if HOG_CAS
-            dn[i] = make_double2(a * dx, a * dy);
-#elif HOG_PLAIN
-            P.pos[nb[i]] = make_double2(pn[i].x + a * dx, pn[i].y + a * dy);
-#else
-            add_row(P.pos, nb[i], a * dx, a * dy);
-#endif
+            add_row(P.pos, D.nb[i], a * dx, a * dy);
           }
         }
       }
@@ -340,58 +316,23 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           gy = fma(-push, dy, gy);
           if (!P.head_only) {
             const double a = -st * push;
-#if HOG_CAS
-            dt[m] = make_double2(a * dx, a * dy);
-#elif HOG_PLAIN
-            P.pos[tl[m]] = make_double2(pt[m].x + a * dx, pt[m].y + a * dy);
-#else
-            add_row(P.pos, tl[m], a * dx, a * dy);
-#endif
+            add_row(P.pos, D.tl[m], a * dx, a * dy);
           }
         }
       }
       // ---- mean repulsion + head update (lane 0 of the group)
       gx = gsum<G>(fma(-2.0 * bgs, s2x, gx));
       gy = gsum<G>(fma(-2.0 * bgs, s2y, gy));
-#if HOG_CAS
-      // All of this lane's row updates go out back to back (independent
-      // ATOMG.CAS.128 in flight), then the rare failed ones are retried.
-      {
-        const bool upd = act && !P.head_only;
-        double2 sn[NPL], stt[TPL], sh = h;
-#pragma unroll
-        for (int i = 0; i < NPL; ++i)
-          if (upd && NPL * gl + i < (int)cnt)
-            sn[i] = cas128(&P.pos[nb[i]], pn[i], make_double2(pn[i].x + dn[i].x, pn[i].y + dn[i].y));
-#pragma unroll
-        for (int m = 0; m < TPL; ++m)
-          if (upd && gl + G * m < (int)s)
-            stt[m] = cas128(&P.pos[tl[m]], pt[m], make_double2(pt[m].x + dt[m].x, pt[m].y + dt[m].y));
-        const double hx = -st * gx, hy = -st * gy;
-        if (act && gl == 0) sh = cas128(&P.pos[head], h, make_double2(h.x + hx, h.y + hy));
-#pragma unroll
-        for (int i = 0; i < NPL; ++i)
-          if (upd && NPL * gl + i < (int)cnt) cas_add_finish(&P.pos[nb[i]], pn[i], sn[i], dn[i].x, dn[i].y);
-#pragma unroll
-        for (int m = 0; m < TPL; ++m)
-          if (upd && gl + G * m < (int)s) cas_add_finish(&P.pos[tl[m]], pt[m], stt[m], dt[m].x, dt[m].y);
-        if (act && gl == 0) {
-          cas_add_finish(&P.pos[head], h, sh, hx, hy);
-          edge_acc += (double)(cnt + s);
-        }
-      }
-#elif HOG_PLAIN
-      if (act && gl == 0) {
-        P.pos[head] = make_double2(h.x - st * gx, h.y - st * gy);
-        edge_acc += (double)(cnt + s);
-      }
-#else
       if (act && gl == 0) {
         add_row(P.pos, head, -st * gx, -st * gy);
         edge_acc += (double)(cnt + s);
       }
-#endif
       loss_acc += (double)lf;
+#if HOG_PF
+      if (more) D = Dn;
+#else
+      if (more) draw(t_base + j + GPB, D);
+#endif
     }
   }
 }
@@ -430,7 +371,7 @@ uint32_t hogwild_group_size(uint32_t kpad, uint32_t s) {
   return (kpad <= 16 && s <= 7) ? HOG_G16 : 8;
 }
 uint32_t hogwild_chunk_rounds() { return HOG_ROUNDS; }
-bool hogwild_double_float() { return HOG_DF && !HOG_CAS && !HOG_PLAIN; }
+bool hogwild_double_float() { return HOG_DF; }
 
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st) {
   hog_dispatch(P, P.kpad, P.s, nblocks, smem, st, nullptr);

@@ -556,6 +556,28 @@ struct nomad_b200_trainer {
     }
   }
 
+  // Continue the schedule at epoch `e` (resume from a checkpoint layout).
+  // Throughput mode: draws are keyed by (seed, epoch, worker, t), nothing to
+  // replay. Replay mode: each worker's mt19937_64 stream is advanced past the
+  // skipped epochs' draws exactly as build_tapes consumes them.
+  void seek(uint64_t e) {
+    if (e > cfg.epochs) fail(kParameter, "epoch out of range for schedule");
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
+      if (e < epochs_done) fail(kParameter, "replay mode cannot seek backwards");
+      for (; epochs_done < e; ++epochs_done)
+        for (uint32_t wl = 0; wl < nwl; ++wl) {
+          const WorkerDev& d = wk[wl];
+          auto& g = rng[wl];
+          for (uint32_t t = 0; t < d.draws; ++t) {
+            const uint32_t h = elig_h[d.elig_off + uniform_index(g, d.n_elig)];
+            const uint64_t pn = cfg.approx_all_but_own ? lcl[local_cluster_of(h)].count : d.npts;
+            for (uint64_t q = 0; q < s; ++q) (void)uniform_index(g, pn);
+          }
+        }
+    }
+    epochs_done = e;
+  }
+
   uint32_t local_cluster_of(uint32_t local_id) const {
     // lcl is sorted by start
     uint32_t lo = 0, hi = (uint32_t)lcl.size();
@@ -929,6 +951,13 @@ int32_t nomad_b200_trainer_timing(nomad_b200_trainer* t, double* sgd_ms, double*
     if (sgd_ms) *sgd_ms = t->sgd_ms;
     if (means_ms) *means_ms = t->means_ms;
     if (epochs) *epochs = t->timed_epochs;
+  });
+}
+
+int32_t nomad_b200_trainer_seek(nomad_b200_trainer* t, uint64_t epoch) {
+  return guard([&] {
+    if (!t) fail(kParameter, "trainer is NULL");
+    t->seek(epoch);
   });
 }
 

@@ -2,6 +2,7 @@
 // own header-only functions (nomad::X) and the B200 engine through the shim
 // (nomad::b200::X) on identical inputs and compares.
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 
 #include "nomad/nomad.hpp"
@@ -39,7 +40,30 @@ int main() {
   bad += ra.clusters.assignment != rb.clusters.assignment;
   bad += ra.graph.neighbors != rb.graph.neighbors;
   const double l0 = ra.epoch_mean_loss.back(), l1 = rb.epoch_mean_loss.back();
-  bad += !(std::fabs(l0 - l1) < 0.05 * l0);
+  // replay mode + bit-exact GPU PCA: the whole fit is bit-identical
+  bad += la.positions != lb.positions || ra.epoch_mean_loss != rb.epoch_mean_loss;
+  const auto npa = nomad::neighborhood_preservation(ds, la, 10, 500, 1);
+  const auto npb = nomad::b200::neighborhood_preservation(ds, la, 10, 500, 1);
+  bad += npa.to_json() != npb.to_json();
+  const auto ta = nomad::random_triplet_accuracy(ds, la, 20000, 2);
+  const auto tb = nomad::b200::random_triplet_accuracy(ds, la, 20000, 2);
+  bad += ta.to_json() != tb.to_json();
+  std::vector<std::string> ids(ds.rows);
+  for (std::size_t i = 0; i < ds.rows; ++i) ids[i] = "row" + std::to_string(i);
+  nomad::save_layout(la, ids, {}, "/tmp/shim_demo_ref.csv");
+  nomad::b200::save_layout(la, ids, {}, "/tmp/shim_demo_b200.csv");
+  {
+    std::FILE* f1 = std::fopen("/tmp/shim_demo_ref.csv", "rb");
+    std::FILE* f2 = std::fopen("/tmp/shim_demo_b200.csv", "rb");
+    int c1 = 0, c2 = 0;
+    do {
+      c1 = f1 ? std::fgetc(f1) : -2;
+      c2 = f2 ? std::fgetc(f2) : -3;
+    } while (c1 == c2 && c1 != EOF);
+    bad += c1 != c2;
+    if (f1) std::fclose(f1);
+    if (f2) std::fclose(f2);
+  }
   bad += rb.comm.epochs.size() != 20 || rb.comm.epochs[0].size() != 2;
   try {
     nomad::b200::lsh_init(ds, 1, 0);

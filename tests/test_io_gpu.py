@@ -49,3 +49,37 @@ def test_fit_checkpoints(port, ctx, tmp_path):
     assert np.array_equal(tr.layout(), y)
     tr.close()
     assert open(prefix + ".epoch4.csv", "rb").read() == open(ref_csv, "rb").read()
+
+
+@pytest.mark.parametrize("mode", ["replay", "hogwild"])
+def test_resume_from_checkpoint(port, ctx, tmp_path, mode):
+    """fit()-style checkpoint after 3 of 6 epochs, reloaded from the CSV into a
+    fresh trainer + seek(3): replay mode continues bit-identically; hogwild
+    continues the same schedule (epoch-keyed draws) to a comparable loss."""
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(3000, 16, 5, 10.0, 4)
+    c = nb.kmeans_em_default_tol(x, nb.lsh_init(x, 6, 2, ctx=ctx), 100, ctx=ctx)
+    g = nb.build_knn(x, c, 15, ctx=ctx)
+    init = nb.pca_init(x, 2, ctx=ctx)
+    cfg = nb.TrainConfig(epochs=6, workers=2, seed=2, sgd_mode=mode)
+    full = nb.Trainer(g, c, init, cfg, ctx=ctx)
+    l_full = full.run(6)
+    y_full = full.layout()
+    full.close()
+    a = nb.Trainer(g, c, init, cfg, ctx=ctx)
+    a.run(3)
+    p = str(tmp_path / "ck.epoch3.csv")
+    nb.save_layout(a.layout(), p)
+    a.close()
+    ck = np.loadtxt(p, delimiter=",", skiprows=1)[:, 1:3]
+    b = nb.Trainer(g, c, ck, cfg, ctx=ctx)
+    b.seek(3)
+    l_res = b.run(3)
+    y_res = b.layout()
+    assert b.progress()[0] == 6
+    b.close()
+    if mode == "replay":
+        assert np.array_equal(y_res, y_full)
+        assert np.array_equal(np.asarray(l_res), np.asarray(l_full)[3:])
+    else:
+        assert abs(l_res[-1] - l_full[-1]) < 0.05 * abs(l_full[-1])
