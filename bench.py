@@ -206,8 +206,9 @@ def main():
     ctx.set_stream(stream.cuda_stream)
     index = {}
     if args.graph == "knn":
-        # the full hot-path index build on this GPU (identical on every rank:
-        # same seeds, deterministic kernels), then the dataset is released
+        # the hot-path index build on this GPU: lsh_init + kmeans_em identical on
+        # every rank (same seeds, deterministic kernels), kNN lists only for this
+        # rank's clusters; then the dataset is released
         x = nbx.generate_mixture(n, d, blobs, 10.0, 42, ctx=ctx)
         torch.cuda.synchronize()
         t_a = time.perf_counter()
@@ -215,7 +216,12 @@ def main():
         t_b = time.perf_counter()
         cl = nbx.kmeans_em_default_tol(x, c0, 100, ctx=ctx)
         t_c = time.perf_counter()
-        g = nbx.build_knn(x, cl, k, mode=args.knn_mode, ctx=ctx)
+        owned = None
+        if world > 1:  # lists only for this rank's shards (clusters are independent)
+            c2w, _ = nbx.shard_plan(cl.assignment, ncl, W, world)
+            per = W // world
+            owned = np.nonzero((c2w >= rank * per) & (c2w < (rank + 1) * per))[0]
+        g = nbx.build_knn(x, cl, k, mode=args.knn_mode, ctx=ctx, owned_clusters=owned)
         t_d = time.perf_counter()
         # kNN recall@15 of the graph the epochs use, against exact fp64 lists
         # recomputed exhaustively for a row sample (exact mode: 1.0 by construction)

@@ -182,6 +182,15 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx,
                              const nomad_b200_clusters* clusters, uint64_t k,
                              int32_t knn_mode, nomad_b200_graph* out);
 
+/* Multi-GPU form of build_knn: lists are built only for the rows of the
+ * `n_owned` clusters in owned_clusters (host array, e.g. the clusters of this
+ * rank's shards from nomad_b200_plan); every other row gets an empty list.
+ * Owned rows' lists are identical to build_knn's (clusters are independent,
+ * knn.hpp:62-64), and the trainer reads only its own rows. */
+int32_t nomad_b200_build_knn_shard(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                                   const nomad_b200_clusters* clusters, uint64_t k,
+                                   int32_t knn_mode, uint64_t n_owned,
+                                   const uint32_t* owned_clusters, nomad_b200_graph* out);
 /* recall@k of `graph` against exact lists recomputed (exhaustive fp64) for
  * `sample` rows drawn without replacement from the rows with a non-empty
  * list (0 = all rows). */

@@ -255,8 +255,9 @@ def kmeans_em_default_tol(data, init: ClusterAssignment, max_iters: int = 100,
 
 
 def build_knn(data, clusters: ClusterAssignment, k: int, mode: str = "exact",
-              ctx: Optional[Context] = None) -> KnnGraph:
-    """knn.hpp:65-109"""
+              ctx: Optional[Context] = None, owned_clusters=None) -> KnnGraph:
+    """knn.hpp:65-109. owned_clusters: build lists only for these clusters'
+    rows (multi-GPU shards; other rows get empty lists)."""
     if k < 1:
         raise NomadError("Parameter", "k must be >= 1")
     dv, keep = _dataset(data)
@@ -266,9 +267,14 @@ def build_knn(data, clusters: ClusterAssignment, k: int, mode: str = "exact",
     nb = np.zeros(max(n * k, 1), np.uint32)
     di = np.zeros(max(n * k, 1), np.float64)
     gv = N.GraphView(n, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
-    check(lib().nomad_b200_build_knn(_ctx(ctx).h, C.byref(dv), C.byref(v), k,
-                                     {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[mode],
-                                     C.byref(gv)))
+    km = {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[mode]
+    if owned_clusters is None:
+        check(lib().nomad_b200_build_knn(_ctx(ctx).h, C.byref(dv), C.byref(v), k, km, C.byref(gv)))
+    else:
+        oc = np.ascontiguousarray(owned_clusters, np.uint32)
+        check(lib().nomad_b200_build_knn_shard(_ctx(ctx).h, C.byref(dv), C.byref(v), k, km,
+                                               len(oc), oc.ctypes.data if len(oc) else None,
+                                               C.byref(gv)))
     m = int(off[n])
     return KnnGraph(n, k, off, nb[:m], di[:m])
 

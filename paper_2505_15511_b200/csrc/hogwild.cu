@@ -40,6 +40,9 @@
 #ifndef HOG_PF
 #define HOG_PF 1          // 1: next head's draws + neighbour ids issued before this head's math
 #endif
+#ifndef HOG_PFH
+#define HOG_PFH 0         // 1: the head row is loaded with the draws (one round ahead)
+#endif
 #ifndef HOG_DF
 #define HOG_DF 1          // 1: double-float rows {hi, lo}, one RED.F32x2 per row update
 #endif
@@ -105,6 +108,9 @@ struct Draw {
   uint32_t tl[TPL], nb[NPL];
   double sf;
   bool act;
+#if HOG_PFH
+  double2 h;  // the head's position, loaded with the draws
+#endif
 };
 
 template <int G, int KMAX, int SMAX>
@@ -213,6 +219,9 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       }
       D.cnt = D.act ? (P.ncnt ? P.ncnt[D.head] : k) : 0u;
       load_ids<NPL>(P.ell + (size_t)D.head * P.kpad + NPL * gl, D.nb);
+#if HOG_PFH
+      D.h = ld_row(P.pos, D.head);
+#endif
     };
     Draw<NPL, TPL> D;
     draw(t_base + grp, D);
@@ -221,7 +230,11 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       const uint32_t head = D.head, cnt = D.cnt, own_gid = D.own_gid;
       const double sf = D.sf;
       // ---- gathers (all issued before any use)
+#if HOG_PFH
+      const double2 h = D.h;
+#else
       const double2 h = ld_row(P.pos, head);
+#endif
       double2 pn[NPL], pt[TPL];
 #pragma unroll
       for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row(P.pos, D.nb[i]) : h;

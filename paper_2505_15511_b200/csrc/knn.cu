@@ -456,7 +456,8 @@ __global__ void k_sizes2(const uint32_t* a, uint64_t n, uint32_t* sizes) {
 
 void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
                        const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
-                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out);
+                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
+                       const std::vector<uint8_t>* own);
 
 // Builds the graph into device buffers (offsets n+1, nb/dist offsets[n]).
 struct KnnResult {
@@ -525,9 +526,12 @@ void ffma_filter(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t
   NB_CUDA(cudaStreamSynchronize(S));
 }
 
+// own: nullptr = every cluster; else own[r] != 0 for the clusters whose lists
+// are built (multi-GPU: the clusters of this rank's shards); rows of the other
+// clusters get empty lists.
 void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
                      const uint32_t* assign_d, uint32_t C, uint32_t k, KnnResult& R,
-                     int mode) {
+                     int mode, const std::vector<uint8_t>* own) {
   cudaStream_t S = ctx->stream;
   if (k < 1) fail(kParameter, "k must be >= 1");
   if (k > 56) fail(kParameter, "k > 56 is not supported by the exact kNN build");
@@ -535,9 +539,22 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   NB_CUDA(cudaMemsetAsync(sizes.p, 0, C * 4, S));
   k_sizes2<<<(unsigned)std::min<uint64_t>(4096, (n + 255) / 256), 256, 0, S>>>(assign_d, n, sizes.p);
   note_launch(ctx, "k_sizes");
+  // list lengths: min(k, size - 1), 0 outside the owned clusters
+  DBuf<uint32_t> sizes_eff;
+  const uint32_t* sizes_want = sizes.p;
+  if (own) {
+    std::vector<uint32_t> sh(C);
+    NB_CUDA(cudaMemcpyAsync(sh.data(), sizes.p, C * 4, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    for (uint32_t r = 0; r < C; ++r)
+      if (!(*own)[r]) sh[r] = 1;
+    sizes_eff.alloc(C);
+    NB_CUDA(cudaMemcpyAsync(sizes_eff.p, sh.data(), C * 4, cudaMemcpyHostToDevice, S));
+    sizes_want = sizes_eff.p;
+  }
   // offsets = exclusive scan of min(k, size-1) (knn.hpp:77-83)
   DBuf<uint32_t> want(n + 1);
-  k_knn_want<<<(unsigned)std::min<uint64_t>(4096, (n + 255) / 256), 256, 0, S>>>(assign_d, sizes.p, n, k, want.p);
+  k_knn_want<<<(unsigned)std::min<uint64_t>(4096, (n + 255) / 256), 256, 0, S>>>(assign_d, sizes_want, n, k, want.p);
   note_launch(ctx, "k_knn_want");
   R.offsets.alloc(n + 1);
   size_t tmp = 0;
@@ -559,7 +576,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   uint32_t tiles = 0;
   for (uint32_t r = 0; r < C; ++r) {
     const uint32_t sz = (uint32_t)(off[r + 1] - off[r]);
-    if (sz < 2) continue;
+    if (sz < 2 || (own && !(*own)[r])) continue;
     segs.push_back(FilterSeg{off[r], off[r], sz, sz, tiles, 0});
     tiles += (sz + QT - 1) / QT;
   }
@@ -575,7 +592,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
     NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
     const unsigned rb = (unsigned)((n * 32 + 255) / 256);
     auto go = [&](auto kern) {
-      kern<<<rb, 256, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d, sizes.p, k, 0u, cid.p, clb.p,
+      kern<<<rb, 256, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d, sizes_want, k, 0u, cid.p, clb.p,
                               ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
     };
     if (KP == 32) go(k_knn_rerank<32>); else go(k_knn_rerank<64>);
@@ -592,7 +609,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
     // stage 1: tensor-core filter (bf16 fast / fp16 certified)
     if (mode == NOMAD_B200_KNN_BF16 && k > 24) fail(kParameter, "bf16 kNN mode supports k <= 24");
     knn_tc_candidates(ctx, x, n, d, assign_d, C, mode == NOMAD_B200_KNN_EXACT, cid, clb, ccnt,
-                      &KP);
+                      &KP, own);
     nf = rerank();
     R.tc_uncertified = nf;
     if (nf && mode == NOMAD_B200_KNN_EXACT) {
@@ -712,9 +729,9 @@ using namespace nb;
 
 extern "C" {
 
-int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
-                             const nomad_b200_clusters* clusters, uint64_t k, int32_t knn_mode,
-                             nomad_b200_graph* out) {
+static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                              const nomad_b200_clusters* clusters, uint64_t k, int32_t knn_mode,
+                              uint64_t n_owned, const uint32_t* owned, nomad_b200_graph* out) {
   return guard([&] {
     if (!ctx || !clusters || !out) fail(kParameter, "NULL argument");
     if (k < 1) fail(kParameter, "k must be >= 1");
@@ -735,8 +752,16 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
     if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16 &&
         knn_mode != NOMAD_B200_KNN_EXACT_FFMA)
       fail(kParameter, "unknown knn_mode");
+    std::vector<uint8_t> own;
+    if (owned) {
+      own.assign(C, 0);
+      for (uint64_t i = 0; i < n_owned; ++i) {
+        if (owned[i] >= C) fail(kParameter, "owned cluster id out of range");
+        own[owned[i]] = 1;
+      }
+    }
     KnnResult R;
-    build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R, knn_mode);
+    build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R, knn_mode, owned ? &own : nullptr);
     ctx->knn_tc_uncertified = R.tc_uncertified;
     ctx->knn_exhaustive = R.fallbacks;
     const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
@@ -751,6 +776,22 @@ int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
     out->rows = dd.n;
     out->k = k;
   });
+}
+
+int32_t nomad_b200_build_knn(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                             const nomad_b200_clusters* clusters, uint64_t k, int32_t knn_mode,
+                             nomad_b200_graph* out) {
+  return build_knn_impl(ctx, data, clusters, k, knn_mode, 0, nullptr, out);
+}
+
+int32_t nomad_b200_build_knn_shard(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                                   const nomad_b200_clusters* clusters, uint64_t k,
+                                   int32_t knn_mode, uint64_t n_owned,
+                                   const uint32_t* owned_clusters, nomad_b200_graph* out) {
+  if (!owned_clusters && n_owned) return guard([&] { fail(kParameter, "owned_clusters is NULL"); });
+  static const uint32_t none = 0;
+  return build_knn_impl(ctx, data, clusters, k, knn_mode, n_owned,
+                        owned_clusters ? owned_clusters : &none, out);
 }
 
 // recall@k of a graph against the exact lists of `sample` rows drawn without

@@ -385,7 +385,8 @@ constexpr uint32_t idesc16(uint32_t M, uint32_t N, bool fp16) {
 // otherwise the bf16 fast filter (KP = 32, cand_lb = +inf).
 void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
                        const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
-                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out) {
+                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
+                       const std::vector<uint8_t>* own) {
   cudaStream_t S = ctx->stream;
   const int KP = fp16 ? 64 : 32;
   *kp_out = KP;
@@ -419,7 +420,7 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
     const uint64_t sz = off[r + 1] - off[r];
     for (uint64_t t = 0; t < (pstart[r + 1] - pstart[r]); ++t) rcl[pstart[r] + t] = r;
     for (uint64_t t = 0; t < sz; ++t) perm[pstart[r] + t] = mem_h[off[r] + t];
-    if (sz < 2) continue;
+    if (sz < 2 || (own && !(*own)[r])) continue;
     for (uint64_t q = 0; q < sz; q += TM)
       tiles.push_back(TcTile{(uint32_t)(pstart[r] + q), (uint32_t)pstart[r], (uint32_t)sz,
                              (uint32_t)q, r});

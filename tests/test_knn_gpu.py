@@ -88,3 +88,23 @@ def test_knn_multiblob_clusters_open_rows(port, ctx, d):
     assert np.array_equal(gg.offsets, g.offsets)
     assert np.array_equal(gg.neighbors, g.neighbors)
     assert np.array_equal(gg.distances, g.distances)
+
+
+@pytest.mark.parametrize("mode", ["exact", "bf16"])
+def test_knn_shard_owned_clusters(port, ctx, mode):
+    """Multi-GPU index build: lists only for the owned clusters (a rank's
+    shards), identical to the full build there, empty elsewhere."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, _ = index_case(3000, 32, 10, 8, 15)
+    ca = nb.ClusterAssignment(c.assignment, c.n_clusters, x.shape[1], c.centroids, c.sizes)
+    full = nb.build_knn(x, ca, 15, mode=mode, ctx=ctx)
+    c2w, _ = nb.shard_plan(c.assignment, c.n_clusters, 4, 2)
+    owned = np.nonzero(c2w >= 2)[0]  # rank 1 of 2 (workers 2, 3)
+    part = nb.build_knn(x, ca, 15, mode=mode, ctx=ctx, owned_clusters=owned)
+    mine = np.isin(c.assignment, owned)
+    cnt_full = np.diff(full.offsets.astype(np.int64))
+    cnt_part = np.diff(part.offsets.astype(np.int64))
+    assert np.array_equal(cnt_part, np.where(mine, cnt_full, 0))
+    for i in np.nonzero(mine)[0][:500]:
+        assert np.array_equal(part.neighbors_of(i), full.neighbors_of(i))
+    assert nb.build_knn(x, ca, 15, mode=mode, ctx=ctx, owned_clusters=[]).offsets[-1] == 0
