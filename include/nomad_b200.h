@@ -279,11 +279,18 @@ int32_t nomad_b200_trainer_progress(nomad_b200_trainer* tr,
                                     uint64_t* epochs_done,
                                     uint64_t* edge_updates);
 
-/* pca.hpp:79-218 pca_init on the GPU (tolerance parity: the covariance
- * passes are tree-reduced fp64; the vector algebra, Rng stream, sign rule and
- * rank-1 jitter follow the reference exactly). layout_out: rows x 2 f64. */
+/* pca.hpp:79-218 pca_init on the GPU, bit-identical to the reference: every
+ * covariance apply is X_c^T (X_c v) / n in the reference's summation orders;
+ * the vector algebra, Rng stream, sign rule and rank-1 jitter are the
+ * reference's. layout_out: rows x 2 f64. */
 int32_t nomad_b200_pca_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                             uint64_t seed, double* layout_out, int32_t location);
+/* The same algorithm with the covariance formed once (fp64 DSYRK over
+ * centred row chunks) and each apply a d x d product: tolerance parity
+ * (~1e-10 on the standardised layout) for ~2 passes over the data instead of
+ * ~2 per power iteration. fit() uses it in throughput (hogwild) mode. */
+int32_t nomad_b200_pca_init_fast(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                                 uint64_t seed, double* layout_out, int32_t location);
 
 /* --------------------------------------------------- fit (L4) */
 /* optimizer.hpp:327-482 fit. init_layout: the PCA initialisation

@@ -512,12 +512,13 @@ def fit(data, config: TrainConfig, init_layout=None, report: Optional[FitReport]
     return out
 
 
-def pca_init(data, seed: int = 0, ctx: Optional[Context] = None) -> np.ndarray:
-    """pca.hpp:79-218 on the GPU (tolerance parity; see nomad_b200_pca_init)."""
+def pca_init(data, seed: int = 0, ctx: Optional[Context] = None, fast: bool = False) -> np.ndarray:
+    """pca.hpp:79-218 on the GPU: bit-identical (default) or, fast=True, with the
+    covariance formed once (tolerance parity, ~2 data passes)."""
     dv, keep = _dataset(data)
     out = np.zeros((dv.rows, 2), np.float64)
-    check(lib().nomad_b200_pca_init(_ctx(ctx).h, C.byref(dv), seed & (2**64 - 1),
-                                    out.ctypes.data, N.HOST))
+    fn = lib().nomad_b200_pca_init_fast if fast else lib().nomad_b200_pca_init
+    check(fn(_ctx(ctx).h, C.byref(dv), seed & (2**64 - 1), out.ctypes.data, N.HOST))
     return out
 
 

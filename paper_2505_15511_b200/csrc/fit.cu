@@ -10,6 +10,8 @@
 extern "C" {
 int32_t nomad_b200_pca_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                             uint64_t seed, double* layout_out, int32_t location);
+int32_t nomad_b200_pca_init_fast(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                                 uint64_t seed, double* layout_out, int32_t location);
 }
 
 namespace nb {
@@ -70,7 +72,12 @@ extern "C" int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_
     if (init_layout) {
       NB_CUDA(cudaMemcpyAsync(init.p, init_layout, n * 16, cudaMemcpyHostToDevice, S));
     } else {
-      chk(nomad_b200_pca_init(ctx, &dv, cfg->seed, init.p, NOMAD_B200_DEVICE));  // :353
+      // :353 — bit-identical PCA where the trajectory is (replay), the
+      // precomputed-covariance form in throughput mode
+      if (cfg->sgd_mode == NOMAD_B200_SGD_HOGWILD)
+        chk(nomad_b200_pca_init_fast(ctx, &dv, cfg->seed, init.p, NOMAD_B200_DEVICE));
+      else
+        chk(nomad_b200_pca_init(ctx, &dv, cfg->seed, init.p, NOMAD_B200_DEVICE));
     }
     nomad_b200_trainer* tr = nullptr;
     chk(nomad_b200_trainer_create(ctx, &g, &cl, init.p, NOMAD_B200_DEVICE, cfg, 0, 1, nullptr,

@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cublas_v2.h>
+
 #include "index_common.cuh"
 
 namespace nb {
@@ -171,6 +173,29 @@ __global__ void k_layout_set(double* lay, uint64_t n, int comp, const double* v)
     lay[2 * i + comp] = v[i];
 }
 
+// Centred fp64 copy of rows [r0, r0 + rows) (row-major, = column-major d x rows).
+__global__ void k_center_f64(const float* __restrict__ x, uint64_t r0, uint64_t rows, uint32_t d,
+                             const double* __restrict__ mean, double* __restrict__ out) {
+  const uint64_t N = rows * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    out[e] = (double)x[r0 * d + e] - mean[e % d];
+}
+
+#define NB_CUBLAS(call)                                                                  \
+  do {                                                                                   \
+    const cublasStatus_t s_ = (call);                                                    \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                     \
+      fail(kInternal, std::string("cuBLAS error ") + std::to_string((int)s_) + " in " #call); \
+  } while (0)
+
+struct Cublas {
+  cublasHandle_t h = nullptr;
+  ~Cublas() {
+    if (h) cublasDestroy(h);
+  }
+};
+
 double dot(const std::vector<double>& a, const std::vector<double>& b) {
   double acc = 0.0;
   for (size_t j = 0; j < a.size(); ++j) acc += a[j] * b[j];
@@ -186,8 +211,15 @@ double normalize(std::vector<double>& v) {
 }  // namespace
 
 // layout_out: device n x 2.
+// fast == false: every covariance apply is the reference's two-pass
+// X_c^T (X_c v) / n with its summation orders (bit-identical result).
+// fast == true: the covariance C = X_c^T X_c / n is formed once (fp64 DSYRK
+// over centred row chunks, cuBLAS) and each apply is C v (DSYMV); the power
+// iteration, deflation, Rayleigh-Ritz step, sign rule and standardisation are
+// unchanged, so the result agrees with the reference to rounding of the
+// covariance products (tolerance parity) at a fraction of the passes over X.
 void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, uint64_t seed,
-                  double* layout_out) {
+                  double* layout_out, bool fast) {
   cudaStream_t S = ctx->stream;
   if (n < 2) fail(kParameter, "need at least 2 rows");
   HostRng rng(HostRng::stream_seed(seed, 0x706361 /* "pca" */));
@@ -209,8 +241,35 @@ void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, u
   const size_t col_smem = 2 * BR * 33 * sizeof(float);
   NB_CUDA(cudaFuncSetAttribute(k_pca_cols<BR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)col_smem));
+  Cublas cb;
+  DBuf<double> cov;
+  if (fast) {
+    NB_CUBLAS(cublasCreate(&cb.h));
+    NB_CUBLAS(cublasSetStream(cb.h, S));
+    cov.alloc(d * d);
+    NB_CUDA(cudaMemsetAsync(cov.p, 0, d * d * 8, S));
+    const uint64_t R = std::max<uint64_t>(1, std::min<uint64_t>(n, (512ull << 20) / (d * 8)));
+    DBuf<double> xc(R * d);
+    const double one = 1.0;
+    for (uint64_t r0 = 0; r0 < n; r0 += R) {
+      const uint64_t rows = std::min(R, n - r0);
+      k_center_f64<<<ctx->sm_count * 8, 256, 0, S>>>(x, r0, rows, (uint32_t)d, mean.p, xc.p);
+      note_launch(ctx, "k_center_f64");
+      NB_CUBLAS(cublasDsyrk(cb.h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, (int)d, (int)rows, &one,
+                            xc.p, (int)d, &one, cov.p, (int)d));
+    }
+  }
   auto cov_apply = [&](const std::vector<double>& v, std::vector<double>& out) {
     NB_CUDA(cudaMemcpyAsync(vd.p, v.data(), d * 8, cudaMemcpyHostToDevice, S));
+    if (fast) {
+      const double alpha = 1.0 / static_cast<double>(n), beta = 0.0;
+      NB_CUBLAS(cublasDsymv(cb.h, CUBLAS_FILL_MODE_UPPER, (int)d, &alpha, cov.p, (int)d, vd.p, 1,
+                            &beta, yd.p, 1));
+      out.resize(d);
+      NB_CUDA(cudaMemcpyAsync(out.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+      return;
+    }
     k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, vd.p, t.p, nullptr, nullptr);
     note_launch(ctx, "k_pca_rows");
     k_pca_cols<BR><<<(unsigned)((d + 31) / 32), 256, col_smem, S>>>(x, n, (uint32_t)d, mean.p,
@@ -336,19 +395,30 @@ void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, u
 
 using namespace nb;
 
-extern "C" int32_t nomad_b200_pca_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
-                                       uint64_t seed, double* layout_out, int32_t location) {
+static int32_t pca_entry(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                         uint64_t seed, double* layout_out, int32_t location, bool fast) {
   return guard([&] {
     if (!ctx || !layout_out) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
     dd.bind(data, ctx->stream);
     if (location == NOMAD_B200_DEVICE) {
-      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, layout_out);
+      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, layout_out, fast);
     } else {
       DBuf<double> lay(2 * dd.n);
-      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, lay.p);
+      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, lay.p, fast);
       NB_CUDA(cudaMemcpy(layout_out, lay.p, dd.n * 16, cudaMemcpyDeviceToHost));
     }
   });
+}
+
+extern "C" int32_t nomad_b200_pca_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                                       uint64_t seed, double* layout_out, int32_t location) {
+  return pca_entry(ctx, data, seed, layout_out, location, false);
+}
+
+extern "C" int32_t nomad_b200_pca_init_fast(nomad_b200_ctx* ctx,
+                                            const nomad_b200_dataset_view* data, uint64_t seed,
+                                            double* layout_out, int32_t location) {
+  return pca_entry(ctx, data, seed, layout_out, location, true);
 }

@@ -52,6 +52,27 @@ def test_gpu_pca_bit_exact(port, ctx, n, d, blobs):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("n,d,blobs", [(3000, 24, 8), (2000, 200, 5), (700, 33, 3)])
+def test_gpu_pca_fast_tolerance(port, ctx, n, d, blobs):
+    """Precomputed-covariance PCA: same algorithm, covariance products formed
+    once; agrees with the reference to 1e-9 on the standardised layout."""
+    import paper_2505_15511_b200 as nb
+    x = port.gaussian_mixture(n, d, blobs, 10.0, 23)
+    ref = port.pca_init(x, 9)
+    got = nb.pca_init(x, 9, ctx=ctx, fast=True)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-9)
+
+
+def test_gpu_pca_fast_rank_one_jitter(port, ctx):
+    import paper_2505_15511_b200 as nb
+    t = np.linspace(-1, 1, 500)
+    x = np.ascontiguousarray(np.outer(t, np.arange(1, 9)).astype(np.float32))
+    ref = port.pca_init(x, 4)
+    got = nb.pca_init(x, 4, ctx=ctx, fast=True)
+    np.testing.assert_allclose(got[:, 0], ref[:, 0], rtol=0, atol=1e-9)
+    assert np.array_equal(got[:, 1], ref[:, 1])  # the seeded jitter
+
+
 def test_fit_fully_on_gpu_is_bit_exact(port, ref, ctx):
     """The whole fit() on the GPU (LSH k-means, certified kNN, PCA, replay
     epochs) reproduces the reference's fit() bit for bit."""

@@ -28,7 +28,7 @@ def main():
     torch.cuda.synchronize()
     out["index_s"] = round(time.perf_counter() - t, 2)
     t = time.perf_counter()
-    init = nb.pca_init(x, 7, ctx=ctx)
+    init = nb.pca_init(x, 7, ctx=ctx, fast=True)
     out["pca_s"] = round(time.perf_counter() - t, 2)
     for mode in ("hogwild", "replay"):
         cfg = nb.TrainConfig(epochs=E, workers=W, seed=7, sgd_mode=mode)

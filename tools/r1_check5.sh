@@ -1,0 +1,15 @@
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 2>&1 | tail -4
+timeout 600 python -c "
+import sys, time; sys.path.insert(0,'.')
+import torch, paper_2505_15511_b200 as nb
+ctx = nb.Context(0)
+for n in (1000000, 10000000):
+    x = nb.generate_mixture(n, 768, 64, 10.0, 42, ctx=ctx)
+    torch.cuda.synchronize(); t = time.perf_counter()
+    y = nb.pca_init(x, 7, ctx=ctx, fast=True)
+    print('fast pca', n, round(time.perf_counter() - t, 2), 's', y[:2].tolist(), flush=True)
+    if n == 1000000:
+        t = time.perf_counter(); z = nb.pca_init(x, 7, ctx=ctx)
+        print('exact pca', n, round(time.perf_counter() - t, 2), 's maxdiff', float(abs(y - z).max()), flush=True)
+    del x
+"
