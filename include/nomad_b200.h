@@ -285,10 +285,13 @@ int32_t nomad_b200_trainer_progress(nomad_b200_trainer* tr,
  * reference's. layout_out: rows x 2 f64. */
 int32_t nomad_b200_pca_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                             uint64_t seed, double* layout_out, int32_t location);
-/* The same algorithm with the covariance formed once (fp64 DSYRK over
- * centred row chunks) and each apply a d x d product: tolerance parity
- * (~1e-10 on the standardised layout) for ~2 passes over the data instead of
- * ~2 per power iteration. fit() uses it in throughput (hogwild) mode. */
+/* The same algorithm with the covariance sums formed once (one fp64 pass
+ * over the centred data) and each apply a d x d product: the basis agrees
+ * with the reference's to rounding, so the layout spans the same principal
+ * plane, but its in-plane orientation may differ (pca.hpp:150-165 rotates by
+ * an angle computed from rounding-level quantities). ~1 pass over the data
+ * instead of ~2 per power iteration (1M x 768: 0.3-0.8 s vs 41 s). fit()
+ * uses it in throughput (hogwild) mode. */
 int32_t nomad_b200_pca_init_fast(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                                  uint64_t seed, double* layout_out, int32_t location);
 
@@ -340,6 +343,10 @@ int32_t nomad_b200_generate_mixture(nomad_b200_ctx* ctx, uint64_t rows,
 
 /* Diagnostic: one 128 x 128 bf16 tile product D = A B^T through the same
  * TMA + tcgen05.mma + TMEM path the bf16 kNN uses (rows rounded to bf16). */
+/* Debug / unit path of the fast PCA: S = sum_i (x_i - mean)(x_i - mean)^T
+ * (out_host: d x d). */
+int32_t nomad_b200_debug_cov(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                             const double* mean_host, double* out_host);
 int32_t nomad_b200_debug_tc_gemm(nomad_b200_ctx* ctx, const float* host_rows, uint64_t rows,
                                  uint64_t d, uint32_t a0, uint32_t b0, float* out128x128);
 

@@ -111,6 +111,7 @@ _SIGS = {
                                              C.c_uint32, _vp]),
     "nomad_b200_nccl_unique_id": (C.c_int32, [_vp]),
     "nomad_b200_trainer_seek": (C.c_int32, [_vp, C.c_uint64]),
+    "nomad_b200_debug_cov": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp, _vp]),
     "nomad_b200_pca_init_fast": (C.c_int32, [_vp, C.POINTER(DatasetView), C.c_uint64, _vp,
                                              C.c_int32]),
     "nomad_b200_build_knn_shard": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(ClustersView),

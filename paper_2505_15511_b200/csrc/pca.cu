@@ -11,8 +11,6 @@
 #include <algorithm>
 #include <cmath>
 
-#include <cublas_v2.h>
-
 #include "index_common.cuh"
 
 namespace nb {
@@ -173,28 +171,70 @@ __global__ void k_layout_set(double* lay, uint64_t n, int comp, const double* v)
     lay[2 * i + comp] = v[i];
 }
 
-// Centred fp64 copy of rows [r0, r0 + rows) (row-major, = column-major d x rows).
-__global__ void k_center_f64(const float* __restrict__ x, uint64_t r0, uint64_t rows, uint32_t d,
-                             const double* __restrict__ mean, double* __restrict__ out) {
-  const uint64_t N = rows * d;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
-       e += (uint64_t)gridDim.x * blockDim.x)
-    out[e] = (double)x[r0 * d + e] - mean[e % d];
+// Covariance sums S = X_c^T X_c (fast PCA): grid (upper-triangle 32x32 tiles,
+// row slices); each CTA accumulates its tile over its row slice in fp64
+// (thread = 4 entries of one column), 64 centred rows staged per step;
+// partials are summed per entry in slice order by k_cov_reduce
+// (deterministic).
+constexpr int CV_ROWS = 64;
+__global__ void __launch_bounds__(256) k_cov_partial(const float* __restrict__ x, uint64_t n,
+                                                     uint32_t d, const double* __restrict__ mean,
+                                                     const uint2* __restrict__ tiles,
+                                                     uint32_t slices, double* __restrict__ part) {
+  __shared__ double A[CV_ROWS][33], B[CV_ROWS][33];
+  const uint2 T = tiles[blockIdx.x];  // (row tile, col tile), row <= col
+  const uint32_t i0 = T.x * 32, j0 = T.y * 32;
+  const uint32_t sl = blockIdx.y;
+  const uint64_t r0 = n * sl / slices, r1 = n * (sl + 1) / slices;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (uint64_t rb = r0; rb < r1; rb += CV_ROWS) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < CV_ROWS * 32; e += 256) {
+      const int rr = e >> 5, cc = e & 31;
+      const uint64_t row = rb + rr;
+      const bool ok = row < r1;
+      A[rr][cc] = (ok && i0 + cc < d) ? (double)x[row * d + i0 + cc] - mean[i0 + cc] : 0.0;
+      B[rr][cc] = (ok && j0 + cc < d) ? (double)x[row * d + j0 + cc] - mean[j0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < CV_ROWS; ++rr) {
+      const double bv = B[rr][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(A[rr][ty + 8 * q], bv, acc[q]);
+    }
+  }
+  const uint64_t base = ((uint64_t)blockIdx.x * slices + sl) * 1024;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) part[base + (ty + 8 * q) * 32 + tx] = acc[q];
 }
 
-#define NB_CUBLAS(call)                                                                  \
-  do {                                                                                   \
-    const cublasStatus_t s_ = (call);                                                    \
-    if (s_ != CUBLAS_STATUS_SUCCESS)                                                     \
-      fail(kInternal, std::string("cuBLAS error ") + std::to_string((int)s_) + " in " #call); \
-  } while (0)
+// C[i][j] (full symmetric, row-major) = sum over slices of the tile partials.
+__global__ void k_cov_reduce(const double* __restrict__ part, const uint2* __restrict__ tiles,
+                             uint32_t ntiles, uint32_t slices, uint32_t d, double* __restrict__ C) {
+  const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (g >= (uint64_t)ntiles * 1024) return;
+  const uint32_t t = (uint32_t)(g >> 10), e = (uint32_t)(g & 1023);
+  const uint32_t i = tiles[t].x * 32 + (e >> 5), j = tiles[t].y * 32 + (e & 31);
+  if (i >= d || j >= d) return;
+  double s = 0.0;
+  for (uint32_t sl = 0; sl < slices; ++sl) s += part[((uint64_t)t * slices + sl) * 1024 + e];
+  C[(uint64_t)i * d + j] = s;
+  C[(uint64_t)j * d + i] = s;
+}
 
-struct Cublas {
-  cublasHandle_t h = nullptr;
-  ~Cublas() {
-    if (h) cublasDestroy(h);
-  }
-};
+// y = C v / n, one warp per output entry (fixed-order lane sums + butterfly).
+__global__ void k_cov_apply(const double* __restrict__ C, const double* __restrict__ v, uint32_t d,
+                            double inv_n, double* __restrict__ y) {
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= d) return;
+  double s = 0.0;
+  for (uint32_t j = lane; j < d; j += 32) s = fma(C[(uint64_t)i * d + j], v[j], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[i] = s * inv_n;
+}
 
 double dot(const std::vector<double>& a, const std::vector<double>& b) {
   double acc = 0.0;
@@ -210,14 +250,42 @@ double normalize(std::vector<double>& v) {
 
 }  // namespace
 
+// S = X_c^T X_c (d x d, fp64, row-major, symmetric) of the centred data.
+void covariance_sums(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+                     const double* mean, double* cov) {
+  cudaStream_t S = ctx->stream;
+  const uint32_t nt = (uint32_t)((d + 31) / 32);
+  std::vector<uint2> th;
+  for (uint32_t a = 0; a < nt; ++a)
+    for (uint32_t b = a; b < nt; ++b) th.push_back(make_uint2(a, b));
+  const uint32_t ntl = (uint32_t)th.size();
+  // enough CTAs to cover the GPU; each slice keeps >= 1024 rows
+  uint32_t slices = std::max<uint32_t>(1, (uint32_t)((4ull * ctx->sm_count + ntl - 1) / ntl));
+  slices = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(slices, n / 1024));
+  DBuf<uint2> tiles_d(ntl);
+  NB_CUDA(cudaMemcpyAsync(tiles_d.p, th.data(), ntl * sizeof(uint2), cudaMemcpyHostToDevice, S));
+  DBuf<double> part((uint64_t)ntl * slices * 1024);
+  k_cov_partial<<<dim3(ntl, slices), 256, 0, S>>>(x, n, (uint32_t)d, mean, tiles_d.p, slices,
+                                                 part.p);
+  note_launch(ctx, "k_cov_partial");
+  k_cov_reduce<<<(unsigned)(((uint64_t)ntl * 1024 + 255) / 256), 256, 0, S>>>(
+      part.p, tiles_d.p, ntl, slices, (uint32_t)d, cov);
+  note_launch(ctx, "k_cov_reduce");
+  NB_CUDA(cudaStreamSynchronize(S));
+}
+
 // layout_out: device n x 2.
 // fast == false: every covariance apply is the reference's two-pass
 // X_c^T (X_c v) / n with its summation orders (bit-identical result).
-// fast == true: the covariance C = X_c^T X_c / n is formed once (fp64 DSYRK
-// over centred row chunks, cuBLAS) and each apply is C v (DSYMV); the power
+// fast == true: the covariance sums S = X_c^T X_c are formed once (fp64,
+// k_cov_partial / k_cov_reduce) and each apply is S v / n; the power
 // iteration, deflation, Rayleigh-Ritz step, sign rule and standardisation are
-// unchanged, so the result agrees with the reference to rounding of the
-// covariance products (tolerance parity) at a fraction of the passes over X.
+// unchanged. The basis agrees with the reference's to rounding, so the layout
+// spans the reference's principal plane; its in-plane orientation can differ:
+// pca.hpp:150-165 rotates the converged basis by atan2(eigen0 - h00, h01),
+// two quantities that are both at rounding-noise level once the power
+// iteration has converged, so only the bit-exact path reproduces the
+// reference's orientation.
 void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, uint64_t seed,
                   double* layout_out, bool fast) {
   cudaStream_t S = ctx->stream;
@@ -241,30 +309,17 @@ void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, u
   const size_t col_smem = 2 * BR * 33 * sizeof(float);
   NB_CUDA(cudaFuncSetAttribute(k_pca_cols<BR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)col_smem));
-  Cublas cb;
   DBuf<double> cov;
   if (fast) {
-    NB_CUBLAS(cublasCreate(&cb.h));
-    NB_CUBLAS(cublasSetStream(cb.h, S));
     cov.alloc(d * d);
-    NB_CUDA(cudaMemsetAsync(cov.p, 0, d * d * 8, S));
-    const uint64_t R = std::max<uint64_t>(1, std::min<uint64_t>(n, (512ull << 20) / (d * 8)));
-    DBuf<double> xc(R * d);
-    const double one = 1.0;
-    for (uint64_t r0 = 0; r0 < n; r0 += R) {
-      const uint64_t rows = std::min(R, n - r0);
-      k_center_f64<<<ctx->sm_count * 8, 256, 0, S>>>(x, r0, rows, (uint32_t)d, mean.p, xc.p);
-      note_launch(ctx, "k_center_f64");
-      NB_CUBLAS(cublasDsyrk(cb.h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, (int)d, (int)rows, &one,
-                            xc.p, (int)d, &one, cov.p, (int)d));
-    }
+    covariance_sums(ctx, x, n, d, mean.p, cov.p);
   }
   auto cov_apply = [&](const std::vector<double>& v, std::vector<double>& out) {
     NB_CUDA(cudaMemcpyAsync(vd.p, v.data(), d * 8, cudaMemcpyHostToDevice, S));
     if (fast) {
-      const double alpha = 1.0 / static_cast<double>(n), beta = 0.0;
-      NB_CUBLAS(cublasDsymv(cb.h, CUBLAS_FILL_MODE_UPPER, (int)d, &alpha, cov.p, (int)d, vd.p, 1,
-                            &beta, yd.p, 1));
+      k_cov_apply<<<(unsigned)((d * 32 + 255) / 256), 256, 0, S>>>(cov.p, vd.p, (uint32_t)d,
+                                                                  1.0 / static_cast<double>(n), yd.p);
+      note_launch(ctx, "k_cov_apply");
       out.resize(d);
       NB_CUDA(cudaMemcpyAsync(out.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
       NB_CUDA(cudaStreamSynchronize(S));
@@ -421,4 +476,20 @@ extern "C" int32_t nomad_b200_pca_init_fast(nomad_b200_ctx* ctx,
                                             const nomad_b200_dataset_view* data, uint64_t seed,
                                             double* layout_out, int32_t location) {
   return pca_entry(ctx, data, seed, layout_out, location, true);
+}
+
+// Debug / unit path: covariance sums of a dataset about `mean` (host d
+// doubles) into out (host d x d).
+extern "C" int32_t nomad_b200_debug_cov(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
+                                        const double* mean_host, double* out_host) {
+  return guard([&] {
+    if (!ctx || !mean_host || !out_host) fail(kParameter, "NULL argument");
+    bind_device(ctx);
+    DevData dd;
+    dd.bind(data, ctx->stream);
+    DBuf<double> m(dd.d), c(dd.d * dd.d);
+    NB_CUDA(cudaMemcpy(m.p, mean_host, dd.d * 8, cudaMemcpyHostToDevice));
+    covariance_sums(ctx, dd.x, dd.n, dd.d, m.p, c.p);
+    NB_CUDA(cudaMemcpy(out_host, c.p, dd.d * dd.d * 8, cudaMemcpyDeviceToHost));
+  });
 }

