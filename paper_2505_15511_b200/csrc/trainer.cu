@@ -7,6 +7,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -491,21 +493,32 @@ struct nomad_b200_trainer {
   // ------------------------------------------------------- replay tapes
   // For each local worker: the reference's draw sequence for this epoch
   // (optimizer.hpp:252-285) and its wavefront levels.
-  void build_tapes(uint64_t epoch_draw_total, std::vector<uint32_t>& th, std::vector<uint32_t>& tt,
-                   std::vector<uint32_t>& tid, std::vector<uint32_t>& loff,
-                   std::vector<uint32_t>& lbase, std::vector<uint32_t>& nlev, uint64_t& edges) {
-    (void)epoch_draw_total;
-    th.clear(); tt.clear(); tid.clear(); loff.clear(); lbase.clear(); nlev.clear();
-    edges = 0;
-    std::vector<uint32_t> last(orig_of.size(), 0);
-    std::vector<uint32_t> head(0), tails(0), lev(0);
-    for (uint32_t wl = 0; wl < nwl; ++wl) {
+  // One epoch's replay tape: every worker's draws (mt19937_64 stream, the
+  // reference's order) grouped by conflict level, worker-major.
+  struct Tape {
+    std::vector<uint32_t> th, tt, tid, loff, lbase, nlev;
+    uint64_t edges = 0;
+  };
+
+  // Workers draw from their own streams and touch disjoint points, so their
+  // tapes are built concurrently (one host thread per worker, up to the
+  // hardware threads) straight into their slices of the epoch tape.
+  void build_tapes(Tape& T) {
+    std::vector<size_t> base(nwl + 1, 0);
+    for (uint32_t wl = 0; wl < nwl; ++wl) base[wl + 1] = base[wl] + wk[wl].draws;
+    T.th.resize(base[nwl]);
+    T.tt.resize(base[nwl] * s);
+    T.tid.resize(base[nwl]);
+    std::vector<std::vector<uint32_t>> loffw(nwl);
+    std::vector<uint32_t> maxl(nwl, 0);
+    std::vector<uint64_t> edg(nwl, 0);
+    std::vector<uint32_t> last(orig_of.size(), 0);  // disjoint point ranges per worker
+    auto one = [&](uint32_t wl) {
       const WorkerDev& d = wk[wl];
       const uint32_t D = d.draws;
-      head.resize(D);
-      tails.resize((size_t)D * s);
-      lev.resize(D);
+      std::vector<uint32_t> head(D), tails((size_t)D * s), lev(D);
       uint32_t maxlev = 0;
+      uint64_t edges = 0;
       auto& g = rng[wl];
       const uint32_t* pool = pool_h.data() + pool_off[wl];
       for (uint32_t t = 0; t < D; ++t) {
@@ -539,20 +552,42 @@ struct nomad_b200_trainer {
       std::vector<uint32_t> cnt_l(maxlev + 1, 0);
       for (uint32_t t = 0; t < D; ++t) ++cnt_l[lev[t] + 1];
       for (uint32_t l = 0; l < maxlev; ++l) cnt_l[l + 1] += cnt_l[l];
-      const size_t base = th.size();
-      lbase.push_back((uint32_t)loff.size());
-      nlev.push_back(maxlev);
-      for (uint32_t l = 0; l <= maxlev; ++l) loff.push_back((uint32_t)(base + cnt_l[l]));
-      th.resize(base + D);
-      tt.resize((base + D) * s);
-      tid.resize(base + D);
+      const size_t b0 = base[wl];
+      auto& lo = loffw[wl];
+      lo.resize(maxlev + 1);
+      for (uint32_t l = 0; l <= maxlev; ++l) lo[l] = (uint32_t)(b0 + cnt_l[l]);
       std::vector<uint32_t> fill(cnt_l.begin(), cnt_l.end() - 1);
       for (uint32_t t = 0; t < D; ++t) {
-        const size_t at = base + fill[lev[t]]++;
-        th[at] = head[t];
-        tid[at] = t;
-        for (uint64_t q = 0; q < s; ++q) tt[at * s + q] = tails[(size_t)t * s + q];
+        const size_t at = b0 + fill[lev[t]]++;
+        T.th[at] = head[t];
+        T.tid[at] = t;
+        for (uint64_t q = 0; q < s; ++q) T.tt[at * s + q] = tails[(size_t)t * s + q];
       }
+      maxl[wl] = maxlev;
+      edg[wl] = edges;
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nth = std::min<unsigned>(nwl, hw);
+    if (nth <= 1) {
+      for (uint32_t wl = 0; wl < nwl; ++wl) one(wl);
+    } else {
+      std::atomic<uint32_t> next{0};
+      std::vector<std::thread> pool_t;
+      for (unsigned i = 0; i < nth; ++i)
+        pool_t.emplace_back([&] {
+          for (uint32_t wl; (wl = next.fetch_add(1)) < nwl;) one(wl);
+        });
+      for (auto& x : pool_t) x.join();
+    }
+    T.loff.clear();
+    T.lbase.assign(nwl, 0);
+    T.nlev.assign(nwl, 0);
+    T.edges = 0;
+    for (uint32_t wl = 0; wl < nwl; ++wl) {
+      T.lbase[wl] = (uint32_t)T.loff.size();
+      T.nlev[wl] = maxl[wl];
+      T.loff.insert(T.loff.end(), loffw[wl].begin(), loffw[wl].end());
+      T.edges += edg[wl];
     }
   }
 
@@ -688,7 +723,18 @@ struct nomad_b200_trainer {
       upload(wk_draw_base, draw_base_h, S);
       loss_slot.alloc(std::max<uint32_t>(acc, 1));
     }
-    std::vector<uint32_t> th, tt, tid, loff, lbase, nlev;
+    // replay: the next epoch's tape is built on host threads while this
+    // epoch runs on the GPU (tapes depend only on the workers' streams);
+    // only within this call, so the streams end exactly n_epochs ahead
+    Tape cur, nxt;
+    std::thread prefetch;
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{prefetch};
+    const bool replay = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY;
     std::vector<double> wl_loss(nwl), all_loss(world * std::max<uint32_t>(nwl, 1));
     std::vector<unsigned long long> wl_edges(nwl);
     DBuf<double> gl;  // gathered per-worker losses (multi-rank)
@@ -704,14 +750,21 @@ struct nomad_b200_trainer {
       uint64_t edges = 0;
       if (!ev[0])
         for (auto& x : ev) NB_CUDA(cudaEventCreate(&x));
-      if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
-        build_tapes(0, th, tt, tid, loff, lbase, nlev, edges);
-        upload(tape_head, th, S);
-        upload(tape_tails, tt, S);
-        upload(tape_t, tid, S);
-        upload(lvl_off, loff, S);
-        upload(wk_lvl_base, lbase, S);
-        upload(wk_nlev, nlev, S);
+      if (replay) {
+        if (it == 0) {
+          build_tapes(cur);
+        } else {
+          prefetch.join();
+          std::swap(cur, nxt);
+        }
+        if (it + 1 < n_epochs) prefetch = std::thread([this, &nxt] { build_tapes(nxt); });
+        edges = cur.edges;
+        upload(tape_head, cur.th, S);
+        upload(tape_tails, cur.tt, S);
+        upload(tape_t, cur.tid, S);
+        upload(lvl_off, cur.loff, S);
+        upload(wk_lvl_base, cur.lbase, S);
+        upload(wk_nlev, cur.nlev, S);
         P.tape_head = tape_head.p;
         P.tape_tails = tape_tails.p;
         P.tape_t = tape_t.p;
