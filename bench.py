@@ -237,11 +237,11 @@ def main():
                  "cluster_sizes_min_max": [int(cl.sizes.min()), int(cl.sizes.max())]}
     else:
         a, offsets, nb, init = synthetic_index(n, ncl, k)
-    nid = None
+    nid = nid64 = None
     if world > 1:
-        obj = [nbx.nccl_unique_id() if rank == 0 else None]
+        obj = [(nbx.nccl_unique_id(), nbx.nccl_unique_id()) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
+        nid, nid64 = obj[0]
     cfg = nbx.TrainConfig(epochs=200, workers=W, seed=7, sgd_mode=args.sgd_mode, k=k)
     graph = nbx.KnnGraph(n, k, offsets, nb, np.zeros(0))
     clusters = nbx.ClusterAssignment(a, ncl, d, np.zeros(0), np.zeros(0))
@@ -322,6 +322,43 @@ def main():
            "path": "C-ABI trainer_set_layout(host) + trainer_run(1) x K (host loss) + "
                    "trainer_layout(host)"}
 
+    # the same K epochs with full f64 position rows (two RED.F64 per row update)
+    # instead of double-float rows: the strict-f64 storage variant, same protocol
+    f64rows = None
+    if args.sgd_mode == "hogwild":
+        cfg64 = nbx.TrainConfig(epochs=200, workers=W, seed=7, sgd_mode="hogwild", k=k,
+                                hogwild_f64_rows=True)
+        tr64 = nbx.Trainer(graph, clusters, init, cfg64, rank=rank, world_size=world,
+                           nccl_id=nid64 if world > 1 else None, ctx=ctx)
+        tr64.run(args.warmup)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s64a, _, _ = tr64.timing()
+        g0 = tr64.progress()[1]
+        ev0.record(stream)
+        tr64.run(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms64 = ev0.elapsed_time(ev1)
+        s64b, _, _ = tr64.timing()
+        ed64 = tr64.progress()[1] - g0
+        if world > 1:
+            t = torch.tensor([ms64], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms64 = float(t[0])
+            t = torch.tensor([float(ed64)], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            ed64 = int(t[0])
+        k64 = (s64b - s64a) / args.steps
+        f64rows = {"value": ed64 / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64 / args.steps,
+                   "kernel_ms": k64,
+                   "roofline_frac": BYTES_PER_HEAD * heads_local / (k64 / 1e3) / 1e9 / peak,
+                   "positions": "f64 rows, two RED.F64 per row update (strict f64 storage)"}
+        tr64.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         which, val, cores, secs = cpu_baseline_reference(a, offsets, nb, init, ncl, W, k,
@@ -358,6 +395,7 @@ def main():
                          "bytes_per_head": BYTES_PER_HEAD, "peak_source": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "f64_rows": f64rows,
             "knn_recall_at_15": index.get("knn_recall_at_15"),
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -43,9 +43,6 @@
 #ifndef HOG_PFH
 #define HOG_PFH 0         // 1: the head row is loaded with the draws (one round ahead)
 #endif
-#ifndef HOG_DF
-#define HOG_DF 1          // 1: double-float rows {hi, lo}, one RED.F32x2 per row update
-#endif
 #ifndef HOG_MF32
 #define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
 #endif
@@ -59,29 +56,31 @@ __device__ __forceinline__ double gsum(double v) {
   return v;
 }
 
-// Position rows. HOG_DF: 16-byte double-float rows {hi.x, hi.y, lo.x, lo.y},
+// Position rows. DF (double-float): 16-byte rows {hi.x, hi.y, lo.x, lo.y},
 // value = hi + lo (exact in fp64), updates are one RED.F32x2 onto lo (the
 // per-request cost of RED.F32x2 equals one RED.F64, tools/micro/red_bench.cu,
 // so a row update costs half); the means pass renormalises every epoch.
-// Otherwise f64 rows and two RED.F64.
+// Otherwise f64 rows and two RED.F64 per row update.
+template <bool DF>
 __device__ __forceinline__ double2 ld_row(const double2* pos, uint32_t i) {
-#if HOG_DF
-  const float4 r = reinterpret_cast<const float4*>(pos)[i];
-  return make_double2((double)r.x + (double)r.z, (double)r.y + (double)r.w);
-#else
-  return pos[i];
-#endif
+  if constexpr (DF) {
+    const float4 r = reinterpret_cast<const float4*>(pos)[i];
+    return make_double2((double)r.x + (double)r.z, (double)r.y + (double)r.w);
+  } else {
+    return pos[i];
+  }
 }
+template <bool DF>
 __device__ __forceinline__ void add_row(double2* pos, uint32_t i, double ax, double ay) {
-#if HOG_DF
-  float* lo = reinterpret_cast<float*>(pos + i) + 2;
-  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(lo), "f"(__double2float_rn(ax)),
-               "f"(__double2float_rn(ay))
-               : "memory");
-#else
-  atomicAdd(&pos[i].x, ax);
-  atomicAdd(&pos[i].y, ay);
-#endif
+  if constexpr (DF) {
+    float* lo = reinterpret_cast<float*>(pos + i) + 2;
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(lo), "f"(__double2float_rn(ax)),
+                 "f"(__double2float_rn(ay))
+                 : "memory");
+  } else {
+    atomicAdd(&pos[i].x, ax);
+    atomicAdd(&pos[i].y, ay);
+  }
 }
 
 template <int NPL>
@@ -113,7 +112,7 @@ struct Draw {
 #endif
 };
 
-template <int G, int KMAX, int SMAX>
+template <int G, int KMAX, int SMAX, bool DF>
 __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
   constexpr int NPL = KMAX / G;            // neighbour slots per lane
   constexpr int TPL = (SMAX + G - 1) / G;  // tail slots per lane
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       D.cnt = D.act ? (P.ncnt ? P.ncnt[D.head] : k) : 0u;
       load_ids<NPL>(P.ell + (size_t)D.head * P.kpad + NPL * gl, D.nb);
 #if HOG_PFH
-      D.h = ld_row(P.pos, D.head);
+      D.h = ld_row<DF>(P.pos, D.head);
 #endif
     };
     Draw<NPL, TPL> D;
@@ -233,13 +232,13 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #if HOG_PFH
       const double2 h = D.h;
 #else
-      const double2 h = ld_row(P.pos, head);
+      const double2 h = ld_row<DF>(P.pos, head);
 #endif
       double2 pn[NPL], pt[TPL];
 #pragma unroll
-      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row(P.pos, D.nb[i]) : h;
+      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row<DF>(P.pos, D.nb[i]) : h;
 #pragma unroll
-      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row(P.pos, D.tl[m]) : h;
+      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row<DF>(P.pos, D.tl[m]) : h;
       const bool more = j + GPB < P.chunk_heads;  // warp-uniform
 #if HOG_PF
       // next head's draws and neighbour ids in flight during this head's math
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           gy = fma(pull, dy, gy);
           if (!P.head_only) {
             const double a = st * pull;
-            add_row(P.pos, D.nb[i], a * dx, a * dy);
+            add_row<DF>(P.pos, D.nb[i], a * dx, a * dy);
           }
         }
       }
@@ -329,7 +328,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           gy = fma(-push, dy, gy);
           if (!P.head_only) {
             const double a = -st * push;
-            add_row(P.pos, D.tl[m], a * dx, a * dy);
+            add_row<DF>(P.pos, D.tl[m], a * dx, a * dy);
           }
         }
       }
@@ -337,7 +336,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       gx = gsum<G>(fma(-2.0 * bgs, s2x, gx));
       gy = gsum<G>(fma(-2.0 * bgs, s2y, gy));
       if (act && gl == 0) {
-        add_row(P.pos, head, -st * gx, -st * gy);
+        add_row<DF>(P.pos, head, -st * gx, -st * gy);
         edge_acc += (double)(cnt + s);
       }
       loss_acc += (double)lf;
@@ -353,7 +352,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 template <int G, int KMAX, int SMAX>
 static void hog_go(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st,
                    int* per_sm) {
-  auto kern = k_sgd_hogwild<G, KMAX, SMAX>;
+  auto kern = P.f64_rows ? k_sgd_hogwild<G, KMAX, SMAX, false> : k_sgd_hogwild<G, KMAX, SMAX, true>;
   if (smem > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (per_sm) {
@@ -384,7 +383,6 @@ uint32_t hogwild_group_size(uint32_t kpad, uint32_t s) {
   return (kpad <= 16 && s <= 7) ? HOG_G16 : 8;
 }
 uint32_t hogwild_chunk_rounds() { return HOG_ROUNDS; }
-bool hogwild_double_float() { return HOG_DF; }
 
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st) {
   hog_dispatch(P, P.kpad, P.s, nblocks, smem, st, nullptr);

@@ -47,6 +47,7 @@ struct SgdParams {
   unsigned long long* diverge;  // first offending key (replay: t * stride + u)
   uint32_t n_workers, kpad, k, s, m_total, n_clusters;
   int head_only, all_but_own;
+  int f64_rows;                 // hogwild: 1 = f64 rows (2 RED.F64), 0 = double-float rows
   double step;
   uint64_t epoch;
   uint32_t seed_lo, seed_hi;
@@ -79,8 +80,6 @@ void launch_means_chunk(double2* pos, bool df, const LocalCluster* lc, uint32_t 
                         unsigned long long* diverge, unsigned long long tag, cudaStream_t st);
 // f64 rows <-> double-float rows {hi.x, hi.y, lo.x, lo.y}, in place.
 void launch_pos_df(double2* pos, uint32_t n, bool to_df, cudaStream_t st);
-// true when the throughput kernel keeps positions as double-float rows
-bool hogwild_double_float();
 void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, double* slot,
                            cudaStream_t st);
 void launch_means_unpack(const double* recv, const uint32_t* slot_gid, uint32_t nslots,
