@@ -40,8 +40,8 @@
 #ifndef HOG_PF
 #define HOG_PF 1          // 1: next head's draws + neighbour ids issued before this head's math
 #endif
-#ifndef HOG_PFH
-#define HOG_PFH 0         // 1: the head row is loaded with the draws (one round ahead)
+#ifndef HOG_SROWS
+#define HOG_SROWS 0       // 1: rows of the next head streamed into shared memory by cp.async mid-round (measured slower)
 #endif
 #ifndef HOG_MF32
 #define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
@@ -83,6 +83,24 @@ __device__ __forceinline__ void add_row(double2* pos, uint32_t i, double ax, dou
   }
 }
 
+// 16-byte row -> shared memory (zero-filled when !ok); value decode as ld_row.
+__device__ __forceinline__ void cp_row(float4* dst, const double2* src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
+               "r"(ok ? 16u : 0u)
+               : "memory");
+}
+template <bool DF>
+__device__ __forceinline__ double2 sm_row(const float4* p) {
+  const float4 r = *p;
+  if constexpr (DF) {
+    return make_double2((double)r.x + (double)r.z, (double)r.y + (double)r.w);
+  } else {
+    return make_double2(__hiloint2double(__float_as_int(r.y), __float_as_int(r.x)),
+                        __hiloint2double(__float_as_int(r.w), __float_as_int(r.z)));
+  }
+}
+
 template <int NPL>
 __device__ __forceinline__ void load_ids(const uint32_t* p, uint32_t (&v)[NPL]) {
   if constexpr (NPL == 4) {
@@ -107,9 +125,6 @@ struct Draw {
   uint32_t tl[TPL], nb[NPL];
   double sf;
   bool act;
-#if HOG_PFH
-  double2 h;  // the head's position, loaded with the draws
-#endif
 };
 
 template <int G, int KMAX, int SMAX, bool DF>
@@ -218,29 +233,54 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       }
       D.cnt = D.act ? (P.ncnt ? P.ncnt[D.head] : k) : 0u;
       load_ids<NPL>(P.ell + (size_t)D.head * P.kpad + NPL * gl, D.nb);
-#if HOG_PFH
-      D.h = ld_row<DF>(P.pos, D.head);
-#endif
     };
     Draw<NPL, TPL> D;
     draw(t_base + grp, D);
+#if HOG_SROWS
+    // this lane's rows of a head (slot 0 head, 1..NPL neighbours, then tails),
+    // double-buffered in shared memory [2][SLOTS][256] (lane-contiguous)
+    constexpr int SLOTS = 1 + NPL + TPL;
+    float4* rb = reinterpret_cast<float4*>(sm + P.rowbuf_off);
+    auto issue_rows = [&](const Draw<NPL, TPL>& X, int b) {
+      float4* base = rb + (size_t)b * SLOTS * 256 + threadIdx.x;
+      cp_row(base, P.pos + X.head, X.act);
+#pragma unroll
+      for (int i = 0; i < NPL; ++i)
+        cp_row(base + (1 + i) * 256, P.pos + X.nb[i], NPL * gl + i < (int)X.cnt);
+#pragma unroll
+      for (int m = 0; m < TPL; ++m)
+        cp_row(base + (1 + NPL + m) * 256, P.pos + X.tl[m], X.act && gl + G * m < (int)s);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int buf = 0;
+    issue_rows(D, 0);
+#endif
     for (uint32_t j = grp; j < P.chunk_heads; j += GPB) {
       const bool act = D.act;
       const uint32_t head = D.head, cnt = D.cnt, own_gid = D.own_gid;
       const double sf = D.sf;
-      // ---- gathers (all issued before any use)
-#if HOG_PFH
-      const double2 h = D.h;
+#if HOG_SROWS
+      // ---- this head's rows: landed in shared memory during the previous round
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      const float4* rbase = rb + (size_t)buf * SLOTS * 256 + threadIdx.x;
+      const double2 h = sm_row<DF>(rbase);
+      double2 pn[NPL], pt[TPL];
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? sm_row<DF>(rbase + (1 + i) * 256) : h;
+#pragma unroll
+      for (int m = 0; m < TPL; ++m)
+        pt[m] = (act && gl + G * m < (int)s) ? sm_row<DF>(rbase + (1 + NPL + m) * 256) : h;
 #else
+      // ---- gathers (all issued before any use)
       const double2 h = ld_row<DF>(P.pos, head);
-#endif
       double2 pn[NPL], pt[TPL];
 #pragma unroll
       for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row<DF>(P.pos, D.nb[i]) : h;
 #pragma unroll
       for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row<DF>(P.pos, D.tl[m]) : h;
+#endif
       const bool more = j + GPB < P.chunk_heads;  // warp-uniform
-#if HOG_PF
+#if HOG_PF || HOG_SROWS
       // next head's draws and neighbour ids in flight during this head's math
       Draw<NPL, TPL> Dn;
       if (more) draw(t_base + j + GPB, Dn);
@@ -278,6 +318,10 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
         s2x = fma(pq2, dx, s2x);
         s2y = fma(pq2, dy, s2y);
       }
+#endif
+#if HOG_SROWS
+      // next head's rows stream in behind the rest of this head's math
+      if (more) issue_rows(Dn, buf ^ 1);
 #endif
       // ---- sampled negatives
       double qn[TPL], qsum = 0.0;
@@ -340,18 +384,28 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
         edge_acc += (double)(cnt + s);
       }
       loss_acc += (double)lf;
-#if HOG_PF
+#if HOG_PF || HOG_SROWS
       if (more) D = Dn;
 #else
       if (more) draw(t_base + j + GPB, D);
+#endif
+#if HOG_SROWS
+      buf ^= 1;
 #endif
     }
   }
 }
 
 template <int G, int KMAX, int SMAX>
-static void hog_go(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st,
+static void hog_go(const SgdParams& P0, uint32_t nblocks, size_t smem, cudaStream_t st,
                    int* per_sm) {
+  SgdParams P = P0;
+#if HOG_SROWS
+  // row double buffer after the weight / cell tables
+  const size_t off = (smem + 15) / 16 * 16;
+  P.rowbuf_off = (uint32_t)(off / sizeof(double));
+  smem = off + (size_t)2 * (1 + KMAX / G + (SMAX + G - 1) / G) * 256 * 16;
+#endif
   auto kern = P.f64_rows ? k_sgd_hogwild<G, KMAX, SMAX, false> : k_sgd_hogwild<G, KMAX, SMAX, true>;
   if (smem > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -48,6 +48,7 @@ struct SgdParams {
   uint32_t n_workers, kpad, k, s, m_total, n_clusters;
   int head_only, all_but_own;
   int f64_rows;                 // hogwild: 1 = f64 rows (2 RED.F64), 0 = double-float rows
+  uint32_t rowbuf_off;          // hogwild: shared-memory row buffer offset (doubles)
   double step;
   uint64_t epoch;
   uint32_t seed_lo, seed_hi;
