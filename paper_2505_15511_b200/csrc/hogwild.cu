@@ -40,11 +40,11 @@
 #ifndef HOG_PF
 #define HOG_PF 1          // 1: next head's draws + neighbour ids issued before this head's math
 #endif
+#ifndef HOG_MF2
+#define HOG_MF2 0         // 1: two independent mean-field accumulator sets
+#endif
 #ifndef HOG_SROWS
 #define HOG_SROWS 0       // 1: rows of the next head streamed into shared memory by cp.async mid-round (measured slower)
-#endif
-#ifndef HOG_MF32
-#define HOG_MF32 0        // 1: mean-field sums in fp32 (positions/updates stay fp64)
 #endif
 
 namespace nb {
@@ -141,9 +141,11 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
   const int grp = threadIdx.x / G;
   const int g0 = (threadIdx.x & 31) & ~(G - 1);  // first lane of my group
   double* wt = sm;
-  double* tab = sm + ((((k + 1) * k) + 1) & ~1u);
+  // cell table: means (double2, 16-byte aligned) then weights
+  double2* tmu = reinterpret_cast<double2*>(sm + ((((k + 1) * k) + 1) & ~1u));
   for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
 
+  double* tpw = reinterpret_cast<double*>(tmu + P.max_cells);
   uint32_t cur = 0xFFFFFFFFu;
   WorkerDev W{};
   uint32_t ncell = 0;
@@ -179,16 +181,8 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
         const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
         const double p = P.all_but_own ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
-#if HOG_MF32
-        float* tf = reinterpret_cast<float*>(tab);
-        tf[3 * q] = (float)P.means[r].x;
-        tf[3 * q + 1] = (float)P.means[r].y;
-        tf[3 * q + 2] = (float)(M * p);
-#else
-        tab[3 * q] = P.means[r].x;
-        tab[3 * q + 1] = P.means[r].y;
-        tab[3 * q + 2] = M * p;
-#endif
+        tmu[q] = P.means[r];  // cell means, then their weights M p_r
+        tpw[q] = M * p;
       }
       __syncthreads();
     }
@@ -287,38 +281,47 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #endif
 
       // ---- mean field over this lane's cells: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
+      // (two independent accumulator sets; own cell skipped in AllButOwn mode)
       double s1 = 0.0, s2x = 0.0, s2y = 0.0;
-#if HOG_MF32
       {
-        const float* tf = reinterpret_cast<const float*>(tab);
-        const float hx = (float)h.x, hy = (float)h.y;
-        float f1 = 0.f, fx = 0.f, fy = 0.f;
-        for (uint32_t q = gl; q < ncell; q += G) {
-          if (P.all_but_own && q == own_gid) continue;
-          const float dx = hx - tf[3 * q], dy = hy - tf[3 * q + 1];
-          const float qq = __frcp_rn(fmaf(dx, dx, fmaf(dy, dy, 1.f)));
-          const float pq = tf[3 * q + 2] * qq;
-          f1 += pq;
-          const float pq2 = pq * qq;
-          fx = fmaf(pq2, dx, fx);
-          fy = fmaf(pq2, dy, fy);
+        const uint32_t skip = P.all_but_own ? own_gid : 0xFFFFFFFFu;
+        uint32_t q = gl;
+#if HOG_MF2
+        double t1 = 0.0, t2x = 0.0, t2y = 0.0;
+        for (; q + G < ncell; q += 2 * G) {
+          const double2 ma = tmu[q], mb = tmu[q + G];
+          const double wa = q == skip ? 0.0 : tpw[q], wb = q + G == skip ? 0.0 : tpw[q + G];
+          const double ax = h.x - ma.x, ay = h.y - ma.y, bx = h.x - mb.x, by = h.y - mb.y;
+          const double qa = frcp(fma(ax, ax, fma(ay, ay, 1.0)));
+          const double qb = frcp(fma(bx, bx, fma(by, by, 1.0)));
+          const double pa = wa * qa, pb = wb * qb;
+          s1 += pa;
+          t1 += pb;
+          const double pa2 = pa * qa, pb2 = pb * qb;
+          s2x = fma(pa2, ax, s2x);
+          s2y = fma(pa2, ay, s2y);
+          t2x = fma(pb2, bx, t2x);
+          t2y = fma(pb2, by, t2y);
         }
-        s1 = f1;
-        s2x = fx;
-        s2y = fy;
-      }
-#else
-      for (uint32_t q = gl; q < ncell; q += G) {
-        if (P.all_but_own && q == own_gid) continue;
-        const double dx = h.x - tab[3 * q], dy = h.y - tab[3 * q + 1];
-        const double qq = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
-        const double pq = tab[3 * q + 2] * qq;
-        s1 += pq;
-        const double pq2 = pq * qq;
-        s2x = fma(pq2, dx, s2x);
-        s2y = fma(pq2, dy, s2y);
-      }
 #endif
+#pragma unroll 2
+        for (; q < ncell; q += G) {
+          const double2 ma = tmu[q];
+          const double wa = q == skip ? 0.0 : tpw[q];
+          const double ax = h.x - ma.x, ay = h.y - ma.y;
+          const double qa = frcp(fma(ax, ax, fma(ay, ay, 1.0)));
+          const double pa = wa * qa;
+          s1 += pa;
+          const double pa2 = pa * qa;
+          s2x = fma(pa2, ax, s2x);
+          s2y = fma(pa2, ay, s2y);
+        }
+#if HOG_MF2
+        s1 += t1;
+        s2x += t2x;
+        s2y += t2y;
+#endif
+      }
 #if HOG_SROWS
       // next head's rows stream in behind the rest of this head's math
       if (more) issue_rows(Dn, buf ^ 1);

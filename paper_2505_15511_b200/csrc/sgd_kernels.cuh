@@ -49,6 +49,7 @@ struct SgdParams {
   int head_only, all_but_own;
   int f64_rows;                 // hogwild: 1 = f64 rows (2 RED.F64), 0 = double-float rows
   uint32_t rowbuf_off;          // hogwild: shared-memory row buffer offset (doubles)
+  uint32_t max_cells;           // hogwild: capacity of the shared cell table
   double step;
   uint64_t epoch;
   uint32_t seed_lo, seed_hi;

@@ -87,6 +87,7 @@ struct nomad_b200_trainer {
   std::vector<std::mt19937_64> rng;
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
+  uint32_t hog_cells = 0;  // capacity of the hogwild kernel's shared cell table
   uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0;
   DBuf<uint32_t> chunk_counter;
 
@@ -359,8 +360,8 @@ struct nomad_b200_trainer {
 
     // shared-memory budgets
     smem_replay = ((k + 1) * k + 3 * C) * sizeof(double);
-    smem_hog = ((((k + 1) * k + 1) & ~1ull) + 3 * (cfg.approx_all_but_own ? C : max_rem)) *
-               sizeof(double);
+    hog_cells = (uint32_t)(cfg.approx_all_but_own ? C : max_rem);
+    smem_hog = ((((k + 1) * k + 1) & ~1ull) + 3 * (uint64_t)hog_cells) * sizeof(double);
     if (smem_replay > 200 * 1024 || smem_hog > 200 * 1024)
       fail(kSize, "too many clusters for the shared-memory cell table (C=" + std::to_string(C) + ")");
     // hogwild grid: per worker share of the resident capacity, capped by
@@ -479,6 +480,7 @@ struct nomad_b200_trainer {
     P.n_clusters = (uint32_t)C;
     P.head_only = cfg.head_only;
     P.f64_rows = cfg.hogwild_f64_rows ? 1 : 0;
+    P.max_cells = hog_cells;
     P.all_but_own = cfg.approx_all_but_own;
     P.step = step;
     P.epoch = epoch;
