@@ -205,6 +205,9 @@ int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
  * certificate did not settle, and rows resolved by the exhaustive fp64 pass. */
 int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
                              uint64_t* exhaustive_rows);
+/* Of the tc_uncertified rows, those settled by the sub-cluster stage (exact
+ * lists inside sub-clusters + a geometric bound on the other sub-clusters). */
+int32_t nomad_b200_knn_subcluster_rows(nomad_b200_ctx* ctx, uint64_t* rows);
 
 /* ------------------------------------------- final-map quality metrics */
 /* metrics.hpp:113-168 neighborhood_preservation on the GPU. Same evaluated

@@ -83,6 +83,7 @@ _SIGS = {
                                           C.POINTER(GraphView), C.c_uint64, C.c_uint64,
                                           C.POINTER(C.c_double)]),
     "nomad_b200_knn_stats": (C.c_int32, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "nomad_b200_knn_subcluster_rows": (C.c_int32, [_vp, C.POINTER(C.c_uint64)]),
     "nomad_b200_neighborhood_preservation": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp, C.c_int32,
                                                          C.c_uint64, C.c_uint64, C.c_uint64,
                                                          C.POINTER(C.c_double),

@@ -171,6 +171,12 @@ class Context:
         check(lib().nomad_b200_knn_stats(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def knn_subcluster_rows(self) -> int:
+        """Rows of the last build_knn settled by the sub-cluster stage."""
+        r = C.c_uint64()
+        check(lib().nomad_b200_knn_subcluster_rows(self.h, C.byref(r)))
+        return r.value
+
     def kernel_launches(self) -> int:
         return int(lib().nomad_b200_kernel_launches(self.h))
 

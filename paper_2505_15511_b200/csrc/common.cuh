@@ -90,7 +90,7 @@ struct nomad_b200_ctx {
   uint64_t launches = 0;
   int sm_count = 148;
   // statistics of the last build_knn call
-  uint64_t knn_tc_uncertified = 0, knn_exhaustive = 0;
+  uint64_t knn_tc_uncertified = 0, knn_exhaustive = 0, knn_sub_certified = 0;
 };
 
 namespace nb {

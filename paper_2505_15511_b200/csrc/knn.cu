@@ -18,6 +18,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "index_common.cuh"
 
@@ -466,6 +469,7 @@ struct KnnResult {
   uint64_t edges = 0;
   uint64_t fallbacks = 0;       // rows resolved by the exhaustive fp64 pass
   uint64_t tc_uncertified = 0;  // rows the tensor-core certificate did not settle
+  uint64_t sub_certified = 0;   // of those, rows settled by the sub-cluster stage
 };
 
 // Concatenate the P partition lists of each query slot (slot-major, KP per
@@ -490,6 +494,135 @@ __global__ void k_merge_parts(uint32_t m, uint32_t P, uint32_t KP, const uint32_
     ccnt[v] = c;
     clb[v] = lb;
   }
+}
+
+// ---- stage 1b (multi-blob clusters): exact kNN inside sub-clusters on the
+// tensor cores + a geometric certificate against the other sub-clusters.
+
+// Xr[i] = x[members[i]] (one cluster's rows, contiguous).
+__global__ void k_gather_rows(const float* __restrict__ x, const uint32_t* __restrict__ members,
+                              uint64_t m, uint32_t d, float* __restrict__ xr) {
+  const uint64_t N = m * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    xr[e] = x[(uint64_t)members[e / d] * d + e % d];
+}
+
+__device__ __forceinline__ double dist_to(const float* __restrict__ row, const double* __restrict__ c,
+                                          uint32_t d) {
+  double acc = 0.0;
+  for (uint32_t j = 0; j < d; ++j) {
+    const double t = (double)row[j] - c[j];
+    acc = fma(t, t, acc);
+  }
+  return sqrt(acc);
+}
+
+// radius[T] >= max over members of ||x - mu_T|| (bits of a positive double, atomicMax).
+__global__ void k_sub_radius(const float* __restrict__ xr, uint64_t m, uint32_t d,
+                             const uint32_t* __restrict__ sa, const double* __restrict__ cent,
+                             double rel, unsigned long long* radius) {
+  const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (v >= m) return;
+  const uint32_t T = sa[v];
+  const double r = dist_to(xr + v * d, cent + (uint64_t)T * d, d) * (1.0 + rel);
+  atomicMax(radius + T, (unsigned long long)__double_as_longlong(r));
+}
+
+// Bisection helpers on index lists into the cluster's rows (heuristics only:
+// they shape the partition, never the certificate).
+// lab[i] = 1 if row idx[i] is closer to cen[1] than to cen[0]; sse[lab] += dist^2.
+__global__ void k_assign2_idx(const float* __restrict__ xr, const uint32_t* __restrict__ idx,
+                              uint64_t cnt, uint32_t d, const double* __restrict__ cen,
+                              uint8_t* lab, double* sse) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  const float* row = xr + (uint64_t)idx[i] * d;
+  const double a = dist_to(row, cen, d), b = dist_to(row, cen + d, d);
+  const int l = b < a ? 1 : 0;
+  lab[i] = (uint8_t)l;
+  atomicAdd(sse + l, l ? b * b : a * a);
+}
+// Power-iteration passes for the segment's principal direction:
+// t_i = (x_i - mu) . v ; y_j += sum_i t_i (x_ij - mu_j).
+__global__ void k_proj_idx(const float* __restrict__ xr, const uint32_t* __restrict__ idx,
+                           uint64_t cnt, uint32_t d, const double* __restrict__ mu,
+                           const double* __restrict__ v, double* __restrict__ t) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  const float* row = xr + (uint64_t)idx[i] * d;
+  double a = 0.0;
+  for (uint32_t j = 0; j < d; ++j) a = fma((double)row[j] - mu[j], v[j], a);
+  t[i] = a;
+}
+__global__ void k_backproj_idx(const float* __restrict__ xr, const uint32_t* __restrict__ idx,
+                               uint64_t cnt, uint32_t d, const double* __restrict__ mu,
+                               const double* __restrict__ t, double* __restrict__ y) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  const uint64_t r0 = cnt * blockIdx.y / gridDim.y, r1 = cnt * (blockIdx.y + 1) / gridDim.y;
+  double a = 0.0;
+  for (uint64_t i = r0; i < r1; ++i) a = fma((double)xr[(uint64_t)idx[i] * d + j] - mu[j], t[i], a);
+  atomicAdd(y + j, a);
+}
+
+// Row v (cluster-local) keeps its within-sub-cluster top-`want` (exact,
+// tensor-core certified inside the sub-cluster) if every other sub-cluster T
+// provably holds no closer point: for c in T, ||x_v - x_c|| >= D_T - R_T with
+// D_T = ||x_v - mu_T||, R_T the sub-cluster radius, both computed in fp64 with
+// a relative margin `rel`, and the reference's fp64 distance of the pair is
+// >= that square times (1 - g64); sub-clusters of <= 64 rows are checked
+// member by member instead. Certified rows are written back as complete
+// candidate lists (global ids, +inf bound) so the re-rank reproduces them.
+__global__ void k_sub_certify(const float* __restrict__ xr, uint64_t m, uint32_t d,
+                              const uint32_t* __restrict__ sa, const double* __restrict__ cent,
+                              const unsigned long long* __restrict__ radius,
+                              const uint32_t* __restrict__ sizes_sub, uint32_t csub,
+                              const uint32_t* __restrict__ seg_beg,
+                              const uint32_t* __restrict__ seg_rows,
+                              const uint8_t* __restrict__ open_sub, const uint32_t* __restrict__ ids2,
+                              const double* __restrict__ d2, uint32_t k, uint32_t want,
+                              const uint32_t* __restrict__ members, double rel, double g64,
+                              uint32_t KP, uint32_t* cand_ids, float* cand_lb, uint32_t* cand_cnt,
+                              unsigned long long* n_cert) {
+  const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (v >= m || open_sub[v]) return;
+  if (ids2[v * k + want - 1] == 0xFFFFFFFFu) return;  // sub-cluster smaller than the list
+  const double kth = d2[v * k + want - 1];
+  const uint32_t S = sa[v];
+  const float* row = xr + v * d;
+  for (uint32_t T = 0; T < csub; ++T) {
+    if (T == S || sizes_sub[T] == 0) continue;
+    double gap;
+    if (sizes_sub[T] <= 64) {  // small sub-cluster: its members directly
+      double best = __longlong_as_double(0x7ff0000000000000ll);
+      for (uint32_t e = 0; e < sizes_sub[T]; ++e) {
+        const float* o = xr + (uint64_t)seg_rows[seg_beg[T] + e] * d;
+        double acc = 0.0;
+        for (uint32_t j = 0; j < d; ++j) {
+          const double t = (double)row[j] - (double)o[j];
+          acc = fma(t, t, acc);
+        }
+        best = fmin(best, acc);
+      }
+      gap = sqrt(best) * (1.0 - rel);
+    } else {
+      const double D = dist_to(row, cent + (uint64_t)T * d, d) * (1.0 - rel);
+      const double R = __longlong_as_double((long long)radius[T]);
+      gap = fmax(D - R, 0.0);
+    }
+    if (!(gap * gap * (1.0 - g64) * (1.0 - 1e-12) > kth)) return;
+  }
+  const uint64_t g = members[v];
+  for (uint32_t i = 0; i < want; ++i) cand_ids[g * KP + i] = members[ids2[v * k + i]];
+  cand_cnt[g] = want;
+  cand_lb[g] = __int_as_float(0x7f800000);
+  atomicAdd(n_cert, 1ull);
+}
+
+__global__ void k_mark_rows(const uint32_t* list, uint32_t n, uint8_t* mask) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) mask[list[i]] = 1;
 }
 
 // FFMA certificate factor: every excluded candidate's reference distance is
@@ -524,6 +657,219 @@ void ffma_filter(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t
   }
   note_launch(ctx, "k_knn_filter");
   NB_CUDA(cudaStreamSynchronize(S));
+}
+
+// Stage 1b for one cluster (members[0..m)): returns the rows it certified.
+uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+                          uint64_t m, uint32_t k, int KP, DBuf<uint32_t>& cid, DBuf<float>& clb,
+                          DBuf<uint32_t>& ccnt) {
+  cudaStream_t S = ctx->stream;
+  DBuf<float> xr(m * d);
+  k_gather_rows<<<ctx->sm_count * 8, 256, 0, S>>>(x, members, m, (uint32_t)d, xr.p);
+  note_launch(ctx, "k_gather_rows");
+  // Sub-clusters by recursive bisection: a segment is split by 2-means
+  // (principal-direction initialisation, then Lloyd steps) when the split
+  // removes >= 3 % of the segment's squared error about its mean (in high
+  // dimension, halving one Gaussian blob removes ~0.1 %, separating blobs far
+  // more), or when one side is a small far group (< 5 %: a fragment of
+  // another blob, peeled off); otherwise it is kept whole. Well-separated blobs end up one per
+  // sub-cluster (a split blob would leave its points without a geometric
+  // certificate, a merged pair without a tight tensor-core one). Any
+  // partition is valid for the certificate; this only decides how many rows
+  // it settles.
+  const double rel = (double)(d + 8) * 0x1p-52;
+  // 2-means of one index list, initialised by its principal direction
+  // (PDDP), then Lloyd steps with exact means; returns false when the split
+  // removes < 3 % of the squared error about the mean (one blob) or is
+  // degenerate.
+  auto bisect = [&](const std::vector<uint32_t>& seg, std::vector<uint32_t>& a0,
+                    std::vector<uint32_t>& a1) -> bool {
+    const uint64_t c = seg.size();
+    DBuf<uint32_t> ix(c);
+    DBuf<uint8_t> lab(c);
+    DBuf<double> cen(2 * d), sse(2);
+    NB_CUDA(cudaMemcpyAsync(ix.p, seg.data(), c * 4, cudaMemcpyHostToDevice, S));
+    seq_column_means(ctx, xr.p, d, ix.p, {0}, {c}, {0}, cen.p);
+    const unsigned gb = (unsigned)((c + 127) / 128);
+    // parent error: everyone to the mean (cen[1] := cen[0] for this pass)
+    NB_CUDA(cudaMemcpyAsync(cen.p + d, cen.p, d * 8, cudaMemcpyDeviceToDevice, S));
+    NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
+    k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p);
+    double ps[2];
+    NB_CUDA(cudaMemcpyAsync(ps, sse.p, 16, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    const double parent = ps[0] + ps[1];
+    // principal direction of the segment (8 power steps from a fixed start);
+    // the initial centres are the means of the two sides of a cut across it
+    {
+      DBuf<double> vd(d), yd(d), td(c);
+      std::vector<double> vh(d);
+      HostRng g(0x70646470 /* "pddp" */);
+      for (auto& e : vh) e = g.gaussian();
+      for (int it = 0; it < 8; ++it) {
+        double nrm = 0.0;
+        for (double e : vh) nrm += e * e;
+        nrm = std::sqrt(nrm);
+        if (!(nrm > 0.0)) return false;
+        for (auto& e : vh) e /= nrm;
+        NB_CUDA(cudaMemcpyAsync(vd.p, vh.data(), d * 8, cudaMemcpyHostToDevice, S));
+        k_proj_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, vd.p, td.p);
+        NB_CUDA(cudaMemsetAsync(yd.p, 0, d * 8, S));
+        k_backproj_idx<<<dim3((unsigned)((d + 127) / 128), 64), 128, 0, S>>>(xr.p, ix.p, c,
+                                                                          (uint32_t)d, cen.p,
+                                                                          td.p, yd.p);
+        NB_CUDA(cudaMemcpyAsync(vh.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
+        NB_CUDA(cudaStreamSynchronize(S));
+      }
+      note_launch(ctx, "k_pddp");
+      std::vector<double> th(c);
+      NB_CUDA(cudaMemcpyAsync(th.data(), td.p, c * 8, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+      // cut at the middle of the projected range: separates a far fragment
+      // (a few rows at one end) as well as two groups of blobs
+      double lo = th[0], hi = th[0];
+      for (double v : th) { lo = std::min(lo, v); hi = std::max(hi, v); }
+      const double cut = 0.5 * (lo + hi);
+      a0.clear();
+      a1.clear();
+      for (uint64_t i = 0; i < c; ++i) (th[i] > cut ? a1 : a0).push_back(seg[i]);
+      if (a0.empty() || a1.empty()) return false;
+      DBuf<uint32_t> o(c);
+      std::vector<uint32_t> both(a0);
+      both.insert(both.end(), a1.begin(), a1.end());
+      NB_CUDA(cudaMemcpyAsync(o.p, both.data(), c * 4, cudaMemcpyHostToDevice, S));
+      seq_column_means(ctx, xr.p, d, o.p, {0, a0.size()}, {a0.size(), a1.size()}, {0, 1}, cen.p);
+      NB_CUDA(cudaStreamSynchronize(S));
+    }
+    std::vector<uint8_t> lh(c);
+    double ss[2] = {0.0, 0.0};
+    for (int it = 0; it < 3; ++it) {
+      NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
+      k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p);
+      NB_CUDA(cudaMemcpyAsync(lh.data(), lab.p, c, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaMemcpyAsync(ss, sse.p, 16, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+      a0.clear();
+      a1.clear();
+      for (uint64_t i = 0; i < c; ++i) (lh[i] ? a1 : a0).push_back(seg[i]);
+      if (a0.empty() || a1.empty()) return false;
+      if (it == 2) break;
+      DBuf<uint32_t> o(c);
+      std::vector<uint32_t> both(a0);
+      both.insert(both.end(), a1.begin(), a1.end());
+      NB_CUDA(cudaMemcpyAsync(o.p, both.data(), c * 4, cudaMemcpyHostToDevice, S));
+      seq_column_means(ctx, xr.p, d, o.p, {0, a0.size()}, {a0.size(), a1.size()}, {0, 1}, cen.p);
+      NB_CUDA(cudaStreamSynchronize(S));
+    }
+    if (std::getenv("NOMAD_B200_DEBUG_KNN"))
+      std::fprintf(stderr, "  bisect %llu rows: parent %.4g split %.4g (%zu / %zu)\n",
+                   (unsigned long long)c, parent, ss[0] + ss[1], a0.size(), a1.size());
+    // a small far group (a fragment of another blob) is peeled off whatever
+    // the error reduction; a balanced split must remove >= 3 %
+    if (std::min(a0.size(), a1.size()) * 20 < c) return true;
+    return ss[0] + ss[1] < 0.97 * parent;
+  };
+  std::vector<std::vector<uint32_t>> done, work;
+  {
+    std::vector<uint32_t> all(m);
+    for (uint64_t i = 0; i < m; ++i) all[i] = (uint32_t)i;
+    work.push_back(std::move(all));
+  }
+  while (!work.empty() && done.size() + work.size() < 256) {
+    std::vector<uint32_t> seg = std::move(work.back());
+    work.pop_back();
+    std::vector<uint32_t> a0, a1;
+    if (seg.size() < 2 || !bisect(seg, a0, a1)) {
+      done.push_back(std::move(seg));
+      continue;
+    }
+    work.push_back(std::move(a0));
+    work.push_back(std::move(a1));
+  }
+  for (auto& w : work) done.push_back(std::move(w));
+  const uint32_t csub = (uint32_t)done.size();
+  if (std::getenv("NOMAD_B200_DEBUG_KNN"))
+    std::fprintf(stderr, "subcluster bisection: m=%llu -> %u segments\n", (unsigned long long)m, csub);
+  if (csub < 2) return 0;
+  // labels, sizes and exact segment means (any centre is valid)
+  std::vector<uint32_t> lab(m), szh(csub);
+  for (uint32_t t = 0; t < csub; ++t) {
+    szh[t] = (uint32_t)done[t].size();
+    for (uint32_t i : done[t]) lab[i] = t;
+  }
+  DBuf<uint32_t> sa(m), ssz(csub), od, segb;
+  DBuf<double> sc((uint64_t)csub * d);
+  NB_CUDA(cudaMemcpyAsync(sa.p, lab.data(), m * 4, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(ssz.p, szh.data(), csub * 4, cudaMemcpyHostToDevice, S));
+  {
+    std::vector<uint32_t> order;
+    std::vector<uint64_t> beg, cnt;
+    std::vector<uint32_t> ids;
+    for (uint32_t t = 0; t < csub; ++t) {
+      beg.push_back(order.size());
+      cnt.push_back(done[t].size());
+      ids.push_back(t);
+      std::vector<uint32_t> sorted = done[t];
+      std::sort(sorted.begin(), sorted.end());
+      order.insert(order.end(), sorted.begin(), sorted.end());
+    }
+    od.alloc(m);
+    NB_CUDA(cudaMemcpyAsync(od.p, order.data(), m * 4, cudaMemcpyHostToDevice, S));
+    seq_column_means(ctx, xr.p, d, od.p, beg, cnt, ids, sc.p);
+    std::vector<uint32_t> b32(beg.begin(), beg.end());
+    segb.alloc(csub);
+    NB_CUDA(cudaMemcpyAsync(segb.p, b32.data(), csub * 4, cudaMemcpyHostToDevice, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+  }
+  DBuf<uint32_t> cid2, ccnt2;
+  DBuf<float> clb2;
+  int KP2 = 0;
+  knn_tc_candidates(ctx, xr.p, m, d, sa.p, csub, true, cid2, clb2, ccnt2, &KP2, nullptr);
+  const uint32_t want = (uint32_t)std::min<uint64_t>(k, m - 1);
+  DBuf<uint32_t> ids2(m * k), fb2(m), nfb2(1);
+  DBuf<double> d2(m * k);
+  NB_CUDA(cudaMemsetAsync(nfb2.p, 0, 4, S));
+  NB_CUDA(cudaMemsetAsync(ids2.p, 0xFF, m * k * 4, S));
+  const unsigned rb = (unsigned)((m * 32 + 255) / 256);
+  k_knn_rerank<64><<<rb, 256, 0, S>>>(xr.p, (uint32_t)d, m, nullptr, nullptr, nullptr, k, want,
+                                      cid2.p, clb2.p, ccnt2.p, nullptr, ids2.p, d2.p, fb2.p,
+                                      nfb2.p, 1.0);
+  note_launch(ctx, "k_knn_rerank");
+  uint32_t nf2 = 0;
+  NB_CUDA(cudaMemcpyAsync(&nf2, nfb2.p, 4, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  DBuf<uint8_t> open(m);
+  NB_CUDA(cudaMemsetAsync(open.p, 0, m, S));
+  if (nf2) {
+    k_mark_rows<<<(nf2 + 255) / 256, 256, 0, S>>>(fb2.p, nf2, open.p);
+    note_launch(ctx, "k_mark_rows");
+  }
+  const double g64 = (double)(d + 1) * 0x1p-53 * 2;
+  DBuf<unsigned long long> rad(csub), ncert(1);
+  NB_CUDA(cudaMemsetAsync(rad.p, 0, csub * 8, S));
+  NB_CUDA(cudaMemsetAsync(ncert.p, 0, 8, S));
+  const unsigned mb = (unsigned)((m + 127) / 128);
+  k_sub_radius<<<mb, 128, 0, S>>>(xr.p, m, (uint32_t)d, sa.p, sc.p, rel, rad.p);
+  note_launch(ctx, "k_sub_radius");
+  k_sub_certify<<<mb, 128, 0, S>>>(xr.p, m, (uint32_t)d, sa.p, sc.p, rad.p, ssz.p, csub, segb.p,
+                                   od.p, open.p,
+                                   ids2.p, d2.p, k, want, members, rel, g64, (uint32_t)KP, cid.p,
+                                   clb.p, ccnt.p, ncert.p);
+  note_launch(ctx, "k_sub_certify");
+  unsigned long long nc = 0;
+  NB_CUDA(cudaMemcpyAsync(&nc, ncert.p, 8, cudaMemcpyDeviceToHost, S));
+  NB_CUDA(cudaStreamSynchronize(S));
+  if (std::getenv("NOMAD_B200_DEBUG_KNN")) {
+    std::fprintf(stderr, "subcluster stage: m=%llu csub=%u open-within=%u certified=%llu sizes:",
+                 (unsigned long long)m, csub, nf2, nc);
+    for (uint32_t t = 0; t < csub; ++t) std::fprintf(stderr, " %u", szh[t]);
+    std::vector<unsigned long long> rh(csub);
+    NB_CUDA(cudaMemcpy(rh.data(), rad.p, csub * 8, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, " radii:");
+    for (uint32_t t = 0; t < csub; ++t) { double r; std::memcpy(&r, &rh[t], 8); std::fprintf(stderr, " %.1f", r); }
+    std::fprintf(stderr, "\n");
+  }
+  return nc;
 }
 
 // own: nullptr = every cluster; else own[r] != 0 for the clusters whose lists
@@ -612,15 +958,43 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
                       &KP, own);
     nf = rerank();
     R.tc_uncertified = nf;
-    if (nf && mode == NOMAD_B200_KNN_EXACT) {
-      // stage 2: clusters where many rows failed the tensor-core certificate
-      // (large norms -> loose accumulation bound) get the FFMA filter, whose
-      // error is relative to the distance itself.
-      std::vector<uint32_t> fbh(nf), ah(n);
-      NB_CUDA(cudaMemcpy(fbh.data(), fb.p, nf * 4, cudaMemcpyDeviceToHost));
-      NB_CUDA(cudaMemcpy(ah.data(), assign_d, n * 4, cudaMemcpyDeviceToHost));
-      std::vector<uint64_t> fail_per(C, 0);
+    std::vector<uint32_t> ah;
+    auto failures = [&](std::vector<uint32_t>& fbh, std::vector<uint64_t>& fail_per) {
+      fbh.resize(nf);
+      if (nf) NB_CUDA(cudaMemcpy(fbh.data(), fb.p, nf * 4, cudaMemcpyDeviceToHost));
+      if (ah.empty()) {
+        ah.resize(n);
+        NB_CUDA(cudaMemcpy(ah.data(), assign_d, n * 4, cudaMemcpyDeviceToHost));
+      }
+      fail_per.assign(C, 0);
       for (uint32_t q : fbh) ++fail_per[ah[q]];
+    };
+    if (nf && mode == NOMAD_B200_KNN_EXACT) {
+      // stage 1b: clusters where many rows failed the tensor-core certificate
+      // (centred norms >> neighbour distances: the cluster spans several
+      // blobs) are split into sub-clusters; exact lists inside each
+      // sub-cluster come from the certified tensor-core filter on the
+      // sub-cluster's own centring, and a row keeps its list when no other
+      // sub-cluster can hold a closer point (k_sub_certify).
+      std::vector<uint32_t> fbh;
+      std::vector<uint64_t> fail_per;
+      failures(fbh, fail_per);
+      uint64_t certified = 0;
+      for (uint32_t r = 0; r < C; ++r) {
+        const uint64_t sz = off[r + 1] - off[r];
+        if (sz < 1024 || own && !(*own)[r] || fail_per[r] * 16 < sz) continue;
+        certified += subcluster_stage(ctx, x, d, mem.p + off[r], sz, k, KP, cid, clb, ccnt);
+      }
+      R.sub_certified = certified;
+      if (certified) nf = rerank();
+    }
+    if (nf && mode == NOMAD_B200_KNN_EXACT) {
+      // stage 2: rows still open (both certificates failed) get the FFMA
+      // filter against their whole cluster, whose error is relative to the
+      // distance itself.
+      std::vector<uint32_t> fbh;
+      std::vector<uint64_t> fail_per;
+      failures(fbh, fail_per);
       // only the open rows are re-filtered (against their whole cluster);
       // clusters with a handful of open rows go straight to the exhaustive pass
       std::vector<uint64_t> qoff(C + 1, 0);
@@ -763,6 +1137,7 @@ static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     KnnResult R;
     build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R, knn_mode, owned ? &own : nullptr);
     ctx->knn_tc_uncertified = R.tc_uncertified;
+    ctx->knn_sub_certified = R.sub_certified;
     ctx->knn_exhaustive = R.fallbacks;
     const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
                                                          : cudaMemcpyDeviceToHost;
@@ -878,6 +1253,13 @@ int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
     if (!ctx) fail(kParameter, "NULL argument");
     if (tc_uncertified) *tc_uncertified = ctx->knn_tc_uncertified;
     if (exhaustive_rows) *exhaustive_rows = ctx->knn_exhaustive;
+  });
+}
+
+int32_t nomad_b200_knn_subcluster_rows(nomad_b200_ctx* ctx, uint64_t* rows) {
+  return guard([&] {
+    if (!ctx || !rows) fail(kParameter, "NULL argument");
+    *rows = ctx->knn_sub_certified;
   });
 }
 

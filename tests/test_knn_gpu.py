@@ -108,3 +108,23 @@ def test_knn_shard_owned_clusters(port, ctx, mode):
     for i in np.nonzero(mine)[0][:500]:
         assert np.array_equal(part.neighbors_of(i), full.neighbors_of(i))
     assert nb.build_knn(x, ca, 15, mode=mode, ctx=ctx, owned_clusters=[]).offsets[-1] == 0
+
+
+def test_knn_subcluster_stage_certifies_blobs(port, ctx):
+    """One cluster holding three far-apart blobs: the fp16 certificate on the
+    cluster's centring fails, the sub-cluster stage (bisection into the
+    blobs, certified tensor-core lists inside each, geometric bound across)
+    settles almost every row; the graph is still bit-identical."""
+    import paper_2505_15511_b200 as nb
+    from oracle import Clusters
+    x = port.gaussian_mixture(9000, 48, 3, 60.0, 5)
+    a = np.zeros(len(x), np.uint32)
+    cl = Clusters(a, np.zeros(48), np.array([len(x)], np.uint32), 1, 48)
+    g = port.build_knn(x, cl, 15)
+    gg = _gpu_graph(nb, ctx, x, cl, 15, "exact")
+    tc_open, _ = ctx.knn_stats()
+    assert tc_open > 0.5 * len(x)
+    assert ctx.knn_subcluster_rows() > 0.9 * tc_open
+    assert np.array_equal(gg.offsets, g.offsets)
+    assert np.array_equal(gg.neighbors, g.neighbors)
+    assert np.array_equal(gg.distances, g.distances)

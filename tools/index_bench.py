@@ -44,6 +44,7 @@ def main():
         e = time.perf_counter() - s
         res[f"knn_{m}_s"] = e
         res[f"knn_{m}_tc_uncertified_exhaustive"] = list(ctx.knn_stats())
+        res[f"knn_{m}_subcluster_rows"] = ctx.knn_subcluster_rows()
         res[f"knn_{m}_tflops_equiv"] = 2 * pairs * a.d / e / 1e12
     if a.recall and "bf16" in graphs and "exact" in graphs:
         ge, gf = graphs["exact"], graphs["bf16"]
