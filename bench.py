@@ -176,7 +176,8 @@ def main():
     ap.add_argument("--graph", choices=["knn", "synthetic"], default="knn",
                     help="knn: full GPU index build (lsh_init -> kmeans_em -> build_knn) on "
                          "device-generated data; synthetic: random within-cluster graph")
-    ap.add_argument("--knn-mode", choices=["bf16", "exact"], default="bf16")
+    ap.add_argument("--knn-mode", choices=["bf16", "exact"], default="exact",
+                    help="exact: the reference's kNN graph bit for bit (default); bf16: fast mode")
     ap.add_argument("--recall-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=2)
