@@ -40,6 +40,9 @@
 #ifndef HOG_PF
 #define HOG_PF 1          // 1: next head's draws + neighbour ids issued before this head's math
 #endif
+#ifndef HOG_LATE
+#define HOG_LATE 0        // 1: neighbour/tail rows prefetched to L1, loaded after the mean field
+#endif
 #ifndef HOG_MF2
 #define HOG_MF2 0         // 1: two independent mean-field accumulator sets
 #endif
@@ -264,6 +267,17 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #pragma unroll
       for (int m = 0; m < TPL; ++m)
         pt[m] = (act && gl + G * m < (int)s) ? sm_row<DF>(rbase + (1 + NPL + m) * 256) : h;
+#elif HOG_LATE
+      // ---- head row now; neighbour / tail rows prefetched into L1 now and
+      // loaded after the mean field (no registers held across it)
+      const double2 h = ld_row<DF>(P.pos, head);
+      double2 pn[NPL], pt[TPL];
+#pragma unroll
+      for (int i = 0; i < NPL; ++i)
+        if (NPL * gl + i < (int)cnt) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pos + D.nb[i]));
+#pragma unroll
+      for (int m = 0; m < TPL; ++m)
+        if (act && gl + G * m < (int)s) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pos + D.tl[m]));
 #else
       // ---- gathers (all issued before any use)
       const double2 h = ld_row<DF>(P.pos, head);
@@ -325,6 +339,11 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #if HOG_SROWS
       // next head's rows stream in behind the rest of this head's math
       if (more) issue_rows(Dn, buf ^ 1);
+#elif HOG_LATE
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row<DF>(P.pos, D.nb[i]) : h;
+#pragma unroll
+      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row<DF>(P.pos, D.tl[m]) : h;
 #endif
       // ---- sampled negatives
       double qn[TPL], qsum = 0.0;
