@@ -231,11 +231,25 @@ def main():
         torch.cuda.empty_cache()
         a, offsets, nb = cl.assignment, g.offsets, g.neighbors
         init = np.random.default_rng(1234).standard_normal((n, 2))
+        # the kNN build as a tensor contraction: 2 d sum_r s_r^2 flop-equivalents
+        # over the build time, against the measured bf16 peak (the fp16 stage
+        # of the exact mode runs at the same tensor rate)
+        pairs = float(sum(int(z) * int(z) for z in cl.sizes))
+        kflops = 2.0 * d * pairs / max(t_d - t_c, 1e-9) / 1e12
+        kpeak = None
+        pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(pk):
+            kpeak = json.load(open(pk)).get("bf16_tflops")
+        index_roof = {"bound": "tensor", "achieved": kflops, "peak": kpeak, "unit": "TFLOP/s",
+                      "frac": kflops / kpeak if kpeak else None,
+                      "what": f"build_knn ({args.knn_mode}) wall time, 2*d*sum(size^2) "
+                              "flop-equivalents, peak = measured bf16 (burst)"}
         index = {"knn_recall_at_15": {"value": recall, "sample_rows": args.recall_sample,
                                       "mode": args.knn_mode, "vs": "exact fp64 (exhaustive)"},
                  "lsh_init_s": round(t_b - t_a, 3), "kmeans_em_s": round(t_c - t_b, 3),
                  "build_knn_s": round(t_d - t_c, 3), "knn_mode": args.knn_mode,
-                 "cluster_sizes_min_max": [int(cl.sizes.min()), int(cl.sizes.max())]}
+                 "cluster_sizes_min_max": [int(cl.sizes.min()), int(cl.sizes.max())],
+                 "knn_roofline": index_roof}
     else:
         a, offsets, nb, init = synthetic_index(n, ncl, k)
     nid = nid64 = None
