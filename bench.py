@@ -234,7 +234,8 @@ def main():
         # the kNN build as a tensor contraction: 2 d sum_r s_r^2 flop-equivalents
         # over the build time, against the measured bf16 peak (the fp16 stage
         # of the exact mode runs at the same tensor rate)
-        pairs = float(sum(int(z) * int(z) for z in cl.sizes))
+        sel = range(ncl) if owned is None else owned
+        pairs = float(sum(int(cl.sizes[r]) ** 2 for r in sel))
         kflops = 2.0 * d * pairs / max(t_d - t_c, 1e-9) / 1e12
         kpeak = None
         pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
