@@ -222,6 +222,14 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
                                              const double* layout, int32_t layout_location,
                                              uint64_t k, uint64_t sample, uint64_t seed,
                                              double* value, double* std_error);
+/* metrics.hpp:174-200 neighborhood_preservation_ann on the GPU: high-d
+ * neighbourhoods from a prebuilt within-cluster graph (first min(k, |list|)
+ * ids), exact 2-D neighbours of every row on the device; bit-identical value.
+ * 1 <= k <= 56, k < rows. */
+int32_t nomad_b200_neighborhood_preservation_ann(nomad_b200_ctx* ctx,
+                                                 const nomad_b200_graph* graph,
+                                                 const double* layout, int32_t layout_location,
+                                                 uint64_t k, double* value);
 /* metrics.hpp:205-243 random_triplet_accuracy on the GPU: triplets drawn on
  * the host from the reference stream stream_seed(seed, "tri"), distances and
  * the agreement count on the device; bit-identical value / std_error. */

@@ -141,6 +141,8 @@ class Oracle:
             self._tri = fn("random_triplet_accuracy", C.c_int,
                            [f32p, C.c_uint64, C.c_uint64, f64p, C.c_uint64, C.c_uint64, f64p,
                             f64p])
+            self._npann = fn("neighborhood_preservation_ann", C.c_int,
+                             [C.c_uint64, u32p, u32p, f64p, C.c_uint64, f64p])
             self._save = fn("save_layout", C.c_int, [C.c_char_p, f64p, C.c_uint64, C.c_void_p,
                                                      C.c_void_p])
             self._loadraw = fn("load_vectors_raw", C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64,
@@ -324,6 +326,18 @@ class Oracle:
         self._check(self._np(_p(x, C.c_float), x.shape[0], x.shape[1], _p(lay, C.c_double), k,
                              sample, seed, _p(v, C.c_double), _p(se, C.c_double)))
         return float(v[0]), float(se[0])
+
+    def neighborhood_preservation_ann(self, offsets, neighbors, layout, k=10):
+        """metrics.hpp:174-200 (reference library only)."""
+        off = np.ascontiguousarray(offsets, np.uint32)
+        nb = np.ascontiguousarray(neighbors, np.uint32)
+        if nb.size == 0:
+            nb = np.zeros(1, np.uint32)
+        lay = np.ascontiguousarray(layout, np.float64)
+        v = np.zeros(1)
+        self._check(self._npann(len(off) - 1, _p(off, C.c_uint32), _p(nb, C.c_uint32),
+                                _p(lay, C.c_double), k, _p(v, C.c_double)))
+        return float(v[0])
 
     def save_layout(self, layout, path, ids=None, labels=None):
         """dataset.hpp:223-250 (reference library only)."""

@@ -389,6 +389,25 @@ int ref_neighborhood_preservation(const float* data, uint64_t n, uint64_t d,
   } catch (const nomad::Error& e) { return fail_code(e); }
 }
 
+// metrics.hpp:174-200 neighborhood_preservation_ann (graph CSR, layout n x 2)
+int ref_neighborhood_preservation_ann(uint64_t n, const uint32_t* offsets,
+                                      const uint32_t* neighbors, const double* layout, uint64_t k,
+                                      double* value) {
+  try {
+    nomad::KnnGraph g;
+    g.rows = n;
+    g.k = k;
+    g.offsets.assign(offsets, offsets + n + 1);
+    g.neighbors.assign(neighbors, neighbors + offsets[n]);
+    g.distances.assign(offsets[n], 0.0);
+    nomad::LayoutMatrix l;
+    l.rows = n;
+    l.positions.assign(layout, layout + 2 * n);
+    *value = nomad::neighborhood_preservation_ann(g, l, k).value;
+    return 0;
+  } catch (const nomad::Error& e) { return fail_code(e); }
+}
+
 int ref_random_triplet_accuracy(const float* data, uint64_t n, uint64_t d,
                                 const double* layout, uint64_t count, uint64_t seed,
                                 double* value, double* std_error) {

@@ -88,6 +88,9 @@ _SIGS = {
                                                          C.c_uint64, C.c_uint64, C.c_uint64,
                                                          C.POINTER(C.c_double),
                                                          C.POINTER(C.c_double)]),
+    "nomad_b200_neighborhood_preservation_ann": (C.c_int32, [_vp, C.POINTER(GraphView), _vp,
+                                                             C.c_int32, C.c_uint64,
+                                                             C.POINTER(C.c_double)]),
     "nomad_b200_random_triplet_accuracy": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp, C.c_int32,
                                                        C.c_uint64, C.c_uint64,
                                                        C.POINTER(C.c_double),

@@ -360,6 +360,21 @@ def neighborhood_preservation(data, layout, k: int = 10, sample: int = 0, seed: 
     return v.value, se.value
 
 
+def neighborhood_preservation_ann(graph: KnnGraph, layout, k: int = 10,
+                                  ctx: Optional[Context] = None) -> float:
+    """metrics.hpp:174-200 on the GPU (graph neighbourhoods vs exact 2-D), bit-identical."""
+    off = np.ascontiguousarray(graph.offsets, np.uint32)
+    nb_ = np.ascontiguousarray(graph.neighbors, np.uint32)
+    if nb_.size == 0:
+        nb_ = np.zeros(1, np.uint32)
+    gv = N.GraphView(graph.rows, graph.k, off.ctypes.data, nb_.ctypes.data, None, N.HOST)
+    lp, lloc, lkeep = _view(layout, np.float64)
+    v = C.c_double()
+    check(lib().nomad_b200_neighborhood_preservation_ann(_ctx(ctx).h, C.byref(gv), lp, lloc, k,
+                                                         C.byref(v)))
+    return v.value
+
+
 def random_triplet_accuracy(data, layout, count: int = 100000, seed: int = 0,
                             ctx: Optional[Context] = None):
     """metrics.hpp:205-243 on the GPU -> (value, std_error), bit-identical."""

@@ -1,5 +1,6 @@
 // Final-map quality metrics on the GPU (metrics.hpp:113-243):
-// neighbourhood preservation NP@k and random-triplet accuracy.
+// neighbourhood preservation NP@k (exact, and NP-ann against a prebuilt
+// graph) and random-triplet accuracy.
 //
 // Both keep the reference's sampling streams (drawn on the host with the
 // reference Rng: stream_seed(seed, "np") partial Fisher-Yates, :127-136;
@@ -229,6 +230,72 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
       }
       if (std_error) *std_error = se;
     }
+  });
+}
+
+int32_t nomad_b200_neighborhood_preservation_ann(nomad_b200_ctx* ctx,
+                                                 const nomad_b200_graph* graph,
+                                                 const double* layout, int32_t layout_location,
+                                                 uint64_t k, double* value) {
+  return guard([&] {
+    if (!ctx || !graph || !value || !graph->offsets) fail(kParameter, "NULL argument");
+    bind_device(ctx);
+    cudaStream_t S = ctx->stream;
+    const uint64_t n = graph->rows;
+    if (k >= n) fail(kParameter, "k must be < n");
+    if (k < 1 || k > (uint64_t)LKMAX)
+      fail(kParameter, "GPU neighborhood_preservation_ann supports 1 <= k <= 56");
+    if (n >= 0xFFFFFFFFull) fail(kSize, "point ids are u32 (n < 2^32)");
+    DevLayout L;
+    L.bind(layout, layout_location, n, S);
+    // graph lists on the host (the intersection runs there, in row order)
+    std::vector<uint32_t> off(n + 1), nbh;
+    const bool dev = graph->location == NOMAD_B200_DEVICE;
+    NB_CUDA(cudaMemcpy(off.data(), graph->offsets, (n + 1) * 4,
+                       dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    nbh.resize(std::max<uint64_t>(off[n], 1));
+    if (off[n])
+      NB_CUDA(cudaMemcpy(nbh.data(), graph->neighbors, (uint64_t)off[n] * 4,
+                         dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    // exact 2-D neighbours of every row (metrics.hpp:187-189), in row batches
+    const uint64_t B = 1ull << 22;
+    DBuf<uint32_t> ql(std::min(B, n)), lo_ids(std::min(B, n) * k);
+    std::vector<uint32_t> lh, idx(std::min(B, n));
+    double sum = 0.0;
+    for (uint64_t r0 = 0; r0 < n; r0 += B) {
+      const uint32_t m = (uint32_t)std::min(B, n - r0);
+      for (uint32_t v = 0; v < m; ++v) idx[v] = (uint32_t)(r0 + v);
+      NB_CUDA(cudaMemcpyAsync(ql.p, idx.data(), (uint64_t)m * 4, cudaMemcpyHostToDevice, S));
+      const uint32_t bx = (m + 127) / 128;
+      uint32_t P = 1;
+      while (P < 64 && bx * P < 4 * (uint32_t)ctx->sm_count && n / (2 * P) >= 4096) P *= 2;
+      DBuf<double> pd((uint64_t)m * P * k);
+      DBuf<uint32_t> pi((uint64_t)m * P * k);
+      k_np_low_partial<<<dim3(bx, P), 128, 0, S>>>(L.p, n, ql.p, m, (uint32_t)k, P, pd.p, pi.p);
+      note_launch(ctx, "k_np_low_partial");
+      k_np_low_merge<<<(m + 127) / 128, 128, 0, S>>>(m, (uint32_t)k, P, pd.p, pi.p, lo_ids.p);
+      note_launch(ctx, "k_np_low_merge");
+      lh.resize((uint64_t)m * k);
+      NB_CUDA(cudaMemcpyAsync(lh.data(), lo_ids.p, lh.size() * 4, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+      std::vector<uint32_t> hi;
+      for (uint32_t v = 0; v < m; ++v) {  // metrics.hpp:182-191, row order
+        const uint64_t i = r0 + v;
+        const uint64_t have = std::min<uint64_t>(k, off[i + 1] - off[i]);
+        hi.assign(nbh.begin() + off[i], nbh.begin() + off[i] + have);
+        std::sort(hi.begin(), hi.end());
+        uint32_t* b = lh.data() + (uint64_t)v * k;
+        std::sort(b, b + k);
+        uint64_t count = 0, ia = 0, ib = 0;
+        while (ia < hi.size() && ib < k) {
+          if (hi[ia] < b[ib]) ++ia;
+          else if (b[ib] < hi[ia]) ++ib;
+          else ++count, ++ia, ++ib;
+        }
+        sum += static_cast<double>(count) / static_cast<double>(k);
+      }
+    }
+    *value = sum / static_cast<double>(n);
   });
 }
 

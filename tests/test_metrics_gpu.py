@@ -56,3 +56,21 @@ def test_metric_errors(ctx, data):
         nb.random_triplet_accuracy(x[:2], lay[:2], 10, ctx=ctx)  # n < 3
     with pytest.raises(nb.NomadError):
         nb.random_triplet_accuracy(x, lay, 0, ctx=ctx)
+
+
+@pytest.mark.parametrize("k", [5, 10, 15])
+def test_np_ann_bit_exact(ref, ctx, port, k):
+    """NP-ann (graph neighbourhoods vs exact 2-D), incl. ragged lists and a
+    singleton cluster (empty list)."""
+    import paper_2505_15511_b200 as nb
+    from common import index_case
+    x, c, g, _ = index_case(3000, 32, 10, 8, 15)
+    lay = np.random.default_rng(k).normal(size=(3000, 2))
+    v = nb.neighborhood_preservation_ann(nb.KnnGraph(3000, 15, g.offsets, g.neighbors, g.distances),
+                                         lay, k, ctx=ctx)
+    assert v == ref.neighborhood_preservation_ann(g.offsets, g.neighbors, lay, k)
+    off = np.concatenate([[0], np.cumsum(np.arange(300) % 4)]).astype(np.uint32)
+    nbr = (np.arange(off[-1]) * 7 % 300).astype(np.uint32)
+    lay2 = np.round(np.random.default_rng(1).normal(size=(300, 2)), 1)  # ties in 2-D
+    v2 = nb.neighborhood_preservation_ann(nb.KnnGraph(300, 3, off, nbr, np.zeros(0)), lay2, k, ctx=ctx)
+    assert v2 == ref.neighborhood_preservation_ann(off, nbr, lay2, k)
