@@ -36,6 +36,8 @@ CONFIGS = {
     "C": (10_000_000, 768, 64, 64, 8),
     "B": (1_000_000, 768, 64, 8, 8),
     "A": (20_000, 64, 10, 5, 1),
+    # one rank's share of config C at N=8 (per-rank scaling diagnostic)
+    "C8": (1_250_000, 768, 8, 8, 1),
 }
 
 

@@ -11,17 +11,23 @@ namespace nb {
 
 // ------------------------------------------------------- K8r replay kernel
 //
-// One CTA per local worker. The host turned the worker's mt19937_64 draw
-// stream into a tape and grouped draws into wavefront levels: draws of one
-// level touch pairwise-disjoint points, and every draw comes after all
-// earlier draws (in sequential order t) that touch any of its points. So
-// executing level by level, with a CTA barrier between levels, performs
-// exactly the reference's sequential per-worker update sequence
-// (optimizer.hpp:253-304). Each draw runs the reference arithmetic in its
-// op order with _rn intrinsics (no FMA), so positions are bit-identical.
+// P.replay_ctas CTAs per local worker (a cooperative launch, so all are
+// resident). The host turned the worker's mt19937_64 draw stream into a tape
+// and grouped draws into wavefront levels: draws of one level touch
+// pairwise-disjoint points, and every draw comes after all earlier draws (in
+// sequential order t) that touch any of its points. So executing level by
+// level — the worker's CTAs split a level's draws, then meet at a per-worker
+// barrier in global memory — performs exactly the reference's sequential
+// per-worker update sequence (optimizer.hpp:253-304). Positions are read
+// through L2 (ld.global.cg), so a CTA sees the previous level's updates made
+// on other SMs. Each draw runs the reference arithmetic in its op order with
+// _rn intrinsics (no FMA), so positions are bit-identical.
+__device__ __forceinline__ double2 ldpos(const double2* p) { return __ldcg(p); }
+
 __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
   extern __shared__ __align__(16) double sm[];
-  const uint32_t w = blockIdx.x;
+  const uint32_t K = P.replay_ctas ? P.replay_ctas : 1;
+  const uint32_t w = blockIdx.x / K, part = blockIdx.x % K;
   const WorkerDev W = P.workers[w];
   const uint32_t k = P.k, s = P.s, C = P.n_clusters;
   // shared tables: weights (k+1)*k, then means/probs of all C cells
@@ -39,11 +45,11 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
   const uint32_t stride = 2 + k + s;
   for (uint32_t L = 0; L < nlev; ++L) {
     const uint32_t b = P.lvl_off[lvl0 + L], e = P.lvl_off[lvl0 + L + 1];
-    for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    for (uint32_t i = b + part * blockDim.x + threadIdx.x; i < e; i += K * blockDim.x) {
       const uint32_t head = P.tape_head[i];
       const uint32_t* tails = P.tape_tails + (size_t)i * s;
       const uint32_t t = P.tape_t[i];
-      const double2 h = P.pos[head];
+      const double2 h = ldpos(P.pos + head);
       // noise terms (objective.hpp:113-145)
       uint32_t own = 0;
       double lm = W.local_mass;
@@ -63,7 +69,7 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
       const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
       double qsum = 0.0;
       for (uint32_t q = 0; q < s; ++q) {
-        const double2 o = P.pos[tails[q]];
+        const double2 o = ldpos(P.pos + tails[q]);
         qsum = __dadd_rn(qsum, cauchy_rn(h.x, h.y, o.x, o.y));
       }
       const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
       double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
       double gn[2 * 64];
       for (uint32_t j = 0; j < cnt; ++j) {
-        const double2 o = P.pos[nb[j]];
+        const double2 o = ldpos(P.pos + nb[j]);
         const double q = cauchy_rn(h.x, h.y, o.x, o.y);
         const double wj = wrow[j];
         const double qb = __dadd_rn(q, bg);
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
       // negative repulsion (objective.hpp:216-226)
       double gm[2 * 16];
       for (uint32_t q = 0; q < s; ++q) {
-        const double2 o = P.pos[tails[q]];
+        const double2 o = ldpos(P.pos + tails[q]);
         const double qn = cauchy_rn(h.x, h.y, o.x, o.y);
         const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
         const double dx = __dsub_rn(h.x, o.x), dy = __dsub_rn(h.y, o.y);
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
       const double st = P.step;
       uint32_t u = 0;
       auto apply = [&](uint32_t p, double ax, double ay) {
-        double2 v = P.pos[p];
+        double2 v = ldpos(P.pos + p);
         v.x = __dsub_rn(v.x, __dmul_rn(st, ax));
         v.y = __dsub_rn(v.y, __dmul_rn(st, ay));
         P.pos[p] = v;
@@ -133,7 +139,19 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
         for (uint32_t q = 0; q < s; ++q) apply(tails[q], gm[2 * q], gm[2 * q + 1]);
       }
     }
+    // level barrier across the worker's CTAs
     __syncthreads();
+    if (K > 1) {
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(P.replay_bar + w, 1u);
+        const uint32_t target = (L + 1) * K;
+        while (*reinterpret_cast<volatile uint32_t*>(P.replay_bar + w) < target) {
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -274,10 +292,27 @@ __global__ void k_gather_layout(const double2* in, const uint32_t* orig_of, uint
 
 static unsigned blocks_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
 
+uint32_t replay_ctas_per_worker(uint32_t n_workers, size_t smem, int sm_count) {
+  if (smem > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(k_sgd_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sgd_replay, 256, smem));
+  const uint32_t resident = (uint32_t)std::max(per_sm, 1) * (uint32_t)sm_count;
+  return std::max<uint32_t>(1, std::min<uint32_t>(32, resident / std::max<uint32_t>(n_workers, 1)));
+}
+
 void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(k_sgd_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_sgd_replay<<<n_workers, 256, smem, st>>>(P);
+  if (P.replay_ctas > 1) {
+    NB_CUDA(cudaMemsetAsync(P.replay_bar, 0, n_workers * sizeof(uint32_t), st));
+    SgdParams Pc = P;
+    void* args[] = {&Pc};
+    NB_CUDA(cudaLaunchCooperativeKernel((const void*)k_sgd_replay, dim3(n_workers * P.replay_ctas),
+                                        dim3(256), args, smem, st));
+  } else {
+    k_sgd_replay<<<n_workers, 256, smem, st>>>(P);
+  }
 }
 
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,

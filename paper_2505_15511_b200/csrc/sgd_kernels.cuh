@@ -50,6 +50,8 @@ struct SgdParams {
   int f64_rows;                 // hogwild: 1 = f64 rows (2 RED.F64), 0 = double-float rows
   uint32_t rowbuf_off;          // hogwild: shared-memory row buffer offset (doubles)
   uint32_t max_cells;           // hogwild: capacity of the shared cell table
+  uint32_t replay_ctas;         // replay: CTAs per worker (level barrier in global memory)
+  uint32_t* replay_bar;         // replay: per-worker barrier counters
   double step;
   uint64_t epoch;
   uint32_t seed_lo, seed_hi;
@@ -69,6 +71,7 @@ struct SgdParams {
 
 // Host launchers (sgd.cu).
 void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cudaStream_t st);
+uint32_t replay_ctas_per_worker(uint32_t n_workers, size_t smem, int sm_count);
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
                      double* out, cudaStream_t st);
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st);

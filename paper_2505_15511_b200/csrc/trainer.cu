@@ -9,10 +9,13 @@
 #include <algorithm>
 #include <atomic>
 #include <thread>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <numeric>
 #include <random>
 
@@ -88,6 +91,8 @@ struct nomad_b200_trainer {
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
   uint32_t hog_cells = 0;  // capacity of the hogwild kernel's shared cell table
+  uint32_t replay_k = 0;   // replay: CTAs per worker
+  DBuf<uint32_t> replay_bar;
   uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0;
   DBuf<uint32_t> chunk_counter;
 
@@ -515,7 +520,6 @@ struct nomad_b200_trainer {
     std::vector<std::vector<uint32_t>> loffw(nwl);
     std::vector<uint32_t> maxl(nwl, 0);
     std::vector<uint64_t> edg(nwl, 0);
-    std::vector<uint32_t> last(orig_of.size(), 0);  // disjoint point ranges per worker
     auto one = [&](uint32_t wl) {
       const WorkerDev& d = wk[wl];
       const uint32_t D = d.draws;
@@ -524,6 +528,7 @@ struct nomad_b200_trainer {
       uint64_t edges = 0;
       auto& g = rng[wl];
       const uint32_t* pool = pool_h.data() + pool_off[wl];
+      // pass 1: the stream's draws (optimizer.hpp:254-255, :284-285)
       for (uint32_t t = 0; t < D; ++t) {
         const uint32_t h = elig_h[d.elig_off + uniform_index(g, d.n_elig)];
         head[t] = h;
@@ -537,19 +542,45 @@ struct nomad_b200_trainer {
         } else {
           for (uint64_t q = 0; q < s; ++q) tails[(size_t)t * s + q] = pool[uniform_index(g, pn)];
         }
-        // level = 1 + max level of every point it reads or writes
-        const uint32_t cnt = ncnt_h[h];
-        const uint32_t* nb = ell_h.data() + (size_t)h * kpad;
-        uint32_t L = last[h];
-        for (uint32_t j = 0; j < cnt; ++j) L = std::max(L, last[nb[j]]);
-        for (uint64_t q = 0; q < s; ++q) L = std::max(L, last[tails[(size_t)t * s + q]]);
-        ++L;
-        last[h] = L;
-        for (uint32_t j = 0; j < cnt; ++j) last[nb[j]] = L;
-        for (uint64_t q = 0; q < s; ++q) last[tails[(size_t)t * s + q]] = L;
-        lev[t] = L - 1;
-        maxlev = std::max(maxlev, L);
-        edges += cnt + s;
+      }
+      // pass 2: conflict levels over the worker's own point range (u16
+      // levels, 2 bytes per point, while they fit; u32 otherwise), with the
+      // neighbour rows of draws ahead prefetched
+      const uint32_t p0w = d.pstart;
+      auto levels = [&](auto& last) -> bool {
+        using LT = typename std::decay_t<decltype(last)>::value_type;
+        constexpr uint32_t AHEAD = 16;
+        maxlev = 0;
+        edges = 0;
+        for (uint32_t t = 0; t < std::min(D, AHEAD); ++t)
+          __builtin_prefetch(ell_h.data() + (size_t)head[t] * kpad);
+        for (uint32_t t = 0; t < D; ++t) {
+          if (t + AHEAD < D) __builtin_prefetch(ell_h.data() + (size_t)head[t + AHEAD] * kpad);
+          const uint32_t h = head[t];
+          // level = 1 + max level of every point it reads or writes
+          const uint32_t cnt = ncnt_h[h];
+          const uint32_t* nb = ell_h.data() + (size_t)h * kpad;
+          const uint32_t* tl = tails.data() + (size_t)t * s;
+          uint32_t L = last[h - p0w];
+          for (uint32_t j = 0; j < cnt; ++j) L = std::max<uint32_t>(L, last[nb[j] - p0w]);
+          for (uint64_t q = 0; q < s; ++q) L = std::max<uint32_t>(L, last[tl[q] - p0w]);
+          ++L;
+          if (L > std::numeric_limits<LT>::max()) return false;
+          last[h - p0w] = (LT)L;
+          for (uint32_t j = 0; j < cnt; ++j) last[nb[j] - p0w] = (LT)L;
+          for (uint64_t q = 0; q < s; ++q) last[tl[q] - p0w] = (LT)L;
+          lev[t] = L - 1;
+          maxlev = std::max(maxlev, L);
+          edges += cnt + s;
+        }
+        return true;
+      };
+      {
+        std::vector<uint16_t> l16(d.npts, 0);
+        if (!levels(l16)) {
+          std::vector<uint32_t> l32(d.npts, 0);
+          levels(l32);
+        }
       }
       // counting sort by level (stable in t)
       std::vector<uint32_t> cnt_l(maxlev + 1, 0);
@@ -762,6 +793,10 @@ struct nomad_b200_trainer {
         }
         if (it + 1 < n_epochs) prefetch = std::thread([this, &nxt] { build_tapes(nxt); });
         edges = cur.edges;
+        if (std::getenv("NOMAD_B200_DEBUG_REPLAY") && it == 0)
+          for (uint32_t wl = 0; wl < nwl; ++wl)
+            std::fprintf(stderr, "replay worker %u: %u draws, %u levels\n", wl, wk[wl].draws,
+                         cur.nlev[wl]);
         upload(tape_head, cur.th, S);
         upload(tape_tails, cur.tt, S);
         upload(tape_t, cur.tid, S);
@@ -776,6 +811,12 @@ struct nomad_b200_trainer {
         P.wk_nlev = wk_nlev.p;
         P.loss_slot = loss_slot.p;
         P.wk_draw_base = wk_draw_base.p;
+        if (!replay_k) {
+          replay_k = replay_ctas_per_worker(nwl, smem_replay, ctx->sm_count);
+          replay_bar.alloc(std::max<uint32_t>(nwl, 1));
+        }
+        P.replay_ctas = replay_k;
+        P.replay_bar = replay_bar.p;
         NB_CUDA(cudaEventRecord(ev[0], S));
         if (nwl) {
           launch_sgd_replay(P, nwl, smem_replay, S);
