@@ -320,11 +320,15 @@ def main():
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     tr.set_layout(host_in)
+    ta = time.perf_counter()
     tr2_edges0 = tr.progress()[1]
     tr.run(min(args.steps, 200 - args.warmup - args.steps) or 1)
+    tb = time.perf_counter()
     tr.layout(host_out.numpy())
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t1
+    e2e_parts_ms = [round(1e3 * (ta - t1), 2), round(1e3 * (tb - ta), 2),
+                    round(1e3 * (t1 + e2e_s - tb), 2)]
     e2e_steps = min(args.steps, 200 - args.warmup - args.steps) or 1
     e2e_edges = tr.progress()[1] - tr2_edges0
     if world > 1:
@@ -337,8 +341,10 @@ def main():
     e2e = {"value": e2e_edges / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(16 * n / e2e_steps),
            "d2h_bytes_per_step": int(16 * n / e2e_steps + 8 * (W // world)),
-           "path": "C-ABI trainer_set_layout(host) + trainer_run(1) x K (host loss) + "
-                   "trainer_layout(host)"}
+           "path": "C-ABI trainer_set_layout(host) + trainer_run(K) (per-epoch losses to host) + "
+                   "trainer_layout(host)",
+           "parts_ms": {"set_layout": e2e_parts_ms[0], "run": e2e_parts_ms[1],
+                        "layout": e2e_parts_ms[2]}}
 
     # the same K epochs with full f64 position rows (two RED.F64 per row update)
     # instead of double-float rows: the strict-f64 storage variant, same protocol
