@@ -135,9 +135,9 @@ typedef struct {
   int32_t sgd_mode;          /* nomad_b200_sgd_mode */
   int32_t knn_mode;          /* nomad_b200_knn_mode */
   uint32_t hogwild_cap;      /* heads in flight per shard <= shard/cap (0: 16) */
-  int32_t hogwild_f64_rows;  /* throughput mode: 1 = f64 position rows updated by two
-                                RED.F64; 0 = double-float rows {hi, lo} (value hi + lo,
-                                48-bit significand) updated by one RED.F32x2 (faster) */
+  int32_t hogwild_double_float; /* throughput mode: 0 = f64 position rows, two RED.F64 per
+                                row update (default); 1 = double-float rows {hi, lo} (value
+                                hi + lo, 48-bit significand), one RED.F32x2 per row update */
   int32_t verbose;           /* per-epoch line to stderr (optimizer.hpp:455-462) */
 } nomad_b200_train_config;
 

@@ -36,7 +36,7 @@ struct EngineOptions {
   int sgd_mode = NOMAD_B200_SGD_REPLAY;  // bit-exact replay by default
   int knn_mode = NOMAD_B200_KNN_EXACT;
   unsigned hogwild_cap = 0;
-  bool hogwild_f64_rows = false;
+  bool hogwild_double_float = false;
 };
 
 inline EngineOptions& options() {
@@ -106,7 +106,7 @@ inline nomad_b200_train_config cfg(const TrainConfig& c) {
   o.sgd_mode = options().sgd_mode;
   o.knn_mode = options().knn_mode;
   o.hogwild_cap = options().hogwild_cap;
-  o.hogwild_f64_rows = options().hogwild_f64_rows ? 1 : 0;
+  o.hogwild_double_float = options().hogwild_double_float ? 1 : 0;
   return o;
 }
 

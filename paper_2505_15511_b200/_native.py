@@ -55,7 +55,7 @@ class TrainConfigC(C.Structure):
                 ("head_only", C.c_int32), ("checkpoint_every", C.c_uint64),
                 ("checkpoint_prefix", C.c_char_p), ("checkpoint_ids", C.c_void_p),
                 ("checkpoint_labels", C.c_void_p), ("sgd_mode", C.c_int32), ("knn_mode", C.c_int32),
-                ("hogwild_cap", C.c_uint32), ("hogwild_f64_rows", C.c_int32),
+                ("hogwild_cap", C.c_uint32), ("hogwild_double_float", C.c_int32),
                 ("verbose", C.c_int32)]
 
 

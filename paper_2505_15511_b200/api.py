@@ -108,7 +108,7 @@ class TrainConfig:
     sgd_mode: str = "replay"        # "replay" (bit-exact) | "hogwild" (throughput)
     knn_mode: str = "exact"         # "exact" | "bf16"
     hogwild_cap: int = 0
-    hogwild_f64_rows: bool = False  # f64 position rows (2 RED.F64) instead of double-float rows
+    hogwild_double_float: bool = False  # double-float position rows (1 RED.F32x2, 48-bit) instead of f64
     checkpoint_every: int = 0       # fit(): layout CSV every N epochs (optimizer.hpp:463-469)
     checkpoint_prefix: str = ""     # "<prefix>.epoch<N>.csv"
 
@@ -143,7 +143,7 @@ class TrainConfig:
             self.checkpoint_every, self.checkpoint_prefix.encode() or None, None, None,
             {"replay": N.SGD_REPLAY, "hogwild": N.SGD_HOGWILD}[self.sgd_mode],
             {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[self.knn_mode],
-            self.hogwild_cap, 1 if self.hogwild_f64_rows else 0, 1 if self.verbose else 0)
+            self.hogwild_cap, 1 if self.hogwild_double_float else 0, 1 if self.verbose else 0)
 
 
 # ---------------------------------------------------------------- context

@@ -428,7 +428,7 @@ static void hog_go(const SgdParams& P0, uint32_t nblocks, size_t smem, cudaStrea
   P.rowbuf_off = (uint32_t)(off / sizeof(double));
   smem = off + (size_t)2 * (1 + KMAX / G + (SMAX + G - 1) / G) * 256 * 16;
 #endif
-  auto kern = P.f64_rows ? k_sgd_hogwild<G, KMAX, SMAX, false> : k_sgd_hogwild<G, KMAX, SMAX, true>;
+  auto kern = P.double_float ? k_sgd_hogwild<G, KMAX, SMAX, true> : k_sgd_hogwild<G, KMAX, SMAX, false>;
   if (smem > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (per_sm) {

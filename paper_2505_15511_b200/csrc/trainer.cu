@@ -408,10 +408,10 @@ struct nomad_b200_trainer {
 
   unsigned long long div_tag = 0;  // run-relative epoch tag of divergence keys (hogwild)
   // The throughput kernel's position rows are double-float while a run is in
-  // progress (unless cfg.hogwild_f64_rows); outside run() they are f64 again.
+  // progress (cfg.hogwild_double_float); outside run() they are f64 again.
   bool pos_is_df = false;
   void pos_format(bool df) {
-    if (df == pos_is_df || cfg.hogwild_f64_rows) return;
+    if (df == pos_is_df || !cfg.hogwild_double_float) return;
     launch_pos_df(pos.p, (uint32_t)orig_of.size(), df, st());
     launched("k_pos_df");
     pos_is_df = df;
@@ -484,7 +484,7 @@ struct nomad_b200_trainer {
     P.m_total = (uint32_t)cfg.negatives;
     P.n_clusters = (uint32_t)C;
     P.head_only = cfg.head_only;
-    P.f64_rows = cfg.hogwild_f64_rows ? 1 : 0;
+    P.double_float = cfg.hogwild_double_float ? 1 : 0;
     P.max_cells = hog_cells;
     P.all_but_own = cfg.approx_all_but_own;
     P.step = step;

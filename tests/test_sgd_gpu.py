@@ -116,14 +116,14 @@ def test_parameter_errors(ctx):
     assert e.value.kind == "Parameter"
 
 
-@pytest.mark.parametrize("workers,f64_rows", [(1, False), (4, False), (4, True)])
-def test_hogwild_statistical_parity(port, ctx, workers, f64_rows):
+@pytest.mark.parametrize("workers,double_float", [(1, False), (4, False), (4, True)])
+def test_hogwild_statistical_parity(port, ctx, workers, double_float):
     """Throughput mode (double-float or f64 position rows): same loss
     trajectory as the reference within 5%."""
     import paper_2505_15511_b200 as nb
     x, c, g, pca = index_case(3000, 32, 10, 8, 15)
     kw = dict(epochs=30, workers=workers, seed=7)
-    tr = _trainer(nb, ctx, c, g, pca, sgd_mode="hogwild", hogwild_f64_rows=f64_rows, **kw)
+    tr = _trainer(nb, ctx, c, g, pca, sgd_mode="hogwild", hogwild_double_float=double_float, **kw)
     loss = tr.run(30)
     lay = tr.layout()
     assert np.isfinite(lay).all()
