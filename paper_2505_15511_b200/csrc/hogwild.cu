@@ -14,8 +14,9 @@
 // double-float position rows (one RED.F32x2 per row, see ld_row/add_row).
 //
 // Scheduling: blocks pull fixed-size chunks of draws from a global counter;
-// chunks are numbered worker-major, so at any moment the GPU works on about
-// one shard and that shard's positions stay resident in L2. Shards are
+// the chunk map orders them in waves of shards (round-robin inside a wave),
+// so at any moment the GPU works on a few shards whose positions stay
+// resident in L2. Shards are
 // disjoint and the means snapshot is read-only, so the order in which shards
 // run does not change the semantics (the reference runs them as independent
 // threads). Heads in flight <= grid threads / G (the hogwild cap).
@@ -161,9 +162,12 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
     if (threadIdx.x == 0) s_chunk = atomicAdd(P.chunk_counter, 1u);
     __syncthreads();
     const uint32_t c = s_chunk;
-    uint32_t w = 0;
-    if (c < P.total_chunks)
-      while (w + 1 < P.n_workers && c >= P.workers[w + 1].chunk0) ++w;
+    uint32_t w = 0, lchunk = 0;
+    if (c < P.total_chunks) {
+      const uint2 cm = P.chunk_map[c];
+      w = cm.x;
+      lchunk = cm.y;
+    }
     if (c >= P.total_chunks || w != cur) {  // block-uniform
       if (cur != 0xFFFFFFFFu) {  // flush the previous shard's statistics
         const double ls = block_sum(loss_acc, red);
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       }
       __syncthreads();
     }
-    const uint32_t t_base = (c - W.chunk0) * P.chunk_heads;
+    const uint32_t t_base = lchunk * P.chunk_heads;
     // draw(t): the Philox draws of head t (lane b of the group computes
     // Philox block b = draws 2b, 2b+1), its tails, and the load of its
     // neighbour ids (this lane's slice of the ELL row). Executed by full warps

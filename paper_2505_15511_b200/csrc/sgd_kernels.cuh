@@ -18,7 +18,7 @@ struct WorkerDev {
   uint32_t elig_off, n_elig;  // eligible heads (local ids) in elig[]
   uint32_t rem_off, n_rem;    // remote cells R~ (RemoteClusters mode)
   uint32_t draws;             // heads drawn this epoch (= n_elig)
-  uint32_t chunk0;            // first hogwild chunk of this worker (worker-major)
+  uint32_t chunk0;            // unused (kept for layout)
   uint32_t all_elig;          // eligible == all points (head = pstart + idx)
   uint32_t id;                // global worker id
   double local_mass;          // optimizer.hpp:369-370
@@ -58,6 +58,7 @@ struct SgdParams {
   // hogwild dynamic schedule (chunks of chunk_heads draws, worker-major)
   uint32_t* chunk_counter;
   uint32_t total_chunks, chunk_heads;
+  const uint2* chunk_map;       // chunk -> (local worker, chunk within the worker)
   // replay tape (level-ordered)
   const uint32_t* tape_head;    // local id per draw (level order)
   const uint32_t* tape_tails;   // s local ids per draw

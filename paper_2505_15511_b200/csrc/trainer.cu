@@ -93,7 +93,8 @@ struct nomad_b200_trainer {
   uint32_t hog_cells = 0;  // capacity of the hogwild kernel's shared cell table
   uint32_t replay_k = 0;   // replay: CTAs per worker
   DBuf<uint32_t> replay_bar;
-  uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0;
+  uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0, hog_wave = 1;
+  DBuf<uint2> chunk_map;  // hogwild chunk -> (local worker, chunk within the worker)
   DBuf<uint32_t> chunk_counter;
 
   DBuf<double2> pos, means;
@@ -381,9 +382,12 @@ struct nomad_b200_trainer {
   }
 
   void plan_hogwild_grid() {
-    // Heads in flight (grid threads / G) <= min shard size / cap (SURVEY
-    // Appendix C.6), and never more blocks than are resident at once (the
-    // kernel pulls chunks dynamically, so extra blocks would only idle).
+    // Heads in flight on one shard <= shard size / cap,
+    // never more blocks than are resident at once (the kernel pulls chunks
+    // dynamically, so extra blocks would only idle). Chunks are ordered in
+    // waves of `wave` shards, round-robin inside a wave: one shard at a time
+    // keeps its positions L2-resident (config C), several at a time fill the
+    // GPU when one shard's cap cannot (small shards, config B).
     const uint32_t cap = cfg.hogwild_cap ? cfg.hogwild_cap : 16;
     const uint32_t G = hogwild_group_size((uint32_t)kpad, (uint32_t)s);
     const uint64_t resident = hogwild_resident_blocks((uint32_t)kpad, (uint32_t)s, smem_hog, ctx->sm_count);
@@ -393,15 +397,30 @@ struct nomad_b200_trainer {
     if (min_pts == ~0ull) min_pts = 1;
     const uint64_t heads_per_block = 256 / G;
     const uint64_t by_cap = std::max<uint64_t>(1, (min_pts / cap + heads_per_block - 1) / heads_per_block);
-    hog_blocks = (uint32_t)std::min<uint64_t>(resident, by_cap);
+    uint32_t nact = 0;
+    for (auto& d : wk) nact += d.draws ? 1u : 0u;
+    const uint32_t wave = (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>(std::max<uint32_t>(nact, 1), (resident + by_cap - 1) / by_cap));
+    hog_blocks = (uint32_t)std::min<uint64_t>(resident, by_cap * wave);
     chunk_heads = (uint32_t)(heads_per_block * hogwild_chunk_rounds());
-    uint32_t c = 0;
-    for (auto& d : wk) {
-      d.chunk0 = c;
+    std::vector<uint32_t> nchunk(nwl);
+    for (uint32_t wl = 0; wl < nwl; ++wl) {
+      WorkerDev& d = wk[wl];
       d.all_elig = d.n_elig == d.npts ? 1u : 0u;
-      c += (d.draws + chunk_heads - 1) / chunk_heads;
+      nchunk[wl] = (d.draws + chunk_heads - 1) / chunk_heads;
     }
-    total_chunks = c;
+    std::vector<uint2> cmap;
+    for (uint32_t w0 = 0; w0 < nwl; w0 += wave) {
+      const uint32_t w1 = std::min<uint32_t>(nwl, w0 + wave);
+      uint32_t maxc = 0;
+      for (uint32_t wl = w0; wl < w1; ++wl) maxc = std::max(maxc, nchunk[wl]);
+      for (uint32_t lc = 0; lc < maxc; ++lc)
+        for (uint32_t wl = w0; wl < w1; ++wl)
+          if (lc < nchunk[wl]) cmap.push_back(make_uint2(wl, lc));
+    }
+    total_chunks = (uint32_t)cmap.size();
+    hog_wave = wave;
+    upload(chunk_map, cmap, st());
     chunk_counter.alloc(1);
     if (total_chunks == 0) hog_blocks = 0;
   }
@@ -495,6 +514,7 @@ struct nomad_b200_trainer {
     P.chunk_counter = chunk_counter.p;
     P.total_chunks = total_chunks;
     P.chunk_heads = chunk_heads;
+    P.chunk_map = chunk_map.p;
     return P;
   }
 
