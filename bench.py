@@ -316,22 +316,29 @@ def main():
     # K epochs (per-epoch loss D2H), layout out (D2H)
     host_in = torch.from_numpy(init).pin_memory()
     host_out = torch.empty((n, 2), dtype=torch.float64).pin_memory()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    tr.set_layout(host_in)
-    ta = time.perf_counter()
-    tr2_edges0 = tr.progress()[1]
-    tr.run(min(args.steps, 200 - args.warmup - args.steps) or 1)
-    tb = time.perf_counter()
-    tr.layout(host_out.numpy())
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t1
-    e2e_parts_ms = [round(1e3 * (ta - t1), 2), round(1e3 * (tb - ta), 2),
-                    round(1e3 * (t1 + e2e_s - tb), 2)]
+    # three repetitions of the whole host -> device -> host pass; the median
+    # is reported (a single pass is exposed to one-off host hiccups)
+    reps = []
+    for _rep in range(3):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        tr.set_layout(host_in)
+        ta = time.perf_counter()
+        tr2_edges0 = tr.progress()[1]
+        tr.run(min(args.steps, 200 - args.warmup - args.steps) or 1)
+        tb = time.perf_counter()
+        tr.layout(host_out.numpy())
+        torch.cuda.synchronize()
+        tc_ = time.perf_counter()
+        reps.append((tc_ - t1, tr.progress()[1] - tr2_edges0, ta - t1, tb - ta, tc_ - tb))
+        if tr.progress()[0] + (min(args.steps, 200 - args.warmup - args.steps) or 1) > 200:
+            break
+    reps.sort(key=lambda r: r[0])
+    e2e_s, e2e_edges, pa, pb, pc = reps[len(reps) // 2]
+    e2e_parts_ms = [round(1e3 * pa, 2), round(1e3 * pb, 2), round(1e3 * pc, 2)]
     e2e_steps = min(args.steps, 200 - args.warmup - args.steps) or 1
-    e2e_edges = tr.progress()[1] - tr2_edges0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -345,7 +352,8 @@ def main():
            "path": "C-ABI trainer_set_layout(host) + trainer_run(K) (per-epoch losses to host) + "
                    "trainer_layout(host)",
            "parts_ms": {"set_layout": e2e_parts_ms[0], "run": e2e_parts_ms[1],
-                        "layout": e2e_parts_ms[2]}}
+                        "layout": e2e_parts_ms[2]},
+           "repetitions": len(reps), "statistic": "median"}
 
     # the same K epochs with double-float position rows (value hi + lo, 48-bit
     # significand, one RED.F32x2 per row update): a reduced-storage-precision
