@@ -38,18 +38,6 @@
 #ifndef HOG_ROUNDS
 #define HOG_ROUNDS 8      // rounds of 256/G heads per scheduled chunk
 #endif
-#ifndef HOG_PF
-#define HOG_PF 1          // 1: next head's draws + neighbour ids issued before this head's math
-#endif
-#ifndef HOG_LATE
-#define HOG_LATE 0        // 1: neighbour/tail rows prefetched to L1, loaded after the mean field
-#endif
-#ifndef HOG_MF2
-#define HOG_MF2 0         // 1: two independent mean-field accumulator sets
-#endif
-#ifndef HOG_SROWS
-#define HOG_SROWS 0       // 1: rows of the next head streamed into shared memory by cp.async mid-round (measured slower)
-#endif
 
 namespace nb {
 
@@ -84,24 +72,6 @@ __device__ __forceinline__ void add_row(double2* pos, uint32_t i, double ax, dou
   } else {
     atomicAdd(&pos[i].x, ax);
     atomicAdd(&pos[i].y, ay);
-  }
-}
-
-// 16-byte row -> shared memory (zero-filled when !ok); value decode as ld_row.
-__device__ __forceinline__ void cp_row(float4* dst, const double2* src, bool ok) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
-               "r"(ok ? 16u : 0u)
-               : "memory");
-}
-template <bool DF>
-__device__ __forceinline__ double2 sm_row(const float4* p) {
-  const float4 r = *p;
-  if constexpr (DF) {
-    return make_double2((double)r.x + (double)r.z, (double)r.y + (double)r.w);
-  } else {
-    return make_double2(__hiloint2double(__float_as_int(r.y), __float_as_int(r.x)),
-                        __hiloint2double(__float_as_int(r.w), __float_as_int(r.z)));
   }
 }
 
@@ -237,52 +207,10 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
     };
     Draw<NPL, TPL> D;
     draw(t_base + grp, D);
-#if HOG_SROWS
-    // this lane's rows of a head (slot 0 head, 1..NPL neighbours, then tails),
-    // double-buffered in shared memory [2][SLOTS][256] (lane-contiguous)
-    constexpr int SLOTS = 1 + NPL + TPL;
-    float4* rb = reinterpret_cast<float4*>(sm + P.rowbuf_off);
-    auto issue_rows = [&](const Draw<NPL, TPL>& X, int b) {
-      float4* base = rb + (size_t)b * SLOTS * 256 + threadIdx.x;
-      cp_row(base, P.pos + X.head, X.act);
-#pragma unroll
-      for (int i = 0; i < NPL; ++i)
-        cp_row(base + (1 + i) * 256, P.pos + X.nb[i], NPL * gl + i < (int)X.cnt);
-#pragma unroll
-      for (int m = 0; m < TPL; ++m)
-        cp_row(base + (1 + NPL + m) * 256, P.pos + X.tl[m], X.act && gl + G * m < (int)s);
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    int buf = 0;
-    issue_rows(D, 0);
-#endif
     for (uint32_t j = grp; j < P.chunk_heads; j += GPB) {
       const bool act = D.act;
       const uint32_t head = D.head, cnt = D.cnt, own_gid = D.own_gid;
       const double sf = D.sf;
-#if HOG_SROWS
-      // ---- this head's rows: landed in shared memory during the previous round
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      const float4* rbase = rb + (size_t)buf * SLOTS * 256 + threadIdx.x;
-      const double2 h = sm_row<DF>(rbase);
-      double2 pn[NPL], pt[TPL];
-#pragma unroll
-      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? sm_row<DF>(rbase + (1 + i) * 256) : h;
-#pragma unroll
-      for (int m = 0; m < TPL; ++m)
-        pt[m] = (act && gl + G * m < (int)s) ? sm_row<DF>(rbase + (1 + NPL + m) * 256) : h;
-#elif HOG_LATE
-      // ---- head row now; neighbour / tail rows prefetched into L1 now and
-      // loaded after the mean field (no registers held across it)
-      const double2 h = ld_row<DF>(P.pos, head);
-      double2 pn[NPL], pt[TPL];
-#pragma unroll
-      for (int i = 0; i < NPL; ++i)
-        if (NPL * gl + i < (int)cnt) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pos + D.nb[i]));
-#pragma unroll
-      for (int m = 0; m < TPL; ++m)
-        if (act && gl + G * m < (int)s) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.pos + D.tl[m]));
-#else
       // ---- gathers (all issued before any use)
       const double2 h = ld_row<DF>(P.pos, head);
       double2 pn[NPL], pt[TPL];
@@ -290,38 +218,17 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row<DF>(P.pos, D.nb[i]) : h;
 #pragma unroll
       for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row<DF>(P.pos, D.tl[m]) : h;
-#endif
       const bool more = j + GPB < P.chunk_heads;  // warp-uniform
-#if HOG_PF || HOG_SROWS
       // next head's draws and neighbour ids in flight during this head's math
       Draw<NPL, TPL> Dn;
       if (more) draw(t_base + j + GPB, Dn);
-#endif
 
       // ---- mean field over this lane's cells: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
-      // (two independent accumulator sets; own cell skipped in AllButOwn mode)
+      // (own cell skipped in AllButOwn mode)
       double s1 = 0.0, s2x = 0.0, s2y = 0.0;
       {
         const uint32_t skip = P.all_but_own ? own_gid : 0xFFFFFFFFu;
         uint32_t q = gl;
-#if HOG_MF2
-        double t1 = 0.0, t2x = 0.0, t2y = 0.0;
-        for (; q + G < ncell; q += 2 * G) {
-          const double2 ma = tmu[q], mb = tmu[q + G];
-          const double wa = q == skip ? 0.0 : tpw[q], wb = q + G == skip ? 0.0 : tpw[q + G];
-          const double ax = h.x - ma.x, ay = h.y - ma.y, bx = h.x - mb.x, by = h.y - mb.y;
-          const double qa = frcp(fma(ax, ax, fma(ay, ay, 1.0)));
-          const double qb = frcp(fma(bx, bx, fma(by, by, 1.0)));
-          const double pa = wa * qa, pb = wb * qb;
-          s1 += pa;
-          t1 += pb;
-          const double pa2 = pa * qa, pb2 = pb * qb;
-          s2x = fma(pa2, ax, s2x);
-          s2y = fma(pa2, ay, s2y);
-          t2x = fma(pb2, bx, t2x);
-          t2y = fma(pb2, by, t2y);
-        }
-#endif
 #pragma unroll 2
         for (; q < ncell; q += G) {
           const double2 ma = tmu[q];
@@ -334,21 +241,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           s2x = fma(pa2, ax, s2x);
           s2y = fma(pa2, ay, s2y);
         }
-#if HOG_MF2
-        s1 += t1;
-        s2x += t2x;
-        s2y += t2y;
-#endif
       }
-#if HOG_SROWS
-      // next head's rows stream in behind the rest of this head's math
-      if (more) issue_rows(Dn, buf ^ 1);
-#elif HOG_LATE
-#pragma unroll
-      for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row<DF>(P.pos, D.nb[i]) : h;
-#pragma unroll
-      for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row<DF>(P.pos, D.tl[m]) : h;
-#endif
       // ---- sampled negatives
       double qn[TPL], qsum = 0.0;
 #pragma unroll
@@ -410,14 +303,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
         edge_acc += (double)(cnt + s);
       }
       loss_acc += (double)lf;
-#if HOG_PF || HOG_SROWS
       if (more) D = Dn;
-#else
-      if (more) draw(t_base + j + GPB, D);
-#endif
-#if HOG_SROWS
-      buf ^= 1;
-#endif
     }
   }
 }
@@ -425,13 +311,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 template <int G, int KMAX, int SMAX>
 static void hog_go(const SgdParams& P0, uint32_t nblocks, size_t smem, cudaStream_t st,
                    int* per_sm) {
-  SgdParams P = P0;
-#if HOG_SROWS
-  // row double buffer after the weight / cell tables
-  const size_t off = (smem + 15) / 16 * 16;
-  P.rowbuf_off = (uint32_t)(off / sizeof(double));
-  smem = off + (size_t)2 * (1 + KMAX / G + (SMAX + G - 1) / G) * 256 * 16;
-#endif
+  const SgdParams& P = P0;
   auto kern = P.double_float ? k_sgd_hogwild<G, KMAX, SMAX, true> : k_sgd_hogwild<G, KMAX, SMAX, false>;
   if (smem > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

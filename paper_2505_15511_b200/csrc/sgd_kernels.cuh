@@ -48,7 +48,6 @@ struct SgdParams {
   uint32_t n_workers, kpad, k, s, m_total, n_clusters;
   int head_only, all_but_own;
   int double_float;             // hogwild: 1 = double-float rows (1 RED.F32x2), 0 = f64 rows (2 RED.F64)
-  uint32_t rowbuf_off;          // hogwild: shared-memory row buffer offset (doubles)
   uint32_t max_cells;           // hogwild: capacity of the shared cell table
   uint32_t replay_ctas;         // replay: CTAs per worker (level barrier in global memory)
   uint32_t* replay_bar;         // replay: per-worker barrier counters
