@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -305,21 +307,75 @@ __global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__
 
 // Pass 2: warp per query slot; lanes own KP/32 survivors each; the `want`
 // smallest (distance, id) keys are extracted in order. Slot v is point
-// qlist[v] (qlist == nullptr: point v); want = min(k, size - 1) of its
-// cluster (assign/sizes) or `fixed_want` when nonzero; list position
-// offsets[point] or v * k when offsets == nullptr.
+// qlist[v] (qlist == nullptr: point v); candidates are indexed by slot, or by
+// point id when by_row (then the fallback list records point ids too);
+// want = min(k, size - 1) of its cluster (assign/sizes) or `fixed_want` when
+// nonzero; list position offsets[point] or v * k when offsets == nullptr.
+// Reference fp64 distances (ref_dist's j-ascending chain, bit for bit) of one
+// query row to each lane's candidates. Candidate rows are staged through
+// shared memory in 64-column chunks by coalesced warp-wide loads (128 bytes
+// of one row per instruction), then each lane runs its own chain over its
+// candidate's chunk (row stride 65: conflict-free). `tile` = 32 x 65 + 64
+// floats per warp.
+template <int PER>
+__device__ __forceinline__ void warp_ref_dists(const float* __restrict__ x, uint32_t d,
+                                               const float* __restrict__ qrow,
+                                               const uint32_t (&iv)[PER], double (&dv)[PER],
+                                               float* tile) {
+  const int lane = threadIdx.x & 31;
+  float* qt = tile + 32 * 65;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) dv[e] = 0.0;
+  for (uint32_t j0 = 0; j0 < d; j0 += 64) {
+    const uint32_t w = min(64u, d - j0);
+    __syncwarp();
+    qt[lane] = lane < (int)w ? qrow[j0 + lane] : 0.f;
+    qt[32 + lane] = 32 + lane < (int)w ? qrow[j0 + 32 + lane] : 0.f;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      __syncwarp();
+#pragma unroll 4
+      for (int c = 0; c < 32; ++c) {
+        const uint32_t r = __shfl_sync(0xffffffffu, iv[e], c);
+        if (r == 0xFFFFFFFFu) continue;  // warp-uniform
+        const float* row = x + (uint64_t)r * d + j0;
+        tile[c * 65 + lane] = lane < (int)w ? row[lane] : 0.f;
+        tile[c * 65 + 32 + lane] = 32 + lane < (int)w ? row[32 + lane] : 0.f;
+      }
+      __syncwarp();
+      if (iv[e] != 0xFFFFFFFFu) {
+        const float* mine = tile + lane * 65;
+        double acc = dv[e];
+        for (uint32_t j = 0; j < w; ++j) {
+          const double t = __dsub_rn((double)qt[j], (double)mine[j]);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+        dv[e] = acc;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < PER; ++e)
+    if (iv[e] == 0xFFFFFFFFu) dv[e] = __longlong_as_double(0x7ff0000000000000ll);
+}
+
+constexpr int RR_WARP_FLOATS = 32 * 65 + 64;  // shared floats per warp of the re-rank
+
 template <int KP>
 __global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t nq,
                              const uint32_t* qlist, const uint32_t* assign, const uint32_t* sizes,
                              uint32_t k, uint32_t fixed_want, const uint32_t* cand_ids,
                              const float* cand_tau, const uint32_t* cand_cnt,
                              const uint32_t* offsets, uint32_t* out_nb, double* out_d,
-                             uint32_t* fallback, uint32_t* n_fallback, double lb_factor) {
+                             uint32_t* fallback, uint32_t* n_fallback, double lb_factor,
+                             int by_row) {
   constexpr int PER = KP / 32;
-  const uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t v0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (v >= nq) return;
-  const uint64_t q = qlist ? qlist[v] : v;
+  if (v0 >= nq) return;
+  const uint64_t q = qlist ? qlist[v0] : v0;
+  // by_row: candidate lists and the fallback record are indexed by point id
+  const uint64_t v = by_row ? q : v0;
   const uint32_t want = fixed_want ? fixed_want : min(k, sizes[assign[q]] - 1);
   if (want == 0) return;
   const uint32_t c = cand_cnt[v];
@@ -328,14 +384,10 @@ __global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t n
 #pragma unroll
   for (int e = 0; e < PER; ++e) {
     const int p = lane + 32 * e;  // slot
-    if (p < (int)c) {
-      iv[e] = cand_ids[v * KP + p];
-      dv[e] = ref_dist(x + q * d, x + (uint64_t)iv[e] * d, d);
-    } else {
-      iv[e] = 0xFFFFFFFFu;
-      dv[e] = __longlong_as_double(0x7ff0000000000000ll);
-    }
+    iv[e] = p < (int)c ? cand_ids[v * KP + p] : 0xFFFFFFFFu;
   }
+  extern __shared__ float rr_smem[];
+  warp_ref_dists<PER>(x, d, x + q * d, iv, dv, rr_smem + (threadIdx.x >> 5) * RR_WARP_FLOATS);
   const uint64_t o = offsets ? (uint64_t)offsets[q] : v * k;
   double dk = 0.0;
   for (uint32_t r = 0; r < want; ++r) {
@@ -369,6 +421,19 @@ __global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t n
   // (every filter writes +inf when its list holds all candidates)
   const bool ok = isinf(t) || (double)t * lb_factor > dk;
   if (!ok && lane == 0) fallback[atomicAdd(n_fallback, 1u)] = (uint32_t)v;
+}
+
+// Launch the re-rank (8 warps per block, RR_WARP_FLOATS shared floats each).
+template <int KP, typename... A>
+void launch_rerank(uint64_t nwarps, cudaStream_t S, A... args) {
+  const size_t smem = 8 * RR_WARP_FLOATS * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    NB_CUDA(cudaFuncSetAttribute(k_knn_rerank<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  k_knn_rerank<KP><<<(unsigned)((nwarps * 32 + 255) / 256), 256, smem, S>>>(args...);
 }
 
 // Pass 3: one block per uncertified slot, exhaustive fp64 over its cluster
@@ -584,7 +649,7 @@ __global__ void k_sub_certify(const float* __restrict__ xr, uint64_t m, uint32_t
                               const double* __restrict__ d2, uint32_t k, uint32_t want,
                               const uint32_t* __restrict__ members, double rel, double g64,
                               uint32_t KP, uint32_t* cand_ids, float* cand_lb, uint32_t* cand_cnt,
-                              unsigned long long* n_cert) {
+                              unsigned long long* n_cert, uint32_t* cert_rows) {
   const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (v >= m || open_sub[v]) return;
   if (ids2[v * k + want - 1] == 0xFFFFFFFFu) return;  // sub-cluster smaller than the list
@@ -617,7 +682,7 @@ __global__ void k_sub_certify(const float* __restrict__ xr, uint64_t m, uint32_t
   for (uint32_t i = 0; i < want; ++i) cand_ids[g * KP + i] = members[ids2[v * k + i]];
   cand_cnt[g] = want;
   cand_lb[g] = __int_as_float(0x7f800000);
-  atomicAdd(n_cert, 1ull);
+  cert_rows[atomicAdd(n_cert, 1ull)] = (uint32_t)g;
 }
 
 __global__ void k_mark_rows(const uint32_t* list, uint32_t n, uint8_t* mask) {
@@ -662,7 +727,7 @@ void ffma_filter(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t
 // Stage 1b for one cluster (members[0..m)): returns the rows it certified.
 uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
                           uint64_t m, uint32_t k, int KP, DBuf<uint32_t>& cid, DBuf<float>& clb,
-                          DBuf<uint32_t>& ccnt) {
+                          DBuf<uint32_t>& ccnt, std::vector<uint32_t>& cert_out) {
   cudaStream_t S = ctx->stream;
   DBuf<float> xr(m * d);
   k_gather_rows<<<ctx->sm_count * 8, 256, 0, S>>>(x, members, m, (uint32_t)d, xr.p);
@@ -831,9 +896,10 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
   NB_CUDA(cudaMemsetAsync(nfb2.p, 0, 4, S));
   NB_CUDA(cudaMemsetAsync(ids2.p, 0xFF, m * k * 4, S));
   const unsigned rb = (unsigned)((m * 32 + 255) / 256);
-  k_knn_rerank<64><<<rb, 256, 0, S>>>(xr.p, (uint32_t)d, m, nullptr, nullptr, nullptr, k, want,
-                                      cid2.p, clb2.p, ccnt2.p, nullptr, ids2.p, d2.p, fb2.p,
-                                      nfb2.p, 1.0);
+  launch_rerank<64>(m, S, xr.p, (uint32_t)d, m, (const uint32_t*)nullptr, (const uint32_t*)nullptr,
+                    (const uint32_t*)nullptr, k, want, (const uint32_t*)cid2.p,
+                    (const float*)clb2.p, (const uint32_t*)ccnt2.p, (const uint32_t*)nullptr,
+                    ids2.p, d2.p, fb2.p, nfb2.p, 1.0, 0);
   note_launch(ctx, "k_knn_rerank");
   uint32_t nf2 = 0;
   NB_CUDA(cudaMemcpyAsync(&nf2, nfb2.p, 4, cudaMemcpyDeviceToHost, S));
@@ -846,6 +912,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
   }
   const double g64 = (double)(d + 1) * 0x1p-53 * 2;
   DBuf<unsigned long long> rad(csub), ncert(1);
+  DBuf<uint32_t> crows(m);
   NB_CUDA(cudaMemsetAsync(rad.p, 0, csub * 8, S));
   NB_CUDA(cudaMemsetAsync(ncert.p, 0, 8, S));
   const unsigned mb = (unsigned)((m + 127) / 128);
@@ -854,11 +921,16 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
   k_sub_certify<<<mb, 128, 0, S>>>(xr.p, m, (uint32_t)d, sa.p, sc.p, rad.p, ssz.p, csub, segb.p,
                                    od.p, open.p,
                                    ids2.p, d2.p, k, want, members, rel, g64, (uint32_t)KP, cid.p,
-                                   clb.p, ccnt.p, ncert.p);
+                                   clb.p, ccnt.p, ncert.p, crows.p);
   note_launch(ctx, "k_sub_certify");
   unsigned long long nc = 0;
   NB_CUDA(cudaMemcpyAsync(&nc, ncert.p, 8, cudaMemcpyDeviceToHost, S));
   NB_CUDA(cudaStreamSynchronize(S));
+  if (nc) {
+    const size_t o = cert_out.size();
+    cert_out.resize(o + nc);
+    NB_CUDA(cudaMemcpy(cert_out.data() + o, crows.p, nc * 4, cudaMemcpyDeviceToHost));
+  }
   if (std::getenv("NOMAD_B200_DEBUG_KNN")) {
     std::fprintf(stderr, "subcluster stage: m=%llu csub=%u open-within=%u certified=%llu sizes:",
                  (unsigned long long)m, csub, nf2, nc);
@@ -933,76 +1005,115 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
   int KP = k <= 24 ? 32 : 64;
   DBuf<uint32_t> cid, ccnt;
   DBuf<float> clb;  // per-row lower bound on every excluded reference distance
+  // Re-rank the listed rows (device list, m rows; candidates indexed by row)
+  // and return the rows whose certificate failed. The first pass walks every
+  // row in cluster order (mem), so concurrently re-ranked queries share their
+  // candidates' rows in L2; later passes touch only the rows a stage changed.
   DBuf<uint32_t> fb(n), nfb(1);
-  auto rerank = [&]() -> uint32_t {
+  auto rerank_rows = [&](const uint32_t* rows_d, uint64_t m) {
+    std::vector<uint32_t> out;
+    if (!m) return out;
     NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
-    const unsigned rb = (unsigned)((n * 32 + 255) / 256);
-    auto go = [&](auto kern) {
-      kern<<<rb, 256, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d, sizes_want, k, 0u, cid.p, clb.p,
-                              ccnt.p, R.offsets.p, R.nb.p, R.dist.p, fb.p, nfb.p, 1.0);
+    auto go = [&](auto kp) {
+      launch_rerank<decltype(kp)::value>(m, S, x, (uint32_t)d, m, rows_d, assign_d, sizes_want, k,
+                                         0u, (const uint32_t*)cid.p, (const float*)clb.p,
+                                         (const uint32_t*)ccnt.p, (const uint32_t*)R.offsets.p,
+                                         R.nb.p, R.dist.p, fb.p, nfb.p, 1.0, 1);
     };
-    if (KP == 32) go(k_knn_rerank<32>); else go(k_knn_rerank<64>);
+    if (KP == 32) go(std::integral_constant<int, 32>{}); else go(std::integral_constant<int, 64>{});
     note_launch(ctx, "k_knn_rerank");
     uint32_t nf = 0;
     NB_CUDA(cudaMemcpyAsync(&nf, nfb.p, 4, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
-    return nf;
+    out.resize(nf);
+    if (nf) NB_CUDA(cudaMemcpy(out.data(), fb.p, nf * 4, cudaMemcpyDeviceToHost));
+    return out;
+  };
+  auto upload_rows = [&](const std::vector<uint32_t>& rows, DBuf<uint32_t>& dst) {
+    dst.alloc(std::max<size_t>(rows.size(), 1));
+    if (!rows.empty())
+      NB_CUDA(cudaMemcpyAsync(dst.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, S));
+  };
+  // open \ settled, then + the settled rows that failed again
+  auto update_open = [&](std::vector<uint32_t>& open, std::vector<uint32_t> settled,
+                         const std::vector<uint32_t>& failed) {
+    std::sort(settled.begin(), settled.end());
+    std::vector<uint32_t> rest;
+    for (uint32_t q : open)
+      if (!std::binary_search(settled.begin(), settled.end(), q)) rest.push_back(q);
+    rest.insert(rest.end(), failed.begin(), failed.end());
+    open.swap(rest);
   };
 
   const bool tc = (mode == NOMAD_B200_KNN_BF16) || (mode == NOMAD_B200_KNN_EXACT && k <= 56);
-  uint32_t nf = 0;
+  std::vector<uint32_t> open;
+  const bool dbg = std::getenv("NOMAD_B200_DEBUG_KNN") != nullptr;
+  auto t_stage = std::chrono::steady_clock::now();
+  auto stage_done = [&](const char* what) {
+    if (!dbg) return;
+    NB_CUDA(cudaStreamSynchronize(S));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "knn stage %-28s %8.1f ms, open rows %zu\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_stage).count(), open.size());
+    t_stage = now;
+  };
   if (tc) {
     // stage 1: tensor-core filter (bf16 fast / fp16 certified)
     if (mode == NOMAD_B200_KNN_BF16 && k > 24) fail(kParameter, "bf16 kNN mode supports k <= 24");
     knn_tc_candidates(ctx, x, n, d, assign_d, C, mode == NOMAD_B200_KNN_EXACT, cid, clb, ccnt,
                       &KP, own);
-    nf = rerank();
-    R.tc_uncertified = nf;
+    stage_done("tensor-core candidates");
+    open = rerank_rows(std::getenv("NOMAD_B200_KNN_IDORDER") ? nullptr : mem.p, n);
+    R.tc_uncertified = open.size();
+    stage_done("re-rank");
     std::vector<uint32_t> ah;
-    auto failures = [&](std::vector<uint32_t>& fbh, std::vector<uint64_t>& fail_per) {
-      fbh.resize(nf);
-      if (nf) NB_CUDA(cudaMemcpy(fbh.data(), fb.p, nf * 4, cudaMemcpyDeviceToHost));
+    auto fail_count = [&](std::vector<uint64_t>& fail_per) {
       if (ah.empty()) {
         ah.resize(n);
         NB_CUDA(cudaMemcpy(ah.data(), assign_d, n * 4, cudaMemcpyDeviceToHost));
       }
       fail_per.assign(C, 0);
-      for (uint32_t q : fbh) ++fail_per[ah[q]];
+      for (uint32_t q : open) ++fail_per[ah[q]];
     };
-    if (nf && mode == NOMAD_B200_KNN_EXACT) {
+    if (!open.empty() && mode == NOMAD_B200_KNN_EXACT) {
       // stage 1b: clusters where many rows failed the tensor-core certificate
       // (centred norms >> neighbour distances: the cluster spans several
       // blobs) are split into sub-clusters; exact lists inside each
       // sub-cluster come from the certified tensor-core filter on the
       // sub-cluster's own centring, and a row keeps its list when no other
       // sub-cluster can hold a closer point (k_sub_certify).
-      std::vector<uint32_t> fbh;
       std::vector<uint64_t> fail_per;
-      failures(fbh, fail_per);
-      uint64_t certified = 0;
+      fail_count(fail_per);
+      std::vector<uint32_t> cert;
       for (uint32_t r = 0; r < C; ++r) {
         const uint64_t sz = off[r + 1] - off[r];
         if (sz < 1024 || own && !(*own)[r] || fail_per[r] * 16 < sz) continue;
-        certified += subcluster_stage(ctx, x, d, mem.p + off[r], sz, k, KP, cid, clb, ccnt);
+        subcluster_stage(ctx, x, d, mem.p + off[r], sz, k, KP, cid, clb, ccnt, cert);
       }
-      R.sub_certified = certified;
-      if (certified) nf = rerank();
+      R.sub_certified = cert.size();
+      stage_done("sub-cluster stage");
+      if (!cert.empty()) {
+        DBuf<uint32_t> cd;
+        upload_rows(cert, cd);
+        const std::vector<uint32_t> again = rerank_rows(cd.p, cert.size());
+        update_open(open, cert, again);
+      }
+      stage_done("re-rank (sub-cluster rows)");
     }
-    if (nf && mode == NOMAD_B200_KNN_EXACT) {
+    if (!open.empty() && mode == NOMAD_B200_KNN_EXACT) {
       // stage 2: rows still open (both certificates failed) get the FFMA
       // filter against their whole cluster, whose error is relative to the
-      // distance itself.
-      std::vector<uint32_t> fbh;
+      // distance itself; clusters with a handful of open rows go straight to
+      // the exhaustive pass
       std::vector<uint64_t> fail_per;
-      failures(fbh, fail_per);
-      // only the open rows are re-filtered (against their whole cluster);
-      // clusters with a handful of open rows go straight to the exhaustive pass
+      fail_count(fail_per);
       std::vector<uint64_t> qoff(C + 1, 0);
       for (uint32_t r = 0; r < C; ++r) qoff[r + 1] = qoff[r] + (fail_per[r] >= 16 ? fail_per[r] : 0);
       std::vector<uint32_t> qh(qoff[C]);
       std::vector<uint64_t> fill(qoff.begin(), qoff.end() - 1);
-      std::sort(fbh.begin(), fbh.end());
-      for (uint32_t q : fbh)
+      std::vector<uint32_t> sorted_open(open);
+      std::sort(sorted_open.begin(), sorted_open.end());
+      for (uint32_t q : sorted_open)
         if (fail_per[ah[q]] >= 16) qh[fill[ah[q]]++] = q;
       std::vector<FilterSeg> sg;
       uint32_t nt = 0;
@@ -1014,11 +1125,13 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
         nt += (uint32_t)((qn + QT - 1) / QT);
       }
       if (nt) {
-        DBuf<uint32_t> ql(qh.size());
-        NB_CUDA(cudaMemcpyAsync(ql.p, qh.data(), qh.size() * 4, cudaMemcpyHostToDevice, S));
+        DBuf<uint32_t> ql;
+        upload_rows(qh, ql);
         ffma_filter(ctx, x, d, mem.p, ql.p, sg, nt, KP, 0, cid.p, clb.p, ccnt.p);
-        nf = rerank();
+        const std::vector<uint32_t> again = rerank_rows(ql.p, qh.size());
+        update_open(open, qh, again);
       }
+      stage_done("FFMA stage");
     }
   } else {
     cid.alloc(n * (uint64_t)KP);
@@ -1026,17 +1139,20 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
     clb.alloc(n);
     NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
     ffma_filter(ctx, x, d, mem.p, mem.p, segs, tiles, KP, 0, cid.p, clb.p, ccnt.p);
-    nf = rerank();
+    open = rerank_rows(mem.p, n);
   }
   // stage 3: exhaustive fp64 for whatever is still uncertified
-  R.fallbacks = nf;
-  if (nf) {
+  R.fallbacks = open.size();
+  if (!open.empty()) {
     std::vector<uint64_t> cb(C);
     for (uint32_t r = 0; r < C; ++r) cb[r] = off[r];
     DBuf<uint64_t> cb_d(C);
     NB_CUDA(cudaMemcpyAsync(cb_d.p, cb.data(), C * 8, cudaMemcpyHostToDevice, S));
-    k_knn_exhaustive<<<nf, 128, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d, mem.p, cb_d.p,
-                                        sizes.p, k, 0u, fb.p, R.offsets.p, R.nb.p, R.dist.p);
+    DBuf<uint32_t> od;
+    upload_rows(open, od);
+    k_knn_exhaustive<<<(unsigned)open.size(), 128, 0, S>>>(x, (uint32_t)d, n, nullptr, assign_d,
+                                                           mem.p, cb_d.p, sizes.p, k, 0u, od.p,
+                                                           R.offsets.p, R.nb.p, R.dist.p);
     note_launch(ctx, "k_knn_exhaustive");
   }
   NB_CUDA(cudaStreamSynchronize(S));
@@ -1073,17 +1189,20 @@ void knn_global_sample(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   k_merge_parts<<<rb, 256, 0, S>>>(m, P, KP, pid.p, plb.p, pcnt.p, cid.p, clb.p, ccnt.p);
   note_launch(ctx, "k_merge_parts");
   NB_CUDA(cudaMemsetAsync(nfb.p, 0, 4, S));
-  auto go = [&](auto kern) {
-    kern<<<rb, 256, 0, S>>>(x, (uint32_t)d, (uint64_t)m, qlist_d, nullptr, nullptr, k, k, cid.p,
-                            clb.p, ccnt.p, nullptr, out_ids_d, nullptr, fb.p, nfb.p, 1.0);
+  auto go = [&](auto kp) {
+    launch_rerank<decltype(kp)::value>((uint64_t)m, S, x, (uint32_t)d, (uint64_t)m, qlist_d,
+                                       (const uint32_t*)nullptr, (const uint32_t*)nullptr, k, k,
+                                       (const uint32_t*)cid.p, (const float*)clb.p,
+                                       (const uint32_t*)ccnt.p, (const uint32_t*)nullptr,
+                                       out_ids_d, (double*)nullptr, fb.p, nfb.p, 1.0, 0);
   };
   switch (KPP) {
-    case 32: go(k_knn_rerank<32>); break;
-    case 64: go(k_knn_rerank<64>); break;
-    case 128: go(k_knn_rerank<128>); break;
-    case 256: go(k_knn_rerank<256>); break;
-    case 512: go(k_knn_rerank<512>); break;
-    default: go(k_knn_rerank<1024>); break;
+    case 32: go(std::integral_constant<int, 32>{}); break;
+    case 64: go(std::integral_constant<int, 64>{}); break;
+    case 128: go(std::integral_constant<int, 128>{}); break;
+    case 256: go(std::integral_constant<int, 256>{}); break;
+    case 512: go(std::integral_constant<int, 512>{}); break;
+    default: go(std::integral_constant<int, 1024>{}); break;
   }
   note_launch(ctx, "k_knn_rerank");
   uint32_t nf = 0;
