@@ -305,6 +305,76 @@ __global__ void __launch_bounds__(256, 2) k_knn_filter(const float* __restrict__
   }
 }
 
+// Per-label column sums over an index list (lab == nullptr: one label):
+// grid (ceil(d / 128), 64 row chunks); sums[2][d], cnts[2] (atomics: the
+// bisection is a heuristic, not part of any certified result).
+__global__ void k_label_sums(const float* __restrict__ xr, const uint32_t* __restrict__ idx,
+                             uint64_t cnt, uint32_t d, const uint8_t* __restrict__ lab,
+                             double* sums, unsigned long long* cnts) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t r0 = cnt * blockIdx.y / gridDim.y, r1 = cnt * (blockIdx.y + 1) / gridDim.y;
+  double a0 = 0.0, a1 = 0.0;
+  unsigned long long n0 = 0, n1 = 0;
+  for (uint64_t i = r0; i < r1; ++i) {
+    const int l = lab ? lab[i] : 0;
+    const double v = j < d ? (double)xr[(uint64_t)idx[i] * d + j] : 0.0;
+    if (l) { a1 += v; ++n1; } else { a0 += v; ++n0; }
+  }
+  if (j < d) {
+    atomicAdd(sums + j, a0);
+    atomicAdd(sums + d + j, a1);
+  }
+  if (j == 0) {
+    atomicAdd(cnts, n0);
+    atomicAdd(cnts + 1, n1);
+  }
+}
+__global__ void k_means_from_sums(const double* sums, const unsigned long long* cnts, uint32_t d,
+                                  double* cen) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < 2 * d; e += gridDim.x * blockDim.x) {
+    const unsigned long long c = cnts[e / d];
+    cen[e] = c ? sums[e] / (double)c : 0.0;
+  }
+}
+// one block: v = y / ||y|| (v unchanged when y == 0)
+__global__ void k_normalize(const double* y, uint32_t d, double* v) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) a += y[j] * y[j];
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    a = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) red[0] = a;
+  }
+  __syncthreads();
+  const double nrm = sqrt(red[0]);
+  if (nrm > 0.0)
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) v[j] = y[j] / nrm;
+}
+// one block: lab[i] = t[i] > (min t + max t) / 2
+__global__ void k_label_by_midcut(const double* t, uint64_t cnt, uint8_t* lab) {
+  __shared__ double lo_s[32], hi_s[32];
+  double lo = INFINITY, hi = -INFINITY;
+  for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) { lo = fmin(lo, t[i]); hi = fmax(hi, t[i]); }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) { lo_s[threadIdx.x >> 5] = lo; hi_s[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) { lo = fmin(lo, lo_s[w]); hi = fmax(hi, hi_s[w]); }
+    lo_s[0] = lo;
+    hi_s[0] = hi;
+  }
+  __syncthreads();
+  const double cut = 0.5 * (lo_s[0] + hi_s[0]);
+  for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) lab[i] = t[i] > cut ? 1 : 0;
+}
+
 // Pass 2: warp per query slot; lanes own KP/32 survivors each; the `want`
 // smallest (distance, id) keys are extracted in order. Slot v is point
 // qlist[v] (qlist == nullptr: point v); candidates are indexed by slot, or by
@@ -744,7 +814,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
   // it settles.
   const double rel = (double)(d + 8) * 0x1p-52;
   // 2-means of one index list, initialised by its principal direction
-  // (PDDP), then Lloyd steps with exact means; returns false when the split
+  // (PDDP), then Lloyd steps, all on the device; returns false when the split
   // removes < 3 % of the squared error about the mean (one blob) or is
   // degenerate.
   auto bisect = [&](const std::vector<uint32_t>& seg, std::vector<uint32_t>& a0,
@@ -752,80 +822,54 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
     const uint64_t c = seg.size();
     DBuf<uint32_t> ix(c);
     DBuf<uint8_t> lab(c);
-    DBuf<double> cen(2 * d), sse(2);
+    DBuf<double> cen(2 * d), sums(2 * d), sse(4), vd(d), yd(d), td(c);
+    DBuf<unsigned long long> cnts(2);
     NB_CUDA(cudaMemcpyAsync(ix.p, seg.data(), c * 4, cudaMemcpyHostToDevice, S));
-    seq_column_means(ctx, xr.p, d, ix.p, {0}, {c}, {0}, cen.p);
     const unsigned gb = (unsigned)((c + 127) / 128);
-    // parent error: everyone to the mean (cen[1] := cen[0] for this pass)
+    const dim3 gs((unsigned)((d + 127) / 128), 64);
+    auto label_means = [&](const uint8_t* l) {
+      NB_CUDA(cudaMemsetAsync(sums.p, 0, 2 * d * 8, S));
+      NB_CUDA(cudaMemsetAsync(cnts.p, 0, 16, S));
+      k_label_sums<<<gs, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, l, sums.p, cnts.p);
+      k_means_from_sums<<<8, 256, 0, S>>>(sums.p, cnts.p, (uint32_t)d, cen.p);
+    };
+    // mean (cen[0]) and the parent error about it (sse[2..3], labels all 0)
+    label_means(nullptr);
     NB_CUDA(cudaMemcpyAsync(cen.p + d, cen.p, d * 8, cudaMemcpyDeviceToDevice, S));
-    NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
-    k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p);
-    double ps[2];
-    NB_CUDA(cudaMemcpyAsync(ps, sse.p, 16, cudaMemcpyDeviceToHost, S));
-    NB_CUDA(cudaStreamSynchronize(S));
-    const double parent = ps[0] + ps[1];
-    // principal direction of the segment (8 power steps from a fixed start);
-    // the initial centres are the means of the two sides of a cut across it
+    NB_CUDA(cudaMemsetAsync(sse.p, 0, 32, S));
+    k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p + 2);
+    // principal direction (5 power steps from a fixed start), cut across it at
+    // the middle of the projected range (separates a far fragment at one end
+    // as well as two groups of blobs), then two Lloyd steps
     {
-      DBuf<double> vd(d), yd(d), td(c);
       std::vector<double> vh(d);
       HostRng g(0x70646470 /* "pddp" */);
       for (auto& e : vh) e = g.gaussian();
-      for (int it = 0; it < 8; ++it) {
-        double nrm = 0.0;
-        for (double e : vh) nrm += e * e;
-        nrm = std::sqrt(nrm);
-        if (!(nrm > 0.0)) return false;
-        for (auto& e : vh) e /= nrm;
-        NB_CUDA(cudaMemcpyAsync(vd.p, vh.data(), d * 8, cudaMemcpyHostToDevice, S));
+      NB_CUDA(cudaMemcpyAsync(yd.p, vh.data(), d * 8, cudaMemcpyHostToDevice, S));
+      for (int it = 0; it < 5; ++it) {
+        k_normalize<<<1, 256, 0, S>>>(yd.p, (uint32_t)d, vd.p);
         k_proj_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, vd.p, td.p);
         NB_CUDA(cudaMemsetAsync(yd.p, 0, d * 8, S));
-        k_backproj_idx<<<dim3((unsigned)((d + 127) / 128), 64), 128, 0, S>>>(xr.p, ix.p, c,
-                                                                          (uint32_t)d, cen.p,
-                                                                          td.p, yd.p);
-        NB_CUDA(cudaMemcpyAsync(vh.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
-        NB_CUDA(cudaStreamSynchronize(S));
+        k_backproj_idx<<<gs, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, td.p, yd.p);
       }
-      note_launch(ctx, "k_pddp");
-      std::vector<double> th(c);
-      NB_CUDA(cudaMemcpyAsync(th.data(), td.p, c * 8, cudaMemcpyDeviceToHost, S));
-      NB_CUDA(cudaStreamSynchronize(S));
-      // cut at the middle of the projected range: separates a far fragment
-      // (a few rows at one end) as well as two groups of blobs
-      double lo = th[0], hi = th[0];
-      for (double v : th) { lo = std::min(lo, v); hi = std::max(hi, v); }
-      const double cut = 0.5 * (lo + hi);
-      a0.clear();
-      a1.clear();
-      for (uint64_t i = 0; i < c; ++i) (th[i] > cut ? a1 : a0).push_back(seg[i]);
-      if (a0.empty() || a1.empty()) return false;
-      DBuf<uint32_t> o(c);
-      std::vector<uint32_t> both(a0);
-      both.insert(both.end(), a1.begin(), a1.end());
-      NB_CUDA(cudaMemcpyAsync(o.p, both.data(), c * 4, cudaMemcpyHostToDevice, S));
-      seq_column_means(ctx, xr.p, d, o.p, {0, a0.size()}, {a0.size(), a1.size()}, {0, 1}, cen.p);
-      NB_CUDA(cudaStreamSynchronize(S));
+      k_label_by_midcut<<<1, 1024, 0, S>>>(td.p, c, lab.p);
     }
-    std::vector<uint8_t> lh(c);
-    double ss[2] = {0.0, 0.0};
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < 2; ++it) {
+      label_means(lab.p);
       NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
       k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p);
-      NB_CUDA(cudaMemcpyAsync(lh.data(), lab.p, c, cudaMemcpyDeviceToHost, S));
-      NB_CUDA(cudaMemcpyAsync(ss, sse.p, 16, cudaMemcpyDeviceToHost, S));
-      NB_CUDA(cudaStreamSynchronize(S));
-      a0.clear();
-      a1.clear();
-      for (uint64_t i = 0; i < c; ++i) (lh[i] ? a1 : a0).push_back(seg[i]);
-      if (a0.empty() || a1.empty()) return false;
-      if (it == 2) break;
-      DBuf<uint32_t> o(c);
-      std::vector<uint32_t> both(a0);
-      both.insert(both.end(), a1.begin(), a1.end());
-      NB_CUDA(cudaMemcpyAsync(o.p, both.data(), c * 4, cudaMemcpyHostToDevice, S));
-      seq_column_means(ctx, xr.p, d, o.p, {0, a0.size()}, {a0.size(), a1.size()}, {0, 1}, cen.p);
-      NB_CUDA(cudaStreamSynchronize(S));
     }
+    note_launch(ctx, "k_bisect");
+    std::vector<uint8_t> lh(c);
+    double ss[4];
+    NB_CUDA(cudaMemcpyAsync(lh.data(), lab.p, c, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaMemcpyAsync(ss, sse.p, 32, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    const double parent = ss[2] + ss[3];
+    a0.clear();
+    a1.clear();
+    for (uint64_t i = 0; i < c; ++i) (lh[i] ? a1 : a0).push_back(seg[i]);
+    if (a0.empty() || a1.empty()) return false;
     if (std::getenv("NOMAD_B200_DEBUG_KNN"))
       std::fprintf(stderr, "  bisect %llu rows: parent %.4g split %.4g (%zu / %zu)\n",
                    (unsigned long long)c, parent, ss[0] + ss[1], a0.size(), a1.size());
