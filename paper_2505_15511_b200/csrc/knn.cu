@@ -817,13 +817,15 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
   // (PDDP), then Lloyd steps, all on the device; returns false when the split
   // removes < 3 % of the squared error about the mean (one blob) or is
   // degenerate.
+  // bisection scratch, sized for the whole cluster once (cudaMalloc / cudaFree
+  // per bisection would dominate the stage)
+  DBuf<uint32_t> ix(m);
+  DBuf<uint8_t> blab(m);
+  DBuf<double> cen(2 * d), sums(2 * d), sse(4), vd(d), yd(d), td(m);
+  DBuf<unsigned long long> cnts(2);
   auto bisect = [&](const std::vector<uint32_t>& seg, std::vector<uint32_t>& a0,
                     std::vector<uint32_t>& a1) -> bool {
     const uint64_t c = seg.size();
-    DBuf<uint32_t> ix(c);
-    DBuf<uint8_t> lab(c);
-    DBuf<double> cen(2 * d), sums(2 * d), sse(4), vd(d), yd(d), td(c);
-    DBuf<unsigned long long> cnts(2);
     NB_CUDA(cudaMemcpyAsync(ix.p, seg.data(), c * 4, cudaMemcpyHostToDevice, S));
     const unsigned gb = (unsigned)((c + 127) / 128);
     const dim3 gs((unsigned)((d + 127) / 128), 64);
@@ -837,7 +839,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
     label_means(nullptr);
     NB_CUDA(cudaMemcpyAsync(cen.p + d, cen.p, d * 8, cudaMemcpyDeviceToDevice, S));
     NB_CUDA(cudaMemsetAsync(sse.p, 0, 32, S));
-    k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p + 2);
+    k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, blab.p, sse.p + 2);
     // principal direction (5 power steps from a fixed start), cut across it at
     // the middle of the projected range (separates a far fragment at one end
     // as well as two groups of blobs), then two Lloyd steps
@@ -852,17 +854,17 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
         NB_CUDA(cudaMemsetAsync(yd.p, 0, d * 8, S));
         k_backproj_idx<<<gs, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, td.p, yd.p);
       }
-      k_label_by_midcut<<<1, 1024, 0, S>>>(td.p, c, lab.p);
+      k_label_by_midcut<<<1, 1024, 0, S>>>(td.p, c, blab.p);
     }
     for (int it = 0; it < 2; ++it) {
-      label_means(lab.p);
+      label_means(blab.p);
       NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
-      k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, lab.p, sse.p);
+      k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, blab.p, sse.p);
     }
     note_launch(ctx, "k_bisect");
     std::vector<uint8_t> lh(c);
     double ss[4];
-    NB_CUDA(cudaMemcpyAsync(lh.data(), lab.p, c, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaMemcpyAsync(lh.data(), blab.p, c, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaMemcpyAsync(ss, sse.p, 32, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
     const double parent = ss[2] + ss[3];
