@@ -54,14 +54,29 @@ __global__ void k_red1(double2* p, uint32_t n, uint32_t per) {
     atomicAdd(&p[r].x, 1e-9);
   }
 }
+// lane pairs (2i, 2i+1) add to x and y of the same row in one RED.F64
+// instruction: 16 rows per warp instruction, half the instructions per row
+__global__ void k_red_pair(double2* p, uint32_t n, uint32_t per) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31;
+  double* q = reinterpret_cast<double*>(p);
+  for (uint32_t i = 0; i < per; ++i) {
+    // 2 rows per thread-pair per iteration keeps the update count equal to k_red
+    const uint32_t pair = (t >> 1);
+    const uint32_t r0 = hsh(pair * 7919u + 2 * i) % n, r1 = hsh(pair * 7919u + 2 * i + 1) % n;
+    atomicAdd(q + 2 * (uint64_t)r0 + (lane & 1), (lane & 1) ? -1e-9 : 1e-9);
+    atomicAdd(q + 2 * (uint64_t)r1 + (lane & 1), (lane & 1) ? -1e-9 : 1e-9);
+  }
+}
 int main() {
   const uint32_t n = 1250000;  // 20 MB of double2
   double2* p; cudaMalloc(&p, n * 16); cudaMemset(p, 0, n * 16);
   const uint32_t blocks = 148 * 8, threads = 256, per = 1400;  // ~424M row updates
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   float ms;
-  const char* names[5] = {"2xRED.F64", "UBLKRED16", "RMW(non-atomic)", "1xRED.F32x2", "1xRED.F64"};
-  for (int v = 0; v < 5; ++v) {
+  const char* names[6] = {"2xRED.F64", "UBLKRED16", "RMW(non-atomic)", "1xRED.F32x2", "1xRED.F64",
+                          "RED.F64 lane pairs"};
+  for (int v = 0; v < 6; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (v == 0) k_red<<<blocks, threads>>>(p, n, per);
@@ -69,6 +84,7 @@ int main() {
       if (v == 2) k_rmw<<<blocks, threads>>>(p, n, per);
       if (v == 3) k_red32x2<<<blocks, threads>>>(p, n, per);
       if (v == 4) k_red1<<<blocks, threads>>>(p, n, per);
+      if (v == 5) k_red_pair<<<blocks, threads>>>(p, n, per);
       cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
     }
     double upd = (double)blocks * threads * per;
