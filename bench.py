@@ -306,11 +306,25 @@ def main():
     achieved = BYTES_PER_HEAD * heads_local / (sgd_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
     traffic = None
+    lsu = None
     tp = os.path.join(ROOT, "profiles", "sgd_traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
         if tj.get("config") == args.config:
             traffic = tj.get("dram_bytes_per_launch")
+            if args.sgd_mode == "hogwild" and "l1_global_red_sectors_per_launch" in tj:
+                # the unit that binds this kernel: L1 -> L2 global requests
+                # (gather sectors + RED sectors, counts from the committed ncu
+                # capture, divided by this run's kernel time) against the
+                # measured RED-sector rate on an L2-resident array
+                sec = tj["l1_global_load_sectors_per_launch"] + tj["l1_global_red_sectors_per_launch"]
+                ach = sec / (sgd_ms / 1e3) / 1e9
+                lsu = {"bound": "l1->l2 global requests (gathers + RED.F64)",
+                       "sectors_per_launch": sec,
+                       "sectors_per_head": round(sec / max(heads_local, 1), 2),
+                       "achieved": ach, "peak": tj["red_sector_peak_g_per_s"], "unit": "G sectors/s",
+                       "frac": ach / tj["red_sector_peak_g_per_s"],
+                       "peak_source": tj["red_sector_peak_source"]}
 
     # end to end through the public API with host buffers: layout in (H2D),
     # K epochs (per-epoch loss D2H), layout out (D2H)
@@ -429,7 +443,8 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_sgd_hogwild" if args.sgd_mode == "hogwild" else "k_sgd_replay",
                          "kernel_ms": sgd_ms, "means_exchange_ms": (means1 - means0) / args.steps,
-                         "bytes_per_head": BYTES_PER_HEAD, "peak_source": peak_kind},
+                         "bytes_per_head": BYTES_PER_HEAD, "peak_source": peak_kind,
+                         "binding_unit": lsu},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "double_float_rows": dfrows,

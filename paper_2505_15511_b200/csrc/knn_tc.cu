@@ -38,6 +38,10 @@ constexpr int TN = 128;       // tile width of the diagnostic GEMM
 constexpr int TN2 = 256;      // candidate rows per tile (UMMA N)
 constexpr int KC = 64;        // 16-bit columns per stage (one 128B swizzle atom)
 constexpr int STAGES2 = 4;
+constexpr int QCAP = 16;     // per-thread queue of below-threshold hits (epilogue)
+#ifndef TC_EXP
+#define TC_EXP 0
+#endif
 constexpr uint32_t STAGE_BYTES = (TM + TN) * KC * 2;    // diagnostic GEMM
 constexpr uint32_t STAGE2_BYTES = (TM + TN2) * KC * 2;  // 48 KB
 
@@ -162,6 +166,9 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
         if (it >= STAGES2) tc::mbar_wait(&empty[s], ((it / STAGES2) - 1) & 1);
         const uint32_t ct = it / kchunks, kc = it % kchunks;
         uint8_t* sa = stage_mem + s * STAGE2_BYTES;
+#if TC_EXP == 2  // timing experiment: no operand traffic after the first fill
+        if (it >= STAGES2) { tc::mbar_arrive(&full[s]); continue; }
+#endif
         tc::mbar_expect_tx(&full[s], STAGE2_BYTES);
         tc::tma_load_2d(sa, &tmap, &full[s], (int32_t)(kc * KC), (int32_t)T.row0);
         tc::tma_load_2d(sa + TM * KC * 2, &tmap, &full[s], (int32_t)(kc * KC),
@@ -207,13 +214,49 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
       li[e] = 0xFFFFFFFFu;
     }
     float tau = ld[KP - 1];
+    float* qd = spill + 128 * 33;  // hit queue, [QCAP][128] (conflict-free)
+    uint8_t* qc = reinterpret_cast<uint8_t*>(qd + QCAP * 128);
+    uint32_t qn_cnt = 0, qtile = 0;
+    // insert the queued hits of tile qtile in column order (strict <, so the
+    // list equals immediate insertion)
+    auto flush = [&]() {
+      for (uint32_t i = 0; i < qn_cnt; ++i) {
+        float cd = qd[i * 128 + et];
+        if (!(cd < tau)) continue;
+        uint32_t ci = qtile * TN2 + qc[i * 128 + et];
+#pragma unroll
+        for (int e = 0; e < KP; ++e) {
+          if (cd < ld[e]) {
+            const float td = ld[e];
+            const uint32_t ti = li[e];
+            ld[e] = cd;
+            li[e] = ci;
+            cd = td;
+            ci = ti;
+          }
+        }
+        tau = ld[KP - 1];
+      }
+      qn_cnt = 0;
+    };
+    // candidate norms (invalid -> +inf), loaded one tile ahead
+    constexpr int NPT = TN2 / 128;
+    float nx[NPT];
+    auto load_norms = [&](uint32_t ct) {
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        const uint32_t cl = ct * TN2 + et + 128 * i;
+        nx[i] = cl < T.size ? __ldg(norms + T.cbase + cl) : __int_as_float(0x7f800000);
+      }
+    };
+    load_norms(0);
     for (uint32_t ct = 0; ct < ntiles; ++ct) {
       const uint32_t b = ct & 1;
+      qtile = ct;
       float* cnb = cn + b * TN2;
-      for (int j = et; j < TN2; j += 128) {  // candidate norms; invalid -> +inf
-        const uint32_t cl = ct * TN2 + j;
-        cnb[j] = cl < T.size ? norms[T.cbase + cl] : __int_as_float(0x7f800000);
-      }
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) cnb[et + 128 * i] = nx[i];
+      if (ct + 1 < ntiles) load_norms(ct + 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       tc::mbar_wait(&tfull[b], (ct >> 1) & 1);
       tc::fence_after();
@@ -222,44 +265,49 @@ __global__ void __launch_bounds__(192, 1) k_knn_tc2(const __grid_constant__ CUte
       for (int cc = 0; cc < TN2; cc += 32) {
         float v[32];
         tc::tmem_ld32(acc + cc, v);
+#if TC_EXP == 1  // timing experiment: epilogue only drains TMEM
+        continue;
+#endif
         if (!qvalid) continue;
-        // distances + below-threshold mask (straight-line); the rare
-        // insertions run afterwards from shared memory, one code copy.
+        // distances (straight-line), then the below-threshold hits
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = fmaf(-2.f, v[j], qn + cnb[cc + j]);
+        // common case: nothing in these 32 columns beats tau (min tree);
+        // the query's own column always does, once per query
+        float t[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t[j] = fminf(v[j], v[j + 16]);
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+          for (int j = 0; j < w; ++j) t[j] = fminf(t[j], t[j + w]);
+        if (!(t[0] < tau)) continue;
         uint32_t mask = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float dist = fmaf(-2.f, v[j], qn + cnb[cc + j]);
-          if (ct * TN2 + cc + j == q_local) dist = __int_as_float(0x7f800000);
-          v[j] = dist;
-          mask |= (dist < tau ? 1u : 0u) << j;
-        }
+        for (int j = 0; j < 32; ++j) mask |= (v[j] < tau ? 1u : 0u) << j;
+        // the query itself is never a candidate
+        const uint32_t self = q_local - (ct * TN2 + cc);
+        if (self < 32) mask &= ~(1u << self);
         if (mask) {
+          // queue this chunk's hits (column offset in the tile as u8); the
+          // list insertions run once per tile, so a warp pays for the lane
+          // with the most hits in the tile rather than in every chunk
           float* row = spill + et * 33;
 #pragma unroll
           for (int j = 0; j < 32; ++j) row[j] = v[j];
           while (mask) {
+            if (qn_cnt == QCAP) flush();
             const int j = __ffs(mask) - 1;
             mask &= mask - 1;
-            float cd = row[j];
-            if (!(cd < tau)) continue;
-            uint32_t ci = ct * TN2 + cc + j;
-#pragma unroll
-            for (int e = 0; e < KP; ++e) {
-              if (cd < ld[e]) {
-                const float td = ld[e];
-                const uint32_t ti = li[e];
-                ld[e] = cd;
-                li[e] = ci;
-                cd = td;
-                ci = ti;
-              }
-            }
-            tau = ld[KP - 1];
+            qd[qn_cnt * 128 + et] = row[j];
+            qc[qn_cnt * 128 + et] = (uint8_t)(cc + j);
+            ++qn_cnt;
           }
         }
       }
       tc::fence_before();
-      tc::mbar_arrive(&tempty[b]);
+      tc::mbar_arrive(&tempty[b]);  // TMEM drained; hits are in the queue
+      flush();
     }
     if (qvalid) {
       const uint32_t gq = perm_pad[T.row0 + r];
@@ -481,7 +529,7 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   cp.inv_s2 = 1.f / (scale * scale);
   cp.g64 = (float)((double)(d + 1) * 0x1p-53 * 2);
   const size_t smem = 1024 + STAGES2 * STAGE2_BYTES + 2 * TN2 * 4 + (2 * STAGES2 + 4) * 8 + 16 +
-                      128 * 33 * 4;
+                      128 * 33 * 4 + QCAP * 128 * 5;
   auto go = [&](auto kern) {
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)tiles.size(), 192, smem, S>>>(tm, tiles_d.p, norms.p, cmax_d.p, perm_d.p,
