@@ -81,12 +81,21 @@ enum nomad_b200_knn_mode {
 typedef struct nomad_b200_ctx nomad_b200_ctx;
 typedef struct nomad_b200_trainer nomad_b200_trainer;
 
-/* VectorDataset (dataset.hpp:35-44): f32 row-major rows x dims. */
+/* VectorDataset (dataset.hpp:35-44): f32 row-major rows x dims.
+ * dtype (appended; 0 from aggregate / zero initialisation = f32):
+ * NOMAD_B200_BF16 marks bf16 rows at `data` (the 60M-row configuration's
+ * storage). bf16 values widen exactly to f32, so every result equals the f32
+ * call on the widened data. Accepted by lsh_init, kmeans_em(_default_tol),
+ * default_kmeans_tol, build_knn (NOMAD_B200_KNN_BF16 mode) and knn_recall;
+ * the other entry points return NOMAD_B200_ERR_PARAMETER for bf16 views. */
+#define NOMAD_B200_F32 0
+#define NOMAD_B200_BF16 1
 typedef struct {
   uint64_t rows;
   uint64_t dims;
   const float* data;
   int32_t location;
+  int32_t dtype;
 } nomad_b200_dataset_view;
 
 /* ClusterAssignment (kmeans.hpp:32-43). Caller-owned, sized from
@@ -354,6 +363,11 @@ int32_t nomad_b200_nccl_unique_id(void* out128);
 int32_t nomad_b200_generate_mixture(nomad_b200_ctx* ctx, uint64_t rows,
                                     uint64_t dims, uint64_t blobs,
                                     double spread, uint64_t seed, float* out);
+/* The same mixture as bf16 rows (each f32 value rounded to nearest even):
+ * the storage of the 60M x 768 bf16 configuration. out: rows*dims bf16. */
+int32_t nomad_b200_generate_mixture_bf16(nomad_b200_ctx* ctx, uint64_t rows,
+                                         uint64_t dims, uint64_t blobs,
+                                         double spread, uint64_t seed, void* out);
 
 /* Diagnostic: one 128 x 128 bf16 tile product D = A B^T through the same
  * TMA + tcgen05.mma + TMEM path the bf16 kNN uses (rows rounded to bf16). */

@@ -71,7 +71,7 @@ inline nomad_b200_ctx* ctx() {
 }
 
 inline nomad_b200_dataset_view view(const VectorDataset& d) {
-  return nomad_b200_dataset_view{d.rows, d.dims, d.data.data(), NOMAD_B200_HOST};
+  return nomad_b200_dataset_view{d.rows, d.dims, d.data.data(), NOMAD_B200_HOST, NOMAD_B200_F32};
 }
 
 inline nomad_b200_clusters cview(ClusterAssignment& ca, std::size_t rows) {

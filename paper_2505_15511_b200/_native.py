@@ -30,9 +30,12 @@ class NomadError(RuntimeError):
         self.message = message
 
 
+F32, BF16 = 0, 1  # nomad_b200_dataset_view.dtype
+
+
 class DatasetView(C.Structure):
     _fields_ = [("rows", C.c_uint64), ("dims", C.c_uint64), ("data", C.c_void_p),
-                ("location", C.c_int32)]
+                ("location", C.c_int32), ("dtype", C.c_int32)]
 
 
 class ClustersView(C.Structure):
@@ -128,6 +131,8 @@ _SIGS = {
     "nomad_b200_save_layout_csv": (C.c_int32, [C.c_char_p, _vp, C.c_uint64, _vp, _vp]),
     "nomad_b200_save_layout_f64": (C.c_int32, [C.c_char_p, _vp, C.c_uint64]),
     "nomad_b200_generate_mixture": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                C.c_double, C.c_uint64, _vp]),
+    "nomad_b200_generate_mixture_bf16": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
                                                 C.c_double, C.c_uint64, _vp]),
 }
 

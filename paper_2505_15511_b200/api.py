@@ -44,9 +44,17 @@ def _view(x, dtype):
 
 
 def _dataset(data):
-    p, loc, keep = _view(data, np.float32)
+    """f32 rows, or bf16 rows when `data` is a torch.bfloat16 tensor (used in
+    place; lsh_init, kmeans_em, build_knn(mode="bf16") and knn_recall)."""
     rows, dims = (int(data.shape[0]), int(data.shape[1]))
-    return N.DatasetView(rows, dims, p, loc), keep
+    if _is_torch(data):
+        import torch
+        if data.dtype == torch.bfloat16:
+            x = data.contiguous()
+            return (N.DatasetView(rows, dims, x.data_ptr(), N.DEVICE if x.is_cuda else N.HOST,
+                                  N.BF16), x)
+    p, loc, keep = _view(data, np.float32)
+    return N.DatasetView(rows, dims, p, loc, N.F32), keep
 
 
 # ---------------------------------------------------------------- types
@@ -545,14 +553,19 @@ def pca_init(data, seed: int = 0, ctx: Optional[Context] = None, fast: bool = Fa
 
 
 def generate_mixture(rows: int, dims: int, blobs: int, spread: float = 10.0, seed: int = 42,
-                     out=None, ctx: Optional[Context] = None):
-    """Device synthetic Gaussian mixture into a CUDA float32 tensor (rows x dims)."""
+                     out=None, ctx: Optional[Context] = None, dtype: str = "f32"):
+    """Device synthetic Gaussian mixture into a CUDA tensor (rows x dims);
+    dtype "bf16": the same values rounded to bfloat16 (the 60M configuration)."""
     import torch
     cx = _ctx(ctx)
+    bf = dtype == "bf16"
+    if dtype not in ("f32", "bf16"):
+        raise NomadError("Parameter", "dtype must be 'f32' or 'bf16'")
     if out is None:
-        out = torch.empty((rows, dims), dtype=torch.float32, device=f"cuda:{cx.device}")
-    check(lib().nomad_b200_generate_mixture(cx.h, rows, dims, blobs, spread, seed,
-                                            out.data_ptr()))
+        out = torch.empty((rows, dims), dtype=torch.bfloat16 if bf else torch.float32,
+                          device=f"cuda:{cx.device}")
+    fn = lib().nomad_b200_generate_mixture_bf16 if bf else lib().nomad_b200_generate_mixture
+    check(fn(cx.h, rows, dims, blobs, spread, seed, out.data_ptr()))
     return out
 
 

@@ -1,4 +1,5 @@
 // Context, error plumbing, config defaults, NCCL id, device data generator.
+#include <cuda_bf16.h>
 #include <nccl.h>
 
 #include <cstdio>
@@ -40,7 +41,16 @@ __global__ void k_mixture_centres(float* centres, uint64_t count, float spread,
     if (q * 4 + t < count) centres[q * 4 + t] = spread * g[t];
 }
 
-__global__ void k_mixture_points(float* out, const float* centres, uint64_t rows,
+template <class T>
+__device__ __forceinline__ T to_out(float v);
+template <>
+__device__ __forceinline__ float to_out<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// T = __nv_bfloat16: the same f32 values rounded to nearest-even bf16.
+template <class T>
+__global__ void k_mixture_points(T* out, const float* centres, uint64_t rows,
                                  uint64_t dims, uint64_t blobs, uint32_t s0, uint32_t s1) {
   const uint64_t total = rows * dims;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q * 4 < total;
@@ -57,13 +67,21 @@ __global__ void k_mixture_points(float* out, const float* centres, uint64_t rows
     if ((dims & 3) == 0 && e0 + 3 < total) {
       const uint64_t i = e0 / dims, j = e0 % dims;
       const float4 c = *reinterpret_cast<const float4*>(centres + (i % blobs) * dims + j);
-      *reinterpret_cast<float4*>(out + e0) = make_float4(c.x + g[0], c.y + g[1], c.z + g[2], c.w + g[3]);
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(out + e0) =
+            make_float4(c.x + g[0], c.y + g[1], c.z + g[2], c.w + g[3]);
+      } else {
+        out[e0] = to_out<T>(c.x + g[0]);
+        out[e0 + 1] = to_out<T>(c.y + g[1]);
+        out[e0 + 2] = to_out<T>(c.z + g[2]);
+        out[e0 + 3] = to_out<T>(c.w + g[3]);
+      }
     } else {
       for (int t = 0; t < 4; ++t) {
         const uint64_t e = e0 + t;
         if (e >= total) break;
         const uint64_t i = e / dims, j = e % dims;
-        out[e] = centres[(i % blobs) * dims + j] + g[t];
+        out[e] = to_out<T>(centres[(i % blobs) * dims + j] + g[t]);
       }
     }
   }
@@ -161,9 +179,8 @@ int32_t nomad_b200_nccl_unique_id(void* out128) {
   });
 }
 
-int32_t nomad_b200_generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
-                                    uint64_t blobs, double spread, uint64_t seed,
-                                    float* out) {
+static int32_t generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims, uint64_t blobs,
+                                double spread, uint64_t seed, void* out, bool bf16) {
   return guard([&] {
     if (!c || !out) fail(kParameter, "NULL argument");
     if (rows < 1 || dims < 1 || blobs < 1) fail(kParameter, "empty mixture shape");
@@ -174,11 +191,27 @@ int32_t nomad_b200_generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t d
     k_mixture_centres<<<(unsigned)((cq + 255) / 256), 256, 0, c->stream>>>(
         centres.p, blobs * dims, (float)spread, s0, s1);
     note_launch(c, "k_mixture_centres");
-    k_mixture_points<<<c->sm_count * 8, 256, 0, c->stream>>>(out, centres.p, rows, dims,
-                                                             blobs, s0, s1);
+    if (bf16)
+      k_mixture_points<<<c->sm_count * 8, 256, 0, c->stream>>>(
+          static_cast<__nv_bfloat16*>(out), centres.p, rows, dims, blobs, s0, s1);
+    else
+      k_mixture_points<<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<float*>(out),
+                                                               centres.p, rows, dims, blobs, s0,
+                                                               s1);
     note_launch(c, "k_mixture_points");
     NB_CUDA(cudaStreamSynchronize(c->stream));
   });
+}
+
+int32_t nomad_b200_generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
+                                    uint64_t blobs, double spread, uint64_t seed, float* out) {
+  return generate_mixture(c, rows, dims, blobs, spread, seed, out, false);
+}
+
+int32_t nomad_b200_generate_mixture_bf16(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
+                                         uint64_t blobs, double spread, uint64_t seed,
+                                         void* out) {
+  return generate_mixture(c, rows, dims, blobs, spread, seed, out, true);
 }
 
 }  // extern "C"

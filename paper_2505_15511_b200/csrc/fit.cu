@@ -51,7 +51,8 @@ extern "C" int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_
       C = std::min<uint64_t>(n, std::max<uint64_t>(std::max<uint64_t>(want, cfg->workers), 2));
     }
     if (C < cfg->workers) fail(kParameter, "clusters must be >= workers");
-    nomad_b200_dataset_view dv{n, d, dd.x, NOMAD_B200_DEVICE};
+    nomad_b200_dataset_view dv{n, d, static_cast<const float*>(dd.x.p), NOMAD_B200_DEVICE,
+                               dd.x.bf ? NOMAD_B200_BF16 : NOMAD_B200_F32};
 
     DBuf<uint32_t> a(n), sizes(C);
     DBuf<double> cent(C * d);

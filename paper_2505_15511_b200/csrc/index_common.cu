@@ -74,7 +74,7 @@ __global__ void k_extract_offsets(const uint32_t* scanned, const uint32_t* hist,
 // order (lanes = columns) with the dependent fp64 adds. Order and rounding
 // are exactly k_seq_colsum's (ascending member order, one add per row).
 template <int BR>
-__global__ void __launch_bounds__(256) k_seq_colsum2(const float* __restrict__ x, uint64_t d,
+__global__ void __launch_bounds__(256) k_seq_colsum2(XPtr x, uint64_t d,
                                                      const uint32_t* members,
                                                      const uint64_t* seg_beg,
                                                      const uint64_t* seg_cnt,
@@ -96,9 +96,14 @@ __global__ void __launch_bounds__(256) k_seq_colsum2(const float* __restrict__ x
       const uint64_t t = r0 + rr;
       if (t < cnt && colok) {
         const uint64_t row = members ? members[beg + t] : beg + t;
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + rr * 33 + lane);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(x + row * d + j)
-                     : "memory");
+        if (x.bf) {  // 2-byte elements: plain load, widened into the buffer
+          dst[rr * 33 + lane] = x[row * d + j];
+        } else {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + rr * 33 + lane);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa),
+                       "l"(static_cast<const float*>(x.p) + row * d + j)
+                       : "memory");
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -150,7 +155,7 @@ void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uin
   note_launch(ctx, "k_chunk_scatter");
 }
 
-void seq_column_means(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
                       const std::vector<uint32_t>& seg_ids, double* out) {
   cudaStream_t S = ctx->stream;

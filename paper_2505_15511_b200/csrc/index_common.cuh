@@ -2,6 +2,7 @@
 // device-resident dataset views, the reference Rng on the host, stable
 // grouping of points by label, exact sequential column sums.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -87,23 +88,74 @@ __device__ __forceinline__ bool key_less(double da, uint32_t ia, double db, uint
 
 // A dataset on the device (uploaded once per call when the caller passed
 // host memory).
+// Dataset rows as kernels read them: f32 (the reference's VectorDataset) or
+// bf16 (large configurations); elements widen exactly to float, so every
+// kernel computes the same values as on the widened f32 data.
+struct XPtr {
+  const void* p = nullptr;
+  int bf = 0;
+  XPtr() = default;
+  __host__ __device__ XPtr(const float* f) : p(f), bf(0) {}  // NOLINT: f32 rows
+  __host__ __device__ XPtr(const void* q, int b) : p(q), bf(b) {}
+  __host__ __device__ XPtr operator+(uint64_t o) const {
+    XPtr r = *this;
+    r.p = bf ? (const void*)(static_cast<const __nv_bfloat16*>(p) + o)
+             : (const void*)(static_cast<const float*>(p) + o);
+    return r;
+  }
+  __device__ __forceinline__ float operator[](uint64_t i) const {
+    return bf ? __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(p) + i))
+              : __ldg(static_cast<const float*>(p) + i);
+  }
+};
+
+// ref_dist on dataset rows (both rows of one dataset)
+__device__ __forceinline__ double ref_dist(XPtr a, XPtr b, uint32_t d) {
+  if (!a.bf) return ref_dist(static_cast<const float*>(a.p), static_cast<const float*>(b.p), d);
+  double acc = 0.0;
+  for (uint32_t j = 0; j < d; ++j) {
+    const double t = __dsub_rn((double)a[j], (double)b[j]);
+    acc = __dadd_rn(acc, __dmul_rn(t, t));
+  }
+  return acc;
+}
+
+// f32 rows for the kernels that stage f32 directly (loud failure for bf16)
+inline const float* need_f32(XPtr x, const char* what) {
+  if (x.bf) fail(kParameter, std::string(what) + ": bf16 datasets are not supported here");
+  return static_cast<const float*>(x.p);
+}
+
 struct DevData {
-  const float* x = nullptr;
+  XPtr x;
   uint64_t n = 0, d = 0;
   DBuf<float> owned;
+  DBuf<uint16_t> owned16;
   void bind(const nomad_b200_dataset_view* v, cudaStream_t st) {
     if (!v || !v->data) fail(kParameter, "dataset view is NULL");
     n = v->rows;
     d = v->dims;
     if (n < 1 || d < 1) fail(kParameter, "empty dataset");
     if (n >= 0xFFFFFFFFull) fail(kSize, "point ids are u32 (n < 2^32)");
+    if (v->dtype != NOMAD_B200_F32 && v->dtype != NOMAD_B200_BF16)
+      fail(kParameter, "dataset dtype must be NOMAD_B200_F32 or NOMAD_B200_BF16");
+    x.bf = v->dtype == NOMAD_B200_BF16;
     if (v->location == NOMAD_B200_DEVICE) {
-      x = v->data;
+      x.p = v->data;
+    } else if (x.bf) {
+      owned16.alloc(n * d);
+      NB_CUDA(cudaMemcpyAsync(owned16.p, v->data, n * d * 2, cudaMemcpyHostToDevice, st));
+      x.p = owned16.p;
     } else {
       owned.alloc(n * d);
       NB_CUDA(cudaMemcpyAsync(owned.p, v->data, n * d * 4, cudaMemcpyHostToDevice, st));
-      x = owned.p;
+      x.p = owned.p;
     }
+  }
+  // f32 rows for the paths that take only f32 (loud failure for bf16)
+  const float* f32(const char* what) const {
+    if (x.bf) fail(kParameter, std::string(what) + ": bf16 datasets are not supported here");
+    return static_cast<const float*>(x.p);
   }
 };
 
@@ -118,7 +170,7 @@ void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uin
 // mean accumulation (kmeans.hpp:75-104, :176-181, :218-226) bit for bit.
 // members == nullptr means the identity list. Segments with count 0 are
 // left untouched.
-void seq_column_means(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
                       const std::vector<uint32_t>& seg_ids, double* out);
 

@@ -26,7 +26,7 @@ namespace {
 // sharing a point then combine by (distance, index) — which reproduces
 // nearest_centroid's first-minimum scan (kmeans.hpp:56-68).
 template <int PPT, int CPT>
-__global__ void __launch_bounds__(256) k_assign(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(256) k_assign(XPtr x, uint64_t n,
                                                 uint32_t d, const double* __restrict__ cent,
                                                 uint32_t C, uint32_t* assign,
                                                 unsigned long long* changes, int count_changes) {
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_assign(const float* __restrict__ x, uin
 // Rows of x staged through shared memory (coalesced), then one thread per
 // point runs its j-ascending fp64 chain: sq_dist (kmeans.hpp:47-54) to the
 // centroid `cent + cidx[i] * d` (cidx == nullptr: the single row `cent`).
-__global__ void __launch_bounds__(128) k_point_sqdist(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(128) k_point_sqdist(XPtr x, uint64_t n,
                                                       uint32_t d, const double* __restrict__ cent,
                                                       const uint32_t* cidx, double* out) {
   constexpr int TP = 128, DK = 32;
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(128) k_point_sqdist(const float* __restrict__ 
 
 // K1: LSH codes (kmeans.hpp:188-201). One thread per point; for each j the
 // centred value ((double)x_j - mean_j) feeds all planes' j-ascending chains.
-__global__ void __launch_bounds__(128) k_lsh_hash(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(128) k_lsh_hash(XPtr x, uint64_t n,
                                                   uint32_t d, const double* __restrict__ mean,
                                                   const double* __restrict__ planes, uint32_t P,
                                                   uint32_t* codes) {
@@ -223,7 +223,7 @@ __global__ void k_seq_sum(const double* v, uint64_t n, double* out) {
 
 // default_kmeans_tol accumulator (kmeans.hpp:157-161): storage-order
 // sequential sum of the exact products (double)v * v.
-__global__ void k_seq_sumsq(const float* v, uint64_t n, double* out) {
+__global__ void k_seq_sumsq(XPtr v, uint64_t n, double* out) {
   constexpr int T = 4096;
   __shared__ float buf[2][T];
   double acc = 0.0;
@@ -248,7 +248,7 @@ __global__ void k_seq_sumsq(const float* v, uint64_t n, double* out) {
 
 // Any-order parallel sum of the same exact products (for the tolerance
 // bracket); partial per block.
-__global__ void k_par_sumsq(const float* v, uint64_t n, double* part) {
+__global__ void k_par_sumsq(XPtr v, uint64_t n, double* part) {
   __shared__ double red[32];
   double acc = 0.0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -305,7 +305,7 @@ unsigned grid_for(uint64_t n, unsigned t, unsigned cap) {
 
 struct KMeans {
   nomad_b200_ctx* ctx;
-  const float* x;
+  XPtr x;
   uint64_t n, d;
   uint32_t C;
   DBuf<uint32_t> a;        // assignment
@@ -316,7 +316,7 @@ struct KMeans {
   DBuf<double> scal;       // scratch scalars
   DBuf<unsigned long long> u64s;
 
-  KMeans(nomad_b200_ctx* c, const float* xx, uint64_t nn, uint64_t dd, uint32_t CC)
+  KMeans(nomad_b200_ctx* c, XPtr xx, uint64_t nn, uint64_t dd, uint32_t CC)
       : ctx(c), x(xx), n(nn), d(dd), C(CC) {
     a.alloc(n);
     cent.alloc((uint64_t)C * d);
@@ -448,7 +448,7 @@ void KMeans::map_eq(uint32_t r, uint32_t* out) {
 }
 
 // Exact default_kmeans_tol (kmeans.hpp:157-161): one sequential chain.
-double default_tol_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d) {
+double default_tol_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d) {
   DBuf<double> o(1);
   k_seq_sumsq<<<1, 1024, 0, ctx->stream>>>(x, n * d, o.p);
   note_launch(ctx, "k_seq_sumsq");
@@ -461,7 +461,7 @@ double default_tol_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64
 // [lo, hi] bracket of default_kmeans_tol from an any-order parallel sum:
 // for N non-negative terms any summation order is within (N-1)u of the
 // exact sum, so the sequential result lies within a factor (1 +- g)^2.
-void default_tol_bracket(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+void default_tol_bracket(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                          double* lo, double* hi) {
   const uint64_t N = n * d;
   const unsigned blocks = grid_for(N, 256, 2048);

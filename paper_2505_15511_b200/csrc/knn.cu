@@ -388,8 +388,7 @@ __global__ void k_label_by_midcut(const double* t, uint64_t cnt, uint8_t* lab) {
 // candidate's chunk (row stride 65: conflict-free). `tile` = 32 x 65 + 64
 // floats per warp.
 template <int PER>
-__device__ __forceinline__ void warp_ref_dists(const float* __restrict__ x, uint32_t d,
-                                               const float* __restrict__ qrow,
+__device__ __forceinline__ void warp_ref_dists(XPtr x, uint32_t d, XPtr qrow,
                                                const uint32_t (&iv)[PER], double (&dv)[PER],
                                                float* tile) {
   const int lane = threadIdx.x & 31;
@@ -408,9 +407,9 @@ __device__ __forceinline__ void warp_ref_dists(const float* __restrict__ x, uint
       for (int c = 0; c < 32; ++c) {
         const uint32_t r = __shfl_sync(0xffffffffu, iv[e], c);
         if (r == 0xFFFFFFFFu) continue;  // warp-uniform
-        const float* row = x + (uint64_t)r * d + j0;
-        tile[c * 65 + lane] = lane < (int)w ? row[lane] : 0.f;
-        tile[c * 65 + 32 + lane] = 32 + lane < (int)w ? row[32 + lane] : 0.f;
+        const uint64_t row = (uint64_t)r * d + j0;
+        tile[c * 65 + lane] = lane < (int)w ? x[row + lane] : 0.f;
+        tile[c * 65 + 32 + lane] = 32 + lane < (int)w ? x[row + 32 + lane] : 0.f;
       }
       __syncwarp();
       if (iv[e] != 0xFFFFFFFFu) {
@@ -432,7 +431,7 @@ __device__ __forceinline__ void warp_ref_dists(const float* __restrict__ x, uint
 constexpr int RR_WARP_FLOATS = 32 * 65 + 64;  // shared floats per warp of the re-rank
 
 template <int KP>
-__global__ void k_knn_rerank(const float* __restrict__ x, uint32_t d, uint64_t nq,
+__global__ void k_knn_rerank(XPtr x, uint32_t d, uint64_t nq,
                              const uint32_t* qlist, const uint32_t* assign, const uint32_t* sizes,
                              uint32_t k, uint32_t fixed_want, const uint32_t* cand_ids,
                              const float* cand_tau, const uint32_t* cand_cnt,
@@ -511,7 +510,7 @@ void launch_rerank(uint64_t nwarps, cudaStream_t S, A... args) {
 // sorted top-`want`, merged by a block reduction. Slot / want / offsets as in
 // pass 2.
 __global__ void __launch_bounds__(128) k_knn_exhaustive(
-    const float* __restrict__ x, uint32_t d, uint64_t n_all, const uint32_t* qlist,
+    XPtr x, uint32_t d, uint64_t n_all, const uint32_t* qlist,
     const uint32_t* assign, const uint32_t* members, const uint64_t* cl_beg,
     const uint32_t* sizes, uint32_t k, uint32_t fixed_want, const uint32_t* fallback,
     const uint32_t* offsets, uint32_t* out_nb, double* out_d) {
@@ -592,7 +591,7 @@ __global__ void k_sizes2(const uint32_t* a, uint64_t n, uint32_t* sizes) {
 
 }  // namespace
 
-void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
                        DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
                        const std::vector<uint8_t>* own);
@@ -635,7 +634,7 @@ __global__ void k_merge_parts(uint32_t m, uint32_t P, uint32_t KP, const uint32_
 // tensor cores + a geometric certificate against the other sub-clusters.
 
 // Xr[i] = x[members[i]] (one cluster's rows, contiguous).
-__global__ void k_gather_rows(const float* __restrict__ x, const uint32_t* __restrict__ members,
+__global__ void k_gather_rows(XPtr x, const uint32_t* __restrict__ members,
                               uint64_t m, uint32_t d, float* __restrict__ xr) {
   const uint64_t N = m * d;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
@@ -795,7 +794,7 @@ void ffma_filter(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t
 }
 
 // Stage 1b for one cluster (members[0..m)): returns the rows it certified.
-uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t* members,
+uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                           uint64_t m, uint32_t k, int KP, DBuf<uint32_t>& cid, DBuf<float>& clb,
                           DBuf<uint32_t>& ccnt, std::vector<uint32_t>& cert_out) {
   cudaStream_t S = ctx->stream;
@@ -993,7 +992,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, const float* x, uint64_t d, const
 // own: nullptr = every cluster; else own[r] != 0 for the clusters whose lists
 // are built (multi-GPU: the clusters of this rank's shards); rows of the other
 // clusters get empty lists.
-void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                      const uint32_t* assign_d, uint32_t C, uint32_t k, KnnResult& R,
                      int mode, const std::vector<uint8_t>* own) {
   cudaStream_t S = ctx->stream;
@@ -1173,7 +1172,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
       if (nt) {
         DBuf<uint32_t> ql;
         upload_rows(qh, ql);
-        ffma_filter(ctx, x, d, mem.p, ql.p, sg, nt, KP, 0, cid.p, clb.p, ccnt.p);
+        ffma_filter(ctx, need_f32(x, "build_knn exact mode"), d, mem.p, ql.p, sg, nt, KP, 0, cid.p, clb.p, ccnt.p);
         const std::vector<uint32_t> again = rerank_rows(ql.p, qh.size());
         update_open(open, qh, again);
       }
@@ -1184,7 +1183,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
     ccnt.alloc(n);
     clb.alloc(n);
     NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
-    ffma_filter(ctx, x, d, mem.p, mem.p, segs, tiles, KP, 0, cid.p, clb.p, ccnt.p);
+    ffma_filter(ctx, need_f32(x, "build_knn exact mode"), d, mem.p, mem.p, segs, tiles, KP, 0, cid.p, clb.p, ccnt.p);
     open = rerank_rows(mem.p, n);
   }
   // stage 3: exhaustive fp64 for whatever is still uncertified
@@ -1291,6 +1290,8 @@ static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16 &&
         knn_mode != NOMAD_B200_KNN_EXACT_FFMA)
       fail(kParameter, "unknown knn_mode");
+    if (dd.x.bf && knn_mode != NOMAD_B200_KNN_BF16)
+      fail(kParameter, "build_knn: bf16 datasets take knn_mode NOMAD_B200_KNN_BF16");
     std::vector<uint8_t> own;
     if (owned) {
       own.assign(C, 0);

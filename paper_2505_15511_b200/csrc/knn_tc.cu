@@ -78,7 +78,7 @@ __device__ __forceinline__ float from16(uint16_t b) {
   else return __bfloat162float(__ushort_as_bfloat16(b));
 }
 
-__global__ void k_tc_absmax(const float* __restrict__ x, uint64_t d, const uint32_t* perm_pad,
+__global__ void k_tc_absmax(XPtr x, uint64_t d, const uint32_t* perm_pad,
                             const uint32_t* row_cl, const double* means, uint64_t rows_pad,
                             unsigned int* amax_bits) {
   const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -96,7 +96,7 @@ __global__ void k_tc_absmax(const float* __restrict__ x, uint64_t d, const uint3
 
 // 16-bit (scale * (x - mu)) into the padded copy; fp32 norms of the rounded rows.
 template <bool FP16>
-__global__ void k_tc_prep(const float* __restrict__ x, uint64_t d, uint64_t dpad,
+__global__ void k_tc_prep(XPtr x, uint64_t d, uint64_t dpad,
                           const uint32_t* __restrict__ perm_pad, const uint32_t* __restrict__ row_cl,
                           const double* __restrict__ means, uint64_t rows_pad, float scale,
                           uint16_t* __restrict__ xb, float* __restrict__ norms) {
@@ -431,49 +431,33 @@ constexpr uint32_t idesc16(uint32_t M, uint32_t N, bool fp16) {
 // Candidate generation on the tensor cores. fp16 == certified exact filter
 // (KP = 64, cand_lb = rigorous lower bound on excluded reference distances);
 // otherwise the bf16 fast filter (KP = 32, cand_lb = +inf).
-void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
-                       const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
-                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
-                       const std::vector<uint8_t>* own) {
+// One group of clusters: the padded cluster-contiguous 16-bit copy (tiles
+// never straddle a cluster start), its norms and scale, and the candidate
+// kernel; candidates land at the rows' global ids.
+static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, bool fp16, int KP,
+                     uint32_t C,
+                     const std::vector<uint64_t>& off, const std::vector<uint32_t>& mem_h,
+                     const std::vector<uint32_t>& grp, const double* means_p,
+                     DBuf<uint32_t>& cand_ids, DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt) {
   cudaStream_t S = ctx->stream;
-  const int KP = fp16 ? 64 : 32;
-  *kp_out = KP;
-  DBuf<uint32_t> mem;
-  std::vector<uint64_t> off;
-  group_by_label(ctx, assign_d, n, C, mem, off);
-  // centring vectors: the clusters' exact means (any fixed vector is valid)
-  DBuf<double> means((uint64_t)C * d);
-  NB_CUDA(cudaMemsetAsync(means.p, 0, (uint64_t)C * d * 8, S));
-  {
-    std::vector<uint64_t> beg, cnt;
-    std::vector<uint32_t> rows;
-    for (uint32_t r = 0; r < C; ++r)
-      if (off[r + 1] > off[r]) {
-        beg.push_back(off[r]);
-        cnt.push_back(off[r + 1] - off[r]);
-        rows.push_back(r);
-      }
-    seq_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
-  }
-  // padded cluster-contiguous layout (tiles never straddle a cluster start)
-  std::vector<uint32_t> mem_h(off[C]);
-  NB_CUDA(cudaMemcpy(mem_h.data(), mem.p, off[C] * 4, cudaMemcpyDeviceToHost));
-  std::vector<uint64_t> pstart(C + 1, 0);
-  for (uint32_t r = 0; r < C; ++r) pstart[r + 1] = pstart[r] + (off[r + 1] - off[r] + TM - 1) / TM * TM;
-  const uint64_t rows_pad = std::max<uint64_t>(pstart[C], TM);
+  const uint32_t G = (uint32_t)grp.size();
+  std::vector<uint64_t> pstart(G + 1, 0);
+  for (uint32_t g = 0; g < G; ++g)
+    pstart[g + 1] = pstart[g] + (off[grp[g] + 1] - off[grp[g]] + TM - 1) / TM * TM;
+  const uint64_t rows_pad = std::max<uint64_t>(pstart[G], TM);
   if (rows_pad >= (1ull << 31)) fail(kSize, "tensor-core kNN: too many rows for TMA coordinates");
-  std::vector<uint32_t> perm(rows_pad, 0xFFFFFFFFu), rcl(rows_pad, 0);
+  // rcl: the row's cluster id (means, certificate); tiles carry the group-local cluster index
+  std::vector<uint32_t> perm(rows_pad, 0xFFFFFFFFu), rcl(rows_pad, grp[0]);
   std::vector<TcTile> tiles;
-  for (uint32_t r = 0; r < C; ++r) {
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t r = grp[g];
     const uint64_t sz = off[r + 1] - off[r];
-    for (uint64_t t = 0; t < (pstart[r + 1] - pstart[r]); ++t) rcl[pstart[r] + t] = r;
-    for (uint64_t t = 0; t < sz; ++t) perm[pstart[r] + t] = mem_h[off[r] + t];
-    if (sz < 2 || (own && !(*own)[r])) continue;
+    for (uint64_t t = 0; t < (pstart[g + 1] - pstart[g]); ++t) rcl[pstart[g] + t] = r;
+    for (uint64_t t = 0; t < sz; ++t) perm[pstart[g] + t] = mem_h[off[r] + t];
     for (uint64_t q = 0; q < sz; q += TM)
-      tiles.push_back(TcTile{(uint32_t)(pstart[r] + q), (uint32_t)pstart[r], (uint32_t)sz,
+      tiles.push_back(TcTile{(uint32_t)(pstart[g] + q), (uint32_t)pstart[g], (uint32_t)sz,
                              (uint32_t)q, r});
   }
-  const uint64_t dpad = (d + KC - 1) / KC * KC;
   DBuf<uint32_t> perm_d(rows_pad), rcl_d(rows_pad);
   NB_CUDA(cudaMemcpyAsync(perm_d.p, perm.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(rcl_d.p, rcl.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
@@ -481,7 +465,7 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   DBuf<unsigned int> amax(1);
   NB_CUDA(cudaMemsetAsync(amax.p, 0, 4, S));
   const unsigned rb = (unsigned)((rows_pad * 32 + 255) / 256);
-  k_tc_absmax<<<rb, 256, 0, S>>>(x, d, perm_d.p, rcl_d.p, means.p, rows_pad, amax.p);
+  k_tc_absmax<<<rb, 256, 0, S>>>(x, d, perm_d.p, rcl_d.p, means_p, rows_pad, amax.p);
   note_launch(ctx, "k_tc_absmax");
   unsigned int ab = 0;
   NB_CUDA(cudaMemcpyAsync(&ab, amax.p, 4, cudaMemcpyDeviceToHost, S));
@@ -496,10 +480,10 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   DBuf<uint16_t> xb(rows_pad * dpad);
   DBuf<float> norms(rows_pad);
   if (fp16)
-    k_tc_prep<true><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means.p, rows_pad, scale,
+    k_tc_prep<true><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means_p, rows_pad, scale,
                                        xb.p, norms.p);
   else
-    k_tc_prep<false><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means.p, rows_pad, scale,
+    k_tc_prep<false><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means_p, rows_pad, scale,
                                         xb.p, norms.p);
   note_launch(ctx, "k_tc_prep");
   // per-cluster max ||u_b|| (scaled), for the certificate
@@ -511,10 +495,6 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   DBuf<float> cmax_d(C);
   NB_CUDA(cudaMemcpyAsync(cmax_d.p, cmax.data(), C * 4, cudaMemcpyHostToDevice, S));
 
-  cand_ids.alloc(n * (uint64_t)KP);
-  cand_lb.alloc(n);
-  cand_cnt.alloc(n);
-  NB_CUDA(cudaMemsetAsync(cand_cnt.p, 0, n * 4, S));
   if (tiles.empty()) return;
   const CUtensorMap tm = make_tmap(xb.p, rows_pad, dpad, fp16);
   DBuf<TcTile> tiles_d(tiles.size());
@@ -540,6 +520,70 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   else go(k_knn_tc2<32, false>);
   note_launch(ctx, "k_knn_tc2");
   NB_CUDA(cudaStreamSynchronize(S));
+}
+
+void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
+                       const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
+                       DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
+                       const std::vector<uint8_t>* own) {
+  cudaStream_t S = ctx->stream;
+  const int KP = fp16 ? 64 : 32;
+  *kp_out = KP;
+  DBuf<uint32_t> mem;
+  std::vector<uint64_t> off;
+  group_by_label(ctx, assign_d, n, C, mem, off);
+  // centring vectors: the clusters' exact means (any fixed vector is valid)
+  DBuf<double> means((uint64_t)C * d);
+  NB_CUDA(cudaMemsetAsync(means.p, 0, (uint64_t)C * d * 8, S));
+  {
+    std::vector<uint64_t> beg, cnt;
+    std::vector<uint32_t> rows;
+    for (uint32_t r = 0; r < C; ++r)
+      if (off[r + 1] > off[r]) {
+        beg.push_back(off[r]);
+        cnt.push_back(off[r + 1] - off[r]);
+        rows.push_back(r);
+      }
+    seq_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
+  }
+  std::vector<uint32_t> mem_h(off[C]);
+  NB_CUDA(cudaMemcpy(mem_h.data(), mem.p, off[C] * 4, cudaMemcpyDeviceToHost));
+  cand_ids.alloc(n * (uint64_t)KP);
+  cand_lb.alloc(n);
+  cand_cnt.alloc(n);
+  NB_CUDA(cudaMemsetAsync(cand_cnt.p, 0, n * 4, S));
+  const uint64_t dpad = (d + KC - 1) / KC * KC;
+  // Clusters are processed in groups whose padded 16-bit copy fits half of
+  // the free device memory (one group unless the dataset is very large, e.g.
+  // 60M x 768 bf16 next to its own 92 GB); only clusters with lists to build
+  // (size >= 2, owned) enter the copy.
+  uint64_t row_budget;
+  {
+    size_t fr = 0, tot = 0;
+    NB_CUDA(cudaMemGetInfo(&fr, &tot));
+    row_budget = std::max<uint64_t>(TM, (uint64_t)(fr / 2) / (dpad * 2 + 16));
+    row_budget = std::min<uint64_t>(row_budget, (1ull << 31) - 2 * TM);
+    if (const char* e = getenv("NOMAD_B200_TC_ROW_BUDGET"))  // tests: force several groups
+      row_budget = std::max<uint64_t>(TM, strtoull(e, nullptr, 10));
+  }
+  std::vector<uint32_t> todo;
+  for (uint32_t r = 0; r < C; ++r)
+    if (off[r + 1] - off[r] >= 2 && !(own && !(*own)[r])) todo.push_back(r);
+  size_t gi = 0;
+  while (gi < todo.size()) {
+    // one group: consecutive clusters of `todo` within the row budget
+    std::vector<uint32_t> grp;
+    uint64_t acc = 0;
+    while (gi < todo.size()) {
+      const uint32_t r = todo[gi];
+      const uint64_t pr = (off[r + 1] - off[r] + TM - 1) / TM * TM;
+      if (!grp.empty() && acc + pr > row_budget) break;
+      grp.push_back(r);
+      acc += pr;
+      ++gi;
+    }
+    tc_group(ctx, x, d, dpad, fp16, KP, C, off, mem_h, grp, means.p, cand_ids, cand_lb, cand_cnt);
+  }
 }
 
 // Unit check of the tcgen05 path: rows of a (rows x d) f32 host matrix are

@@ -458,10 +458,10 @@ static int32_t pca_entry(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* dat
     DevData dd;
     dd.bind(data, ctx->stream);
     if (location == NOMAD_B200_DEVICE) {
-      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, layout_out, fast);
+      pca_init_dev(ctx, dd.f32("pca_init"), dd.n, dd.d, seed, layout_out, fast);
     } else {
       DBuf<double> lay(2 * dd.n);
-      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, lay.p, fast);
+      pca_init_dev(ctx, dd.f32("pca_init"), dd.n, dd.d, seed, lay.p, fast);
       NB_CUDA(cudaMemcpy(layout_out, lay.p, dd.n * 16, cudaMemcpyDeviceToHost));
     }
   });
@@ -489,7 +489,7 @@ extern "C" int32_t nomad_b200_debug_cov(nomad_b200_ctx* ctx, const nomad_b200_da
     dd.bind(data, ctx->stream);
     DBuf<double> m(dd.d), c(dd.d * dd.d);
     NB_CUDA(cudaMemcpy(m.p, mean_host, dd.d * 8, cudaMemcpyHostToDevice));
-    covariance_sums(ctx, dd.x, dd.n, dd.d, m.p, c.p);
+    covariance_sums(ctx, dd.f32("covariance"), dd.n, dd.d, m.p, c.p);
     NB_CUDA(cudaMemcpy(out_host, c.p, dd.d * dd.d * 8, cudaMemcpyDeviceToHost));
   });
 }
