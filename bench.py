@@ -39,7 +39,11 @@ CONFIGS = {
     "A": (20_000, 64, 10, 5, 1),
     # one rank's share of config C at N=8 (per-rank scaling diagnostic)
     "C8": (1_250_000, 768, 8, 8, 1),
+    # 60M x 768 bf16 (256 blobs; C = 64 chosen, ~937k rows per
+    # cluster); bf16 rows on the device, bf16 tensor-core kNN
+    "E": (60_000_000, 768, 256, 64, 8),
 }
+BF16_CONFIGS = {"E"}
 
 
 def dist_env():
@@ -201,6 +205,7 @@ def main():
         dist.init_process_group("gloo", init_method="env://", rank=rank, world_size=world)
 
     n, d, blobs, ncl, W = CONFIGS[args.config]
+    bf = args.config in BF16_CONFIGS
     if W % world:
         W = world * ((W + world - 1) // world)
     k = 15
@@ -213,7 +218,9 @@ def main():
         # the hot-path index build on this GPU: lsh_init + kmeans_em identical on
         # every rank (same seeds, deterministic kernels), kNN lists only for this
         # rank's clusters; then the dataset is released
-        x = nbx.generate_mixture(n, d, blobs, 10.0, 42, ctx=ctx)
+        if bf and args.knn_mode != "bf16":
+            args.knn_mode = "bf16"  # bf16 rows: the bf16 tensor-core kNN mode
+        x = nbx.generate_mixture(n, d, blobs, 10.0, 42, ctx=ctx, dtype="bf16" if bf else "f32")
         torch.cuda.synchronize()
         t_a = time.perf_counter()
         c0 = nbx.lsh_init(x, ncl, 7, ctx=ctx)
@@ -436,6 +443,7 @@ def main():
                 "index": index,
                 "positions": ("f64 rows, fp64 arithmetic, two RED.F64 per row update"
                               if args.sgd_mode == "hogwild" else "f64 rows (replay)"),
+                "input_rows": "bf16" if bf else "f32",
                 "init": "N(0,1) layout", "parallelism": f"cluster-sharded dp{world}",
                 "l2": "inputs larger than L2 (positions 16n B + ELL 64n B > 126 MB)",
                 "setup_s": round(setup_s, 2), "final_loss": float(losses[-1])},
