@@ -516,7 +516,8 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
                                                    (uint32_t)(dpad / KC), idesc16(TM, TN2, fp16),
                                                    cp, cand_ids.p, cand_lb.p, cand_cnt.p);
   };
-  if (fp16) go(k_knn_tc2<64, true>);
+  if (fp16 && KP == 64) go(k_knn_tc2<64, true>);
+  else if (fp16) go(k_knn_tc2<32, true>);
   else go(k_knn_tc2<32, false>);
   note_launch(ctx, "k_knn_tc2");
   NB_CUDA(cudaStreamSynchronize(S));
@@ -525,9 +526,9 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
 void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
                        DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
-                       const std::vector<uint8_t>* own) {
+                       const std::vector<uint8_t>* own, int kp16) {
   cudaStream_t S = ctx->stream;
-  const int KP = fp16 ? 64 : 32;
+  const int KP = fp16 ? (kp16 == 32 ? 32 : 64) : 32;
   *kp_out = KP;
   DBuf<uint32_t> mem;
   std::vector<uint64_t> off;
