@@ -798,6 +798,16 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
                           uint64_t m, uint32_t k, int KP, DBuf<uint32_t>& cid, DBuf<float>& clb,
                           DBuf<uint32_t>& ccnt, std::vector<uint32_t>& cert_out) {
   cudaStream_t S = ctx->stream;
+  const bool dbg = std::getenv("NOMAD_B200_DEBUG_KNN") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    NB_CUDA(cudaStreamSynchronize(S));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "    1b %-22s %7.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   DBuf<float> xr(m * d);
   k_gather_rows<<<ctx->sm_count * 8, 256, 0, S>>>(x, members, m, (uint32_t)d, xr.p);
   note_launch(ctx, "k_gather_rows");
@@ -897,6 +907,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
     work.push_back(std::move(a1));
   }
   for (auto& w : work) done.push_back(std::move(w));
+  lap("gather + bisection");
   const uint32_t csub = (uint32_t)done.size();
   if (std::getenv("NOMAD_B200_DEBUG_KNN"))
     std::fprintf(stderr, "subcluster bisection: m=%llu -> %u segments\n", (unsigned long long)m, csub);
@@ -934,7 +945,9 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
   DBuf<uint32_t> cid2, ccnt2;
   DBuf<float> clb2;
   int KP2 = 0;
+  lap("labels + means");
   knn_tc_candidates(ctx, xr.p, m, d, sa.p, csub, true, cid2, clb2, ccnt2, &KP2, nullptr, 64);
+  lap("tensor-core lists");
   const uint32_t want = (uint32_t)std::min<uint64_t>(k, m - 1);
   DBuf<uint32_t> ids2(m * k), fb2(m), nfb2(1);
   DBuf<double> d2(m * k);
@@ -954,6 +967,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
   uint32_t nf2 = 0;
   NB_CUDA(cudaMemcpyAsync(&nf2, nfb2.p, 4, cudaMemcpyDeviceToHost, S));
   NB_CUDA(cudaStreamSynchronize(S));
+  lap("re-rank");
   DBuf<uint8_t> open(m);
   NB_CUDA(cudaMemsetAsync(open.p, 0, m, S));
   if (nf2) {
@@ -976,6 +990,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
   unsigned long long nc = 0;
   NB_CUDA(cudaMemcpyAsync(&nc, ncert.p, 8, cudaMemcpyDeviceToHost, S));
   NB_CUDA(cudaStreamSynchronize(S));
+  lap("radius + certify");
   if (nc) {
     const size_t o = cert_out.size();
     cert_out.resize(o + nc);
@@ -1147,7 +1162,11 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
       for (uint32_t r = 0; r < C; ++r) {
         const uint64_t sz = off[r + 1] - off[r];
         if (sz < 1024 || own && !(*own)[r] || fail_per[r] * 16 < sz) continue;
+        const auto t_sc = std::chrono::steady_clock::now();
         subcluster_stage(ctx, x, d, mem.p + off[r], sz, k, KP, cid, clb, ccnt, cert);
+        if (std::getenv("NOMAD_B200_DEBUG_KNN"))
+          std::fprintf(stderr, "    1b cluster %u: %.1f ms in total\n", r,
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_sc).count());
       }
       R.sub_certified = cert.size();
       stage_done("sub-cluster stage");
