@@ -86,8 +86,9 @@ typedef struct nomad_b200_trainer nomad_b200_trainer;
  * NOMAD_B200_BF16 marks bf16 rows at `data` (the 60M-row configuration's
  * storage). bf16 values widen exactly to f32, so every result equals the f32
  * call on the widened data. Accepted by lsh_init, kmeans_em(_default_tol),
- * default_kmeans_tol, build_knn (NOMAD_B200_KNN_BF16 mode) and knn_recall;
- * the other entry points return NOMAD_B200_ERR_PARAMETER for bf16 views. */
+ * default_kmeans_tol, build_knn (NOMAD_B200_KNN_BF16 mode), knn_recall,
+ * pca_init(_fast) and random_triplet_accuracy; the other entry points return
+ * NOMAD_B200_ERR_PARAMETER for bf16 views. */
 #define NOMAD_B200_F32 0
 #define NOMAD_B200_BF16 1
 typedef struct {

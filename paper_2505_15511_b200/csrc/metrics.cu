@@ -111,7 +111,7 @@ __global__ void k_np_low_merge(uint32_t m, uint32_t k, uint32_t P, const double*
 }
 
 // thread per triplet (a, b, c): agreement of the two orderings (:229-235).
-__global__ void k_triplet(const float* __restrict__ x, uint32_t d, const double* __restrict__ lay,
+__global__ void k_triplet(XPtr x, uint32_t d, const double* __restrict__ lay,
                           const uint32_t* __restrict__ trip, uint64_t T,
                           unsigned long long* agree) {
   const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -336,7 +336,7 @@ int32_t nomad_b200_random_triplet_accuracy(nomad_b200_ctx* ctx,
         th[3 * t + 2] = (uint32_t)c;
       }
       NB_CUDA(cudaMemcpyAsync(td.p, th.data(), 3 * T * 4, cudaMemcpyHostToDevice, S));
-      k_triplet<<<(unsigned)((T + 255) / 256), 256, 0, S>>>(dd.f32("random_triplet_accuracy"), (uint32_t)dd.d, L.p, td.p, T,
+      k_triplet<<<(unsigned)((T + 255) / 256), 256, 0, S>>>(dd.x, (uint32_t)dd.d, L.p, td.p, T,
                                                             agree.p);
       note_launch(ctx, "k_triplet");
     }

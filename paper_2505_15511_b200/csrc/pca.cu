@@ -19,7 +19,7 @@ namespace {
 
 // t_i = sum_{j ascending} ((double)x_ij - mean_j) * v_j   (pca.hpp:40-45)
 // thread per row; a 128-row x 32-column tile is staged through shared memory.
-__global__ void __launch_bounds__(128) k_pca_rows(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(128) k_pca_rows(XPtr x, uint64_t n,
                                                   uint32_t d, const double* __restrict__ mean,
                                                   const double* __restrict__ v,
                                                   double* __restrict__ t, double* __restrict__ t2,
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(128) k_pca_rows(const float* __restrict__ x, u
 // CTA per 32-column group: 8 warps stream BR-row slices (cp.async, double
 // buffer) and t; warp 0 runs the 32 column chains in order.
 template <int BR>
-__global__ void __launch_bounds__(256) k_pca_cols(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(256) k_pca_cols(XPtr x, uint64_t n,
                                                   uint32_t d, const double* __restrict__ mean,
                                                   const double* __restrict__ t,
                                                   double* __restrict__ y) {
@@ -76,9 +76,14 @@ __global__ void __launch_bounds__(256) k_pca_cols(const float* __restrict__ x, u
     for (int rr = warp; rr < BR; rr += 8) {
       const uint64_t row = r0 + rr;
       if (row < n && colok) {
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + rr * 33 + lane);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(x + row * d + j)
-                     : "memory");
+        if (x.bf) {  // 2-byte elements: plain load, widened into the buffer
+          dst[rr * 33 + lane] = x[row * d + j];
+        } else {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + rr * 33 + lane);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa),
+                       "l"(static_cast<const float*>(x.p) + row * d + j)
+                       : "memory");
+        }
       }
     }
     for (int rr = threadIdx.x; rr < BR; rr += 256)
@@ -139,7 +144,7 @@ __global__ void k_seq_col(const double* lay, uint64_t n, int comp, int mode, dou
 }
 
 // sums of (x - mean)^2 and x^2 over all entries; column sums / sq of layout
-__global__ void k_pca_moments(const float* __restrict__ x, uint64_t N, uint32_t d,
+__global__ void k_pca_moments(XPtr x, uint64_t N, uint32_t d,
                               const double* __restrict__ mean, double* out2) {
   double v = 0.0, s = 0.0;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
@@ -177,7 +182,7 @@ __global__ void k_layout_set(double* lay, uint64_t n, int comp, const double* v)
 // partials are summed per entry in slice order by k_cov_reduce
 // (deterministic).
 constexpr int CV_ROWS = 64;
-__global__ void __launch_bounds__(256) k_cov_partial(const float* __restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(256) k_cov_partial(XPtr x, uint64_t n,
                                                      uint32_t d, const double* __restrict__ mean,
                                                      const uint2* __restrict__ tiles,
                                                      uint32_t slices, double* __restrict__ part) {
@@ -251,7 +256,7 @@ double normalize(std::vector<double>& v) {
 }  // namespace
 
 // S = X_c^T X_c (d x d, fp64, row-major, symmetric) of the centred data.
-void covariance_sums(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+void covariance_sums(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                      const double* mean, double* cov) {
   cudaStream_t S = ctx->stream;
   const uint32_t nt = (uint32_t)((d + 31) / 32);
@@ -286,7 +291,7 @@ void covariance_sums(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d
 // two quantities that are both at rounding-noise level once the power
 // iteration has converged, so only the bit-exact path reproduces the
 // reference's orientation.
-void pca_init_dev(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d, uint64_t seed,
+void pca_init_dev(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d, uint64_t seed,
                   double* layout_out, bool fast) {
   cudaStream_t S = ctx->stream;
   if (n < 2) fail(kParameter, "need at least 2 rows");
@@ -458,10 +463,10 @@ static int32_t pca_entry(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* dat
     DevData dd;
     dd.bind(data, ctx->stream);
     if (location == NOMAD_B200_DEVICE) {
-      pca_init_dev(ctx, dd.f32("pca_init"), dd.n, dd.d, seed, layout_out, fast);
+      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, layout_out, fast);
     } else {
       DBuf<double> lay(2 * dd.n);
-      pca_init_dev(ctx, dd.f32("pca_init"), dd.n, dd.d, seed, lay.p, fast);
+      pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, lay.p, fast);
       NB_CUDA(cudaMemcpy(layout_out, lay.p, dd.n * 16, cudaMemcpyDeviceToHost));
     }
   });
@@ -489,7 +494,7 @@ extern "C" int32_t nomad_b200_debug_cov(nomad_b200_ctx* ctx, const nomad_b200_da
     dd.bind(data, ctx->stream);
     DBuf<double> m(dd.d), c(dd.d * dd.d);
     NB_CUDA(cudaMemcpy(m.p, mean_host, dd.d * 8, cudaMemcpyHostToDevice));
-    covariance_sums(ctx, dd.f32("covariance"), dd.n, dd.d, m.p, c.p);
+    covariance_sums(ctx, dd.x, dd.n, dd.d, m.p, c.p);
     NB_CUDA(cudaMemcpy(out_host, c.p, dd.d * dd.d * 8, cudaMemcpyDeviceToHost));
   });
 }

@@ -3,7 +3,8 @@
 bf16 values widen exactly to f32, so every index-build result on a bf16
 dataset must equal the reference's result on the widened f32 data: LSH
 seeding, k-means and the tolerance bit-identical to the oracle; the bf16-mode
-kNN graph and recall identical to the f32 call on the widened rows. Also: the
+kNN graph and recall, PCA (exact and fast) and triplet accuracy identical to
+the f32 call on the widened rows. Also: the
 grouped tensor-core copy (clusters processed in memory-bounded groups) equals
 the single-group result, and the f32-only entry points refuse bf16 views."""
 import os
@@ -80,13 +81,26 @@ def test_knn_grouped_copy_equals_single(ctx, mode, monkeypatch):
     assert np.array_equal(g1.distances, g2.distances)
 
 
+def test_pca_and_triplets_bf16_equal_widened(ctx):
+    import paper_2505_15511_b200 as nb
+    x16, xw = _bf16_pair(nb, ctx, 4000, 48, 6)
+    for fast in (False, True):
+        a = nb.pca_init(x16, 7, ctx=ctx, fast=fast)
+        b = nb.pca_init(xw, 7, ctx=ctx, fast=fast)
+        assert np.array_equal(a, b)
+    lay = nb.pca_init(xw, 7, ctx=ctx)
+    assert (nb.random_triplet_accuracy(x16, lay, 20000, 3, ctx=ctx)
+            == nb.random_triplet_accuracy(xw, lay, 20000, 3, ctx=ctx))
+
+
 def test_f32_only_paths_refuse_bf16(ctx):
     import paper_2505_15511_b200 as nb
-    x16, _ = _bf16_pair(nb, ctx, 3000, 32, 5)
+    x16, xw = _bf16_pair(nb, ctx, 3000, 32, 5)
     c = nb.kmeans_em_default_tol(x16, nb.lsh_init(x16, 4, 7, ctx=ctx), 100, ctx=ctx)
     with pytest.raises(nb.NomadError) as e:
         nb.build_knn(x16, c, 15, mode="exact", ctx=ctx)
     assert e.value.kind == "Parameter"
+    lay = nb.pca_init(xw, 7, ctx=ctx)
     with pytest.raises(nb.NomadError) as e:
-        nb.pca_init(x16, 7, ctx=ctx)
+        nb.neighborhood_preservation(x16, lay, 10, 100, 1, ctx=ctx)
     assert e.value.kind == "Parameter"
