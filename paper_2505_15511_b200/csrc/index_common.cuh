@@ -177,7 +177,7 @@ void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* m
 // Exact global kNN of m sampled points (knn.cu): out_ids_d[v * k + r] = the
 // r-th smallest (reference fp64 distance, id) key of point qlist_d[v] among
 // all other points. 1 <= k <= 56, k < n.
-void knn_global_sample(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+void knn_global_sample(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d);
 
 }  // namespace nb

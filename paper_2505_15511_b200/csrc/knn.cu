@@ -1241,7 +1241,36 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
 // distance, id) keys of point qlist_d[v], in that order (metrics.hpp:77-91
 // exact_knn_ids before its final id sort). FFMA certified filter over the
 // whole dataset -> fp64 re-rank -> exhaustive fp64 for uncertified slots.
-void knn_global_sample(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t d,
+// bf16 rows for the FFMA filter: rows ids[i] (or lo + i) widened to f32.
+__global__ void k_widen_rows(XPtr x, const uint32_t* ids, uint64_t lo, uint64_t rows, uint32_t d,
+                             float* out) {
+  const uint64_t N = rows * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = e / d, j = e % d;
+    out[e] = x[(ids ? (uint64_t)ids[r] : lo + r) * d + j];
+  }
+}
+
+// Partition `part` of a widened-chunk filter: candidate ids are scratch rows
+// (off_m + local row) -> global ids lo + local row; the query itself (it is
+// not excluded inside the scratch) is dropped. The partition bound stays
+// valid (every excluded candidate is >= it).
+__global__ void k_remap_part(uint32_t m, uint32_t P, uint32_t KP, uint32_t part, uint32_t off_m,
+                             uint64_t lo, const uint32_t* qlist, uint32_t* pid, uint32_t* pcnt) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= m) return;
+  const uint64_t o = (uint64_t)v * P + part;
+  const uint32_t c = pcnt[o], gq = qlist[v];
+  uint32_t w = 0;
+  for (uint32_t e = 0; e < c; ++e) {
+    const uint32_t id = (uint32_t)(pid[o * KP + e] - off_m + lo);
+    if (id != gq) pid[o * KP + w++] = id;
+  }
+  pcnt[o] = w;
+}
+
+void knn_global_sample(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d) {
   cudaStream_t S = ctx->stream;
   if (k < 1 || k > 56) fail(kParameter, "GPU exact kNN supports 1 <= k <= 56");
@@ -1251,15 +1280,56 @@ void knn_global_sample(nomad_b200_ctx* ctx, const float* x, uint64_t n, uint64_t
   // candidates split into P partitions so that the grid covers the GPU
   const uint32_t nt = (m + QT - 1) / QT;
   uint32_t P = 1;
-  while (P < 16 && nt * P < 2 * (uint32_t)ctx->sm_count && n / (2 * P) >= (uint64_t)CT) P *= 2;
+  if (x.bf) {
+    P = KP == 32 ? 32 : 16;  // widened chunk by chunk: the most partitions the merge takes
+    while (P > 1 && n / P < (uint64_t)CT) P /= 2;
+  } else {
+    while (P < 16 && nt * P < 2 * (uint32_t)ctx->sm_count && n / (2 * P) >= (uint64_t)CT) P *= 2;
+  }
   DBuf<uint32_t> pid((uint64_t)m * P * KP), pcnt((uint64_t)m * P);
   DBuf<float> plb((uint64_t)m * P);
-  std::vector<FilterSeg> sg;
-  for (uint32_t p = 0; p < P; ++p) {
-    const uint64_t lo = n * p / P, hi = n * (p + 1) / P;
-    sg.push_back(FilterSeg{lo, 0, (uint32_t)(hi - lo), m, nt * p, p});
+  if (!x.bf) {
+    std::vector<FilterSeg> sg;
+    for (uint32_t p = 0; p < P; ++p) {
+      const uint64_t lo = n * p / P, hi = n * (p + 1) / P;
+      sg.push_back(FilterSeg{lo, 0, (uint32_t)(hi - lo), m, nt * p, p});
+    }
+    ffma_filter(ctx, static_cast<const float*>(x.p), d, nullptr, qlist_d, sg, nt * P, (int)KP,
+                (int)P, pid.p, plb.p, pcnt.p);
+  } else {
+    // bf16 rows: the queries and a chunk of partitions at a time are widened
+    // into an f32 scratch [queries | chunk] (<= ~8 GB), filtered, and the
+    // chunk's partition lists remapped to global ids
+    uint32_t per = P;  // partitions per chunk
+    while (per > 1 && (n / P * per + m) * d * 4 > (8ull << 30)) per /= 2;
+    const uint64_t max_rows = (n + P - 1) / P * per + per;
+    DBuf<float> scr((m + max_rows) * d);
+    DBuf<uint32_t> qid(m);
+    {
+      std::vector<uint32_t> h(m);
+      for (uint32_t i = 0; i < m; ++i) h[i] = i;
+      NB_CUDA(cudaMemcpyAsync(qid.p, h.data(), m * 4, cudaMemcpyHostToDevice, S));
+    }
+    k_widen_rows<<<ctx->sm_count * 8, 256, 0, S>>>(x, qlist_d, 0, m, (uint32_t)d, scr.p);
+    note_launch(ctx, "k_widen_rows");
+    for (uint32_t p0 = 0; p0 < P; p0 += per) {
+      const uint64_t clo = n * p0 / P, chi = n * (p0 + per) / P;
+      k_widen_rows<<<ctx->sm_count * 8, 256, 0, S>>>(x, nullptr, clo, chi - clo, (uint32_t)d,
+                                                     scr.p + (uint64_t)m * d);
+      note_launch(ctx, "k_widen_rows");
+      std::vector<FilterSeg> sg;
+      for (uint32_t p = p0; p < p0 + per; ++p) {
+        const uint64_t lo = n * p / P, hi = n * (p + 1) / P;
+        sg.push_back(FilterSeg{m + (lo - clo), 0, (uint32_t)(hi - lo), m, nt * (p - p0), p});
+      }
+      ffma_filter(ctx, scr.p, d, nullptr, qid.p, sg, nt * per, (int)KP, (int)P, pid.p, plb.p,
+                  pcnt.p);
+      for (uint32_t p = p0; p < p0 + per; ++p) {
+        k_remap_part<<<(m + 127) / 128, 128, 0, S>>>(m, P, KP, p, m, clo, qlist_d, pid.p, pcnt.p);
+        note_launch(ctx, "k_remap_part");
+      }
+    }
   }
-  ffma_filter(ctx, x, d, nullptr, qlist_d, sg, nt * P, (int)KP, (int)P, pid.p, plb.p, pcnt.p);
   const uint32_t KPP = P * KP;
   DBuf<uint32_t> cid((uint64_t)m * KPP), ccnt(m), fb(m), nfb(1);
   DBuf<float> clb(m);

@@ -189,7 +189,7 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
     const uint32_t m = (uint32_t)ev.size();
     DBuf<uint32_t> ql(m), hi_ids((uint64_t)m * k), lo_ids((uint64_t)m * k);
     NB_CUDA(cudaMemcpyAsync(ql.p, ev.data(), (uint64_t)m * 4, cudaMemcpyHostToDevice, S));
-    knn_global_sample(ctx, dd.f32("neighborhood_preservation"), n, dd.d, ql.p, m, (uint32_t)k, hi_ids.p);
+    knn_global_sample(ctx, dd.x, n, dd.d, ql.p, m, (uint32_t)k, hi_ids.p);
     {
       const uint32_t bx = (m + 127) / 128;
       uint32_t P = 1;

@@ -3,8 +3,8 @@
 bf16 values widen exactly to f32, so every index-build result on a bf16
 dataset must equal the reference's result on the widened f32 data: LSH
 seeding, k-means and the tolerance bit-identical to the oracle; the bf16-mode
-kNN graph and recall, PCA (exact and fast) and triplet accuracy identical to
-the f32 call on the widened rows. Also: the
+kNN graph and recall, PCA (exact and fast), NP@k, triplet accuracy and fit()
+identical to the f32 call on the widened rows. Also: the
 grouped tensor-core copy (clusters processed in memory-bounded groups) equals
 the single-group result, and the f32-only entry points refuse bf16 views."""
 import os
@@ -93,6 +93,18 @@ def test_pca_and_triplets_bf16_equal_widened(ctx):
             == nb.random_triplet_accuracy(xw, lay, 20000, 3, ctx=ctx))
 
 
+@pytest.mark.parametrize("n,d,k", [(6000, 48, 10), (40000, 64, 30)])
+def test_neighborhood_preservation_bf16_equals_widened(ctx, n, d, k):
+    """NP@k on bf16 rows: the global high-d search widens the rows chunk by
+    chunk for the FFMA filter (many candidate partitions); same value and
+    standard error as on the widened f32 rows."""
+    import paper_2505_15511_b200 as nb
+    x16, xw = _bf16_pair(nb, ctx, n, d, 9)
+    lay = nb.pca_init(xw, 7, ctx=ctx)
+    assert (nb.neighborhood_preservation(x16, lay, k, 300, 1, ctx=ctx)
+            == nb.neighborhood_preservation(xw, lay, k, 300, 1, ctx=ctx))
+
+
 def test_f32_only_paths_refuse_bf16(ctx):
     import paper_2505_15511_b200 as nb
     x16, xw = _bf16_pair(nb, ctx, 3000, 32, 5)
@@ -100,7 +112,14 @@ def test_f32_only_paths_refuse_bf16(ctx):
     with pytest.raises(nb.NomadError) as e:
         nb.build_knn(x16, c, 15, mode="exact", ctx=ctx)
     assert e.value.kind == "Parameter"
-    lay = nb.pca_init(xw, 7, ctx=ctx)
-    with pytest.raises(nb.NomadError) as e:
-        nb.neighborhood_preservation(x16, lay, 10, 100, 1, ctx=ctx)
-    assert e.value.kind == "Parameter"
+
+
+def test_fit_bf16_rows_equals_widened(ctx):
+    """fit() end to end on bf16 rows (bf16 kNN mode, GPU PCA, replay epochs)
+    is bit-identical to fit() on the widened f32 rows."""
+    import paper_2505_15511_b200 as nb
+    x16, xw = _bf16_pair(nb, ctx, 3000, 32, 6)
+    cfg = nb.TrainConfig(epochs=3, workers=2, seed=7, knn_mode="bf16", n_clusters=4)
+    a = nb.fit(x16, cfg, ctx=ctx)
+    b = nb.fit(xw, cfg, ctx=ctx)
+    assert np.array_equal(a, b)
