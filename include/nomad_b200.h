@@ -86,10 +86,8 @@ typedef struct nomad_b200_trainer nomad_b200_trainer;
  * NOMAD_B200_BF16 marks bf16 rows at `data` (the 60M-row configuration's
  * storage). bf16 values widen exactly to f32, so every result equals the f32
  * call on the widened data. Accepted by every entry point that takes a
- * dataset (lsh_init, kmeans_em, build_knn, knn_recall, pca_init, fit, the
- * metrics), except the exact kNN modes: build_knn with NOMAD_B200_KNN_EXACT /
- * _EXACT_FFMA on bf16 rows returns NOMAD_B200_ERR_PARAMETER (use
- * NOMAD_B200_KNN_BF16). */
+ * dataset (lsh_init, kmeans_em, build_knn in every mode, knn_recall,
+ * pca_init, fit, the metrics). */
 #define NOMAD_B200_F32 0
 #define NOMAD_B200_BF16 1
 typedef struct {

@@ -1009,6 +1009,31 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
   return nc;
 }
 
+// bf16 rows for the FFMA filter: rows ids[i] (or lo + i) widened to f32.
+__global__ void k_widen_rows(XPtr x, const uint32_t* ids, uint64_t lo, uint64_t rows, uint32_t d,
+                             float* out) {
+  const uint64_t N = rows * d;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = e / d, j = e % d;
+    out[e] = x[(ids ? (uint64_t)ids[r] : lo + r) * d + j];
+  }
+}
+
+// Slot-indexed lists of one cluster's widened-row filter -> row-indexed
+// lists with global ids (members of the cluster, ascending).
+__global__ void k_scatter_slots(uint32_t qn, uint32_t KP, const uint32_t* qglob,
+                                const uint32_t* cmem, const uint32_t* tid, const float* tlb,
+                                const uint32_t* tcnt, uint32_t* cid, float* clb, uint32_t* ccnt) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= qn) return;
+  const uint64_t gq = qglob[v];
+  const uint32_t c = tcnt[v];
+  for (uint32_t e = 0; e < c; ++e) cid[gq * KP + e] = cmem[tid[(uint64_t)v * KP + e]];
+  ccnt[gq] = c;
+  clb[gq] = tlb[v];
+}
+
 // own: nullptr = every cluster; else own[r] != 0 for the clusters whose lists
 // are built (multi-GPU: the clusters of this rank's shards); rows of the other
 // clusters get empty lists.
@@ -1098,6 +1123,47 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
     dst.alloc(std::max<size_t>(rows.size(), 1));
     if (!rows.empty())
       NB_CUDA(cudaMemcpyAsync(dst.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, S));
+  };
+  // FFMA certified filter over segments of clusters (queries qh[sg.qbeg ..]
+  // are global ids, candidates the cluster's members). bf16 rows: each
+  // cluster's rows are widened into an f32 scratch and filtered in local
+  // indices (self excluded there), then scattered back to global ids.
+  std::vector<uint32_t> mem_h;
+  auto ffma_segments = [&](const std::vector<FilterSeg>& sg, uint32_t ntiles,
+                           const std::vector<uint32_t>& qh, const uint32_t* ql_d) {
+    if (!x.bf) {
+      ffma_filter(ctx, static_cast<const float*>(x.p), d, mem.p, ql_d, sg, ntiles, KP, 0, cid.p,
+                  clb.p, ccnt.p);
+      return;
+    }
+    if (mem_h.empty()) {
+      mem_h.resize(n);
+      NB_CUDA(cudaMemcpy(mem_h.data(), mem.p, n * 4, cudaMemcpyDeviceToHost));
+    }
+    for (const FilterSeg& g : sg) {
+      const uint64_t sz = g.size, qn = g.qn;
+      DBuf<float> scr(sz * d);
+      k_widen_rows<<<ctx->sm_count * 8, 256, 0, S>>>(x, mem.p + g.beg, 0, sz, (uint32_t)d, scr.p);
+      note_launch(ctx, "k_widen_rows");
+      std::vector<uint32_t> lq(qn), gq(qn);
+      for (uint64_t v = 0; v < qn; ++v) {
+        gq[v] = qh[g.qbeg + v];
+        lq[v] = (uint32_t)(std::lower_bound(mem_h.begin() + g.beg, mem_h.begin() + g.beg + sz,
+                                            gq[v]) - (mem_h.begin() + g.beg));
+      }
+      DBuf<uint32_t> lq_d, gq_d, tid(qn * KP), tcnt(qn);
+      DBuf<float> tlb(qn);
+      upload_rows(lq, lq_d);
+      upload_rows(gq, gq_d);
+      const std::vector<FilterSeg> one{FilterSeg{0, 0, (uint32_t)sz, (uint32_t)qn, 0, 0}};
+      ffma_filter(ctx, scr.p, d, nullptr, lq_d.p, one, (uint32_t)((qn + QT - 1) / QT), KP, 1,
+                  tid.p, tlb.p, tcnt.p);
+      k_scatter_slots<<<(unsigned)((qn + 127) / 128), 128, 0, S>>>(
+          (uint32_t)qn, (uint32_t)KP, gq_d.p, mem.p + g.beg, tid.p, tlb.p, tcnt.p, cid.p, clb.p,
+          ccnt.p);
+      note_launch(ctx, "k_scatter_slots");
+      NB_CUDA(cudaStreamSynchronize(S));
+    }
   };
   // open \ settled, then + the settled rows that failed again
   auto update_open = [&](std::vector<uint32_t>& open, std::vector<uint32_t> settled,
@@ -1205,7 +1271,7 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
       if (nt) {
         DBuf<uint32_t> ql;
         upload_rows(qh, ql);
-        ffma_filter(ctx, need_f32(x, "build_knn exact mode"), d, mem.p, ql.p, sg, nt, KP, 0, cid.p, clb.p, ccnt.p);
+        ffma_segments(sg, nt, qh, ql.p);
         const std::vector<uint32_t> again = rerank_rows(ql.p, qh.size());
         update_open(open, qh, again);
       }
@@ -1216,7 +1282,13 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
     ccnt.alloc(n);
     clb.alloc(n);
     NB_CUDA(cudaMemsetAsync(ccnt.p, 0, n * 4, S));
-    ffma_filter(ctx, need_f32(x, "build_knn exact mode"), d, mem.p, mem.p, segs, tiles, KP, 0, cid.p, clb.p, ccnt.p);
+    if (x.bf) {
+      std::vector<uint32_t> all(n);
+      NB_CUDA(cudaMemcpy(all.data(), mem.p, n * 4, cudaMemcpyDeviceToHost));
+      ffma_segments(segs, tiles, all, mem.p);
+    } else {
+      ffma_segments(segs, tiles, {}, mem.p);
+    }
     open = rerank_rows(mem.p, n);
   }
   // stage 3: exhaustive fp64 for whatever is still uncertified
@@ -1234,22 +1306,6 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
     note_launch(ctx, "k_knn_exhaustive");
   }
   NB_CUDA(cudaStreamSynchronize(S));
-}
-
-// Exact global kNN (over all n points, self excluded) of the m query points
-// qlist_d[0..m): out_ids_d[v * k ..] = the k smallest (reference fp64
-// distance, id) keys of point qlist_d[v], in that order (metrics.hpp:77-91
-// exact_knn_ids before its final id sort). FFMA certified filter over the
-// whole dataset -> fp64 re-rank -> exhaustive fp64 for uncertified slots.
-// bf16 rows for the FFMA filter: rows ids[i] (or lo + i) widened to f32.
-__global__ void k_widen_rows(XPtr x, const uint32_t* ids, uint64_t lo, uint64_t rows, uint32_t d,
-                             float* out) {
-  const uint64_t N = rows * d;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < N;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = e / d, j = e % d;
-    out[e] = x[(ids ? (uint64_t)ids[r] : lo + r) * d + j];
-  }
 }
 
 // Partition `part` of a widened-chunk filter: candidate ids are scratch rows
@@ -1270,6 +1326,11 @@ __global__ void k_remap_part(uint32_t m, uint32_t P, uint32_t KP, uint32_t part,
   pcnt[o] = w;
 }
 
+// Exact global kNN (over all n points, self excluded) of the m query points
+// qlist_d[0..m): out_ids_d[v * k ..] = the k smallest (reference fp64
+// distance, id) keys of point qlist_d[v], in that order (metrics.hpp:77-91
+// exact_knn_ids before its final id sort). FFMA certified filter over the
+// whole dataset -> fp64 re-rank -> exhaustive fp64 for uncertified slots.
 void knn_global_sample(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d) {
   cudaStream_t S = ctx->stream;
@@ -1393,8 +1454,6 @@ static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16 &&
         knn_mode != NOMAD_B200_KNN_EXACT_FFMA)
       fail(kParameter, "unknown knn_mode");
-    if (dd.x.bf && knn_mode != NOMAD_B200_KNN_BF16)
-      fail(kParameter, "build_knn: bf16 datasets take knn_mode NOMAD_B200_KNN_BF16");
     std::vector<uint8_t> own;
     if (owned) {
       own.assign(C, 0);

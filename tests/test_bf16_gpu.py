@@ -6,7 +6,8 @@ seeding, k-means and the tolerance bit-identical to the oracle; the bf16-mode
 kNN graph and recall, PCA (exact and fast), NP@k, triplet accuracy and fit()
 identical to the f32 call on the widened rows. Also: the
 grouped tensor-core copy (clusters processed in memory-bounded groups) equals
-the single-group result, and the f32-only entry points refuse bf16 views."""
+the single-group result, and the exact kNN modes on bf16 rows equal the exact
+f32 build on the widened rows."""
 import os
 
 import numpy as np
@@ -105,13 +106,21 @@ def test_neighborhood_preservation_bf16_equals_widened(ctx, n, d, k):
             == nb.neighborhood_preservation(xw, lay, k, 300, 1, ctx=ctx))
 
 
-def test_f32_only_paths_refuse_bf16(ctx):
+@pytest.mark.parametrize("mode", ["exact", "exact_ffma"])
+@pytest.mark.parametrize("n,d,blobs,C", [(8000, 64, 6, 6), (20000, 64, 24, 4), (3000, 768, 5, 2)])
+def test_knn_exact_modes_bf16_equal_widened(ctx, mode, n, d, blobs, C):
+    """Exact kNN on bf16 rows (tensor-core certificate, sub-cluster stage and
+    the FFMA filter on per-cluster widened copies, exhaustive fallback): ids
+    and fp64 distances identical to the exact build on the widened f32 rows
+    (which tests/test_knn_gpu.py pins to the reference)."""
     import paper_2505_15511_b200 as nb
-    x16, xw = _bf16_pair(nb, ctx, 3000, 32, 5)
-    c = nb.kmeans_em_default_tol(x16, nb.lsh_init(x16, 4, 7, ctx=ctx), 100, ctx=ctx)
-    with pytest.raises(nb.NomadError) as e:
-        nb.build_knn(x16, c, 15, mode="exact", ctx=ctx)
-    assert e.value.kind == "Parameter"
+    x16, xw = _bf16_pair(nb, ctx, n, d, blobs)
+    c = nb.kmeans_em_default_tol(xw, nb.lsh_init(xw, C, 7, ctx=ctx), 100, ctx=ctx)
+    g16 = nb.build_knn(x16, c, 15, mode=mode, ctx=ctx)
+    gw = nb.build_knn(xw, c, 15, mode=mode, ctx=ctx)
+    assert np.array_equal(g16.offsets, gw.offsets)
+    assert np.array_equal(g16.neighbors, gw.neighbors)
+    assert np.array_equal(g16.distances, gw.distances)
 
 
 def test_fit_bf16_rows_equals_widened(ctx):
