@@ -80,3 +80,24 @@ def test_config_mirror():
         nb.TrainConfig(workers=0).validate()
     with pytest.raises(nb.NomadError):
         nb.TrainConfig(workers=4, n_clusters=2).validate()
+
+
+def test_dataset_view_dtype_plumbing():
+    """The dataset view carries dtype (appended field, 0 = f32): f32 arrays and
+    tensors map to F32, torch.bfloat16 tensors to BF16 in place (no copy)."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import paper_2505_15511_b200 as nb
+    from paper_2505_15511_b200 import _native as N
+    from paper_2505_15511_b200.api import _dataset
+    assert [f[0] for f in N.DatasetView._fields_] == ["rows", "dims", "data", "location", "dtype"]
+    assert C.sizeof(N.DatasetView) == 32
+    v, _ = _dataset(np.zeros((3, 4), np.float64))
+    assert (v.rows, v.dims, v.location, v.dtype) == (3, 4, N.HOST, N.F32)
+    t = torch.zeros((5, 6), dtype=torch.bfloat16)
+    v, keep = _dataset(t)
+    assert (v.rows, v.dims, v.location, v.dtype) == (5, 6, N.HOST, N.BF16)
+    assert v.data == t.data_ptr()
+    hdr = open(os.path.join(ROOT, "include", "nomad_b200.h")).read()
+    assert "#define NOMAD_B200_BF16 1" in hdr and "#define NOMAD_B200_F32 0" in hdr
