@@ -953,7 +953,6 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
   DBuf<double> d2(m * k);
   NB_CUDA(cudaMemsetAsync(nfb2.p, 0, 4, S));
   NB_CUDA(cudaMemsetAsync(ids2.p, 0xFF, m * k * 4, S));
-  const unsigned rb = (unsigned)((m * 32 + 255) / 256);
   auto go2 = [&](auto kp) {
     launch_rerank<decltype(kp)::value>(m, S, XPtr(xr.p), (uint32_t)d, m,
                                        (const uint32_t*)nullptr, (const uint32_t*)nullptr,
