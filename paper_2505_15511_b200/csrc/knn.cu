@@ -403,13 +403,42 @@ __device__ __forceinline__ void warp_ref_dists(XPtr x, uint32_t d, XPtr qrow,
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
       __syncwarp();
+      if (!x.bf) {
+        // f32 rows: all 32 candidate rows' chunks in flight at once
+        // (cp.async, no registers held), then one wait
+        const float* xf = static_cast<const float*>(x.p);
+        for (int c = 0; c < 32; ++c) {
+          const uint32_t r = __shfl_sync(0xffffffffu, iv[e], c);
+          if (r == 0xFFFFFFFFu) continue;  // warp-uniform
+          const float* row = xf + (uint64_t)r * d + j0;
+          float* t = tile + c * 65;
+          if (lane < (int)w) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(t + lane)),
+                         "l"(row + lane)
+                         : "memory");
+          } else {
+            t[lane] = 0.f;
+          }
+          if (32 + lane < (int)w) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(t + 32 + lane)),
+                         "l"(row + 32 + lane)
+                         : "memory");
+          } else {
+            t[32 + lane] = 0.f;
+          }
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+      } else {
 #pragma unroll 4
-      for (int c = 0; c < 32; ++c) {
-        const uint32_t r = __shfl_sync(0xffffffffu, iv[e], c);
-        if (r == 0xFFFFFFFFu) continue;  // warp-uniform
-        const uint64_t row = (uint64_t)r * d + j0;
-        tile[c * 65 + lane] = lane < (int)w ? x[row + lane] : 0.f;
-        tile[c * 65 + 32 + lane] = 32 + lane < (int)w ? x[row + 32 + lane] : 0.f;
+        for (int c = 0; c < 32; ++c) {
+          const uint32_t r = __shfl_sync(0xffffffffu, iv[e], c);
+          if (r == 0xFFFFFFFFu) continue;  // warp-uniform
+          const uint64_t row = (uint64_t)r * d + j0;
+          tile[c * 65 + lane] = lane < (int)w ? x[row + lane] : 0.f;
+          tile[c * 65 + 32 + lane] = 32 + lane < (int)w ? x[row + 32 + lane] : 0.f;
+        }
       }
       __syncwarp();
       if (iv[e] != 0xFFFFFFFFu) {
