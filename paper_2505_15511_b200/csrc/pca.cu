@@ -103,7 +103,16 @@ __global__ void __launch_bounds__(256) k_pca_cols(XPtr x, uint64_t n,
       const float* src = sbuf + (b & 1) * BR * 33;
       const double* tb = ts[b & 1];
       const int mrows = (int)umin64(BR, n - b * BR);
-      for (int r = 0; r < mrows; ++r)
+      int r = 0;
+      for (; r + 8 <= mrows; r += 8) {  // products ahead of the in-order adds
+        double p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          p[u] = __dmul_rn(__dsub_rn((double)src[(r + u) * 33 + lane], m), tb[r + u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, p[u]);
+      }
+      for (; r < mrows; ++r)
         acc = __dadd_rn(acc, __dmul_rn(__dsub_rn((double)src[r * 33 + lane], m), tb[r]));
     }
     __syncthreads();
