@@ -31,8 +31,13 @@ __global__ void __launch_bounds__(256) k_assign(XPtr x, uint64_t n,
                                                 uint32_t C, uint32_t* assign,
                                                 unsigned long long* changes, int count_changes) {
   constexpr int TP = 16 * PPT, TC = 16 * CPT, DK = 32;
-  __shared__ double xs[TP][DK + 1];
-  __shared__ double cs[TC][DK + 1];
+  // dynamic: xs[TP][DK+1] doubles, cs[TC][DK+1] doubles, xf[TP*DK] f32 (the
+  // next x tile in flight by cp.async while the current one is consumed;
+  // each thread widens exactly the elements it copied)
+  extern __shared__ __align__(16) double kasm[];
+  double (*xs)[DK + 1] = reinterpret_cast<double (*)[DK + 1]>(kasm);
+  double (*cs)[DK + 1] = reinterpret_cast<double (*)[DK + 1]>(kasm + TP * (DK + 1));
+  float* xf = reinterpret_cast<float*>(kasm + (TP + TC) * (DK + 1));
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const uint64_t p0 = (uint64_t)blockIdx.x * TP;
   double best[PPT];
@@ -48,20 +53,38 @@ __global__ void __launch_bounds__(256) k_assign(XPtr x, uint64_t n,
     for (int i = 0; i < PPT; ++i)
 #pragma unroll
       for (int c = 0; c < CPT; ++c) acc[i][c] = 0.0;
-    for (uint32_t j0 = 0; j0 < d; j0 += DK) {
-      __syncthreads();
+    // x tile j0 -> xf (f32 rows: cp.async; bf16 rows: widened plain loads)
+    auto stage_x = [&](uint32_t j0) {
       for (int e = threadIdx.x; e < TP * DK; e += 256) {
         const int p = e / DK, jj = e % DK;
         const uint64_t gp = p0 + p;
         const uint32_t j = j0 + jj;
-        xs[p][jj] = (gp < n && j < d) ? (double)x[gp * d + j] : 0.0;
+        if (gp < n && j < d) {
+          if (x.bf) {
+            xf[e] = x[gp * d + j];
+          } else {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(xf + e)),
+                         "l"(static_cast<const float*>(x.p) + gp * d + j)
+                         : "memory");
+          }
+        } else {
+          xf[e] = 0.f;
+        }
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage_x(0);
+    for (uint32_t j0 = 0; j0 < d; j0 += DK) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      for (int e = threadIdx.x; e < TP * DK; e += 256) xs[e / DK][e % DK] = (double)xf[e];
       for (int e = threadIdx.x; e < TC * DK; e += 256) {
         const int r = e / DK, jj = e % DK;
         const uint32_t gr = c0 + r, j = j0 + jj;
         cs[r][jj] = (gr < C && j < d) ? cent[(uint64_t)gr * d + j] : 0.0;
       }
       __syncthreads();
+      if (j0 + DK < d) stage_x(j0 + DK);  // own elements only: already widened
       const int jmax = min(DK, (int)(d - j0));
       for (int jj = 0; jj < jmax; ++jj) {
         double xv[PPT], cv[CPT];
@@ -77,6 +100,7 @@ __global__ void __launch_bounds__(256) k_assign(XPtr x, uint64_t n,
             acc[i][c] = __dadd_rn(acc[i][c], __dmul_rn(diff, diff));
           }
       }
+      __syncthreads();  // xs / cs are rewritten by the next step
     }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -328,13 +352,15 @@ struct KMeans {
 
   void assign(bool count, unsigned long long* changes_out) {
     NB_CUDA(cudaMemsetAsync(u64s.p, 0, 8, S()));
-    auto go = [&](auto kern, int tp) {
-      kern<<<(unsigned)((n + tp - 1) / tp), 256, 0, S()>>>(x, n, (uint32_t)d, cent.p, C, a.p,
-                                                            u64s.p, count ? 1 : 0);
+    auto go = [&](auto kern, int tp, int tc) {
+      const size_t smem = (size_t)(tp + tc) * 33 * 8 + (size_t)tp * 32 * 4;
+      NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<(unsigned)((n + tp - 1) / tp), 256, smem, S()>>>(x, n, (uint32_t)d, cent.p, C, a.p,
+                                                              u64s.p, count ? 1 : 0);
     };
-    if (C > 32) go(k_assign<4, 4>, 64);
-    else if (C > 16) go(k_assign<8, 2>, 128);
-    else go(k_assign<8, 1>, 128);
+    if (C > 32) go(k_assign<4, 4>, 64, 64);
+    else if (C > 16) go(k_assign<8, 2>, 128, 32);
+    else go(k_assign<8, 1>, 128, 16);
     note_launch(ctx, "k_assign");
     if (changes_out) {
       NB_CUDA(cudaMemcpyAsync(changes_out, u64s.p, 8, cudaMemcpyDeviceToHost, S()));
