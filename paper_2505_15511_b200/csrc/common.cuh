@@ -52,6 +52,15 @@ int32_t guard(F&& f) {
   }
 }
 
+// Large device blocks (>= 64 MB) are recycled instead of returned to the
+// driver: cudaMalloc / cudaFree of GB-sized blocks occasionally stall for
+// hundreds of ms (mapping / unmapping), which made the index build's
+// per-cluster stages jittery. A released block is kept only after a device
+// synchronisation (the semantics cudaFree had), so reuse is race-free; the
+// cache is bounded and flushed when an allocation runs out of memory.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+
 // RAII device buffer on the current device.
 template <class T>
 struct DBuf {
@@ -70,10 +79,10 @@ struct DBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) NB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }

@@ -4,6 +4,8 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "philox.cuh"
@@ -14,6 +16,80 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& m) { g_last_error = m; }
 
 void bind_device(nomad_b200_ctx* c) { NB_CUDA(cudaSetDevice(c->device)); }
+
+namespace {
+constexpr size_t kCacheMin = 64ull << 20;   // blocks below this go straight to the driver
+constexpr size_t kCacheCap = 24ull << 30;   // cached bytes per device
+struct Cached {
+  void* p;
+  size_t bytes;
+};
+std::mutex g_cache_mu;
+std::vector<Cached> g_cache[64];  // per device
+size_t g_cached[64];
+
+void flush_cache(int dev) {  // caller holds the lock
+  for (auto& c : g_cache[dev]) cudaFree(c.p);
+  g_cache[dev].clear();
+  g_cached[dev] = 0;
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  int dev = 0;
+  NB_CUDA(cudaGetDevice(&dev));
+  if (bytes >= kCacheMin && dev < 64) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto& v = g_cache[dev];
+    size_t best = v.size();
+    for (size_t i = 0; i < v.size(); ++i)  // smallest block in [bytes, 1.5 bytes]
+      if (v[i].bytes >= bytes && v[i].bytes <= bytes + bytes / 2 &&
+          (best == v.size() || v[i].bytes < v[best].bytes))
+        best = i;
+    if (best != v.size()) {
+      void* p = v[best].p;
+      g_cached[dev] -= v[best].bytes;
+      v.erase(v.begin() + best);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation && dev < 64) {
+    cudaGetLastError();
+    {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      flush_cache(dev);
+    }
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess)
+    fail(kInternal, std::string("CUDA error ") + cudaGetErrorString(e) + " allocating " +
+                        std::to_string(bytes) + " bytes");
+  return p;
+}
+
+void dev_free(void* p, size_t bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || bytes < kCacheMin || dev >= 64 || bytes > kCacheCap) {
+    cudaFree(p);
+    return;
+  }
+  // a block is reused only once every kernel that may still touch it is done
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(p);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto& v = g_cache[dev];
+  while (!v.empty() && g_cached[dev] + bytes > kCacheCap) {  // evict the oldest
+    cudaFree(v.front().p);
+    g_cached[dev] -= v.front().bytes;
+    v.erase(v.begin());
+  }
+  v.push_back(Cached{p, bytes});
+  g_cached[dev] += bytes;
+}
 
 void note_launch(nomad_b200_ctx* c, const char* name) {
   ++c->launches;

@@ -1024,6 +1024,13 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
     cert_out.resize(o + nc);
     NB_CUDA(cudaMemcpy(cert_out.data() + o, crows.p, nc * 4, cudaMemcpyDeviceToHost));
   }
+  if (dbg) {
+    const auto t0 = std::chrono::steady_clock::now();
+    DBuf<float> probe(m * d);  // debug: cost of one cluster-sized allocation + free (cached)
+    probe.release();
+    std::fprintf(stderr, "    1b alloc+free %zu MB: %.1f ms\n", (size_t)(m * d * 4 >> 20),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
   if (std::getenv("NOMAD_B200_DEBUG_KNN")) {
     std::fprintf(stderr, "subcluster stage: m=%llu csub=%u open-within=%u certified=%llu sizes:",
                  (unsigned long long)m, csub, nf2, nc);
