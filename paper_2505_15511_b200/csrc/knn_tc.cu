@@ -23,6 +23,9 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -431,6 +434,21 @@ constexpr uint32_t idesc16(uint32_t M, uint32_t N, bool fp16) {
 // Candidate generation on the tensor cores. fp16 == certified exact filter
 // (KP = 64, cand_lb = rigorous lower bound on excluded reference distances);
 // otherwise the bf16 fast filter (KP = 32, cand_lb = +inf).
+// NOMAD_B200_DEBUG_KNN=2: per-step timing of the tensor-core stage
+static void tc_lap(cudaStream_t S, const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("NOMAD_B200_DEBUG_KNN");
+    return e && std::atoi(e) >= 2;
+  }();
+  if (!on) return;
+  static auto t_last = std::chrono::steady_clock::now();
+  NB_CUDA(cudaStreamSynchronize(S));
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "      tc %-20s %7.1f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - t_last).count());
+  t_last = now;
+}
+
 // One group of clusters: the padded cluster-contiguous 16-bit copy (tiles
 // never straddle a cluster start), its norms and scale, and the candidate
 // kernel; candidates land at the rows' global ids.
@@ -461,6 +479,7 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
   DBuf<uint32_t> perm_d(rows_pad), rcl_d(rows_pad);
   NB_CUDA(cudaMemcpyAsync(perm_d.p, perm.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(rcl_d.p, rcl.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
+  tc_lap(S, "layout");
   // power-of-two scale keeping |u| well inside the 16-bit range
   DBuf<unsigned int> amax(1);
   NB_CUDA(cudaMemsetAsync(amax.p, 0, 4, S));
@@ -486,6 +505,7 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
     k_tc_prep<false><<<rb, 256, 0, S>>>(x, d, dpad, perm_d.p, rcl_d.p, means_p, rows_pad, scale,
                                         xb.p, norms.p);
   note_launch(ctx, "k_tc_prep");
+  tc_lap(S, "absmax + prep");
   // per-cluster max ||u_b|| (scaled), for the certificate
   std::vector<float> nh(rows_pad), cmax(C, 0.f);
   NB_CUDA(cudaMemcpyAsync(nh.data(), norms.p, rows_pad * 4, cudaMemcpyDeviceToHost, S));
@@ -495,6 +515,7 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
   DBuf<float> cmax_d(C);
   NB_CUDA(cudaMemcpyAsync(cmax_d.p, cmax.data(), C * 4, cudaMemcpyHostToDevice, S));
 
+  tc_lap(S, "norms + cmax");
   if (tiles.empty()) return;
   const CUtensorMap tm = make_tmap(xb.p, rows_pad, dpad, fp16);
   DBuf<TcTile> tiles_d(tiles.size());
@@ -521,6 +542,7 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
   else go(k_knn_tc2<32, false>);
   note_launch(ctx, "k_knn_tc2");
   NB_CUDA(cudaStreamSynchronize(S));
+  tc_lap(S, "k_knn_tc2");
 }
 
 void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
@@ -547,6 +569,7 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
       }
     seq_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
   }
+  tc_lap(S, "grouping + means");
   std::vector<uint32_t> mem_h(off[C]);
   NB_CUDA(cudaMemcpy(mem_h.data(), mem.p, off[C] * 4, cudaMemcpyDeviceToHost));
   cand_ids.alloc(n * (uint64_t)KP);
