@@ -187,7 +187,7 @@ def main():
                     help="exact: the reference's kNN graph bit for bit (default); bf16: fast mode")
     ap.add_argument("--recall-sample", type=int, default=20000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-epochs", type=int, default=2)
+    ap.add_argument("--cpu-epochs", type=int, default=5)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
