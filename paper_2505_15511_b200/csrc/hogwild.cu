@@ -75,6 +75,23 @@ __device__ __forceinline__ void add_row(double2* pos, uint32_t i, double ax, dou
   }
 }
 
+// f64 rows, lane pairs: lanes 2i and 2i+1 of a group exchange one component
+// of their row updates and then write x and y of the SAME row in one RED.F64
+// instruction, so the two 8-byte reductions share one L1->L2 request: 2
+// instructions per two rows instead of 2 per row (tools/micro/red_bench.cu:
+// 196.8 G row-updates/s for lane pairs vs 98.1 G for 2x RED.F64 per lane,
+// profiles/r1_red_bench.txt). Called by every lane of the warp (shuffles);
+// id = 0xFFFFFFFF for no update.
+__device__ __forceinline__ void pair_red(double2* pos, uint32_t id, double ux, double uy, int e) {
+  const double recv = __shfl_xor_sync(0xffffffffu, e ? ux : uy, 1);
+  const uint32_t pid = __shfl_xor_sync(0xffffffffu, id, 1);
+  double* q = reinterpret_cast<double*>(pos);
+  const uint32_t r1 = e ? pid : id;  // the even lane's row: x by the even, y by the odd lane
+  if (r1 != 0xFFFFFFFFu) atomicAdd(q + 2 * (size_t)r1 + e, e ? recv : ux);
+  const uint32_t r2 = e ? id : pid;  // the odd lane's row
+  if (r2 != 0xFFFFFFFFu) atomicAdd(q + 2 * (size_t)r2 + e, e ? uy : recv);
+}
+
 template <int NPL>
 __device__ __forceinline__ void load_ids(const uint32_t* p, uint32_t (&v)[NPL]) {
   if constexpr (NPL == 4) {
@@ -263,6 +280,8 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
 #pragma unroll
       for (int i = 0; i < NPL; ++i) {
         const int jj = NPL * gl + i;
+        uint32_t uid = 0xFFFFFFFFu;
+        double ux = 0.0, uy = 0.0;
         if (jj < (int)cnt) {
           const double dx = h.x - pn[i].x, dy = h.y - pn[i].y;
           const double q = frcp(fma(dx, dx, fma(dy, dy, 1.0)));
@@ -275,15 +294,21 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           gy = fma(pull, dy, gy);
           if (!P.head_only) {
             const double a = st * pull;
-            add_row<DF>(P.pos, D.nb[i], a * dx, a * dy);
+            uid = D.nb[i];
+            ux = a * dx;
+            uy = a * dy;
+            if constexpr (DF) add_row<DF>(P.pos, uid, ux, uy);
           }
         }
+        if constexpr (!DF) pair_red(P.pos, uid, ux, uy, gl & 1);
       }
       bgs = gsum<G>(bgs);
       // ---- negative repulsion
       const double c2 = 2.0 * bgs * sf;
 #pragma unroll
       for (int m = 0; m < TPL; ++m) {
+        uint32_t uid = 0xFFFFFFFFu;
+        double ux = 0.0, uy = 0.0;
         if (act && gl + G * m < (int)s) {
           const double dx = h.x - pt[m].x, dy = h.y - pt[m].y;
           const double push = c2 * qn[m] * qn[m];
@@ -291,17 +316,24 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
           gy = fma(-push, dy, gy);
           if (!P.head_only) {
             const double a = -st * push;
-            add_row<DF>(P.pos, D.tl[m], a * dx, a * dy);
+            uid = D.tl[m];
+            ux = a * dx;
+            uy = a * dy;
+            if constexpr (DF) add_row<DF>(P.pos, uid, ux, uy);
           }
         }
+        if constexpr (!DF) pair_red(P.pos, uid, ux, uy, gl & 1);
       }
       // ---- mean repulsion + head update (lane 0 of the group)
       gx = gsum<G>(fma(-2.0 * bgs, s2x, gx));
       gy = gsum<G>(fma(-2.0 * bgs, s2y, gy));
-      if (act && gl == 0) {
-        add_row<DF>(P.pos, head, -st * gx, -st * gy);
-        edge_acc += (double)(cnt + s);
+      if constexpr (DF) {
+        if (act && gl == 0) add_row<DF>(P.pos, head, -st * gx, -st * gy);
+      } else {  // x by lane 0, y by lane 1 of the group: one RED.F64 instruction
+        if (act && gl < 2) atomicAdd(reinterpret_cast<double*>(P.pos) + 2 * (size_t)head + gl,
+                                     gl ? -st * gy : -st * gx);
       }
+      if (act && gl == 0) edge_acc += (double)(cnt + s);
       loss_acc += (double)lf;
       if (more) D = Dn;
     }
