@@ -326,7 +326,7 @@ def main():
                 # measured RED-sector rate on an L2-resident array
                 sec = tj["l1_global_load_sectors_per_launch"] + tj["l1_global_red_sectors_per_launch"]
                 ach = sec / (sgd_ms / 1e3) / 1e9
-                lsu = {"bound": "l1->l2 global requests (gathers + RED.F64)",
+                lsu = {"bound": "l1->l2 global requests (gather sectors + lane-pair RED.F64 sectors)",
                        "sectors_per_launch": sec,
                        "sectors_per_head": round(sec / max(heads_local, 1), 2),
                        "achieved": ach, "peak": tj["red_sector_peak_g_per_s"], "unit": "G sectors/s",
@@ -441,7 +441,7 @@ def main():
                           if args.graph == "knn" else
                           "random within-cluster k-regular graph, clusters = mixture components"),
                 "index": index,
-                "positions": ("f64 rows, fp64 arithmetic, two RED.F64 per row update"
+                "positions": ("f64 rows, fp64 arithmetic, one lane-pair RED.F64 instruction per row update"
                               if args.sgd_mode == "hogwild" else "f64 rows (replay)"),
                 "input_rows": "bf16" if bf else "f32",
                 "init": "N(0,1) layout", "parallelism": f"cluster-sharded dp{world}",
