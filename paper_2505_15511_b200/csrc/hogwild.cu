@@ -35,6 +35,8 @@
 #ifndef HOG_G16
 #define HOG_G16 4         // lanes per head when k <= 16
 #endif
+// a head needs (s + 2) / 2 Philox blocks, one per lane of its group: s <= 7 needs 4 lanes
+static_assert(HOG_G16 >= 4, "HOG_G16 < 4 cannot draw s = 7 negatives per head");
 #ifndef HOG_ROUNDS
 #define HOG_ROUNDS 8      // rounds of 256/G heads per scheduled chunk
 #endif
