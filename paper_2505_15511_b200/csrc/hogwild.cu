@@ -120,7 +120,7 @@ struct Draw {
   bool act;
 };
 
-template <int G, int KMAX, int SMAX, bool DF>
+template <int G, int KMAX, int SMAX, bool DF, bool ABO>
 __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
   constexpr int NPL = KMAX / G;            // neighbour slots per lane
   constexpr int TPL = (SMAX + G - 1) / G;  // tail slots per lane
@@ -171,12 +171,12 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       if (c >= P.total_chunks) break;
       cur = w;
       W = P.workers[w];
-      ncell = P.all_but_own ? C : W.n_rem;
+      ncell = ABO ? C : W.n_rem;
       sf_w = M * W.local_mass / (double)s;
       __syncthreads();
       for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
-        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
-        const double p = P.all_but_own ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
+        const uint32_t r = ABO ? q : P.remote_ids[W.rem_off + q];
+        const double p = ABO ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
         tmu[q] = P.means[r];  // cell means, then their weights M p_r
         tpw[q] = M * p;
       }
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       uint32_t pool0 = W.pstart, pooln = W.npts;
       D.own_gid = 0xFFFFFFFFu;
       D.sf = sf_w;
-      if (P.all_but_own) {  // optimizer.hpp:264-277
+      if constexpr (ABO) {  // optimizer.hpp:264-277
         const LocalCluster L = P.lclusters[P.cl_of[D.head]];
         pool0 = L.start;
         pooln = L.count;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       // (own cell skipped in AllButOwn mode)
       double s1 = 0.0, s2x = 0.0, s2y = 0.0;
       {
-        const uint32_t skip = P.all_but_own ? own_gid : 0xFFFFFFFFu;
+        const uint32_t skip = ABO ? own_gid : 0xFFFFFFFFu;
         uint32_t q = gl;
 #pragma unroll 2
         for (; q < ncell; q += G) {
@@ -346,7 +346,11 @@ template <int G, int KMAX, int SMAX>
 static void hog_go(const SgdParams& P0, uint32_t nblocks, size_t smem, cudaStream_t st,
                    int* per_sm) {
   const SgdParams& P = P0;
-  auto kern = P.double_float ? k_sgd_hogwild<G, KMAX, SMAX, true> : k_sgd_hogwild<G, KMAX, SMAX, false>;
+  // all-but-own-cluster ablation (optimizer.hpp:264-277) as a template flag: the default
+  // mode keeps no per-head pool / own-cell registers
+  auto kern = P.double_float
+                  ? (P.all_but_own ? k_sgd_hogwild<G, KMAX, SMAX, true, true> : k_sgd_hogwild<G, KMAX, SMAX, true, false>)
+                  : (P.all_but_own ? k_sgd_hogwild<G, KMAX, SMAX, false, true> : k_sgd_hogwild<G, KMAX, SMAX, false, false>);
   if (smem > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (per_sm) {
