@@ -24,7 +24,9 @@ def main(path, header):
     for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         print(f"{name:<60} {n:>8} {t:>10.3f} {100 * t / total:5.1f}%")
     print(f"{'total':<60} {sum(n for n, _ in agg.values()):>8} {total:>10.3f}")
-    sgd = [(k, v) for k, v in agg.items() if "k_sgd_hogwild" in k and k.endswith("0>")]
+    # headline = f64 rows: the 4th template argument (DF) is 0
+    sgd = [(k, v) for k, v in agg.items()
+           if "k_sgd_hogwild<" in k and k.split("<")[1].rstrip(">").split(",")[3].strip() == "0"]
     for k, (n, t) in sgd:
         print(f"\nheadline SGD kernel {k}: {n} launches, {t / n:.3f} ms per launch (cold-cache, serialised)")
 
