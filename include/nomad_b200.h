@@ -163,6 +163,26 @@ int32_t nomad_b200_set_stream(nomad_b200_ctx* ctx, void* cuda_stream);
 /* Number of kernels this context has launched so far (evidence counter). */
 uint64_t nomad_b200_kernel_launches(const nomad_b200_ctx* ctx);
 
+/* ------------------------------------------- multi-device group (one process)
+ * The reference's fit() drives all W workers from one call (one std::thread
+ * per worker, optimizer.hpp:327-328, :399-408). A group is the engine's
+ * equivalent: one context per entry of `devices`, driven by the calling host
+ * thread. Logical workers map to group ranks in contiguous blocks.
+ *  - all devices distinct: one NCCL communicator per device (ncclCommInitAll);
+ *    the per-epoch means exchange is ncclAllGather over NVLink / NVSwitch.
+ *  - all devices equal (e.g. {0,0,0,0}): an in-process loopback exchange
+ *    (device copies on one shared stream) — G ranks' trainers on one GPU, for
+ *    testing the G-rank math without G GPUs.
+ * Mixed lists are rejected (NOMAD_B200_ERR_PARAMETER). */
+typedef struct nomad_b200_group nomad_b200_group;
+int32_t nomad_b200_group_create(const int32_t* devices, int32_t n_devices,
+                                nomad_b200_group** out);
+int32_t nomad_b200_group_destroy(nomad_b200_group* g);
+/* Ranks in the group, and whether the exchange is the loopback form. */
+int32_t nomad_b200_group_size(const nomad_b200_group* g, int32_t* size, int32_t* loopback);
+/* Context of rank r (owned by the group; valid until group_destroy). */
+int32_t nomad_b200_group_context(nomad_b200_group* g, int32_t rank, nomad_b200_ctx** out);
+
 /* ------------------------------------------------ index build (L2) */
 /* kmeans.hpp:157-161 default_kmeans_tol */
 int32_t nomad_b200_default_kmeans_tol(nomad_b200_ctx* ctx,
@@ -265,7 +285,22 @@ int32_t nomad_b200_trainer_create(nomad_b200_ctx* ctx,
                                   int32_t rank, int32_t world_size,
                                   const void* nccl_id,
                                   nomad_b200_trainer** out);
+/* The same trainer over a group: rank r of the group trains workers
+ * [r*W/G, (r+1)*W/G) on the group's r-th context, and every trainer_* call
+ * below drives all G ranks (one epoch = every rank's SGD, then one means
+ * exchange). Results are those of a G-process run: replay mode is
+ * bit-identical for every G at fixed W. Inputs may be host buffers or
+ * device buffers on rank 0's device. */
+int32_t nomad_b200_group_trainer_create(nomad_b200_group* g,
+                                        const nomad_b200_graph* graph,
+                                        const nomad_b200_clusters* clusters,
+                                        const double* init_layout,
+                                        int32_t init_location,
+                                        const nomad_b200_train_config* cfg,
+                                        nomad_b200_trainer** out);
 int32_t nomad_b200_trainer_destroy(nomad_b200_trainer* tr);
+/* Ranks driven by this trainer object (1 for trainer_create, G for a group). */
+int32_t nomad_b200_trainer_ranks(nomad_b200_trainer* tr, int32_t* ranks);
 /* Runs the next n_epochs epochs of the cfg->epochs schedule
  * (optimizer.hpp:388-470): SGD epoch, means all-gather, mean loss.
  * epoch_loss: NULL or n_epochs doubles. */

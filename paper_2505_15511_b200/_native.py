@@ -102,6 +102,14 @@ _SIGS = {
                                               _vp, C.c_int32, C.POINTER(TrainConfigC),
                                               C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
     "nomad_b200_trainer_destroy": (C.c_int32, [_vp]),
+    "nomad_b200_group_create": (C.c_int32, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "nomad_b200_group_destroy": (C.c_int32, [_vp]),
+    "nomad_b200_group_size": (C.c_int32, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "nomad_b200_group_context": (C.c_int32, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "nomad_b200_group_trainer_create": (C.c_int32, [_vp, C.POINTER(GraphView),
+                                                    C.POINTER(ClustersView), _vp, C.c_int32,
+                                                    C.POINTER(TrainConfigC), C.POINTER(_vp)]),
+    "nomad_b200_trainer_ranks": (C.c_int32, [_vp, C.POINTER(C.c_int32)]),
     "nomad_b200_trainer_run": (C.c_int32, [_vp, C.c_uint64, _vp]),
     "nomad_b200_trainer_layout": (C.c_int32, [_vp, _vp, C.c_int32]),
     "nomad_b200_trainer_means": (C.c_int32, [_vp, _vp, _vp]),

@@ -192,13 +192,50 @@ class Context:
         check(lib().nomad_b200_set_stream(self.h, stream_ptr))
 
     def close(self) -> None:
-        if self.h:
+        if self.h and not getattr(self, "_borrowed", False):
             lib().nomad_b200_destroy(self.h)
-            self.h = None
+        self.h = None
 
 
 def _ctx(ctx: Optional[Context]) -> Context:
     return ctx if ctx is not None else Context.default()
+
+
+class Group:
+    """Several devices driven by this process (nomad_b200_group_create): the
+    one-call form of the reference's W workers (optimizer.hpp:327-328,
+    :399-408). Distinct devices are joined by NCCL (ncclCommInitAll); a
+    repeated device ([0, 0, 0, 0]) runs G ranks on one GPU with a loopback
+    exchange. Pass it to Trainer(..., group=g)."""
+
+    def __init__(self, devices):
+        devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        check(lib().nomad_b200_group_create(C.cast(devs, C.c_void_p), len(devices), C.byref(h)))
+        self.h = h
+        self.devices = list(devices)
+        n, lb = C.c_int32(), C.c_int32()
+        check(lib().nomad_b200_group_size(self.h, C.byref(n), C.byref(lb)))
+        self.size, self.loopback = n.value, bool(lb.value)
+
+    def context(self, rank: int = 0) -> "Context":
+        """Rank r's context (owned by the group) for index builds etc."""
+        h = C.c_void_p()
+        check(lib().nomad_b200_group_context(self.h, rank, C.byref(h)))
+        c = Context.__new__(Context)
+        c.device, c.h, c._borrowed = self.devices[rank], h, True
+        return c
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().nomad_b200_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- index
@@ -410,14 +447,16 @@ class Trainer:
 
     graph: KnnGraph (or a dict of device tensors offsets/neighbors), clusters:
     ClusterAssignment (assignment + n_clusters), init_layout: n x 2 f64.
-    Multi-GPU: rank/world_size and a 128-byte NCCL unique id.
+    Multi-GPU: rank/world_size and a 128-byte NCCL unique id (one process
+    per GPU), or group=Group([...]) (one process drives every rank).
     """
 
     def __init__(self, graph, clusters, init_layout, cfg: TrainConfig, rank: int = 0,
                  world_size: int = 1, nccl_id: Optional[bytes] = None,
-                 ctx: Optional[Context] = None):
+                 ctx: Optional[Context] = None, group: Optional[Group] = None):
         cfg.validate()
-        self.ctx = _ctx(ctx)
+        self.group = group
+        self.ctx = group.context(0) if group is not None else _ctx(ctx)
         self.cfg = cfg
         if isinstance(graph, KnnGraph):
             n, k = graph.rows, graph.k
@@ -443,9 +482,16 @@ class Trainer:
         c = cfg.c_struct()
         idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         h = C.c_void_p()
-        check(lib().nomad_b200_trainer_create(self.ctx.h, C.byref(gv), C.byref(cv), pl, ll,
-                                              C.byref(c), rank, world_size, idbuf, C.byref(h)))
+        if group is not None:
+            check(lib().nomad_b200_group_trainer_create(group.h, C.byref(gv), C.byref(cv), pl, ll,
+                                                        C.byref(c), C.byref(h)))
+        else:
+            check(lib().nomad_b200_trainer_create(self.ctx.h, C.byref(gv), C.byref(cv), pl, ll,
+                                                  C.byref(c), rank, world_size, idbuf, C.byref(h)))
         self.h = h
+        r = C.c_int32()
+        check(lib().nomad_b200_trainer_ranks(self.h, C.byref(r)))
+        self.ranks = r.value
 
     def run(self, n_epochs: int) -> np.ndarray:
         out = np.zeros(max(n_epochs, 1), np.float64)

@@ -102,6 +102,15 @@ struct nomad_b200_ctx {
   uint64_t knn_tc_uncertified = 0, knn_exhaustive = 0, knn_sub_certified = 0;
 };
 
+// A set of contexts driven by one host thread (nomad_b200_group_create):
+// distinct devices joined by NCCL communicators, or G contexts on one device
+// sharing one stream (loopback exchange).
+struct nomad_b200_group {
+  std::vector<nomad_b200_ctx*> ctx;  // owned, one per rank
+  std::vector<void*> comm;           // ncclComm_t per rank (distinct devices), else empty
+  bool loopback = false;
+};
+
 namespace nb {
 // Makes ctx's device current for this host thread.
 void bind_device(nomad_b200_ctx* c);

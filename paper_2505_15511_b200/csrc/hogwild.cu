@@ -174,12 +174,13 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       ncell = ABO ? C : W.n_rem;
       sf_w = M * W.local_mass / (double)s;
       __syncthreads();
-      for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
-        const uint32_t r = ABO ? q : P.remote_ids[W.rem_off + q];
-        const double p = ABO ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
-        tmu[q] = P.means[r];  // cell means, then their weights M p_r
-        tpw[q] = M * p;
-      }
+      if (!P.gcells)
+        for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
+          const uint32_t r = ABO ? q : P.remote_ids[W.rem_off + q];
+          const double p = ABO ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
+          tmu[q] = P.means[r];  // cell means, then their weights M p_r
+          tpw[q] = M * p;
+        }
       __syncthreads();
     }
     const uint32_t t_base = lchunk * P.chunk_heads;
@@ -247,19 +248,27 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       double s1 = 0.0, s2x = 0.0, s2y = 0.0;
       {
         const uint32_t skip = ABO ? own_gid : 0xFFFFFFFFu;
-        uint32_t q = gl;
+        // cell table in shared memory, or (many clusters) this worker's row
+        // of the global tables; inlined twice so each loop keeps its space
+        auto field = [&](const double2* mu, const double* wv) {
+          uint32_t q = gl;
 #pragma unroll 2
-        for (; q < ncell; q += G) {
-          const double2 ma = tmu[q];
-          const double wa = q == skip ? 0.0 : tpw[q];
-          const double ax = h.x - ma.x, ay = h.y - ma.y;
-          const double qa = frcp(fma(ax, ax, fma(ay, ay, 1.0)));
-          const double pa = wa * qa;
-          s1 += pa;
-          const double pa2 = pa * qa;
-          s2x = fma(pa2, ax, s2x);
-          s2y = fma(pa2, ay, s2y);
-        }
+          for (; q < ncell; q += G) {
+            const double2 ma = mu[q];
+            const double wa = q == skip ? 0.0 : wv[q];
+            const double ax = h.x - ma.x, ay = h.y - ma.y;
+            const double qa = frcp(fma(ax, ax, fma(ay, ay, 1.0)));
+            const double pa = wa * qa;
+            s1 += pa;
+            const double pa2 = pa * qa;
+            s2x = fma(pa2, ax, s2x);
+            s2y = fma(pa2, ay, s2y);
+          }
+        };
+        if (P.gcells)
+          field(P.gcell_mu + (size_t)cur * P.max_cells, P.gcell_w + (size_t)cur * P.max_cells);
+        else
+          field(tmu, tpw);
       }
       // ---- sampled negatives
       double qn[TPL], qsum = 0.0;

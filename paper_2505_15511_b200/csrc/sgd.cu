@@ -30,15 +30,18 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
   const uint32_t w = blockIdx.x / K, part = blockIdx.x % K;
   const WorkerDev W = P.workers[w];
   const uint32_t k = P.k, s = P.s, C = P.n_clusters;
-  // shared tables: weights (k+1)*k, then means/probs of all C cells
+  // shared tables: weights (k+1)*k, then means/probs of all C cells (or,
+  // when 3C doubles do not fit, the same [C][3] table in global memory)
   double* wt = sm;
-  double* cm = sm + (k + 1) * k;  // 3*C: mu.x, mu.y, p
+  double* cms = sm + (k + 1) * k;  // 3*C: mu.x, mu.y, p
   for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
-  for (uint32_t r = threadIdx.x; r < C; r += blockDim.x) {
-    cm[3 * r] = P.means[r].x;
-    cm[3 * r + 1] = P.means[r].y;
-    cm[3 * r + 2] = P.cell_probs[r];
-  }
+  if (!P.gcells)
+    for (uint32_t r = threadIdx.x; r < C; r += blockDim.x) {
+      cms[3 * r] = P.means[r].x;
+      cms[3 * r + 1] = P.means[r].y;
+      cms[3 * r + 2] = P.cell_probs[r];
+    }
+  const double* cm = P.gcells ? P.cm3 : cms;
   __syncthreads();
   const double M = (double)P.m_total;
   const uint32_t lvl0 = P.wk_lvl_base[w], nlev = P.wk_nlev[w];
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
         v.y = __dsub_rn(v.y, __dmul_rn(st, ay));
         P.pos[p] = v;
         if (diverged(v.x, v.y))
-          atomicMin(P.diverge, ((unsigned long long)t * stride + u) << 32 | p);
+          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | p);
         ++u;
       };
       apply(head, gx, gy);
@@ -255,25 +258,56 @@ __global__ void k_means_unpack(const double* recv, const uint32_t* slot_gid, uin
   if (gid != 0xFFFFFFFFu) means[gid] = make_double2(recv[2 * g], recv[2 * g + 1]);
 }
 
-// Local ELL graph in local ids from the global CSR in original ids.
+// Local ELL graph in local ids from the global CSR in original ids. A list
+// longer than k, or a neighbour that is not a point of the row's own worker
+// shard (another rank's, or another worker's on this rank), is rejected:
+// positive edges stay inside a shard (optimizer.hpp:292-300).
 __global__ void k_build_ell(const uint32_t* offsets, const uint32_t* nbrs,
-                            const uint32_t* orig_of, const uint32_t* new_of, uint32_t n_loc,
-                            uint32_t kpad, uint32_t* ell, uint8_t* ncnt,
+                            const uint32_t* orig_of, const uint32_t* new_of,
+                            const uint32_t* cl_of, const LocalCluster* lcl, uint32_t n_loc,
+                            uint32_t k, uint32_t kpad, uint32_t* ell, uint8_t* ncnt,
                             unsigned long long* bad) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_loc) return;
   const uint32_t o = orig_of[i];
   const uint32_t b = offsets[o], c = offsets[o + 1] - b;
-  if (c > kpad) { atomicMin(bad, (unsigned long long)i); return; }
+  if (c > k) { atomicMin(bad, (unsigned long long)i); return; }
+  const uint32_t wi = lcl[cl_of[i]].worker;
   for (uint32_t t = 0; t < kpad; ++t) {
     uint32_t v = i;  // pad with self (never read beyond count)
     if (t < c) {
       v = new_of[nbrs[b + t]];
-      if (v == 0xFFFFFFFFu) { atomicMin(bad, (unsigned long long)i); v = i; }
+      if (v == 0xFFFFFFFFu || lcl[cl_of[v]].worker != wi) {
+        atomicMin(bad, (unsigned long long)i);
+        v = i;
+      }
     }
     ell[(size_t)i * kpad + t] = v;
   }
   if (ncnt) ncnt[i] = (uint8_t)c;
+}
+
+// Global-memory cell tables (see launch_cell_tables).
+__global__ void k_cell_tables(const double2* means, const WorkerDev* wk, uint32_t nwl,
+                              const uint32_t* remote_ids, const double* remote_probs,
+                              const double* cell_probs, uint32_t C, int abo, double M,
+                              uint32_t stride, double2* gmu, double* gw, double* cm3) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.y == nwl) {  // replay table
+    if (q < C) {
+      cm3[3 * (size_t)q] = means[q].x;
+      cm3[3 * (size_t)q + 1] = means[q].y;
+      cm3[3 * (size_t)q + 2] = cell_probs[q];
+    }
+    return;
+  }
+  const WorkerDev W = wk[blockIdx.y];
+  const uint32_t ncell = abo ? C : W.n_rem;
+  if (q >= ncell) return;
+  const uint32_t r = abo ? q : remote_ids[W.rem_off + q];
+  const double p = abo ? cell_probs[r] : remote_probs[W.rem_off + q];
+  gmu[(size_t)blockIdx.y * stride + q] = means[r];
+  gw[(size_t)blockIdx.y * stride + q] = M * p;
 }
 
 // Layout in original order: out[orig_of[i]] = pos[i].
@@ -349,10 +383,20 @@ void launch_means_unpack(const double* recv, const uint32_t* slot_gid, uint32_t 
 }
 
 void launch_build_ell(const uint32_t* offsets, const uint32_t* nbrs, const uint32_t* orig_of,
-                      const uint32_t* new_of, uint32_t n_loc, uint32_t kpad, uint32_t* ell,
-                      uint8_t* ncnt, unsigned long long* bad, cudaStream_t st) {
-  k_build_ell<<<blocks_for(n_loc, 256), 256, 0, st>>>(offsets, nbrs, orig_of, new_of, n_loc,
-                                                      kpad, ell, ncnt, bad);
+                      const uint32_t* new_of, const uint32_t* cl_of, const LocalCluster* lcl,
+                      uint32_t n_loc, uint32_t k, uint32_t kpad, uint32_t* ell, uint8_t* ncnt,
+                      unsigned long long* bad, cudaStream_t st) {
+  k_build_ell<<<blocks_for(n_loc, 256), 256, 0, st>>>(offsets, nbrs, orig_of, new_of, cl_of, lcl,
+                                                      n_loc, k, kpad, ell, ncnt, bad);
+}
+
+void launch_cell_tables(const double2* means, const WorkerDev* wk, uint32_t nwl,
+                        const uint32_t* remote_ids, const double* remote_probs,
+                        const double* cell_probs, uint32_t C, int all_but_own, double M,
+                        uint32_t stride, double2* gmu, double* gw, double* cm3, cudaStream_t st) {
+  const dim3 grid(blocks_for(std::max<uint32_t>(std::max(stride, C), 1), 128), nwl + 1);
+  k_cell_tables<<<grid, 128, 0, st>>>(means, wk, nwl, remote_ids, remote_probs, cell_probs, C,
+                                      all_but_own, M, stride, gmu, gw, cm3);
 }
 
 void launch_scatter_layout(const double2* pos, const uint32_t* orig_of, uint32_t n_loc,

@@ -44,11 +44,18 @@ struct SgdParams {
   const double* cell_probs;     // global C: size_r / n
   double* loss_acc;             // per local worker
   unsigned long long* edge_acc; // per local worker: sum of |N(h)| + s
-  unsigned long long* diverge;  // first offending key (replay: t * stride + u)
+  unsigned long long* diverge;  // first offending key (hogwild: one; replay: one per local
+                                // worker, (t * stride + u) << 32 | local point)
   uint32_t n_workers, kpad, k, s, m_total, n_clusters;
   int head_only, all_but_own;
   int double_float;             // hogwild: 1 = double-float rows (1 RED.F32x2), 0 = f64 rows (2 RED.F64)
-  uint32_t max_cells;           // hogwild: capacity of the shared cell table
+  uint32_t max_cells;           // hogwild: capacity of the shared cell table (per worker row of the global tables)
+  // cell tables in global memory when they do not fit in shared memory
+  // (many clusters, e.g. the reference's auto C = ceil(n / 4096) at 60M rows)
+  int gcells;                   // 1: hogwild reads gcell_mu / gcell_w, replay reads cm3
+  const double2* gcell_mu;      // hogwild: [local worker][max_cells] cell means
+  const double* gcell_w;        // hogwild: [local worker][max_cells] weights M p_r
+  const double* cm3;            // replay: [C][3] = mu.x, mu.y, p_r
   uint32_t replay_ctas;         // replay: CTAs per worker (level barrier in global memory)
   uint32_t* replay_bar;         // replay: per-worker barrier counters
   double step;
@@ -89,9 +96,19 @@ void launch_means_finalize(double* sums, const LocalCluster* lc, uint32_t ncl, d
                            cudaStream_t st);
 void launch_means_unpack(const double* recv, const uint32_t* slot_gid, uint32_t nslots,
                          double2* means, cudaStream_t st);
+// bad: first local row whose list is longer than k or names a point outside
+// the row's own worker shard (optimizer.hpp:292-300 ownership asserts).
 void launch_build_ell(const uint32_t* offsets, const uint32_t* nbrs, const uint32_t* orig_of,
-                      const uint32_t* new_of, uint32_t n_loc, uint32_t kpad, uint32_t* ell,
-                      uint8_t* ncnt, unsigned long long* bad, cudaStream_t st);
+                      const uint32_t* new_of, const uint32_t* cl_of, const LocalCluster* lcl,
+                      uint32_t n_loc, uint32_t k, uint32_t kpad, uint32_t* ell, uint8_t* ncnt,
+                      unsigned long long* bad, cudaStream_t st);
+// Per-epoch cell tables for the global-memory form (gcells): per local worker
+// its remote cells (or all cells, AllButOwn) as mean + weight M p_r, and the
+// [C][3] table of the replay kernel.
+void launch_cell_tables(const double2* means, const WorkerDev* wk, uint32_t nwl,
+                        const uint32_t* remote_ids, const double* remote_probs,
+                        const double* cell_probs, uint32_t C, int all_but_own, double M,
+                        uint32_t stride, double2* gmu, double* gw, double* cm3, cudaStream_t st);
 void launch_scatter_layout(const double2* pos, const uint32_t* orig_of, uint32_t n_loc,
                            double2* out, cudaStream_t st);
 void launch_gather_layout(const double2* in, const uint32_t* orig_of, uint32_t n_loc,

@@ -1,7 +1,9 @@
 // Host orchestration of the epoch loop: the setup half of fit()
 // (optimizer.hpp:342-386), the epoch loop (:388-470) and the cross-shard
-// means all-gather (:411-442) over NCCL. All numerics run in sgd.cu kernels;
-// the host builds the shard plan / local numbering (O(n) integer work), and,
+// means all-gather (:411-442) over NCCL (one process per GPU, or one process
+// driving a group of GPUs) or a loopback exchange (a group on one GPU). All
+// numerics run in sgd.cu kernels; the host builds the shard plan / local
+// numbering (O(n) integer work), and,
 // in replay mode only, expands the reference's mt19937_64 draw stream into a
 // level-ordered tape (the RNG itself is the reference's integer stream).
 #include <nccl.h>
@@ -16,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <numeric>
 #include <random>
 
@@ -71,12 +74,31 @@ void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
 
 }  // namespace
 
-struct nomad_b200_trainer {
+namespace nb {
+
+struct DivKey {
+  uint64_t worker = ~0ull, key = ~0ull;
+  bool operator<(const DivKey& o) const {
+    return worker != o.worker ? worker < o.worker : key < o.key;
+  }
+  bool none() const { return key == ~0ull; }
+};
+
+// One rank's share of the epoch loop: the workers [rank*W/world,
+// (rank+1)*W/world) on one context. A trainer object (below) drives one rank
+// (one process per GPU, NCCL between processes) or all G ranks of a group
+// (one process, NCCL between devices or a loopback exchange on one device).
+// An epoch is split into phases so a group can interleave its ranks:
+// launch (SGD + this rank's means into its slot) -> exchange -> finish
+// (unpack the all-gathered means, results to host).
+struct RankTrainer {
   nomad_b200_ctx* ctx = nullptr;
   nomad_b200_train_config cfg{};
   uint64_t n = 0, C = 0, k = 0, kpad = 0, s = 0;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  bool own_comm = false;
+  bool grouped = false;  // the means exchange is driven by the group trainer
   uint32_t W = 0, w0 = 0, nwl = 0;
   double lr0 = 0.0;
   bool uniform_k = true;
@@ -90,17 +112,18 @@ struct nomad_b200_trainer {
   std::vector<std::mt19937_64> rng;
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
-  uint32_t hog_cells = 0;  // capacity of the hogwild kernel's shared cell table
+  uint32_t hog_cells = 0;  // cells per worker of the hogwild cell table
+  bool gcells = false;     // cell tables in global memory (too many clusters for shared memory)
   uint32_t replay_k = 0;   // replay: CTAs per worker
   DBuf<uint32_t> replay_bar;
   uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0, hog_wave = 1;
   DBuf<uint2> chunk_map;  // hogwild chunk -> (local worker, chunk within the worker)
   DBuf<uint32_t> chunk_counter;
 
-  DBuf<double2> pos, means;
+  DBuf<double2> pos, means, gcell_mu;
   DBuf<uint32_t> ell, elig, remote_ids, orig_of_d, cl_of, slot_gid, chunk_off;
   DBuf<uint8_t> ncnt;
-  DBuf<double> wtab, remote_probs, cell_probs, slot, recv, sums, loss_acc;
+  DBuf<double> wtab, remote_probs, cell_probs, slot, recv, sums, loss_acc, gcell_w, cm3;
   DBuf<unsigned long long> edge_acc, diverge;
   DBuf<WorkerDev> wk_d;
   DBuf<LocalCluster> lcl_d;
@@ -119,9 +142,11 @@ struct nomad_b200_trainer {
   uint64_t comm_epochs = 0, comm_msgs = 0, comm_doubles = 0, comm_counts = 0;
 
   cudaStream_t st() const { return ctx->stream; }
+  void bind() { bind_device(ctx); }
   void launched(const char* name) { note_launch(ctx, name); }
-  ~nomad_b200_trainer() {
-    if (comm) ncclCommDestroy(comm);
+  ~RankTrainer() {
+    join_prefetch();
+    if (comm && own_comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
   }
@@ -143,6 +168,7 @@ struct nomad_b200_trainer {
   }
 
   // ---------------------------------------------------------------- setup
+  // Everything but the epoch-0 means (the caller runs the first exchange).
   void setup(const nomad_b200_graph* g, const nomad_b200_clusters* cl, const double* init,
              int init_loc, const void* nccl_id) {
     validate();
@@ -155,9 +181,10 @@ struct nomad_b200_trainer {
     if (g->k != k) fail(kParameter, "graph k differs from config k");
     if (n >= 0xFFFFFFFFull) fail(kSize, "point ids are u32 (n < 2^32)");
     if (C < 1) fail(kParameter, "n_clusters must be >= 1");
-    kpad = std::max<uint64_t>(16, (k + 15) / 16 * 16);
     if (k > 64) fail(kParameter, "k > 64 is not supported");
     if (s > 16) fail(kParameter, "local_draws > 16 is not supported");
+    // ELL row width = the throughput kernel's compiled neighbour capacity
+    kpad = k <= 16 ? 16 : (k <= 32 ? 32 : 64);
     lr0 = cfg.lr0 > 0.0 ? cfg.lr0 : static_cast<double>(n) / 10.0;  // optimizer.hpp:79-81
 
     // host copies of assignment + offsets
@@ -227,7 +254,6 @@ struct nomad_b200_trainer {
     elig_h.clear();
     std::vector<uint32_t> rem_ids;
     std::vector<double> rem_probs;
-    uint64_t total_elig = 0;
     uint32_t max_rem = 0;
     for (uint32_t wl = 0; wl < nwl; ++wl) {
       WorkerDev& d = wk[wl];
@@ -237,7 +263,6 @@ struct nomad_b200_trainer {
       d.n_elig = (uint32_t)eligs[wl].size();
       d.draws = d.n_elig;
       elig_h.insert(elig_h.end(), eligs[wl].begin(), eligs[wl].end());
-      total_elig += d.n_elig;
       d.rem_off = (uint32_t)rem_ids.size();
       uint64_t remote = 0;
       for (uint64_t r = 0; r < C; ++r) {
@@ -257,7 +282,6 @@ struct nomad_b200_trainer {
       for (uint64_t i = 0; i < n && !any; ++i) any = offs[i + 1] > offs[i];
       if (!any) fail(kConfig, "no point has any neighbor; nothing to train on");
     }
-    (void)total_elig;
 
     // weights table (affinity.hpp:65-84: one table per neighbour count)
     std::vector<double> wt((k + 1) * k, 0.0);
@@ -295,18 +319,19 @@ struct nomad_b200_trainer {
       upload(new_of_d, new_of, S);
       ell.alloc(std::max<uint64_t>(n_loc * kpad, 1));
       ncnt.alloc(std::max<uint64_t>(n_loc, 1));
-      diverge.alloc(1);
-      NB_CUDA(cudaMemsetAsync(diverge.p, 0xFF, 8, S));
+      diverge.alloc(std::max<uint32_t>(nwl, 1));
+      NB_CUDA(cudaMemsetAsync(diverge.p, 0xFF, diverge.bytes(), S));
       if (n_loc) {
-        launch_build_ell(off_p, nb_p, orig_of_d.p, new_of_d.p, (uint32_t)n_loc, (uint32_t)kpad,
-                         ell.p, ncnt.p, diverge.p, S);
+        launch_build_ell(off_p, nb_p, orig_of_d.p, new_of_d.p, cl_of.p, lcl_d.p, (uint32_t)n_loc,
+                         (uint32_t)k, (uint32_t)kpad, ell.p, ncnt.p, diverge.p, S);
         launched("k_build_ell");
       }
       unsigned long long bad = 0;
       NB_CUDA(cudaMemcpyAsync(&bad, diverge.p, 8, cudaMemcpyDeviceToHost, S));
       NB_CUDA(cudaStreamSynchronize(S));
-      if (bad != ~0ull) fail(kInternal, "kNN edge crosses shards or exceeds k (local point " +
-                                            std::to_string(bad) + ")");
+      if (bad != ~0ull)
+        fail(kParameter, "kNN list of point " + std::to_string(orig_of[(uint32_t)bad]) +
+                             " is longer than k or names a point outside its worker's shard");
     }
     uniform_k = true;
     for (uint64_t i = 0; i < n; ++i)
@@ -357,28 +382,41 @@ struct nomad_b200_trainer {
     loss_acc.alloc(std::max<uint32_t>(nwl, 1));
     edge_acc.alloc(std::max<uint32_t>(nwl, 1));
     wloss.alloc(std::max<uint32_t>(nwl, 1));
-    if (world > 1) {
+    if (world > 1 && !grouped) {
       if (!nccl_id) fail(kParameter, "nccl_id required when world_size > 1");
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof id);
       NB_NCCL(ncclCommInitRank(&comm, world, id, rank));
+      own_comm = true;
     }
 
-    // shared-memory budgets
-    smem_replay = ((k + 1) * k + 3 * C) * sizeof(double);
-    hog_cells = (uint32_t)(cfg.approx_all_but_own ? C : max_rem);
-    smem_hog = ((((k + 1) * k + 1) & ~1ull) + 3 * (uint64_t)hog_cells) * sizeof(double);
-    if (smem_replay > 200 * 1024 || smem_hog > 200 * 1024)
-      fail(kSize, "too many clusters for the shared-memory cell table (C=" + std::to_string(C) + ")");
+    // cell tables: shared memory while they fit (the headline configs), else
+    // global memory read through L1 (the reference's auto C = ceil(n/4096)
+    // has ~14.6k clusters at 60M rows, optimizer.hpp:73-77)
+    const uint64_t wts = (((k + 1) * k) + 1) & ~1ull;
+    hog_cells = (uint32_t)std::max<uint64_t>(cfg.approx_all_but_own ? C : max_rem, 1);
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
+      smem_replay = ((k + 1) * k + 3 * C) * sizeof(double);
+      if (smem_replay > 96 * 1024) {
+        gcells = true;
+        smem_replay = (k + 1) * k * sizeof(double);
+      }
+    } else {
+      smem_hog = (wts + 3 * (uint64_t)hog_cells) * sizeof(double);
+      if (smem_hog > 48 * 1024) {
+        gcells = true;
+        smem_hog = wts * sizeof(double);
+      }
+    }
+    if (gcells) {
+      gcell_mu.alloc((size_t)std::max<uint32_t>(nwl, 1) * hog_cells);
+      gcell_w.alloc((size_t)std::max<uint32_t>(nwl, 1) * hog_cells);
+      cm3.alloc(3 * C);
+    }
     // hogwild grid: per worker share of the resident capacity, capped by
     // npts / cap heads in flight
     if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD) plan_hogwild_grid();
     upload(wk_d, wk, S);
-
-    // epoch-0 means of the init layout (optimizer.hpp:384)
-    compute_means_and_exchange();
-    NB_CUDA(cudaStreamSynchronize(S));
-    check_divergence(0, false);
   }
 
   void plan_hogwild_grid() {
@@ -410,12 +448,12 @@ struct nomad_b200_trainer {
       nchunk[wl] = (d.draws + chunk_heads - 1) / chunk_heads;
     }
     std::vector<uint2> cmap;
-    for (uint32_t w0 = 0; w0 < nwl; w0 += wave) {
-      const uint32_t w1 = std::min<uint32_t>(nwl, w0 + wave);
+    for (uint32_t a = 0; a < nwl; a += wave) {
+      const uint32_t b = std::min<uint32_t>(nwl, a + wave);
       uint32_t maxc = 0;
-      for (uint32_t wl = w0; wl < w1; ++wl) maxc = std::max(maxc, nchunk[wl]);
+      for (uint32_t wl = a; wl < b; ++wl) maxc = std::max(maxc, nchunk[wl]);
       for (uint32_t lc = 0; lc < maxc; ++lc)
-        for (uint32_t wl = w0; wl < w1; ++wl)
+        for (uint32_t wl = a; wl < b; ++wl)
           if (lc < nchunk[wl]) cmap.push_back(make_uint2(wl, lc));
     }
     total_chunks = (uint32_t)cmap.size();
@@ -427,7 +465,7 @@ struct nomad_b200_trainer {
 
   unsigned long long div_tag = 0;  // run-relative epoch tag of divergence keys (hogwild)
   // The throughput kernel's position rows are double-float while a run is in
-  // progress (cfg.hogwild_double_float); outside run() they are f64 again.
+  // progress (cfg.hogwild_double_float); outside a run they are f64 again.
   bool pos_is_df = false;
   void pos_format(bool df) {
     if (df == pos_is_df || !cfg.hogwild_double_float) return;
@@ -436,47 +474,84 @@ struct nomad_b200_trainer {
     pos_is_df = df;
   }
 
-  void compute_means_and_exchange() {
+  // ------------------------------------------------ means exchange (K9)
+  // This rank's cluster means into its slot (optimizer.hpp:414-433).
+  void compute_means() {
     cudaStream_t S = st();
     const uint32_t ncl = (uint32_t)lcl.size();
-    if (ncl) {
-      if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
-        launch_means_exact(pos.p, lcl_d.p, ncl, slot.p, S);
-        launched("k_means_exact");
-      } else {
-        launch_means_chunk(pos.p, pos_is_df, lcl_d.p, ncl, chunk, chunk_off.p, nchunks, sums.p,
-                           diverge.p, div_tag, S);
-        launched("k_means_chunk");
-        launch_means_finalize(sums.p, lcl_d.p, ncl, slot.p, S);
-        launched("k_means_finalize");
-      }
+    if (!ncl) return;
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
+      launch_means_exact(pos.p, lcl_d.p, ncl, slot.p, S);
+      launched("k_means_exact");
+    } else {
+      launch_means_chunk(pos.p, pos_is_df, lcl_d.p, ncl, chunk, chunk_off.p, nchunks, sums.p,
+                         diverge.p, div_tag, S);
+      launched("k_means_chunk");
+      launch_means_finalize(sums.p, lcl_d.p, ncl, slot.p, S);
+      launched("k_means_finalize");
     }
-    const double* src = slot.p;
-    if (world > 1) {
-      NB_NCCL(ncclAllGather(slot.p, recv.p, 2 * (size_t)max_slots, ncclDouble, comm, S));
-      src = recv.p;
-    }
-    launch_means_unpack(src, slot_gid.p, (uint32_t)world * max_slots, means.p, S);
+  }
+  // One process per rank: the all-gather of the slots over NCCL.
+  void exchange_self() {
+    if (world > 1 && !grouped)
+      NB_NCCL(ncclAllGather(slot.p, recv.p, 2 * (size_t)max_slots, ncclDouble, comm, st()));
+  }
+  // The all-gathered slots -> the C-entry means snapshot (+ global cell tables).
+  void unpack_means() {
+    cudaStream_t S = st();
+    launch_means_unpack(world > 1 ? recv.p : slot.p, slot_gid.p, (uint32_t)world * max_slots,
+                        means.p, S);
     launched("k_means_unpack");
+    if (gcells) {
+      launch_cell_tables(means.p, wk_d.p, nwl, remote_ids.p, remote_probs.p, cell_probs.p,
+                         (uint32_t)C, cfg.approx_all_but_own, (double)cfg.negatives, hog_cells,
+                         gcell_mu.p, gcell_w.p, cm3.p, S);
+      launched("k_cell_tables");
+    }
+  }
+  void count_comm() {  // CommLog: one message per worker (optimizer.hpp:429-440)
+    ++comm_epochs;
+    comm_msgs += W;
+    comm_doubles += 2 * C;
+    comm_counts += C;
   }
 
-  void check_divergence(uint64_t epoch, bool replay_key) {
-    unsigned long long key = 0;
-    NB_CUDA(cudaMemcpyAsync(&key, diverge.p, 8, cudaMemcpyDeviceToHost, st()));
+  // ------------------------------------------------------ divergence
+  // The first offender, ordered (global worker, key): replay keeps one key
+  // per worker, (t * stride + u) << 32 | point, so the reported draw is the
+  // first one of the lowest diverging worker — the order in which workers
+  // are run one after another; throughput mode keeps one key (worker 0).
+  // Point ids are mapped to original ids so every rank decodes the same way.
+  DivKey host_key(const unsigned long long* keys) const {
+    const uint32_t nk = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? nwl : 1;
+    for (uint32_t wl = 0; wl < nk; ++wl)
+      if (keys[wl] != ~0ull)
+        return DivKey{cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? (uint64_t)(w0 + wl) : 0ull,
+                      (keys[wl] & 0xFFFFFFFF00000000ull) | orig_of[(uint32_t)keys[wl]]};
+    return DivKey{};
+  }
+  DivKey local_key() {
+    std::vector<unsigned long long> keys(std::max<uint32_t>(nwl, 1));
+    NB_CUDA(cudaMemcpyAsync(keys.data(), diverge.p, diverge.bytes(), cudaMemcpyDeviceToHost, st()));
     NB_CUDA(cudaStreamSynchronize(st()));
-    if (key == ~0ull) return;
-    char m[200];
-    if (replay_key) {
-      const uint64_t stride = 2 + k + s;
-      const uint64_t t = (key >> 32) / stride;
-      const uint32_t p = orig_of[(uint32_t)key];
-      snprintf(m, sizeof m, "positions diverged at epoch %llu, head draw %llu (point %u)",
-               (unsigned long long)epoch, (unsigned long long)t, p);
-    } else {
-      snprintf(m, sizeof m, "positions diverged at epoch %llu (point %u)",
-               (unsigned long long)epoch, orig_of[(uint32_t)key]);
-    }
-    fail(kDivergence, m);
+    return host_key(keys.data());
+  }
+  // One process per rank: every rank must reach the same decision, or the
+  // next collective hangs — lexicographic min over ranks (two ncclMin).
+  DivKey agree_key(DivKey k) {
+    if (grouped || world == 1) return k;
+    DBuf<unsigned long long> kb(1);
+    auto allmin = [&](uint64_t v) {
+      unsigned long long x = v;
+      NB_CUDA(cudaMemcpyAsync(kb.p, &x, 8, cudaMemcpyHostToDevice, st()));
+      NB_NCCL(ncclAllReduce(kb.p, kb.p, 1, ncclUint64, ncclMin, comm, st()));
+      NB_CUDA(cudaMemcpyAsync(&x, kb.p, 8, cudaMemcpyDeviceToHost, st()));
+      NB_CUDA(cudaStreamSynchronize(st()));
+      return (uint64_t)x;
+    };
+    const uint64_t w = allmin(k.worker);
+    const uint64_t key = allmin(k.worker == w ? k.key : ~0ull);
+    return DivKey{w, key};
   }
 
   SgdParams params(double step, uint64_t epoch) {
@@ -506,6 +581,10 @@ struct nomad_b200_trainer {
     P.double_float = cfg.hogwild_double_float ? 1 : 0;
     P.max_cells = hog_cells;
     P.all_but_own = cfg.approx_all_but_own;
+    P.gcells = gcells ? 1 : 0;
+    P.gcell_mu = gcell_mu.p;
+    P.gcell_w = gcell_w.p;
+    P.cm3 = cm3.p;
     P.step = step;
     P.epoch = epoch;
     const uint64_t sk = mix_seed(cfg.seed ^ 0x686f67776c64ull);
@@ -518,11 +597,15 @@ struct nomad_b200_trainer {
     return P;
   }
 
+  double step_of(uint64_t e) const {  // optimizer.hpp:85-91, :390-391
+    const double lr = lr0 * (1.0 - static_cast<double>(e) / static_cast<double>(cfg.epochs));
+    return lr / static_cast<double>(cfg.batch_size);
+  }
+
   // ------------------------------------------------------- replay tapes
-  // For each local worker: the reference's draw sequence for this epoch
-  // (optimizer.hpp:252-285) and its wavefront levels.
   // One epoch's replay tape: every worker's draws (mt19937_64 stream, the
-  // reference's order) grouped by conflict level, worker-major.
+  // reference's order, optimizer.hpp:252-285) grouped by conflict level,
+  // worker-major.
   struct Tape {
     std::vector<uint32_t> th, tt, tid, loff, lbase, nlev;
     uint64_t edges = 0;
@@ -677,247 +760,227 @@ struct nomad_b200_trainer {
     return lo;
   }
 
-  // ---------------------------------------------------------------- run
-  // Throughput mode without per-epoch host round trips: every epoch's SGD
-  // kernel, means pass and all-gather are queued back to back; per-epoch
-  // loss / edge sums land in device arrays and are read (and, multi-rank,
-  // gathered) once at the end; divergence keys carry the epoch.
-  void run_async(uint64_t n_epochs, double* epoch_loss) {
-    cudaStream_t S = st();
-    if (epochs_done + n_epochs > cfg.epochs) fail(kParameter, "epoch out of range for schedule");
-    const uint64_t E = n_epochs, L = std::max<uint32_t>(nwl, 1);
-    DBuf<double> lossb(E * L);
-    DBuf<unsigned long long> edgeb(E * L);
-    NB_CUDA(cudaMemsetAsync(lossb.p, 0, lossb.bytes(), S));
-    NB_CUDA(cudaMemsetAsync(edgeb.p, 0, edgeb.bytes(), S));
-    std::vector<cudaEvent_t> evs(3 * E);
-    for (auto& x : evs) NB_CUDA(cudaEventCreate(&x));
-    const uint64_t e_first = epochs_done;
+  // ------------------------------------------- throughput run (async)
+  // Every epoch's SGD kernel, means pass and exchange are queued back to
+  // back; per-epoch loss / edge sums land in device arrays read once at the
+  // end; divergence keys carry the run-relative epoch.
+  uint64_t a_E = 0, a_first = 0;
+  DBuf<double> a_loss;
+  DBuf<unsigned long long> a_edge;
+  std::vector<cudaEvent_t> a_ev;
+  std::vector<double> a_lh, a_all;  // per epoch x local worker; multi-process: all ranks
+  std::vector<unsigned long long> a_eh;
+  std::vector<unsigned long long> a_keys;
+
+  void async_begin(uint64_t E) {
+    if (epochs_done + E > cfg.epochs) fail(kParameter, "epoch out of range for schedule");
+    const uint64_t L = std::max<uint32_t>(nwl, 1);
+    a_E = E;
+    a_first = epochs_done;
+    a_loss.alloc(std::max<uint64_t>(E * L, 1));
+    a_edge.alloc(std::max<uint64_t>(E * L, 1));
+    NB_CUDA(cudaMemsetAsync(a_loss.p, 0, a_loss.bytes(), st()));
+    NB_CUDA(cudaMemsetAsync(a_edge.p, 0, a_edge.bytes(), st()));
+    for (auto& x : a_ev) cudaEventDestroy(x);
+    a_ev.assign(3 * E, nullptr);
+    for (auto& x : a_ev) NB_CUDA(cudaEventCreate(&x));
     pos_format(true);
-    for (uint64_t it = 0; it < E; ++it) {
-      const uint64_t e = epochs_done;
-      const double lr = lr0 * (1.0 - static_cast<double>(e) / static_cast<double>(cfg.epochs));
-      const double step = lr / static_cast<double>(cfg.batch_size);
-      SgdParams P = params(step, e);
-      P.loss_acc = lossb.p + it * L;
-      P.edge_acc = edgeb.p + it * L;
-      NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
-      NB_CUDA(cudaEventRecord(evs[3 * it], S));
-      if (hog_blocks) {
-        launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
-        launched("k_sgd_hogwild");
-      }
-      NB_CUDA(cudaEventRecord(evs[3 * it + 1], S));
-      div_tag = it;
-      compute_means_and_exchange();
-      NB_CUDA(cudaEventRecord(evs[3 * it + 2], S));
-      ++comm_epochs;
-      comm_msgs += W;
-      comm_doubles += 2 * C;
-      comm_counts += C;
-      ++epochs_done;
+  }
+  void async_launch(uint64_t it) {
+    cudaStream_t S = st();
+    const uint64_t L = std::max<uint32_t>(nwl, 1);
+    SgdParams P = params(step_of(epochs_done), epochs_done);
+    P.loss_acc = a_loss.p + it * L;
+    P.edge_acc = a_edge.p + it * L;
+    NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
+    NB_CUDA(cudaEventRecord(a_ev[3 * it], S));
+    if (hog_blocks) {
+      launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
+      launched("k_sgd_hogwild");
     }
+    NB_CUDA(cudaEventRecord(a_ev[3 * it + 1], S));
+    div_tag = it;
+    compute_means();
+  }
+  void async_finish(uint64_t it) {
+    unpack_means();
+    NB_CUDA(cudaEventRecord(a_ev[3 * it + 2], st()));
+    count_comm();
+    ++epochs_done;
+  }
+  void async_end() {  // results to host (collective in multi-process mode)
+    cudaStream_t S = st();
+    const uint64_t E = a_E, L = std::max<uint32_t>(nwl, 1);
     div_tag = 0;
     pos_format(false);
-    std::vector<double> lh(E * L);
-    std::vector<unsigned long long> eh(E * L);
-    NB_CUDA(cudaMemcpyAsync(lh.data(), lossb.p, E * L * 8, cudaMemcpyDeviceToHost, S));
-    NB_CUDA(cudaMemcpyAsync(eh.data(), edgeb.p, E * L * 8, cudaMemcpyDeviceToHost, S));
-    std::vector<double> all;
-    if (world > 1) {
+    a_lh.assign(E * L, 0.0);
+    a_eh.assign(E * L, 0);
+    if (E) {
+      NB_CUDA(cudaMemcpyAsync(a_lh.data(), a_loss.p, E * L * 8, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaMemcpyAsync(a_eh.data(), a_edge.p, E * L * 8, cudaMemcpyDeviceToHost, S));
+    }
+    a_all.clear();
+    if (world > 1 && !grouped && E) {
       DBuf<double> g((size_t)world * E * L);
-      NB_NCCL(ncclAllGather(lossb.p, g.p, E * L, ncclDouble, comm, S));
-      all.resize((size_t)world * E * L);
-      NB_CUDA(cudaMemcpyAsync(all.data(), g.p, all.size() * 8, cudaMemcpyDeviceToHost, S));
+      NB_NCCL(ncclAllGather(a_loss.p, g.p, E * L, ncclDouble, comm, S));
+      a_all.resize((size_t)world * E * L);
+      NB_CUDA(cudaMemcpyAsync(a_all.data(), g.p, a_all.size() * 8, cudaMemcpyDeviceToHost, S));
       NB_CUDA(cudaStreamSynchronize(S));
     }
-    unsigned long long key = 0;
-    NB_CUDA(cudaMemcpyAsync(&key, diverge.p, 8, cudaMemcpyDeviceToHost, S));
+    a_keys.assign(std::max<uint32_t>(nwl, 1), ~0ull);
+    NB_CUDA(cudaMemcpyAsync(a_keys.data(), diverge.p, diverge.bytes(), cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
     for (uint64_t it = 0; it < E; ++it) {
       float a = 0.f, b = 0.f;
-      NB_CUDA(cudaEventElapsedTime(&a, evs[3 * it], evs[3 * it + 1]));
-      NB_CUDA(cudaEventElapsedTime(&b, evs[3 * it + 1], evs[3 * it + 2]));
+      NB_CUDA(cudaEventElapsedTime(&a, a_ev[3 * it], a_ev[3 * it + 1]));
+      NB_CUDA(cudaEventElapsedTime(&b, a_ev[3 * it + 1], a_ev[3 * it + 2]));
       sgd_ms += a;
       means_ms += b;
       ++timed_epochs;
     }
-    for (auto& x : evs) cudaEventDestroy(x);
-    if (key != ~0ull) {
-      char m[200];
-      snprintf(m, sizeof m, "positions diverged at epoch %llu (point %u)",
-               (unsigned long long)(e_first + (key >> 32)), orig_of[(uint32_t)key]);
-      fail(kDivergence, m);
-    }
-    const uint64_t heads = world > 1 ? total_heads_global() : [&] {
-      uint64_t h = 0;
-      for (auto& d : wk) h += d.draws;
-      return h;
-    }();
-    for (uint64_t it = 0; it < E; ++it) {
-      double loss_sum = 0.0;  // worker order: rank-major, then local worker
-      if (world > 1) {
-        for (int r = 0; r < world; ++r)
-          for (uint32_t wl = 0; wl < nwl; ++wl) loss_sum += all[((size_t)r * E + it) * L + wl];
-      } else {
-        for (uint32_t wl = 0; wl < nwl; ++wl) loss_sum += lh[it * L + wl];
-      }
-      for (uint32_t wl = 0; wl < nwl; ++wl) edge_updates += eh[it * L + wl];
-      if (epoch_loss) epoch_loss[it] = heads > 0 ? loss_sum / static_cast<double>(heads) : 0.0;
-    }
+    for (auto& x : a_ev) cudaEventDestroy(x);
+    a_ev.clear();
+    for (uint64_t i = 0; i < E * L && i < a_eh.size(); ++i)
+      if (i % L < nwl) edge_updates += a_eh[i];
   }
 
-  void run(uint64_t n_epochs, double* epoch_loss) {
-    if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD && !cfg.verbose) return run_async(n_epochs, epoch_loss);
-    cudaStream_t S = st();
-    if (draw_base_h.empty()) {
+  // -------------------------------------- replay / verbose run (per epoch sync)
+  Tape cur, nxt;
+  std::thread prefetch;
+  uint64_t s_E = 0;
+  std::vector<double> s_wl_loss, s_all_loss;
+  std::vector<unsigned long long> s_wl_edges;
+  DBuf<double> s_gl;  // gathered per-worker losses (multi-process)
+  uint64_t s_edges = 0;
+  std::chrono::steady_clock::time_point s_t0;
+
+  void join_prefetch() {
+    if (prefetch.joinable()) prefetch.join();
+  }
+  void sync_begin(uint64_t E) {
+    s_E = E;
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY && draw_base_h.empty()) {
       draw_base_h.assign(nwl, 0);
       uint32_t acc = 0;
       for (uint32_t wl = 0; wl < nwl; ++wl) { draw_base_h[wl] = acc; acc += wk[wl].draws; }
-      upload(wk_draw_base, draw_base_h, S);
+      upload(wk_draw_base, draw_base_h, st());
       loss_slot.alloc(std::max<uint32_t>(acc, 1));
     }
-    // replay: the next epoch's tape is built on host threads while this
-    // epoch runs on the GPU (tapes depend only on the workers' streams);
-    // only within this call, so the streams end exactly n_epochs ahead
-    Tape cur, nxt;
-    std::thread prefetch;
-    struct Joiner {
-      std::thread& t;
-      ~Joiner() {
-        if (t.joinable()) t.join();
-      }
-    } joiner{prefetch};
+    s_wl_loss.assign(nwl, 0.0);
+    s_wl_edges.assign(nwl, 0);
+    s_all_loss.assign((size_t)world * std::max<uint32_t>(nwl, 1), 0.0);
+    if (!ev[0])
+      for (auto& x : ev) NB_CUDA(cudaEventCreate(&x));
+  }
+  void sync_launch(uint64_t it) {
+    cudaStream_t S = st();
+    const uint64_t e = epochs_done;
+    if (e >= cfg.epochs) fail(kParameter, "epoch out of range for schedule");
+    s_t0 = std::chrono::steady_clock::now();
+    SgdParams P = params(step_of(e), e);
+    s_edges = 0;
     const bool replay = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY;
-    std::vector<double> wl_loss(nwl), all_loss(world * std::max<uint32_t>(nwl, 1));
-    std::vector<unsigned long long> wl_edges(nwl);
-    DBuf<double> gl;  // gathered per-worker losses (multi-rank)
-    DBuf<double> gheads;
-    for (uint64_t it = 0; it < n_epochs; ++it) {
-      const uint64_t e = epochs_done;
-      if (e >= cfg.epochs) fail(kParameter, "epoch out of range for schedule");
-      const auto t0 = std::chrono::steady_clock::now();
-      // optimizer.hpp:85-91, :390-391
-      const double lr = lr0 * (1.0 - static_cast<double>(e) / static_cast<double>(cfg.epochs));
-      const double step = lr / static_cast<double>(cfg.batch_size);
-      SgdParams P = params(step, e);
-      uint64_t edges = 0;
-      if (!ev[0])
-        for (auto& x : ev) NB_CUDA(cudaEventCreate(&x));
-      if (replay) {
-        if (it == 0) {
-          build_tapes(cur);
-        } else {
-          prefetch.join();
-          std::swap(cur, nxt);
-        }
-        if (it + 1 < n_epochs) prefetch = std::thread([this, &nxt] { build_tapes(nxt); });
-        edges = cur.edges;
-        if (std::getenv("NOMAD_B200_DEBUG_REPLAY") && it == 0)
-          for (uint32_t wl = 0; wl < nwl; ++wl)
-            std::fprintf(stderr, "replay worker %u: %u draws, %u levels\n", wl, wk[wl].draws,
-                         cur.nlev[wl]);
-        upload(tape_head, cur.th, S);
-        upload(tape_tails, cur.tt, S);
-        upload(tape_t, cur.tid, S);
-        upload(lvl_off, cur.loff, S);
-        upload(wk_lvl_base, cur.lbase, S);
-        upload(wk_nlev, cur.nlev, S);
-        P.tape_head = tape_head.p;
-        P.tape_tails = tape_tails.p;
-        P.tape_t = tape_t.p;
-        P.lvl_off = lvl_off.p;
-        P.wk_lvl_base = wk_lvl_base.p;
-        P.wk_nlev = wk_nlev.p;
-        P.loss_slot = loss_slot.p;
-        P.wk_draw_base = wk_draw_base.p;
-        if (!replay_k) {
-          replay_k = replay_ctas_per_worker(nwl, smem_replay, ctx->sm_count);
-          replay_bar.alloc(std::max<uint32_t>(nwl, 1));
-        }
-        P.replay_ctas = replay_k;
-        P.replay_bar = replay_bar.p;
-        NB_CUDA(cudaEventRecord(ev[0], S));
-        if (nwl) {
-          launch_sgd_replay(P, nwl, smem_replay, S);
-          launched("k_sgd_replay");
-          launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
-          launched("k_loss_seq");
-        }
-        NB_CUDA(cudaEventRecord(ev[1], S));
+    if (replay) {
+      // the next epoch's tape is built on host threads while this epoch runs
+      // on the GPU (tapes depend only on the workers' streams); only within
+      // this run, so the streams end exactly n_epochs ahead
+      if (it == 0) {
+        build_tapes(cur);
       } else {
-        NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
-        NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
-        NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
-        pos_format(true);
-        NB_CUDA(cudaEventRecord(ev[0], S));
-        if (hog_blocks) {
-          launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
-          launched("k_sgd_hogwild");
-        }
-        NB_CUDA(cudaEventRecord(ev[1], S));
+        join_prefetch();
+        std::swap(cur, nxt);
       }
-      compute_means_and_exchange();
-      pos_format(false);
-      NB_CUDA(cudaEventRecord(ev[2], S));
-      // per-worker loss sums -> epoch mean (optimizer.hpp:444-451)
-      const double* lsrc = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? wloss.p : loss_acc.p;
-      if (nwl) NB_CUDA(cudaMemcpyAsync(wl_loss.data(), lsrc, nwl * 8, cudaMemcpyDeviceToHost, S));
-      if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD && nwl)
-        NB_CUDA(cudaMemcpyAsync(wl_edges.data(), edge_acc.p, nwl * 8, cudaMemcpyDeviceToHost, S));
-      if (world > 1) {
-        if (!gl.p) { gl.alloc((size_t)world * nwl); }
-        NB_NCCL(ncclAllGather(lsrc, gl.p, nwl, ncclDouble, comm, S));
-        NB_CUDA(cudaMemcpyAsync(all_loss.data(), gl.p, (size_t)world * nwl * 8,
-                                cudaMemcpyDeviceToHost, S));
+      if (it + 1 < s_E) prefetch = std::thread([this] { build_tapes(nxt); });
+      s_edges = cur.edges;
+      if (std::getenv("NOMAD_B200_DEBUG_REPLAY") && it == 0)
+        for (uint32_t wl = 0; wl < nwl; ++wl)
+          std::fprintf(stderr, "replay worker %u: %u draws, %u levels\n", wl, wk[wl].draws,
+                       cur.nlev[wl]);
+      upload(tape_head, cur.th, S);
+      upload(tape_tails, cur.tt, S);
+      upload(tape_t, cur.tid, S);
+      upload(lvl_off, cur.loff, S);
+      upload(wk_lvl_base, cur.lbase, S);
+      upload(wk_nlev, cur.nlev, S);
+      P.tape_head = tape_head.p;
+      P.tape_tails = tape_tails.p;
+      P.tape_t = tape_t.p;
+      P.lvl_off = lvl_off.p;
+      P.wk_lvl_base = wk_lvl_base.p;
+      P.wk_nlev = wk_nlev.p;
+      P.loss_slot = loss_slot.p;
+      P.wk_draw_base = wk_draw_base.p;
+      if (!replay_k) {
+        replay_k = replay_ctas_per_worker(nwl, smem_replay, ctx->sm_count);
+        replay_bar.alloc(std::max<uint32_t>(nwl, 1));
       }
-      check_divergence(e, cfg.sgd_mode == NOMAD_B200_SGD_REPLAY);  // syncs the stream
-      {
-        float a = 0.f, b = 0.f;
-        NB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
-        NB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
-        sgd_ms += a;
-        means_ms += b;
-        ++timed_epochs;
+      P.replay_ctas = replay_k;
+      P.replay_bar = replay_bar.p;
+      NB_CUDA(cudaEventRecord(ev[0], S));
+      if (nwl) {
+        launch_sgd_replay(P, nwl, smem_replay, S);
+        launched("k_sgd_replay");
+        launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
+        launched("k_loss_seq");
       }
-      if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD)
-        for (uint32_t wl = 0; wl < nwl; ++wl) edges += wl_edges[wl];
-      edge_updates += edges;
-      double loss_sum = 0.0;
-      uint64_t heads = 0;
-      if (world > 1) {
-        for (size_t i = 0; i < all_loss.size(); ++i) loss_sum += all_loss[i];
-        // every worker draws its eligible count (global, identical on ranks)
-        heads = total_heads_global();
-      } else {
-        for (uint32_t wl = 0; wl < nwl; ++wl) { loss_sum += wl_loss[wl]; heads += wk[wl].draws; }
+      NB_CUDA(cudaEventRecord(ev[1], S));
+    } else {
+      NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
+      NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
+      NB_CUDA(cudaMemsetAsync(chunk_counter.p, 0, 4, S));
+      pos_format(true);
+      NB_CUDA(cudaEventRecord(ev[0], S));
+      if (hog_blocks) {
+        launch_sgd_hogwild(P, hog_blocks, smem_hog, S);
+        launched("k_sgd_hogwild");
       }
-      const double mean_loss = heads > 0 ? loss_sum / static_cast<double>(heads) : 0.0;
-      if (epoch_loss) epoch_loss[it] = mean_loss;
-      // CommLog: one message per worker (optimizer.hpp:429-440)
-      ++comm_epochs;
-      comm_msgs += W;
-      comm_doubles += 2 * C;
-      comm_counts += C;
-      ++epochs_done;
-      if (cfg.verbose) {
-        const double secs =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        std::fprintf(stderr, "epoch %llu/%llu lr %.6g loss %.6f time %.2fs\n",
-                     (unsigned long long)(e + 1), (unsigned long long)cfg.epochs, lr, mean_loss,
-                     secs);
-      }
+      NB_CUDA(cudaEventRecord(ev[1], S));
+    }
+    compute_means();
+  }
+  void sync_finish() {  // after the exchange; results to host (collective in multi-process mode)
+    cudaStream_t S = st();
+    unpack_means();
+    pos_format(false);
+    NB_CUDA(cudaEventRecord(ev[2], S));
+    // per-worker loss sums -> epoch mean (optimizer.hpp:444-451)
+    const double* lsrc = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? wloss.p : loss_acc.p;
+    if (nwl) NB_CUDA(cudaMemcpyAsync(s_wl_loss.data(), lsrc, nwl * 8, cudaMemcpyDeviceToHost, S));
+    if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD && nwl)
+      NB_CUDA(cudaMemcpyAsync(s_wl_edges.data(), edge_acc.p, nwl * 8, cudaMemcpyDeviceToHost, S));
+    if (world > 1 && !grouped) {
+      if (!s_gl.p) s_gl.alloc((size_t)world * nwl);
+      NB_NCCL(ncclAllGather(lsrc, s_gl.p, nwl, ncclDouble, comm, S));
+      NB_CUDA(cudaMemcpyAsync(s_all_loss.data(), s_gl.p, (size_t)world * nwl * 8,
+                              cudaMemcpyDeviceToHost, S));
     }
   }
+  DivKey sync_collect() {  // waits for this rank's epoch; returns its divergence key
+    const DivKey key = local_key();  // syncs the stream
+    float a = 0.f, b = 0.f;
+    NB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    NB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    sgd_ms += a;
+    means_ms += b;
+    ++timed_epochs;
+    if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD)
+      for (uint32_t wl = 0; wl < nwl; ++wl) s_edges += s_wl_edges[wl];
+    edge_updates += s_edges;
+    return key;
+  }
 
+  uint64_t local_heads() const {
+    uint64_t h = 0;
+    for (auto& d : wk) h += d.draws;
+    return h;
+  }
   uint64_t global_heads = 0;
+  // Heads of all ranks (multi-process: every rank knows the plan but only
+  // its own eligibility; gathered once).
   uint64_t total_heads_global() {
     if (!global_heads) {
-      // eligible counts of all workers: every rank knows the plan but only
-      // its own eligibility; gather once.
       DBuf<double> a(1), b((size_t)world);
-      double mine = 0;
-      for (auto& d : wk) mine += d.draws;
+      double mine = (double)local_heads();
       NB_CUDA(cudaMemcpy(a.p, &mine, 8, cudaMemcpyHostToDevice));
       NB_NCCL(ncclAllGather(a.p, b.p, 1, ncclDouble, comm, st()));
       std::vector<double> h(world);
@@ -928,11 +991,12 @@ struct nomad_b200_trainer {
     return global_heads;
   }
 
-  // Replace the positions (original order, n x 2) and re-gather the means
-  // snapshot, as if the epoch loop had been given this layout.
+  // ----------------------------------------------------- layout in / out
   DBuf<double2> stage;  // n rows, original order (host <-> device staging)
 
-  void set_layout(const double* in, int loc) {
+  // Replace this rank's positions from a layout in ORIGINAL order (the
+  // caller re-gathers the means).
+  void set_rows(const double* in, int loc) {
     cudaStream_t S = st();
     const uint32_t n_loc = (uint32_t)orig_of.size();
     const double* src = in;
@@ -945,10 +1009,9 @@ struct nomad_b200_trainer {
       launch_gather_layout(reinterpret_cast<const double2*>(src), orig_of_d.p, n_loc, pos.p, S);
       launched("k_gather_layout");
     }
-    compute_means_and_exchange();
-    NB_CUDA(cudaStreamSynchronize(S));
   }
 
+  // This rank's rows into `out` (ORIGINAL order); only_mine: other rows untouched.
   void layout(double* out, int loc) {
     cudaStream_t S = st();
     const uint32_t n_loc = (uint32_t)orig_of.size();
@@ -960,7 +1023,7 @@ struct nomad_b200_trainer {
       NB_CUDA(cudaStreamSynchronize(S));
       return;
     }
-    if (world == 1) {  // every row is local: scatter on the device, one D2H copy
+    if (n_loc == n) {  // every row is local: scatter on the device, one D2H copy
       if (stage.n != n) stage.alloc(n);
       if (n_loc) {
         launch_scatter_layout(pos.p, orig_of_d.p, n_loc, stage.p, S);
@@ -980,6 +1043,214 @@ struct nomad_b200_trainer {
   }
 };
 
+}  // namespace nb
+
+// The trainer of the C-ABI: one rank (one process per GPU) or every rank of
+// a group (one process, G contexts), driven epoch by epoch in lockstep.
+struct nomad_b200_trainer {
+  std::vector<std::unique_ptr<RankTrainer>> r;
+  nomad_b200_group* grp = nullptr;
+
+  RankTrainer& R0() { return *r[0]; }
+  bool replay() const { return r[0]->cfg.sgd_mode == NOMAD_B200_SGD_REPLAY; }
+  bool multiproc() const { return !grp && r[0]->world > 1; }
+
+  // The per-epoch all-gather of every rank's slot into every rank's recv.
+  void exchange() {
+    if (!grp) {
+      R0().exchange_self();
+      return;
+    }
+    if (r.size() == 1) return;
+    const size_t cnt = 2 * (size_t)R0().max_slots;
+    if (grp->loopback) {  // one device, one stream: device copies in program order
+      for (auto& q : r)
+        for (size_t src = 0; src < r.size(); ++src)
+          NB_CUDA(cudaMemcpyAsync(q->recv.p + src * cnt, r[src]->slot.p, cnt * 8,
+                                  cudaMemcpyDeviceToDevice, q->st()));
+      return;
+    }
+    NB_NCCL(ncclGroupStart());
+    for (auto& t : r) {
+      t->bind();
+      NB_NCCL(ncclAllGather(t->slot.p, t->recv.p, cnt, ncclDouble, t->comm, t->st()));
+    }
+    NB_NCCL(ncclGroupEnd());
+  }
+
+  void means_all() {
+    for (auto& t : r) { t->bind(); t->compute_means(); }
+    exchange();
+    for (auto& t : r) { t->bind(); t->unpack_means(); }
+  }
+
+  // Same decision on every rank; throws Divergence (optimizer.hpp:222-225).
+  void check_key(DivKey dk, uint64_t epoch_base, bool replay_key) {
+    if (multiproc()) dk = R0().agree_key(dk);
+    if (dk.none()) return;
+    const uint64_t gk = dk.key;
+    char m[200];
+    const uint32_t p = (uint32_t)gk;
+    if (replay_key) {
+      const uint64_t stride = 2 + R0().k + R0().s;
+      snprintf(m, sizeof m, "positions diverged at epoch %llu, head draw %llu (point %u)",
+               (unsigned long long)epoch_base, (unsigned long long)((gk >> 32) / stride), p);
+    } else {
+      snprintf(m, sizeof m, "positions diverged at epoch %llu (point %u)",
+               (unsigned long long)(epoch_base + (gk >> 32)), p);
+    }
+    fail(kDivergence, m);
+  }
+
+  void after_setup() {
+    means_all();  // epoch-0 means of the init layout (optimizer.hpp:384)
+    DivKey dk;
+    for (auto& t : r) { t->bind(); dk = std::min(dk, t->local_key()); }
+    check_key(dk, 0, false);
+  }
+
+  uint64_t all_heads() {
+    if (multiproc()) return R0().total_heads_global();
+    uint64_t h = 0;
+    for (auto& t : r) h += t->local_heads();
+    return h;
+  }
+  void run(uint64_t E, double* epoch_loss) {
+    if (!replay() && !R0().cfg.verbose) return run_async(E, epoch_loss);
+    run_sync(E, epoch_loss);
+  }
+
+  void run_async(uint64_t E, double* epoch_loss) {
+    for (auto& t : r) { t->bind(); t->async_begin(E); }
+    for (uint64_t it = 0; it < E; ++it) {
+      for (auto& t : r) { t->bind(); t->async_launch(it); }
+      exchange();
+      for (auto& t : r) { t->bind(); t->async_finish(it); }
+    }
+    for (auto& t : r) { t->bind(); t->async_end(); }
+    DivKey dk;
+    for (auto& t : r) dk = std::min(dk, t->host_key(t->a_keys.data()));
+    check_key(dk, R0().a_first, false);
+    const uint64_t heads = all_heads();
+    const size_t L = std::max<uint32_t>(R0().nwl, 1), nwl = R0().nwl;
+    for (uint64_t it = 0; it < E; ++it) {
+      double acc = 0.0;  // worker order: rank-major, then local worker
+      if (multiproc()) {
+        for (int rk = 0; rk < R0().world; ++rk)
+          for (size_t wl = 0; wl < nwl; ++wl) acc += R0().a_all[((size_t)rk * E + it) * L + wl];
+      } else {
+        for (auto& t : r)
+          for (size_t wl = 0; wl < nwl; ++wl) acc += t->a_lh[it * L + wl];
+      }
+      if (epoch_loss) epoch_loss[it] = heads > 0 ? acc / static_cast<double>(heads) : 0.0;
+    }
+  }
+
+  void run_sync(uint64_t E, double* epoch_loss) {
+    struct Joiner {
+      nomad_b200_trainer* t;
+      ~Joiner() {
+        for (auto& x : t->r) x->join_prefetch();
+      }
+    } joiner{this};
+    for (auto& t : r) { t->bind(); t->sync_begin(E); }
+    for (uint64_t it = 0; it < E; ++it) {
+      const uint64_t e = R0().epochs_done;
+      for (auto& t : r) { t->bind(); t->sync_launch(it); }
+      exchange();
+      for (auto& t : r) { t->bind(); t->sync_finish(); }
+      DivKey dk;
+      for (auto& t : r) { t->bind(); dk = std::min(dk, t->sync_collect()); }
+      check_key(dk, e, replay());
+      double acc = 0.0;
+      if (multiproc()) {
+        for (double v : R0().s_all_loss) acc += v;
+      } else {
+        for (auto& t : r)
+          for (double v : t->s_wl_loss) acc += v;
+      }
+      const uint64_t heads = all_heads();
+      const double mean_loss = heads > 0 ? acc / static_cast<double>(heads) : 0.0;
+      if (epoch_loss) epoch_loss[it] = mean_loss;
+      for (auto& t : r) {
+        t->count_comm();
+        ++t->epochs_done;
+      }
+      if (R0().cfg.verbose) {
+        const double secs =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - R0().s_t0).count();
+        const double lr = R0().lr0 * (1.0 - static_cast<double>(e) /
+                                                static_cast<double>(R0().cfg.epochs));
+        std::fprintf(stderr, "epoch %llu/%llu lr %.6g loss %.6f time %.2fs\n",
+                     (unsigned long long)(e + 1), (unsigned long long)R0().cfg.epochs, lr,
+                     mean_loss, secs);
+      }
+    }
+  }
+
+  void set_layout(const double* in, int loc) {
+    std::vector<double> host;
+    if (loc == NOMAD_B200_DEVICE && grp && !grp->loopback && r.size() > 1) {
+      R0().bind();  // ranks on other devices read a host copy
+      host.resize(2 * R0().n);
+      NB_CUDA(cudaMemcpy(host.data(), in, host.size() * 8, cudaMemcpyDeviceToHost));
+      in = host.data();
+      loc = NOMAD_B200_HOST;
+    }
+    for (auto& t : r) { t->bind(); t->set_rows(in, loc); }
+    means_all();
+    for (auto& t : r) { t->bind(); NB_CUDA(cudaStreamSynchronize(t->st())); }
+  }
+
+  void layout(double* out, int loc) {
+    if (loc == NOMAD_B200_DEVICE && grp && !grp->loopback && r.size() > 1)
+      fail(kParameter, "device layout output of a multi-device group: use a host buffer");
+    for (auto& t : r) { t->bind(); t->layout(out, loc); }
+  }
+};
+
+namespace {
+
+// Host copies of device-resident trainer inputs (ranks on other devices).
+struct HostInputs {
+  std::vector<uint32_t> off, nbr, asg;
+  std::vector<double> init;
+  nomad_b200_graph g{};
+  nomad_b200_clusters c{};
+};
+
+void to_host(const nomad_b200_graph* g, const nomad_b200_clusters* c, const double* init,
+             int init_loc, HostInputs& H) {
+  const uint64_t n = c->rows;
+  H.g = *g;
+  H.c = *c;
+  if (g->location == NOMAD_B200_DEVICE) {
+    H.off.resize(n + 1);
+    NB_CUDA(cudaMemcpy(H.off.data(), g->offsets, (n + 1) * 4, cudaMemcpyDeviceToHost));
+    H.nbr.resize(std::max<uint32_t>(H.off[n], 1));
+    if (H.off[n])
+      NB_CUDA(cudaMemcpy(H.nbr.data(), g->neighbors, (size_t)H.off[n] * 4, cudaMemcpyDeviceToHost));
+    H.g.offsets = H.off.data();
+    H.g.neighbors = H.nbr.data();
+    H.g.distances = nullptr;
+    H.g.location = NOMAD_B200_HOST;
+  }
+  if (c->location == NOMAD_B200_DEVICE) {
+    H.asg.resize(n);
+    NB_CUDA(cudaMemcpy(H.asg.data(), c->assignment, n * 4, cudaMemcpyDeviceToHost));
+    H.c.assignment = H.asg.data();
+    H.c.centroids = nullptr;
+    H.c.sizes = nullptr;
+    H.c.location = NOMAD_B200_HOST;
+  }
+  if (init_loc == NOMAD_B200_DEVICE) {
+    H.init.resize(2 * n);
+    NB_CUDA(cudaMemcpy(H.init.data(), init, n * 16, cudaMemcpyDeviceToHost));
+  }
+}
+
+}  // namespace
+
 extern "C" {
 
 int32_t nomad_b200_trainer_create(nomad_b200_ctx* ctx, const nomad_b200_graph* graph,
@@ -990,34 +1261,87 @@ int32_t nomad_b200_trainer_create(nomad_b200_ctx* ctx, const nomad_b200_graph* g
   return guard([&] {
     if (!ctx || !graph || !clusters || !init || !cfg || !out) fail(kParameter, "NULL argument");
     bind_device(ctx);
-    auto* t = new nomad_b200_trainer();
+    auto tr = std::make_unique<nomad_b200_trainer>();
+    auto t = std::make_unique<RankTrainer>();
     t->ctx = ctx;
     t->cfg = *cfg;
     t->rank = rank;
     t->world = world;
-    try {
-      t->setup(graph, clusters, init, init_loc, nccl_id);
-    } catch (...) {
-      delete t;
-      throw;
+    t->setup(graph, clusters, init, init_loc, nccl_id);
+    tr->r.push_back(std::move(t));
+    tr->after_setup();
+    *out = tr.release();
+  });
+}
+
+int32_t nomad_b200_group_trainer_create(nomad_b200_group* grp, const nomad_b200_graph* graph,
+                                        const nomad_b200_clusters* clusters, const double* init,
+                                        int32_t init_loc, const nomad_b200_train_config* cfg,
+                                        nomad_b200_trainer** out) {
+  return guard([&] {
+    if (!grp || !graph || !clusters || !init || !cfg || !out) fail(kParameter, "NULL argument");
+    const int G = (int)grp->ctx.size();
+    auto tr = std::make_unique<nomad_b200_trainer>();
+    tr->grp = grp;
+    HostInputs H;
+    const nomad_b200_graph* g = graph;
+    const nomad_b200_clusters* c = clusters;
+    const double* in = init;
+    int in_loc = init_loc;
+    const bool on_dev = graph->location == NOMAD_B200_DEVICE ||
+                        clusters->location == NOMAD_B200_DEVICE || init_loc == NOMAD_B200_DEVICE;
+    if (G > 1 && !grp->loopback && on_dev) {  // inputs live on rank 0's device
+      bind_device(grp->ctx[0]);
+      to_host(graph, clusters, init, init_loc, H);
+      g = &H.g;
+      c = &H.c;
+      if (init_loc == NOMAD_B200_DEVICE) {
+        in = H.init.data();
+        in_loc = NOMAD_B200_HOST;
+      }
     }
-    *out = t;
+    for (int rk = 0; rk < G; ++rk) {
+      auto t = std::make_unique<RankTrainer>();
+      t->ctx = grp->ctx[rk];
+      t->cfg = *cfg;
+      t->rank = rk;
+      t->world = G;
+      t->grouped = true;
+      t->comm = grp->comm.empty() ? nullptr : static_cast<ncclComm_t>(grp->comm[rk]);
+      t->bind();
+      t->setup(g, c, in, in_loc, nullptr);
+      tr->r.push_back(std::move(t));
+    }
+    tr->after_setup();
+    *out = tr.release();
   });
 }
 
 int32_t nomad_b200_trainer_destroy(nomad_b200_trainer* t) {
   return guard([&] {
     if (!t) return;
-    bind_device(t->ctx);
-    cudaStreamSynchronize(t->ctx->stream);
+    for (auto& x : t->r) {
+      bind_device(x->ctx);
+      cudaStreamSynchronize(x->ctx->stream);
+    }
+    for (auto& x : t->r) {  // each rank's buffers on its own device
+      bind_device(x->ctx);
+      x.reset();
+    }
     delete t;
+  });
+}
+
+int32_t nomad_b200_trainer_ranks(nomad_b200_trainer* t, int32_t* ranks) {
+  return guard([&] {
+    if (!t || !ranks) fail(kParameter, "NULL argument");
+    *ranks = (int32_t)t->r.size();
   });
 }
 
 int32_t nomad_b200_trainer_run(nomad_b200_trainer* t, uint64_t n_epochs, double* epoch_loss) {
   return guard([&] {
     if (!t) fail(kParameter, "trainer is NULL");
-    bind_device(t->ctx);
     t->run(n_epochs, epoch_loss);
   });
 }
@@ -1025,7 +1349,6 @@ int32_t nomad_b200_trainer_run(nomad_b200_trainer* t, uint64_t n_epochs, double*
 int32_t nomad_b200_trainer_layout(nomad_b200_trainer* t, double* out, int32_t loc) {
   return guard([&] {
     if (!t || !out) fail(kParameter, "NULL argument");
-    bind_device(t->ctx);
     t->layout(out, loc);
   });
 }
@@ -1033,12 +1356,13 @@ int32_t nomad_b200_trainer_layout(nomad_b200_trainer* t, double* out, int32_t lo
 int32_t nomad_b200_trainer_means(nomad_b200_trainer* t, double* means, uint32_t* counts) {
   return guard([&] {
     if (!t) fail(kParameter, "trainer is NULL");
-    bind_device(t->ctx);
+    RankTrainer& R = t->R0();
+    R.bind();
     if (means) {
-      NB_CUDA(cudaMemcpyAsync(means, t->means.p, t->C * 16, cudaMemcpyDeviceToHost, t->st()));
-      NB_CUDA(cudaStreamSynchronize(t->st()));
+      NB_CUDA(cudaMemcpyAsync(means, R.means.p, R.C * 16, cudaMemcpyDeviceToHost, R.st()));
+      NB_CUDA(cudaStreamSynchronize(R.st()));
     }
-    if (counts) std::memcpy(counts, t->sizes.data(), t->C * 4);
+    if (counts) std::memcpy(counts, R.sizes.data(), R.C * 4);
   });
 }
 
@@ -1046,17 +1370,17 @@ int32_t nomad_b200_trainer_comm(nomad_b200_trainer* t, uint64_t* epochs, uint64_
                                 uint64_t* doubles, uint64_t* counts) {
   return guard([&] {
     if (!t) fail(kParameter, "trainer is NULL");
-    if (epochs) *epochs = t->comm_epochs;
-    if (messages) *messages = t->comm_msgs;
-    if (doubles) *doubles = t->comm_doubles;
-    if (counts) *counts = t->comm_counts;
+    RankTrainer& R = t->R0();
+    if (epochs) *epochs = R.comm_epochs;
+    if (messages) *messages = R.comm_msgs;
+    if (doubles) *doubles = R.comm_doubles;
+    if (counts) *counts = R.comm_counts;
   });
 }
 
 int32_t nomad_b200_trainer_set_layout(nomad_b200_trainer* t, const double* layout, int32_t loc) {
   return guard([&] {
     if (!t || !layout) fail(kParameter, "NULL argument");
-    bind_device(t->ctx);
     t->set_layout(layout, loc);
   });
 }
@@ -1065,16 +1389,28 @@ int32_t nomad_b200_trainer_timing(nomad_b200_trainer* t, double* sgd_ms, double*
                                   uint64_t* epochs) {
   return guard([&] {
     if (!t) fail(kParameter, "trainer is NULL");
-    if (sgd_ms) *sgd_ms = t->sgd_ms;
-    if (means_ms) *means_ms = t->means_ms;
-    if (epochs) *epochs = t->timed_epochs;
+    // device time of the slowest rank (ranks of a loopback group share one
+    // GPU and run one after another: their sum)
+    double a = 0.0, b = 0.0;
+    for (auto& x : t->r) {
+      if (t->grp && t->grp->loopback) {
+        a += x->sgd_ms;
+        b += x->means_ms;
+      } else {
+        a = std::max(a, x->sgd_ms);
+        b = std::max(b, x->means_ms);
+      }
+    }
+    if (sgd_ms) *sgd_ms = a;
+    if (means_ms) *means_ms = b;
+    if (epochs) *epochs = t->R0().timed_epochs;
   });
 }
 
 int32_t nomad_b200_trainer_seek(nomad_b200_trainer* t, uint64_t epoch) {
   return guard([&] {
     if (!t) fail(kParameter, "trainer is NULL");
-    t->seek(epoch);
+    for (auto& x : t->r) x->seek(epoch);
   });
 }
 
@@ -1082,8 +1418,10 @@ int32_t nomad_b200_trainer_progress(nomad_b200_trainer* t, uint64_t* epochs_done
                                     uint64_t* edge_updates) {
   return guard([&] {
     if (!t) fail(kParameter, "trainer is NULL");
-    if (epochs_done) *epochs_done = t->epochs_done;
-    if (edge_updates) *edge_updates = t->edge_updates;
+    uint64_t e = 0;
+    for (auto& x : t->r) e += x->edge_updates;
+    if (epochs_done) *epochs_done = t->R0().epochs_done;
+    if (edge_updates) *edge_updates = e;
   });
 }
 

@@ -143,3 +143,86 @@ def test_config_a_replay(port, ctx):
     rl, rloss, _, _ = _oracle(port, c, g, pca, 3, **kw)
     assert np.array_equal(tr.layout(), rl)
     np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
+def _many_clusters(C, per, k, seed=3):
+    """C clusters of `per` points (cluster of i = i mod C), lists of the other
+    min(k, per - 1) members: more cells than the shared-memory tables hold."""
+    n = C * per
+    rng = np.random.default_rng(seed)
+    i = np.arange(n)
+    a = (i % C).astype(np.uint32)
+    q = i // C
+    m = min(k, per - 1)
+    nb = np.stack([a + C * ((q + r) % per) for r in range(1, m + 1)], 1).astype(np.uint32)
+    offsets = (np.arange(n + 1) * m).astype(np.uint32)
+    return n, a, offsets, nb.reshape(-1), rng.normal(size=(n, 2))
+
+
+@pytest.mark.parametrize("mode", ["replay", "hogwild"])
+def test_many_clusters_global_cell_tables(port, ctx, mode):
+    """C = 9000 > the old shared-memory cap (~8450 cells): the cell
+    tables move to global memory. The reference's auto C = ceil(n / 4096)
+    (optimizer.hpp:73-77) reaches 14.6k at 60M rows."""
+    import paper_2505_15511_b200 as nb
+    from oracle import train_config
+    C = 9000
+    n, a, off, nbr, init = _many_clusters(C, 6, 15)
+    kw = dict(epochs=10, workers=8, seed=7)
+    tr = nb.Trainer(nb.KnnGraph(n, 15, off, nbr, np.zeros(0)),
+                    nb.ClusterAssignment(a, C, 0, np.zeros(0), np.zeros(0)), init,
+                    nb.TrainConfig(sgd_mode=mode, **kw), ctx=ctx)
+    n_run = 2 if mode == "replay" else 6
+    loss = tr.run(n_run)
+    rl, rloss, rmeans, _ = port.train_epochs(a, C, off, nbr, 15, train_config(**kw), init, 0, n_run)
+    if mode == "replay":
+        assert np.array_equal(tr.layout(), rl)
+        np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+        assert np.array_equal(tr.means()[0], rmeans)
+    else:
+        assert np.isfinite(tr.layout()).all()
+        assert abs(loss[-3:].mean() - rloss[-3:].mean()) < 0.05 * rloss[-3:].mean()
+        assert tr.progress()[1] == n_run * n * (5 + 5)
+
+
+def test_list_longer_than_k_is_rejected(ctx):
+    """k_build_ell: a list longer than k or naming another
+    worker's point is a Parameter error, not a silent out-of-table read."""
+    import paper_2505_15511_b200 as nb
+    n, a, off, nbr, init = _many_clusters(64, 20, 15)
+    g = nb.KnnGraph(n, 12, off, nbr, np.zeros(0))  # lists hold 15 > k = 12
+    with pytest.raises(nb.NomadError) as e:
+        nb.Trainer(g, nb.ClusterAssignment(a, 64, 0, np.zeros(0), np.zeros(0)), init,
+                   nb.TrainConfig(epochs=2, workers=2, k=12), ctx=ctx)
+    assert e.value.kind == "Parameter"
+    bad = nbr.copy().reshape(n, 15)
+    bad[0, 0] = 1  # point 1 is in cluster 1; with W=64 workers it is another worker's
+    with pytest.raises(nb.NomadError) as e:
+        nb.Trainer(nb.KnnGraph(n, 15, off, bad.reshape(-1), np.zeros(0)),
+                   nb.ClusterAssignment(a, 64, 0, np.zeros(0), np.zeros(0)), init,
+                   nb.TrainConfig(epochs=2, workers=64), ctx=ctx)
+    assert e.value.kind == "Parameter"
+
+
+@pytest.mark.parametrize("mode", ["all_but_own", "head_only"])
+@pytest.mark.parametrize("double_float", [False, True])
+def test_hogwild_ablation_modes(port, ctx, mode, double_float):
+    """The throughput kernel's ablation instances (k_sgd_hogwild<..., ABO>,
+    head_only; optimizer.hpp:264-277, :294): loss trajectory within 5% of the
+    reference's in the same mode, every edge counted."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=30, workers=4, seed=7)
+    okw = dict(kw)
+    if mode == "all_but_own":
+        kw["approx"] = "non-own-cluster"
+        okw["approx_all_but_own"] = 1
+    else:
+        kw["head_only"] = True
+        okw["head_only"] = 1
+    tr = _trainer(nb, ctx, c, g, pca, sgd_mode="hogwild", hogwild_double_float=double_float, **kw)
+    loss = tr.run(30)
+    assert np.isfinite(tr.layout()).all()
+    _, rloss, _, _ = _oracle(port, c, g, pca, 30, **okw)
+    assert abs(loss[-5:].mean() - rloss[-5:].mean()) < 0.05 * rloss[-5:].mean()
+    assert tr.progress()[1] == 30 * 3000 * 20
