@@ -363,6 +363,33 @@ int32_t nomad_b200_fit(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* data,
                        nomad_b200_clusters* clusters_out,
                        nomad_b200_graph* graph_out, double* epoch_loss_out);
 
+/* Everything fit() produced besides the layout (FitReport,
+ * optimizer.hpp:312-321), each taken from the engine's own outputs. Every
+ * pointer may be NULL; host buffers unless the view says otherwise. */
+typedef struct {
+  nomad_b200_clusters* clusters;  /* ClusterAssignment (kmeans.hpp:32-43) */
+  nomad_b200_graph* graph;        /* KnnGraph (knn.hpp:31-47) */
+  double* epoch_mean_loss;        /* epochs */
+  double* pca;                    /* rows x 2: the init layout the epochs started from */
+  double* final_means;            /* n_clusters x 2: the last all-gathered ClusterMeans */
+  uint32_t* cluster_to_worker;    /* n_clusters: ShardPlan (optimizer.hpp:94-144) */
+  double* affinity_weights;       /* rows * k: p(j|i) per edge, CSR as the graph (affinity.hpp:65-84) */
+  uint32_t* eligible_heads;       /* rows: points with >= 1 neighbour, ascending */
+  /* out */
+  uint64_t n_clusters;            /* resolved C (optimizer.hpp:73-77) */
+  uint64_t n_eligible;
+  uint64_t comm_epochs, comm_messages, comm_payload_doubles, comm_payload_counts; /* CommLog */
+} nomad_b200_fit_report;
+
+/* fit() with the whole report, on one context (group == NULL) or on a group
+ * (ctx == NULL: the index is built on rank 0's device, the epochs run on
+ * every rank of the group). init_layout NULL: the GPU PCA (bit-identical in
+ * replay mode, the precomputed-covariance form in throughput mode). */
+int32_t nomad_b200_fit_ex(nomad_b200_ctx* ctx, nomad_b200_group* group,
+                          const nomad_b200_dataset_view* data,
+                          const nomad_b200_train_config* cfg, const double* init_layout,
+                          double* layout_out, nomad_b200_fit_report* report);
+
 /* ----------------------------------------------------------- data I/O */
 /* dataset.hpp:122-173 load_vectors_raw: little-endian f32 row-major file;
  * rows or dims may be 0 (derived from the file size; both given = strict).

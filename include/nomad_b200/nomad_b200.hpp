@@ -33,6 +33,10 @@ namespace nomad::b200 {
 /// Engine-only knobs (not part of the reference's TrainConfig).
 struct EngineOptions {
   int device = 0;
+  /// fit() over several GPUs from this one call (the reference runs its W
+  /// workers from one fit() call, optimizer.hpp:399-408): empty = {device}.
+  /// Distinct devices: NCCL; one device repeated: loopback ranks on it.
+  std::vector<int> devices;
   int sgd_mode = NOMAD_B200_SGD_REPLAY;  // bit-exact replay by default
   int knn_mode = NOMAD_B200_KNN_EXACT;
   unsigned hogwild_cap = 0;
@@ -68,6 +72,27 @@ inline nomad_b200_ctx* ctx() {
     h.dev = options().device;
   }
   return h.c;
+}
+
+/// The group over options().devices (created on first use, per thread).
+inline nomad_b200_group* group() {
+  struct Holder {
+    nomad_b200_group* g = nullptr;
+    std::vector<int> devs;
+    ~Holder() {
+      if (g) nomad_b200_group_destroy(g);
+    }
+  };
+  static thread_local Holder h;
+  const auto& want = options().devices;
+  if (!h.g || h.devs != want) {
+    if (h.g) nomad_b200_group_destroy(h.g);
+    h.g = nullptr;
+    std::vector<int32_t> d(want.begin(), want.end());
+    check(nomad_b200_group_create(d.data(), (int32_t)d.size(), &h.g));
+    h.devs = want;
+  }
+  return h.g;
 }
 
 inline nomad_b200_dataset_view view(const VectorDataset& d) {
@@ -181,33 +206,54 @@ inline LayoutMatrix pca_init(const VectorDataset& data, std::uint64_t seed = 0) 
   return l;
 }
 
-/// optimizer.hpp:327-482. The report's affinity / plan / final means are
-/// rebuilt on the host from the engine's clusters and graph with the
-/// reference's own build_affinity / shard_clusters / gather_means.
+/// optimizer.hpp:327-482. Every FitReport field comes from the engine: the
+/// index, the PCA the epochs started from (bit-identical in replay mode, the
+/// precomputed-covariance form in throughput mode), the affinity weights and
+/// eligible heads, the shard plan, the last all-gathered means and CommLog.
 inline LayoutMatrix fit(const VectorDataset& data, const TrainConfig& config,
                         FitReport* report = nullptr) {
   config.validate();
   const std::size_t n = data.rows;
   const std::size_t C = config.resolve_clusters(n);
-  const LayoutMatrix pca = nomad::b200::pca_init(data, config.seed);
   LayoutMatrix out = LayoutMatrix::zeros(n);
   ClusterAssignment ca;
-  ca.n_clusters = C;
-  ca.dims = data.dims;
-  ca.assignment.assign(n, 0);
-  ca.centroids.assign(C * data.dims, 0.0);
-  ca.sizes.assign(C, 0);
   KnnGraph g;
-  g.rows = n;
-  g.k = config.k;
-  g.offsets.assign(n + 1, 0);
-  g.neighbors.assign(n * config.k, 0);
-  g.distances.assign(n * config.k, 0.0);
-  std::vector<double> losses(config.epochs > 0 ? config.epochs : 1);
+  LayoutMatrix pca;
+  std::vector<double> losses, means, weights;
+  std::vector<std::uint32_t> c2w, elig;
+  nomad_b200_clusters cv{};
+  nomad_b200_graph gv{};
+  nomad_b200_fit_report rep{};
+  if (report) {  // the full outputs only when asked for (12 n k bytes of graph)
+    ca.n_clusters = C;
+    ca.dims = data.dims;
+    ca.assignment.assign(n, 0);
+    ca.centroids.assign(C * data.dims, 0.0);
+    ca.sizes.assign(C, 0);
+    g.rows = n;
+    g.k = config.k;
+    g.offsets.assign(n + 1, 0);
+    g.neighbors.assign(n * config.k, 0);
+    g.distances.assign(n * config.k, 0.0);
+    pca = LayoutMatrix::zeros(n);
+    losses.assign(config.epochs > 0 ? config.epochs : 1, 0.0);
+    means.assign(2 * C, 0.0);
+    weights.assign(n * config.k, 0.0);
+    c2w.assign(C, 0);
+    elig.assign(n, 0);
+    cv = detail::cview(ca, n);
+    gv = nomad_b200_graph{n, config.k, g.offsets.data(), g.neighbors.data(), g.distances.data(),
+                          NOMAD_B200_HOST};
+    rep.clusters = &cv;
+    rep.graph = &gv;
+    rep.epoch_mean_loss = losses.data();
+    rep.pca = pca.positions.data();
+    rep.final_means = means.data();
+    rep.cluster_to_worker = c2w.data();
+    rep.affinity_weights = weights.data();
+    rep.eligible_heads = elig.data();
+  }
   const auto v = detail::view(data);
-  auto cv = detail::cview(ca, n);
-  nomad_b200_graph gv{n, config.k, g.offsets.data(), g.neighbors.data(), g.distances.data(),
-                      NOMAD_B200_HOST};
   auto c = detail::cfg(config);
   // checkpoint rows carry the dataset's ids / labels, as save_layout does
   std::vector<const char*> idp, lbp;
@@ -215,24 +261,45 @@ inline LayoutMatrix fit(const VectorDataset& data, const TrainConfig& config,
   for (const auto& s : data.labels) lbp.push_back(s.c_str());
   c.checkpoint_ids = idp.size() == n ? idp.data() : nullptr;
   c.checkpoint_labels = lbp.size() == n ? lbp.data() : nullptr;
-  detail::check(nomad_b200_fit(detail::ctx(), &v, &c, pca.positions.data(),
-                               out.positions.data(), &cv, &gv, losses.data()));
+  const bool multi = options().devices.size() > 1;
+  detail::check(nomad_b200_fit_ex(multi ? nullptr : detail::ctx(), multi ? detail::group() : nullptr,
+                                  &v, &c, nullptr, out.positions.data(), report ? &rep : nullptr));
   out.epoch = config.epochs;
   if (report) {
     g.neighbors.resize(g.offsets[n]);
     g.distances.resize(g.offsets[n]);
+    weights.resize(g.offsets[n]);
+    elig.resize(rep.n_eligible);
     report->clusters = ca;
-    report->graph = g;
-    report->affinity = nomad::build_affinity(g);
-    report->plan = nomad::shard_clusters(ca, config.workers);
-    report->pca = pca;
-    report->final_means = nomad::gather_means(out, ca, config.epochs);
+    report->affinity.rows = n;
+    report->affinity.offsets = g.offsets;
+    report->affinity.neighbors = g.neighbors;
+    report->affinity.weights = std::move(weights);
+    report->affinity.eligible_heads = std::move(elig);
+    report->graph = std::move(g);
+    // ShardPlan (optimizer.hpp:94-144) from the engine's cluster -> worker map
+    ShardPlan& P = report->plan;
+    P.workers = config.workers;
+    P.cluster_to_worker = c2w;
+    P.worker_clusters.assign(config.workers, {});
+    P.worker_points.assign(config.workers, {});
+    P.worker_point_counts.assign(config.workers, 0);
+    for (std::size_t r = 0; r < C; ++r) P.worker_clusters[c2w[r]].push_back((std::uint32_t)r);
+    for (std::size_t i = 0; i < n; ++i) {
+      const std::uint32_t w = c2w[ca.assignment[i]];
+      P.worker_points[w].push_back((std::uint32_t)i);
+      ++P.worker_point_counts[w];
+    }
+    report->pca = std::move(pca);
+    report->final_means.means = std::move(means);
+    report->final_means.counts = ca.sizes;
+    report->final_means.epoch_stamp = config.epochs;
     report->comm.epochs.assign(config.epochs, {});
     for (auto& msgs : report->comm.epochs)
       for (std::size_t w = 0; w < config.workers; ++w) {
         MeansMessage m;
         m.worker = static_cast<std::uint32_t>(w);
-        m.clusters = static_cast<std::uint32_t>(report->plan.worker_clusters[w].size());
+        m.clusters = static_cast<std::uint32_t>(P.worker_clusters[w].size());
         m.payload_doubles = 2ull * m.clusters;
         m.payload_counts = m.clusters;
         msgs.push_back(m);

@@ -128,6 +128,11 @@ class Oracle:
                         [f64p, C.c_uint64, C.c_uint32, u32p, f64p, C.c_uint64, u32p,
                          C.c_uint64, u32p, f64p, C.c_uint64, f64p, C.c_uint64, C.c_double,
                          C.c_uint64, f64p, f64p])
+        self._knn_rows = fn("knn_rows", C.c_int, [f32p, u32p, C.c_uint64, C.c_uint64, u64p,
+                                                 C.c_uint64, C.c_uint64, u32p, f64p, C.c_int32])
+        self._nc_rows = fn("nearest_centroid_rows", None, [f32p, C.c_uint64, C.c_uint64, f64p,
+                                                          C.c_uint64, u32p, C.c_int32])
+        self._ccent = fn("cluster_centroid", None, [f32p, C.c_uint64, C.c_uint64, f64p])
         self._train = fn("train_epochs", C.c_int,
                          [C.c_uint64, C.c_uint64, u32p, u32p, u32p, C.c_uint64,
                           C.POINTER(TrainConfig), f64p, C.c_uint64, C.c_uint64, f64p, f64p,
@@ -153,6 +158,41 @@ class Oracle:
             self._qe = fn("quantization_error", C.c_double, [f32p, C.c_uint64, C.c_uint64, u32p, f64p])
             self._mix = fn("gaussian_mixture", None, [C.c_uint64, C.c_uint64, C.c_uint64,
                                                      C.c_double, C.c_uint64, f32p])
+
+    # -- per-row checkers (row samples of configurations B-E) ------------
+    def knn_rows(self, members: np.ndarray, ids: np.ndarray, queries, k: int,
+                 threads: int = 0):
+        """knn.hpp:88-106 for `queries` (indices into `members`, one cluster's
+        rows in ascending id): (ids[nq, want], dists[nq, want])."""
+        members = np.ascontiguousarray(members, np.float32)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        q = np.ascontiguousarray(queries, np.uint64)
+        m, d = members.shape
+        oi = np.zeros((len(q), k), np.uint32)
+        od = np.zeros((len(q), k), np.float64)
+        want = self._knn_rows(_p(members, C.c_float), _p(ids, C.c_uint32), m, d,
+                              _p(q, C.c_uint64), len(q), k, _p(oi, C.c_uint32),
+                              _p(od, C.c_double), threads or (os.cpu_count() or 1))
+        return oi[:, :want], od[:, :want]
+
+    def nearest_centroid_rows(self, rows: np.ndarray, centroids: np.ndarray,
+                              threads: int = 0) -> np.ndarray:
+        """kmeans.hpp:56-68 per row."""
+        rows = np.ascontiguousarray(rows, np.float32)
+        cent = np.ascontiguousarray(centroids, np.float64).reshape(-1)
+        nr, d = rows.shape
+        out = np.zeros(nr, np.uint32)
+        self._nc_rows(_p(rows, C.c_float), nr, d, _p(cent, C.c_double), len(cent) // d,
+                      _p(out, C.c_uint32), threads or (os.cpu_count() or 1))
+        return out
+
+    def cluster_centroid(self, members: np.ndarray) -> np.ndarray:
+        """kmeans.hpp:75-88 recompute_centroid from the member rows (ascending id)."""
+        members = np.ascontiguousarray(members, np.float32)
+        m, d = members.shape
+        out = np.zeros(d, np.float64)
+        self._ccent(_p(members, C.c_float), m, d, _p(out, C.c_double))
+        return out
 
     # -- errors ---------------------------------------------------------
     def _check(self, rc: int):

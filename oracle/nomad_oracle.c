@@ -471,6 +471,64 @@ int orc_build_knn(const float* x, uint64_t n, uint64_t d, uint64_t C,
   return 0;
 }
 
+/* Per-row checkers (config B/C parity on a row sample). knn.hpp:88-106 for
+ * the queries (indices into `members`, one cluster's rows in ascending id):
+ * the min(k, m-1) smallest (sq_dist_ff, id) pairs over the other members.
+ * Returns want. `threads` is ignored (single-threaded restatement). */
+int orc_knn_rows(const float* members, const uint32_t* ids, uint64_t m, uint64_t d,
+                 const uint64_t* queries, uint64_t nq, uint64_t k, uint32_t* out_ids,
+                 double* out_dist, int32_t threads) {
+  (void)threads;
+  const uint64_t want = k < (m ? m - 1 : 0) ? k : (m ? m - 1 : 0);
+  if (want == 0) return 0;
+  double* bd = (double*)malloc((want + 1) * 8);
+  uint32_t* bi = (uint32_t*)malloc((want + 1) * 4);
+  for (uint64_t q = 0; q < nq; ++q) {
+    const uint64_t qi = queries[q];
+    uint64_t cnt = 0;
+    for (uint64_t jj = 0; jj < m; ++jj) {
+      if (jj == qi) continue;
+      const uint32_t j = ids[jj];
+      const double dd = sq_dist_ff(members + qi * d, members + jj * d, d);
+      if (cnt == want && !(dd < bd[want - 1] || (dd == bd[want - 1] && j < bi[want - 1])))
+        continue;
+      uint64_t pos = cnt < want ? cnt : want - 1;
+      while (pos > 0 && (dd < bd[pos - 1] || (dd == bd[pos - 1] && j < bi[pos - 1]))) {
+        bd[pos] = bd[pos - 1];
+        bi[pos] = bi[pos - 1];
+        --pos;
+      }
+      bd[pos] = dd;
+      bi[pos] = j;
+      if (cnt < want) ++cnt;
+    }
+    for (uint64_t t = 0; t < want; ++t) {
+      out_ids[q * k + t] = bi[t];
+      out_dist[q * k + t] = bd[t];
+    }
+  }
+  free(bd);
+  free(bi);
+  return (int)want;
+}
+
+/* kmeans.hpp:56-68 nearest_centroid for a set of rows (strict <). */
+void orc_nearest_centroid_rows(const float* rows, uint64_t nr, uint64_t d,
+                               const double* centroids, uint64_t C, uint32_t* out,
+                               int32_t threads) {
+  (void)threads;
+  for (uint64_t i = 0; i < nr; ++i) out[i] = nearest_centroid(centroids, C, d, rows + i * d);
+}
+
+/* kmeans.hpp:75-88 one cluster's centroid from its member rows (ascending id). */
+void orc_cluster_centroid(const float* members, uint64_t m, uint64_t d, double* out) {
+  for (uint64_t j = 0; j < d; ++j) out[j] = 0.0;
+  for (uint64_t i = 0; i < m; ++i)
+    for (uint64_t j = 0; j < d; ++j) out[j] += (double)members[i * d + j];
+  if (m)
+    for (uint64_t j = 0; j < d; ++j) out[j] /= (double)m;
+}
+
 /* -------------------------------------------------------- optimizer.hpp */
 
 static int cmp_cluster_order_sizes_ctx_dummy;

@@ -16,6 +16,7 @@
 // Error convention (mirrors the product C-ABI): 0 = ok, else 1 + ErrorKind
 // (error.hpp:25-36); message via ref_last_error().
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -113,6 +114,73 @@ int ref_inverse_rank_weights(uint64_t k, double* out) {
 
 double ref_lr_schedule(uint64_t epoch, uint64_t total, double lr0) {
   return nomad::lr_schedule(epoch, total, lr0);
+}
+
+// Per-row checkers for configurations too large for the whole reference
+// build (1M-10M rows): the reference's own distance functions and selection
+// rule applied to a row sample.
+//
+// knn.hpp:51-58, :88-106 — for each query (an index into `members`, the rows
+// of one cluster in ascending point id), the min(k, m - 1) smallest
+// (detail::sq_dist_ff, id) pairs over the other members, by std::partial_sort
+// on std::pair<double, uint32_t> exactly as build_knn selects them.
+int ref_knn_rows(const float* members, const uint32_t* ids, uint64_t m, uint64_t d,
+                 const uint64_t* queries, uint64_t nq, uint64_t k, uint32_t* out_ids,
+                 double* out_dist, int32_t threads) {
+  const uint64_t want = std::min<uint64_t>(k, m ? m - 1 : 0);
+  auto one = [&](uint64_t q) {
+    const uint64_t qi = queries[q];
+    std::vector<std::pair<double, std::uint32_t>> cand;
+    cand.reserve(m);
+    for (uint64_t j = 0; j < m; ++j) {
+      if (j == qi) continue;
+      cand.emplace_back(nomad::detail::sq_dist_ff(members + qi * d, members + j * d, d), ids[j]);
+    }
+    std::partial_sort(cand.begin(), cand.begin() + want, cand.end());
+    for (uint64_t t = 0; t < want; ++t) {
+      out_ids[q * k + t] = cand[t].second;
+      out_dist[q * k + t] = cand[t].first;
+    }
+  };
+  const uint64_t nt = std::max<int32_t>(1, threads);
+  std::vector<std::thread> pool;
+  for (uint64_t t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      for (uint64_t q = t; q < nq; q += nt) one(q);
+    });
+  for (auto& x : pool) x.join();
+  return (int)want;
+}
+
+// kmeans.hpp:47-68 detail::nearest_centroid for a set of rows.
+void ref_nearest_centroid_rows(const float* rows, uint64_t nr, uint64_t d,
+                               const double* centroids, uint64_t C, uint32_t* out,
+                               int32_t threads) {
+  nomad::ClusterAssignment ca;
+  ca.n_clusters = C;
+  ca.dims = d;
+  ca.centroids.assign(centroids, centroids + C * d);
+  const uint64_t nt = std::max<int32_t>(1, threads);
+  std::vector<std::thread> pool;
+  for (uint64_t t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      for (uint64_t i = t; i < nr; i += nt) out[i] = nomad::detail::nearest_centroid(ca, rows + i * d);
+    });
+  for (auto& x : pool) x.join();
+}
+
+// kmeans.hpp:75-88 detail::recompute_centroid of one cluster, given only its
+// member rows in ascending point id (the other rows are skipped by the
+// reference's pass and do not change the sums).
+void ref_cluster_centroid(const float* members, uint64_t m, uint64_t d, double* out) {
+  nomad::VectorDataset ds = make_ds(members, m, d);
+  nomad::ClusterAssignment ca;
+  ca.n_clusters = 1;
+  ca.dims = d;
+  ca.assignment.assign(m, 0);
+  ca.centroids.assign(d, 0.0);
+  nomad::detail::recompute_centroid(ds, ca, 0);
+  std::memcpy(out, ca.centroids.data(), d * 8);
 }
 
 // kmeans.hpp:157-161

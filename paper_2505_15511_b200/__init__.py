@@ -5,7 +5,8 @@ Drop-in for the reference library's index build + epoch loop
 C-ABI in include/nomad_b200.h (libnomad_b200.so), bound here with ctypes.
 """
 from ._native import NomadError, build, lib, EXPORTED  # noqa: F401
-from .api import (ClusterAssignment, CommLog, Context, FitReport, Group, KnnGraph,  # noqa: F401
+from .api import (ClusterAssignment, CommLog, ConditionalAffinity, Context, FitReport,  # noqa: F401
+                  Group, KnnGraph, ShardPlan,
                   TrainConfig, Trainer, build_knn, default_kmeans_tol, fit,
                   kmeans_em_default_tol, knn_recall, pca_init, shard_plan,
                   generate_mixture, kmeans_em, lsh_init, nccl_unique_id,

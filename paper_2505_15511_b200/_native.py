@@ -62,6 +62,16 @@ class TrainConfigC(C.Structure):
                 ("verbose", C.c_int32)]
 
 
+class FitReportC(C.Structure):
+    _fields_ = [("clusters", C.c_void_p), ("graph", C.c_void_p), ("epoch_mean_loss", C.c_void_p),
+                ("pca", C.c_void_p), ("final_means", C.c_void_p),
+                ("cluster_to_worker", C.c_void_p), ("affinity_weights", C.c_void_p),
+                ("eligible_heads", C.c_void_p), ("n_clusters", C.c_uint64),
+                ("n_eligible", C.c_uint64), ("comm_epochs", C.c_uint64),
+                ("comm_messages", C.c_uint64), ("comm_payload_doubles", C.c_uint64),
+                ("comm_payload_counts", C.c_uint64)]
+
+
 _vp = C.c_void_p
 _SIGS = {
     "nomad_b200_last_error": (C.c_char_p, []),
@@ -121,6 +131,8 @@ _SIGS = {
     "nomad_b200_pca_init": (C.c_int32, [_vp, C.POINTER(DatasetView), C.c_uint64, _vp, C.c_int32]),
     "nomad_b200_fit": (C.c_int32, [_vp, C.POINTER(DatasetView), C.POINTER(TrainConfigC), _vp,
                                    _vp, C.POINTER(ClustersView), C.POINTER(GraphView), _vp]),
+    "nomad_b200_fit_ex": (C.c_int32, [_vp, _vp, C.POINTER(DatasetView), C.POINTER(TrainConfigC),
+                                      _vp, _vp, C.POINTER(FitReportC)]),
     "nomad_b200_plan": (C.c_int32, [C.c_uint64, C.c_uint64, _vp, C.c_uint64, C.c_int32, _vp, _vp,
                                     C.POINTER(C.c_uint32)]),
     "nomad_b200_debug_tc_gemm": (C.c_int32, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint32,

@@ -549,41 +549,93 @@ class Trainer:
 
 
 @dataclass
+class ConditionalAffinity:
+    """affinity.hpp:47-63: inverse-rank p(j|i) per edge (CSR as the graph)."""
+    rows: int
+    offsets: np.ndarray
+    neighbors: np.ndarray
+    weights: np.ndarray
+    eligible_heads: np.ndarray
+
+
+@dataclass
+class ShardPlan:
+    """optimizer.hpp:94-100."""
+    workers: int
+    cluster_to_worker: np.ndarray
+    worker_clusters: list
+    worker_points: list
+
+
+@dataclass
 class FitReport:
-    """optimizer.hpp:312-321 (the parts the engine reports)."""
+    """optimizer.hpp:312-321, every field from the engine's outputs."""
     clusters: Optional[ClusterAssignment] = None
     graph: Optional[KnnGraph] = None
+    affinity: Optional[ConditionalAffinity] = None
+    plan: Optional[ShardPlan] = None
+    pca: Optional[np.ndarray] = None
+    final_means: Optional[np.ndarray] = None
+    comm: Optional[CommLog] = None
     epoch_mean_loss: list = field(default_factory=list)
 
 
 def fit(data, config: TrainConfig, init_layout=None, report: Optional[FitReport] = None,
-        ctx: Optional[Context] = None) -> np.ndarray:
-    """optimizer.hpp:327-482. init_layout: the PCA initialisation (n x 2)."""
+        ctx: Optional[Context] = None, group: Optional[Group] = None) -> np.ndarray:
+    """optimizer.hpp:327-482. init_layout: the PCA initialisation (n x 2; None:
+    the GPU PCA). group: run the epochs on every rank of a Group."""
     config.validate()
     dv, keep = _dataset(data)
     n, d = dv.rows, dv.dims
     ncl = config.resolve_clusters(n)
-    ca = ClusterAssignment(np.zeros(n, np.uint32), ncl, d, np.zeros(ncl * d, np.float64),
-                           np.zeros(ncl, np.uint32))
-    cv = ca._view()
     k = config.k
-    off = np.zeros(n + 1, np.uint32)
-    nb = np.zeros(max(n * k, 1), np.uint32)
-    di = np.zeros(max(n * k, 1), np.float64)
-    gv = N.GraphView(n, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
     out = np.zeros((n, 2), np.float64)
-    losses = np.zeros(max(config.epochs, 1), np.float64)
     pl = None
     if init_layout is not None:
         il = np.ascontiguousarray(init_layout, np.float64)
         pl = il.ctypes.data
     c = config.c_struct()
-    check(lib().nomad_b200_fit(_ctx(ctx).h, C.byref(dv), C.byref(c), pl, out.ctypes.data,
-                               C.byref(cv), C.byref(gv), losses.ctypes.data))
+    rep = N.FitReportC()
+    hold = []
+    if report is not None:  # full outputs only when asked for (12 n k bytes of graph)
+        ca = ClusterAssignment(np.zeros(n, np.uint32), ncl, d, np.zeros(ncl * d, np.float64),
+                               np.zeros(ncl, np.uint32))
+        cv = ca._view()
+        off = np.zeros(n + 1, np.uint32)
+        nb = np.zeros(max(n * k, 1), np.uint32)
+        di = np.zeros(max(n * k, 1), np.float64)
+        gv = N.GraphView(n, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
+        losses = np.zeros(max(config.epochs, 1), np.float64)
+        pca = np.zeros((n, 2), np.float64)
+        means = np.zeros((ncl, 2), np.float64)
+        c2w = np.zeros(ncl, np.uint32)
+        aw = np.zeros(max(n * k, 1), np.float64)
+        el = np.zeros(max(n, 1), np.uint32)
+        hold = [cv, gv]
+        rep.clusters, rep.graph = C.addressof(cv), C.addressof(gv)
+        rep.epoch_mean_loss, rep.pca = losses.ctypes.data, pca.ctypes.data
+        rep.final_means, rep.cluster_to_worker = means.ctypes.data, c2w.ctypes.data
+        rep.affinity_weights, rep.eligible_heads = aw.ctypes.data, el.ctypes.data
+    h = group.h if group is not None else _ctx(ctx).h
+    check(lib().nomad_b200_fit_ex(None if group is not None else h,
+                                  h if group is not None else None, C.byref(dv), C.byref(c), pl,
+                                  out.ctypes.data, C.byref(rep)))
+    del hold
     if report is not None:
         m = int(off[n])
         report.clusters = ca
         report.graph = KnnGraph(n, k, off, nb[:m], di[:m])
+        report.affinity = ConditionalAffinity(n, off, nb[:m], aw[:m], el[:rep.n_eligible])
+        a = ca.assignment
+        report.plan = ShardPlan(config.workers, c2w,
+                                [np.nonzero(c2w == w)[0].astype(np.uint32)
+                                 for w in range(config.workers)],
+                                [np.nonzero(c2w[a] == w)[0].astype(np.uint32)
+                                 for w in range(config.workers)])
+        report.pca = pca
+        report.final_means = means
+        report.comm = CommLog(rep.comm_epochs, rep.comm_messages, rep.comm_payload_doubles,
+                              rep.comm_payload_counts)
         report.epoch_mean_loss = losses[: config.epochs].tolist()
     return out
 

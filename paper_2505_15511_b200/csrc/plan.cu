@@ -3,12 +3,33 @@
 // the static slot layout of the per-epoch means all-gather. Shared by the
 // trainer and the C-ABI (so multi-rank host logic is testable without GPUs).
 #include <algorithm>
+#include <cmath>
 #include <numeric>
 
 #include "common.cuh"
 #include "plan.cuh"
 
 namespace nb {
+
+std::vector<double> inverse_rank_weights(uint64_t k) {
+  std::vector<double> w(k);
+  double total = 0.0;
+  for (uint64_t t = 1; t <= k; ++t) {
+    w[t - 1] = std::exp(1.0 / static_cast<double>(t));
+    total += w[t - 1];
+  }
+  for (double& x : w) x /= total;
+  return w;
+}
+
+std::vector<double> weight_table(uint64_t k) {
+  std::vector<double> wt((k + 1) * k, 0.0);
+  for (uint64_t c = 1; c <= k; ++c) {
+    auto w = inverse_rank_weights(c);
+    std::copy(w.begin(), w.end(), wt.begin() + c * k);
+  }
+  return wt;
+}
 
 ShardPlan make_plan(const std::vector<uint32_t>& sizes, uint32_t W, int world) {
   const uint32_t C = (uint32_t)sizes.size();

@@ -54,18 +54,6 @@ inline uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {
   return d % n;
 }
 
-// affinity.hpp:32-42 inverse-rank weights (host libm exp, as the reference).
-std::vector<double> inverse_rank_weights(uint64_t k) {
-  std::vector<double> w(k);
-  double total = 0.0;
-  for (uint64_t t = 1; t <= k; ++t) {
-    w[t - 1] = std::exp(1.0 / static_cast<double>(t));
-    total += w[t - 1];
-  }
-  for (double& x : w) x /= total;
-  return w;
-}
-
 template <class T>
 void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
   d.alloc(std::max<size_t>(h.size(), 1));
@@ -284,11 +272,7 @@ struct RankTrainer {
     }
 
     // weights table (affinity.hpp:65-84: one table per neighbour count)
-    std::vector<double> wt((k + 1) * k, 0.0);
-    for (uint64_t c = 1; c <= k; ++c) {
-      auto w = inverse_rank_weights(c);
-      std::copy(w.begin(), w.end(), wt.begin() + c * k);
-    }
+    const std::vector<double> wt = weight_table(k);
     std::vector<double> cp(C);
     for (uint64_t r = 0; r < C; ++r) cp[r] = static_cast<double>(sizes[r]) / static_cast<double>(n);
 

@@ -65,6 +65,43 @@ int main() {
     if (f2) std::fclose(f2);
   }
   bad += rb.comm.epochs.size() != 20 || rb.comm.epochs[0].size() != 2;
+  // every FitReport field from the engine equals the reference's
+  bad += ra.affinity.offsets != rb.affinity.offsets || ra.affinity.neighbors != rb.affinity.neighbors ||
+         ra.affinity.weights != rb.affinity.weights ||
+         ra.affinity.eligible_heads != rb.affinity.eligible_heads;
+  bad += ra.plan.cluster_to_worker != rb.plan.cluster_to_worker ||
+         ra.plan.worker_clusters != rb.plan.worker_clusters ||
+         ra.plan.worker_points != rb.plan.worker_points ||
+         ra.plan.worker_point_counts != rb.plan.worker_point_counts;
+  bad += ra.pca.positions != rb.pca.positions;
+  bad += ra.final_means.means != rb.final_means.means || ra.final_means.counts != rb.final_means.counts ||
+         ra.final_means.epoch_stamp != rb.final_means.epoch_stamp;
+  for (std::size_t e = 0; e < ra.comm.epochs.size() && e < rb.comm.epochs.size(); ++e)
+    for (std::size_t w = 0; w < ra.comm.epochs[e].size() && w < rb.comm.epochs[e].size(); ++w) {
+      const auto &x = ra.comm.epochs[e][w], &y = rb.comm.epochs[e][w];
+      bad += x.worker != y.worker || x.clusters != y.clusters ||
+             x.payload_doubles != y.payload_doubles || x.payload_counts != y.payload_counts;
+    }
+  const int after_report = bad;
+  // TrainConfig{} defaults (auto C = max(ceil(n / 4096), W, 2), 200 epochs)
+  {
+    nomad::TrainConfig def;
+    auto da = nomad::fit(ds, def), db = nomad::b200::fit(ds, def);
+    bad += da.positions != db.positions;
+  }
+  const int after_defaults = bad;
+  // the same fit driven over a 2-rank group from this one call (loopback
+  // ranks on device 0; distinct devices would be joined by NCCL)
+  {
+    nomad::b200::options().devices = {0, 0};
+    nomad::FitReport rg;
+    auto lg = nomad::b200::fit(ds, cfg, &rg);
+    nomad::b200::options().devices.clear();
+    bad += la.positions != lg.positions || ra.epoch_mean_loss != rg.epoch_mean_loss ||
+           ra.final_means.means != rg.final_means.means;
+  }
+  if (bad) std::fprintf(stderr, "mismatch: report %d defaults %d group %d\n", after_report,
+                        after_defaults - after_report, bad - after_defaults);
   try {
     nomad::b200::lsh_init(ds, 1, 0);
     ++bad;

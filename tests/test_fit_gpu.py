@@ -91,6 +91,21 @@ def test_fit_fully_on_gpu_is_bit_exact(port, ref, ctx):
     out = nb.fit(x, nb.TrainConfig(seed=3, **kw), report=rep, ctx=ctx)
     assert np.array_equal(out, r["layout"])
     np.testing.assert_allclose(rep.epoch_mean_loss, r["epoch_loss"], rtol=1e-13, atol=0)
+    # FitReport (optimizer.hpp:312-321), every field from the engine's outputs
+    assert np.array_equal(rep.clusters.assignment, r["assignment"])
+    assert np.array_equal(rep.graph.offsets, r["offsets"])
+    assert np.array_equal(rep.graph.neighbors, r["neighbors"])
+    assert np.array_equal(rep.graph.distances, r["distances"])
+    assert np.array_equal(rep.pca, r["pca"])
+    assert np.array_equal(rep.final_means, r["final_means"])
+    cnt = np.diff(rep.graph.offsets.astype(np.int64))
+    want = np.concatenate([ref.inverse_rank_weights(int(c)) for c in cnt if c > 0])
+    assert np.array_equal(rep.affinity.weights, want)  # affinity.hpp:65-84
+    assert np.array_equal(rep.affinity.eligible_heads, np.nonzero(cnt)[0])
+    c2w, wpts = ref.shard_clusters(r["assignment"], r["n_clusters"], kw["workers"])
+    assert np.array_equal(rep.plan.cluster_to_worker, c2w)
+    assert all(np.array_equal(a, b) for a, b in zip(rep.plan.worker_points, wpts))
+    assert (rep.comm.epochs, rep.comm.messages) == (12, 12 * 2)
 
 
 def test_gpu_pca_rank_one_jitter(port, ctx):

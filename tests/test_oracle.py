@@ -142,3 +142,27 @@ def test_oracle_error_kinds(port):
     with pytest.raises(OracleError) as e:
         port.pca_init(np.ones((10, 3), np.float32))
     assert e.value.kind == "Degenerate"
+
+
+@pytest.mark.parametrize("which", ["port", "reference"])
+def test_row_checkers_match_whole_builds(which):
+    """The per-row checkers used at configs B/C (knn_rows, nearest_centroid_rows,
+    cluster_centroid) reproduce the whole reference build on a small case."""
+    from oracle import Oracle, available
+    if not available(which):
+        pytest.skip(f"{which} checker not built")
+    o = Oracle(which)
+    x = Oracle("port").gaussian_mixture(3000, 16, 5, 10.0, 42)
+    c = o.lsh_init(x, 4, 7)
+    c = o.kmeans_em(x, c, 100, o.default_kmeans_tol(x))
+    g = o.build_knn(x, c, 15)
+    for r in range(4):
+        mem = np.nonzero(c.assignment == r)[0]
+        q = np.arange(0, len(mem), 29)
+        ids, ds = o.knn_rows(x[mem], mem, q, 15)
+        for t, qi in enumerate(q):
+            i = mem[qi]
+            assert np.array_equal(ids[t], g.neighbors[g.offsets[i]:g.offsets[i + 1]])
+            assert np.array_equal(ds[t], g.distances[g.offsets[i]:g.offsets[i + 1]])
+        assert np.array_equal(o.cluster_centroid(x[mem]), c.centroids[r * 16:(r + 1) * 16])
+    assert np.array_equal(o.nearest_centroid_rows(x, c.centroids), c.assignment)

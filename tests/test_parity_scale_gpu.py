@@ -1,0 +1,91 @@
+"""BASELINE configs B (1M x 768, 8 clusters) and C (10M x 768, 64 clusters)
+pinned to the reference on row samples.
+
+The whole reference build is infeasible here (knn.hpp at 10M is ~46 CPU-days,
+SURVEY §6.3), but its per-row rules are cheap, so the reference's own
+functions check the GPU outputs row by row (oracle/ref_capi.cpp, or the C
+restatement where the compiled reference is absent):
+
+* kNN (knn.hpp:51-58, :88-106): for sampled rows of the smallest, a middle
+  and the largest cluster, the reference's sq_dist_ff against every member of
+  the row's cluster, selected by std::partial_sort on (distance, id) — ids
+  and fp64 distances must equal the GPU lists bit for bit.
+* k-means step (kmeans.hpp:56-68, :90-104): the last Lloyd iteration's
+  assignment of sampled rows must be the reference's nearest_centroid against
+  the previous iteration's centroids, and the final centroids of the sampled
+  clusters must be the reference's ascending-id recompute of their members.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {"B": (1_000_000, 768, 64, 8), "C": (10_000_000, 768, 64, 64)}
+
+
+def _checker():
+    from oracle import Oracle, available
+    return Oracle("reference" if available("reference") else "port")
+
+
+@pytest.fixture(scope="module", params=sorted(CONFIGS))
+def scale(request, ctx):
+    import torch
+    import paper_2505_15511_b200 as nb
+    n, d, blobs, C = CONFIGS[request.param]
+    x = nb.generate_mixture(n, d, blobs, 10.0, 42, ctx=ctx)
+    c0 = nb.lsh_init(x, C, 7, ctx=ctx)
+    trace = []
+    cl = nb.kmeans_em_default_tol(x, c0, 100, qe_trace=trace, ctx=ctx)
+    g = nb.build_knn(x, cl, 15, mode="exact", ctx=ctx)
+    yield request.param, x, c0, cl, len(trace), g
+    del x
+    torch.cuda.empty_cache()
+
+
+def _rows(x, idx):
+    import torch
+    t = torch.from_numpy(np.asarray(idx, np.int64)).to(x.device)
+    return x.index_select(0, t).cpu().numpy()
+
+
+def _sample_clusters(sizes):
+    order = np.argsort(sizes, kind="stable")
+    return sorted({int(order[0]), int(order[len(order) // 2]), int(order[-1])})
+
+
+def test_knn_rows_match_reference(scale):
+    name, x, c0, cl, iters, g = scale
+    orc = _checker()
+    rng = np.random.default_rng(17)
+    checked = 0
+    for r in _sample_clusters(cl.sizes):
+        mem = np.nonzero(cl.assignment == r)[0]  # ascending point id
+        rows = _rows(x, mem)
+        q = np.sort(rng.choice(len(mem), size=min(40, len(mem)), replace=False))
+        ids, dist = orc.knn_rows(rows, mem, q, 15)
+        for t, qi in enumerate(q):
+            i = mem[qi]
+            a, b = g.offsets[i], g.offsets[i + 1]
+            assert np.array_equal(g.neighbors[a:b], ids[t]), f"{name}: row {i} ids"
+            assert np.array_equal(g.distances[a:b], dist[t]), f"{name}: row {i} distances"
+            checked += 1
+    print(f"config {name}: {checked} rows' lists identical to the reference ({orc.which})")
+
+
+def test_kmeans_last_step_matches_reference(scale, ctx):
+    import paper_2505_15511_b200 as nb
+    name, x, c0, cl, iters, g = scale
+    orc = _checker()
+    prev = nb.kmeans_em_default_tol(x, c0, iters - 1, ctx=ctx) if iters > 1 else c0
+    n, d = x.shape
+    rng = np.random.default_rng(23)
+    idx = np.sort(rng.choice(n, size=20000, replace=False))
+    a = orc.nearest_centroid_rows(_rows(x, idx), prev.centroids)
+    assert np.array_equal(a, cl.assignment[idx]), f"{name}: assignment step"
+    for r in _sample_clusters(cl.sizes):
+        mem = np.nonzero(cl.assignment == r)[0]
+        ref = orc.cluster_centroid(_rows(x, mem))
+        assert np.array_equal(ref, cl.centroids[r * d:(r + 1) * d]), f"{name}: centroid {r}"
+    print(f"config {name}: {iters} Lloyd iterations; last assignment step and centroids "
+          f"identical to the reference ({orc.which})")
