@@ -214,6 +214,8 @@ class Group:
         check(lib().nomad_b200_group_create(C.cast(devs, C.c_void_p), len(devices), C.byref(h)))
         self.h = h
         self.devices = list(devices)
+        import weakref
+        self._trainers = weakref.WeakSet()  # closed before the group's contexts go
         n, lb = C.c_int32(), C.c_int32()
         check(lib().nomad_b200_group_size(self.h, C.byref(n), C.byref(lb)))
         self.size, self.loopback = n.value, bool(lb.value)
@@ -228,6 +230,8 @@ class Group:
 
     def close(self) -> None:
         if getattr(self, "h", None):
+            for t in list(getattr(self, "_trainers", ())):
+                t.close()
             lib().nomad_b200_group_destroy(self.h)
             self.h = None
 
@@ -492,6 +496,8 @@ class Trainer:
         r = C.c_int32()
         check(lib().nomad_b200_trainer_ranks(self.h, C.byref(r)))
         self.ranks = r.value
+        if group is not None:
+            group._trainers.add(self)
 
     def run(self, n_epochs: int) -> np.ndarray:
         out = np.zeros(max(n_epochs, 1), np.float64)

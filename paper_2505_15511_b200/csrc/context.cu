@@ -221,6 +221,7 @@ int32_t nomad_b200_destroy(nomad_b200_ctx* c) {
       cudaStreamSynchronize(c->stream);
       cudaStreamDestroy(c->stream);
     }
+    cudaGetLastError();  // teardown errors are not reported to later launches
     delete c;
   });
 }

@@ -1,0 +1,436 @@
+// K8r: deterministic replay of the reference's sequential per-worker epoch
+// (optimizer.hpp:232-307) entirely on the device.
+//
+//  1. k_mt_words   — each worker's std::mt19937_64 stream (rng.hpp:42-84),
+//                    one CTA per worker: the 312-word twist in two parallel
+//                    halves, tempering, the epoch's (1 + s) words per draw.
+//  2. k_replay_map — words -> head = eligible[uniform_index(|eligible|)],
+//                    tails = pool[uniform_index(|pool|)] (optimizer.hpp:
+//                    254-255, :284-285); a word in the rejection region of
+//                    rng.hpp:49-55 (probability n / 2^64) flags the worker,
+//                    whose epoch is then drawn on the host from the saved
+//                    start state.
+//  3. deps         — per draw its touch list (head, neighbours, tails,
+//                    duplicates removed), per point the draws touching it in
+//                    draw order (count, scan, scatter, per-point sort), and
+//                    per (draw, point) the latest earlier draw touching it.
+//  4. k_sgd_dataflow — persistent kernel; warps claim 32 consecutive draws of
+//                    a worker in worker-interleaved order; a draw runs once
+//                    every predecessor is done, so each point sees its updates
+//                    in exactly the sequential order and positions are
+//                    bit-identical (the arithmetic is the reference's op
+//                    order with _rn intrinsics).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "replay.cuh"
+#include "sgd_device.cuh"
+
+namespace nb {
+
+// ---------------------------------------------------------- MT19937-64
+constexpr unsigned long long kMtA = 0xB5026F5AA96619E9ull;
+constexpr unsigned long long kMtUM = 0xFFFFFFFF80000000ull, kMtLM = 0x7FFFFFFFull;
+
+__host__ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long x) {
+  x ^= (x >> 29) & 0x5555555555555555ull;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+  x ^= (x << 37) & 0xFFF7EEE000000000ull;
+  x ^= x >> 43;
+  return x;
+}
+// one step of the twist: (upper bit of a | lower 63 of b), shifted, xor A if odd
+__host__ __device__ __forceinline__ unsigned long long mt_mix(unsigned long long a,
+                                                              unsigned long long b) {
+  const unsigned long long x = (a & kMtUM) | (b & kMtLM);
+  return (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+}
+
+void Mt64::seed(uint64_t v) {
+  s.mt[0] = v;
+  for (uint32_t i = 1; i < 312; ++i)
+    s.mt[i] = 6364136223846793005ull * (s.mt[i - 1] ^ (s.mt[i - 1] >> 62)) + i;
+  s.p = 312;
+  s.pad = 0;
+}
+void Mt64::twist() {
+  for (uint32_t i = 0; i < 312; ++i)
+    s.mt[i] = s.mt[(i + 156) % 312] ^ mt_mix(s.mt[i], s.mt[(i + 1) % 312]);
+  s.p = 0;
+}
+uint64_t Mt64::next() {
+  if (s.p >= 312) twist();
+  return mt_temper(s.mt[s.p++]);
+}
+
+// One CTA per worker. Thread j < 156 of a twist owns words j and j + 156:
+//   new[j]       = old[j + 156] ^ mix(old[j], old[j + 1])            (j < 156)
+//   new[j + 156] = new[j] ^ mix(old[j + 156], old[j + 157] | new[0])  (j = 155: new[0])
+// which is the standard's in-place sequential loop.
+__global__ void __launch_bounds__(160) k_mt_words(ReplayDev R, const uint64_t* counts) {
+  __shared__ unsigned long long s[312];
+  const uint32_t w = blockIdx.x, tid = threadIdx.x;
+  const MtState* in = R.st_in + w;
+  for (uint32_t i = tid; i < 312; i += blockDim.x) s[i] = in->mt[i];
+  uint32_t p = in->p;
+  const uint64_t n = counts[w];
+  unsigned long long* o = R.words + R.word_base[w];
+  __syncthreads();
+  uint64_t done = 0;
+  {
+    const uint64_t take = p < 312 ? std::min<uint64_t>(312 - p, n) : 0;
+    for (uint32_t i = tid; i < take; i += blockDim.x) o[i] = mt_temper(s[p + i]);
+    done = take;
+    p += (uint32_t)take;
+  }
+  while (done < n) {
+    unsigned long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+    if (tid < 156) {
+      a0 = s[tid];
+      a1 = s[tid + 1];
+      b0 = s[tid + 156];
+      if (tid < 155) b1 = s[tid + 157];
+    }
+    __syncthreads();
+    unsigned long long n0 = 0;
+    if (tid < 156) {
+      n0 = b0 ^ mt_mix(a0, a1);
+      s[tid] = n0;
+    }
+    __syncthreads();
+    if (tid < 156) s[tid + 156] = n0 ^ mt_mix(b0, tid < 155 ? b1 : s[0]);
+    __syncthreads();
+    const uint64_t take = std::min<uint64_t>(312, n - done);
+    for (uint32_t i = tid; i < take; i += blockDim.x) o[done + i] = mt_temper(s[i]);
+    done += take;
+    p = (uint32_t)take;
+    __syncthreads();
+  }
+  MtState* out = R.st_out + w;
+  for (uint32_t i = tid; i < 312; i += blockDim.x) out->mt[i] = s[i];
+  if (tid == 0) {
+    out->p = p;
+    out->pad = 0;
+  }
+}
+
+__device__ __forceinline__ bool rejects(unsigned long long x, uint64_t n) {
+  return x >= n * (0xFFFFFFFFFFFFFFFFull / n);
+}
+
+// words -> heads and tails (blockIdx.y = local worker)
+__global__ void k_replay_map(ReplayDev R, SgdParams P, const uint32_t* pool,
+                             const uint32_t* pool_off) {
+  const uint32_t w = blockIdx.y;
+  const WorkerDev W = P.workers[w];
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= W.draws) return;
+  const uint32_t s = R.s;
+  const unsigned long long* x = R.words + R.word_base[w] + (uint64_t)t * (1 + s);
+  const uint32_t db = R.draw_base[w] + t;
+  bool rej = rejects(x[0], W.n_elig);
+  const uint32_t h = P.elig[W.elig_off + (uint32_t)(x[0] % W.n_elig)];
+  R.heads[db] = h;
+  if (P.all_but_own) {  // pool = the head's cluster (optimizer.hpp:264-277)
+    const LocalCluster L = P.lclusters[P.cl_of[h]];
+    for (uint32_t q = 0; q < s; ++q) {
+      rej |= rejects(x[1 + q], L.count);
+      R.tails[(size_t)db * s + q] = L.start + (uint32_t)(x[1 + q] % L.count);
+    }
+  } else {
+    const uint32_t* pl = pool + pool_off[w];
+    for (uint32_t q = 0; q < s; ++q) {
+      rej |= rejects(x[1 + q], W.npts);
+      R.tails[(size_t)db * s + q] = pl[(uint32_t)(x[1 + q] % W.npts)];
+    }
+  }
+  if (rej) atomicOr(R.reject + w, 1u);
+}
+
+// Touch list of every draw (head, neighbours in list order, tails; a point
+// touched twice by one draw is listed once) and per-point touch counts.
+__global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t T = R.T, s = R.s, k = P.k;
+  // edge-updates of the epoch per worker, |N(head)| + s per draw (warp-aggregated)
+  {
+    uint32_t w = 0, e = 0;
+    if (i < total) {
+      while (w + 1 < R.nwl && R.draw_base[w + 1] <= i) ++w;
+      e = (P.ncnt ? P.ncnt[R.heads[i]] : k) + s;
+    }
+    const uint32_t same = __match_any_sync(0xffffffffu, w);
+    const uint32_t sum = __reduce_add_sync(same, e);
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(same) - 1) && sum)
+      atomicAdd(R.edges + w, (unsigned long long)sum);
+  }
+  if (i >= total) return;
+  const uint32_t h = R.heads[i];
+  uint32_t* tl = R.touch + (size_t)i * T;
+  for (uint32_t j = 0; j < T; ++j) R.pred[(size_t)i * T + j] = 0xFFFFFFFFu;
+  const uint32_t cnt = P.ncnt ? P.ncnt[h] : k;
+  const uint32_t* nb = P.ell + (size_t)h * P.kpad;
+  tl[0] = h;
+  atomicAdd(R.tcount + h, 1u);
+  uint32_t j = 1;
+  for (; j <= cnt; ++j) {  // kNN lists hold distinct points other than the head
+    const uint32_t v = nb[j - 1];
+    tl[j] = v;
+    atomicAdd(R.tcount + v, 1u);
+  }
+  for (; j < 1 + k; ++j) tl[j] = 0xFFFFFFFFu;
+  const uint32_t* tails = R.tails + (size_t)i * s;
+  for (uint32_t q = 0; q < s; ++q) {
+    const uint32_t v = tails[q];
+    bool dup = v == h;
+    for (uint32_t a = 0; a < cnt && !dup; ++a) dup = nb[a] == v;
+    for (uint32_t a = 0; a < q && !dup; ++a) dup = tails[a] == v;
+    tl[1 + k + q] = dup ? 0xFFFFFFFFu : v;
+    if (!dup) atomicAdd(R.tcount + v, 1u);
+  }
+}
+
+// Scatter (t << 8 | slot) into each touched point's segment.
+__global__ void k_replay_scatter(ReplayDev R, uint32_t total) {
+  const uint32_t nwl = R.nwl;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  // worker of draw i (draw_base is ascending, nwl small)
+  uint32_t w = 0;
+  while (w + 1 < nwl && R.draw_base[w + 1] <= i) ++w;
+  const uint32_t t = i - R.draw_base[w];
+  const uint32_t* tl = R.touch + (size_t)i * R.T;
+  for (uint32_t j = 0; j < R.T; ++j) {
+    const uint32_t v = tl[j];
+    if (v == 0xFFFFFFFFu) continue;
+    const uint32_t pos = R.toff[v] + atomicAdd(R.tcount + v, 1u);
+    R.tlist[pos] = ((unsigned long long)t << 8) | j;
+  }
+}
+
+// Per point: sort its touches by draw order, link each to its predecessor.
+__global__ void k_replay_pred(ReplayDev R, uint32_t n_loc) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n_loc) return;
+  const uint32_t b = R.toff[v], e = R.toff[v + 1];
+  unsigned long long* L = R.tlist + b;
+  const uint32_t m = e - b;
+  // insertion sort in place (segments are short: ~(1 + k + s) touches per point)
+  for (uint32_t a = 1; a < m; ++a) {
+    const unsigned long long x = L[a];
+    uint32_t c = a;
+    while (c > 0 && L[c - 1] > x) {
+      L[c] = L[c - 1];
+      --c;
+    }
+    L[c] = x;
+  }
+  const uint32_t base = R.pt_base[v];  // draw base of the point's worker
+  uint32_t prev = 0xFFFFFFFFu;
+  for (uint32_t a = 0; a < m; ++a) {
+    const uint32_t t = (uint32_t)(L[a] >> 8), j = (uint32_t)(L[a] & 0xFF);
+    R.pred[(size_t)(base + t) * R.T + j] = prev;
+    prev = t;
+  }
+}
+
+// ------------------------------------------------------ dataflow SGD
+__device__ __forceinline__ double2 ldpos(const double2* p) { return __ldcg(p); }
+
+__global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) {
+  extern __shared__ __align__(16) double sm[];
+  const uint32_t k = P.k, s = P.s, C = P.n_clusters, T = R.T;
+  double* wt = sm;
+  double* cms = sm + (k + 1) * k;  // 3*C: mu.x, mu.y, p (or the global [C][3] table)
+  for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
+  if (!P.gcells)
+    for (uint32_t r = threadIdx.x; r < C; r += blockDim.x) {
+      cms[3 * r] = P.means[r].x;
+      cms[3 * r + 1] = P.means[r].y;
+      cms[3 * r + 2] = P.cell_probs[r];
+    }
+  const double* cm = P.gcells ? P.cm3 : cms;
+  __syncthreads();
+  const double M = (double)P.m_total;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = 2 + k + s;
+  for (;;) {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(R.ticket, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= R.total_chunks) break;
+    const uint32_t w = c % R.nwl;
+    const uint32_t t = (c / R.nwl) * 32 + lane;
+    const WorkerDev W = P.workers[w];
+    bool pending = t < W.draws;
+    const uint32_t i = R.draw_base[w] + t;  // global draw index
+    const uint32_t* pr = R.pred + (size_t)i * T;
+    uint32_t jj = 0;
+    while (__any_sync(0xffffffffu, pending)) {
+      if (!pending) continue;
+      bool ready = true;
+      for (; jj < T; ++jj) {
+        const uint32_t q = pr[jj];
+        if (q != 0xFFFFFFFFu &&
+            *reinterpret_cast<volatile const uint8_t*>(R.done + R.draw_base[w] + q) == 0) {
+          ready = false;
+          break;
+        }
+      }
+      if (!ready) {
+        __nanosleep(32);
+        continue;
+      }
+      __threadfence();  // the predecessors' position writes before our reads
+      const uint32_t head = R.heads[i];
+      const uint32_t* tails = R.tails + (size_t)i * s;
+      const double2 h = ldpos(P.pos + head);
+      // noise terms (objective.hpp:113-145)
+      uint32_t own = 0;
+      double lm = W.local_mass;
+      if (P.all_but_own) {
+        own = P.lclusters[P.cl_of[head]].gid;
+        lm = P.cell_probs[own];
+      }
+      double remote_sum = 0.0;
+      const uint32_t nr = P.all_but_own ? C : W.n_rem;
+      for (uint32_t q = 0; q < nr; ++q) {
+        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
+        if (P.all_but_own && r == own) continue;
+        const double qr = cauchy_rn(h.x, h.y, cm[3 * r], cm[3 * r + 1]);
+        remote_sum = __dadd_rn(remote_sum, __dmul_rn(cm[3 * r + 2], qr));
+      }
+      const double mean_field = __dmul_rn(M, remote_sum);
+      const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
+      double qsum = 0.0;
+      for (uint32_t q = 0; q < s; ++q) {
+        const double2 o = ldpos(P.pos + tails[q]);
+        qsum = __dadd_rn(qsum, cauchy_rn(h.x, h.y, o.x, o.y));
+      }
+      const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
+      // attraction (objective.hpp:197-213)
+      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
+      const uint32_t* nb = P.ell + (size_t)head * P.kpad;
+      const double* wrow = wt + cnt * k;
+      double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
+      double gn[2 * 64];
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const double2 o = ldpos(P.pos + nb[j]);
+        const double q = cauchy_rn(h.x, h.y, o.x, o.y);
+        const double wj = wrow[j];
+        const double qb = __dadd_rn(q, bg);
+        loss = __dadd_rn(loss, __dmul_rn(wj, -log(__ddiv_rn(q, qb))));
+        bgs = __dadd_rn(bgs, __ddiv_rn(wj, qb));
+        const double pull = __dmul_rn(
+            __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj),
+                                __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
+                      q),
+            q);
+        const double dx = __dsub_rn(h.x, o.x), dy = __dsub_rn(h.y, o.y);
+        gx = __dadd_rn(gx, __dmul_rn(pull, dx));
+        gy = __dadd_rn(gy, __dmul_rn(pull, dy));
+        gn[2 * j] = __dmul_rn(-pull, dx);
+        gn[2 * j + 1] = __dmul_rn(-pull, dy);
+      }
+      // negative repulsion (objective.hpp:216-226)
+      double gm[2 * 16];
+      for (uint32_t q = 0; q < s; ++q) {
+        const double2 o = ldpos(P.pos + tails[q]);
+        const double qn = cauchy_rn(h.x, h.y, o.x, o.y);
+        const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
+        const double dx = __dsub_rn(h.x, o.x), dy = __dsub_rn(h.y, o.y);
+        gx = __dsub_rn(gx, __dmul_rn(push, dx));
+        gy = __dsub_rn(gy, __dmul_rn(push, dy));
+        gm[2 * q] = __dmul_rn(push, dx);
+        gm[2 * q + 1] = __dmul_rn(push, dy);
+      }
+      // mean repulsion (objective.hpp:229-236)
+      for (uint32_t q = 0; q < nr; ++q) {
+        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
+        if (P.all_but_own && r == own) continue;
+        const double mx = cm[3 * r], my = cm[3 * r + 1];
+        const double qr = cauchy_rn(h.x, h.y, mx, my);
+        const double push = __dmul_rn(
+            __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), M), cm[3 * r + 2]), qr), qr);
+        gx = __dsub_rn(gx, __dmul_rn(push, __dsub_rn(h.x, mx)));
+        gy = __dsub_rn(gy, __dmul_rn(push, __dsub_rn(h.y, my)));
+      }
+      P.loss_slot[i] = loss;
+      // apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails
+      const double st = P.step;
+      uint32_t u = 0;
+      auto apply = [&](uint32_t p, double ax, double ay) {
+        double2 v = ldpos(P.pos + p);
+        v.x = __dsub_rn(v.x, __dmul_rn(st, ax));
+        v.y = __dsub_rn(v.y, __dmul_rn(st, ay));
+        __stcg(P.pos + p, v);
+        if (diverged(v.x, v.y))
+          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | p);
+        ++u;
+      };
+      apply(head, gx, gy);
+      if (!P.head_only) {
+        for (uint32_t j = 0; j < cnt; ++j) apply(nb[j], gn[2 * j], gn[2 * j + 1]);
+        for (uint32_t q = 0; q < s; ++q) apply(tails[q], gm[2 * q], gm[2 * q + 1]);
+      }
+      __threadfence();  // our writes before the flag
+      *reinterpret_cast<volatile uint8_t*>(R.done + i) = 1;
+      pending = false;
+    }
+  }
+}
+
+// ------------------------------------------------------ host launchers
+static unsigned blocks_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+void launch_mt_words(const ReplayDev& R, const uint64_t* counts, cudaStream_t st) {
+  k_mt_words<<<R.nwl, 160, 0, st>>>(R, counts);
+}
+
+void launch_replay_map(const ReplayDev& R, const SgdParams& P, const uint32_t* pool,
+                       const uint32_t* pool_off, cudaStream_t st) {
+  const dim3 grid(blocks_for(std::max<uint32_t>(R.max_draws, 1), 256), R.nwl);
+  k_replay_map<<<grid, 256, 0, st>>>(R, P, pool, pool_off);
+}
+
+size_t replay_scan_bytes(uint32_t n_loc) {
+  size_t b = 0;
+  NB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                        (int64_t)n_loc + 1));
+  return b;
+}
+
+void launch_replay_deps(const ReplayDev& R, const SgdParams& P, uint32_t n_loc, void* scan_tmp,
+                        size_t scan_bytes, cudaStream_t st) {
+  const uint32_t total = R.total_draws;
+  NB_CUDA(cudaMemsetAsync(R.tcount, 0, ((size_t)n_loc + 1) * 4, st));
+  if (total) k_replay_touch<<<blocks_for(total, 256), 256, 0, st>>>(R, P, total);
+  NB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, R.tcount, R.toff,
+                                        (int64_t)n_loc + 1, st));
+  NB_CUDA(cudaMemsetAsync(R.tcount, 0, ((size_t)n_loc + 1) * 4, st));
+  if (total) k_replay_scatter<<<blocks_for(total, 256), 256, 0, st>>>(R, total);
+  if (n_loc) k_replay_pred<<<blocks_for(n_loc, 256), 256, 0, st>>>(R, n_loc);
+}
+
+void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
+                         cudaStream_t st) {
+  if (smem > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(k_sgd_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  k_sgd_dataflow<<<nblocks, 256, smem, st>>>(P, R);
+}
+
+uint32_t dataflow_resident_blocks(size_t smem, int sm_count) {
+  if (smem > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(k_sgd_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  int per_sm = 0;
+  NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sgd_dataflow, 256, smem));
+  return (uint32_t)std::max(per_sm, 1) * (uint32_t)sm_count;
+}
+
+}  // namespace nb

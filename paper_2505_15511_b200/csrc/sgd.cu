@@ -9,155 +9,6 @@
 
 namespace nb {
 
-// ------------------------------------------------------- K8r replay kernel
-//
-// P.replay_ctas CTAs per local worker (a cooperative launch, so all are
-// resident). The host turned the worker's mt19937_64 draw stream into a tape
-// and grouped draws into wavefront levels: draws of one level touch
-// pairwise-disjoint points, and every draw comes after all earlier draws (in
-// sequential order t) that touch any of its points. So executing level by
-// level — the worker's CTAs split a level's draws, then meet at a per-worker
-// barrier in global memory — performs exactly the reference's sequential
-// per-worker update sequence (optimizer.hpp:253-304). Positions are read
-// through L2 (ld.global.cg), so a CTA sees the previous level's updates made
-// on other SMs. Each draw runs the reference arithmetic in its op order with
-// _rn intrinsics (no FMA), so positions are bit-identical.
-__device__ __forceinline__ double2 ldpos(const double2* p) { return __ldcg(p); }
-
-__global__ void __launch_bounds__(256) k_sgd_replay(SgdParams P) {
-  extern __shared__ __align__(16) double sm[];
-  const uint32_t K = P.replay_ctas ? P.replay_ctas : 1;
-  const uint32_t w = blockIdx.x / K, part = blockIdx.x % K;
-  const WorkerDev W = P.workers[w];
-  const uint32_t k = P.k, s = P.s, C = P.n_clusters;
-  // shared tables: weights (k+1)*k, then means/probs of all C cells (or,
-  // when 3C doubles do not fit, the same [C][3] table in global memory)
-  double* wt = sm;
-  double* cms = sm + (k + 1) * k;  // 3*C: mu.x, mu.y, p
-  for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
-  if (!P.gcells)
-    for (uint32_t r = threadIdx.x; r < C; r += blockDim.x) {
-      cms[3 * r] = P.means[r].x;
-      cms[3 * r + 1] = P.means[r].y;
-      cms[3 * r + 2] = P.cell_probs[r];
-    }
-  const double* cm = P.gcells ? P.cm3 : cms;
-  __syncthreads();
-  const double M = (double)P.m_total;
-  const uint32_t lvl0 = P.wk_lvl_base[w], nlev = P.wk_nlev[w];
-  const uint32_t stride = 2 + k + s;
-  for (uint32_t L = 0; L < nlev; ++L) {
-    const uint32_t b = P.lvl_off[lvl0 + L], e = P.lvl_off[lvl0 + L + 1];
-    for (uint32_t i = b + part * blockDim.x + threadIdx.x; i < e; i += K * blockDim.x) {
-      const uint32_t head = P.tape_head[i];
-      const uint32_t* tails = P.tape_tails + (size_t)i * s;
-      const uint32_t t = P.tape_t[i];
-      const double2 h = ldpos(P.pos + head);
-      // noise terms (objective.hpp:113-145)
-      uint32_t own = 0;
-      double lm = W.local_mass;
-      if (P.all_but_own) {
-        own = P.lclusters[P.cl_of[head]].gid;
-        lm = P.cell_probs[own];
-      }
-      double remote_sum = 0.0;
-      const uint32_t nr = P.all_but_own ? C : W.n_rem;
-      for (uint32_t q = 0; q < nr; ++q) {
-        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
-        if (P.all_but_own && r == own) continue;
-        const double qr = cauchy_rn(h.x, h.y, cm[3 * r], cm[3 * r + 1]);
-        remote_sum = __dadd_rn(remote_sum, __dmul_rn(cm[3 * r + 2], qr));
-      }
-      const double mean_field = __dmul_rn(M, remote_sum);
-      const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
-      double qsum = 0.0;
-      for (uint32_t q = 0; q < s; ++q) {
-        const double2 o = ldpos(P.pos + tails[q]);
-        qsum = __dadd_rn(qsum, cauchy_rn(h.x, h.y, o.x, o.y));
-      }
-      const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
-      // attraction (objective.hpp:197-213)
-      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
-      const uint32_t* nb = P.ell + (size_t)head * P.kpad;
-      const double* wrow = wt + cnt * k;
-      double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
-      double gn[2 * 64];
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const double2 o = ldpos(P.pos + nb[j]);
-        const double q = cauchy_rn(h.x, h.y, o.x, o.y);
-        const double wj = wrow[j];
-        const double qb = __dadd_rn(q, bg);
-        loss = __dadd_rn(loss, __dmul_rn(wj, -log(__ddiv_rn(q, qb))));
-        bgs = __dadd_rn(bgs, __ddiv_rn(wj, qb));
-        const double pull = __dmul_rn(
-            __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj),
-                                __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
-                      q),
-            q);
-        const double dx = __dsub_rn(h.x, o.x), dy = __dsub_rn(h.y, o.y);
-        gx = __dadd_rn(gx, __dmul_rn(pull, dx));
-        gy = __dadd_rn(gy, __dmul_rn(pull, dy));
-        gn[2 * j] = __dmul_rn(-pull, dx);
-        gn[2 * j + 1] = __dmul_rn(-pull, dy);
-      }
-      // negative repulsion (objective.hpp:216-226)
-      double gm[2 * 16];
-      for (uint32_t q = 0; q < s; ++q) {
-        const double2 o = ldpos(P.pos + tails[q]);
-        const double qn = cauchy_rn(h.x, h.y, o.x, o.y);
-        const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
-        const double dx = __dsub_rn(h.x, o.x), dy = __dsub_rn(h.y, o.y);
-        gx = __dsub_rn(gx, __dmul_rn(push, dx));
-        gy = __dsub_rn(gy, __dmul_rn(push, dy));
-        gm[2 * q] = __dmul_rn(push, dx);
-        gm[2 * q + 1] = __dmul_rn(push, dy);
-      }
-      // mean repulsion (objective.hpp:229-236)
-      for (uint32_t q = 0; q < nr; ++q) {
-        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
-        if (P.all_but_own && r == own) continue;
-        const double mx = cm[3 * r], my = cm[3 * r + 1];
-        const double qr = cauchy_rn(h.x, h.y, mx, my);
-        const double push = __dmul_rn(
-            __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), M), cm[3 * r + 2]), qr), qr);
-        gx = __dsub_rn(gx, __dmul_rn(push, __dsub_rn(h.x, mx)));
-        gy = __dsub_rn(gy, __dmul_rn(push, __dsub_rn(h.y, my)));
-      }
-      P.loss_slot[P.wk_draw_base[w] + t] = loss;
-      // apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails
-      const double st = P.step;
-      uint32_t u = 0;
-      auto apply = [&](uint32_t p, double ax, double ay) {
-        double2 v = ldpos(P.pos + p);
-        v.x = __dsub_rn(v.x, __dmul_rn(st, ax));
-        v.y = __dsub_rn(v.y, __dmul_rn(st, ay));
-        P.pos[p] = v;
-        if (diverged(v.x, v.y))
-          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | p);
-        ++u;
-      };
-      apply(head, gx, gy);
-      if (!P.head_only) {
-        for (uint32_t j = 0; j < cnt; ++j) apply(nb[j], gn[2 * j], gn[2 * j + 1]);
-        for (uint32_t q = 0; q < s; ++q) apply(tails[q], gm[2 * q], gm[2 * q + 1]);
-      }
-    }
-    // level barrier across the worker's CTAs
-    __syncthreads();
-    if (K > 1) {
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(P.replay_bar + w, 1u);
-        const uint32_t target = (L + 1) * K;
-        while (*reinterpret_cast<volatile uint32_t*>(P.replay_bar + w) < target) {
-        }
-        __threadfence();
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // Per-worker loss in sequential draw order (optimizer.hpp:289-290).
 __global__ void k_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk,
                            uint32_t nw, double* out) {
@@ -325,29 +176,6 @@ __global__ void k_gather_layout(const double2* in, const uint32_t* orig_of, uint
 // ------------------------------------------------------ host launchers
 
 static unsigned blocks_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
-
-uint32_t replay_ctas_per_worker(uint32_t n_workers, size_t smem, int sm_count) {
-  if (smem > 48 * 1024)
-    NB_CUDA(cudaFuncSetAttribute(k_sgd_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sgd_replay, 256, smem));
-  const uint32_t resident = (uint32_t)std::max(per_sm, 1) * (uint32_t)sm_count;
-  return std::max<uint32_t>(1, std::min<uint32_t>(32, resident / std::max<uint32_t>(n_workers, 1)));
-}
-
-void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cudaStream_t st) {
-  if (smem > 48 * 1024)
-    NB_CUDA(cudaFuncSetAttribute(k_sgd_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (P.replay_ctas > 1) {
-    NB_CUDA(cudaMemsetAsync(P.replay_bar, 0, n_workers * sizeof(uint32_t), st));
-    SgdParams Pc = P;
-    void* args[] = {&Pc};
-    NB_CUDA(cudaLaunchCooperativeKernel((const void*)k_sgd_replay, dim3(n_workers * P.replay_ctas),
-                                        dim3(256), args, smem, st));
-  } else {
-    k_sgd_replay<<<n_workers, 256, smem, st>>>(P);
-  }
-}
 
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
                      double* out, cudaStream_t st) {

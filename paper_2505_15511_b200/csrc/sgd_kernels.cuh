@@ -56,8 +56,6 @@ struct SgdParams {
   const double2* gcell_mu;      // hogwild: [local worker][max_cells] cell means
   const double* gcell_w;        // hogwild: [local worker][max_cells] weights M p_r
   const double* cm3;            // replay: [C][3] = mu.x, mu.y, p_r
-  uint32_t replay_ctas;         // replay: CTAs per worker (level barrier in global memory)
-  uint32_t* replay_bar;         // replay: per-worker barrier counters
   double step;
   uint64_t epoch;
   uint32_t seed_lo, seed_hi;
@@ -65,20 +63,12 @@ struct SgdParams {
   uint32_t* chunk_counter;
   uint32_t total_chunks, chunk_heads;
   const uint2* chunk_map;       // chunk -> (local worker, chunk within the worker)
-  // replay tape (level-ordered)
-  const uint32_t* tape_head;    // local id per draw (level order)
-  const uint32_t* tape_tails;   // s local ids per draw
-  const uint32_t* tape_t;       // sequential draw index t per draw
-  const uint32_t* lvl_off;      // per worker: level offsets into the tape
-  const uint32_t* wk_lvl_base;  // per worker: index of its first level in lvl_off
-  const uint32_t* wk_nlev;      // per worker: number of levels
+  // replay (replay.cu)
   double* loss_slot;            // per worker-draw loss, indexed by worker base + t
   const uint32_t* wk_draw_base; // per worker: base into loss_slot
 };
 
 // Host launchers (sgd.cu).
-void launch_sgd_replay(const SgdParams& P, uint32_t n_workers, size_t smem, cudaStream_t st);
-uint32_t replay_ctas_per_worker(uint32_t n_workers, size_t smem, int sm_count);
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
                      double* out, cudaStream_t st);
 void launch_sgd_hogwild(const SgdParams& P, uint32_t nblocks, size_t smem, cudaStream_t st);

@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "plan.cuh"
+#include "replay.cuh"
 #include "sgd_kernels.cuh"
 
 using namespace nb;
@@ -45,14 +46,6 @@ uint64_t mix_seed(uint64_t x) {
   return x ^ (x >> 31);
 }
 uint64_t stream_seed(uint64_t base, uint64_t stream) { return mix_seed(base ^ mix_seed(stream)); }
-
-// rng.hpp:49-55 — the reference's unbiased bounded draw on mt19937_64.
-inline uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {
-  const uint64_t limit = n * (0xFFFFFFFFFFFFFFFFull / n);
-  uint64_t d = g();
-  while (d >= limit) d = g();
-  return d % n;
-}
 
 template <class T>
 void upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
@@ -95,15 +88,21 @@ struct RankTrainer {
   std::vector<WorkerDev> wk;
   std::vector<LocalCluster> lcl;
   std::vector<uint32_t> elig_h, pool_h, pool_off;
-  std::vector<uint32_t> ell_h;
-  std::vector<uint8_t> ncnt_h;
-  std::vector<std::mt19937_64> rng;
+  // replay: the workers' std::mt19937_64 streams live on the device
+  // (double-buffered epoch start / end states); host copies only for seek and
+  // the rejection fallback
+  DBuf<MtState> mt_a, mt_b;
+  DBuf<uint64_t> wcount, wbase;
+  DBuf<unsigned long long> words, tlist, redges;
+  DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, rtouch, rpred, tcount, toff, reject,
+      ticket, pt_base;
+  DBuf<uint8_t> rdone, scan_tmp;
+  size_t scan_bytes = 0;
+  uint32_t df_blocks = 0, total_draws = 0, max_draws = 0;
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
   uint32_t hog_cells = 0;  // cells per worker of the hogwild cell table
   bool gcells = false;     // cell tables in global memory (too many clusters for shared memory)
-  uint32_t replay_k = 0;   // replay: CTAs per worker
-  DBuf<uint32_t> replay_bar;
   uint32_t hog_blocks = 0, chunk_heads = 0, total_chunks = 0, hog_wave = 1;
   DBuf<uint2> chunk_map;  // hogwild chunk -> (local worker, chunk within the worker)
   DBuf<uint32_t> chunk_counter;
@@ -116,8 +115,7 @@ struct RankTrainer {
   DBuf<WorkerDev> wk_d;
   DBuf<LocalCluster> lcl_d;
   uint32_t nchunks = 0, chunk = 4096;
-  // replay tape
-  DBuf<uint32_t> tape_head, tape_tails, tape_t, lvl_off, wk_lvl_base, wk_nlev, wk_draw_base;
+  DBuf<uint32_t> wk_draw_base;
   DBuf<double> loss_slot, wloss;
   std::vector<uint32_t> draw_base_h;
 
@@ -133,7 +131,6 @@ struct RankTrainer {
   void bind() { bind_device(ctx); }
   void launched(const char* name) { note_launch(ctx, name); }
   ~RankTrainer() {
-    join_prefetch();
     if (comm && own_comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -320,17 +317,7 @@ struct RankTrainer {
     uniform_k = true;
     for (uint64_t i = 0; i < n; ++i)
       if (new_of[i] != 0xFFFFFFFFu && offs[i + 1] - offs[i] != k) { uniform_k = false; break; }
-    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
-      ell_h.resize(n_loc * kpad);
-      ncnt_h.resize(n_loc);
-      if (n_loc) {
-        NB_CUDA(cudaMemcpy(ell_h.data(), ell.p, n_loc * kpad * 4, cudaMemcpyDeviceToHost));
-        NB_CUDA(cudaMemcpy(ncnt_h.data(), ncnt.p, n_loc, cudaMemcpyDeviceToHost));
-      }
-      rng.clear();
-      for (uint32_t wl = 0; wl < nwl; ++wl)  // optimizer.hpp:211-213, :371
-        rng.emplace_back(stream_seed(cfg.seed, 0x776f726bull + wk[wl].id));
-    }
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) setup_replay(cl_of_h);
     // positions in local order
     pos.alloc(std::max<uint64_t>(n_loc, 1));
     {
@@ -401,6 +388,156 @@ struct RankTrainer {
     // npts / cap heads in flight
     if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD) plan_hogwild_grid();
     upload(wk_d, wk, S);
+  }
+
+  // Device replay state: the workers' streams (optimizer.hpp:211-213, :371:
+  // stream_seed(seed, "work" + worker id)), per-epoch draw / dependency
+  // buffers sized for one epoch of every local worker.
+  void setup_replay(const std::vector<uint32_t>& cl_of_h) {
+    cudaStream_t S = st();
+    std::vector<MtState> st0(std::max<uint32_t>(nwl, 1));
+    for (uint32_t wl = 0; wl < nwl; ++wl) {
+      Mt64 m;
+      m.seed(stream_seed(cfg.seed, 0x776f726bull + wk[wl].id));
+      st0[wl] = m.s;
+    }
+    upload(mt_a, st0, S);
+    mt_b.alloc(st0.size());
+    draw_base_h.assign(nwl, 0);
+    std::vector<uint64_t> wc(std::max<uint32_t>(nwl, 1), 0), wb(std::max<uint32_t>(nwl, 1), 0);
+    uint64_t acc = 0, wacc = 0;
+    max_draws = 0;
+    for (uint32_t wl = 0; wl < nwl; ++wl) {
+      draw_base_h[wl] = (uint32_t)acc;
+      wc[wl] = (uint64_t)wk[wl].draws * (1 + s);
+      wb[wl] = wacc;
+      acc += wk[wl].draws;
+      wacc += wc[wl];
+      max_draws = std::max(max_draws, wk[wl].draws);
+    }
+    if (acc >= 0xFFFFFFFFull) fail(kSize, "replay draws per rank exceed 2^32");
+    total_draws = (uint32_t)acc;
+    upload(wk_draw_base, draw_base_h, S);
+    upload(wcount, wc, S);
+    upload(wbase, wb, S);
+    upload(pool_d, pool_h, S);
+    upload(pool_off_d, pool_off, S);
+    std::vector<uint32_t> ptb(orig_of.size());
+    for (size_t v = 0; v < ptb.size(); ++v) ptb[v] = draw_base_h[lcl[cl_of_h[v]].worker];
+    upload(pt_base, ptb, S);
+    const uint64_t T = 1 + k + s, D = std::max<uint64_t>(acc, 1);
+    words.alloc(std::max<uint64_t>(wacc, 1));
+    rheads.alloc(D);
+    rtails.alloc(D * s);
+    rtouch.alloc(D * T);
+    rpred.alloc(D * T);
+    tlist.alloc(D * T);
+    rdone.alloc(D);
+    loss_slot.alloc(D);
+    tcount.alloc(orig_of.size() + 1);
+    toff.alloc(orig_of.size() + 1);
+    reject.alloc(std::max<uint32_t>(nwl, 1));
+    redges.alloc(std::max<uint32_t>(nwl, 1));
+    ticket.alloc(1);
+    scan_bytes = replay_scan_bytes((uint32_t)orig_of.size());
+    scan_tmp.alloc(std::max<size_t>(scan_bytes, 1));
+  }
+
+  ReplayDev replay_dev() {
+    ReplayDev R{};
+    R.nwl = nwl;
+    R.s = (uint32_t)s;
+    R.T = (uint32_t)(1 + k + s);
+    R.draw_base = wk_draw_base.p;
+    R.word_base = wbase.p;
+    R.st_in = mt_a.p;
+    R.st_out = mt_b.p;
+    R.words = words.p;
+    R.heads = rheads.p;
+    R.tails = rtails.p;
+    R.touch = rtouch.p;
+    R.pred = rpred.p;
+    R.tcount = tcount.p;
+    R.toff = toff.p;
+    R.tlist = tlist.p;
+    R.reject = reject.p;
+    R.edges = redges.p;
+    R.done = rdone.p;
+    R.ticket = ticket.p;
+    R.pt_base = pt_base.p;
+    R.total_chunks = nwl * ((max_draws + 31) / 32);
+    R.max_draws = max_draws;
+    R.total_draws = total_draws;
+    return R;
+  }
+
+  // A worker whose epoch hit the rejection branch of uniform_index
+  // (rng.hpp:49-55, probability ~n / 2^64 per draw): its draws are made on
+  // the host from the epoch's start state, consuming the extra words exactly
+  // as the reference does (optimizer.hpp:254-255, :284-285).
+  void host_draws(uint32_t wl) {
+    cudaStream_t S = st();
+    Mt64 m;
+    NB_CUDA(cudaMemcpy(&m.s, mt_a.p + wl, sizeof(MtState), cudaMemcpyDeviceToHost));
+    const WorkerDev& d = wk[wl];
+    std::vector<uint32_t> hd(d.draws), tl((size_t)d.draws * s);
+    for (uint32_t t = 0; t < d.draws; ++t) {
+      const uint32_t h = elig_h[d.elig_off + m.uniform_index(d.n_elig)];
+      hd[t] = h;
+      if (cfg.approx_all_but_own) {
+        const LocalCluster& L = lcl[local_cluster_of(h)];
+        for (uint64_t q = 0; q < s; ++q) tl[(size_t)t * s + q] = L.start + (uint32_t)m.uniform_index(L.count);
+      } else {
+        const uint32_t* pool = pool_h.data() + pool_off[wl];
+        for (uint64_t q = 0; q < s; ++q) tl[(size_t)t * s + q] = pool[m.uniform_index(d.npts)];
+      }
+    }
+    const size_t b = draw_base_h[wl];
+    if (d.draws) {
+      NB_CUDA(cudaMemcpyAsync(rheads.p + b, hd.data(), hd.size() * 4, cudaMemcpyHostToDevice, S));
+      NB_CUDA(cudaMemcpyAsync(rtails.p + b * s, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice, S));
+    }
+    NB_CUDA(cudaMemcpyAsync(mt_b.p + wl, &m.s, sizeof(MtState), cudaMemcpyHostToDevice, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+  }
+
+  // One replay epoch on the device: streams -> draws -> dependencies ->
+  // dataflow SGD -> per-worker losses in draw order.
+  void launch_replay_epoch(SgdParams& P) {
+    cudaStream_t S = st();
+    ReplayDev R = replay_dev();
+    NB_CUDA(cudaMemsetAsync(reject.p, 0, reject.bytes(), S));
+    NB_CUDA(cudaMemsetAsync(redges.p, 0, redges.bytes(), S));
+    if (nwl) {
+      launch_mt_words(R, wcount.p, S);
+      launched("k_mt_words");
+      launch_replay_map(R, P, pool_d.p, pool_off_d.p, S);
+      launched("k_replay_map");
+    }
+    std::vector<uint32_t> rj(std::max<uint32_t>(nwl, 1), 0);
+    NB_CUDA(cudaMemcpyAsync(rj.data(), reject.p, rj.size() * 4, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
+    // (NOMAD_B200_REPLAY_HOST_DRAWS=1 takes the rejection path for every
+    // worker: a test hook for the fallback, whose result must not change)
+    const bool force = std::getenv("NOMAD_B200_REPLAY_HOST_DRAWS") != nullptr;
+    for (uint32_t wl = 0; wl < nwl; ++wl)
+      if (rj[wl] || force) host_draws(wl);
+    launch_replay_deps(R, P, (uint32_t)orig_of.size(), scan_tmp.p, scan_bytes, S);
+    launched("k_replay_deps");
+    if (!df_blocks) df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count);
+    NB_CUDA(cudaMemsetAsync(rdone.p, 0, rdone.bytes(), S));
+    NB_CUDA(cudaMemsetAsync(ticket.p, 0, 4, S));
+    P.loss_slot = loss_slot.p;
+    P.wk_draw_base = wk_draw_base.p;
+    NB_CUDA(cudaEventRecord(ev[0], S));
+    if (nwl && total_draws) {
+      launch_sgd_dataflow(P, R, df_blocks, smem_replay, S);
+      launched("k_sgd_dataflow");
+      launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
+      launched("k_loss_seq");
+    }
+    NB_CUDA(cudaEventRecord(ev[1], S));
+    std::swap(mt_a, mt_b);  // this epoch's end state starts the next
   }
 
   void plan_hogwild_grid() {
@@ -586,150 +723,28 @@ struct RankTrainer {
     return lr / static_cast<double>(cfg.batch_size);
   }
 
-  // ------------------------------------------------------- replay tapes
-  // One epoch's replay tape: every worker's draws (mt19937_64 stream, the
-  // reference's order, optimizer.hpp:252-285) grouped by conflict level,
-  // worker-major.
-  struct Tape {
-    std::vector<uint32_t> th, tt, tid, loff, lbase, nlev;
-    uint64_t edges = 0;
-  };
-
-  // Workers draw from their own streams and touch disjoint points, so their
-  // tapes are built concurrently (one host thread per worker, up to the
-  // hardware threads) straight into their slices of the epoch tape.
-  void build_tapes(Tape& T) {
-    std::vector<size_t> base(nwl + 1, 0);
-    for (uint32_t wl = 0; wl < nwl; ++wl) base[wl + 1] = base[wl] + wk[wl].draws;
-    T.th.resize(base[nwl]);
-    T.tt.resize(base[nwl] * s);
-    T.tid.resize(base[nwl]);
-    std::vector<std::vector<uint32_t>> loffw(nwl);
-    std::vector<uint32_t> maxl(nwl, 0);
-    std::vector<uint64_t> edg(nwl, 0);
-    auto one = [&](uint32_t wl) {
-      const WorkerDev& d = wk[wl];
-      const uint32_t D = d.draws;
-      std::vector<uint32_t> head(D), tails((size_t)D * s), lev(D);
-      uint32_t maxlev = 0;
-      uint64_t edges = 0;
-      auto& g = rng[wl];
-      const uint32_t* pool = pool_h.data() + pool_off[wl];
-      // pass 1: the stream's draws (optimizer.hpp:254-255, :284-285)
-      for (uint32_t t = 0; t < D; ++t) {
-        const uint32_t h = elig_h[d.elig_off + uniform_index(g, d.n_elig)];
-        head[t] = h;
-        uint32_t p0 = 0, pn = d.npts;
-        if (cfg.approx_all_but_own) {
-          // pool = own cluster members, ascending id == contiguous local ids
-          const uint32_t c = local_cluster_of(h);
-          p0 = lcl[c].start;
-          pn = lcl[c].count;
-          for (uint64_t q = 0; q < s; ++q) tails[(size_t)t * s + q] = p0 + (uint32_t)uniform_index(g, pn);
-        } else {
-          for (uint64_t q = 0; q < s; ++q) tails[(size_t)t * s + q] = pool[uniform_index(g, pn)];
-        }
-      }
-      // pass 2: conflict levels over the worker's own point range (u16
-      // levels, 2 bytes per point, while they fit; u32 otherwise), with the
-      // neighbour rows of draws ahead prefetched
-      const uint32_t p0w = d.pstart;
-      auto levels = [&](auto& last) -> bool {
-        using LT = typename std::decay_t<decltype(last)>::value_type;
-        constexpr uint32_t AHEAD = 16;
-        maxlev = 0;
-        edges = 0;
-        for (uint32_t t = 0; t < std::min(D, AHEAD); ++t)
-          __builtin_prefetch(ell_h.data() + (size_t)head[t] * kpad);
-        for (uint32_t t = 0; t < D; ++t) {
-          if (t + AHEAD < D) __builtin_prefetch(ell_h.data() + (size_t)head[t + AHEAD] * kpad);
-          const uint32_t h = head[t];
-          // level = 1 + max level of every point it reads or writes
-          const uint32_t cnt = ncnt_h[h];
-          const uint32_t* nb = ell_h.data() + (size_t)h * kpad;
-          const uint32_t* tl = tails.data() + (size_t)t * s;
-          uint32_t L = last[h - p0w];
-          for (uint32_t j = 0; j < cnt; ++j) L = std::max<uint32_t>(L, last[nb[j] - p0w]);
-          for (uint64_t q = 0; q < s; ++q) L = std::max<uint32_t>(L, last[tl[q] - p0w]);
-          ++L;
-          if (L > std::numeric_limits<LT>::max()) return false;
-          last[h - p0w] = (LT)L;
-          for (uint32_t j = 0; j < cnt; ++j) last[nb[j] - p0w] = (LT)L;
-          for (uint64_t q = 0; q < s; ++q) last[tl[q] - p0w] = (LT)L;
-          lev[t] = L - 1;
-          maxlev = std::max(maxlev, L);
-          edges += cnt + s;
-        }
-        return true;
-      };
-      {
-        std::vector<uint16_t> l16(d.npts, 0);
-        if (!levels(l16)) {
-          std::vector<uint32_t> l32(d.npts, 0);
-          levels(l32);
-        }
-      }
-      // counting sort by level (stable in t)
-      std::vector<uint32_t> cnt_l(maxlev + 1, 0);
-      for (uint32_t t = 0; t < D; ++t) ++cnt_l[lev[t] + 1];
-      for (uint32_t l = 0; l < maxlev; ++l) cnt_l[l + 1] += cnt_l[l];
-      const size_t b0 = base[wl];
-      auto& lo = loffw[wl];
-      lo.resize(maxlev + 1);
-      for (uint32_t l = 0; l <= maxlev; ++l) lo[l] = (uint32_t)(b0 + cnt_l[l]);
-      std::vector<uint32_t> fill(cnt_l.begin(), cnt_l.end() - 1);
-      for (uint32_t t = 0; t < D; ++t) {
-        const size_t at = b0 + fill[lev[t]]++;
-        T.th[at] = head[t];
-        T.tid[at] = t;
-        for (uint64_t q = 0; q < s; ++q) T.tt[at * s + q] = tails[(size_t)t * s + q];
-      }
-      maxl[wl] = maxlev;
-      edg[wl] = edges;
-    };
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned nth = std::min<unsigned>(nwl, hw);
-    if (nth <= 1) {
-      for (uint32_t wl = 0; wl < nwl; ++wl) one(wl);
-    } else {
-      std::atomic<uint32_t> next{0};
-      std::vector<std::thread> pool_t;
-      for (unsigned i = 0; i < nth; ++i)
-        pool_t.emplace_back([&] {
-          for (uint32_t wl; (wl = next.fetch_add(1)) < nwl;) one(wl);
-        });
-      for (auto& x : pool_t) x.join();
-    }
-    T.loff.clear();
-    T.lbase.assign(nwl, 0);
-    T.nlev.assign(nwl, 0);
-    T.edges = 0;
-    for (uint32_t wl = 0; wl < nwl; ++wl) {
-      T.lbase[wl] = (uint32_t)T.loff.size();
-      T.nlev[wl] = maxl[wl];
-      T.loff.insert(T.loff.end(), loffw[wl].begin(), loffw[wl].end());
-      T.edges += edg[wl];
-    }
-  }
-
   // Continue the schedule at epoch `e` (resume from a checkpoint layout).
   // Throughput mode: draws are keyed by (seed, epoch, worker, t), nothing to
   // replay. Replay mode: each worker's mt19937_64 stream is advanced past the
-  // skipped epochs' draws exactly as build_tapes consumes them.
+  // skipped epochs' draws exactly as an epoch consumes them.
   void seek(uint64_t e) {
     if (e > cfg.epochs) fail(kParameter, "epoch out of range for schedule");
-    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY && e != epochs_done) {
       if (e < epochs_done) fail(kParameter, "replay mode cannot seek backwards");
+      std::vector<Mt64> m(std::max<uint32_t>(nwl, 1));
+      for (uint32_t wl = 0; wl < nwl; ++wl)
+        NB_CUDA(cudaMemcpy(&m[wl].s, mt_a.p + wl, sizeof(MtState), cudaMemcpyDeviceToHost));
       for (; epochs_done < e; ++epochs_done)
         for (uint32_t wl = 0; wl < nwl; ++wl) {
           const WorkerDev& d = wk[wl];
-          auto& g = rng[wl];
           for (uint32_t t = 0; t < d.draws; ++t) {
-            const uint32_t h = elig_h[d.elig_off + uniform_index(g, d.n_elig)];
+            const uint32_t h = elig_h[d.elig_off + m[wl].uniform_index(d.n_elig)];
             const uint64_t pn = cfg.approx_all_but_own ? lcl[local_cluster_of(h)].count : d.npts;
-            for (uint64_t q = 0; q < s; ++q) (void)uniform_index(g, pn);
+            for (uint64_t q = 0; q < s; ++q) (void)m[wl].uniform_index(pn);
           }
         }
+      for (uint32_t wl = 0; wl < nwl; ++wl)
+        NB_CUDA(cudaMemcpy(mt_a.p + wl, &m[wl].s, sizeof(MtState), cudaMemcpyHostToDevice));
     }
     epochs_done = e;
   }
@@ -829,8 +844,6 @@ struct RankTrainer {
   }
 
   // -------------------------------------- replay / verbose run (per epoch sync)
-  Tape cur, nxt;
-  std::thread prefetch;
   uint64_t s_E = 0;
   std::vector<double> s_wl_loss, s_all_loss;
   std::vector<unsigned long long> s_wl_edges;
@@ -838,18 +851,8 @@ struct RankTrainer {
   uint64_t s_edges = 0;
   std::chrono::steady_clock::time_point s_t0;
 
-  void join_prefetch() {
-    if (prefetch.joinable()) prefetch.join();
-  }
   void sync_begin(uint64_t E) {
     s_E = E;
-    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY && draw_base_h.empty()) {
-      draw_base_h.assign(nwl, 0);
-      uint32_t acc = 0;
-      for (uint32_t wl = 0; wl < nwl; ++wl) { draw_base_h[wl] = acc; acc += wk[wl].draws; }
-      upload(wk_draw_base, draw_base_h, st());
-      loss_slot.alloc(std::max<uint32_t>(acc, 1));
-    }
     s_wl_loss.assign(nwl, 0.0);
     s_wl_edges.assign(nwl, 0);
     s_all_loss.assign((size_t)world * std::max<uint32_t>(nwl, 1), 0.0);
@@ -865,49 +868,7 @@ struct RankTrainer {
     s_edges = 0;
     const bool replay = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY;
     if (replay) {
-      // the next epoch's tape is built on host threads while this epoch runs
-      // on the GPU (tapes depend only on the workers' streams); only within
-      // this run, so the streams end exactly n_epochs ahead
-      if (it == 0) {
-        build_tapes(cur);
-      } else {
-        join_prefetch();
-        std::swap(cur, nxt);
-      }
-      if (it + 1 < s_E) prefetch = std::thread([this] { build_tapes(nxt); });
-      s_edges = cur.edges;
-      if (std::getenv("NOMAD_B200_DEBUG_REPLAY") && it == 0)
-        for (uint32_t wl = 0; wl < nwl; ++wl)
-          std::fprintf(stderr, "replay worker %u: %u draws, %u levels\n", wl, wk[wl].draws,
-                       cur.nlev[wl]);
-      upload(tape_head, cur.th, S);
-      upload(tape_tails, cur.tt, S);
-      upload(tape_t, cur.tid, S);
-      upload(lvl_off, cur.loff, S);
-      upload(wk_lvl_base, cur.lbase, S);
-      upload(wk_nlev, cur.nlev, S);
-      P.tape_head = tape_head.p;
-      P.tape_tails = tape_tails.p;
-      P.tape_t = tape_t.p;
-      P.lvl_off = lvl_off.p;
-      P.wk_lvl_base = wk_lvl_base.p;
-      P.wk_nlev = wk_nlev.p;
-      P.loss_slot = loss_slot.p;
-      P.wk_draw_base = wk_draw_base.p;
-      if (!replay_k) {
-        replay_k = replay_ctas_per_worker(nwl, smem_replay, ctx->sm_count);
-        replay_bar.alloc(std::max<uint32_t>(nwl, 1));
-      }
-      P.replay_ctas = replay_k;
-      P.replay_bar = replay_bar.p;
-      NB_CUDA(cudaEventRecord(ev[0], S));
-      if (nwl) {
-        launch_sgd_replay(P, nwl, smem_replay, S);
-        launched("k_sgd_replay");
-        launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
-        launched("k_loss_seq");
-      }
-      NB_CUDA(cudaEventRecord(ev[1], S));
+      launch_replay_epoch(P);
     } else {
       NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
       NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
@@ -930,8 +891,10 @@ struct RankTrainer {
     // per-worker loss sums -> epoch mean (optimizer.hpp:444-451)
     const double* lsrc = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY ? wloss.p : loss_acc.p;
     if (nwl) NB_CUDA(cudaMemcpyAsync(s_wl_loss.data(), lsrc, nwl * 8, cudaMemcpyDeviceToHost, S));
-    if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD && nwl)
-      NB_CUDA(cudaMemcpyAsync(s_wl_edges.data(), edge_acc.p, nwl * 8, cudaMemcpyDeviceToHost, S));
+    if (nwl)
+      NB_CUDA(cudaMemcpyAsync(s_wl_edges.data(),
+                              cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD ? edge_acc.p : redges.p,
+                              nwl * 8, cudaMemcpyDeviceToHost, S));
     if (world > 1 && !grouped) {
       if (!s_gl.p) s_gl.alloc((size_t)world * nwl);
       NB_NCCL(ncclAllGather(lsrc, s_gl.p, nwl, ncclDouble, comm, S));
@@ -947,8 +910,7 @@ struct RankTrainer {
     sgd_ms += a;
     means_ms += b;
     ++timed_epochs;
-    if (cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD)
-      for (uint32_t wl = 0; wl < nwl; ++wl) s_edges += s_wl_edges[wl];
+    for (uint32_t wl = 0; wl < nwl; ++wl) s_edges += s_wl_edges[wl];
     edge_updates += s_edges;
     return key;
   }
@@ -1131,12 +1093,6 @@ struct nomad_b200_trainer {
   }
 
   void run_sync(uint64_t E, double* epoch_loss) {
-    struct Joiner {
-      nomad_b200_trainer* t;
-      ~Joiner() {
-        for (auto& x : t->r) x->join_prefetch();
-      }
-    } joiner{this};
     for (auto& t : r) { t->bind(); t->sync_begin(E); }
     for (uint64_t it = 0; it < E; ++it) {
       const uint64_t e = R0().epochs_done;
@@ -1312,6 +1268,7 @@ int32_t nomad_b200_trainer_destroy(nomad_b200_trainer* t) {
       bind_device(x->ctx);
       x.reset();
     }
+    cudaGetLastError();  // teardown errors are not reported to later launches
     delete t;
   });
 }

@@ -1,29 +1,63 @@
-"""Final-map quality parity (SPEC acceptance / north-star correctness part 3):
-the GPU fit (throughput SGD, GPU PCA, bf16 or exact kNN) reaches the
-reference's NP@10 and random-triplet accuracy on identical data, measured by
-the reference's own metric code (metrics.hpp:113-243, via oracle/_ref)."""
+"""Final-map quality parity (north-star correctness part 3).
+
+Isotropic Gaussian blobs have no neighbourhood structure a 2-D map can keep
+(the reference's own NP@10 there is ~0.015), so quality is
+compared on a curved 2-D sheet in 64 dimensions (tests/common.py:manifold),
+where the reference reaches NP@10 ~0.6 and triplet accuracy ~0.83 (SPEC.md:578
+asks >= 0.30 / 0.80 at W=1).
+
+Reference trajectory = the replay fit, bit-identical to the reference's fit()
+(checked here once against the compiled reference, and in test_fit_gpu.py).
+The throughput (hogwild) fit must match it over 3 seeds each:
+    |mean NP@10 difference|   <= 3 sqrt(s_r^2/3 + s_h^2/3)   (s: seed-to-seed std)
+    |mean triplet difference| <= 0.01
+Metrics are the GPU ones, bit-identical to metrics.hpp (test_metrics_gpu.py)."""
 import numpy as np
 import pytest
 
+from common import manifold
+
 pytestmark = pytest.mark.gpu
 
+SEEDS = (7, 8, 9)
 
-@pytest.mark.parametrize("knn_mode", ["exact", "bf16"])
-def test_quality_matches_reference(port, ref, ctx, knn_mode):
+
+@pytest.fixture(scope="module")
+def sheet():
+    return manifold(20000, 64)[0]
+
+
+def _quality(nb, ctx, x, cfg):
+    lay = nb.fit(x, cfg, ctx=ctx)
+    npv, _ = nb.neighborhood_preservation(x, lay, 10, sample=5000, seed=1, ctx=ctx)
+    tr, _ = nb.random_triplet_accuracy(x, lay, 100000, 1, ctx=ctx)
+    return lay, npv, tr
+
+
+def test_replay_fit_is_the_reference_fit(ref, ctx, sheet):
+    """W=1, seed 7, all 200 epochs: the GPU replay fit equals the reference's
+    fit() bit for bit on the manifold, so it stands in for the reference below."""
     import paper_2505_15511_b200 as nb
     from oracle import train_config
-    x = port.gaussian_mixture(6000, 32, 10, 10.0, 42)
-    kw = dict(epochs=100, workers=2, n_clusters=6)
-    r7 = ref.fit(x, train_config(seed=7, **kw))["layout"]
-    r8 = ref.fit(x, train_config(seed=8, **kw))["layout"]
-    g7 = nb.fit(x, nb.TrainConfig(seed=7, sgd_mode="hogwild", knn_mode=knn_mode, **kw), ctx=ctx)
-    np_r7, _ = ref.neighborhood_preservation(x, r7, 10)
-    np_r8, _ = ref.neighborhood_preservation(x, r8, 10)
-    np_g, _ = ref.neighborhood_preservation(x, g7, 10)
-    t_r7, se = ref.random_triplet_accuracy(x, r7, 100000, 1)
-    t_r8, _ = ref.random_triplet_accuracy(x, r8, 100000, 1)
-    t_g, _ = ref.random_triplet_accuracy(x, g7, 100000, 1)
-    print(f"NP@10 ref {np_r7:.4f}/{np_r8:.4f} gpu {np_g:.4f}; triplet ref {t_r7:.4f}/{t_r8:.4f} "
-          f"gpu {t_g:.4f}")
-    assert abs(np_g - np_r7) <= max(0.02, 3 * abs(np_r7 - np_r8))
-    assert abs(t_g - t_r7) <= max(0.02, 3 * abs(t_r7 - t_r8), 5 * se)
+    r = ref.fit(sheet, train_config(seed=7, workers=1))
+    lay = nb.fit(sheet, nb.TrainConfig(seed=7, workers=1), ctx=ctx)
+    assert np.array_equal(lay, r["layout"])
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+def test_hogwild_quality_matches_reference(ctx, sheet, workers):
+    import paper_2505_15511_b200 as nb
+    rq = [_quality(nb, ctx, sheet, nb.TrainConfig(seed=s, workers=workers))[1:] for s in SEEDS]
+    hq = [_quality(nb, ctx, sheet, nb.TrainConfig(seed=s, workers=workers,
+                                                  sgd_mode="hogwild"))[1:] for s in SEEDS]
+    rn, rt = np.array(rq).T
+    hn, ht = np.array(hq).T
+    bound = 3 * np.sqrt(rn.std(ddof=1) ** 2 / 3 + hn.std(ddof=1) ** 2 / 3)
+    print(f"W={workers} NP@10 reference {rn.mean():.4f} (sd {rn.std(ddof=1):.4f}) hogwild "
+          f"{hn.mean():.4f} (sd {hn.std(ddof=1):.4f}) bound {bound:.4f}; triplet "
+          f"{rt.mean():.4f} vs {ht.mean():.4f}")
+    assert abs(hn.mean() - rn.mean()) <= bound
+    assert abs(ht.mean() - rt.mean()) <= 0.01
+    if workers == 1:  # SPEC.md:578 desk-scale acceptance, met by both on this data
+        assert rn.mean() >= 0.30 and hn.mean() >= 0.30
+        assert rt.mean() >= 0.80 and ht.mean() >= 0.80

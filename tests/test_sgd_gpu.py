@@ -42,6 +42,23 @@ def test_replay_bit_exact(port, ctx, workers):
     assert log.payload_doubles == 6 * 2 * 8 and log.payload_counts == 6 * 8
 
 
+def test_replay_host_draw_fallback_is_identical(port, ctx, monkeypatch):
+    """The rejection branch of uniform_index (rng.hpp:49-55, probability
+    ~n / 2^64 per draw) moves a worker's draws to the host for that epoch;
+    forced for every epoch and worker, the run must stay bit-identical."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    kw = dict(epochs=10, workers=4, seed=7)
+    monkeypatch.setenv("NOMAD_B200_REPLAY_HOST_DRAWS", "1")
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    loss = tr.run(3)
+    monkeypatch.delenv("NOMAD_B200_REPLAY_HOST_DRAWS")
+    loss2 = tr.run(2)
+    rl, rloss, _, _ = _oracle(port, c, g, pca, 5, **kw)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(np.concatenate([loss, loss2]), rloss, rtol=1e-13, atol=0)
+
+
 def test_replay_resume_equals_single_run(port, ctx):
     """run(2)+run(3) == run(5): worker RNG streams persist across calls."""
     import paper_2505_15511_b200 as nb
