@@ -247,6 +247,8 @@ def main():
     ap.add_argument("--recall-sample", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-epochs", type=int, default=5)
+    ap.add_argument("--replay-epochs", type=int, default=3,
+                    help="deterministic-mode epochs timed after the throughput run (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
@@ -505,6 +507,43 @@ def main():
                                "bytes_per_head": BYTES_PER_HEAD_DF}}
         trdf.close()
 
+    # deterministic (replay) mode on the same index: the reference's own
+    # mt19937_64 draws and sequential per-worker update order, bit-identical
+    # layouts; streams, draws, dependency lists and the dataflow SGD all on
+    # the device. Reported next to the same-index CPU reference epoch.
+    replay = None
+    if args.sgd_mode == "hogwild" and args.replay_epochs > 0:
+        cfgr = nbx.TrainConfig(epochs=200, workers=W, seed=7, sgd_mode="replay", k=k)
+        trr = nbx.Trainer(graph, clusters, init, cfgr, rank=rank, world_size=world,
+                          nccl_id=nid64 if world > 1 else None, ctx=ctx)
+        trr.run(1)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        r0 = trr.progress()[1]
+        sr0, _, _ = trr.timing()
+        ev0.record(stream)
+        trr.run(args.replay_epochs)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        msr = ev0.elapsed_time(ev1)
+        sr1, _, _ = trr.timing()
+        er = trr.progress()[1] - r0
+        if world > 1:
+            t = torch.tensor([msr], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            msr = float(t[0])
+            t = torch.tensor([float(er)], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            er = int(t[0])
+        replay = {"value": er / (msr / 1e3), "unit": UNIT, "ms_per_step": msr / args.replay_epochs,
+                  "steps": args.replay_epochs, "sgd_kernel_ms": (sr1 - sr0) / args.replay_epochs,
+                  "what": "deterministic mode (bit-identical to the reference's sequential "
+                          "per-worker epochs): device mt19937_64 draws + dependency lists + "
+                          "dataflow SGD + sequential per-worker loss, epoch wall time on the "
+                          "stream (host syncs included)"}
+        trr.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         which, val, cores, secs = cpu_baseline_reference(a, offsets, nb, init, ncl, W, k,
@@ -546,6 +585,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "double_float_rows": dfrows,
+            "replay_mode": dict(replay, vs_cpu_baseline=(replay["value"] / cpu["value"]
+                                                         if cpu else None)) if replay else None,
             "knn_recall_at_15": (index.get("knn_recall_at_15") or {}).get("value"),
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -53,9 +53,10 @@ enum nomad_b200_location { NOMAD_B200_HOST = 0, NOMAD_B200_DEVICE = 1 };
 /* SGD execution mode of the epoch loop (optimizer.hpp:232-307). */
 enum nomad_b200_sgd_mode {
   /* Deterministic replay: the reference's per-worker mt19937_64 draw stream
-   * (rng.hpp:42-84, optimizer.hpp:254-255, :284-285) scheduled into
-   * conflict-free wavefront levels; fp64 in the reference's op order, no FMA,
-   * non-atomic. Layouts are bit-identical to the reference. */
+   * (rng.hpp:42-84, optimizer.hpp:254-255, :284-285) generated on the GPU,
+   * every draw run once the earlier draws touching its points are done
+   * (dataflow); fp64 in the reference's op order, no FMA, non-atomic.
+   * Layouts are bit-identical to the reference. */
   NOMAD_B200_SGD_REPLAY = 0,
   /* Throughput mode: counter-based (Philox4x32-10) draws with the reference's
    * distributions, thread-per-head, atomic fp64 scatter-add (Hogwild),
@@ -244,8 +245,9 @@ int32_t nomad_b200_knn_subcluster_rows(nomad_b200_ctx* ctx, uint64_t* rows);
  * reference stream stream_seed(seed, "np")), exact high-d neighbours by
  * (reference fp64 distance, id), exact 2-D neighbours, overlaps accumulated
  * in evaluation order: value and std_error are bit-identical to the
- * reference's. layout: rows x 2 f64 at layout_location. 1 <= k <= 56,
- * k < rows (else NOMAD_B200_ERR_PARAMETER). std_error may be NULL. */
+ * reference's. layout: rows x 2 f64 at layout_location. 1 <= k <= 1024,
+ * k < rows (else NOMAD_B200_ERR_PARAMETER); k > 56 searches the high-d rows
+ * exhaustively in fp64. std_error may be NULL. */
 int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
                                              const nomad_b200_dataset_view* high,
                                              const double* layout, int32_t layout_location,
@@ -254,7 +256,7 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
 /* metrics.hpp:174-200 neighborhood_preservation_ann on the GPU: high-d
  * neighbourhoods from a prebuilt within-cluster graph (first min(k, |list|)
  * ids), exact 2-D neighbours of every row on the device; bit-identical value.
- * 1 <= k <= 56, k < rows. */
+ * 1 <= k <= 1024, k < rows. */
 int32_t nomad_b200_neighborhood_preservation_ann(nomad_b200_ctx* ctx,
                                                  const nomad_b200_graph* graph,
                                                  const double* layout, int32_t layout_location,

@@ -309,7 +309,7 @@ inline LayoutMatrix fit(const VectorDataset& data, const TrainConfig& config,
   return out;
 }
 
-/// metrics.hpp:113-168 on the GPU (bit-identical value and std_error; k <= 56)
+/// metrics.hpp:113-168 on the GPU (bit-identical value and std_error; k <= 1024)
 inline MetricReport neighborhood_preservation(const VectorDataset& high, const LayoutMatrix& low,
                                               std::size_t k, std::size_t sample = 0,
                                               std::uint64_t seed = 0) {

@@ -214,8 +214,8 @@ class Group:
         check(lib().nomad_b200_group_create(C.cast(devs, C.c_void_p), len(devices), C.byref(h)))
         self.h = h
         self.devices = list(devices)
-        import weakref
-        self._trainers = weakref.WeakSet()  # closed before the group's contexts go
+        self._live = 0          # trainers on this group; the contexts outlive them
+        self._closing = False
         n, lb = C.c_int32(), C.c_int32()
         check(lib().nomad_b200_group_size(self.h, C.byref(n), C.byref(lb)))
         self.size, self.loopback = n.value, bool(lb.value)
@@ -229,11 +229,19 @@ class Group:
         return c
 
     def close(self) -> None:
+        """Destroys the contexts once no trainer uses them (garbage collection
+        may finalise a trainer after its group)."""
         if getattr(self, "h", None):
-            for t in list(getattr(self, "_trainers", ())):
-                t.close()
+            if self._live > 0:
+                self._closing = True
+                return
             lib().nomad_b200_group_destroy(self.h)
             self.h = None
+
+    def _release(self) -> None:
+        self._live -= 1
+        if self._live == 0 and self._closing:
+            self.close()
 
     def __del__(self):
         try:
@@ -497,7 +505,7 @@ class Trainer:
         check(lib().nomad_b200_trainer_ranks(self.h, C.byref(r)))
         self.ranks = r.value
         if group is not None:
-            group._trainers.add(self)
+            group._live += 1
 
     def run(self, n_epochs: int) -> np.ndarray:
         out = np.zeros(max(n_epochs, 1), np.float64)
@@ -546,6 +554,8 @@ class Trainer:
         if getattr(self, "h", None):
             lib().nomad_b200_trainer_destroy(self.h)
             self.h = None
+            if getattr(self, "group", None) is not None:
+                self.group._release()
 
     def __del__(self):
         try:

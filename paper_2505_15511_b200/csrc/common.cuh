@@ -42,6 +42,7 @@ int32_t guard(F&& f) {
     return NOMAD_B200_OK;
   } catch (const Error& e) {
     set_last_error(e.what());
+    cudaGetLastError();  // a reported CUDA error must not resurface at a later launch
     return 1 + static_cast<int32_t>(e.kind);
   } catch (const std::bad_alloc&) {
     set_last_error("host allocation failed");

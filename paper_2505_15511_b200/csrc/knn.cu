@@ -538,12 +538,12 @@ void launch_rerank(uint64_t nwarps, cudaStream_t S, A... args) {
 // (members[cl_beg[r] ..], or every point when members == nullptr); per-thread
 // sorted top-`want`, merged by a block reduction. Slot / want / offsets as in
 // pass 2.
-__global__ void __launch_bounds__(128) k_knn_exhaustive(
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_knn_exhaustive_t(
     XPtr x, uint32_t d, uint64_t n_all, const uint32_t* qlist,
     const uint32_t* assign, const uint32_t* members, const uint64_t* cl_beg,
     const uint32_t* sizes, uint32_t k, uint32_t fixed_want, const uint32_t* fallback,
     const uint32_t* offsets, uint32_t* out_nb, double* out_d) {
-  constexpr int KMAX = 64;
   __shared__ double sd[128 * 8];
   __shared__ uint32_t si[128 * 8];
   const uint32_t v = fallback[blockIdx.x];
@@ -600,6 +600,33 @@ __global__ void __launch_bounds__(128) k_knn_exhaustive(
     if (head < cnt && bi[head] == win) ++head;
     __syncthreads();
   }
+}
+
+// the lists of the index build (k <= 64)
+#define k_knn_exhaustive k_knn_exhaustive_t<64>
+
+// Exact global top-k of every query in qlist over all n rows (reference fp64
+// distance, (distance, id) order) for k beyond the filter's capacity
+// (quality metrics with large k): one block per query.
+void knn_exhaustive_rows(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
+                         const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d) {
+  cudaStream_t S = ctx->stream;
+  if (k > 1024) fail(kParameter, "GPU exact kNN supports k <= 1024");
+  DBuf<uint32_t> all(m);
+  {
+    std::vector<uint32_t> h(m);
+    for (uint32_t i = 0; i < m; ++i) h[i] = i;
+    NB_CUDA(cudaMemcpyAsync(all.p, h.data(), (uint64_t)m * 4, cudaMemcpyHostToDevice, S));
+  }
+  auto go = [&](auto kern) {
+    kern<<<m, 128, 0, S>>>(x, (uint32_t)d, n, qlist_d, nullptr, nullptr, nullptr, nullptr, k, k,
+                           all.p, nullptr, out_ids_d, nullptr);
+  };
+  if (k <= 64) go(k_knn_exhaustive_t<64>);
+  else if (k <= 256) go(k_knn_exhaustive_t<256>);
+  else go(k_knn_exhaustive_t<1024>);
+  note_launch(ctx, "k_knn_exhaustive");
+  NB_CUDA(cudaStreamSynchronize(S));
 }
 
 __global__ void k_knn_want(const uint32_t* assign, const uint32_t* sizes, uint64_t n, uint32_t k,
@@ -1369,9 +1396,10 @@ __global__ void k_remap_part(uint32_t m, uint32_t P, uint32_t KP, uint32_t part,
 void knn_global_sample(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* qlist_d, uint32_t m, uint32_t k, uint32_t* out_ids_d) {
   cudaStream_t S = ctx->stream;
-  if (k < 1 || k > 56) fail(kParameter, "GPU exact kNN supports 1 <= k <= 56");
+  if (k < 1) fail(kParameter, "k must be >= 1");
   if (k >= n) fail(kParameter, "k must be < n");
   if (m == 0) return;
+  if (k > 56) return knn_exhaustive_rows(ctx, x, n, d, qlist_d, m, k, out_ids_d);
   const uint32_t KP = k <= 24 ? 32 : 64;
   // candidates split into P partitions so that the grid covers the GPU
   const uint32_t nt = (m + QT - 1) / QT;

@@ -25,7 +25,8 @@ namespace nb {
 
 namespace {
 
-constexpr int LKMAX = 56;   // k bound shared with the high-d search
+constexpr int LKMAX = 1024;  // k bound (k <= 56: the certified filter + register lists;
+                             // larger k: exhaustive high-d rows, local-memory lists)
 constexpr int LTILE = 1024; // layout rows per shared-memory tile
 
 __device__ __forceinline__ double sq_dist_2d(double ax, double ay, double bx, double by) {
@@ -36,6 +37,7 @@ __device__ __forceinline__ double sq_dist_2d(double ax, double ay, double bx, do
 // grid (ceil(m / 128), P): thread = sampled slot v, blockIdx.y = candidate
 // partition [n p / P, n (p + 1) / P). Output: the partition's k smallest
 // (distance, id) keys of slot v, sorted, padded with (+inf, ~0).
+template <int LK>
 __global__ void __launch_bounds__(128) k_np_low_partial(const double* __restrict__ lay, uint64_t n,
                                                         const uint32_t* __restrict__ qlist,
                                                         uint32_t m, uint32_t k, uint32_t P,
@@ -47,8 +49,8 @@ __global__ void __launch_bounds__(128) k_np_low_partial(const double* __restrict
   const bool valid = v < m;
   const uint32_t q = valid ? qlist[v] : 0u;
   const double qx = valid ? lay[2 * (uint64_t)q] : 0.0, qy = valid ? lay[2 * (uint64_t)q + 1] : 0.0;
-  double bd[LKMAX];
-  uint32_t bi[LKMAX];
+  double bd[LK];
+  uint32_t bi[LK];
   uint32_t cnt = 0;
   for (uint64_t t0 = lo; t0 < hi; t0 += LTILE) {
     __syncthreads();
@@ -82,6 +84,16 @@ __global__ void __launch_bounds__(128) k_np_low_partial(const double* __restrict
     pd[o + r] = r < cnt ? bd[r] : __longlong_as_double(0x7ff0000000000000ll);
     pi[o + r] = r < cnt ? bi[r] : 0xFFFFFFFFu;
   }
+}
+
+void np_low_partial(dim3 grid, cudaStream_t S, const double* lay, uint64_t n, const uint32_t* ql,
+                    uint32_t m, uint32_t k, uint32_t P, double* pd, uint32_t* pi) {
+  if (k <= 56)
+    k_np_low_partial<56><<<grid, 128, 0, S>>>(lay, n, ql, m, k, P, pd, pi);
+  else if (k <= 256)
+    k_np_low_partial<256><<<grid, 128, 0, S>>>(lay, n, ql, m, k, P, pd, pi);
+  else
+    k_np_low_partial<1024><<<grid, 128, 0, S>>>(lay, n, ql, m, k, P, pd, pi);
 }
 
 // thread per slot: P-way merge of the sorted partition lists, first k keys.
@@ -167,7 +179,8 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
     dd.bind(high, S);
     const uint64_t n = dd.n;
     if (k >= n) fail(kParameter, "k must be < n");
-    if (k < 1 || k > (uint64_t)LKMAX) fail(kParameter, "GPU neighborhood_preservation supports 1 <= k <= 56");
+    if (k < 1 || k > (uint64_t)LKMAX)
+      fail(kParameter, "GPU neighborhood_preservation supports 1 <= k <= 1024");
     DevLayout L;
     L.bind(layout, layout_location, n, S);
     // evaluated points (metrics.hpp:122-136)
@@ -196,7 +209,7 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
       while (P < 64 && bx * P < 4 * (uint32_t)ctx->sm_count && n / (2 * P) >= 4096) P *= 2;
       DBuf<double> pd((uint64_t)m * P * k);
       DBuf<uint32_t> pi((uint64_t)m * P * k);
-      k_np_low_partial<<<dim3(bx, P), 128, 0, S>>>(L.p, n, ql.p, m, (uint32_t)k, P, pd.p, pi.p);
+      np_low_partial(dim3(bx, P), S, L.p, n, ql.p, m, (uint32_t)k, P, pd.p, pi.p);
       note_launch(ctx, "k_np_low_partial");
       k_np_low_merge<<<(m + 127) / 128, 128, 0, S>>>(m, (uint32_t)k, P, pd.p, pi.p, lo_ids.p);
       note_launch(ctx, "k_np_low_merge");
@@ -244,7 +257,7 @@ int32_t nomad_b200_neighborhood_preservation_ann(nomad_b200_ctx* ctx,
     const uint64_t n = graph->rows;
     if (k >= n) fail(kParameter, "k must be < n");
     if (k < 1 || k > (uint64_t)LKMAX)
-      fail(kParameter, "GPU neighborhood_preservation_ann supports 1 <= k <= 56");
+      fail(kParameter, "GPU neighborhood_preservation_ann supports 1 <= k <= 1024");
     if (n >= 0xFFFFFFFFull) fail(kSize, "point ids are u32 (n < 2^32)");
     DevLayout L;
     L.bind(layout, layout_location, n, S);
@@ -271,7 +284,7 @@ int32_t nomad_b200_neighborhood_preservation_ann(nomad_b200_ctx* ctx,
       while (P < 64 && bx * P < 4 * (uint32_t)ctx->sm_count && n / (2 * P) >= 4096) P *= 2;
       DBuf<double> pd((uint64_t)m * P * k);
       DBuf<uint32_t> pi((uint64_t)m * P * k);
-      k_np_low_partial<<<dim3(bx, P), 128, 0, S>>>(L.p, n, ql.p, m, (uint32_t)k, P, pd.p, pi.p);
+      np_low_partial(dim3(bx, P), S, L.p, n, ql.p, m, (uint32_t)k, P, pd.p, pi.p);
       note_launch(ctx, "k_np_low_partial");
       k_np_low_merge<<<(m + 127) / 128, 128, 0, S>>>(m, (uint32_t)k, P, pd.p, pi.p, lo_ids.p);
       note_launch(ctx, "k_np_low_merge");

@@ -177,10 +177,14 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
   tl[0] = h;
   atomicAdd(R.tcount + h, 1u);
   uint32_t j = 1;
-  for (; j <= cnt; ++j) {  // kNN lists hold distinct points other than the head
+  for (; j <= cnt; ++j) {
+    // build_knn's lists hold distinct points other than the head; a caller's
+    // graph may repeat one (the reference then applies both updates in turn)
     const uint32_t v = nb[j - 1];
-    tl[j] = v;
-    atomicAdd(R.tcount + v, 1u);
+    bool dup = v == h;
+    for (uint32_t a = 0; a + 1 < j && !dup; ++a) dup = nb[a] == v;
+    tl[j] = dup ? 0xFFFFFFFFu : v;
+    if (!dup) atomicAdd(R.tcount + v, 1u);
   }
   for (; j < 1 + k; ++j) tl[j] = 0xFFFFFFFFu;
   const uint32_t* tails = R.tails + (size_t)i * s;
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
     bool pending = t < W.draws;
     const uint32_t i = R.draw_base[w] + t;  // global draw index
     const uint32_t* pr = R.pred + (size_t)i * T;
-    uint32_t jj = 0;
+    uint32_t jj = 0, spins = 0;
     while (__any_sync(0xffffffffu, pending)) {
       if (!pending) continue;
       bool ready = true;
@@ -282,6 +286,13 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
         }
       }
       if (!ready) {
+        // watchdog: a predecessor is always an earlier draw of a running
+        // warp, so this only fires on a schedule bug; report, never hang
+        if (++spins > (1u << 25)) {
+          atomicExch(R.stall, 1u);
+          pending = false;
+          continue;
+        }
         __nanosleep(32);
         continue;
       }

@@ -54,6 +54,7 @@ struct ReplayDev {
   unsigned long long* edges;   // per worker: sum over draws of |N(head)| + s
   uint8_t* done;               // per draw: completed
   uint32_t* ticket;            // dataflow work counter
+  uint32_t* stall;             // set if a draw waited beyond the watchdog (never expected)
   const uint32_t* pt_base;     // per local point: draw_base of its worker
   uint32_t total_chunks;       // warps' chunks of 32 draws, worker-interleaved
   uint32_t max_draws, total_draws;

@@ -95,7 +95,7 @@ struct RankTrainer {
   DBuf<uint64_t> wcount, wbase;
   DBuf<unsigned long long> words, tlist, redges;
   DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, rtouch, rpred, tcount, toff, reject,
-      ticket, pt_base;
+      ticket, pt_base, stall;
   DBuf<uint8_t> rdone, scan_tmp;
   size_t scan_bytes = 0;
   uint32_t df_blocks = 0, total_draws = 0, max_draws = 0;
@@ -439,6 +439,8 @@ struct RankTrainer {
     reject.alloc(std::max<uint32_t>(nwl, 1));
     redges.alloc(std::max<uint32_t>(nwl, 1));
     ticket.alloc(1);
+    stall.alloc(1);
+    NB_CUDA(cudaMemsetAsync(stall.p, 0, 4, S));
     scan_bytes = replay_scan_bytes((uint32_t)orig_of.size());
     scan_tmp.alloc(std::max<size_t>(scan_bytes, 1));
   }
@@ -464,6 +466,7 @@ struct RankTrainer {
     R.edges = redges.p;
     R.done = rdone.p;
     R.ticket = ticket.p;
+    R.stall = stall.p;
     R.pt_base = pt_base.p;
     R.total_chunks = nwl * ((max_draws + 31) / 32);
     R.max_draws = max_draws;
@@ -904,6 +907,11 @@ struct RankTrainer {
   }
   DivKey sync_collect() {  // waits for this rank's epoch; returns its divergence key
     const DivKey key = local_key();  // syncs the stream
+    if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
+      uint32_t stalled = 0;
+      NB_CUDA(cudaMemcpy(&stalled, stall.p, 4, cudaMemcpyDeviceToHost));
+      if (stalled) fail(kInternal, "replay dataflow stalled (schedule watchdog)");
+    }
     float a = 0.f, b = 0.f;
     NB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
     NB_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));

@@ -16,7 +16,8 @@ def data(port):
 
 
 @pytest.mark.parametrize("k,sample,seed", [(10, 0, 0), (10, 500, 5), (1, 300, 2), (24, 400, 9),
-                                           (25, 200, 1), (56, 100, 4)])
+                                           (25, 200, 1), (56, 100, 4), (57, 100, 6),
+                                           (100, 200, 8), (300, 50, 3)])
 def test_np_bit_exact(ref, ctx, data, k, sample, seed):
     import paper_2505_15511_b200 as nb
     x, lay = data

@@ -59,6 +59,27 @@ def test_replay_host_draw_fallback_is_identical(port, ctx, monkeypatch):
     np.testing.assert_allclose(np.concatenate([loss, loss2]), rloss, rtol=1e-13, atol=0)
 
 
+def test_replay_repeated_list_entries(port, ctx):
+    """A caller's graph may repeat a neighbour inside a list (the reference then
+    applies both updates in turn); the dependency lists must not make the
+    draw wait on itself."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    nbr = g.neighbors.copy().reshape(-1, 15)
+    nbr[::7, 3] = nbr[::7, 1]
+    nbr[::11, 14] = nbr[::11, 0]
+    kw = dict(epochs=10, workers=4, seed=7)
+    tr = nb.Trainer(nb.KnnGraph(3000, 15, g.offsets, nbr.reshape(-1), g.distances),
+                    nb.ClusterAssignment(c.assignment, c.n_clusters, c.dims, c.centroids, c.sizes),
+                    pca, nb.TrainConfig(**kw), ctx=ctx)
+    loss = tr.run(3)
+    from oracle import train_config
+    rl, rloss, _, _ = port.train_epochs(c.assignment, c.n_clusters, g.offsets, nbr.reshape(-1), 15,
+                                        train_config(**kw), pca, 0, 3)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
 def test_replay_resume_equals_single_run(port, ctx):
     """run(2)+run(3) == run(5): worker RNG streams persist across calls."""
     import paper_2505_15511_b200 as nb
