@@ -395,6 +395,225 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
   }
 }
 
+// Warp-per-draw form (1 + k + s <= 32: the default k = 15, s = 5): lane u
+// owns update slot u (0 head, 1..cnt neighbours, then tails) and its pred
+// slot; every term is computed on its lane with the reference's operations
+// and lane 0 accumulates the sums in the reference's order from shared
+// memory, so results are bit-identical to the sequential
+// loop while one draw's ~100 divisions run 32-wide. Warps claim 8
+// consecutive draws of a worker (worker-interleaved) and run them in order.
+constexpr uint32_t kDfBatch = 8;
+
+__global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDev R) {
+  extern __shared__ __align__(16) double sm[];
+  const uint32_t k = P.k, s = P.s, C = P.n_clusters, T = R.T;
+  double* wt = sm;
+  double* cms = sm + (k + 1) * k;
+  const size_t tab = (size_t)(k + 1) * k + (P.gcells ? 0 : 3 * (size_t)C);
+  double* scr = sm + ((tab + 1) & ~(size_t)1) + (threadIdx.x >> 5) * 4 * 32;
+  double *sa = scr, *sb = scr + 32, *sc = scr + 64, *sd = scr + 96;
+  for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
+  if (!P.gcells)
+    for (uint32_t r = threadIdx.x; r < C; r += blockDim.x) {
+      cms[3 * r] = P.means[r].x;
+      cms[3 * r + 1] = P.means[r].y;
+      cms[3 * r + 2] = P.cell_probs[r];
+    }
+  const double* cm = P.gcells ? P.cm3 : cms;
+  __syncthreads();
+  constexpr uint32_t FULL = 0xffffffffu;
+  const double M = (double)P.m_total;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = 2 + k + s;
+  const double st = P.step;
+  for (;;) {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(R.ticket, 1u);
+    c = __shfl_sync(FULL, c, 0);
+    if (c >= R.total_chunks) break;
+    const uint32_t w = c % R.nwl;
+    const WorkerDev W = P.workers[w];
+    const uint32_t t0 = (c / R.nwl) * kDfBatch;
+    for (uint32_t t = t0; t < t0 + kDfBatch && t < W.draws; ++t) {
+      const uint32_t i = R.draw_base[w] + t;
+      // ---- wait until every predecessor is done
+      {
+        const uint32_t q = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
+        const volatile uint8_t* dn = R.done + R.draw_base[w];
+        uint32_t spins = 0;
+        bool abort = false;
+        for (;;) {
+          const bool ok = q == 0xFFFFFFFFu || dn[q] != 0;
+          if (__all_sync(FULL, ok)) break;
+          if (*reinterpret_cast<volatile uint32_t*>(R.stall) || ++spins > (1u << 25)) {
+            abort = true;  // watchdog (a schedule bug): report, never hang
+            break;
+          }
+          __nanosleep(32);
+        }
+        if (__any_sync(FULL, abort)) {
+          if (lane == 0) atomicExch(R.stall, 1u);
+          continue;
+        }
+      }
+      __threadfence();  // the predecessors' position writes before our reads
+      const uint32_t head = R.heads[i];
+      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
+      const uint32_t nsl = 1 + cnt + s;
+      uint32_t pt = head;
+      if (lane >= 1 && lane <= cnt) pt = P.ell[(size_t)head * P.kpad + lane - 1];
+      else if (lane > cnt && lane < nsl) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
+      const double2 pv = ldpos(P.pos + pt);  // every slot's position before this draw
+      const double hx = __shfl_sync(FULL, pv.x, 0), hy = __shfl_sync(FULL, pv.y, 0);
+      // ---- noise terms (objective.hpp:113-145)
+      uint32_t own = 0;
+      double lm = W.local_mass;
+      if (P.all_but_own) {
+        own = P.lclusters[P.cl_of[head]].gid;
+        lm = P.cell_probs[own];
+      }
+      const uint32_t nr = P.all_but_own ? C : W.n_rem;
+      double remote_sum = 0.0;
+      for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        double term = 0.0, use = 0.0;
+        if (q < nr) {
+          const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
+          if (!(P.all_but_own && r == own)) {
+            term = __dmul_rn(cm[3 * r + 2], cauchy_rn(hx, hy, cm[3 * r], cm[3 * r + 1]));
+            use = 1.0;
+          }
+        }
+        sa[lane] = term;
+        sb[lane] = use;
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t m = min(32u, nr - q0);
+          for (uint32_t j = 0; j < m; ++j)
+            if (sb[j] != 0.0) remote_sum = __dadd_rn(remote_sum, sa[j]);
+        }
+        __syncwarp();
+      }
+      const double mean_field = __dmul_rn(M, __shfl_sync(FULL, remote_sum, 0));
+      const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
+      const bool is_tail = lane > cnt && lane < nsl;
+      const bool is_nb = lane >= 1 && lane <= cnt;
+      const double qn = is_tail ? cauchy_rn(hx, hy, pv.x, pv.y) : 0.0;
+      sa[lane] = qn;
+      __syncwarp();
+      double qsum = 0.0;
+      if (lane == 0)
+        for (uint32_t q = 0; q < s; ++q) qsum = __dadd_rn(qsum, sa[1 + cnt + q]);
+      qsum = __shfl_sync(FULL, qsum, 0);
+      const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
+      // ---- attraction (objective.hpp:197-213), neighbour j on lane 1 + j
+      double ax = 0.0, ay = 0.0;
+      if (is_nb) {
+        const double q = cauchy_rn(hx, hy, pv.x, pv.y);
+        const double wj = wt[cnt * k + lane - 1];
+        const double qb = __dadd_rn(q, bg);
+        sa[lane] = __dmul_rn(wj, -log(__ddiv_rn(q, qb)));
+        sb[lane] = __ddiv_rn(wj, qb);
+        const double pull = __dmul_rn(
+            __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj),
+                                __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
+                      q),
+            q);
+        const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
+        sc[lane] = __dmul_rn(pull, dx);
+        sd[lane] = __dmul_rn(pull, dy);
+        ax = __dmul_rn(-pull, dx);
+        ay = __dmul_rn(-pull, dy);
+      }
+      __syncwarp();
+      double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
+      if (lane == 0)
+        for (uint32_t j = 1; j <= cnt; ++j) {
+          loss = __dadd_rn(loss, sa[j]);
+          bgs = __dadd_rn(bgs, sb[j]);
+          gx = __dadd_rn(gx, sc[j]);
+          gy = __dadd_rn(gy, sd[j]);
+        }
+      bgs = __shfl_sync(FULL, bgs, 0);
+      __syncwarp();
+      // ---- negative repulsion (objective.hpp:216-226), tail q on lane 1 + cnt + q
+      if (is_tail) {
+        const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
+        const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
+        ax = __dmul_rn(push, dx);
+        ay = __dmul_rn(push, dy);
+        sc[lane] = ax;
+        sd[lane] = ay;
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (uint32_t q = 0; q < s; ++q) {
+          gx = __dsub_rn(gx, sc[1 + cnt + q]);
+          gy = __dsub_rn(gy, sd[1 + cnt + q]);
+        }
+      __syncwarp();
+      // ---- mean repulsion (objective.hpp:229-236), q_r recomputed per cell
+      for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        double px = 0.0, py = 0.0, use = 0.0;
+        if (q < nr) {
+          const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
+          if (!(P.all_but_own && r == own)) {
+            const double mx = cm[3 * r], my = cm[3 * r + 1];
+            const double qr = cauchy_rn(hx, hy, mx, my);
+            const double push = __dmul_rn(
+                __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), M), cm[3 * r + 2]), qr), qr);
+            px = __dmul_rn(push, __dsub_rn(hx, mx));
+            py = __dmul_rn(push, __dsub_rn(hy, my));
+            use = 1.0;
+          }
+        }
+        sa[lane] = px;
+        sb[lane] = py;
+        sc[lane] = use;
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t m = min(32u, nr - q0);
+          for (uint32_t j = 0; j < m; ++j)
+            if (sc[j] != 0.0) {
+              gx = __dsub_rn(gx, sa[j]);
+              gy = __dsub_rn(gy, sb[j]);
+            }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        P.loss_slot[i] = loss;
+        ax = gx;
+        ay = gy;
+      }
+      // ---- apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails;
+      // a point in several slots gets its updates in slot order from the lane
+      // of its first slot
+      const bool slot = lane < nsl && (lane == 0 || !P.head_only);
+      sa[lane] = ax;
+      sb[lane] = ay;
+      __syncwarp();
+      const uint32_t act = __ballot_sync(FULL, slot);
+      const uint32_t same = __match_any_sync(FULL, slot ? pt : 0xFFFFFFFFu) & act;
+      if (slot && (uint32_t)(__ffs(same) - 1) == lane) {
+        double2 v = pv;
+        for (uint32_t m = same; m; m &= m - 1) {
+          const uint32_t u = __ffs(m) - 1;
+          v.x = __dsub_rn(v.x, __dmul_rn(st, sa[u]));
+          v.y = __dsub_rn(v.y, __dmul_rn(st, sb[u]));
+          if (diverged(v.x, v.y))
+            atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | pt);
+        }
+        __stcg(P.pos + pt, v);
+      }
+      __threadfence();  // our writes before the flag
+      __syncwarp();
+      if (lane == 0) *reinterpret_cast<volatile uint8_t*>(R.done + i) = 1;
+    }
+  }
+}
+
 // ------------------------------------------------------ host launchers
 static unsigned blocks_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
 
@@ -427,20 +646,33 @@ void launch_replay_deps(const ReplayDev& R, const SgdParams& P, uint32_t n_loc, 
   if (n_loc) k_replay_pred<<<blocks_for(n_loc, 256), 256, 0, st>>>(R, n_loc);
 }
 
-void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
-                         cudaStream_t st) {
-  if (smem > 48 * 1024)
-    NB_CUDA(cudaFuncSetAttribute(k_sgd_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  k_sgd_dataflow<<<nblocks, 256, smem, st>>>(P, R);
+bool dataflow_warp_form(uint32_t k, uint32_t s) { return 1 + k + s <= 32; }
+uint32_t dataflow_draws_per_chunk(uint32_t k, uint32_t s) {
+  return dataflow_warp_form(k, s) ? kDfBatch : 32;
+}
+// per-warp scratch of the warp form: 4 x 32 doubles (8 warps per block)
+static size_t df_smem(size_t smem, uint32_t k, uint32_t s) {
+  return dataflow_warp_form(k, s) ? ((smem + 15) & ~(size_t)15) + 8 * 4 * 32 * sizeof(double) : smem;
 }
 
-uint32_t dataflow_resident_blocks(size_t smem, int sm_count) {
-  if (smem > 48 * 1024)
-    NB_CUDA(cudaFuncSetAttribute(k_sgd_dataflow, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
+                         cudaStream_t st) {
+  const bool wf = dataflow_warp_form(P.k, P.s);
+  const size_t sm = df_smem(smem, P.k, P.s);
+  auto kern = wf ? k_sgd_dataflow_warp : k_sgd_dataflow;
+  if (sm > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  kern<<<nblocks, 256, sm, st>>>(P, R);
+}
+
+uint32_t dataflow_resident_blocks(size_t smem, int sm_count, uint32_t k, uint32_t s) {
+  const bool wf = dataflow_warp_form(k, s);
+  const size_t sm = df_smem(smem, k, s);
+  auto kern = wf ? k_sgd_dataflow_warp : k_sgd_dataflow;
+  if (sm > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 0;
-  NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sgd_dataflow, 256, smem));
+  NB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, sm));
   return (uint32_t)std::max(per_sm, 1) * (uint32_t)sm_count;
 }
 

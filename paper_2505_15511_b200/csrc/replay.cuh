@@ -56,7 +56,7 @@ struct ReplayDev {
   uint32_t* ticket;            // dataflow work counter
   uint32_t* stall;             // set if a draw waited beyond the watchdog (never expected)
   const uint32_t* pt_base;     // per local point: draw_base of its worker
-  uint32_t total_chunks;       // warps' chunks of 32 draws, worker-interleaved
+  uint32_t total_chunks;       // warps' chunks of draws, worker-interleaved
   uint32_t max_draws, total_draws;
 };
 
@@ -69,6 +69,9 @@ void launch_replay_deps(const ReplayDev& R, const SgdParams& P, uint32_t n_loc, 
 size_t replay_scan_bytes(uint32_t n_loc);
 void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
                          cudaStream_t st);
-uint32_t dataflow_resident_blocks(size_t smem, int sm_count);
+uint32_t dataflow_resident_blocks(size_t smem, int sm_count, uint32_t k, uint32_t s);
+// the warp-per-draw form applies when 1 + k + s <= 32; draws claimed per ticket
+bool dataflow_warp_form(uint32_t k, uint32_t s);
+uint32_t dataflow_draws_per_chunk(uint32_t k, uint32_t s);
 
 }  // namespace nb

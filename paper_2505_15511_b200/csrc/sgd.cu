@@ -10,14 +10,32 @@
 namespace nb {
 
 // Per-worker loss in sequential draw order (optimizer.hpp:289-290).
+// One warp per worker: coalesced loads of the next 128 slots, the chain added
+// in draw order by every lane (as k_means_exact).
 __global__ void k_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk,
                            uint32_t nw, double* out) {
-  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
   if (w >= nw) return;
   double acc = 0.0;
   const double* p = slot + base[w];
-  for (uint32_t t = 0; t < wk[w].draws; ++t) acc = __dadd_rn(acc, p[t]);
-  out[w] = acc;
+  const uint32_t D = wk[w].draws;
+  for (uint32_t b = 0; b < D; b += 128) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = b + 32 * u + lane;
+      v[u] = i < D ? p[i] : 0.0;
+    }
+    const uint32_t m = min(128u, D - b);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      for (uint32_t l = 0; l < 32; ++l) {
+        const double x = __shfl_sync(0xffffffffu, v[u], l);
+        if (32 * u + l < m) acc = __dadd_rn(acc, x);
+      }
+  }
+  if (lane == 0) out[w] = acc;
 }
 
 // ------------------------------------------------------ K9 cluster means
@@ -25,16 +43,35 @@ __global__ void k_loss_seq(const double* slot, const uint32_t* base, const Worke
 // Exact: per local cluster and coordinate, a sequential sum over the
 // cluster's contiguous segment (ascending original id == the order of
 // gather_means, optimizer.hpp:163-168 / :420-428), then / count.
+// One warp per (cluster, coordinate) chain: the lanes load the next 128
+// values (coalesced, four per lane, in flight together) and the chain is
+// added in ascending order from them (each lane adds every value, in order,
+// so every lane holds the same sum), then / count.
 __global__ void k_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl,
                               double* slot /* ncl x 2 */) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
   if (g >= 2 * ncl) return;
   const uint32_t c = g >> 1, dim = g & 1;
   const LocalCluster L = lc[c];
   const double* p = reinterpret_cast<const double*>(pos) + 2 * (size_t)L.start + dim;
   double acc = 0.0;
-  for (uint32_t i = 0; i < L.count; ++i) acc = __dadd_rn(acc, p[2 * (size_t)i]);
-  slot[g] = __ddiv_rn(acc, (double)L.count);
+  for (uint32_t b = 0; b < L.count; b += 128) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = b + 32 * u + lane;
+      v[u] = i < L.count ? p[2 * (size_t)i] : 0.0;
+    }
+    const uint32_t m = min(128u, L.count - b);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      for (uint32_t l = 0; l < 32; ++l) {
+        const double x = __shfl_sync(0xffffffffu, v[u], l);
+        if (32 * u + l < m) acc = __dadd_rn(acc, x);
+      }
+  }
+  if (lane == 0) slot[g] = __ddiv_rn(acc, (double)L.count);
 }
 
 // Throughput: chunked tree reduction into per-cluster sums (atomics), fused
@@ -179,12 +216,12 @@ static unsigned blocks_for(uint64_t n, unsigned t) { return (unsigned)((n + t - 
 
 void launch_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk, uint32_t nw,
                      double* out, cudaStream_t st) {
-  k_loss_seq<<<blocks_for(nw, 32), 32, 0, st>>>(slot, base, wk, nw, out);
+  k_loss_seq<<<blocks_for(nw, 4), 128, 0, st>>>(slot, base, wk, nw, out);
 }
 
 void launch_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl, double* slot,
                         cudaStream_t st) {
-  k_means_exact<<<blocks_for(2 * ncl, 64), 64, 0, st>>>(pos, lc, ncl, slot);
+  k_means_exact<<<blocks_for(2 * ncl, 4), 128, 0, st>>>(pos, lc, ncl, slot);
 }
 
 void launch_means_chunk(double2* pos, bool df, const LocalCluster* lc, uint32_t ncl, uint32_t chunk,

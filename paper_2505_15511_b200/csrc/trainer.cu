@@ -468,7 +468,8 @@ struct RankTrainer {
     R.ticket = ticket.p;
     R.stall = stall.p;
     R.pt_base = pt_base.p;
-    R.total_chunks = nwl * ((max_draws + 31) / 32);
+    const uint32_t per = dataflow_draws_per_chunk((uint32_t)k, (uint32_t)s);
+    R.total_chunks = nwl * ((max_draws + per - 1) / per);
     R.max_draws = max_draws;
     R.total_draws = total_draws;
     return R;
@@ -527,7 +528,8 @@ struct RankTrainer {
       if (rj[wl] || force) host_draws(wl);
     launch_replay_deps(R, P, (uint32_t)orig_of.size(), scan_tmp.p, scan_bytes, S);
     launched("k_replay_deps");
-    if (!df_blocks) df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count);
+    if (!df_blocks)
+      df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
     NB_CUDA(cudaMemsetAsync(rdone.p, 0, rdone.bytes(), S));
     NB_CUDA(cudaMemsetAsync(ticket.p, 0, 4, S));
     P.loss_slot = loss_slot.p;
