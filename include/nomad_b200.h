@@ -231,6 +231,35 @@ int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
                               const nomad_b200_clusters* clusters,
                               const nomad_b200_graph* graph, uint64_t sample, uint64_t seed,
                               double* recall_out);
+/* Row-sharded index build (the 60M-row configuration): this
+ * rank holds only rows [row0, row0 + rows->rows) of an n_total-row dataset
+ * (ranks tile [0, n_total) in rank order). lsh_init + kmeans_em run
+ * row-sharded as fit() calls them (optimizer.hpp:336-339; kmeans_tol < 0:
+ * default_kmeans_tol): integer counts are all-reduced and every sum the
+ * reference accumulates in ascending point id is carried rank to rank, so
+ * clusters and centroids are bit-identical to the one-GPU build. Rows then
+ * move once to the rank owning their cluster (shard_clusters over `workers`
+ * in contiguous rank blocks, optimizer.hpp:106-144) and each rank builds the
+ * kNN lists of its clusters (knn.hpp:65-109; identical to the full build's).
+ * One process per GPU over NCCL (128-byte nccl_id; NULL when world == 1).
+ * Outputs (host, nullable): clusters_out (n_total assignment, centroids,
+ * sizes: every rank's copy is the same) and graph_out (CSR over n_total rows
+ * holding this rank's lists only; neighbors / distances capacity n_total*k). */
+int32_t nomad_b200_index_sharded(nomad_b200_ctx* ctx, int32_t rank, int32_t world,
+                                 const void* nccl_id, const nomad_b200_dataset_view* rows,
+                                 uint64_t row0, uint64_t n_total, uint64_t n_clusters,
+                                 uint64_t seed, uint64_t kmeans_max_iters, double kmeans_tol,
+                                 uint64_t workers, uint64_t k, int32_t knn_mode,
+                                 nomad_b200_clusters* clusters_out, nomad_b200_graph* graph_out);
+/* The same over the ranks of a group (one host thread per rank): rows[r] /
+ * row0[r] on rank r's device; graph_out receives every rank's lists. */
+int32_t nomad_b200_group_index_sharded(nomad_b200_group* g, const nomad_b200_dataset_view* rows,
+                                       const uint64_t* row0, uint64_t n_total,
+                                       uint64_t n_clusters, uint64_t seed,
+                                       uint64_t kmeans_max_iters, double kmeans_tol,
+                                       uint64_t workers, uint64_t k, int32_t knn_mode,
+                                       nomad_b200_clusters* clusters_out,
+                                       nomad_b200_graph* graph_out);
 /* Statistics of the context's last build_knn: rows the tensor-core
  * certificate did not settle, and rows resolved by the exhaustive fp64 pass. */
 int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,
@@ -432,6 +461,13 @@ int32_t nomad_b200_generate_mixture(nomad_b200_ctx* ctx, uint64_t rows,
 int32_t nomad_b200_generate_mixture_bf16(nomad_b200_ctx* ctx, uint64_t rows,
                                          uint64_t dims, uint64_t blobs,
                                          double spread, uint64_t seed, void* out);
+
+/* Rows [row0, row0 + rows) of the same mixture (one rank's share of a
+ * row-sharded dataset; identical to those rows of the full matrix). dtype:
+ * NOMAD_B200_F32 or NOMAD_B200_BF16. */
+int32_t nomad_b200_generate_mixture_rows(nomad_b200_ctx* ctx, uint64_t row0, uint64_t rows,
+                                         uint64_t dims, uint64_t blobs, double spread,
+                                         uint64_t seed, int32_t dtype, void* out);
 
 /* Diagnostic: one 128 x 128 bf16 tile product D = A B^T through the same
  * TMA + tcgen05.mma + TMEM path the bf16 kNN uses (rows rounded to bf16). */

@@ -133,6 +133,18 @@ _SIGS = {
                                    _vp, C.POINTER(ClustersView), C.POINTER(GraphView), _vp]),
     "nomad_b200_fit_ex": (C.c_int32, [_vp, _vp, C.POINTER(DatasetView), C.POINTER(TrainConfigC),
                                       _vp, _vp, C.POINTER(FitReportC)]),
+    "nomad_b200_index_sharded": (C.c_int32, [_vp, C.c_int32, C.c_int32, _vp, C.POINTER(DatasetView),
+                                             C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                             C.c_uint64, C.c_double, C.c_uint64, C.c_uint64,
+                                             C.c_int32, C.POINTER(ClustersView),
+                                             C.POINTER(GraphView)]),
+    "nomad_b200_group_index_sharded": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp, C.c_uint64,
+                                                   C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
+                                                   C.c_uint64, C.c_uint64, C.c_int32,
+                                                   C.POINTER(ClustersView), C.POINTER(GraphView)]),
+    "nomad_b200_generate_mixture_rows": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                     C.c_uint64, C.c_double, C.c_uint64, C.c_int32,
+                                                     _vp]),
     "nomad_b200_plan": (C.c_int32, [C.c_uint64, C.c_uint64, _vp, C.c_uint64, C.c_int32, _vp, _vp,
                                     C.POINTER(C.c_uint32)]),
     "nomad_b200_debug_tc_gemm": (C.c_int32, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint32,

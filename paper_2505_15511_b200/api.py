@@ -683,6 +683,74 @@ def generate_mixture(rows: int, dims: int, blobs: int, spread: float = 10.0, see
     return out
 
 
+def generate_mixture_rows(row0: int, rows: int, dims: int, blobs: int, spread: float = 10.0,
+                          seed: int = 42, ctx: Optional[Context] = None, dtype: str = "f32"):
+    """Rows [row0, row0 + rows) of generate_mixture's matrix (a rank's share)."""
+    import torch
+    cx = _ctx(ctx)
+    bf = dtype == "bf16"
+    out = torch.empty((rows, dims), dtype=torch.bfloat16 if bf else torch.float32,
+                      device=f"cuda:{cx.device}")
+    check(lib().nomad_b200_generate_mixture_rows(cx.h, row0, rows, dims, blobs, spread, seed,
+                                                 N.BF16 if bf else N.F32, out.data_ptr()))
+    return out
+
+
+def _sharded_outputs(n_total, C, d, k):
+    ca = ClusterAssignment(np.zeros(n_total, np.uint32), C, d, np.zeros(C * d, np.float64),
+                           np.zeros(C, np.uint32))
+    off = np.zeros(n_total + 1, np.uint32)
+    nb = np.zeros(max(n_total * k, 1), np.uint32)
+    di = np.zeros(max(n_total * k, 1), np.float64)
+    return ca, off, nb, di
+
+
+def index_sharded(rows, row0: int, n_total: int, n_clusters: int, seed: int, workers: int,
+                  k: int = 15, knn_mode: str = "exact", rank: int = 0, world_size: int = 1,
+                  nccl_id: Optional[bytes] = None, max_iters: int = 100, tol: float = -1.0,
+                  ctx: Optional[Context] = None):
+    """Row-sharded lsh_init + kmeans_em + build_knn for one rank of a
+    multi-process run (nomad_b200_index_sharded): this rank holds rows
+    [row0, row0 + len(rows)). Returns (ClusterAssignment over all n_total
+    rows, KnnGraph holding this rank's clusters' lists)."""
+    dv, keep = _dataset(rows)
+    C_, d = int(n_clusters), dv.dims
+    ca, off, nb, di = _sharded_outputs(n_total, C_, d, k)
+    cv = ca._view()
+    gv = N.GraphView(n_total, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
+    idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+    km = {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[knn_mode]
+    check(lib().nomad_b200_index_sharded(_ctx(ctx).h, rank, world_size, idbuf, C.byref(dv), row0,
+                                         n_total, C_, seed & (2**64 - 1), max_iters, tol, workers,
+                                         k, km, C.byref(cv), C.byref(gv)))
+    m = int(off[n_total])
+    return ca, KnnGraph(n_total, k, off, nb[:m], di[:m])
+
+
+def group_index_sharded(group: "Group", rows: list, row0: list, n_total: int, n_clusters: int,
+                        seed: int, workers: int, k: int = 15, knn_mode: str = "exact",
+                        max_iters: int = 100, tol: float = -1.0):
+    """The row-sharded index build over the ranks of a Group (rows[r] on rank
+    r's device): (ClusterAssignment, KnnGraph with every rank's lists)."""
+    views, keeps = [], []
+    for r in rows:
+        v, kp = _dataset(r)
+        views.append(v)
+        keeps.append(kp)
+    arr = (N.DatasetView * len(views))(*views)
+    r0 = np.ascontiguousarray(row0, np.uint64)
+    C_, d = int(n_clusters), views[0].dims
+    ca, off, nb, di = _sharded_outputs(n_total, C_, d, k)
+    cv = ca._view()
+    gv = N.GraphView(n_total, k, off.ctypes.data, nb.ctypes.data, di.ctypes.data, N.HOST)
+    km = {"exact": N.KNN_EXACT, "bf16": N.KNN_BF16, "exact_ffma": N.KNN_EXACT_FFMA}[knn_mode]
+    check(lib().nomad_b200_group_index_sharded(group.h, arr, r0.ctypes.data, n_total, C_,
+                                               seed & (2**64 - 1), max_iters, tol, workers, k, km,
+                                               C.byref(cv), C.byref(gv)))
+    m = int(off[n_total])
+    return ca, KnnGraph(n_total, k, off, nb[:m], di[:m])
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().nomad_b200_nccl_unique_id(buf))

@@ -125,12 +125,33 @@ template <>
 __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 // T = __nv_bfloat16: the same f32 values rounded to nearest-even bf16.
+// Rows [row0, row0 + rows) of the mixture: element e of the full matrix is
+// value e % 4 of Philox block e / 4, so any row slice (one rank's share of a
+// row-sharded dataset) holds exactly the full matrix's values.
 template <class T>
-__global__ void k_mixture_points(T* out, const float* centres, uint64_t rows,
+__global__ void k_mixture_points(T* out, const float* centres, uint64_t row0, uint64_t rows,
                                  uint64_t dims, uint64_t blobs, uint32_t s0, uint32_t s1) {
-  const uint64_t total = rows * dims;
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q * 4 < total;
-       q += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t base = row0 * dims, total = rows * dims;
+  if (base & 3) {  // slice not aligned to a Philox block: per element
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t ge = base + e, q = ge / 4;
+      const u32x4 r = philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0x9Au, 1u}, s0, s1);
+      const float u0 = ((r.x >> 8) + 1) * 0x1p-24f, v0 = (r.y >> 8) * 0x1p-24f;
+      const float u1 = ((r.z >> 8) + 1) * 0x1p-24f, v1 = (r.w >> 8) * 0x1p-24f;
+      const float a = sqrtf(-2.f * __logf(u0)), b = sqrtf(-2.f * __logf(u1));
+      float g[4];
+      sincospif(2.f * v0, &g[1], &g[0]);
+      sincospif(2.f * v1, &g[3], &g[2]);
+      g[0] *= a; g[1] *= a; g[2] *= b; g[3] *= b;
+      const uint64_t i = ge / dims, j = ge % dims;
+      out[e] = to_out<T>(centres[(i % blobs) * dims + j] + g[ge & 3]);
+    }
+    return;
+  }
+  out -= base;  // index by global element below (only [base, base + total) is written)
+  for (uint64_t q = base / 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+       q * 4 < base + total; q += (uint64_t)gridDim.x * blockDim.x) {
     const u32x4 r = philox4x32_10(u32x4{(uint32_t)q, (uint32_t)(q >> 32), 0x9Au, 1u}, s0, s1);
     const float u0 = ((r.x >> 8) + 1) * 0x1p-24f, v0 = (r.y >> 8) * 0x1p-24f;
     const float u1 = ((r.z >> 8) + 1) * 0x1p-24f, v1 = (r.w >> 8) * 0x1p-24f;
@@ -140,7 +161,7 @@ __global__ void k_mixture_points(T* out, const float* centres, uint64_t rows,
     sincospif(2.f * v1, &g[3], &g[2]);
     g[0] *= a; g[1] *= a; g[2] *= b; g[3] *= b;
     const uint64_t e0 = q * 4;
-    if ((dims & 3) == 0 && e0 + 3 < total) {
+    if ((dims & 3) == 0 && e0 + 3 < base + total) {
       const uint64_t i = e0 / dims, j = e0 % dims;
       const float4 c = *reinterpret_cast<const float4*>(centres + (i % blobs) * dims + j);
       if constexpr (sizeof(T) == 4) {
@@ -155,7 +176,7 @@ __global__ void k_mixture_points(T* out, const float* centres, uint64_t rows,
     } else {
       for (int t = 0; t < 4; ++t) {
         const uint64_t e = e0 + t;
-        if (e >= total) break;
+        if (e >= base + total) break;
         const uint64_t i = e / dims, j = e % dims;
         out[e] = to_out<T>(centres[(i % blobs) * dims + j] + g[t]);
       }
@@ -256,8 +277,9 @@ int32_t nomad_b200_nccl_unique_id(void* out128) {
   });
 }
 
-static int32_t generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims, uint64_t blobs,
-                                double spread, uint64_t seed, void* out, bool bf16) {
+static int32_t generate_mixture(nomad_b200_ctx* c, uint64_t row0, uint64_t rows, uint64_t dims,
+                                uint64_t blobs, double spread, uint64_t seed, void* out,
+                                bool bf16) {
   return guard([&] {
     if (!c || !out) fail(kParameter, "NULL argument");
     if (rows < 1 || dims < 1 || blobs < 1) fail(kParameter, "empty mixture shape");
@@ -270,11 +292,11 @@ static int32_t generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
     note_launch(c, "k_mixture_centres");
     if (bf16)
       k_mixture_points<<<c->sm_count * 8, 256, 0, c->stream>>>(
-          static_cast<__nv_bfloat16*>(out), centres.p, rows, dims, blobs, s0, s1);
+          static_cast<__nv_bfloat16*>(out), centres.p, row0, rows, dims, blobs, s0, s1);
     else
       k_mixture_points<<<c->sm_count * 8, 256, 0, c->stream>>>(static_cast<float*>(out),
-                                                               centres.p, rows, dims, blobs, s0,
-                                                               s1);
+                                                               centres.p, row0, rows, dims, blobs,
+                                                               s0, s1);
     note_launch(c, "k_mixture_points");
     NB_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -282,13 +304,19 @@ static int32_t generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
 
 int32_t nomad_b200_generate_mixture(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
                                     uint64_t blobs, double spread, uint64_t seed, float* out) {
-  return generate_mixture(c, rows, dims, blobs, spread, seed, out, false);
+  return generate_mixture(c, 0, rows, dims, blobs, spread, seed, out, false);
 }
 
 int32_t nomad_b200_generate_mixture_bf16(nomad_b200_ctx* c, uint64_t rows, uint64_t dims,
                                          uint64_t blobs, double spread, uint64_t seed,
                                          void* out) {
-  return generate_mixture(c, rows, dims, blobs, spread, seed, out, true);
+  return generate_mixture(c, 0, rows, dims, blobs, spread, seed, out, true);
+}
+
+int32_t nomad_b200_generate_mixture_rows(nomad_b200_ctx* c, uint64_t row0, uint64_t rows,
+                                         uint64_t dims, uint64_t blobs, double spread,
+                                         uint64_t seed, int32_t dtype, void* out) {
+  return generate_mixture(c, row0, rows, dims, blobs, spread, seed, out, dtype == NOMAD_B200_BF16);
 }
 
 }  // extern "C"

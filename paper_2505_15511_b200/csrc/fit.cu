@@ -9,6 +9,7 @@
 #include <initializer_list>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "index_common.cuh"
 #include "plan.cuh"
@@ -186,7 +187,7 @@ static void fit_impl(nomad_b200_ctx* ctx, nomad_b200_group* grp, const nomad_b20
       // eligible heads: the ascending ids of rows with a list (stable compaction)
       DBuf<uint32_t> ids(n);
       DBuf<unsigned long long> cnt(1);
-      cub::CountingInputIterator<uint32_t> it(0);
+      thrust::counting_iterator<uint32_t> it(0);
       size_t tmp = 0;
       NB_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flag.p, ids.p, cnt.p, (int64_t)n, S));
       DBuf<uint8_t> tb(std::max<size_t>(tmp, 1));

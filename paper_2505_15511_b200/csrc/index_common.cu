@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) k_seq_colsum2(XPtr x, uint64_t d,
                                                      const uint64_t* seg_beg,
                                                      const uint64_t* seg_cnt,
                                                      const uint32_t* seg_row, uint32_t nseg,
-                                                     double* out) {
+                                                     double* out, int carry) {
   extern __shared__ float sbuf[];  // [2][BR][33]
   const uint32_t groups = (uint32_t)((d + 31) / 32);
   const uint32_t sidx = blockIdx.x / groups;
@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(256) k_seq_colsum2(XPtr x, uint64_t d,
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   const uint64_t nb = (cnt + BR - 1) / BR;
-  double acc = 0.0;
+  // carry: continue the running sums already in `out` (the previous rank's,
+  // row-sharded build) and leave them undivided
+  double acc = (carry && colok) ? out[(uint64_t)seg_row[sidx] * d + j] : 0.0;
   issue(0);
   for (uint64_t b = 0; b < nb; ++b) {
     if (b + 1 < nb) issue(b + 1);
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(256) k_seq_colsum2(XPtr x, uint64_t d,
     }
     __syncthreads();
   }
-  if (warp == 0 && colok) out[(uint64_t)seg_row[sidx] * d + j] = __ddiv_rn(acc, (double)cnt);
+  if (warp == 0 && colok)
+    out[(uint64_t)seg_row[sidx] * d + j] = carry ? acc : __ddiv_rn(acc, (double)cnt);
 }
 
 }  // namespace
@@ -157,7 +160,7 @@ void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uin
 
 void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
-                      const std::vector<uint32_t>& seg_ids, double* out) {
+                      const std::vector<uint32_t>& seg_ids, double* out, bool carry) {
   cudaStream_t S = ctx->stream;
   const uint32_t nseg = (uint32_t)seg_ids.size();
   if (!nseg) return;
@@ -171,7 +174,8 @@ void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* m
   const size_t smem = 2 * BR * 33 * sizeof(float);
   NB_CUDA(cudaFuncSetAttribute(k_seq_colsum2<BR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
-  k_seq_colsum2<BR><<<(unsigned)ctas, 256, smem, S>>>(x, d, members, db.p, dc.p, dr.p, nseg, out);
+  k_seq_colsum2<BR><<<(unsigned)ctas, 256, smem, S>>>(x, d, members, db.p, dc.p, dr.p, nseg, out,
+                                                      carry ? 1 : 0);
   note_launch(ctx, "k_seq_colsum2");
   NB_CUDA(cudaStreamSynchronize(S));
 }

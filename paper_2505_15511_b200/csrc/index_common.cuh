@@ -169,10 +169,11 @@ void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uin
 // in order, of (double) x[m * d + j]) / cnt[s]  — the reference's sequential centroid /
 // mean accumulation (kmeans.hpp:75-104, :176-181, :218-226) bit for bit.
 // members == nullptr means the identity list. Segments with count 0 are
-// left untouched.
+// left untouched. carry: `out` holds running sums that the segments continue
+// (a row-sharded build's carry chain, shard.cuh), written back undivided.
 void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
-                      const std::vector<uint32_t>& seg_ids, double* out);
+                      const std::vector<uint32_t>& seg_ids, double* out, bool carry = false);
 
 // Exact global kNN of m sampled points (knn.cu): out_ids_d[v * k + r] = the
 // r-th smallest (reference fp64 distance, id) key of point qlist_d[v] among

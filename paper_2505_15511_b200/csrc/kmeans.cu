@@ -11,6 +11,7 @@
 #include <numeric>
 
 #include "index_common.cuh"
+#include "shard.cuh"
 
 namespace nb {
 
@@ -225,10 +226,10 @@ __global__ void k_sizes(const uint32_t* a, uint64_t n, uint32_t* sizes) {
 // Sequential fp64 sum of v[0..n) in order (one thread adds; the block stages
 // the next tile into shared memory). Used where the reference accumulates a
 // scalar over points in order (quantization_error, the perturbation scale).
-__global__ void k_seq_sum(const double* v, uint64_t n, double* out) {
+__global__ void k_seq_sum(const double* v, uint64_t n, double* out, int carry) {
   constexpr int T = 2048;
   __shared__ double buf[2][T];
-  double acc = 0.0;
+  double acc = carry ? *out : 0.0;  // carry: continue the previous rank's running sum
   int cur = 0;
   for (uint64_t e = threadIdx.x; e < T && e < n; e += blockDim.x) buf[0][e] = v[e];
   __syncthreads();
@@ -247,10 +248,10 @@ __global__ void k_seq_sum(const double* v, uint64_t n, double* out) {
 
 // default_kmeans_tol accumulator (kmeans.hpp:157-161): storage-order
 // sequential sum of the exact products (double)v * v.
-__global__ void k_seq_sumsq(XPtr v, uint64_t n, double* out) {
+__global__ void k_seq_sumsq(XPtr v, uint64_t n, double* out, int carry) {
   constexpr int T = 4096;
   __shared__ float buf[2][T];
-  double acc = 0.0;
+  double acc = carry ? *out : 0.0;
   int cur = 0;
   for (uint64_t e = threadIdx.x; e < T && e < n; e += blockDim.x) buf[0][e] = v[e];
   __syncthreads();
@@ -319,6 +320,15 @@ __global__ void k_far_argmin(const double* dist, const uint32_t* a, uint64_t n, 
 }
 __global__ void k_set_u32(uint32_t* p, uint64_t i, uint32_t v) { p[i] = v; }
 
+// rows r of `m` (rows x d sums) with div[r] > 0 divided by div[r] (the carry
+// chain's final step: kmeans.hpp:98-103 skips empty clusters)
+__global__ void k_div_rows(double* m, uint32_t rows, uint32_t d, const double* div) {
+  const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (e >= (uint64_t)rows * d) return;
+  const double v = div[e / d];
+  if (v > 0.0) m[e] = __ddiv_rn(m[e], v);
+}
+
 unsigned grid_for(uint64_t n, unsigned t, unsigned cap) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(cap, (n + t - 1) / t));
 }
@@ -330,8 +340,11 @@ unsigned grid_for(uint64_t n, unsigned t, unsigned cap) {
 struct KMeans {
   nomad_b200_ctx* ctx;
   XPtr x;
-  uint64_t n, d;
+  uint64_t n, d;  // this rank's rows (all rows on one GPU)
   uint32_t C;
+  // row-sharded build (shard.cuh): rows [row0, row0 + n) of n_total
+  Comm* comm = nullptr;
+  uint64_t row0 = 0, n_total = 0;
   DBuf<uint32_t> a;        // assignment
   DBuf<double> cent;       // C x d
   DBuf<uint32_t> sizes_d;  // C
@@ -341,7 +354,7 @@ struct KMeans {
   DBuf<unsigned long long> u64s;
 
   KMeans(nomad_b200_ctx* c, XPtr xx, uint64_t nn, uint64_t dd, uint32_t CC)
-      : ctx(c), x(xx), n(nn), d(dd), C(CC) {
+      : ctx(c), x(xx), n(nn), d(dd), C(CC), n_total(nn) {
     a.alloc(n);
     cent.alloc((uint64_t)C * d);
     sizes_d.alloc(C);
@@ -352,6 +365,17 @@ struct KMeans {
 
   void assign(bool count, unsigned long long* changes_out) {
     NB_CUDA(cudaMemsetAsync(u64s.p, 0, 8, S()));
+    if (!n) {  // a rank without rows still takes part in the count
+      if (changes_out) {
+        *changes_out = 0;
+        if (comm) {
+          uint64_t c = 0;
+          comm->allreduce_u64(&c, 1);
+          *changes_out = c;
+        }
+      }
+      return;
+    }
     auto go = [&](auto kern, int tp, int tc) {
       const size_t smem = (size_t)(tp + tc) * 33 * 8 + (size_t)tp * 32 * 4;
       NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -365,7 +389,47 @@ struct KMeans {
     if (changes_out) {
       NB_CUDA(cudaMemcpyAsync(changes_out, u64s.p, 8, cudaMemcpyDeviceToHost, S()));
       NB_CUDA(cudaStreamSynchronize(S()));
+      if (comm) {
+        uint64_t c = *changes_out;
+        comm->allreduce_u64(&c, 1);
+        *changes_out = c;
+      }
     }
+  }
+
+  // Sequential ascending-id column sums over segments of this rank's rows
+  // (members: local row indices), divided by the global counts `div` — on
+  // one GPU seq_column_means itself; row-sharded, the carry chain.
+  void seq_means(const uint32_t* members, const std::vector<uint64_t>& beg,
+                 const std::vector<uint64_t>& cnt, const std::vector<uint32_t>& rows,
+                 const std::vector<double>& div, double* out, uint32_t out_rows) {
+    if (!comm) {
+      seq_column_means(ctx, x, d, members, beg, cnt, rows, out);
+      return;
+    }
+    comm->chain(out, (size_t)out_rows * d, [&] {
+      seq_column_means(ctx, x, d, members, beg, cnt, rows, out, true);
+    });
+    DBuf<double> dv(out_rows);
+    NB_CUDA(cudaMemcpyAsync(dv.p, div.data(), out_rows * 8, cudaMemcpyHostToDevice, S()));
+    const uint64_t e = (uint64_t)out_rows * d;
+    k_div_rows<<<(unsigned)((e + 255) / 256), 256, 0, S()>>>(out, out_rows, (uint32_t)d, dv.p);
+    note_launch(ctx, "k_div_rows");
+    NB_CUDA(cudaStreamSynchronize(S()));
+  }
+  // Sequential sum of v[0..n) (kmeans.hpp:148-154, :228-231): a carry chain
+  // when row-sharded.
+  double seq_sum(const double* v) {
+    auto run = [&](int carry) {
+      k_seq_sum<<<1, 256, 0, S()>>>(v, n, scal.p, carry);
+      note_launch(ctx, "k_seq_sum");
+    };
+    if (comm) comm->chain(scal.p, 1, [&] { run(1); });
+    else run(0);
+    double acc = 0.0;
+    NB_CUDA(cudaMemcpyAsync(&acc, scal.p, 8, cudaMemcpyDeviceToHost, S()));
+    NB_CUDA(cudaStreamSynchronize(S()));
+    return acc;
   }
 
   void recompute_sizes() {
@@ -375,6 +439,13 @@ struct KMeans {
     sizes.resize(C);
     NB_CUDA(cudaMemcpyAsync(sizes.data(), sizes_d.p, C * 4, cudaMemcpyDeviceToHost, S()));
     NB_CUDA(cudaStreamSynchronize(S()));
+    if (comm) {  // global sizes on every rank
+      std::vector<uint64_t> g(sizes.begin(), sizes.end());
+      comm->allreduce_u64(g.data(), C);
+      for (uint32_t r = 0; r < C; ++r) sizes[r] = (uint32_t)g[r];
+      NB_CUDA(cudaMemcpyAsync(sizes_d.p, sizes.data(), C * 4, cudaMemcpyHostToDevice, S()));
+      NB_CUDA(cudaStreamSynchronize(S()));
+    }
   }
 
   // kmeans.hpp:90-104: zero every centroid, sum members ascending, divide
@@ -386,13 +457,16 @@ struct KMeans {
     group_by_label(ctx, a.p, n, C, mem, off);
     std::vector<uint64_t> beg, cnt;
     std::vector<uint32_t> rows;
-    for (uint32_t r = 0; r < C; ++r)
+    std::vector<double> div(C, 0.0);
+    for (uint32_t r = 0; r < C; ++r) {
+      div[r] = (double)sizes[r];
       if (off[r + 1] > off[r]) {
         beg.push_back(off[r]);
         cnt.push_back(off[r + 1] - off[r]);
         rows.push_back(r);
       }
-    seq_column_means(ctx, x, d, mem.p, beg, cnt, rows, cent.p);
+    }
+    seq_means(mem.p, beg, cnt, rows, div, cent.p, C);
   }
 
   // kmeans.hpp:75-88 for one cluster (members ascending; zero if empty).
@@ -405,7 +479,22 @@ struct KMeans {
     DBuf<uint32_t> mem;
     std::vector<uint64_t> off;
     group_by_label(ctx, lab.p, n, 1, mem, off);
-    if (off[1] > 0) seq_column_means(ctx, x, d, mem.p, {0}, {off[1]}, {r}, cent.p);
+    if (!comm) {
+      if (off[1] > 0) seq_column_means(ctx, x, d, mem.p, {0}, {off[1]}, {r}, cent.p);
+      return;
+    }
+    // row-sharded: chain over the one row, then / its global size
+    DBuf<double> row(d);
+    std::vector<uint64_t> b, c;
+    std::vector<uint32_t> rr;
+    if (off[1] > 0) {
+      b.push_back(0);
+      c.push_back(off[1]);
+      rr.push_back(0);
+    }
+    seq_means(mem.p, b, c, rr, {(double)sizes[r]}, row.p, 1);
+    NB_CUDA(cudaMemcpyAsync(cent.p + (uint64_t)r * d, row.p, d * 8, cudaMemcpyDeviceToDevice, S()));
+    NB_CUDA(cudaStreamSynchronize(S()));
   }
 
   void map_eq(uint32_t r, uint32_t* out);
@@ -433,11 +522,28 @@ struct KMeans {
       k_far_argmin<<<grid_for(n, 256, 4096), 256, 0, S()>>>(dist.p, a.p, n, donor, u64s.p,
                                                             u64s.p + 1);
       note_launch(ctx, "k_far_argmin");
-      unsigned long long victim = 0;
-      NB_CUDA(cudaMemcpyAsync(&victim, u64s.p + 1, 8, cudaMemcpyDeviceToHost, S()));
+      unsigned long long best[2] = {0, 0};  // distance bits (0: none), local index
+      NB_CUDA(cudaMemcpyAsync(best, u64s.p, 16, cudaMemcpyDeviceToHost, S()));
       NB_CUDA(cudaStreamSynchronize(S()));
-      k_set_u32<<<1, 1, 0, S()>>>(a.p, victim, empty);
-      note_launch(ctx, "k_set_u32");
+      unsigned long long victim = best[1];
+      bool mine = true;
+      if (comm) {  // the farthest over all ranks (larger distance, then lower id)
+        unsigned long long cand[2] = {best[0], best[1] == ~0ull ? ~0ull : row0 + best[1]};
+        std::vector<unsigned long long> all(2 * (size_t)comm->world);
+        comm->allgather(cand, 16, all.data());
+        int win = -1;
+        for (int rk = 0; rk < comm->world; ++rk) {
+          const unsigned long long b = all[2 * rk], id = all[2 * rk + 1];
+          if (id == ~0ull) continue;
+          if (win < 0 || b > all[2 * win] || (b == all[2 * win] && id < all[2 * win + 1])) win = rk;
+        }
+        mine = win == comm->rank;
+        victim = best[1];
+      }
+      if (mine) {
+        k_set_u32<<<1, 1, 0, S()>>>(a.p, victim, empty);
+        note_launch(ctx, "k_set_u32");
+      }
       --sizes[donor];
       ++sizes[empty];
       NB_CUDA(cudaMemcpyAsync(sizes_d.p, sizes.data(), C * 4, cudaMemcpyHostToDevice, S()));
@@ -447,16 +553,13 @@ struct KMeans {
   }
 
   double quantization_error() {  // kmeans.hpp:148-154
-    dist.alloc(n);
-    k_point_sqdist<<<(unsigned)((n + 127) / 128), 128, 0, S()>>>(x, n, (uint32_t)d, cent.p, a.p,
-                                                                dist.p);
-    note_launch(ctx, "k_point_sqdist");
-    k_seq_sum<<<1, 256, 0, S()>>>(dist.p, n, scal.p);
-    note_launch(ctx, "k_seq_sum");
-    double acc = 0.0;
-    NB_CUDA(cudaMemcpyAsync(&acc, scal.p, 8, cudaMemcpyDeviceToHost, S()));
-    NB_CUDA(cudaStreamSynchronize(S()));
-    return acc / static_cast<double>(n);
+    dist.alloc(std::max<uint64_t>(n, 1));
+    if (n) {
+      k_point_sqdist<<<(unsigned)((n + 127) / 128), 128, 0, S()>>>(x, n, (uint32_t)d, cent.p,
+                                                                  a.p, dist.p);
+      note_launch(ctx, "k_point_sqdist");
+    }
+    return seq_sum(dist.p) / static_cast<double>(n_total);
   }
 };
 
@@ -473,37 +576,55 @@ void KMeans::map_eq(uint32_t r, uint32_t* out) {
   note_launch(ctx, "k_map_eq");
 }
 
-// Exact default_kmeans_tol (kmeans.hpp:157-161): one sequential chain.
-double default_tol_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d) {
+// Exact default_kmeans_tol (kmeans.hpp:157-161): one sequential chain (a
+// carry chain over the ranks when row-sharded).
+double default_tol_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
+                         Comm* comm = nullptr, uint64_t n_total = 0) {
   DBuf<double> o(1);
-  k_seq_sumsq<<<1, 1024, 0, ctx->stream>>>(x, n * d, o.p);
-  note_launch(ctx, "k_seq_sumsq");
+  auto run = [&](int carry) {
+    k_seq_sumsq<<<1, 1024, 0, ctx->stream>>>(x, n * d, o.p, carry);
+    note_launch(ctx, "k_seq_sumsq");
+  };
+  if (comm) comm->chain(o.p, 1, [&] { run(1); });
+  else run(0);
   double acc = 0.0;
   NB_CUDA(cudaMemcpyAsync(&acc, o.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
   NB_CUDA(cudaStreamSynchronize(ctx->stream));
-  return 1e-6 * (acc / static_cast<double>(n));
+  return 1e-6 * (acc / static_cast<double>(comm ? n_total : n));
 }
 
 // [lo, hi] bracket of default_kmeans_tol from an any-order parallel sum:
 // for N non-negative terms any summation order is within (N-1)u of the
 // exact sum, so the sequential result lies within a factor (1 +- g)^2.
 void default_tol_bracket(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
-                         double* lo, double* hi) {
+                         double* lo, double* hi, Comm* comm = nullptr, uint64_t n_total = 0) {
   const uint64_t N = n * d;
-  const unsigned blocks = grid_for(N, 256, 2048);
+  const unsigned blocks = grid_for(std::max<uint64_t>(N, 1), 256, 2048);
   DBuf<double> part(blocks);
-  k_par_sumsq<<<blocks, 256, 0, ctx->stream>>>(x, N, part.p);
-  note_launch(ctx, "k_par_sumsq");
+  NB_CUDA(cudaMemsetAsync(part.p, 0, blocks * 8, ctx->stream));
+  if (N) {
+    k_par_sumsq<<<blocks, 256, 0, ctx->stream>>>(x, N, part.p);
+    note_launch(ctx, "k_par_sumsq");
+  }
   std::vector<double> h(blocks);
   NB_CUDA(cudaMemcpyAsync(h.data(), part.p, blocks * 8, cudaMemcpyDeviceToHost, ctx->stream));
   NB_CUDA(cudaStreamSynchronize(ctx->stream));
   double s = 0.0;
   for (double v : h) s += v;
+  uint64_t NT = N + blocks, nn = n;
+  if (comm) {  // any order of any partial sums stays inside the bracket
+    std::vector<double> all(comm->world);
+    comm->allgather(&s, 8, all.data());
+    s = 0.0;
+    for (double v : all) s += v;
+    NT = n_total * d + (uint64_t)blocks * comm->world + comm->world;
+    nn = n_total;
+  }
   const double u = 0x1p-53;
-  const double g = (double)(N + blocks) * u * 1.0001;
+  const double g = (double)NT * u * 1.0001;
   const double slo = s * (1.0 - g) * (1.0 - g), shi = s * (1.0 + g) * (1.0 + g);
-  *lo = 1e-6 * (std::nextafter(slo, 0.0) / static_cast<double>(n));
-  *hi = 1e-6 * (std::nextafter(shi, INFINITY) / static_cast<double>(n));
+  *lo = 1e-6 * (std::nextafter(slo, 0.0) / static_cast<double>(nn));
+  *hi = 1e-6 * (std::nextafter(shi, INFINITY) / static_cast<double>(nn));
 }
 
 // kmeans.hpp:167-250
@@ -514,7 +635,16 @@ void lsh_init_dev(nomad_b200_ctx* ctx, KMeans& km, uint64_t seed) {
   HostRng rng(HostRng::stream_seed(seed, 0x6c7368 /* "lsh" */));
   // data mean, ascending i (kmeans.hpp:176-181)
   DBuf<double> mean(d);
-  seq_column_means(ctx, km.x, d, nullptr, {0}, {n}, {0}, mean.p);
+  {
+    std::vector<uint64_t> b, c;
+    std::vector<uint32_t> r;
+    if (n) {
+      b.push_back(0);
+      c.push_back(n);
+      r.push_back(0);
+    }
+    km.seq_means(nullptr, b, c, r, {(double)km.n_total}, mean.p, 1);
+  }
   // planes (kmeans.hpp:183-186)
   const uint64_t P = static_cast<uint64_t>(std::ceil(std::log2(4.0 * static_cast<double>(C))));
   if (P > 24) fail(kSize, "too many LSH planes (n_clusters too large)");
@@ -523,46 +653,54 @@ void lsh_init_dev(nomad_b200_ctx* ctx, KMeans& km, uint64_t seed) {
   DBuf<double> planes_d(P * d);
   NB_CUDA(cudaMemcpyAsync(planes_d.p, planes.data(), P * d * 8, cudaMemcpyHostToDevice, S));
   // codes + buckets in code order, members ascending (the std::map)
-  DBuf<uint32_t> codes(n);
-  k_lsh_hash<<<(unsigned)((n + 127) / 128), 128, 0, S>>>(km.x, n, (uint32_t)d, mean.p,
-                                                         planes_d.p, (uint32_t)P, codes.p);
-  note_launch(ctx, "k_lsh_hash");
+  DBuf<uint32_t> codes(std::max<uint64_t>(n, 1));
+  if (n) {
+    k_lsh_hash<<<(unsigned)((n + 127) / 128), 128, 0, S>>>(km.x, n, (uint32_t)d, mean.p,
+                                                           planes_d.p, (uint32_t)P, codes.p);
+    note_launch(ctx, "k_lsh_hash");
+  }
   const uint32_t L = 1u << P;
   DBuf<uint32_t> mem;
   std::vector<uint64_t> off;
   group_by_label(ctx, codes.p, n, L, mem, off);
+  // bucket sizes over every rank (the std::map's, kmeans.hpp:189-201)
+  std::vector<uint64_t> bsz(L);
+  for (uint32_t c = 0; c < L; ++c) bsz[c] = off[c + 1] - off[c];
+  if (km.comm) km.comm->allreduce_u64(bsz.data(), L);
   // rank: stable sort by size descending over ascending codes (kmeans.hpp:204-210)
   std::vector<uint32_t> ranked;
   for (uint32_t c = 0; c < L; ++c)
-    if (off[c + 1] > off[c]) ranked.push_back(c);
-  std::stable_sort(ranked.begin(), ranked.end(), [&](uint32_t a, uint32_t b) {
-    return off[a + 1] - off[a] > off[b + 1] - off[b];
-  });
+    if (bsz[c] > 0) ranked.push_back(c);
+  std::stable_sort(ranked.begin(), ranked.end(),
+                   [&](uint32_t a, uint32_t b) { return bsz[a] > bsz[b]; });
   const uint32_t seeded = std::min<uint32_t>(C, (uint32_t)ranked.size());
   NB_CUDA(cudaMemsetAsync(km.cent.p, 0, (uint64_t)C * d * 8, S));
   {
     std::vector<uint64_t> beg, cnt;
     std::vector<uint32_t> rows;
+    std::vector<double> div(C, 0.0);
     for (uint32_t r = 0; r < seeded; ++r) {
-      beg.push_back(off[ranked[r]]);
-      cnt.push_back(off[ranked[r] + 1] - off[ranked[r]]);
-      rows.push_back(r);
+      div[r] = (double)bsz[ranked[r]];
+      if (off[ranked[r] + 1] > off[ranked[r]]) {
+        beg.push_back(off[ranked[r]]);
+        cnt.push_back(off[ranked[r] + 1] - off[ranked[r]]);
+        rows.push_back(r);
+      }
     }
-    seq_column_means(ctx, km.x, d, mem.p, beg, cnt, rows, km.cent.p);  // kmeans.hpp:218-226
+    km.seq_means(mem.p, beg, cnt, rows, div, km.cent.p, C);  // kmeans.hpp:218-226
   }
   if (seeded < C) {  // kmeans.hpp:228-242 perturbation
-    km.dist.alloc(n);
-    k_point_sqdist<<<(unsigned)((n + 127) / 128), 128, 0, S>>>(km.x, n, (uint32_t)d, mean.p,
-                                                              nullptr, km.dist.p);
-    note_launch(ctx, "k_point_sqdist");
-    k_seq_sum<<<1, 256, 0, S>>>(km.dist.p, n, km.scal.p);
-    note_launch(ctx, "k_seq_sum");
-    double scale = 0.0;
-    NB_CUDA(cudaMemcpyAsync(&scale, km.scal.p, 8, cudaMemcpyDeviceToHost, S));
+    km.dist.alloc(std::max<uint64_t>(n, 1));
+    if (n) {
+      k_point_sqdist<<<(unsigned)((n + 127) / 128), 128, 0, S>>>(km.x, n, (uint32_t)d, mean.p,
+                                                                nullptr, km.dist.p);
+      note_launch(ctx, "k_point_sqdist");
+    }
+    double scale = km.seq_sum(km.dist.p);
     std::vector<double> c((uint64_t)C * d);
     NB_CUDA(cudaMemcpyAsync(c.data(), km.cent.p, c.size() * 8, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
-    scale = std::sqrt(scale / static_cast<double>(n)) * 1e-3 + 1e-12;
+    scale = std::sqrt(scale / static_cast<double>(km.n_total)) * 1e-3 + 1e-12;
     uint64_t source = 0;
     for (uint64_t r = seeded; r < C; ++r) {
       for (uint64_t j = 0; j < d; ++j) c[r * d + j] = c[source * d + j] + scale * rng.gaussian();
@@ -608,7 +746,7 @@ uint64_t kmeans_em_dev(nomad_b200_ctx* ctx, KMeans& km, uint64_t max_iters, doub
     } else if (!(max_move < tol_hi)) {
       below = false;
     } else {
-      tol_exact = default_tol_exact(ctx, km.x, km.n, km.d);
+      tol_exact = default_tol_exact(ctx, km.x, km.n, km.d, km.comm, km.n_total);
       have_exact = true;
       below = max_move < tol_exact;
     }
@@ -618,6 +756,35 @@ uint64_t kmeans_em_dev(nomad_b200_ctx* ctx, KMeans& km, uint64_t max_iters, doub
     }
   }
   return it;
+}
+
+// Row-sharded lsh_init + kmeans_em (fit's call, optimizer.hpp:336-339; tol
+// < 0: default_kmeans_tol) for this rank's rows [row0, row0 + n).
+void sharded_kmeans(nomad_b200_ctx* ctx, Comm* comm, XPtr x, uint64_t n, uint64_t row0,
+                    uint64_t n_total, uint64_t d, uint32_t C, uint64_t seed, uint64_t max_iters,
+                    double tol, std::vector<uint32_t>& a_local, std::vector<double>& cent,
+                    std::vector<uint32_t>& sizes) {
+  if (C < 2 || C > n_total)
+    fail(kParameter, "cluster count must be in [2, n]; got " + std::to_string(C));
+  KMeans km(ctx, x, n, d, C);
+  km.comm = comm;
+  km.row0 = row0;
+  km.n_total = n_total;
+  lsh_init_dev(ctx, km, seed);
+  if (tol >= 0.0) {
+    kmeans_em_dev(ctx, km, max_iters, tol, tol, false, nullptr);
+  } else {
+    double lo = 0.0, hi = 0.0;
+    default_tol_bracket(ctx, x, n, d, &lo, &hi, comm, n_total);
+    kmeans_em_dev(ctx, km, max_iters, lo, hi, true, nullptr);
+  }
+  if (max_iters == 0) km.recompute_sizes();
+  a_local.resize(n);
+  cent.resize((size_t)C * d);
+  NB_CUDA(cudaMemcpyAsync(a_local.data(), km.a.p, n * 4, cudaMemcpyDeviceToHost, km.S()));
+  NB_CUDA(cudaMemcpyAsync(cent.data(), km.cent.p, cent.size() * 8, cudaMemcpyDeviceToHost, km.S()));
+  NB_CUDA(cudaStreamSynchronize(km.S()));
+  sizes = km.sizes;
 }
 
 }  // namespace nb

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <cub/cub.cuh>
 
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
     bool pending = t < W.draws;
     const uint32_t i = R.draw_base[w] + t;  // global draw index
     const uint32_t* pr = R.pred + (size_t)i * T;
-    uint32_t jj = 0, spins = 0;
+    uint32_t jj = 0, spins = 0, nap = 64;
     while (__any_sync(0xffffffffu, pending)) {
       if (!pending) continue;
       bool ready = true;
@@ -288,14 +289,16 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
       if (!ready) {
         // watchdog: a predecessor is always an earlier draw of a running
         // warp, so this only fires on a schedule bug; report, never hang
-        if (++spins > (1u << 25)) {
+        if (*reinterpret_cast<volatile uint32_t*>(R.stall) || ++spins > (1u << 22)) {
           atomicExch(R.stall, 1u);
           pending = false;
           continue;
         }
-        __nanosleep(32);
+        __nanosleep(nap);  // exponential backoff (see the warp form)
+        nap = min(nap * 2, 2048u);
         continue;
       }
+      nap = 64;
       __threadfence();  // the predecessors' position writes before our reads
       const uint32_t head = R.heads[i];
       const uint32_t* tails = R.tails + (size_t)i * s;
@@ -440,16 +443,18 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
       {
         const uint32_t q = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
         const volatile uint8_t* dn = R.done + R.draw_base[w];
-        uint32_t spins = 0;
-        bool abort = false;
+        uint32_t spins = 0, nap = 64;
+        bool abort = false, ok = q == 0xFFFFFFFFu;
         for (;;) {
-          const bool ok = q == 0xFFFFFFFFu || dn[q] != 0;
+          if (!ok) ok = dn[q] != 0;  // a lane stops polling once its predecessor is done
           if (__all_sync(FULL, ok)) break;
-          if (*reinterpret_cast<volatile uint32_t*>(R.stall) || ++spins > (1u << 25)) {
+          if (*reinterpret_cast<volatile uint32_t*>(R.stall) || ++spins > (1u << 22)) {
             abort = true;  // watchdog (a schedule bug): report, never hang
             break;
           }
-          __nanosleep(32);
+          // exponential backoff: thousands of waiting warps must not saturate L2
+          __nanosleep(nap);
+          nap = min(nap * 2, 2048u);
         }
         if (__any_sync(FULL, abort)) {
           if (lane == 0) atomicExch(R.stall, 1u);
@@ -646,7 +651,10 @@ void launch_replay_deps(const ReplayDev& R, const SgdParams& P, uint32_t n_loc, 
   if (n_loc) k_replay_pred<<<blocks_for(n_loc, 256), 256, 0, st>>>(R, n_loc);
 }
 
-bool dataflow_warp_form(uint32_t k, uint32_t s) { return 1 + k + s <= 32; }
+bool dataflow_warp_form(uint32_t k, uint32_t s) {
+  static const bool thread_form = std::getenv("NOMAD_B200_DATAFLOW_THREAD") != nullptr;
+  return 1 + k + s <= 32 && !thread_form;
+}
 uint32_t dataflow_draws_per_chunk(uint32_t k, uint32_t s) {
   return dataflow_warp_form(k, s) ? kDfBatch : 32;
 }
