@@ -280,7 +280,35 @@ def main():
     stream = torch.cuda.Stream(device=local)
     ctx.set_stream(stream.cuda_stream)
     index = {}
-    if args.graph == "knn":
+    nid = nid64 = nidr = nidx = None
+    if world > 1:
+        obj = [tuple(nbx.nccl_unique_id() for _ in range(4)) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid, nid64, nidr, nidx = obj[0]
+    if args.graph == "knn" and world > 1:
+        # row-sharded build: this rank generates and holds only its rows; LSH
+        # + Lloyd with the ascending-id sums carried rank to rank (bit-identical
+        # to one GPU), rows moved once to their cluster's owner, kNN lists for
+        # the owned clusters only
+        if bf and args.knn_mode != "bf16":
+            args.knn_mode = "bf16"
+        r0, r1 = n * rank // world, n * (rank + 1) // world
+        xl = nbx.generate_mixture_rows(r0, r1 - r0, d, blobs, 10.0, 42, ctx=ctx,
+                                       dtype="bf16" if bf else "f32")
+        torch.cuda.synchronize()
+        t_a = time.perf_counter()
+        cl, g = nbx.index_sharded(xl, r0, n, ncl, 7, W, k=k, knn_mode=args.knn_mode, rank=rank,
+                                  world_size=world, nccl_id=nidx, ctx=ctx)
+        t_d = time.perf_counter()
+        del xl
+        torch.cuda.empty_cache()
+        a, offsets, nb = cl.assignment, g.offsets, g.neighbors
+        init = np.random.default_rng(1234).standard_normal((n, 2))
+        index = {"row_sharded_build_s": round(t_d - t_a, 3), "knn_mode": args.knn_mode,
+                 "rows_per_rank": r1 - r0,
+                 "per_rank_dataset_bytes": (r1 - r0) * d * (2 if bf else 4),
+                 "cluster_sizes_min_max": [int(cl.sizes.min()), int(cl.sizes.max())]}
+    elif args.graph == "knn":
         # the hot-path index build on this GPU: lsh_init + kmeans_em identical on
         # every rank (same seeds, deterministic kernels), kNN lists only for this
         # rank's clusters; then the dataset is released
@@ -349,11 +377,6 @@ def main():
                  "knn_roofline": index_roof}
     else:
         a, offsets, nb, init = synthetic_index(n, ncl, k)
-    nid = nid64 = None
-    if world > 1:
-        obj = [(nbx.nccl_unique_id(), nbx.nccl_unique_id()) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid, nid64 = obj[0]
     cfg = nbx.TrainConfig(epochs=200, workers=W, seed=7, sgd_mode=args.sgd_mode, k=k)
     graph = nbx.KnnGraph(n, k, offsets, nb, np.zeros(0))
     clusters = nbx.ClusterAssignment(a, ncl, d, np.zeros(0), np.zeros(0))
@@ -515,7 +538,7 @@ def main():
     if args.sgd_mode == "hogwild" and args.replay_epochs > 0:
         cfgr = nbx.TrainConfig(epochs=200, workers=W, seed=7, sgd_mode="replay", k=k)
         trr = nbx.Trainer(graph, clusters, init, cfgr, rank=rank, world_size=world,
-                          nccl_id=nid64 if world > 1 else None, ctx=ctx)
+                          nccl_id=nidr if world > 1 else None, ctx=ctx)
         trr.run(1)
         if world > 1:
             dist.barrier()

@@ -261,8 +261,11 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
   const double* cm = P.gcells ? P.cm3 : cms;
   __syncthreads();
   const double M = (double)P.m_total;
-  const uint32_t lane = threadIdx.x & 31;
   const uint32_t stride = 2 + k + s;
+  // (fallback for 1 + k + s > 32) warps claim 32 consecutive draws of a
+  // worker in worker-interleaved order, one per lane; claims follow draw
+  // order, so a draw only waits on draws already claimed by running warps
+  const uint32_t lane = threadIdx.x & 31;
   for (;;) {
     uint32_t c = 0;
     if (lane == 0) c = atomicAdd(R.ticket, 1u);
@@ -302,7 +305,16 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
       __threadfence();  // the predecessors' position writes before our reads
       const uint32_t head = R.heads[i];
       const uint32_t* tails = R.tails + (size_t)i * s;
-      const double2 h = ldpos(P.pos + head);
+      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
+      const uint32_t* nb = P.ell + (size_t)head * P.kpad;
+      // every slot's position (head, neighbours, tails), loads in flight together
+      uint32_t sid[1 + 64 + 16];
+      double2 sp[1 + 64 + 16];
+      const uint32_t nsl = 1 + cnt + s;
+      for (uint32_t u = 0; u < nsl; ++u)
+        sid[u] = u == 0 ? head : (u <= cnt ? nb[u - 1] : tails[u - 1 - cnt]);
+      for (uint32_t u = 0; u < nsl; ++u) sp[u] = ldpos(P.pos + sid[u]);
+      const double2 h = sp[0];
       // noise terms (objective.hpp:113-145)
       uint32_t own = 0;
       double lm = W.local_mass;
@@ -322,18 +334,16 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
       const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
       double qsum = 0.0;
       for (uint32_t q = 0; q < s; ++q) {
-        const double2 o = ldpos(P.pos + tails[q]);
+        const double2 o = sp[1 + cnt + q];
         qsum = __dadd_rn(qsum, cauchy_rn(h.x, h.y, o.x, o.y));
       }
       const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
       // attraction (objective.hpp:197-213)
-      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
-      const uint32_t* nb = P.ell + (size_t)head * P.kpad;
       const double* wrow = wt + cnt * k;
       double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
       double gn[2 * 64];
       for (uint32_t j = 0; j < cnt; ++j) {
-        const double2 o = ldpos(P.pos + nb[j]);
+        const double2 o = sp[1 + j];
         const double q = cauchy_rn(h.x, h.y, o.x, o.y);
         const double wj = wrow[j];
         const double qb = __dadd_rn(q, bg);
@@ -353,7 +363,7 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
       // negative repulsion (objective.hpp:216-226)
       double gm[2 * 16];
       for (uint32_t q = 0; q < s; ++q) {
-        const double2 o = ldpos(P.pos + tails[q]);
+        const double2 o = sp[1 + cnt + q];
         const double qn = cauchy_rn(h.x, h.y, o.x, o.y);
         const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
         const double dx = __dsub_rn(h.x, o.x), dy = __dsub_rn(h.y, o.y);
@@ -375,21 +385,27 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
       }
       P.loss_slot[i] = loss;
       // apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails
+      // updates in slot order on the preloaded positions; a point in several
+      // slots continues from its first slot's running value, and every
+      // distinct point is stored once at the end
       const double st = P.step;
-      uint32_t u = 0;
-      auto apply = [&](uint32_t p, double ax, double ay) {
-        double2 v = ldpos(P.pos + p);
+      const uint32_t na = P.head_only ? 1 : nsl;
+      for (uint32_t u = 0; u < na; ++u) {
+        const double ax = u == 0 ? gx : (u <= cnt ? gn[2 * (u - 1)] : gm[2 * (u - 1 - cnt)]);
+        const double ay = u == 0 ? gy : (u <= cnt ? gn[2 * (u - 1) + 1] : gm[2 * (u - 1 - cnt) + 1]);
+        uint32_t f = 0;
+        while (sid[f] != sid[u]) ++f;
+        double2 v = sp[f];
         v.x = __dsub_rn(v.x, __dmul_rn(st, ax));
         v.y = __dsub_rn(v.y, __dmul_rn(st, ay));
-        __stcg(P.pos + p, v);
+        sp[f] = v;
         if (diverged(v.x, v.y))
-          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | p);
-        ++u;
-      };
-      apply(head, gx, gy);
-      if (!P.head_only) {
-        for (uint32_t j = 0; j < cnt; ++j) apply(nb[j], gn[2 * j], gn[2 * j + 1]);
-        for (uint32_t q = 0; q < s; ++q) apply(tails[q], gm[2 * q], gm[2 * q + 1]);
+          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | sid[u]);
+      }
+      for (uint32_t u = 0; u < na; ++u) {
+        uint32_t f = 0;
+        while (sid[f] != sid[u]) ++f;
+        if (f == u) __stcg(P.pos + sid[u], sp[u]);
       }
       __threadfence();  // our writes before the flag
       *reinterpret_cast<volatile uint8_t*>(R.done + i) = 1;
@@ -429,15 +445,20 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t stride = 2 + k + s;
   const double st = P.step;
-  for (;;) {
-    uint32_t c = 0;
-    if (lane == 0) c = atomicAdd(R.ticket, 1u);
-    c = __shfl_sync(FULL, c, 0);
-    if (c >= R.total_chunks) break;
-    const uint32_t w = c % R.nwl;
+  // Static round-robin: warp g runs the worker-interleaved draw sequence
+  // g, g + nwarps, ... in order. Every draw's predecessors are earlier
+  // draws, so the smallest unfinished draw is always runnable on its
+  // (resident: cooperative launch) warp — no claim counter, and a waiting
+  // draw holds up only its own warp.
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint64_t total = (uint64_t)R.nwl * R.max_draws;
+  for (uint64_t c = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < total;
+       c += nwarps) {
+    const uint32_t w = (uint32_t)(c % R.nwl);
     const WorkerDev W = P.workers[w];
-    const uint32_t t0 = (c / R.nwl) * kDfBatch;
-    for (uint32_t t = t0; t < t0 + kDfBatch && t < W.draws; ++t) {
+    {
+      const uint32_t t = (uint32_t)(c / R.nwl);
+      if (t >= W.draws) continue;
       const uint32_t i = R.draw_base[w] + t;
       // ---- wait until every predecessor is done
       {
@@ -670,7 +691,11 @@ void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblock
   auto kern = wf ? k_sgd_dataflow_warp : k_sgd_dataflow;
   if (sm > 48 * 1024)
     NB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  kern<<<nblocks, 256, sm, st>>>(P, R);
+  // every block resident at once (the static schedule relies on it)
+  SgdParams Pc = P;
+  ReplayDev Rc = R;
+  void* args[] = {&Pc, &Rc};
+  NB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(nblocks), dim3(256), args, sm, st));
 }
 
 uint32_t dataflow_resident_blocks(size_t smem, int sm_count, uint32_t k, uint32_t s) {

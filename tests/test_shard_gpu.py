@@ -22,7 +22,7 @@ def _slices(n, G, rng):
 def test_sharded_index_equals_one_gpu(ctx, G, dtype, mode):
     import torch
     import paper_2505_15511_b200 as nb
-    n, d, blobs, C, W = 6000, 32, 10, 8, 4
+    n, d, blobs, C, W = 6000, 32, 10, 8, 2 * G
     x = nb.generate_mixture(n, d, blobs, 10.0, 42, ctx=ctx, dtype=dtype)
     c1 = nb.kmeans_em_default_tol(x, nb.lsh_init(x, C, 7, ctx=ctx), 100, ctx=ctx)
     g1 = nb.build_knn(x, c1, 15, mode=mode, ctx=ctx)
