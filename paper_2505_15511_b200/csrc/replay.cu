@@ -222,22 +222,43 @@ __global__ void k_replay_pred(ReplayDev R, uint32_t n_loc) {
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n_loc) return;
   const uint32_t b = R.toff[v], e = R.toff[v + 1];
-  unsigned long long* L = R.tlist + b;
+  unsigned long long* G = R.tlist + b;
   const uint32_t m = e - b;
-  // insertion sort in place (segments are short: ~(1 + k + s) touches per point)
+  const uint32_t base = R.pt_base[v];  // draw base of the point's worker
+  constexpr uint32_t LM = 48;
+  if (m <= LM) {  // the usual case (~1 + k + s touches per point): sorted locally
+    unsigned long long L[LM];
+    for (uint32_t a = 0; a < m; ++a) L[a] = G[a];
+    for (uint32_t a = 1; a < m; ++a) {
+      const unsigned long long x = L[a];
+      uint32_t c = a;
+      while (c > 0 && L[c - 1] > x) {
+        L[c] = L[c - 1];
+        --c;
+      }
+      L[c] = x;
+    }
+    uint32_t prev = 0xFFFFFFFFu;
+    for (uint32_t a = 0; a < m; ++a) {
+      const uint32_t t = (uint32_t)(L[a] >> 8), j = (uint32_t)(L[a] & 0xFF);
+      R.pred[(size_t)(base + t) * R.T + j] = prev;
+      prev = t;
+    }
+    return;
+  }
+  // long segment (a point touched by many draws): insertion sort in place
   for (uint32_t a = 1; a < m; ++a) {
-    const unsigned long long x = L[a];
+    const unsigned long long x = G[a];
     uint32_t c = a;
-    while (c > 0 && L[c - 1] > x) {
-      L[c] = L[c - 1];
+    while (c > 0 && G[c - 1] > x) {
+      G[c] = G[c - 1];
       --c;
     }
-    L[c] = x;
+    G[c] = x;
   }
-  const uint32_t base = R.pt_base[v];  // draw base of the point's worker
   uint32_t prev = 0xFFFFFFFFu;
   for (uint32_t a = 0; a < m; ++a) {
-    const uint32_t t = (uint32_t)(L[a] >> 8), j = (uint32_t)(L[a] & 0xFF);
+    const uint32_t t = (uint32_t)(G[a] >> 8), j = (uint32_t)(G[a] & 0xFF);
     R.pred[(size_t)(base + t) * R.T + j] = prev;
     prev = t;
   }
