@@ -152,11 +152,13 @@ __global__ void k_replay_map(ReplayDev R, SgdParams P, const uint32_t* pool,
   if (rej) atomicOr(R.reject + w, 1u);
 }
 
-// Touch list of every draw (head, neighbours in list order, tails; a point
-// touched twice by one draw is listed once) and per-point touch counts.
+// Touch list of every draw as sort keys: slot j of draw i (0 head, then the
+// neighbours in list order, then the tails; a point touched twice by one draw
+// is listed once) -> key = its local point, value = i * T + j; plus the
+// epoch's edge-updates per worker.
 __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t T = R.T, s = R.s, k = P.k;
+  const uint32_t T = R.T, s = R.s, k = P.k, NONE = R.n_loc;
   // edge-updates of the epoch per worker, |N(head)| + s per draw (warp-aggregated)
   {
     uint32_t w = 0, e = 0;
@@ -171,12 +173,15 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
   }
   if (i >= total) return;
   const uint32_t h = R.heads[i];
-  uint32_t* tl = R.touch + (size_t)i * T;
-  for (uint32_t j = 0; j < T; ++j) R.pred[(size_t)i * T + j] = 0xFFFFFFFFu;
+  uint32_t* key = R.tkey + (size_t)i * T;
+  uint32_t* val = R.tval + (size_t)i * T;
+  for (uint32_t j = 0; j < T; ++j) {
+    R.pred[(size_t)i * T + j] = 0xFFFFFFFFu;
+    val[j] = i * T + j;
+  }
   const uint32_t cnt = P.ncnt ? P.ncnt[h] : k;
   const uint32_t* nb = P.ell + (size_t)h * P.kpad;
-  tl[0] = h;
-  atomicAdd(R.tcount + h, 1u);
+  key[0] = h;
   uint32_t j = 1;
   for (; j <= cnt; ++j) {
     // build_knn's lists hold distinct points other than the head; a caller's
@@ -184,84 +189,28 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
     const uint32_t v = nb[j - 1];
     bool dup = v == h;
     for (uint32_t a = 0; a + 1 < j && !dup; ++a) dup = nb[a] == v;
-    tl[j] = dup ? 0xFFFFFFFFu : v;
-    if (!dup) atomicAdd(R.tcount + v, 1u);
+    key[j] = dup ? NONE : v;
   }
-  for (; j < 1 + k; ++j) tl[j] = 0xFFFFFFFFu;
+  for (; j < 1 + k; ++j) key[j] = NONE;
   const uint32_t* tails = R.tails + (size_t)i * s;
   for (uint32_t q = 0; q < s; ++q) {
     const uint32_t v = tails[q];
     bool dup = v == h;
     for (uint32_t a = 0; a < cnt && !dup; ++a) dup = nb[a] == v;
     for (uint32_t a = 0; a < q && !dup; ++a) dup = tails[a] == v;
-    tl[1 + k + q] = dup ? 0xFFFFFFFFu : v;
-    if (!dup) atomicAdd(R.tcount + v, 1u);
+    key[1 + k + q] = dup ? NONE : v;
   }
 }
 
-// Scatter (t << 8 | slot) into each touched point's segment.
-__global__ void k_replay_scatter(ReplayDev R, uint32_t total) {
-  const uint32_t nwl = R.nwl;
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  // worker of draw i (draw_base is ascending, nwl small)
-  uint32_t w = 0;
-  while (w + 1 < nwl && R.draw_base[w + 1] <= i) ++w;
-  const uint32_t t = i - R.draw_base[w];
-  const uint32_t* tl = R.touch + (size_t)i * R.T;
-  for (uint32_t j = 0; j < R.T; ++j) {
-    const uint32_t v = tl[j];
-    if (v == 0xFFFFFFFFu) continue;
-    const uint32_t pos = R.toff[v] + atomicAdd(R.tcount + v, 1u);
-    R.tlist[pos] = ((unsigned long long)t << 8) | j;
-  }
-}
-
-// Per point: sort its touches by draw order, link each to its predecessor.
-__global__ void k_replay_pred(ReplayDev R, uint32_t n_loc) {
-  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= n_loc) return;
-  const uint32_t b = R.toff[v], e = R.toff[v + 1];
-  unsigned long long* G = R.tlist + b;
-  const uint32_t m = e - b;
-  const uint32_t base = R.pt_base[v];  // draw base of the point's worker
-  constexpr uint32_t LM = 48;
-  if (m <= LM) {  // the usual case (~1 + k + s touches per point): sorted locally
-    unsigned long long L[LM];
-    for (uint32_t a = 0; a < m; ++a) L[a] = G[a];
-    for (uint32_t a = 1; a < m; ++a) {
-      const unsigned long long x = L[a];
-      uint32_t c = a;
-      while (c > 0 && L[c - 1] > x) {
-        L[c] = L[c - 1];
-        --c;
-      }
-      L[c] = x;
-    }
-    uint32_t prev = 0xFFFFFFFFu;
-    for (uint32_t a = 0; a < m; ++a) {
-      const uint32_t t = (uint32_t)(L[a] >> 8), j = (uint32_t)(L[a] & 0xFF);
-      R.pred[(size_t)(base + t) * R.T + j] = prev;
-      prev = t;
-    }
-    return;
-  }
-  // long segment (a point touched by many draws): insertion sort in place
-  for (uint32_t a = 1; a < m; ++a) {
-    const unsigned long long x = G[a];
-    uint32_t c = a;
-    while (c > 0 && G[c - 1] > x) {
-      G[c] = G[c - 1];
-      --c;
-    }
-    G[c] = x;
-  }
-  uint32_t prev = 0xFFFFFFFFu;
-  for (uint32_t a = 0; a < m; ++a) {
-    const uint32_t t = (uint32_t)(G[a] >> 8), j = (uint32_t)(G[a] & 0xFF);
-    R.pred[(size_t)(base + t) * R.T + j] = prev;
-    prev = t;
-  }
+// After the stable sort by point: each touch's predecessor is the previous
+// entry of the same point (draw order is kept inside a point's run).
+__global__ void k_replay_pred(ReplayDev R, uint64_t items) {
+  const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (e >= items) return;
+  const uint32_t v = R.tkey[e];
+  if (v == R.n_loc || e == 0 || R.tkey[e - 1] != v) return;
+  const uint32_t prev_draw = R.tval[e - 1] / R.T;  // global draw index
+  R.pred[R.tval[e]] = prev_draw - R.pt_base[v];     // the worker's draw t
 }
 
 // ------------------------------------------------------ dataflow SGD
@@ -674,23 +623,34 @@ void launch_replay_map(const ReplayDev& R, const SgdParams& P, const uint32_t* p
   k_replay_map<<<grid, 256, 0, st>>>(R, P, pool, pool_off);
 }
 
-size_t replay_scan_bytes(uint32_t n_loc) {
-  size_t b = 0;
-  NB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                        (int64_t)n_loc + 1));
+static int bits_for(uint32_t v) {
+  int b = 1;
+  while (b < 32 && (v >> b)) ++b;
   return b;
 }
 
-void launch_replay_deps(const ReplayDev& R, const SgdParams& P, uint32_t n_loc, void* scan_tmp,
-                        size_t scan_bytes, cudaStream_t st) {
+size_t replay_sort_bytes(uint64_t items, uint32_t n_loc) {
+  size_t b = 0;
+  NB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                          (uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)items,
+                                          0, bits_for(n_loc)));
+  return b;
+}
+
+void launch_replay_deps(const ReplayDev& R, const SgdParams& P, void* sort_tmp, size_t sort_bytes,
+                        cudaStream_t st) {
   const uint32_t total = R.total_draws;
-  NB_CUDA(cudaMemsetAsync(R.tcount, 0, ((size_t)n_loc + 1) * 4, st));
-  if (total) k_replay_touch<<<blocks_for(total, 256), 256, 0, st>>>(R, P, total);
-  NB_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, R.tcount, R.toff,
-                                        (int64_t)n_loc + 1, st));
-  NB_CUDA(cudaMemsetAsync(R.tcount, 0, ((size_t)n_loc + 1) * 4, st));
-  if (total) k_replay_scatter<<<blocks_for(total, 256), 256, 0, st>>>(R, total);
-  if (n_loc) k_replay_pred<<<blocks_for(n_loc, 256), 256, 0, st>>>(R, n_loc);
+  const uint64_t items = (uint64_t)total * R.T;
+  if (!total) return;
+  k_replay_touch<<<blocks_for(total, 256), 256, 0, st>>>(R, P, total);
+  // stable LSD radix sort by point over the draw-ordered touches
+  size_t b = sort_bytes;
+  NB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp, b, R.tkey, R.tkey2, R.tval, R.tval2,
+                                          (int64_t)items, 0, bits_for(R.n_loc), st));
+  ReplayDev Rs = R;
+  Rs.tkey = R.tkey2;
+  Rs.tval = R.tval2;
+  k_replay_pred<<<blocks_for(items, 256), 256, 0, st>>>(Rs, items);
 }
 
 bool dataflow_warp_form(uint32_t k, uint32_t s) {

@@ -45,11 +45,13 @@ struct ReplayDev {
   unsigned long long* words;   // raw tempered words, worker-major
   uint32_t* heads;             // per draw: local head id
   uint32_t* tails;             // per draw: s local tail ids
-  uint32_t* touch;             // per draw: T local point ids (0xFFFFFFFF: none / duplicate)
+  uint32_t* tkey;              // per draw and slot: the slot's local point (n_loc: none /
+                               // a repeat within the draw); sorted in place by point
+  uint32_t* tval;              // per draw and slot: its flat index i * T + slot
+  uint32_t* tkey2;             // radix-sort buffers
+  uint32_t* tval2;
   uint32_t* pred;              // per draw and slot: latest earlier draw touching it (none: ~0)
-  uint32_t* tcount;            // per local point: touches this epoch (then a fill cursor)
-  uint32_t* toff;              // per local point + 1: exclusive scan of tcount
-  unsigned long long* tlist;   // per touch: (t << 8) | slot, grouped by point
+  uint32_t n_loc;              // local points (the "none" key)
   uint32_t* reject;            // per worker: a draw hit the rejection branch
   unsigned long long* edges;   // per worker: sum over draws of |N(head)| + s
   uint8_t* done;               // per draw: completed
@@ -63,10 +65,10 @@ struct ReplayDev {
 void launch_mt_words(const ReplayDev& R, const uint64_t* counts, cudaStream_t st);
 void launch_replay_map(const ReplayDev& R, const SgdParams& P, const uint32_t* pool,
                        const uint32_t* pool_off, cudaStream_t st);
-// touch lists + per-point counts, scatter, per-point sort -> pred
-void launch_replay_deps(const ReplayDev& R, const SgdParams& P, uint32_t n_loc, void* scan_tmp,
-                        size_t scan_bytes, cudaStream_t st);
-size_t replay_scan_bytes(uint32_t n_loc);
+// touch lists -> stable sort by point (draw order kept inside a point) -> pred
+void launch_replay_deps(const ReplayDev& R, const SgdParams& P, void* sort_tmp, size_t sort_bytes,
+                        cudaStream_t st);
+size_t replay_sort_bytes(uint64_t items, uint32_t n_loc);
 void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
                          cudaStream_t st);
 uint32_t dataflow_resident_blocks(size_t smem, int sm_count, uint32_t k, uint32_t s);

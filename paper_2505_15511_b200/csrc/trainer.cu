@@ -93,11 +93,11 @@ struct RankTrainer {
   // the rejection fallback
   DBuf<MtState> mt_a, mt_b;
   DBuf<uint64_t> wcount, wbase;
-  DBuf<unsigned long long> words, tlist, redges;
-  DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, rtouch, rpred, tcount, toff, reject,
+  DBuf<unsigned long long> words, redges;
+  DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, tkey, tval, tkey2, tval2, rpred, reject,
       ticket, pt_base, stall;
-  DBuf<uint8_t> rdone, scan_tmp;
-  size_t scan_bytes = 0;
+  DBuf<uint8_t> rdone, sort_tmp;
+  size_t sort_bytes = 0;
   uint32_t df_blocks = 0, total_draws = 0, max_draws = 0;
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
@@ -429,20 +429,21 @@ struct RankTrainer {
     words.alloc(std::max<uint64_t>(wacc, 1));
     rheads.alloc(D);
     rtails.alloc(D * s);
-    rtouch.alloc(D * T);
+    if (D * T >= 0xFFFFFFFFull) fail(kSize, "replay touches per rank exceed 2^32");
+    tkey.alloc(D * T);
+    tval.alloc(D * T);
+    tkey2.alloc(D * T);
+    tval2.alloc(D * T);
     rpred.alloc(D * T);
-    tlist.alloc(D * T);
     rdone.alloc(D);
     loss_slot.alloc(D);
-    tcount.alloc(orig_of.size() + 1);
-    toff.alloc(orig_of.size() + 1);
     reject.alloc(std::max<uint32_t>(nwl, 1));
     redges.alloc(std::max<uint32_t>(nwl, 1));
     ticket.alloc(1);
     stall.alloc(1);
     NB_CUDA(cudaMemsetAsync(stall.p, 0, 4, S));
-    scan_bytes = replay_scan_bytes((uint32_t)orig_of.size());
-    scan_tmp.alloc(std::max<size_t>(scan_bytes, 1));
+    sort_bytes = replay_sort_bytes(D * T, (uint32_t)orig_of.size());
+    sort_tmp.alloc(std::max<size_t>(sort_bytes, 1));
   }
 
   ReplayDev replay_dev() {
@@ -457,11 +458,12 @@ struct RankTrainer {
     R.words = words.p;
     R.heads = rheads.p;
     R.tails = rtails.p;
-    R.touch = rtouch.p;
+    R.tkey = tkey.p;
+    R.tval = tval.p;
+    R.tkey2 = tkey2.p;
+    R.tval2 = tval2.p;
     R.pred = rpred.p;
-    R.tcount = tcount.p;
-    R.toff = toff.p;
-    R.tlist = tlist.p;
+    R.n_loc = (uint32_t)orig_of.size();
     R.reject = reject.p;
     R.edges = redges.p;
     R.done = rdone.p;
@@ -526,7 +528,7 @@ struct RankTrainer {
     const bool force = std::getenv("NOMAD_B200_REPLAY_HOST_DRAWS") != nullptr;
     for (uint32_t wl = 0; wl < nwl; ++wl)
       if (rj[wl] || force) host_draws(wl);
-    launch_replay_deps(R, P, (uint32_t)orig_of.size(), scan_tmp.p, scan_bytes, S);
+    launch_replay_deps(R, P, sort_tmp.p, sort_bytes, S);
     launched("k_replay_deps");
     if (!df_blocks)
       df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
