@@ -26,7 +26,7 @@ struct NcclComm : Comm {
     if (c) ncclCommDestroy(c);
   }
   void allreduce_u64(uint64_t* v, size_t n) override {
-    if (!n) return;
+    if (!n || world == 1) return;
     DBuf<uint64_t> d(n);
     NB_CUDA(cudaMemcpyAsync(d.p, v, n * 8, cudaMemcpyHostToDevice, stream));
     NB_NCCL2(ncclAllReduce(d.p, d.p, n, ncclUint64, ncclSum, c, stream));
@@ -37,11 +37,17 @@ struct NcclComm : Comm {
     if (rank == 0) NB_CUDA(cudaMemsetAsync(dev, 0, n * 8, stream));
     else NB_NCCL2(ncclRecv(dev, n, ncclDouble, rank - 1, c, stream));
     step();
-    if (rank + 1 < world) NB_NCCL2(ncclSend(dev, n, ncclDouble, rank + 1, c, stream));
-    NB_NCCL2(ncclBroadcast(dev, dev, n, ncclDouble, world - 1, c, stream));
+    if (world > 1) {
+      if (rank + 1 < world) NB_NCCL2(ncclSend(dev, n, ncclDouble, rank + 1, c, stream));
+      NB_NCCL2(ncclBroadcast(dev, dev, n, ncclDouble, world - 1, c, stream));
+    }
     NB_CUDA(cudaStreamSynchronize(stream));
   }
   void allgather(const void* mine, size_t bytes, void* all) override {
+    if (world == 1) {
+      std::memcpy(all, mine, bytes);
+      return;
+    }
     DBuf<uint8_t> a(std::max<size_t>(bytes, 1)), b(std::max<size_t>(bytes * world, 1));
     NB_CUDA(cudaMemcpyAsync(a.p, mine, bytes, cudaMemcpyHostToDevice, stream));
     NB_NCCL2(ncclAllGather(a.p, b.p, bytes, ncclChar, c, stream));
@@ -50,6 +56,14 @@ struct NcclComm : Comm {
   }
   void alltoallv(const void* send, const uint64_t* soff, void* recv,
                  const uint64_t* roff) override {
+    if (world == 1) {
+      if (soff[1] > soff[0])
+        NB_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + roff[0],
+                                static_cast<const char*>(send) + soff[0], soff[1] - soff[0],
+                                cudaMemcpyDeviceToDevice, stream));
+      NB_CUDA(cudaStreamSynchronize(stream));
+      return;
+    }
     NB_NCCL2(ncclGroupStart());
     for (int p = 0; p < world; ++p) {
       const uint64_t sb = soff[p + 1] - soff[p], rb = roff[p + 1] - roff[p];

@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
       {
         const uint32_t q = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
         const volatile uint8_t* dn = R.done + R.draw_base[w];
-        uint32_t spins = 0, nap = 64;
+        uint32_t spins = 0, nap = min(64u, R.nap_cap);
         bool abort = false, ok = q == 0xFFFFFFFFu;
         for (;;) {
           if (!ok) ok = dn[q] != 0;  // a lane stops polling once its predecessor is done
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
           }
           // exponential backoff: thousands of waiting warps must not saturate L2
           __nanosleep(nap);
-          nap = min(nap * 2, 2048u);
+          nap = min(nap * 2, R.nap_cap);
         }
         if (__any_sync(FULL, abort)) {
           if (lane == 0) atomicExch(R.stall, 1u);
@@ -461,7 +461,10 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
       else if (lane > cnt && lane < nsl) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
       const double2 pv = ldpos(P.pos + pt);  // every slot's position before this draw
       const double hx = __shfl_sync(FULL, pv.x, 0), hy = __shfl_sync(FULL, pv.y, 0);
-      // ---- noise terms (objective.hpp:113-145)
+      // ---- noise terms (objective.hpp:113-145). Terms are computed on their
+      // lanes; every sum is then taken in the reference's order by all lanes
+      // together from shuffles (unrolled: the adds' dependency chain is the
+      // only serial part), so every lane holds the same bits.
       uint32_t own = 0;
       double lm = W.local_mass;
       if (P.all_but_own) {
@@ -472,86 +475,85 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
       double remote_sum = 0.0;
       for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
         const uint32_t q = q0 + lane;
-        double term = 0.0, use = 0.0;
+        double term = 0.0;
+        bool use = false;
         if (q < nr) {
           const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
           if (!(P.all_but_own && r == own)) {
             term = __dmul_rn(cm[3 * r + 2], cauchy_rn(hx, hy, cm[3 * r], cm[3 * r + 1]));
-            use = 1.0;
+            use = true;
           }
         }
-        sa[lane] = term;
-        sb[lane] = use;
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t m = min(32u, nr - q0);
-          for (uint32_t j = 0; j < m; ++j)
-            if (sb[j] != 0.0) remote_sum = __dadd_rn(remote_sum, sa[j]);
+        const uint32_t um = __ballot_sync(FULL, use);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double x = __shfl_sync(FULL, term, j);
+          if ((um >> j) & 1u) remote_sum = __dadd_rn(remote_sum, x);
         }
-        __syncwarp();
       }
-      const double mean_field = __dmul_rn(M, __shfl_sync(FULL, remote_sum, 0));
+      const double mean_field = __dmul_rn(M, remote_sum);
       const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
       const bool is_tail = lane > cnt && lane < nsl;
       const bool is_nb = lane >= 1 && lane <= cnt;
       const double qn = is_tail ? cauchy_rn(hx, hy, pv.x, pv.y) : 0.0;
-      sa[lane] = qn;
-      __syncwarp();
       double qsum = 0.0;
-      if (lane == 0)
-        for (uint32_t q = 0; q < s; ++q) qsum = __dadd_rn(qsum, sa[1 + cnt + q]);
-      qsum = __shfl_sync(FULL, qsum, 0);
+#pragma unroll
+      for (int j = 1; j < 32; ++j) {
+        const double x = __shfl_sync(FULL, qn, j);
+        if ((uint32_t)j > cnt && (uint32_t)j < nsl) qsum = __dadd_rn(qsum, x);
+      }
       const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
       // ---- attraction (objective.hpp:197-213), neighbour j on lane 1 + j
-      double ax = 0.0, ay = 0.0;
+      double ax = 0.0, ay = 0.0, tl = 0.0, tb = 0.0, tx = 0.0, ty = 0.0;
       if (is_nb) {
         const double q = cauchy_rn(hx, hy, pv.x, pv.y);
         const double wj = wt[cnt * k + lane - 1];
         const double qb = __dadd_rn(q, bg);
-        sa[lane] = __dmul_rn(wj, -log(__ddiv_rn(q, qb)));
-        sb[lane] = __ddiv_rn(wj, qb);
+        tl = __dmul_rn(wj, -log(__ddiv_rn(q, qb)));
+        tb = __ddiv_rn(wj, qb);
         const double pull = __dmul_rn(
             __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj),
                                 __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
                       q),
             q);
         const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
-        sc[lane] = __dmul_rn(pull, dx);
-        sd[lane] = __dmul_rn(pull, dy);
+        tx = __dmul_rn(pull, dx);
+        ty = __dmul_rn(pull, dy);
         ax = __dmul_rn(-pull, dx);
         ay = __dmul_rn(-pull, dy);
       }
-      __syncwarp();
       double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
-      if (lane == 0)
-        for (uint32_t j = 1; j <= cnt; ++j) {
-          loss = __dadd_rn(loss, sa[j]);
-          bgs = __dadd_rn(bgs, sb[j]);
-          gx = __dadd_rn(gx, sc[j]);
-          gy = __dadd_rn(gy, sd[j]);
+#pragma unroll
+      for (int j = 1; j < 32; ++j) {  // four independent chains, list order
+        const double xl = __shfl_sync(FULL, tl, j), xb = __shfl_sync(FULL, tb, j);
+        const double xx = __shfl_sync(FULL, tx, j), xy = __shfl_sync(FULL, ty, j);
+        if ((uint32_t)j <= cnt) {
+          loss = __dadd_rn(loss, xl);
+          bgs = __dadd_rn(bgs, xb);
+          gx = __dadd_rn(gx, xx);
+          gy = __dadd_rn(gy, xy);
         }
-      bgs = __shfl_sync(FULL, bgs, 0);
-      __syncwarp();
+      }
       // ---- negative repulsion (objective.hpp:216-226), tail q on lane 1 + cnt + q
       if (is_tail) {
         const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
         const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
         ax = __dmul_rn(push, dx);
         ay = __dmul_rn(push, dy);
-        sc[lane] = ax;
-        sd[lane] = ay;
       }
+      sa[lane] = ax;  // tails' pushes, subtracted in draw order
+      sb[lane] = ay;
       __syncwarp();
-      if (lane == 0)
-        for (uint32_t q = 0; q < s; ++q) {
-          gx = __dsub_rn(gx, sc[1 + cnt + q]);
-          gy = __dsub_rn(gy, sd[1 + cnt + q]);
-        }
+      for (uint32_t q = 0; q < s; ++q) {
+        gx = __dsub_rn(gx, sa[1 + cnt + q]);
+        gy = __dsub_rn(gy, sb[1 + cnt + q]);
+      }
       __syncwarp();
       // ---- mean repulsion (objective.hpp:229-236), q_r recomputed per cell
       for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
         const uint32_t q = q0 + lane;
-        double px = 0.0, py = 0.0, use = 0.0;
+        double px = 0.0, py = 0.0;
+        bool use = false;
         if (q < nr) {
           const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
           if (!(P.all_but_own && r == own)) {
@@ -561,22 +563,18 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
                 __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), M), cm[3 * r + 2]), qr), qr);
             px = __dmul_rn(push, __dsub_rn(hx, mx));
             py = __dmul_rn(push, __dsub_rn(hy, my));
-            use = 1.0;
+            use = true;
           }
         }
-        sa[lane] = px;
-        sb[lane] = py;
-        sc[lane] = use;
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t m = min(32u, nr - q0);
-          for (uint32_t j = 0; j < m; ++j)
-            if (sc[j] != 0.0) {
-              gx = __dsub_rn(gx, sa[j]);
-              gy = __dsub_rn(gy, sb[j]);
-            }
+        const uint32_t um = __ballot_sync(FULL, use);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double xx = __shfl_sync(FULL, px, j), xy = __shfl_sync(FULL, py, j);
+          if ((um >> j) & 1u) {
+            gx = __dsub_rn(gx, xx);
+            gy = __dsub_rn(gy, xy);
+          }
         }
-        __syncwarp();
       }
       if (lane == 0) {
         P.loss_slot[i] = loss;

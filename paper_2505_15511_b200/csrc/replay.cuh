@@ -60,6 +60,7 @@ struct ReplayDev {
   const uint32_t* pt_base;     // per local point: draw_base of its worker
   uint32_t total_chunks;       // warps' chunks of draws, worker-interleaved
   uint32_t max_draws, total_draws;
+  uint32_t nap_cap;            // longest back-off sleep of a waiting draw (ns)
 };
 
 void launch_mt_words(const ReplayDev& R, const uint64_t* counts, cudaStream_t st);

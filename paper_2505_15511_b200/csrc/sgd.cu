@@ -10,30 +10,35 @@
 namespace nb {
 
 // Per-worker loss in sequential draw order (optimizer.hpp:289-290).
-// One warp per worker: coalesced loads of the next 128 slots, the chain added
-// in draw order by every lane (as k_means_exact).
+// One warp per worker: the warp stages the next 256 slots in shared memory
+// (coalesced), then lane 0 adds them in draw order with the loads ahead of the
+// dependent adds (the chain is bound by DADD latency, ~8 cycles).
 __global__ void k_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk,
                            uint32_t nw, double* out) {
-  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint32_t lane = threadIdx.x & 31;
+  __shared__ double buf[4][256];
+  const uint32_t wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + wi;
   if (w >= nw) return;
+  double* b = buf[wi];
   double acc = 0.0;
   const double* p = slot + base[w];
   const uint32_t D = wk[w].draws;
-  for (uint32_t b = 0; b < D; b += 128) {
-    double v[4];
+  for (uint32_t b0 = 0; b0 < D; b0 += 256) {
+    const uint32_t m = min(256u, D - b0);
+    for (uint32_t e = lane; e < m; e += 32) b[e] = p[b0 + e];
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t e = 0;
+      for (; e + 8 <= m; e += 8) {
+        double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = b + 32 * u + lane;
-      v[u] = i < D ? p[i] : 0.0;
-    }
-    const uint32_t m = min(128u, D - b);
+        for (int u = 0; u < 8; ++u) v[u] = b[e + u];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      for (uint32_t l = 0; l < 32; ++l) {
-        const double x = __shfl_sync(0xffffffffu, v[u], l);
-        if (32 * u + l < m) acc = __dadd_rn(acc, x);
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
       }
+      for (; e < m; ++e) acc = __dadd_rn(acc, b[e]);
+    }
+    __syncwarp();
   }
   if (lane == 0) out[w] = acc;
 }
@@ -43,33 +48,36 @@ __global__ void k_loss_seq(const double* slot, const uint32_t* base, const Worke
 // Exact: per local cluster and coordinate, a sequential sum over the
 // cluster's contiguous segment (ascending original id == the order of
 // gather_means, optimizer.hpp:163-168 / :420-428), then / count.
-// One warp per (cluster, coordinate) chain: the lanes load the next 128
-// values (coalesced, four per lane, in flight together) and the chain is
-// added in ascending order from them (each lane adds every value, in order,
-// so every lane holds the same sum), then / count.
+// One warp per (cluster, coordinate) chain: the warp stages the next 256
+// values in shared memory, lane 0 adds them in ascending order (loads ahead
+// of the dependent adds), then / count.
 __global__ void k_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl,
                               double* slot /* ncl x 2 */) {
-  const uint32_t g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint32_t lane = threadIdx.x & 31;
+  __shared__ double buf[4][256];
+  const uint32_t wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t g = blockIdx.x * (blockDim.x >> 5) + wi;
   if (g >= 2 * ncl) return;
   const uint32_t c = g >> 1, dim = g & 1;
   const LocalCluster L = lc[c];
   const double* p = reinterpret_cast<const double*>(pos) + 2 * (size_t)L.start + dim;
+  double* b = buf[wi];
   double acc = 0.0;
-  for (uint32_t b = 0; b < L.count; b += 128) {
-    double v[4];
+  for (uint32_t b0 = 0; b0 < L.count; b0 += 256) {
+    const uint32_t m = min(256u, L.count - b0);
+    for (uint32_t e = lane; e < m; e += 32) b[e] = p[2 * (size_t)(b0 + e)];
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t e = 0;
+      for (; e + 8 <= m; e += 8) {
+        double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = b + 32 * u + lane;
-      v[u] = i < L.count ? p[2 * (size_t)i] : 0.0;
-    }
-    const uint32_t m = min(128u, L.count - b);
+        for (int u = 0; u < 8; ++u) v[u] = b[e + u];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      for (uint32_t l = 0; l < 32; ++l) {
-        const double x = __shfl_sync(0xffffffffu, v[u], l);
-        if (32 * u + l < m) acc = __dadd_rn(acc, x);
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
       }
+      for (; e < m; ++e) acc = __dadd_rn(acc, b[e]);
+    }
+    __syncwarp();
   }
   if (lane == 0) slot[g] = __ddiv_rn(acc, (double)L.count);
 }

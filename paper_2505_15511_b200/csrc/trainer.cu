@@ -474,6 +474,11 @@ struct RankTrainer {
     R.total_chunks = nwl * ((max_draws + per - 1) / per);
     R.max_draws = max_draws;
     R.total_draws = total_draws;
+    static const uint32_t nap = [] {
+      const char* e = std::getenv("NOMAD_B200_DF_NAP");
+      return e ? (uint32_t)std::max(1, std::atoi(e)) : 512u;
+    }();
+    R.nap_cap = nap;
     return R;
   }
 

@@ -65,3 +65,17 @@ def test_sharded_index_trains_to_the_oracle(port):
                                         train_config(**kw), pca, 0, 3)
     assert np.array_equal(tr.layout(), rl)
     np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
+def test_single_rank_sharded_build(ctx):
+    """nomad_b200_index_sharded with world_size 1 (the multi-process entry on one
+    rank) is the one-GPU build."""
+    import paper_2505_15511_b200 as nb
+    n, d, blobs, C = 5000, 24, 8, 6
+    x = nb.generate_mixture(n, d, blobs, 10.0, 3, ctx=ctx)
+    c1 = nb.kmeans_em_default_tol(x, nb.lsh_init(x, C, 5, ctx=ctx), 100, ctx=ctx)
+    g1 = nb.build_knn(x, c1, 15, ctx=ctx)
+    cs, gs = nb.index_sharded(x, 0, n, C, 5, 2, k=15, ctx=ctx)
+    assert np.array_equal(cs.assignment, c1.assignment)
+    assert np.array_equal(cs.centroids, c1.centroids)
+    assert np.array_equal(gs.neighbors, g1.neighbors) and np.array_equal(gs.distances, g1.distances)
