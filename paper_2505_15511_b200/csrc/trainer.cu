@@ -93,19 +93,12 @@ struct RankTrainer {
   // the rejection fallback
   DBuf<MtState> mt_a, mt_b;
   DBuf<uint64_t> wcount, wbase;
-  DBuf<unsigned long long> words, redges[2];
-  DBuf<uint32_t> pool_d, pool_off_d, tkey, tval, tkey2, tval2, ticket, pt_base, stall;
-  // two draw sets: the next epoch's draws and dependencies are prepared on a
-  // side stream while this epoch's dataflow kernel runs
-  DBuf<uint32_t> rheads[2], rtails[2], rpred[2], reject[2];
+  DBuf<unsigned long long> words, redges;
+  DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, tkey, tval, tkey2, tval2, rpred, reject,
+      ticket, pt_base, stall;
   DBuf<uint8_t> rdone, sort_tmp;
   size_t sort_bytes = 0;
   uint32_t df_blocks = 0, total_draws = 0, max_draws = 0;
-  cudaStream_t prep_st = nullptr;
-  cudaEvent_t ev_prep[2] = {nullptr, nullptr}, ev_top = nullptr;
-  std::vector<uint32_t> rj_h[2];
-  int rset = 0;           // draw set of the next epoch to run
-  bool prepped = false;   // rset already prepared (on prep_st) by the previous epoch
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
   uint32_t hog_cells = 0;  // cells per worker of the hogwild cell table
@@ -138,13 +131,6 @@ struct RankTrainer {
   void bind() { bind_device(ctx); }
   void launched(const char* name) { note_launch(ctx, name); }
   ~RankTrainer() {
-    if (prep_st) {
-      cudaStreamSynchronize(prep_st);
-      cudaStreamDestroy(prep_st);
-    }
-    for (auto& e : ev_prep)
-      if (e) cudaEventDestroy(e);
-    if (ev_top) cudaEventDestroy(ev_top);
     if (comm && own_comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -441,24 +427,18 @@ struct RankTrainer {
     upload(pt_base, ptb, S);
     const uint64_t T = 1 + k + s, D = std::max<uint64_t>(acc, 1);
     words.alloc(std::max<uint64_t>(wacc, 1));
+    rheads.alloc(D);
+    rtails.alloc(D * s);
     if (D * T >= 0xFFFFFFFFull) fail(kSize, "replay touches per rank exceed 2^32");
-    for (int b = 0; b < 2; ++b) {
-      rheads[b].alloc(D);
-      rtails[b].alloc(D * s);
-      rpred[b].alloc(D * T);
-      reject[b].alloc(std::max<uint32_t>(nwl, 1));
-      redges[b].alloc(std::max<uint32_t>(nwl, 1));
-      rj_h[b].assign(std::max<uint32_t>(nwl, 1), 0);
-      NB_CUDA(cudaEventCreateWithFlags(&ev_prep[b], cudaEventDisableTiming));
-    }
-    NB_CUDA(cudaEventCreateWithFlags(&ev_top, cudaEventDisableTiming));
-    NB_CUDA(cudaStreamCreateWithFlags(&prep_st, cudaStreamNonBlocking));
     tkey.alloc(D * T);
     tval.alloc(D * T);
     tkey2.alloc(D * T);
     tval2.alloc(D * T);
+    rpred.alloc(D * T);
     rdone.alloc(D);
     loss_slot.alloc(D);
+    reject.alloc(std::max<uint32_t>(nwl, 1));
+    redges.alloc(std::max<uint32_t>(nwl, 1));
     ticket.alloc(1);
     stall.alloc(1);
     NB_CUDA(cudaMemsetAsync(stall.p, 0, 4, S));
@@ -466,7 +446,7 @@ struct RankTrainer {
     sort_tmp.alloc(std::max<size_t>(sort_bytes, 1));
   }
 
-  ReplayDev replay_dev(int set) {
+  ReplayDev replay_dev() {
     ReplayDev R{};
     R.nwl = nwl;
     R.s = (uint32_t)s;
@@ -476,16 +456,16 @@ struct RankTrainer {
     R.st_in = mt_a.p;
     R.st_out = mt_b.p;
     R.words = words.p;
-    R.heads = rheads[set].p;
-    R.tails = rtails[set].p;
+    R.heads = rheads.p;
+    R.tails = rtails.p;
     R.tkey = tkey.p;
     R.tval = tval.p;
     R.tkey2 = tkey2.p;
     R.tval2 = tval2.p;
-    R.pred = rpred[set].p;
+    R.pred = rpred.p;
     R.n_loc = (uint32_t)orig_of.size();
-    R.reject = reject[set].p;
-    R.edges = redges[set].p;
+    R.reject = reject.p;
+    R.edges = redges.p;
     R.done = rdone.p;
     R.ticket = ticket.p;
     R.stall = stall.p;
@@ -496,7 +476,7 @@ struct RankTrainer {
     R.total_draws = total_draws;
     static const uint32_t nap = [] {
       const char* e = std::getenv("NOMAD_B200_DF_NAP");
-      return e ? (uint32_t)std::max(1, std::atoi(e)) : 256u;
+      return e ? (uint32_t)std::max(1, std::atoi(e)) : 512u;
     }();
     R.nap_cap = nap;
     return R;
@@ -506,10 +486,10 @@ struct RankTrainer {
   // (rng.hpp:49-55, probability ~n / 2^64 per draw): its draws are made on
   // the host from the epoch's start state, consuming the extra words exactly
   // as the reference does (optimizer.hpp:254-255, :284-285).
-  void host_draws(uint32_t wl, int set, MtState* st_in, MtState* st_out) {
+  void host_draws(uint32_t wl) {
     cudaStream_t S = st();
     Mt64 m;
-    NB_CUDA(cudaMemcpy(&m.s, st_in + wl, sizeof(MtState), cudaMemcpyDeviceToHost));
+    NB_CUDA(cudaMemcpy(&m.s, mt_a.p + wl, sizeof(MtState), cudaMemcpyDeviceToHost));
     const WorkerDev& d = wk[wl];
     std::vector<uint32_t> hd(d.draws), tl((size_t)d.draws * s);
     for (uint32_t t = 0; t < d.draws; ++t) {
@@ -525,75 +505,38 @@ struct RankTrainer {
     }
     const size_t b = draw_base_h[wl];
     if (d.draws) {
-      NB_CUDA(cudaMemcpyAsync(rheads[set].p + b, hd.data(), hd.size() * 4, cudaMemcpyHostToDevice, S));
-      NB_CUDA(cudaMemcpyAsync(rtails[set].p + b * s, tl.data(), tl.size() * 4,
-                              cudaMemcpyHostToDevice, S));
+      NB_CUDA(cudaMemcpyAsync(rheads.p + b, hd.data(), hd.size() * 4, cudaMemcpyHostToDevice, S));
+      NB_CUDA(cudaMemcpyAsync(rtails.p + b * s, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice, S));
     }
-    NB_CUDA(cudaMemcpyAsync(st_out + wl, &m.s, sizeof(MtState), cudaMemcpyHostToDevice, S));
+    NB_CUDA(cudaMemcpyAsync(mt_b.p + wl, &m.s, sizeof(MtState), cudaMemcpyHostToDevice, S));
     NB_CUDA(cudaStreamSynchronize(S));
   }
 
-  // Draws and dependencies of one epoch into draw set `set` on stream `S`:
-  // streams (mt_a -> mt_b), heads / tails, touches sorted by point,
-  // predecessors; the reject flags are copied back for the host check.
-  void prep_epoch(int set, SgdParams& P, cudaStream_t S) {
-    ReplayDev R = replay_dev(set);
-    NB_CUDA(cudaMemsetAsync(reject[set].p, 0, reject[set].bytes(), S));
-    NB_CUDA(cudaMemsetAsync(redges[set].p, 0, redges[set].bytes(), S));
+  // One replay epoch on the device: streams -> draws -> dependencies ->
+  // dataflow SGD -> per-worker losses in draw order.
+  void launch_replay_epoch(SgdParams& P) {
+    cudaStream_t S = st();
+    ReplayDev R = replay_dev();
+    NB_CUDA(cudaMemsetAsync(reject.p, 0, reject.bytes(), S));
+    NB_CUDA(cudaMemsetAsync(redges.p, 0, redges.bytes(), S));
     if (nwl) {
       launch_mt_words(R, wcount.p, S);
       launched("k_mt_words");
       launch_replay_map(R, P, pool_d.p, pool_off_d.p, S);
       launched("k_replay_map");
     }
-    NB_CUDA(cudaMemcpyAsync(rj_h[set].data(), reject[set].p, rj_h[set].size() * 4,
-                            cudaMemcpyDeviceToHost, S));
-    launch_replay_deps(R, P, sort_tmp.p, sort_bytes, S);
-    launched("k_replay_deps");
-    NB_CUDA(cudaEventRecord(ev_prep[set], S));
-    std::swap(mt_a, mt_b);  // mt_a: the start state of the epoch after this one
-  }
-
-  // One replay epoch on the device: streams -> draws -> dependencies ->
-  // dataflow SGD -> per-worker losses in draw order. The next epoch of this
-  // run is prepared on prep_st while the dataflow kernel runs.
-  int cur_set = 0;
-  void launch_replay_epoch(SgdParams& P, bool another) {
-    cudaStream_t S = st();
-    const int set = rset;
-    cur_set = set;
-    if (!prepped) prep_epoch(set, P, S);
-    NB_CUDA(cudaEventSynchronize(ev_prep[set]));  // reject flags on the host
+    std::vector<uint32_t> rj(std::max<uint32_t>(nwl, 1), 0);
+    NB_CUDA(cudaMemcpyAsync(rj.data(), reject.p, rj.size() * 4, cudaMemcpyDeviceToHost, S));
+    NB_CUDA(cudaStreamSynchronize(S));
     // (NOMAD_B200_REPLAY_HOST_DRAWS=1 takes the rejection path for every
     // worker: a test hook for the fallback, whose result must not change)
     const bool force = std::getenv("NOMAD_B200_REPLAY_HOST_DRAWS") != nullptr;
-    bool redo = false;
     for (uint32_t wl = 0; wl < nwl; ++wl)
-      if (rj_h[set][wl] || force) {
-        host_draws(wl, set, mt_b.p, mt_a.p);  // this epoch: start mt_b, end mt_a
-        redo = true;
-      }
-    if (redo) {
-      ReplayDev R = replay_dev(set);
-      NB_CUDA(cudaMemsetAsync(redges[set].p, 0, redges[set].bytes(), S));
-      launch_replay_deps(R, P, sort_tmp.p, sort_bytes, S);
-      launched("k_replay_deps");
-    }
-    prepped = false;
-    rset = set ^ 1;
-    if (another) {  // the next epoch's draws overlap this epoch's dataflow
-      NB_CUDA(cudaEventRecord(ev_top, S));
-      NB_CUDA(cudaStreamWaitEvent(prep_st, ev_top, 0));
-      prep_epoch(set ^ 1, P, prep_st);
-      prepped = true;
-    }
-    if (!df_blocks) {
-      // one block per SM fewer than fit: the overlapped preparation needs room
-      const uint32_t full =
-          dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
-      df_blocks = std::max<uint32_t>(ctx->sm_count, full - (uint32_t)ctx->sm_count);
-    }
-    ReplayDev R = replay_dev(set);
+      if (rj[wl] || force) host_draws(wl);
+    launch_replay_deps(R, P, sort_tmp.p, sort_bytes, S);
+    launched("k_replay_deps");
+    if (!df_blocks)
+      df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
     NB_CUDA(cudaMemsetAsync(rdone.p, 0, rdone.bytes(), S));
     NB_CUDA(cudaMemsetAsync(ticket.p, 0, 4, S));
     P.loss_slot = loss_slot.p;
@@ -606,6 +549,7 @@ struct RankTrainer {
       launched("k_loss_seq");
     }
     NB_CUDA(cudaEventRecord(ev[1], S));
+    std::swap(mt_a, mt_b);  // this epoch's end state starts the next
   }
 
   void plan_hogwild_grid() {
@@ -799,7 +743,6 @@ struct RankTrainer {
     if (e > cfg.epochs) fail(kParameter, "epoch out of range for schedule");
     if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY && e != epochs_done) {
       if (e < epochs_done) fail(kParameter, "replay mode cannot seek backwards");
-      if (prepped) fail(kInternal, "replay: a prepared epoch is pending");
       std::vector<Mt64> m(std::max<uint32_t>(nwl, 1));
       for (uint32_t wl = 0; wl < nwl; ++wl)
         NB_CUDA(cudaMemcpy(&m[wl].s, mt_a.p + wl, sizeof(MtState), cudaMemcpyDeviceToHost));
@@ -937,7 +880,7 @@ struct RankTrainer {
     s_edges = 0;
     const bool replay = cfg.sgd_mode == NOMAD_B200_SGD_REPLAY;
     if (replay) {
-      launch_replay_epoch(P, it + 1 < s_E);
+      launch_replay_epoch(P);
     } else {
       NB_CUDA(cudaMemsetAsync(loss_acc.p, 0, loss_acc.bytes(), S));
       NB_CUDA(cudaMemsetAsync(edge_acc.p, 0, edge_acc.bytes(), S));
@@ -962,7 +905,7 @@ struct RankTrainer {
     if (nwl) NB_CUDA(cudaMemcpyAsync(s_wl_loss.data(), lsrc, nwl * 8, cudaMemcpyDeviceToHost, S));
     if (nwl)
       NB_CUDA(cudaMemcpyAsync(s_wl_edges.data(),
-                              cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD ? edge_acc.p : redges[cur_set].p,
+                              cfg.sgd_mode == NOMAD_B200_SGD_HOGWILD ? edge_acc.p : redges.p,
                               nwl * 8, cudaMemcpyDeviceToHost, S));
     if (world > 1 && !grouped) {
       if (!s_gl.p) s_gl.alloc((size_t)world * nwl);
