@@ -216,6 +216,15 @@ __global__ void k_replay_pred(ReplayDev R, uint64_t items) {
 // ------------------------------------------------------ dataflow SGD
 __device__ __forceinline__ double2 ldpos(const double2* p) { return __ldcg(p); }
 
+__device__ __forceinline__ uint32_t ld_acquire_u8(const uint8_t* p) {
+  uint16_t v;
+  asm volatile("ld.acquire.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return v & 0xFF;
+}
+__device__ __forceinline__ void st_release_u8(uint8_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u8 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) {
   extern __shared__ __align__(16) double sm[];
   const uint32_t k = P.k, s = P.s, C = P.n_clusters, T = R.T;
@@ -430,20 +439,31 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
       const uint32_t t = (uint32_t)(c / R.nwl);
       if (t >= W.draws) continue;
       const uint32_t i = R.draw_base[w] + t;
+      // slot points (head, neighbours, tails): epoch-static, loaded before the
+      // wait so that only the position loads follow the predecessors
+      const uint32_t head = R.heads[i];
+      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
+      const uint32_t nsl = 1 + cnt + s;
+      uint32_t pt = head;
+      if (lane >= 1 && lane <= cnt) pt = P.ell[(size_t)head * P.kpad + lane - 1];
+      else if (lane > cnt && lane < nsl) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
       // ---- wait until every predecessor is done
       {
         const uint32_t q = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
-        const volatile uint8_t* dn = R.done + R.draw_base[w];
+        const uint8_t* dn = R.done + R.draw_base[w];
         uint32_t spins = 0, nap = min(64u, R.nap_cap);
         bool abort = false, ok = q == 0xFFFFFFFFu;
         for (;;) {
-          if (!ok) ok = dn[q] != 0;  // a lane stops polling once its predecessor is done
+          // acquire: this lane's later loads (its slot's position) see the
+          // predecessor's writes; a lane stops polling once its flag is set
+          if (!ok) ok = ld_acquire_u8(dn + q) != 0;
           if (__all_sync(FULL, ok)) break;
-          if (*reinterpret_cast<volatile uint32_t*>(R.stall) || ++spins > (1u << 22)) {
+          if ((++spins & 63) == 0 &&
+              (*reinterpret_cast<volatile uint32_t*>(R.stall) || spins > (1u << 22))) {
             abort = true;  // watchdog (a schedule bug): report, never hang
             break;
           }
-          // exponential backoff: thousands of waiting warps must not saturate L2
+          // exponential back-off: thousands of waiting warps share L2
           __nanosleep(nap);
           nap = min(nap * 2, R.nap_cap);
         }
@@ -452,13 +472,6 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
           continue;
         }
       }
-      __threadfence();  // the predecessors' position writes before our reads
-      const uint32_t head = R.heads[i];
-      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
-      const uint32_t nsl = 1 + cnt + s;
-      uint32_t pt = head;
-      if (lane >= 1 && lane <= cnt) pt = P.ell[(size_t)head * P.kpad + lane - 1];
-      else if (lane > cnt && lane < nsl) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
       const double2 pv = ldpos(P.pos + pt);  // every slot's position before this draw
       const double hx = __shfl_sync(FULL, pv.x, 0), hy = __shfl_sync(FULL, pv.y, 0);
       // ---- noise terms (objective.hpp:113-145). Terms are computed on their
@@ -601,9 +614,10 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
         }
         __stcg(P.pos + pt, v);
       }
-      __threadfence();  // our writes before the flag
+      // release: the warp barrier orders every lane's position store before
+      // lane 0's release store of the flag (release is cumulative)
       __syncwarp();
-      if (lane == 0) *reinterpret_cast<volatile uint8_t*>(R.done + i) = 1;
+      if (lane == 0) st_release_u8(R.done + i, 1);
     }
   }
 }

@@ -476,7 +476,7 @@ struct RankTrainer {
     R.total_draws = total_draws;
     static const uint32_t nap = [] {
       const char* e = std::getenv("NOMAD_B200_DF_NAP");
-      return e ? (uint32_t)std::max(1, std::atoi(e)) : 512u;
+      return e ? (uint32_t)std::max(1, std::atoi(e)) : 256u;
     }();
     R.nap_cap = nap;
     return R;
