@@ -182,7 +182,6 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
   const uint32_t cnt = P.ncnt ? P.ncnt[h] : k;
   const uint32_t* nb = P.ell + (size_t)h * P.kpad;
   key[0] = h;
-  atomicAdd(R.tcount + h, 1u);
   uint32_t j = 1;
   for (; j <= cnt; ++j) {
     // build_knn's lists hold distinct points other than the head; a caller's
@@ -191,7 +190,6 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
     bool dup = v == h;
     for (uint32_t a = 0; a + 1 < j && !dup; ++a) dup = nb[a] == v;
     key[j] = dup ? NONE : v;
-    if (!dup) atomicAdd(R.tcount + v, 1u);
   }
   for (; j < 1 + k; ++j) key[j] = NONE;
   const uint32_t* tails = R.tails + (size_t)i * s;
@@ -201,48 +199,7 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
     for (uint32_t a = 0; a < cnt && !dup; ++a) dup = nb[a] == v;
     for (uint32_t a = 0; a < q && !dup; ++a) dup = tails[a] == v;
     key[1 + k + q] = dup ? NONE : v;
-    if (!dup) atomicAdd(R.tcount + v, 1u);
   }
-}
-
-// Heavy points: touched at least heavy_min times this epoch; each gets a
-// queue (ids in arrival order: which warp runs a queue does not change the
-// result, the dataflow order does).
-__global__ void k_replay_heavy(ReplayDev R) {
-  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= R.n_loc) return;
-  uint32_t q = 0xFFFFFFFFu;
-  if (R.tcount[v] >= R.heavy_min) {
-    const uint32_t id = atomicAdd(R.nheavy, 1u);
-    if (id < R.max_queues) q = id;
-  }
-  R.hq[v] = q;
-}
-
-// Per draw: the queue of its most-touched heavy point (the rest: the shared
-// queue max_queues), key = queue << 40 | t << 8 | worker.
-__global__ void k_replay_qkeys(ReplayDev R, uint32_t total) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  uint32_t w = 0;
-  while (w + 1 < R.nwl && R.draw_base[w + 1] <= i) ++w;
-  const uint32_t t = i - R.draw_base[w];
-  uint32_t best = R.max_queues, bc = 0;
-  const uint32_t* key = R.tkey + (size_t)i * R.T;
-  for (uint32_t j = 0; j < R.T; ++j) {
-    const uint32_t v = key[j];
-    if (v == R.n_loc) continue;
-    const uint32_t q = R.hq[v];
-    if (q == 0xFFFFFFFFu) continue;
-    const uint32_t c = R.tcount[v];
-    if (c > bc) {
-      bc = c;
-      best = q;
-    }
-  }
-  atomicAdd(R.qcnt + best, 1u);
-  R.qkey[i] = ((unsigned long long)best << 40) | ((unsigned long long)t << 8) | w;
-  R.qval[i] = i;
 }
 
 // After the stable sort by point: each touch's predecessor is the previous
@@ -472,30 +429,16 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
   // draws, so the smallest unfinished draw is always runnable on its
   // (resident: cooperative launch) warp — no claim counter, and a waiting
   // draw holds up only its own warp.
-  // Queues: warp g < n_queues runs heavy queue g (the draws touching one hub
-  // point, in draw order: consecutive links of that point's chain never wait
-  // on another SM); the other warps share the rest, sorted (t, worker), in
-  // round-robin. Every warp runs its draws in draw order.
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint32_t NQ = R.n_queues;
-  uint64_t c0, c1, cs;
-  if (gw < NQ) {
-    c0 = R.qoff[gw];
-    c1 = R.qoff[gw + 1];
-    cs = 1;
-  } else {
-    c0 = R.qoff[R.max_queues] + (gw - NQ);
-    c1 = R.qoff[R.max_queues + 1];
-    cs = nwarps - NQ;
-  }
-  for (uint64_t c = c0; c < c1; c += cs) {
-    const unsigned long long key = R.qkey2[c];
-    const uint32_t w = (uint32_t)(key & 0xFF);
+  const uint64_t total = (uint64_t)R.nwl * R.max_draws;
+  for (uint64_t c = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < total;
+       c += nwarps) {
+    const uint32_t w = (uint32_t)(c % R.nwl);
     const WorkerDev W = P.workers[w];
     {
-      const uint32_t t = (uint32_t)((key >> 8) & 0xFFFFFFFFull);
-      const uint32_t i = R.qval2[c];
+      const uint32_t t = (uint32_t)(c / R.nwl);
+      if (t >= W.draws) continue;
+      const uint32_t i = R.draw_base[w] + t;
       // slot points (head, neighbours, tails): epoch-static, loaded before the
       // wait so that only the position loads follow the predecessors
       const uint32_t head = R.heads[i];
@@ -711,9 +654,6 @@ void launch_replay_deps(const ReplayDev& R, const SgdParams& P, void* sort_tmp, 
   const uint32_t total = R.total_draws;
   const uint64_t items = (uint64_t)total * R.T;
   if (!total) return;
-  NB_CUDA(cudaMemsetAsync(R.tcount, 0, (size_t)R.n_loc * 4, st));
-  NB_CUDA(cudaMemsetAsync(R.nheavy, 0, 4, st));
-  NB_CUDA(cudaMemsetAsync(R.qcnt, 0, ((size_t)R.max_queues + 1) * 4, st));
   k_replay_touch<<<blocks_for(total, 256), 256, 0, st>>>(R, P, total);
   // stable LSD radix sort by point over the draw-ordered touches
   size_t b = sort_bytes;
@@ -723,24 +663,6 @@ void launch_replay_deps(const ReplayDev& R, const SgdParams& P, void* sort_tmp, 
   Rs.tkey = R.tkey2;
   Rs.tval = R.tval2;
   k_replay_pred<<<blocks_for(items, 256), 256, 0, st>>>(Rs, items);
-  k_replay_heavy<<<blocks_for(R.n_loc, 256), 256, 0, st>>>(R);
-  k_replay_qkeys<<<blocks_for(total, 256), 256, 0, st>>>(R, total);
-}
-
-size_t replay_sched_bytes(uint64_t draws) {
-  size_t b = 0;
-  NB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, (unsigned long long*)nullptr,
-                                          (unsigned long long*)nullptr, (uint32_t*)nullptr,
-                                          (uint32_t*)nullptr, (int64_t)draws, 0, 64));
-  return b;
-}
-
-void launch_replay_schedule(const ReplayDev& R, void* sort_tmp, size_t sort_bytes, cudaStream_t st) {
-  if (!R.total_draws) return;
-  size_t b = sort_bytes;
-  NB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp, b, R.qkey, R.qkey2, R.qval, R.qval2,
-                                          (int64_t)R.total_draws, 0,
-                                          40 + bits_for(R.max_queues + 1), st));
 }
 
 bool dataflow_warp_form(uint32_t k, uint32_t s) {

@@ -52,18 +52,6 @@ struct ReplayDev {
   uint32_t* tval2;
   uint32_t* pred;              // per draw and slot: latest earlier draw touching it (none: ~0)
   uint32_t n_loc;              // local points (the "none" key)
-  // chain-aware schedule: the draws touching a heavily touched point (a hub
-  // of the kNN graph) run in order on one warp of their own
-  uint32_t* tcount;            // per local point: touches this epoch
-  uint32_t* hq;                // per local point: its heavy queue, or ~0
-  uint32_t* nheavy;            // heavy points found
-  uint32_t* qcnt;              // per queue (max_queues + 1, the last = the rest): draws
-  unsigned long long* qkey;    // per draw: queue << 40 | t << 8 | worker
-  unsigned long long* qkey2;   // (sorted)
-  uint32_t* qval;              // per draw: its global index
-  uint32_t* qval2;             // (sorted: the schedule)
-  const uint32_t* qoff;        // per queue + 1: offsets into the schedule (device copy)
-  uint32_t max_queues, heavy_min, n_queues;
   uint32_t* reject;            // per worker: a draw hit the rejection branch
   unsigned long long* edges;   // per worker: sum over draws of |N(head)| + s
   uint8_t* done;               // per draw: completed
@@ -78,15 +66,10 @@ struct ReplayDev {
 void launch_mt_words(const ReplayDev& R, const uint64_t* counts, cudaStream_t st);
 void launch_replay_map(const ReplayDev& R, const SgdParams& P, const uint32_t* pool,
                        const uint32_t* pool_off, cudaStream_t st);
-// touch lists -> stable sort by point (draw order kept inside a point) -> pred,
-// touch counts -> heavy points -> per-draw queue keys (then sorted by the caller
-// through launch_replay_schedule once the queue counts are known)
+// touch lists -> stable sort by point (draw order kept inside a point) -> pred
 void launch_replay_deps(const ReplayDev& R, const SgdParams& P, void* sort_tmp, size_t sort_bytes,
                         cudaStream_t st);
 size_t replay_sort_bytes(uint64_t items, uint32_t n_loc);
-// the schedule: draws sorted by (queue, t, worker)
-void launch_replay_schedule(const ReplayDev& R, void* sort_tmp, size_t sort_bytes, cudaStream_t st);
-size_t replay_sched_bytes(uint64_t draws);
 void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
                          cudaStream_t st);
 uint32_t dataflow_resident_blocks(size_t smem, int sm_count, uint32_t k, uint32_t s);

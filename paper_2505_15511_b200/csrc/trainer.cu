@@ -96,12 +96,8 @@ struct RankTrainer {
   DBuf<unsigned long long> words, redges;
   DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, tkey, tval, tkey2, tval2, rpred, reject,
       ticket, pt_base, stall;
-  DBuf<uint8_t> rdone, sort_tmp, sched_tmp;
-  DBuf<uint32_t> tcount, hq, nheavy, qcnt, qval, qval2, qoff;
-  DBuf<unsigned long long> qkey, qkey2;
-  std::vector<uint32_t> qcnt_h, qoff_h;
-  uint32_t max_queues = 0, n_queues = 0;
-  size_t sort_bytes = 0, sched_bytes = 0;
+  DBuf<uint8_t> rdone, sort_tmp;
+  size_t sort_bytes = 0;
   uint32_t df_blocks = 0, total_draws = 0, max_draws = 0;
   uint32_t max_slots = 0;
   size_t smem_replay = 0, smem_hog = 0;
@@ -449,23 +445,6 @@ struct RankTrainer {
     NB_CUDA(cudaMemsetAsync(stall.p, 0, 4, S));
     sort_bytes = replay_sort_bytes(D * T, (uint32_t)orig_of.size());
     sort_tmp.alloc(std::max<size_t>(sort_bytes, 1));
-    // chain-aware schedule (replay.cuh): one queue per heavy point, at most a
-    // quarter of the dataflow kernel's resident warps
-    df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
-    max_queues = std::min<uint32_t>(1024, df_blocks * 8 / 4);
-    tcount.alloc(orig_of.size() + 1);
-    hq.alloc(orig_of.size() + 1);
-    nheavy.alloc(1);
-    qcnt.alloc(max_queues + 1);
-    qoff.alloc(max_queues + 2);
-    qkey.alloc(D);
-    qkey2.alloc(D);
-    qval.alloc(D);
-    qval2.alloc(D);
-    qcnt_h.assign(max_queues + 1, 0);
-    qoff_h.assign(max_queues + 2, 0);
-    sched_bytes = replay_sched_bytes(D);
-    sched_tmp.alloc(std::max<size_t>(sched_bytes, 1));
   }
 
   ReplayDev replay_dev() {
@@ -492,18 +471,6 @@ struct RankTrainer {
     R.ticket = ticket.p;
     R.stall = stall.p;
     R.pt_base = pt_base.p;
-    R.tcount = tcount.p;
-    R.hq = hq.p;
-    R.nheavy = nheavy.p;
-    R.qcnt = qcnt.p;
-    R.qkey = qkey.p;
-    R.qkey2 = qkey2.p;
-    R.qval = qval.p;
-    R.qval2 = qval2.p;
-    R.qoff = qoff.p;
-    R.max_queues = max_queues;
-    R.heavy_min = 128;
-    R.n_queues = n_queues;
     const uint32_t per = dataflow_draws_per_chunk((uint32_t)k, (uint32_t)s);
     R.total_chunks = nwl * ((max_draws + per - 1) / per);
     R.max_draws = max_draws;
@@ -569,18 +536,8 @@ struct RankTrainer {
       if (rj[wl] || force) host_draws(wl);
     launch_replay_deps(R, P, sort_tmp.p, sort_bytes, S);
     launched("k_replay_deps");
-    {  // queue sizes -> offsets, then the schedule (draws by queue, t, worker)
-      uint32_t nh = 0;
-      NB_CUDA(cudaMemcpyAsync(qcnt_h.data(), qcnt.p, qcnt_h.size() * 4, cudaMemcpyDeviceToHost, S));
-      NB_CUDA(cudaMemcpyAsync(&nh, nheavy.p, 4, cudaMemcpyDeviceToHost, S));
-      NB_CUDA(cudaStreamSynchronize(S));
-      n_queues = std::min(nh, max_queues);
-      for (uint32_t q = 0; q <= max_queues; ++q) qoff_h[q + 1] = qoff_h[q] + qcnt_h[q];
-      NB_CUDA(cudaMemcpyAsync(qoff.p, qoff_h.data(), qoff_h.size() * 4, cudaMemcpyHostToDevice, S));
-      R = replay_dev();
-      launch_replay_schedule(R, sched_tmp.p, sched_bytes, S);
-      launched("k_replay_schedule");
-    }
+    if (!df_blocks)
+      df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
     NB_CUDA(cudaMemsetAsync(rdone.p, 0, rdone.bytes(), S));
     NB_CUDA(cudaMemsetAsync(ticket.p, 0, 4, S));
     P.loss_slot = loss_slot.p;
