@@ -38,7 +38,7 @@
 // a head needs (s + 2) / 2 Philox blocks, one per lane of its group: s <= 7 needs 4 lanes
 static_assert(HOG_G16 >= 4, "HOG_G16 < 4 cannot draw s = 7 negatives per head");
 #ifndef HOG_ROUNDS
-#define HOG_ROUNDS 32     // rounds of 32/G heads per warp-claimed chunk
+#define HOG_ROUNDS 8      // rounds of 256/G heads per scheduled chunk
 #endif
 
 namespace nb {
@@ -124,84 +124,72 @@ template <int G, int KMAX, int SMAX, bool DF, bool ABO>
 __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
   constexpr int NPL = KMAX / G;            // neighbour slots per lane
   constexpr int TPL = (SMAX + G - 1) / G;  // tail slots per lane
+  constexpr int GPB = 256 / G;             // heads per block per round
   extern __shared__ __align__(16) double sm[];
-  constexpr uint32_t FULL = 0xffffffffu;
-  constexpr int GPW = 32 / G;  // heads per warp per round
+  __shared__ double red[8];
+  __shared__ uint32_t s_chunk;
   const uint32_t k = P.k, s = P.s, C = P.n_clusters;
   const double M = (double)P.m_total;
   const int gl = threadIdx.x % G;
-  const int grp = (threadIdx.x & 31) / G;        // head slot of my group within the warp
+  const int grp = threadIdx.x / G;
   const int g0 = (threadIdx.x & 31) & ~(G - 1);  // first lane of my group
   double* wt = sm;
-  // cell tables of every local worker, loaded once: means (double2, 16-byte
-  // aligned) then weights, [worker][max_cells]; so warps claim chunks on
-  // their own, with no block barrier
-  double2* tmu_all = reinterpret_cast<double2*>(sm + ((((k + 1) * k) + 1) & ~1u));
-  double* tpw_all = reinterpret_cast<double*>(tmu_all + (size_t)P.n_workers * P.max_cells);
+  // cell table: means (double2, 16-byte aligned) then weights
+  double2* tmu = reinterpret_cast<double2*>(sm + ((((k + 1) * k) + 1) & ~1u));
   for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
-  if (!P.gcells)
-    for (uint32_t wl = 0; wl < P.n_workers; ++wl) {
-      const WorkerDev Wl = P.workers[wl];
-      const uint32_t nc = ABO ? C : Wl.n_rem;
-      for (uint32_t q = threadIdx.x; q < nc; q += blockDim.x) {
-        const uint32_t r = ABO ? q : P.remote_ids[Wl.rem_off + q];
-        const double p = ABO ? P.cell_probs[r] : P.remote_probs[Wl.rem_off + q];
-        tmu_all[(size_t)wl * P.max_cells + q] = P.means[r];  // cell means, then weights M p_r
-        tpw_all[(size_t)wl * P.max_cells + q] = M * p;
-      }
-    }
-  __syncthreads();
 
+  double* tpw = reinterpret_cast<double*>(tmu + P.max_cells);
   uint32_t cur = 0xFFFFFFFFu;
   WorkerDev W{};
   uint32_t ncell = 0;
-  const double2* tmu = tmu_all;
-  const double* tpw = tpw_all;
   double sf_w = 0.0, loss_acc = 0.0, edge_acc = 0.0;
   const double st = P.step;
   const uint32_t nblk_draw = (s + 2) / 2;  // Philox blocks per head (2 draws each)
-  auto flush = [&] {  // this warp's statistics of shard `cur`
-    double ls = loss_acc, es = edge_acc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ls += __shfl_xor_sync(FULL, ls, o);
-      es += __shfl_xor_sync(FULL, es, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicAdd(&P.loss_acc[cur], ls);
-      atomicAdd(&P.edge_acc[cur], (unsigned long long)es);
-    }
-    loss_acc = 0.0;
-    edge_acc = 0.0;
-  };
 
   for (;;) {
-    uint32_t c = 0;
-    if ((threadIdx.x & 31) == 0) c = atomicAdd(P.chunk_counter, 1u);
-    c = __shfl_sync(FULL, c, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = atomicAdd(P.chunk_counter, 1u);
+    __syncthreads();
+    const uint32_t c = s_chunk;
     uint32_t w = 0, lchunk = 0;
     if (c < P.total_chunks) {
       const uint2 cm = P.chunk_map[c];
       w = cm.x;
       lchunk = cm.y;
     }
-    if (c >= P.total_chunks || w != cur) {  // warp-uniform
-      if (cur != 0xFFFFFFFFu) flush();
+    if (c >= P.total_chunks || w != cur) {  // block-uniform
+      if (cur != 0xFFFFFFFFu) {  // flush the previous shard's statistics
+        const double ls = block_sum(loss_acc, red);
+        const double es = block_sum(edge_acc, red);
+        if (threadIdx.x == 0) {
+          atomicAdd(&P.loss_acc[cur], ls);
+          atomicAdd(&P.edge_acc[cur], (unsigned long long)es);
+        }
+        loss_acc = 0.0;
+        edge_acc = 0.0;
+      }
       if (c >= P.total_chunks) break;
       cur = w;
       W = P.workers[w];
       ncell = ABO ? C : W.n_rem;
       sf_w = M * W.local_mass / (double)s;
-      tmu = tmu_all + (size_t)w * P.max_cells;
-      tpw = tpw_all + (size_t)w * P.max_cells;
+      __syncthreads();
+      if (!P.gcells)
+        for (uint32_t q = threadIdx.x; q < ncell; q += blockDim.x) {
+          const uint32_t r = ABO ? q : P.remote_ids[W.rem_off + q];
+          const double p = ABO ? P.cell_probs[r] : P.remote_probs[W.rem_off + q];
+          tmu[q] = P.means[r];  // cell means, then their weights M p_r
+          tpw[q] = M * p;
+        }
+      __syncthreads();
     }
     const uint32_t t_base = lchunk * P.chunk_heads;
     // draw(t): the Philox draws of head t (lane b of the group computes
     // Philox block b = draws 2b, 2b+1), its tails, and the load of its
     // neighbour ids (this lane's slice of the ELL row). Executed by full warps
-    // (shuffles): chunk_heads is a multiple of GPW, so every group of the warp
-    // runs the same number of rounds; inactive groups at the end of a shard
-    // run predicated off.
+    // (shuffles): chunk_heads is a multiple of GPB, so every warp runs the
+    // same number of rounds; inactive groups at the end of a shard run
+    // predicated off.
     auto draw = [&](uint32_t t, Draw<NPL, TPL>& D) {
       D.act = t < W.draws;
       uint64_t dA = 0, dB = 0;
@@ -239,7 +227,7 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
     };
     Draw<NPL, TPL> D;
     draw(t_base + grp, D);
-    for (uint32_t j = grp; j < P.chunk_heads; j += GPW) {
+    for (uint32_t j = grp; j < P.chunk_heads; j += GPB) {
       const bool act = D.act;
       const uint32_t head = D.head, cnt = D.cnt, own_gid = D.own_gid;
       const double sf = D.sf;
@@ -250,10 +238,10 @@ __global__ void __launch_bounds__(256, HOG_MINB) k_sgd_hogwild(SgdParams P) {
       for (int i = 0; i < NPL; ++i) pn[i] = (NPL * gl + i < (int)cnt) ? ld_row<DF>(P.pos, D.nb[i]) : h;
 #pragma unroll
       for (int m = 0; m < TPL; ++m) pt[m] = (act && gl + G * m < (int)s) ? ld_row<DF>(P.pos, D.tl[m]) : h;
-      const bool more = j + GPW < P.chunk_heads;  // warp-uniform
+      const bool more = j + GPB < P.chunk_heads;  // warp-uniform
       // next head's draws and neighbour ids in flight during this head's math
       Draw<NPL, TPL> Dn;
-      if (more) draw(t_base + j + GPW, Dn);
+      if (more) draw(t_base + j + GPB, Dn);
 
       // ---- mean field over this lane's cells: S1 = M sum p q, S2 = M sum p q^2 (h - mu)
       // (own cell skipped in AllButOwn mode)

@@ -373,8 +373,7 @@ struct RankTrainer {
         smem_replay = (k + 1) * k * sizeof(double);
       }
     } else {
-      // every local worker's table (warps claim chunks of any shard)
-      smem_hog = (wts + 3 * (uint64_t)hog_cells * std::max<uint32_t>(nwl, 1)) * sizeof(double);
+      smem_hog = (wts + 3 * (uint64_t)hog_cells) * sizeof(double);
       if (smem_hog > 48 * 1024) {
         gcells = true;
         smem_hog = wts * sizeof(double);
@@ -569,13 +568,12 @@ struct RankTrainer {
     if (min_pts == ~0ull) min_pts = 1;
     const uint64_t heads_per_block = 256 / G;
     const uint64_t by_cap = std::max<uint64_t>(1, (min_pts / cap + heads_per_block - 1) / heads_per_block);
-    const uint64_t heads_per_warp = 32 / G;
     uint32_t nact = 0;
     for (auto& d : wk) nact += d.draws ? 1u : 0u;
     const uint32_t wave = (uint32_t)std::max<uint64_t>(
         1, std::min<uint64_t>(std::max<uint32_t>(nact, 1), (resident + by_cap - 1) / by_cap));
     hog_blocks = (uint32_t)std::min<uint64_t>(resident, by_cap * wave);
-    chunk_heads = (uint32_t)(heads_per_warp * hogwild_chunk_rounds());  // claimed per warp
+    chunk_heads = (uint32_t)(heads_per_block * hogwild_chunk_rounds());
     std::vector<uint32_t> nchunk(nwl);
     for (uint32_t wl = 0; wl < nwl; ++wl) {
       WorkerDev& d = wk[wl];
