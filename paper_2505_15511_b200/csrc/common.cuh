@@ -101,6 +101,9 @@ struct nomad_b200_ctx {
   int sm_count = 148;
   // statistics of the last build_knn call
   uint64_t knn_tc_uncertified = 0, knn_exhaustive = 0, knn_sub_certified = 0;
+  // pinned staging ring for bulk copies to / from caller host memory (hostcopy.cu)
+  void* pin[2] = {nullptr, nullptr};
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
 };
 
 // A set of contexts driven by one host thread (nomad_b200_group_create):

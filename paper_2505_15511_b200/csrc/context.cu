@@ -2,12 +2,15 @@
 #include <cuda_bf16.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
 
 #include "common.cuh"
+#include "hostcopy.cuh"
 #include "philox.cuh"
 
 namespace nb {
@@ -18,50 +21,101 @@ void set_last_error(const std::string& m) { g_last_error = m; }
 void bind_device(nomad_b200_ctx* c) { NB_CUDA(cudaSetDevice(c->device)); }
 
 namespace {
-constexpr size_t kCacheMin = 64ull << 20;   // blocks below this go straight to the driver
-constexpr size_t kCacheCap = 24ull << 30;   // cached bytes per device
+// Device allocations are cached: on this driver every cudaMalloc / cudaFree
+// costs ~2 ms even for a 1 MB block (NOMAD_B200_DEBUG_ALLOC, profiles/
+// r2_knn_wall.txt), and the index build makes hundreds of them. Blocks
+// >= 64 MB are reused for requests in [size / 1.5, size]; smaller ones are
+// rounded up to power-of-two classes and reused within their class.
+constexpr size_t kCacheMin = 64ull << 20;   // large blocks: best fit
+constexpr size_t kCacheCap = 24ull << 30;   // cached large bytes per device
+constexpr size_t kSmallCap = 2ull << 30;    // cached small bytes per device
 struct Cached {
   void* p;
   size_t bytes;
 };
 std::mutex g_cache_mu;
-std::vector<Cached> g_cache[64];  // per device
+std::vector<Cached> g_cache[64];  // per device, large blocks
 size_t g_cached[64];
+std::vector<void*> g_small[64][32];  // per device, per power-of-two class (2^9 .. 2^26 bytes)
+size_t g_small_bytes[64];
+
+size_t small_class(size_t bytes, int* ci) {
+  int c = 9;
+  while (((size_t)1 << c) < bytes) ++c;
+  *ci = c;
+  return (size_t)1 << c;
+}
+
+// NOMAD_B200_DEBUG_ALLOC: report driver allocations / frees slower than 2 ms
+bool alloc_dbg() {
+  static const bool on = std::getenv("NOMAD_B200_DEBUG_ALLOC") != nullptr;
+  return on;
+}
+struct SlowCall {
+  const char* what;
+  size_t bytes;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~SlowCall() {
+    if (!alloc_dbg()) return;
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 2.0) std::fprintf(stderr, "alloc: %s %zu MB took %.1f ms\n", what, bytes >> 20, ms);
+  }
+};
 
 void flush_cache(int dev) {  // caller holds the lock
   for (auto& c : g_cache[dev]) cudaFree(c.p);
   g_cache[dev].clear();
   g_cached[dev] = 0;
+  for (auto& cl : g_small[dev]) {
+    for (void* q : cl) cudaFree(q);
+    cl.clear();
+  }
+  g_small_bytes[dev] = 0;
 }
 }  // namespace
 
 void* dev_alloc(size_t bytes) {
   int dev = 0;
   NB_CUDA(cudaGetDevice(&dev));
-  if (bytes >= kCacheMin && dev < 64) {
+  size_t want = bytes;
+  if (dev < 64) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto& v = g_cache[dev];
-    size_t best = v.size();
-    for (size_t i = 0; i < v.size(); ++i)  // smallest block in [bytes, 1.5 bytes]
-      if (v[i].bytes >= bytes && v[i].bytes <= bytes + bytes / 2 &&
-          (best == v.size() || v[i].bytes < v[best].bytes))
-        best = i;
-    if (best != v.size()) {
-      void* p = v[best].p;
-      g_cached[dev] -= v[best].bytes;
-      v.erase(v.begin() + best);
-      return p;
+    if (bytes >= kCacheMin) {
+      auto& v = g_cache[dev];
+      size_t best = v.size();
+      for (size_t i = 0; i < v.size(); ++i)  // smallest block in [bytes, 1.5 bytes]
+        if (v[i].bytes >= bytes && v[i].bytes <= bytes + bytes / 2 &&
+            (best == v.size() || v[i].bytes < v[best].bytes))
+          best = i;
+      if (best != v.size()) {
+        void* p = v[best].p;
+        g_cached[dev] -= v[best].bytes;
+        v.erase(v.begin() + best);
+        return p;
+      }
+    } else {
+      int ci = 0;
+      want = small_class(bytes, &ci);
+      auto& cl = g_small[dev][ci];
+      if (!cl.empty()) {
+        void* p = cl.back();
+        cl.pop_back();
+        g_small_bytes[dev] -= want;
+        return p;
+      }
     }
   }
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes);
+  SlowCall sc{"cudaMalloc", want};
+  cudaError_t e = cudaMalloc(&p, want);
   if (e == cudaErrorMemoryAllocation && dev < 64) {
     cudaGetLastError();
     {
       std::lock_guard<std::mutex> lk(g_cache_mu);
       flush_cache(dev);
     }
-    e = cudaMalloc(&p, bytes);
+    e = cudaMalloc(&p, want);
   }
   if (e != cudaSuccess)
     fail(kInternal, std::string("CUDA error ") + cudaGetErrorString(e) + " allocating " +
@@ -71,16 +125,29 @@ void* dev_alloc(size_t bytes) {
 
 void dev_free(void* p, size_t bytes) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || bytes < kCacheMin || dev >= 64 || bytes > kCacheCap) {
+  SlowCall sc{"free", bytes};
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64 || bytes > kCacheCap) {
     cudaFree(p);
     return;
   }
   // a block is reused only once every kernel that may still touch it is done
+  // (cudaFree would synchronise the device as well)
   if (cudaDeviceSynchronize() != cudaSuccess) {
     cudaFree(p);
     return;
   }
   std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (bytes < kCacheMin) {
+    int ci = 0;
+    const size_t cls = small_class(bytes, &ci);
+    if (g_small_bytes[dev] + cls > kSmallCap) {
+      cudaFree(p);
+      return;
+    }
+    g_small[dev][ci].push_back(p);
+    g_small_bytes[dev] += cls;
+    return;
+  }
   auto& v = g_cache[dev];
   while (!v.empty() && g_cached[dev] + bytes > kCacheCap) {  // evict the oldest
     cudaFree(v.front().p);
@@ -238,6 +305,7 @@ int32_t nomad_b200_destroy(nomad_b200_ctx* c) {
   return guard([&] {
     if (!c) return;
     cudaSetDevice(c->device);
+    nb::release_ring(c);  // waits for its own copies only
     if (c->own_stream && c->stream) {
       cudaStreamSynchronize(c->stream);
       cudaStreamDestroy(c->stream);

@@ -65,7 +65,7 @@ static void fit_impl(nomad_b200_ctx* ctx, nomad_b200_group* grp, const nomad_b20
   if (grp && cfg->workers % grp->ctx.size() != 0)
     fail(kParameter, "workers must be a multiple of world_size");
   DevData dd;
-  dd.bind(data, S);
+  dd.bind(data, ctx);
   const uint64_t n = dd.n, d = dd.d, k = cfg->k;
   uint64_t C = cfg->n_clusters;
   if (C != 0) {
@@ -148,7 +148,7 @@ static void fit_impl(nomad_b200_ctx* ctx, nomad_b200_group* grp, const nomad_b20
     const auto kind = clusters_out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
                                                                   : cudaMemcpyDeviceToHost;
     if (clusters_out->assignment)
-      NB_CUDA(cudaMemcpyAsync(clusters_out->assignment, a.p, n * 4, kind, S));
+      copy_out(ctx, clusters_out->assignment, a.p, n * 4, clusters_out->location == NOMAD_B200_DEVICE);
     if (clusters_out->centroids)
       NB_CUDA(cudaMemcpyAsync(clusters_out->centroids, cent.p, C * d * 8, kind, S));
     if (clusters_out->sizes) NB_CUDA(cudaMemcpyAsync(clusters_out->sizes, sizes.p, C * 4, kind, S));
@@ -159,13 +159,12 @@ static void fit_impl(nomad_b200_ctx* ctx, nomad_b200_group* grp, const nomad_b20
   uint32_t edges = 0;
   NB_CUDA(cudaMemcpy(&edges, off.p + n, 4, cudaMemcpyDeviceToHost));
   if (graph_out) {
-    const auto kind = graph_out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
-                                                               : cudaMemcpyDeviceToHost;
-    NB_CUDA(cudaMemcpyAsync(graph_out->offsets, off.p, (n + 1) * 4, kind, S));
+    const bool dev = graph_out->location == NOMAD_B200_DEVICE;
+    copy_out(ctx, graph_out->offsets, off.p, (n + 1) * 4, dev);
     if (edges) {
-      NB_CUDA(cudaMemcpyAsync(graph_out->neighbors, nbr.p, (uint64_t)edges * 4, kind, S));
+      copy_out(ctx, graph_out->neighbors, nbr.p, (uint64_t)edges * 4, dev);
       if (graph_out->distances)
-        NB_CUDA(cudaMemcpyAsync(graph_out->distances, dist.p, (uint64_t)edges * 8, kind, S));
+        copy_out(ctx, graph_out->distances, dist.p, (uint64_t)edges * 8, dev);
     }
     graph_out->rows = n;
     graph_out->k = k;

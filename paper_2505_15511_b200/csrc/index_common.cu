@@ -180,4 +180,85 @@ void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* m
   NB_CUDA(cudaStreamSynchronize(S));
 }
 
+// ---- fast_column_means: deterministic parallel form (fixed 1024-row chunks,
+// chunk sums added in chunk order) for centres whose exact value does not
+// matter, only that it is fixed: the tensor-core kNN centring and the
+// sub-cluster certificate centres (knn_tc.cu, knn.cu). One CTA per chunk, one
+// column per thread, rows walked in order.
+namespace {
+constexpr uint32_t kMeanChunk = 1024;
+
+__global__ void k_chunk_colsum(XPtr x, uint32_t d, const uint32_t* __restrict__ members,
+                               const uint64_t* __restrict__ cbeg, const uint32_t* __restrict__ ccnt,
+                               double* __restrict__ part) {
+  const uint64_t b = cbeg[blockIdx.x];
+  const uint32_t c = ccnt[blockIdx.x];
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    uint32_t i = 0;
+    for (; i + 4 <= c; i += 4) {
+      const uint64_t r0 = members ? members[b + i] : b + i;
+      const uint64_t r1 = members ? members[b + i + 1] : b + i + 1;
+      const uint64_t r2 = members ? members[b + i + 2] : b + i + 2;
+      const uint64_t r3 = members ? members[b + i + 3] : b + i + 3;
+      a0 += (double)x[r0 * d + j];
+      a1 += (double)x[r1 * d + j];
+      a2 += (double)x[r2 * d + j];
+      a3 += (double)x[r3 * d + j];
+    }
+    for (; i < c; ++i) a0 += (double)x[(members ? members[b + i] : b + i) * (uint64_t)d + j];
+    part[(uint64_t)blockIdx.x * d + j] = (a0 + a1) + (a2 + a3);
+  }
+}
+
+__global__ void k_chunk_means(uint32_t d, const double* __restrict__ part,
+                              const uint32_t* __restrict__ sfirst, const uint32_t* __restrict__ snum,
+                              const uint64_t* __restrict__ scnt, const uint32_t* __restrict__ sid,
+                              double* __restrict__ out) {
+  const uint32_t s = blockIdx.x;
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) {
+    double a = 0.0;
+    for (uint32_t t = 0; t < snum[s]; ++t) a += part[(uint64_t)(sfirst[s] + t) * d + j];
+    out[(uint64_t)sid[s] * d + j] = a / (double)scnt[s];
+  }
+}
+}  // namespace
+
+void fast_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
+                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
+                       const std::vector<uint32_t>& seg_ids, double* out) {
+  cudaStream_t S = ctx->stream;
+  std::vector<uint64_t> cb;
+  std::vector<uint32_t> cc, sfirst, snum, sid;
+  std::vector<uint64_t> scnt;
+  for (size_t s = 0; s < seg_ids.size(); ++s) {
+    if (!cnt[s]) continue;
+    sfirst.push_back((uint32_t)cb.size());
+    for (uint64_t o = 0; o < cnt[s]; o += kMeanChunk) {
+      cb.push_back(beg[s] + o);
+      cc.push_back((uint32_t)std::min<uint64_t>(kMeanChunk, cnt[s] - o));
+    }
+    snum.push_back((uint32_t)(cb.size() - sfirst.back()));
+    scnt.push_back(cnt[s]);
+    sid.push_back(seg_ids[s]);
+  }
+  if (cb.empty()) return;
+  const uint32_t nch = (uint32_t)cb.size(), nseg = (uint32_t)sid.size();
+  DBuf<uint64_t> cb_d(nch), scnt_d(nseg);
+  DBuf<uint32_t> cc_d(nch), sf_d(nseg), sn_d(nseg), sid_d(nseg);
+  DBuf<double> part((uint64_t)nch * d);
+  NB_CUDA(cudaMemcpyAsync(cb_d.p, cb.data(), nch * 8, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(cc_d.p, cc.data(), nch * 4, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(sf_d.p, sfirst.data(), nseg * 4, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(sn_d.p, snum.data(), nseg * 4, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(scnt_d.p, scnt.data(), nseg * 8, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(sid_d.p, sid.data(), nseg * 4, cudaMemcpyHostToDevice, S));
+  const unsigned th = (unsigned)std::min<uint64_t>(256, (d + 31) / 32 * 32);
+  k_chunk_colsum<<<nch, th, 0, S>>>(x, (uint32_t)d, members, cb_d.p, cc_d.p, part.p);
+  note_launch(ctx, "k_chunk_colsum");
+  k_chunk_means<<<nseg, th, 0, S>>>((uint32_t)d, part.p, sf_d.p, sn_d.p, scnt_d.p, sid_d.p, out);
+  note_launch(ctx, "k_chunk_means");
+  NB_CUDA(cudaStreamSynchronize(S));
+}
+
 }  // namespace nb

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hostcopy.cuh"
 
 namespace nb {
 
@@ -131,7 +132,8 @@ struct DevData {
   uint64_t n = 0, d = 0;
   DBuf<float> owned;
   DBuf<uint16_t> owned16;
-  void bind(const nomad_b200_dataset_view* v, cudaStream_t st) {
+  // host rows are uploaded through the context's pinned staging ring
+  void bind(const nomad_b200_dataset_view* v, nomad_b200_ctx* ctx) {
     if (!v || !v->data) fail(kParameter, "dataset view is NULL");
     n = v->rows;
     d = v->dims;
@@ -144,11 +146,11 @@ struct DevData {
       x.p = v->data;
     } else if (x.bf) {
       owned16.alloc(n * d);
-      NB_CUDA(cudaMemcpyAsync(owned16.p, v->data, n * d * 2, cudaMemcpyHostToDevice, st));
+      copy_h2d(ctx, owned16.p, v->data, n * d * 2);
       x.p = owned16.p;
     } else {
       owned.alloc(n * d);
-      NB_CUDA(cudaMemcpyAsync(owned.p, v->data, n * d * 4, cudaMemcpyHostToDevice, st));
+      copy_h2d(ctx, owned.p, v->data, n * d * 4);
       x.p = owned.p;
     }
   }
@@ -174,6 +176,11 @@ void group_by_label(nomad_b200_ctx* ctx, const uint32_t* labels, uint64_t n, uin
 void seq_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
                       const std::vector<uint32_t>& seg_ids, double* out, bool carry = false);
+// Same outputs up to rounding, summed in a fixed parallel order (1024-row
+// chunks): for centres that only need to be fixed, not the reference's value.
+void fast_column_means(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
+                       const std::vector<uint64_t>& beg, const std::vector<uint64_t>& cnt,
+                       const std::vector<uint32_t>& seg_ids, double* out);
 
 // Exact global kNN of m sampled points (knn.cu): out_ids_d[v * k + r] = the
 // r-th smallest (reference fp64 distance, id) key of point qlist_d[v] among

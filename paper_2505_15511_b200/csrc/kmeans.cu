@@ -798,7 +798,7 @@ void export_clusters(KMeans& km, nomad_b200_clusters* out) {
   const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
                                                        : cudaMemcpyDeviceToHost;
   if (out->assignment)
-    NB_CUDA(cudaMemcpyAsync(out->assignment, km.a.p, km.n * 4, kind, S));
+    copy_out(km.ctx, out->assignment, km.a.p, km.n * 4, out->location == NOMAD_B200_DEVICE);
   if (out->centroids)
     NB_CUDA(cudaMemcpyAsync(out->centroids, km.cent.p, (uint64_t)km.C * km.d * 8, kind, S));
   if (out->sizes) NB_CUDA(cudaMemcpyAsync(out->sizes, km.sizes_d.p, km.C * 4, kind, S));
@@ -813,7 +813,10 @@ void import_clusters(KMeans& km, const nomad_b200_clusters* in) {
   const auto kind = in->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
                                                       : cudaMemcpyHostToDevice;
   if (!in->assignment || !in->centroids) fail(kParameter, "init assignment/centroids are NULL");
-  NB_CUDA(cudaMemcpyAsync(km.a.p, in->assignment, km.n * 4, kind, S));
+  if (in->location == NOMAD_B200_DEVICE)
+    NB_CUDA(cudaMemcpyAsync(km.a.p, in->assignment, km.n * 4, kind, S));
+  else
+    copy_h2d(km.ctx, km.a.p, in->assignment, km.n * 4);
   NB_CUDA(cudaMemcpyAsync(km.cent.p, in->centroids, (uint64_t)km.C * km.d * 8, kind, S));
   NB_CUDA(cudaStreamSynchronize(S));
 }
@@ -828,7 +831,7 @@ int32_t nomad_b200_default_kmeans_tol(nomad_b200_ctx* ctx, const nomad_b200_data
     if (!ctx || !tol_out) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
-    dd.bind(data, ctx->stream);
+    dd.bind(data, ctx);
     *tol_out = default_tol_exact(ctx, dd.x, dd.n, dd.d);
   });
 }
@@ -839,7 +842,7 @@ int32_t nomad_b200_lsh_init(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* 
     if (!ctx || !out) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
-    dd.bind(data, ctx->stream);
+    dd.bind(data, ctx);
     if (n_clusters < 2 || n_clusters > dd.n)
       fail(kParameter, "cluster count must be in [2, n]; got " + std::to_string(n_clusters));
     KMeans km(ctx, dd.x, dd.n, dd.d, (uint32_t)n_clusters);
@@ -855,7 +858,7 @@ int32_t nomad_b200_kmeans_em(nomad_b200_ctx* ctx, const nomad_b200_dataset_view*
     if (!ctx || !inout) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
-    dd.bind(data, ctx->stream);
+    dd.bind(data, ctx);
     if (inout->rows != dd.n || inout->dims != dd.d)
       fail(kParameter, "init assignment does not match dataset");
     if (inout->n_clusters < 1) fail(kParameter, "n_clusters must be >= 1");
@@ -875,7 +878,7 @@ int32_t nomad_b200_kmeans_em_default_tol(nomad_b200_ctx* ctx, const nomad_b200_d
     if (!ctx || !inout) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
-    dd.bind(data, ctx->stream);
+    dd.bind(data, ctx);
     if (inout->rows != dd.n || inout->dims != dd.d)
       fail(kParameter, "init assignment does not match dataset");
     if (inout->n_clusters < 1) fail(kParameter, "n_clusters must be >= 1");

@@ -992,7 +992,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
     }
     od.alloc(m);
     NB_CUDA(cudaMemcpyAsync(od.p, order.data(), m * 4, cudaMemcpyHostToDevice, S));
-    seq_column_means(ctx, xr.p, d, od.p, beg, cnt, ids, sc.p);
+    fast_column_means(ctx, xr.p, d, od.p, beg, cnt, ids, sc.p);  // any fixed centre
     std::vector<uint32_t> b32(beg.begin(), beg.end());
     segb.alloc(csub);
     NB_CUDA(cudaMemcpyAsync(segb.p, b32.data(), csub * 4, cudaMemcpyHostToDevice, S));
@@ -1503,7 +1503,7 @@ static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     bind_device(ctx);
     cudaStream_t S = ctx->stream;
     DevData dd;
-    dd.bind(data, S);
+    dd.bind(data, ctx);
     if (clusters->rows != dd.n) fail(kParameter, "clusters and dataset cover different points");
     if (!clusters->assignment) fail(kParameter, "assignment is NULL");
     const uint32_t C = (uint32_t)clusters->n_clusters;
@@ -1511,7 +1511,7 @@ static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     const uint32_t* a = clusters->assignment;
     if (clusters->location != NOMAD_B200_DEVICE) {
       a_own.alloc(dd.n);
-      NB_CUDA(cudaMemcpyAsync(a_own.p, a, dd.n * 4, cudaMemcpyHostToDevice, S));
+      copy_h2d(ctx, a_own.p, a, dd.n * 4);
       a = a_own.p;
     }
     if (knn_mode != NOMAD_B200_KNN_EXACT && knn_mode != NOMAD_B200_KNN_BF16 &&
@@ -1525,20 +1525,30 @@ static int32_t build_knn_impl(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
         own[owned[i]] = 1;
       }
     }
+    const bool dbg = std::getenv("NOMAD_B200_DEBUG_KNN") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!dbg) return;
+      NB_CUDA(cudaStreamSynchronize(S));
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "knn call  %-28s %8.1f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - t0).count());
+      t0 = now;
+    };
+    lap("inputs");
     KnnResult R;
     build_knn_exact(ctx, dd.x, dd.n, dd.d, a, C, (uint32_t)k, R, knn_mode, owned ? &own : nullptr);
+    lap("build");
     ctx->knn_tc_uncertified = R.tc_uncertified;
     ctx->knn_sub_certified = R.sub_certified;
     ctx->knn_exhaustive = R.fallbacks;
-    const auto kind = out->location == NOMAD_B200_DEVICE ? cudaMemcpyDeviceToDevice
-                                                         : cudaMemcpyDeviceToHost;
-    NB_CUDA(cudaMemcpyAsync(out->offsets, R.offsets.p, (dd.n + 1) * 4, kind, S));
+    const bool dev = out->location == NOMAD_B200_DEVICE;
+    copy_out(ctx, out->offsets, R.offsets.p, (dd.n + 1) * 4, dev);
     if (R.edges) {
-      NB_CUDA(cudaMemcpyAsync(out->neighbors, R.nb.p, R.edges * 4, kind, S));
-      if (out->distances)
-        NB_CUDA(cudaMemcpyAsync(out->distances, R.dist.p, R.edges * 8, kind, S));
+      copy_out(ctx, out->neighbors, R.nb.p, R.edges * 4, dev);
+      if (out->distances) copy_out(ctx, out->distances, R.dist.p, R.edges * 8, dev);
     }
-    NB_CUDA(cudaStreamSynchronize(S));
+    lap("outputs");
     out->rows = dd.n;
     out->k = k;
   });
@@ -1571,7 +1581,7 @@ int32_t nomad_b200_knn_recall(nomad_b200_ctx* ctx, const nomad_b200_dataset_view
     bind_device(ctx);
     cudaStream_t S = ctx->stream;
     DevData dd;
-    dd.bind(data, S);
+    dd.bind(data, ctx);
     const uint64_t n = dd.n, k = graph->k;
     const uint32_t C = (uint32_t)clusters->n_clusters;
     if (graph->rows != n || clusters->rows != n) fail(kParameter, "row counts differ");

@@ -449,12 +449,40 @@ static void tc_lap(cudaStream_t S, const char* what) {
   t_last = now;
 }
 
+// Padded cluster-contiguous layout of one group: row p of cluster slot g
+// (padded start gl[3g]) holds member p - gl[3g] (or no row: padding);
+// rcl[p] = that cluster's id. Rows past the last slot belong to slot 0.
+__global__ void k_tc_layout(const uint32_t* __restrict__ mem, const uint32_t* __restrict__ grp,
+                            const uint64_t* __restrict__ gl, uint32_t G, uint64_t rows,
+                            uint32_t* perm, uint32_t* rcl) {
+  const uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p >= rows) return;
+  uint32_t lo = 0, hi = G;  // last slot with start <= p
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (gl[3 * mid] <= p) lo = mid; else hi = mid;
+  }
+  const uint64_t t = p - gl[3 * lo];
+  const bool in = gl[3 * lo] <= p && t < gl[3 * lo + 2];
+  perm[p] = in ? mem[gl[3 * lo + 1] + t] : 0xFFFFFFFFu;
+  rcl[p] = grp[lo];
+}
+
+// cmax[c] = max over the cluster's padded rows of sqrt(norm) * 1.0001 (the
+// float bits of non-negative values order like unsigned integers)
+__global__ void k_tc_cmax(const float* __restrict__ norms, const uint32_t* __restrict__ rcl,
+                          uint64_t rows, unsigned* cmax) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  atomicMax(cmax + rcl[i], __float_as_uint(sqrtf(norms[i]) * 1.0001f));
+}
+
 // One group of clusters: the padded cluster-contiguous 16-bit copy (tiles
 // never straddle a cluster start), its norms and scale, and the candidate
 // kernel; candidates land at the rows' global ids.
 static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, bool fp16, int KP,
                      uint32_t C,
-                     const std::vector<uint64_t>& off, const std::vector<uint32_t>& mem_h,
+                     const std::vector<uint64_t>& off, const uint32_t* mem_d,
                      const std::vector<uint32_t>& grp, const double* means_p,
                      DBuf<uint32_t>& cand_ids, DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt) {
   cudaStream_t S = ctx->stream;
@@ -465,20 +493,25 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
   const uint64_t rows_pad = std::max<uint64_t>(pstart[G], TM);
   if (rows_pad >= (1ull << 31)) fail(kSize, "tensor-core kNN: too many rows for TMA coordinates");
   // rcl: the row's cluster id (means, certificate); tiles carry the group-local cluster index
-  std::vector<uint32_t> perm(rows_pad, 0xFFFFFFFFu), rcl(rows_pad, grp[0]);
   std::vector<TcTile> tiles;
+  std::vector<uint64_t> gl(3 * (size_t)G);  // per group cluster: padded start, member offset, size
   for (uint32_t g = 0; g < G; ++g) {
     const uint32_t r = grp[g];
     const uint64_t sz = off[r + 1] - off[r];
-    for (uint64_t t = 0; t < (pstart[g + 1] - pstart[g]); ++t) rcl[pstart[g] + t] = r;
-    for (uint64_t t = 0; t < sz; ++t) perm[pstart[g] + t] = mem_h[off[r] + t];
+    gl[3 * g] = pstart[g];
+    gl[3 * g + 1] = off[r];
+    gl[3 * g + 2] = sz;
     for (uint64_t q = 0; q < sz; q += TM)
       tiles.push_back(TcTile{(uint32_t)(pstart[g] + q), (uint32_t)pstart[g], (uint32_t)sz,
                              (uint32_t)q, r});
   }
-  DBuf<uint32_t> perm_d(rows_pad), rcl_d(rows_pad);
-  NB_CUDA(cudaMemcpyAsync(perm_d.p, perm.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
-  NB_CUDA(cudaMemcpyAsync(rcl_d.p, rcl.data(), rows_pad * 4, cudaMemcpyHostToDevice, S));
+  DBuf<uint32_t> perm_d(rows_pad), rcl_d(rows_pad), grp_d(G);
+  DBuf<uint64_t> gl_d(3 * (size_t)G);
+  NB_CUDA(cudaMemcpyAsync(grp_d.p, grp.data(), G * 4, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemcpyAsync(gl_d.p, gl.data(), gl.size() * 8, cudaMemcpyHostToDevice, S));
+  k_tc_layout<<<(unsigned)((rows_pad + 255) / 256), 256, 0, S>>>(mem_d, grp_d.p, gl_d.p, G,
+                                                                 rows_pad, perm_d.p, rcl_d.p);
+  note_launch(ctx, "k_tc_layout");
   tc_lap(S, "layout");
   // power-of-two scale keeping |u| well inside the 16-bit range
   DBuf<unsigned int> amax(1);
@@ -507,13 +540,11 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
   note_launch(ctx, "k_tc_prep");
   tc_lap(S, "absmax + prep");
   // per-cluster max ||u_b|| (scaled), for the certificate
-  std::vector<float> nh(rows_pad), cmax(C, 0.f);
-  NB_CUDA(cudaMemcpyAsync(nh.data(), norms.p, rows_pad * 4, cudaMemcpyDeviceToHost, S));
-  NB_CUDA(cudaStreamSynchronize(S));
-  for (uint64_t row = 0; row < rows_pad; ++row)
-    cmax[rcl[row]] = std::max(cmax[rcl[row]], std::sqrt(nh[row]) * 1.0001f);
   DBuf<float> cmax_d(C);
-  NB_CUDA(cudaMemcpyAsync(cmax_d.p, cmax.data(), C * 4, cudaMemcpyHostToDevice, S));
+  NB_CUDA(cudaMemsetAsync(cmax_d.p, 0, C * 4, S));
+  k_tc_cmax<<<(unsigned)((rows_pad + 255) / 256), 256, 0, S>>>(norms.p, rcl_d.p, rows_pad,
+                                                               reinterpret_cast<unsigned*>(cmax_d.p));
+  note_launch(ctx, "k_tc_cmax");
 
   tc_lap(S, "norms + cmax");
   if (tiles.empty()) return;
@@ -555,7 +586,8 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
   DBuf<uint32_t> mem;
   std::vector<uint64_t> off;
   group_by_label(ctx, assign_d, n, C, mem, off);
-  // centring vectors: the clusters' exact means (any fixed vector is valid)
+  // centring vectors: the clusters' means in a fixed parallel summation order
+  // (any fixed vector keeps the certificate valid)
   DBuf<double> means((uint64_t)C * d);
   NB_CUDA(cudaMemsetAsync(means.p, 0, (uint64_t)C * d * 8, S));
   {
@@ -567,11 +599,9 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
         cnt.push_back(off[r + 1] - off[r]);
         rows.push_back(r);
       }
-    seq_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
+    fast_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
   }
   tc_lap(S, "grouping + means");
-  std::vector<uint32_t> mem_h(off[C]);
-  NB_CUDA(cudaMemcpy(mem_h.data(), mem.p, off[C] * 4, cudaMemcpyDeviceToHost));
   cand_ids.alloc(n * (uint64_t)KP);
   cand_lb.alloc(n);
   cand_cnt.alloc(n);
@@ -606,7 +636,7 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
       acc += pr;
       ++gi;
     }
-    tc_group(ctx, x, d, dpad, fp16, KP, C, off, mem_h, grp, means.p, cand_ids, cand_lb, cand_cnt);
+    tc_group(ctx, x, d, dpad, fp16, KP, C, off, mem.p, grp, means.p, cand_ids, cand_lb, cand_cnt);
   }
 }
 

@@ -176,7 +176,7 @@ int32_t nomad_b200_neighborhood_preservation(nomad_b200_ctx* ctx,
     bind_device(ctx);
     cudaStream_t S = ctx->stream;
     DevData dd;
-    dd.bind(high, S);
+    dd.bind(high, ctx);
     const uint64_t n = dd.n;
     if (k >= n) fail(kParameter, "k must be < n");
     if (k < 1 || k > (uint64_t)LKMAX)
@@ -322,7 +322,7 @@ int32_t nomad_b200_random_triplet_accuracy(nomad_b200_ctx* ctx,
     bind_device(ctx);
     cudaStream_t S = ctx->stream;
     DevData dd;
-    dd.bind(high, S);
+    dd.bind(high, ctx);
     const uint64_t n = dd.n;
     if (n < 3) fail(kParameter, "need at least 3 points");
     if (n_triplets < 1) fail(kParameter, "need at least 1 triplet");

@@ -470,7 +470,7 @@ static int32_t pca_entry(nomad_b200_ctx* ctx, const nomad_b200_dataset_view* dat
     if (!ctx || !layout_out) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
-    dd.bind(data, ctx->stream);
+    dd.bind(data, ctx);
     if (location == NOMAD_B200_DEVICE) {
       pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, layout_out, fast);
     } else {
@@ -500,7 +500,7 @@ extern "C" int32_t nomad_b200_debug_cov(nomad_b200_ctx* ctx, const nomad_b200_da
     if (!ctx || !mean_host || !out_host) fail(kParameter, "NULL argument");
     bind_device(ctx);
     DevData dd;
-    dd.bind(data, ctx->stream);
+    dd.bind(data, ctx);
     DBuf<double> m(dd.d), c(dd.d * dd.d);
     NB_CUDA(cudaMemcpy(m.p, mean_host, dd.d * 8, cudaMemcpyHostToDevice));
     covariance_sums(ctx, dd.x, dd.n, dd.d, m.p, c.p);

@@ -58,7 +58,7 @@ void index_rank(nomad_b200_ctx* ctx, Comm* comm, const nomad_b200_dataset_view* 
                 double tol, uint64_t W, uint64_t k, int32_t knn_mode, ShardOut& out) {
   cudaStream_t S = ctx->stream;
   DevData dd;
-  dd.bind(rows, S);
+  dd.bind(rows, ctx);
   const uint64_t n = dd.n, d = dd.d;
   const int world = comm->world, rank = comm->rank;
   if (W % (uint64_t)world) fail(kParameter, "workers must be a multiple of world_size");

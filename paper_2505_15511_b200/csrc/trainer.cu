@@ -23,6 +23,7 @@
 #include <random>
 
 #include "common.cuh"
+#include "hostcopy.cuh"
 #include "plan.cuh"
 #include "replay.cuh"
 #include "sgd_kernels.cuh"
@@ -965,7 +966,7 @@ struct RankTrainer {
     const double* src = in;
     if (loc != NOMAD_B200_DEVICE) {
       if (stage.n != n) stage.alloc(n);
-      NB_CUDA(cudaMemcpyAsync(stage.p, in, n * 16, cudaMemcpyHostToDevice, S));
+      copy_h2d(ctx, stage.p, in, n * 16);
       src = reinterpret_cast<const double*>(stage.p);
     }
     if (n_loc) {
@@ -992,8 +993,7 @@ struct RankTrainer {
         launch_scatter_layout(pos.p, orig_of_d.p, n_loc, stage.p, S);
         launched("k_scatter_layout");
       }
-      NB_CUDA(cudaMemcpyAsync(out, stage.p, n * 16, cudaMemcpyDeviceToHost, S));
-      NB_CUDA(cudaStreamSynchronize(S));
+      copy_d2h(ctx, out, stage.p, n * 16);
       return;
     }
     std::vector<double> h(2 * (size_t)n_loc);

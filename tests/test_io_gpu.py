@@ -83,3 +83,51 @@ def test_resume_from_checkpoint(port, ctx, tmp_path, mode):
         assert np.array_equal(np.asarray(l_res), np.asarray(l_full)[3:])
     else:
         assert abs(l_res[-1] - l_full[-1]) < 0.05 * abs(l_full[-1])
+
+
+def test_staged_host_copies_roundtrip(ctx):
+    """Bulk copies to / from pageable host memory go through the context's
+    pinned two-buffer ring (hostcopy.cu, 64 MB chunks, several host threads):
+    a layout of 5,000,003 rows (80 MB: two chunks, the second partial) set
+    from and read back into fresh numpy arrays is unchanged, and equals the
+    device-side read."""
+    import torch
+    import paper_2505_15511_b200 as nb
+    n, C, k = 5_000_003, 8, 4
+    rng = np.random.default_rng(5)
+    a = (np.arange(n) % C).astype(np.uint32)
+    q = np.arange(n) // C
+    m = (n - a.astype(np.int64) + C - 1) // C
+    nbr = np.stack([(a + C * ((q + t + 1) % m)).astype(np.uint32) for t in range(k)], 1).reshape(-1)
+    off = (np.arange(n + 1, dtype=np.uint64) * k).astype(np.uint32)
+    g = nb.KnnGraph(n, k, off, nbr, np.zeros(0))
+    c = nb.ClusterAssignment(a, C, 16, np.zeros(0), np.zeros(0))
+    init = rng.standard_normal((n, 2))
+    tr = nb.Trainer(g, c, init, nb.TrainConfig(epochs=10, workers=2, seed=3, k=k), ctx=ctx)
+    lay = tr.layout()
+    assert np.array_equal(lay, init)
+    new = rng.standard_normal((n, 2))
+    tr.set_layout(new)
+    dev = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    tr.layout(dev)
+    assert np.array_equal(dev.cpu().numpy(), new)
+    assert np.array_equal(tr.layout(), new)
+
+
+def test_host_dataset_upload_matches_device(ctx):
+    """A host (pageable) dataset above the staging threshold gives the same
+    k-means and kNN graph as the same rows already on the device."""
+    import torch
+    import paper_2505_15511_b200 as nb
+    x = nb.generate_mixture(200_003, 64, 6, 10.0, 9, ctx=ctx)  # 51 MB of f32 rows
+    xh = x.cpu().numpy()
+    cd = nb.kmeans_em_default_tol(x, nb.lsh_init(x, 6, 7, ctx=ctx), 100, ctx=ctx)
+    ch = nb.kmeans_em_default_tol(xh, nb.lsh_init(xh, 6, 7, ctx=ctx), 100, ctx=ctx)
+    assert np.array_equal(cd.assignment, ch.assignment)
+    assert np.array_equal(cd.centroids, ch.centroids)
+    gd = nb.build_knn(x, cd, 15, ctx=ctx)
+    gh = nb.build_knn(xh, ch, 15, ctx=ctx)
+    assert np.array_equal(gd.offsets, gh.offsets)
+    assert np.array_equal(gd.neighbors, gh.neighbors)
+    assert np.array_equal(gd.distances, gh.distances)
+    torch.cuda.synchronize()
