@@ -395,14 +395,45 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
 
 // Warp-per-draw form (1 + k + s <= 32: the default k = 15, s = 5): lane u
 // owns update slot u (0 head, 1..cnt neighbours, then tails) and its pred
-// slot; every term is computed on its lane with the reference's operations
-// and lane 0 accumulates the sums in the reference's order from shared
-// memory, so results are bit-identical to the sequential
-// loop while one draw's ~100 divisions run 32-wide. Warps claim 8
-// consecutive draws of a worker (worker-interleaved) and run them in order.
-constexpr uint32_t kDfBatch = 8;
+// slot; every term is computed on its lane with the reference's operations,
+// staged in the warp's shared scratch, and every lane accumulates the sums in
+// the reference's order from broadcast reads over warp-uniform bounds (SURVEY
+// Appendix A), so all lanes hold bits identical to the sequential loop while
+// one draw's ~100 divisions run 32-wide. (Chains read through shuffles cost
+// a shuffle round trip per term; profiles/r2_replay_chain.txt.)
+constexpr uint32_t kDfBatch = 8;  // R.total_chunks granularity reported for the warp form
 
-__global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDev R) {
+// Chains of the warp form: acc[c] = acc[c] (+|-) v[c][j] for j in [j0, j1)
+// whose bit in `mask` is set, in ascending j — the reference's summation
+// order. Terms sit in the warp's shared scratch (broadcast reads); loads are
+// issued 8 at a time so one shared-memory latency covers 8 dependent adds.
+template <int NC, bool SUB>
+__device__ __forceinline__ void df_chains(double (&acc)[NC], const double* const (&v)[NC],
+                                          uint32_t j0, uint32_t j1, uint32_t mask) {
+  uint32_t j = j0;
+  for (; j + 8 <= j1; j += 8) {
+    double x[NC][8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) x[c][e] = v[c][j + e];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if ((mask >> (j + e)) & 1u)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          acc[c] = SUB ? __dsub_rn(acc[c], x[c][e]) : __dadd_rn(acc[c], x[c][e]);
+  }
+  for (; j < j1; ++j)
+    if ((mask >> j) & 1u)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] = SUB ? __dsub_rn(acc[c], v[c][j]) : __dadd_rn(acc[c], v[c][j]);
+}
+
+#ifndef DF_MINB
+#define DF_MINB 3  // min resident blocks per SM of the warp form (register cap: 80)
+#endif
+__global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P, ReplayDev R) {
   extern __shared__ __align__(16) double sm[];
   const uint32_t k = P.k, s = P.s, C = P.n_clusters, T = R.T;
   double* wt = sm;
@@ -435,190 +466,283 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow_warp(SgdParams P, ReplayDe
        c += nwarps) {
     const uint32_t w = (uint32_t)(c % R.nwl);
     const WorkerDev W = P.workers[w];
+    const uint32_t t = (uint32_t)(c / R.nwl);
+    if (t >= W.draws) continue;
+    const uint32_t i = R.draw_base[w] + t;
+    // ---- everything that does not depend on positions, before any wait:
+    // slot points (head, neighbours, tails), predecessor slots, weights, sf
+    const uint32_t head = R.heads[i];
+    const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
+    const uint32_t nsl = 1 + cnt + s;
+    const bool is_nb = lane >= 1 && lane <= cnt;
+    const bool is_tail = lane > cnt && lane < nsl;
+    uint32_t pt = head;
+    if (is_nb) pt = P.ell[(size_t)head * P.kpad + lane - 1];
+    else if (is_tail) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
+    const uint32_t pq = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
+    const uint8_t* dn = R.done + R.draw_base[w];
+    uint32_t own = 0;
+    double lm = W.local_mass;
+    if (P.all_but_own) {
+      own = P.lclusters[P.cl_of[head]].gid;
+      lm = P.cell_probs[own];
+    }
+    const uint32_t nr = P.all_but_own ? C : W.n_rem;
+    const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
+    const double wj = is_nb ? wt[cnt * k + lane - 1] : 0.0;
+#ifdef DF_TRACE  // per-stage SM cycles of sampled draws (diagnostic build only)
+    long long tr[8];
+    tr[0] = clock64();
+#define DF_MARK(j) tr[j] = clock64()
+#else
+#define DF_MARK(j)
+#endif
+    // Wait until the predecessors of the lanes in `mine` are done. Acquire:
+    // a lane's later load of its slot's position sees the predecessor's
+    // writes; a lane stops polling once its flag is set. Returns true when
+    // the watchdog fired (a schedule bug: report, never hang).
+    auto wait_for = [&](bool mine) -> bool {
+      uint32_t spins = 0, nap = min(64u, R.nap_cap);
+      bool abort = false, ok = !mine || pq == 0xFFFFFFFFu;
+      for (;;) {
+        if (!ok) ok = ld_acquire_u8(dn + pq) != 0;
+        if (__all_sync(FULL, ok)) break;
+        if ((++spins & 63) == 0 &&
+            (*reinterpret_cast<volatile uint32_t*>(R.stall) || spins > (1u << 22))) {
+          abort = true;
+          break;
+        }
+        // exponential back-off: thousands of waiting warps share L2
+        __nanosleep(nap);
+        nap = min(nap * 2, R.nap_cap);
+      }
+      if (__any_sync(FULL, abort)) {
+        if (lane == 0) atomicExch(R.stall, 1u);
+        return true;
+      }
+      return false;
+    };
+    // ---- phase A: the head and the tails. Everything up to bg depends only
+    // on them (and the epoch's cell means), so it overlaps the wait for the
+    // neighbours — in the kNN graph the long dependency chains run through
+    // heavily listed points, i.e. through neighbour slots. Slot lanes: 0 head,
+    // 1..cnt neighbours, cnt+1.. tails; predecessor lanes follow the touch
+    // layout of k_replay_touch (0 head, 1..k neighbour slots, 1+k.. tails)
+    // and a repeated point carries its predecessor on its first slot only, so
+    // a neighbour slot holding a tail's point belongs to phase A as well.
+    const uint32_t tailmask = __ballot_sync(FULL, is_tail);
+    const uint32_t grp = __match_any_sync(FULL, lane < nsl ? pt : 0xFFFFFFFFu);
+    const bool needA = lane < nsl && (lane == 0 || (grp & (tailmask | 1u)) != 0);
+    uint32_t sl = lane;  // predecessor lane -> slot lane
+    if (lane > k && lane < 1 + k + s) sl = 1 + cnt + (lane - 1 - k);
+    else if (lane > cnt && lane <= k) sl = 0;  // padded neighbour slots (no predecessor)
+    const bool predA = __shfl_sync(FULL, needA, sl & 31);
+    // apply grouping (positions not needed): a point in several slots gets
+    // its updates in slot order from the lane of its first slot
+    const bool slot = lane < nsl && (lane == 0 || !P.head_only);
+    const uint32_t act = __ballot_sync(FULL, slot);
+    const uint32_t same = __match_any_sync(FULL, slot ? pt : 0xFFFFFFFFu) & act;
+    if (wait_for(predA)) continue;
+    __syncwarp();  // the polling lanes' acquires before the other lanes' loads
+    double2 pv = make_double2(0.0, 0.0);
+    if (needA) pv = ldpos(P.pos + pt);
+    const double hx = __shfl_sync(FULL, pv.x, 0), hy = __shfl_sync(FULL, pv.y, 0);
+    DF_MARK(1);
+    // noise terms (objective.hpp:113-145): terms on their lanes, every sum in
+    // the reference's order by every lane from the staged terms
+    // (the first 64 cells also keep q_r, p_r and h - mu_r for the mean
+    // repulsion, which then needs only bgs after the neighbours arrive)
+    double remote_sum = 0.0;
+    double cq0 = 0.0, cp0 = 0.0, cdx0 = 0.0, cdy0 = 0.0, cq1 = 0.0, cp1 = 0.0, cdx1 = 0.0,
+           cdy1 = 0.0;
+    uint32_t cu0 = 0u, cu1 = 0u;
+    for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      double term = 0.0;
+      bool use = false;
+      if (q < nr) {
+        const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
+        if (!(P.all_but_own && r == own)) {
+          const double mx = cm[3 * r], my = cm[3 * r + 1], pr = cm[3 * r + 2];
+          const double qr = cauchy_rn(hx, hy, mx, my);
+          term = __dmul_rn(pr, qr);
+          use = true;
+          if (q0 == 0) {
+            cq0 = qr;
+            cp0 = pr;
+            cdx0 = __dsub_rn(hx, mx);
+            cdy0 = __dsub_rn(hy, my);
+          } else if (q0 == 32) {
+            cq1 = qr;
+            cp1 = pr;
+            cdx1 = __dsub_rn(hx, mx);
+            cdy1 = __dsub_rn(hy, my);
+          }
+        }
+      }
+      const uint32_t um = __ballot_sync(FULL, use);
+      if (q0 == 0) cu0 = um;
+      else if (q0 == 32) cu1 = um;
+      sa[lane] = term;
+      __syncwarp();
+      double acc[1] = {remote_sum};
+      const double* const v[1] = {sa};
+      df_chains<1, false>(acc, v, 0, min(32u, nr - q0), um);
+      remote_sum = acc[0];
+      __syncwarp();
+    }
+    const double mean_field = __dmul_rn(M, remote_sum);
+    const double qn = is_tail ? cauchy_rn(hx, hy, pv.x, pv.y) : 0.0;
+    double qsum;
     {
-      const uint32_t t = (uint32_t)(c / R.nwl);
-      if (t >= W.draws) continue;
-      const uint32_t i = R.draw_base[w] + t;
-      // slot points (head, neighbours, tails): epoch-static, loaded before the
-      // wait so that only the position loads follow the predecessors
-      const uint32_t head = R.heads[i];
-      const uint32_t cnt = P.ncnt ? P.ncnt[head] : k;
-      const uint32_t nsl = 1 + cnt + s;
-      uint32_t pt = head;
-      if (lane >= 1 && lane <= cnt) pt = P.ell[(size_t)head * P.kpad + lane - 1];
-      else if (lane > cnt && lane < nsl) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
-      // ---- wait until every predecessor is done
-      {
-        const uint32_t q = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
-        const uint8_t* dn = R.done + R.draw_base[w];
-        uint32_t spins = 0, nap = min(64u, R.nap_cap);
-        bool abort = false, ok = q == 0xFFFFFFFFu;
-        for (;;) {
-          // acquire: this lane's later loads (its slot's position) see the
-          // predecessor's writes; a lane stops polling once its flag is set
-          if (!ok) ok = ld_acquire_u8(dn + q) != 0;
-          if (__all_sync(FULL, ok)) break;
-          if ((++spins & 63) == 0 &&
-              (*reinterpret_cast<volatile uint32_t*>(R.stall) || spins > (1u << 22))) {
-            abort = true;  // watchdog (a schedule bug): report, never hang
-            break;
-          }
-          // exponential back-off: thousands of waiting warps share L2
-          __nanosleep(nap);
-          nap = min(nap * 2, R.nap_cap);
-        }
-        if (__any_sync(FULL, abort)) {
-          if (lane == 0) atomicExch(R.stall, 1u);
-          continue;
-        }
-      }
-      const double2 pv = ldpos(P.pos + pt);  // every slot's position before this draw
-      const double hx = __shfl_sync(FULL, pv.x, 0), hy = __shfl_sync(FULL, pv.y, 0);
-      // ---- noise terms (objective.hpp:113-145). Terms are computed on their
-      // lanes; every sum is then taken in the reference's order by all lanes
-      // together from shuffles (unrolled: the adds' dependency chain is the
-      // only serial part), so every lane holds the same bits.
-      uint32_t own = 0;
-      double lm = W.local_mass;
-      if (P.all_but_own) {
-        own = P.lclusters[P.cl_of[head]].gid;
-        lm = P.cell_probs[own];
-      }
-      const uint32_t nr = P.all_but_own ? C : W.n_rem;
-      double remote_sum = 0.0;
-      for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        double term = 0.0;
-        bool use = false;
-        if (q < nr) {
-          const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
-          if (!(P.all_but_own && r == own)) {
-            term = __dmul_rn(cm[3 * r + 2], cauchy_rn(hx, hy, cm[3 * r], cm[3 * r + 1]));
-            use = true;
-          }
-        }
-        const uint32_t um = __ballot_sync(FULL, use);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double x = __shfl_sync(FULL, term, j);
-          if ((um >> j) & 1u) remote_sum = __dadd_rn(remote_sum, x);
-        }
-      }
-      const double mean_field = __dmul_rn(M, remote_sum);
-      const double sf = __ddiv_rn(__dmul_rn(M, lm), (double)s);
-      const bool is_tail = lane > cnt && lane < nsl;
-      const bool is_nb = lane >= 1 && lane <= cnt;
-      const double qn = is_tail ? cauchy_rn(hx, hy, pv.x, pv.y) : 0.0;
-      double qsum = 0.0;
-#pragma unroll
-      for (int j = 1; j < 32; ++j) {
-        const double x = __shfl_sync(FULL, qn, j);
-        if ((uint32_t)j > cnt && (uint32_t)j < nsl) qsum = __dadd_rn(qsum, x);
-      }
-      const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
-      // ---- attraction (objective.hpp:197-213), neighbour j on lane 1 + j
-      double ax = 0.0, ay = 0.0, tl = 0.0, tb = 0.0, tx = 0.0, ty = 0.0;
-      if (is_nb) {
-        const double q = cauchy_rn(hx, hy, pv.x, pv.y);
-        const double wj = wt[cnt * k + lane - 1];
-        const double qb = __dadd_rn(q, bg);
-        tl = __dmul_rn(wj, -log(__ddiv_rn(q, qb)));
-        tb = __ddiv_rn(wj, qb);
-        const double pull = __dmul_rn(
-            __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj),
-                                __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
-                      q),
-            q);
-        const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
-        tx = __dmul_rn(pull, dx);
-        ty = __dmul_rn(pull, dy);
-        ax = __dmul_rn(-pull, dx);
-        ay = __dmul_rn(-pull, dy);
-      }
-      double loss = 0.0, bgs = 0.0, gx = 0.0, gy = 0.0;
-#pragma unroll
-      for (int j = 1; j < 32; ++j) {  // four independent chains, list order
-        const double xl = __shfl_sync(FULL, tl, j), xb = __shfl_sync(FULL, tb, j);
-        const double xx = __shfl_sync(FULL, tx, j), xy = __shfl_sync(FULL, ty, j);
-        if ((uint32_t)j <= cnt) {
-          loss = __dadd_rn(loss, xl);
-          bgs = __dadd_rn(bgs, xb);
-          gx = __dadd_rn(gx, xx);
-          gy = __dadd_rn(gy, xy);
-        }
-      }
-      // ---- negative repulsion (objective.hpp:216-226), tail q on lane 1 + cnt + q
-      if (is_tail) {
-        const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
-        const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
-        ax = __dmul_rn(push, dx);
-        ay = __dmul_rn(push, dy);
-      }
+      sa[lane] = qn;
+      __syncwarp();
+      double acc[1] = {0.0};
+      const double* const v[1] = {sa};
+      df_chains<1, false>(acc, v, cnt + 1, nsl, FULL);
+      qsum = acc[0];
+      __syncwarp();
+    }
+    const double bg = __dadd_rn(mean_field, __dmul_rn(sf, qsum));
+    DF_MARK(2);
+    // ---- phase B: the neighbours
+    if (wait_for(!predA)) continue;
+    __syncwarp();
+    if (lane < nsl && !needA) pv = ldpos(P.pos + pt);
+    DF_MARK(3);
+    // attraction (objective.hpp:197-213), neighbour j on lane 1 + j
+    // (the loss terms wj * -log(q / qb) feed no position: formed after the release)
+    double ax = 0.0, ay = 0.0, q = 1.0, qb = 1.0, tb = 0.0, tx = 0.0, ty = 0.0;
+    if (is_nb) {
+      q = cauchy_rn(hx, hy, pv.x, pv.y);
+      qb = __dadd_rn(q, bg);
+      tb = __ddiv_rn(wj, qb);
+      const double pull = __dmul_rn(
+          __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj), __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
+                    q),
+          q);
+      const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
+      tx = __dmul_rn(pull, dx);
+      ty = __dmul_rn(pull, dy);
+      ax = __dmul_rn(-pull, dx);
+      ay = __dmul_rn(-pull, dy);
+    }
+    double bgs, gx, gy;
+    {
+      sb[lane] = tb;
+      sc[lane] = tx;
+      sd[lane] = ty;
+      __syncwarp();
+      double acc[3] = {0.0, 0.0, 0.0};  // three independent chains, list order
+      const double* const v[3] = {sb, sc, sd};
+      df_chains<3, false>(acc, v, 1, cnt + 1, FULL);
+      bgs = acc[0];
+      gx = acc[1];
+      gy = acc[2];
+      __syncwarp();
+    }
+    DF_MARK(4);
+    // negative repulsion (objective.hpp:216-226), tail q on lane 1 + cnt + q
+    if (is_tail) {
+      const double push = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), sf), qn), qn);
+      const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
+      ax = __dmul_rn(push, dx);
+      ay = __dmul_rn(push, dy);
+    }
+    {
       sa[lane] = ax;  // tails' pushes, subtracted in draw order
       sb[lane] = ay;
       __syncwarp();
-      for (uint32_t q = 0; q < s; ++q) {
-        gx = __dsub_rn(gx, sa[1 + cnt + q]);
-        gy = __dsub_rn(gy, sb[1 + cnt + q]);
-      }
+      double acc[2] = {gx, gy};
+      const double* const v[2] = {sa, sb};
+      df_chains<2, true>(acc, v, cnt + 1, nsl, FULL);
+      gx = acc[0];
+      gy = acc[1];
       __syncwarp();
-      // ---- mean repulsion (objective.hpp:229-236), q_r recomputed per cell
-      for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        double px = 0.0, py = 0.0;
+    }
+    // mean repulsion (objective.hpp:229-236), q_r recomputed per cell
+    const double bgsM = __dmul_rn(__dmul_rn(2.0, bgs), M);
+    for (uint32_t q0 = 0; q0 < nr; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      double px = 0.0, py = 0.0;
+      uint32_t um;
+      if (q0 < 64) {  // factors from phase A
+        const bool b = q0 != 0;
+        um = b ? cu1 : cu0;
+        if ((um >> lane) & 1u) {
+          const double qr = b ? cq1 : cq0;
+          const double push = __dmul_rn(__dmul_rn(__dmul_rn(bgsM, b ? cp1 : cp0), qr), qr);
+          px = __dmul_rn(push, b ? cdx1 : cdx0);
+          py = __dmul_rn(push, b ? cdy1 : cdy0);
+        }
+      } else {
         bool use = false;
         if (q < nr) {
           const uint32_t r = P.all_but_own ? q : P.remote_ids[W.rem_off + q];
           if (!(P.all_but_own && r == own)) {
             const double mx = cm[3 * r], my = cm[3 * r + 1];
             const double qr = cauchy_rn(hx, hy, mx, my);
-            const double push = __dmul_rn(
-                __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, bgs), M), cm[3 * r + 2]), qr), qr);
+            const double push = __dmul_rn(__dmul_rn(__dmul_rn(bgsM, cm[3 * r + 2]), qr), qr);
             px = __dmul_rn(push, __dsub_rn(hx, mx));
             py = __dmul_rn(push, __dsub_rn(hy, my));
             use = true;
           }
         }
-        const uint32_t um = __ballot_sync(FULL, use);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double xx = __shfl_sync(FULL, px, j), xy = __shfl_sync(FULL, py, j);
-          if ((um >> j) & 1u) {
-            gx = __dsub_rn(gx, xx);
-            gy = __dsub_rn(gy, xy);
-          }
-        }
+        um = __ballot_sync(FULL, use);
       }
-      if (lane == 0) {
-        P.loss_slot[i] = loss;
-        ax = gx;
-        ay = gy;
-      }
-      // ---- apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails;
-      // a point in several slots gets its updates in slot order from the lane
-      // of its first slot
-      const bool slot = lane < nsl && (lane == 0 || !P.head_only);
-      sa[lane] = ax;
-      sb[lane] = ay;
+      sa[lane] = px;
+      sb[lane] = py;
       __syncwarp();
-      const uint32_t act = __ballot_sync(FULL, slot);
-      const uint32_t same = __match_any_sync(FULL, slot ? pt : 0xFFFFFFFFu) & act;
-      if (slot && (uint32_t)(__ffs(same) - 1) == lane) {
-        double2 v = pv;
-        for (uint32_t m = same; m; m &= m - 1) {
-          const uint32_t u = __ffs(m) - 1;
-          v.x = __dsub_rn(v.x, __dmul_rn(st, sa[u]));
-          v.y = __dsub_rn(v.y, __dmul_rn(st, sb[u]));
-          if (diverged(v.x, v.y))
-            atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | pt);
-        }
-        __stcg(P.pos + pt, v);
-      }
-      // release: the warp barrier orders every lane's position store before
-      // lane 0's release store of the flag (release is cumulative)
+      double acc[2] = {gx, gy};
+      const double* const v[2] = {sa, sb};
+      df_chains<2, true>(acc, v, 0, min(32u, nr - q0), um);
+      gx = acc[0];
+      gy = acc[1];
       __syncwarp();
-      if (lane == 0) st_release_u8(R.done + i, 1);
     }
+    DF_MARK(5);
+    if (lane == 0) {
+      ax = gx;
+      ay = gy;
+    }
+    // ---- apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails
+    sa[lane] = ax;
+    sb[lane] = ay;
+    __syncwarp();
+    if (slot && (uint32_t)(__ffs(same) - 1) == lane) {
+      double2 v = pv;
+      for (uint32_t m = same; m; m &= m - 1) {
+        const uint32_t u = __ffs(m) - 1;
+        v.x = __dsub_rn(v.x, __dmul_rn(st, sa[u]));
+        v.y = __dsub_rn(v.y, __dmul_rn(st, sb[u]));
+        if (diverged(v.x, v.y))
+          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | pt);
+      }
+      __stcg(P.pos + pt, v);
+    }
+    // release: the warp barrier orders every lane's position store before
+    // lane 0's release store of the flag (release is cumulative)
+    DF_MARK(6);
+    __syncwarp();
+    if (lane == 0) st_release_u8(R.done + i, 1);
+    // the draw's loss (objective.hpp:197-213): sum over the list in order
+    {
+      sa[lane] = is_nb ? __dmul_rn(wj, -log(__ddiv_rn(q, qb))) : 0.0;
+      __syncwarp();
+      double acc[1] = {0.0};
+      const double* const v[1] = {sa};
+      df_chains<1, false>(acc, v, 1, cnt + 1, FULL);
+      if (lane == 0) P.loss_slot[i] = acc[0];
+      __syncwarp();
+    }
+#ifdef DF_TRACE
+    DF_MARK(7);
+    if (lane == 0 && w == 0 && t % 2048 == 777)
+      printf("dftrace t=%u waitA %lld noise %lld waitB+load %lld attract %lld repulse %lld apply %lld release+loss %lld\n",
+             t, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4],
+             tr[6] - tr[5], tr[7] - tr[6]);
+
+#endif
   }
 }
 
