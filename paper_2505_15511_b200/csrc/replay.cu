@@ -405,29 +405,25 @@ constexpr uint32_t kDfBatch = 8;  // R.total_chunks granularity reported for the
 
 // Chains of the warp form: acc[c] = acc[c] (+|-) v[c][j] for j in [j0, j1)
 // whose bit in `mask` is set, in ascending j — the reference's summation
-// order. Terms sit in the warp's shared scratch (broadcast reads); loads are
-// issued 8 at a time so one shared-memory latency covers 8 dependent adds.
+// order. Terms sit in the warp's 32-entry shared scratch (broadcast reads);
+// each batch issues its 8 loads together (indices clamped to the scratch,
+// adds predicated), so one shared-memory latency covers 8 dependent adds.
 template <int NC, bool SUB>
 __device__ __forceinline__ void df_chains(double (&acc)[NC], const double* const (&v)[NC],
                                           uint32_t j0, uint32_t j1, uint32_t mask) {
-  uint32_t j = j0;
-  for (; j + 8 <= j1; j += 8) {
+  for (uint32_t j = j0; j < j1; j += 8) {
     double x[NC][8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
 #pragma unroll
-      for (int c = 0; c < NC; ++c) x[c][e] = v[c][j + e];
+      for (int c = 0; c < NC; ++c) x[c][e] = v[c][min(j + e, 31u)];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      if ((mask >> (j + e)) & 1u)
+      if (j + e < j1 && ((mask >> ((j + e) & 31)) & 1u))
 #pragma unroll
         for (int c = 0; c < NC; ++c)
           acc[c] = SUB ? __dsub_rn(acc[c], x[c][e]) : __dadd_rn(acc[c], x[c][e]);
   }
-  for (; j < j1; ++j)
-    if ((mask >> j) & 1u)
-#pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] = SUB ? __dsub_rn(acc[c], v[c][j]) : __dadd_rn(acc[c], v[c][j]);
 }
 
 #ifndef DF_MINB
@@ -616,11 +612,18 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     if (is_nb) {
       q = cauchy_rn(hx, hy, pv.x, pv.y);
       qb = __dadd_rn(q, bg);
-      tb = __ddiv_rn(wj, qb);
-      const double pull = __dmul_rn(
-          __dmul_rn(__dmul_rn(__dmul_rn(2.0, wj), __dsub_rn(__ddiv_rn(1.0, q), __ddiv_rn(1.0, qb))),
-                    q),
-          q);
+      // wj / qb, 1 / qb and 1 / q: the three fast paths overlap (one branch)
+      double iqb, iq, iq2;
+      bool o1, o2;
+      ddiv2_fp(wj, 1.0, qb, tb, iqb, o1);
+      ddiv2_fp(1.0, 1.0, q, iq, iq2, o2);
+      if (!(o1 && o2)) {
+        tb = __ddiv_rn(wj, qb);
+        iqb = __ddiv_rn(1.0, qb);
+        iq = __ddiv_rn(1.0, q);
+      }
+      const double pull =
+          __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(2.0, wj), __dsub_rn(iq, iqb)), q), q);
       const double dx = __dsub_rn(hx, pv.x), dy = __dsub_rn(hy, pv.y);
       tx = __dmul_rn(pull, dx);
       ty = __dmul_rn(pull, dy);
