@@ -9,37 +9,55 @@
 
 namespace nb {
 
-// Per-worker loss in sequential draw order (optimizer.hpp:289-290).
-// One warp per worker: the warp stages the next 256 slots in shared memory
-// (coalesced), then lane 0 adds them in draw order with the loads ahead of the
-// dependent adds (the chain is bound by DADD latency, ~8 cycles).
+// Sequential fp64 sum of p[0], p[stride], ..., p[(m-1) stride] in that order
+// by one warp (the reference's accumulation order; lane 0 holds the result).
+// The warp stages 256 values in shared memory, and while lane 0 adds them
+// (loads ahead of the dependent adds: the chain runs at DADD latency, ~8
+// cycles) the next 256 are already in flight into every lane's registers.
+__device__ __forceinline__ double warp_seq_sum(const double* __restrict__ p, size_t stride,
+                                               uint32_t m, double* buf) {
+  const uint32_t lane = threadIdx.x & 31;
+  double acc = 0.0;
+  double nx[8];
+  auto fetch = [&](uint32_t b0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t e = b0 + lane + 32 * u;
+      nx[u] = e < m ? p[stride * e] : 0.0;
+    }
+  };
+  fetch(0);
+  for (uint32_t b0 = 0; b0 < m; b0 += 256) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) buf[lane + 32 * u] = nx[u];
+    __syncwarp();
+    if (b0 + 256 < m) fetch(b0 + 256);  // in flight during the adds below
+    if (lane == 0) {
+      const uint32_t n = min(256u, m - b0);
+      uint32_t e = 0;
+      for (; e + 8 <= n; e += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = buf[e + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+      }
+      for (; e < n; ++e) acc = __dadd_rn(acc, buf[e]);
+    }
+    __syncwarp();
+  }
+  return acc;
+}
+
+// Per-worker loss in sequential draw order (optimizer.hpp:289-290), one warp
+// per worker.
 __global__ void k_loss_seq(const double* slot, const uint32_t* base, const WorkerDev* wk,
                            uint32_t nw, double* out) {
   __shared__ double buf[4][256];
   const uint32_t wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t w = blockIdx.x * (blockDim.x >> 5) + wi;
   if (w >= nw) return;
-  double* b = buf[wi];
-  double acc = 0.0;
-  const double* p = slot + base[w];
-  const uint32_t D = wk[w].draws;
-  for (uint32_t b0 = 0; b0 < D; b0 += 256) {
-    const uint32_t m = min(256u, D - b0);
-    for (uint32_t e = lane; e < m; e += 32) b[e] = p[b0 + e];
-    __syncwarp();
-    if (lane == 0) {
-      uint32_t e = 0;
-      for (; e + 8 <= m; e += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = b[e + u];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
-      }
-      for (; e < m; ++e) acc = __dadd_rn(acc, b[e]);
-    }
-    __syncwarp();
-  }
+  const double acc = warp_seq_sum(slot + base[w], 1, wk[w].draws, buf[wi]);
   if (lane == 0) out[w] = acc;
 }
 
@@ -47,10 +65,8 @@ __global__ void k_loss_seq(const double* slot, const uint32_t* base, const Worke
 //
 // Exact: per local cluster and coordinate, a sequential sum over the
 // cluster's contiguous segment (ascending original id == the order of
-// gather_means, optimizer.hpp:163-168 / :420-428), then / count.
-// One warp per (cluster, coordinate) chain: the warp stages the next 256
-// values in shared memory, lane 0 adds them in ascending order (loads ahead
-// of the dependent adds), then / count.
+// gather_means, optimizer.hpp:163-168 / :420-428), then / count; one warp
+// per (cluster, coordinate) chain.
 __global__ void k_means_exact(const double2* pos, const LocalCluster* lc, uint32_t ncl,
                               double* slot /* ncl x 2 */) {
   __shared__ double buf[4][256];
@@ -60,25 +76,7 @@ __global__ void k_means_exact(const double2* pos, const LocalCluster* lc, uint32
   const uint32_t c = g >> 1, dim = g & 1;
   const LocalCluster L = lc[c];
   const double* p = reinterpret_cast<const double*>(pos) + 2 * (size_t)L.start + dim;
-  double* b = buf[wi];
-  double acc = 0.0;
-  for (uint32_t b0 = 0; b0 < L.count; b0 += 256) {
-    const uint32_t m = min(256u, L.count - b0);
-    for (uint32_t e = lane; e < m; e += 32) b[e] = p[2 * (size_t)(b0 + e)];
-    __syncwarp();
-    if (lane == 0) {
-      uint32_t e = 0;
-      for (; e + 8 <= m; e += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = b[e + u];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
-      }
-      for (; e < m; ++e) acc = __dadd_rn(acc, b[e]);
-    }
-    __syncwarp();
-  }
+  const double acc = warp_seq_sum(p, 2, L.count, buf[wi]);
   if (lane == 0) slot[g] = __ddiv_rn(acc, (double)L.count);
 }
 
