@@ -88,28 +88,32 @@ __global__ void __launch_bounds__(160) k_mt_words(ReplayDev R, const uint64_t* c
     done = take;
     p += (uint32_t)take;
   }
+  // One twist per 312 words (rng.hpp:42-84; Mt64::twist): thread t < 156
+  // forms new[t] = old[t+156] ^ mix(old[t], old[t+1]) and new[t+156] =
+  // new[t] ^ mix(old[t+156], old[t+157]) — the last one mixing with new[0],
+  // which thread 155 forms itself from the old words — and writes both
+  // tempered words from registers: two barriers per 312 words.
   while (done < n) {
     unsigned long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
     if (tid < 156) {
       a0 = s[tid];
       a1 = s[tid + 1];
       b0 = s[tid + 156];
-      if (tid < 155) b1 = s[tid + 157];
+      b1 = tid < 155 ? s[tid + 157] : s[156] ^ mt_mix(s[0], s[1]);
     }
-    __syncthreads();
-    unsigned long long n0 = 0;
-    if (tid < 156) {
-      n0 = b0 ^ mt_mix(a0, a1);
-      s[tid] = n0;
-    }
-    __syncthreads();
-    if (tid < 156) s[tid + 156] = n0 ^ mt_mix(b0, tid < 155 ? b1 : s[0]);
-    __syncthreads();
+    __syncthreads();  // every old word read before any is replaced
     const uint64_t take = std::min<uint64_t>(312, n - done);
-    for (uint32_t i = tid; i < take; i += blockDim.x) o[done + i] = mt_temper(s[i]);
+    if (tid < 156) {
+      const unsigned long long n0 = b0 ^ mt_mix(a0, a1);
+      const unsigned long long n2 = n0 ^ mt_mix(b0, b1);
+      s[tid] = n0;
+      s[tid + 156] = n2;
+      if (tid < take) o[done + tid] = mt_temper(n0);
+      if (tid + 156 < take) o[done + tid + 156] = mt_temper(n2);
+    }
     done += take;
     p = (uint32_t)take;
-    __syncthreads();
+    __syncthreads();  // the new state complete before the next twist reads it
   }
   MtState* out = R.st_out + w;
   for (uint32_t i = tid; i < 312; i += blockDim.x) out->mt[i] = s[i];
@@ -156,7 +160,11 @@ __global__ void k_replay_map(ReplayDev R, SgdParams P, const uint32_t* pool,
 // neighbours in list order, then the tails; a point touched twice by one draw
 // is listed once) -> key = its local point, value = i * T + j; plus the
 // epoch's edge-updates per worker.
-__global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
+__global__ void __launch_bounds__(256) k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
+  // The block's touch rows (one draw per thread, T keys each) are formed in
+  // shared memory — the list and tails copied in once, duplicates removed
+  // there (no global reloads) — and written out as one contiguous run.
+  extern __shared__ uint32_t sk[];  // blockDim.x * T
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t T = R.T, s = R.s, k = P.k, NONE = R.n_loc;
   // edge-updates of the epoch per worker, |N(head)| + s per draw (warp-aggregated)
@@ -171,34 +179,44 @@ __global__ void k_replay_touch(ReplayDev R, SgdParams P, uint32_t total) {
     if ((threadIdx.x & 31) == (uint32_t)(__ffs(same) - 1) && sum)
       atomicAdd(R.edges + w, (unsigned long long)sum);
   }
-  if (i >= total) return;
-  const uint32_t h = R.heads[i];
-  uint32_t* key = R.tkey + (size_t)i * T;
-  uint32_t* val = R.tval + (size_t)i * T;
-  for (uint32_t j = 0; j < T; ++j) {
-    R.pred[(size_t)i * T + j] = 0xFFFFFFFFu;
-    val[j] = i * T + j;
+  if (i < total) {
+    const uint32_t h = R.heads[i];
+    uint32_t* key = sk + threadIdx.x * T;
+    const uint32_t cnt = P.ncnt ? P.ncnt[h] : k;
+    const uint32_t* nb = P.ell + (size_t)h * P.kpad;
+    key[0] = h;
+    for (uint32_t j = 1; j <= cnt; ++j) key[j] = nb[j - 1];
+    for (uint32_t j = cnt + 1; j < 1 + k; ++j) key[j] = NONE;
+    const uint32_t* tails = R.tails + (size_t)i * s;
+    for (uint32_t q = 0; q < s; ++q) key[1 + k + q] = tails[q];
+    // a point touched twice by one draw is listed at its first slot only:
+    // build_knn's lists hold distinct points other than the head, a caller's
+    // graph may repeat one (the reference then applies both updates in turn).
+    // Comparing against already-cleared slots is harmless: the first
+    // occurrence of every point is kept.
+    for (uint32_t j = 1; j <= cnt; ++j) {
+      const uint32_t v = key[j];
+      bool dup = v == h;
+      for (uint32_t a = 1; a < j && !dup; ++a) dup = key[a] == v;
+      if (dup) key[j] = NONE;
+    }
+    for (uint32_t q = 0; q < s; ++q) {
+      const uint32_t v = key[1 + k + q];
+      bool dup = v == h;
+      for (uint32_t a = 1; a <= cnt && !dup; ++a) dup = key[a] == v;
+      for (uint32_t a = 0; a < q && !dup; ++a) dup = key[1 + k + a] == v;
+      if (dup) key[1 + k + q] = NONE;
+    }
   }
-  const uint32_t cnt = P.ncnt ? P.ncnt[h] : k;
-  const uint32_t* nb = P.ell + (size_t)h * P.kpad;
-  key[0] = h;
-  uint32_t j = 1;
-  for (; j <= cnt; ++j) {
-    // build_knn's lists hold distinct points other than the head; a caller's
-    // graph may repeat one (the reference then applies both updates in turn)
-    const uint32_t v = nb[j - 1];
-    bool dup = v == h;
-    for (uint32_t a = 0; a + 1 < j && !dup; ++a) dup = nb[a] == v;
-    key[j] = dup ? NONE : v;
-  }
-  for (; j < 1 + k; ++j) key[j] = NONE;
-  const uint32_t* tails = R.tails + (size_t)i * s;
-  for (uint32_t q = 0; q < s; ++q) {
-    const uint32_t v = tails[q];
-    bool dup = v == h;
-    for (uint32_t a = 0; a < cnt && !dup; ++a) dup = nb[a] == v;
-    for (uint32_t a = 0; a < q && !dup; ++a) dup = tails[a] == v;
-    key[1 + k + q] = dup ? NONE : v;
+  __syncthreads();
+  const uint32_t i0 = blockIdx.x * blockDim.x;
+  if (i0 >= total) return;
+  const uint32_t m = min(blockDim.x, total - i0) * T;
+  const size_t base = (size_t)i0 * T;
+  for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) {
+    R.tkey[base + e] = sk[e];
+    R.tval[base + e] = (uint32_t)(base + e);  // draw * T + slot
+    R.pred[base + e] = 0xFFFFFFFFu;
   }
 }
 
@@ -781,7 +799,11 @@ void launch_replay_deps(const ReplayDev& R, const SgdParams& P, void* sort_tmp, 
   const uint32_t total = R.total_draws;
   const uint64_t items = (uint64_t)total * R.T;
   if (!total) return;
-  k_replay_touch<<<blocks_for(total, 256), 256, 0, st>>>(R, P, total);
+  const size_t tsm = (size_t)256 * R.T * sizeof(uint32_t);
+  if (tsm > 48 * 1024)
+    NB_CUDA(cudaFuncSetAttribute(k_replay_touch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tsm));
+  k_replay_touch<<<blocks_for(total, 256), 256, tsm, st>>>(R, P, total);
   // stable LSD radix sort by point over the draw-ordered touches
   size_t b = sort_bytes;
   NB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp, b, R.tkey, R.tkey2, R.tval, R.tval2,

@@ -42,6 +42,20 @@ def test_replay_bit_exact(port, ctx, workers):
     assert log.payload_doubles == 6 * 2 * 8 and log.payload_counts == 6 * 8
 
 
+@pytest.mark.parametrize("k,s", [(40, 5), (20, 14)])
+def test_replay_long_touch_lists(port, ctx, k, s):
+    """1 + k + s > 32 slots per draw: the per-thread dataflow form (and touch
+    rows wider than a warp) must stay bit-identical too."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(2000, 16, 10, 8, k)
+    kw = dict(epochs=10, workers=4, seed=11, k=k, local_draws=s)
+    tr = _trainer(nb, ctx, c, g, pca, **kw)
+    loss = tr.run(3)
+    rl, rloss, _, _ = _oracle(port, c, g, pca, 3, **kw)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
 def test_replay_host_draw_fallback_is_identical(port, ctx, monkeypatch):
     """The rejection branch of uniform_index (rng.hpp:49-55, probability
     ~n / 2^64 per draw) moves a worker's draws to the host for that epoch;
