@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(256) k_replay_touch(ReplayDev R, SgdParams P, 
     R.tkey[base + e] = sk[e];
     R.tval[base + e] = (uint32_t)(base + e);  // draw * T + slot
     R.pred[base + e] = 0xFFFFFFFFu;
+    if (R.succ) R.succ[base + e] = 0xFFFFFFFFu;
   }
 }
 
@@ -226,9 +227,12 @@ __global__ void k_replay_pred(ReplayDev R, uint64_t items) {
   const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (e >= items) return;
   const uint32_t v = R.tkey[e];
-  if (v == R.n_loc || e == 0 || R.tkey[e - 1] != v) return;
-  const uint32_t prev_draw = R.tval[e - 1] / R.T;  // global draw index
-  R.pred[R.tval[e]] = prev_draw - R.pt_base[v];     // the worker's draw t
+  if (v == R.n_loc) return;
+  if (e > 0 && R.tkey[e - 1] == v) {
+    const uint32_t prev_draw = R.tval[e - 1] / R.T;  // global draw index
+    R.pred[R.tval[e]] = prev_draw - R.pt_base[v];     // the worker's draw t
+  }
+  if (R.succ && e + 1 < items && R.tkey[e + 1] == v) R.succ[R.tval[e]] = R.tval[e + 1];
 }
 
 // ------------------------------------------------------ dataflow SGD
@@ -241,6 +245,24 @@ __device__ __forceinline__ uint32_t ld_acquire_u8(const uint8_t* p) {
 }
 __device__ __forceinline__ void st_release_u8(uint8_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u8 [%0], %1;" ::"l"(p), "h"((uint16_t)v) : "memory");
+}
+// Position mailboxes of the warp form: the draw that last touched a point
+// stores its new position straight into the slot of the point's next touch;
+// each 8-byte half is single-copy atomic and starts as all-ones (a NaN no
+// arithmetic produces), so a half is final once it differs from that.
+constexpr unsigned long long kMboxEmpty = ~0ull;
+__device__ __forceinline__ bool mbox_take(const double2* mb, double2& v) {
+  unsigned long long x, y;
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(mb) : "memory");
+  if (x == kMboxEmpty || y == kMboxEmpty) return false;
+  v = make_double2(__longlong_as_double((long long)x), __longlong_as_double((long long)y));
+  return true;
+}
+__device__ __forceinline__ void mbox_put(double2* mb, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(mb),
+               "l"((unsigned long long)__double_as_longlong(v.x)),
+               "l"((unsigned long long)__double_as_longlong(v.y))
+               : "memory");
 }
 
 __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) {
@@ -493,8 +515,12 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     uint32_t pt = head;
     if (is_nb) pt = P.ell[(size_t)head * P.kpad + lane - 1];
     else if (is_tail) pt = R.tails[(size_t)i * s + (lane - 1 - cnt)];
-    const uint32_t pq = lane < T ? R.pred[(size_t)i * T + lane] : 0xFFFFFFFFu;
-    const uint8_t* dn = R.done + R.draw_base[w];
+    // predecessor-layout lane j (touch slot j): has an earlier touch this
+    // epoch (its position arrives in mailbox i*T + j), and the touch to
+    // forward the new position to (none: the epoch's last touch -> pos)
+    const bool has_pred = lane < T && R.pred[(size_t)i * T + lane] != 0xFFFFFFFFu;
+    const uint32_t succ = lane < T ? R.succ[(size_t)i * T + lane] : 0xFFFFFFFFu;
+    double2* const mb = R.mbox + (size_t)i * T;
     uint32_t own = 0;
     double lm = W.local_mass;
     if (P.all_but_own) {
@@ -511,15 +537,16 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
 #else
 #define DF_MARK(j)
 #endif
-    // Wait until the predecessors of the lanes in `mine` are done. Acquire:
-    // a lane's later load of its slot's position sees the predecessor's
-    // writes; a lane stops polling once its flag is set. Returns true when
-    // the watchdog fired (a schedule bug: report, never hang).
+    // Wait until the positions of the predecessor lanes in `mine` have been
+    // forwarded into their mailboxes (the values themselves: no flag, no
+    // fence). Returns true when the watchdog fired (a schedule bug: report,
+    // never hang).
+    double2 got = make_double2(0.0, 0.0);
     auto wait_for = [&](bool mine) -> bool {
       uint32_t spins = 0, nap = min(64u, R.nap_cap);
-      bool abort = false, ok = !mine || pq == 0xFFFFFFFFu;
+      bool abort = false, ok = !mine || !has_pred;
       for (;;) {
-        if (!ok) ok = ld_acquire_u8(dn + pq) != 0;
+        if (!ok) ok = mbox_take(mb + lane, got);
         if (__all_sync(FULL, ok)) break;
         if ((++spins & 63) == 0 &&
             (*reinterpret_cast<volatile uint32_t*>(R.stall) || spins > (1u << 22))) {
@@ -551,15 +578,29 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     if (lane > k && lane < 1 + k + s) sl = 1 + cnt + (lane - 1 - k);
     else if (lane > cnt && lane <= k) sl = 0;  // padded neighbour slots (no predecessor)
     const bool predA = __shfl_sync(FULL, needA, sl & 31);
+    // slot lane -> its predecessor-layout lane; the first slot lane of each
+    // point's group holds the point's touch (the repeats carry none)
+    const uint32_t pl = lane == 0 ? 0u : (lane <= cnt ? lane : 1 + k + (lane - 1 - cnt));
+    const uint32_t fl = (uint32_t)(__ffs(grp) - 1);
+    const uint32_t fwd = __shfl_sync(FULL, succ, pl & 31);  // for the group's first lane
     // apply grouping (positions not needed): a point in several slots gets
     // its updates in slot order from the lane of its first slot
     const bool slot = lane < nsl && (lane == 0 || !P.head_only);
     const uint32_t act = __ballot_sync(FULL, slot);
     const uint32_t same = __match_any_sync(FULL, slot ? pt : 0xFFFFFFFFu) & act;
+    // a slot's position: forwarded by the predecessor touch, or (the epoch's
+    // first touch of the point) the position array; repeats copy their first
+    auto position = [&](bool phase, double2& pv) {
+      const double fx = __shfl_sync(FULL, got.x, pl & 31), fy = __shfl_sync(FULL, got.y, pl & 31);
+      const bool fp = __shfl_sync(FULL, has_pred, pl & 31);
+      double2 v = pv;
+      if (phase && lane == fl) v = fp ? make_double2(fx, fy) : ldpos(P.pos + pt);
+      const double vx = __shfl_sync(FULL, v.x, fl), vy = __shfl_sync(FULL, v.y, fl);
+      if (phase) pv = make_double2(vx, vy);
+    };
     if (wait_for(predA)) continue;
-    __syncwarp();  // the polling lanes' acquires before the other lanes' loads
     double2 pv = make_double2(0.0, 0.0);
-    if (needA) pv = ldpos(P.pos + pt);
+    position(needA, pv);
     const double hx = __shfl_sync(FULL, pv.x, 0), hy = __shfl_sync(FULL, pv.y, 0);
     DF_MARK(1);
     // noise terms (objective.hpp:113-145): terms on their lanes, every sum in
@@ -621,8 +662,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     DF_MARK(2);
     // ---- phase B: the neighbours
     if (wait_for(!predA)) continue;
-    __syncwarp();
-    if (lane < nsl && !needA) pv = ldpos(P.pos + pt);
+    position(lane < nsl && !needA, pv);
     DF_MARK(3);
     // attraction (objective.hpp:197-213), neighbour j on lane 1 + j
     // (the loss terms wj * -log(q / qb) feed no position: formed after the release)
@@ -726,26 +766,32 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       ax = gx;
       ay = gy;
     }
-    // ---- apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails
+    // ---- apply (optimizer.hpp:215-227, :293-303): head, neighbours, tails;
+    // the first lane of each point's group applies its slots' updates in slot
+    // order and forwards the result to the point's next touch (or stores it)
     sa[lane] = ax;
     sb[lane] = ay;
     __syncwarp();
-    if (slot && (uint32_t)(__ffs(same) - 1) == lane) {
-      double2 v = pv;
-      for (uint32_t m = same; m; m &= m - 1) {
-        const uint32_t u = __ffs(m) - 1;
-        v.x = __dsub_rn(v.x, __dmul_rn(st, sa[u]));
-        v.y = __dsub_rn(v.y, __dmul_rn(st, sb[u]));
-        if (diverged(v.x, v.y))
-          atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | pt);
-      }
-      __stcg(P.pos + pt, v);
-    }
-    // release: the warp barrier orders every lane's position store before
-    // lane 0's release store of the flag (release is cumulative)
     DF_MARK(6);
-    __syncwarp();
-    if (lane == 0) st_release_u8(R.done + i, 1);
+    if (lane < nsl && lane == fl) {
+      double2 v = pv;
+      if (slot)
+        for (uint32_t m = same; m; m &= m - 1) {
+          const uint32_t u = __ffs(m) - 1;
+          v.x = __dsub_rn(v.x, __dmul_rn(st, sa[u]));
+          v.y = __dsub_rn(v.y, __dmul_rn(st, sb[u]));
+          if (diverged(v.x, v.y))
+            atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | pt);
+        }
+      if (fwd != 0xFFFFFFFFu) mbox_put(R.mbox + fwd, v);
+      else __stcg(P.pos + pt, v);
+    }
+    // every mailbox is read once: empty it again for the next epoch (no
+    // per-epoch fill), off the dependency chain
+    if (has_pred)
+      mbox_put(mb + lane, make_double2(__longlong_as_double((long long)kMboxEmpty),
+                                       __longlong_as_double((long long)kMboxEmpty)));
+    __syncwarp();  // the updates read from the scratch before it is reused
     // the draw's loss (objective.hpp:197-213): sum over the list in order
     {
       sa[lane] = is_nb ? __dmul_rn(wj, -log(__ddiv_rn(q, qb))) : 0.0;
@@ -759,7 +805,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
 #ifdef DF_TRACE
     DF_MARK(7);
     if (lane == 0 && w == 0 && t % 2048 == 777)
-      printf("dftrace t=%u waitA %lld noise %lld waitB+load %lld attract %lld repulse %lld apply %lld release+loss %lld\n",
+      printf("dftrace t=%u waitA %lld noise %lld waitB+load %lld attract %lld repulse %lld tail %lld apply+loss %lld\n",
              t, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4],
              tr[6] - tr[5], tr[7] - tr[6]);
 

@@ -51,6 +51,10 @@ struct ReplayDev {
   uint32_t* tkey2;             // radix-sort buffers
   uint32_t* tval2;
   uint32_t* pred;              // per draw and slot: latest earlier draw touching it (none: ~0)
+  uint32_t* succ;              // per draw and slot: the next touch of its point, as a flat
+                               // touch index (none: ~0); warp form only (else nullptr)
+  double2* mbox;               // per touch: the point's position forwarded by its
+                               // predecessor (all-ones bits: not yet); warp form only
   uint32_t n_loc;              // local points (the "none" key)
   uint32_t* reject;            // per worker: a draw hit the rejection branch
   unsigned long long* edges;   // per worker: sum over draws of |N(head)| + s

@@ -95,6 +95,8 @@ struct RankTrainer {
   DBuf<MtState> mt_a, mt_b;
   DBuf<uint64_t> wcount, wbase;
   DBuf<unsigned long long> words, redges;
+  DBuf<double2> rmbox;
+  DBuf<uint32_t> rsucc;
   DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, tkey, tval, tkey2, tval2, rpred, reject,
       ticket, pt_base, stall;
   DBuf<uint8_t> rdone, sort_tmp;
@@ -436,6 +438,12 @@ struct RankTrainer {
     tkey2.alloc(D * T);
     tval2.alloc(D * T);
     rpred.alloc(D * T);
+    if (dataflow_warp_form((uint32_t)k, (uint32_t)s)) {  // position mailboxes (replay.cu)
+      rsucc.alloc(D * T);
+      rmbox.alloc(D * T);
+      // all empty; every mailbox is emptied again by its reader, so one fill lasts
+      NB_CUDA(cudaMemsetAsync(rmbox.p, 0xFF, rmbox.bytes(), S));
+    }
     rdone.alloc(D);
     loss_slot.alloc(D);
     reject.alloc(std::max<uint32_t>(nwl, 1));
@@ -464,6 +472,8 @@ struct RankTrainer {
     R.tkey2 = tkey2.p;
     R.tval2 = tval2.p;
     R.pred = rpred.p;
+    R.succ = rsucc.p;
+    R.mbox = rmbox.p;
     R.n_loc = (uint32_t)orig_of.size();
     R.reject = reject.p;
     R.edges = redges.p;
@@ -920,7 +930,12 @@ struct RankTrainer {
     if (cfg.sgd_mode == NOMAD_B200_SGD_REPLAY) {
       uint32_t stalled = 0;
       NB_CUDA(cudaMemcpy(&stalled, stall.p, 4, cudaMemcpyDeviceToHost));
-      if (stalled) fail(kInternal, "replay dataflow stalled (schedule watchdog)");
+      if (stalled) {
+        // leave the mailboxes empty for any later epoch (a stalled epoch
+        // may have left values in them)
+        if (rmbox.p) NB_CUDA(cudaMemsetAsync(rmbox.p, 0xFF, rmbox.bytes(), st()));
+        fail(kInternal, "replay dataflow stalled (schedule watchdog)");
+      }
     }
     float a = 0.f, b = 0.f;
     NB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
