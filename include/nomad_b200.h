@@ -260,6 +260,23 @@ int32_t nomad_b200_group_index_sharded(nomad_b200_group* g, const nomad_b200_dat
                                        uint64_t workers, uint64_t k, int32_t knn_mode,
                                        nomad_b200_clusters* clusters_out,
                                        nomad_b200_graph* graph_out);
+/* Row-sharded PCA initialisation (pca.hpp:79-218): rank `rank`
+ * holds rows [row0, row0 + rows->rows) of an n_total-row dataset and receives
+ * those rows' layout (rows->rows x 2, `location`). Every ascending-row sum is
+ * carried rank to rank, so fast == 0 is bit-identical to nomad_b200_pca_init
+ * on the whole dataset; fast != 0 adds the ranks' covariance sums in rank
+ * order (nomad_b200_pca_init_fast's principal plane). NCCL between processes
+ * (nccl_id as for nomad_b200_trainer_create; world 1 needs none). */
+int32_t nomad_b200_pca_init_sharded(nomad_b200_ctx* ctx, int32_t rank, int32_t world,
+                                    const void* nccl_id, const nomad_b200_dataset_view* rows,
+                                    uint64_t row0, uint64_t n_total, uint64_t seed, int32_t fast,
+                                    double* layout_out, int32_t location);
+/* The same over the ranks of a group: rows[r] / row0[r] / layout_out[r] on
+ * rank r's device. */
+int32_t nomad_b200_group_pca_init_sharded(nomad_b200_group* g, const nomad_b200_dataset_view* rows,
+                                          const uint64_t* row0, uint64_t n_total, uint64_t seed,
+                                          int32_t fast, double* const* layout_out,
+                                          int32_t location);
 /* Statistics of the context's last build_knn: rows the tensor-core
  * certificate did not settle, and rows resolved by the exhaustive fp64 pass. */
 int32_t nomad_b200_knn_stats(nomad_b200_ctx* ctx, uint64_t* tc_uncertified,

@@ -10,6 +10,7 @@ from .api import (ClusterAssignment, CommLog, ConditionalAffinity, Context, FitR
                   TrainConfig, Trainer, build_knn, default_kmeans_tol, fit,
                   kmeans_em_default_tol, knn_recall, pca_init, shard_plan,
                   generate_mixture, generate_mixture_rows, group_index_sharded,
+                  group_pca_init_sharded, pca_init_sharded,
                   index_sharded, kmeans_em, lsh_init, nccl_unique_id,
                   neighborhood_preservation, neighborhood_preservation_ann,
                   random_triplet_accuracy,

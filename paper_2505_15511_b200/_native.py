@@ -142,6 +142,12 @@ _SIGS = {
                                                    C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                                    C.c_uint64, C.c_uint64, C.c_int32,
                                                    C.POINTER(ClustersView), C.POINTER(GraphView)]),
+    "nomad_b200_pca_init_sharded": (C.c_int32, [_vp, C.c_int32, C.c_int32, _vp,
+                                                C.POINTER(DatasetView), C.c_uint64, C.c_uint64,
+                                                C.c_uint64, C.c_int32, _vp, C.c_int32]),
+    "nomad_b200_group_pca_init_sharded": (C.c_int32, [_vp, C.POINTER(DatasetView), _vp,
+                                                      C.c_uint64, C.c_uint64, C.c_int32, _vp,
+                                                      C.c_int32]),
     "nomad_b200_generate_mixture_rows": (C.c_int32, [_vp, C.c_uint64, C.c_uint64, C.c_uint64,
                                                      C.c_uint64, C.c_double, C.c_uint64, C.c_int32,
                                                      _vp]),

@@ -751,6 +751,39 @@ def group_index_sharded(group: "Group", rows: list, row0: list, n_total: int, n_
     return ca, KnnGraph(n_total, k, off, nb[:m], di[:m])
 
 
+def pca_init_sharded(rows, row0: int, n_total: int, seed: int = 0, fast: bool = False,
+                     rank: int = 0, world_size: int = 1, nccl_id: Optional[bytes] = None,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    """Row-sharded pca_init (pca.hpp:79-218) for one rank of a multi-process
+    run: this rank holds rows [row0, row0 + len(rows)) and gets their layout
+    rows; fast=False is bit-identical to pca_init on the whole dataset."""
+    dv, keep = _dataset(rows)
+    out = np.zeros((dv.rows, 2), np.float64)
+    idbuf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+    check(lib().nomad_b200_pca_init_sharded(_ctx(ctx).h, rank, world_size, idbuf, C.byref(dv),
+                                            row0, n_total, seed & (2**64 - 1), int(fast),
+                                            out.ctypes.data, N.HOST))
+    return out
+
+
+def group_pca_init_sharded(group: "Group", rows: list, row0: list, n_total: int, seed: int = 0,
+                           fast: bool = False) -> list:
+    """Row-sharded pca_init over the ranks of a Group (rows[r] on rank r's
+    device): the layout rows of every rank's slice, in rank order."""
+    views, keeps, outs = [], [], []
+    for r in rows:
+        v, kp = _dataset(r)
+        views.append(v)
+        keeps.append(kp)
+        outs.append(np.zeros((v.rows, 2), np.float64))
+    arr = (N.DatasetView * len(views))(*views)
+    r0 = np.ascontiguousarray(row0, np.uint64)
+    ptrs = (C.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+    check(lib().nomad_b200_group_pca_init_sharded(group.h, arr, r0.ctypes.data, n_total,
+                                                  seed & (2**64 - 1), int(fast), ptrs, N.HOST))
+    return outs
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().nomad_b200_nccl_unique_id(buf))

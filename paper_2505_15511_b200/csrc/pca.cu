@@ -10,8 +10,12 @@
 // own "pca" Rng stream.
 #include <algorithm>
 #include <cmath>
+#include <exception>
+#include <memory>
+#include <thread>
 
 #include "index_common.cuh"
+#include "shard.cuh"
 
 namespace nb {
 
@@ -59,11 +63,13 @@ __global__ void __launch_bounds__(128) k_pca_rows(XPtr x, uint64_t n,
 // y_j = (sum_{i ascending} ((double)x_ij - mean_j) * t_i) / n   (pca.hpp:47-54)
 // CTA per 32-column group: 8 warps stream BR-row slices (cp.async, double
 // buffer) and t; warp 0 runs the 32 column chains in order.
+// carry: y holds running sums (a row-sharded carry chain): continue them and
+// store them undivided.
 template <int BR>
 __global__ void __launch_bounds__(256) k_pca_cols(XPtr x, uint64_t n,
                                                   uint32_t d, const double* __restrict__ mean,
                                                   const double* __restrict__ t,
-                                                  double* __restrict__ y) {
+                                                  double* __restrict__ y, int carry) {
   extern __shared__ float sbuf[];  // [2][BR][33]
   __shared__ double ts[2][BR];
   const uint64_t j0 = (uint64_t)blockIdx.x * 32;
@@ -92,7 +98,7 @@ __global__ void __launch_bounds__(256) k_pca_cols(XPtr x, uint64_t n,
   };
   const uint64_t nb = (n + BR - 1) / BR;
   const double m = colok ? mean[j] : 0.0;
-  double acc = 0.0;
+  double acc = (carry && colok) ? y[j] : 0.0;
   issue(0);
   for (uint64_t b = 0; b < nb; ++b) {
     if (b + 1 < nb) issue(b + 1);
@@ -117,17 +123,22 @@ __global__ void __launch_bounds__(256) k_pca_cols(XPtr x, uint64_t n,
     }
     __syncthreads();
   }
-  if (warp == 0 && colok) y[j] = __ddiv_rn(acc, (double)n);
+  if (warp == 0 && colok) y[j] = carry ? acc : __ddiv_rn(acc, (double)n);
+}
+
+__global__ void k_div_vec(double* v, uint32_t d, double n) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < d) v[j] = __ddiv_rn(v[j], n);
 }
 
 // Sequential chains over a strided column of the layout (pca.hpp:197-212):
 // mode 0: sum_i v_i; mode 1: sum_i (v_i - mu)^2. One adding thread; the
 // block stages the next tile.
 __global__ void k_seq_col(const double* lay, uint64_t n, int comp, int mode, double mu,
-                          double* out) {
+                          double* out, int carry) {
   constexpr int T = 2048;
   __shared__ double buf[2][T];
-  double acc = 0.0;
+  double acc = carry ? *out : 0.0;  // carry: continue the previous rank's chain
   int cur = 0;
   for (uint64_t e = threadIdx.x; e < T && e < n; e += blockDim.x) buf[0][e] = lay[2 * e + comp];
   __syncthreads();
@@ -300,21 +311,51 @@ void covariance_sums(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
 // two quantities that are both at rounding-noise level once the power
 // iteration has converged, so only the bit-exact path reproduces the
 // reference's orientation.
+//
+// Row-sharded (comm != nullptr): this rank holds rows
+// [row0, row0 + n) of an N-row dataset and writes their layout rows. Every
+// ascending-row sum — the data mean, each exact covariance apply's column
+// chains, the layout's column mean and spread — is a carry chain over the
+// ranks (shard.cuh), so the exact form is bit-identical to one GPU; the fast
+// form's covariance sums are added over the ranks in rank order; the
+// zero-variance test's moments likewise; the host-side vector algebra runs
+// identically on every rank; rank r skips the first row0 jitter draws.
 void pca_init_dev(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d, uint64_t seed,
-                  double* layout_out, bool fast) {
+                  double* layout_out, bool fast, Comm* comm = nullptr, uint64_t row0 = 0,
+                  uint64_t N = 0) {
   cudaStream_t S = ctx->stream;
-  if (n < 2) fail(kParameter, "need at least 2 rows");
+  if (!comm) N = n;
+  if (N < 2) fail(kParameter, "need at least 2 rows");
   HostRng rng(HostRng::stream_seed(seed, 0x706361 /* "pca" */));
-  DBuf<double> mean(d), vd(d), yd(d), t(n), mom(2);
-  seq_column_means(ctx, x, d, nullptr, {0}, {n}, {0}, mean.p);  // pca.hpp:84-89
+  DBuf<double> mean(d), vd(d), yd(d), t(std::max<uint64_t>(n, 1)), mom(2);
+  if (!comm) {
+    seq_column_means(ctx, x, d, nullptr, {0}, {n}, {0}, mean.p);  // pca.hpp:84-89
+  } else {
+    comm->chain(mean.p, d, [&] {
+      if (n) seq_column_means(ctx, x, d, nullptr, {0}, {n}, {0}, mean.p, true);
+    });
+    k_div_vec<<<(unsigned)((d + 255) / 256), 256, 0, S>>>(mean.p, (uint32_t)d, (double)N);
+    note_launch(ctx, "k_div_vec");
+  }
   NB_CUDA(cudaMemsetAsync(mom.p, 0, 16, S));
-  k_pca_moments<<<ctx->sm_count * 8, 256, 0, S>>>(x, n * d, (uint32_t)d, mean.p, mom.p);
-  note_launch(ctx, "k_pca_moments");
+  if (n) {
+    k_pca_moments<<<ctx->sm_count * 8, 256, 0, S>>>(x, n * d, (uint32_t)d, mean.p, mom.p);
+    note_launch(ctx, "k_pca_moments");
+  }
   double mh[2];
   NB_CUDA(cudaMemcpyAsync(mh, mom.p, 16, cudaMemcpyDeviceToHost, S));
   NB_CUDA(cudaStreamSynchronize(S));
-  const double total_var = mh[0] / static_cast<double>(n);
-  const double total_sq = mh[1] / static_cast<double>(n);
+  if (comm) {  // rank-order sums of the ranks' moments
+    std::vector<double> all(2 * (size_t)comm->world);
+    comm->allgather(mh, 16, all.data());
+    mh[0] = mh[1] = 0.0;
+    for (int r = 0; r < comm->world; ++r) {
+      mh[0] += all[2 * r];
+      mh[1] += all[2 * r + 1];
+    }
+  }
+  const double total_var = mh[0] / static_cast<double>(N);
+  const double total_sq = mh[1] / static_cast<double>(N);
   if (total_var <= 1e-18 * std::max(1.0, total_sq))
     fail(kDegenerate, "data has zero variance");
 
@@ -326,24 +367,48 @@ void pca_init_dev(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d, uint64_t 
   DBuf<double> cov;
   if (fast) {
     cov.alloc(d * d);
-    covariance_sums(ctx, x, n, d, mean.p, cov.p);
+    if (n) covariance_sums(ctx, x, n, d, mean.p, cov.p);
+    else NB_CUDA(cudaMemsetAsync(cov.p, 0, d * d * 8, S));
+    if (comm) {  // S = sum over ranks in rank order
+      std::vector<double> mine(d * d), all((size_t)comm->world * d * d);
+      NB_CUDA(cudaMemcpyAsync(mine.data(), cov.p, d * d * 8, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+      comm->allgather(mine.data(), d * d * 8, all.data());
+      for (size_t e = 0; e < d * d; ++e) {
+        double acc = all[e];
+        for (int r = 1; r < comm->world; ++r) acc += all[(size_t)r * d * d + e];
+        mine[e] = acc;
+      }
+      NB_CUDA(cudaMemcpyAsync(cov.p, mine.data(), d * d * 8, cudaMemcpyHostToDevice, S));
+    }
   }
   auto cov_apply = [&](const std::vector<double>& v, std::vector<double>& out) {
     NB_CUDA(cudaMemcpyAsync(vd.p, v.data(), d * 8, cudaMemcpyHostToDevice, S));
     if (fast) {
       k_cov_apply<<<(unsigned)((d * 32 + 255) / 256), 256, 0, S>>>(cov.p, vd.p, (uint32_t)d,
-                                                                  1.0 / static_cast<double>(n), yd.p);
+                                                                  1.0 / static_cast<double>(N), yd.p);
       note_launch(ctx, "k_cov_apply");
       out.resize(d);
       NB_CUDA(cudaMemcpyAsync(out.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
       NB_CUDA(cudaStreamSynchronize(S));
       return;
     }
-    k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, vd.p, t.p, nullptr, nullptr);
-    note_launch(ctx, "k_pca_rows");
-    k_pca_cols<BR><<<(unsigned)((d + 31) / 32), 256, col_smem, S>>>(x, n, (uint32_t)d, mean.p,
-                                                                      t.p, yd.p);
-    note_launch(ctx, "k_pca_cols");
+    auto cols = [&](int carry) {
+      if (!n) return;
+      k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, vd.p, t.p, nullptr,
+                                            nullptr);
+      note_launch(ctx, "k_pca_rows");
+      k_pca_cols<BR><<<(unsigned)((d + 31) / 32), 256, col_smem, S>>>(x, n, (uint32_t)d, mean.p,
+                                                                        t.p, yd.p, carry);
+      note_launch(ctx, "k_pca_cols");
+    };
+    if (!comm) {
+      cols(0);
+    } else {  // y_j: the i-ascending chains continue rank to rank, then / N
+      comm->chain(yd.p, d, [&] { cols(1); });
+      k_div_vec<<<(unsigned)((d + 255) / 256), 256, 0, S>>>(yd.p, (uint32_t)d, (double)N);
+      note_launch(ctx, "k_div_vec");
+    }
     out.resize(d);
     NB_CUDA(cudaMemcpyAsync(out.data(), yd.p, d * 8, cudaMemcpyDeviceToHost, S));
     NB_CUDA(cudaStreamSynchronize(S));
@@ -426,33 +491,43 @@ void pca_init_dev(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d, uint64_t 
   NB_CUDA(cudaMemcpyAsync(b0.p, basis[0].data(), d * 8, cudaMemcpyHostToDevice, S));
   NB_CUDA(cudaMemcpyAsync(b1.p, basis[1].data(), d * 8, cudaMemcpyHostToDevice, S));
   // layout_i[comp] = j-ascending chain (pca.hpp:199-204), both components in one pass
-  k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, b0.p, layout_out,
-                                        layout_out + 1, b1.p);
-  note_launch(ctx, "k_pca_rows");
+  if (n) {
+    k_pca_rows<<<row_blocks, 128, 0, S>>>(x, n, (uint32_t)d, mean.p, b0.p, layout_out,
+                                          layout_out + 1, b1.p);
+    note_launch(ctx, "k_pca_rows");
+  }
   const bool rank_deficient = eigen[1] <= 1e-12 * std::max(eigen[0], 0.0);
   for (int comp = 0; comp < 2; ++comp) {  // pca.hpp:189-216
     if (comp == 1 && rank_deficient) {
-      std::vector<double> jit(n);
-      for (uint64_t i = 0; i < n; ++i) jit[i] = -1e-4 + (1e-4 - -1e-4) * rng.uniform01();
-      DBuf<double> jd(n);
-      NB_CUDA(cudaMemcpyAsync(jd.p, jit.data(), n * 8, cudaMemcpyHostToDevice, S));
-      k_layout_set<<<ctx->sm_count * 4, 256, 0, S>>>(layout_out, n, 1, jd.p);
-      note_launch(ctx, "k_layout_set");
+      if (n) {
+        rng.g.discard(row0);  // the draws of the rows before this rank's
+        std::vector<double> jit(n);
+        for (uint64_t i = 0; i < n; ++i) jit[i] = -1e-4 + (1e-4 - -1e-4) * rng.uniform01();
+        DBuf<double> jd(n);
+        NB_CUDA(cudaMemcpyAsync(jd.p, jit.data(), n * 8, cudaMemcpyHostToDevice, S));
+        k_layout_set<<<ctx->sm_count * 4, 256, 0, S>>>(layout_out, n, 1, jd.p);
+        note_launch(ctx, "k_layout_set");
+      }
       NB_CUDA(cudaStreamSynchronize(S));
       break;
     }
-    double h = 0.0;
-    k_seq_col<<<1, 256, 0, S>>>(layout_out, n, comp, 0, 0.0, st.p);
-    note_launch(ctx, "k_seq_col");
-    NB_CUDA(cudaMemcpyAsync(&h, st.p, 8, cudaMemcpyDeviceToHost, S));
-    NB_CUDA(cudaStreamSynchronize(S));
-    const double col_mean = h / static_cast<double>(n);
-    k_seq_col<<<1, 256, 0, S>>>(layout_out, n, comp, 1, col_mean, st.p);
-    note_launch(ctx, "k_seq_col");
-    NB_CUDA(cudaMemcpyAsync(&h, st.p, 8, cudaMemcpyDeviceToHost, S));
-    NB_CUDA(cudaStreamSynchronize(S));
-    const double sd = std::sqrt(h / static_cast<double>(n));
-    if (sd > 0.0) {
+    // sequential column sums (pca.hpp:197-212), carried over the ranks
+    auto col_sum = [&](int mode, double mu) {
+      auto run = [&](int carry) {
+        if (!n) return;
+        k_seq_col<<<1, 256, 0, S>>>(layout_out, n, comp, mode, mu, st.p, carry);
+        note_launch(ctx, "k_seq_col");
+      };
+      if (comm) comm->chain(st.p, 1, [&] { run(1); });
+      else run(0);
+      double h = 0.0;
+      NB_CUDA(cudaMemcpyAsync(&h, st.p, 8, cudaMemcpyDeviceToHost, S));
+      NB_CUDA(cudaStreamSynchronize(S));
+      return h;
+    };
+    const double col_mean = col_sum(0, 0.0) / static_cast<double>(N);
+    const double sd = std::sqrt(col_sum(1, col_mean) / static_cast<double>(N));
+    if (sd > 0.0 && n) {
       k_layout_scale<<<ctx->sm_count * 4, 256, 0, S>>>(layout_out, n, comp, sd);
       note_launch(ctx, "k_layout_scale");
     }
@@ -490,6 +565,79 @@ extern "C" int32_t nomad_b200_pca_init_fast(nomad_b200_ctx* ctx,
                                             const nomad_b200_dataset_view* data, uint64_t seed,
                                             double* layout_out, int32_t location) {
   return pca_entry(ctx, data, seed, layout_out, location, true);
+}
+
+// ---- row-sharded PCA: one rank's share of the rows
+namespace nb {
+static void pca_rank(nomad_b200_ctx* ctx, Comm* comm, const nomad_b200_dataset_view* rows,
+                     uint64_t row0, uint64_t n_total, uint64_t seed, bool fast, double* layout_out,
+                     int32_t location) {
+  DevData dd;
+  dd.bind(rows, ctx);
+  if (row0 + dd.n > n_total) fail(kParameter, "row slice outside the dataset");
+  if (location == NOMAD_B200_DEVICE) {
+    pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, layout_out, fast, comm, row0, n_total);
+  } else {
+    DBuf<double> lay(2 * dd.n);
+    pca_init_dev(ctx, dd.x, dd.n, dd.d, seed, lay.p, fast, comm, row0, n_total);
+    copy_d2h(ctx, layout_out, lay.p, dd.n * 16);
+  }
+}
+}  // namespace nb
+
+extern "C" int32_t nomad_b200_pca_init_sharded(nomad_b200_ctx* ctx, int32_t rank, int32_t world,
+                                               const void* nccl_id,
+                                               const nomad_b200_dataset_view* rows, uint64_t row0,
+                                               uint64_t n_total, uint64_t seed, int32_t fast,
+                                               double* layout_out, int32_t location) {
+  return guard([&] {
+    if (!ctx || !rows || !layout_out) fail(kParameter, "NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(kParameter, "bad rank / world_size");
+    bind_device(ctx);
+    std::unique_ptr<Comm> comm(make_nccl_comm(rank, world, nccl_id, ctx->stream));
+    pca_rank(ctx, comm.get(), rows, row0, n_total, seed, fast != 0, layout_out, location);
+  });
+}
+
+extern "C" int32_t nomad_b200_group_pca_init_sharded(nomad_b200_group* grp,
+                                                     const nomad_b200_dataset_view* rows,
+                                                     const uint64_t* row0, uint64_t n_total,
+                                                     uint64_t seed, int32_t fast,
+                                                     double* const* layout_out, int32_t location) {
+  return guard([&] {
+    if (!grp || !rows || !row0 || !layout_out) fail(kParameter, "NULL argument");
+    const int G = (int)grp->ctx.size();
+    GroupRendezvous* rz = make_rendezvous(G);
+    std::vector<std::exception_ptr> errs(G);
+    std::vector<std::thread> th;
+    for (int r = 0; r < G; ++r)
+      th.emplace_back([&, r] {
+        nomad_b200_ctx* c = grp->ctx[r];
+        cudaStream_t shared = c->stream;
+        cudaStream_t own = nullptr;
+        try {
+          bind_device(c);
+          // a private stream per rank thread (loopback ranks share one)
+          NB_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+          c->stream = own;
+          std::unique_ptr<Comm> comm(make_group_comm(rz, r, own, c->device));
+          pca_rank(c, comm.get(), rows + r, row0[r], n_total, seed, fast != 0, layout_out[r],
+                   location);
+        } catch (...) {
+          errs[r] = std::current_exception();
+          rendezvous_abort(rz);
+        }
+        if (own) {
+          cudaStreamSynchronize(own);
+          cudaStreamDestroy(own);
+        }
+        c->stream = shared;
+      });
+    for (auto& t : th) t.join();
+    free_rendezvous(rz);
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  });
 }
 
 // Debug / unit path: covariance sums of a dataset about `mean` (host d

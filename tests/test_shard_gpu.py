@@ -79,3 +79,56 @@ def test_single_rank_sharded_build(ctx):
     assert np.array_equal(cs.assignment, c1.assignment)
     assert np.array_equal(cs.centroids, c1.centroids)
     assert np.array_equal(gs.neighbors, g1.neighbors) and np.array_equal(gs.distances, g1.distances)
+
+
+@pytest.mark.parametrize("G,dtype", [(2, "f32"), (3, "f32"), (4, "bf16")])
+def test_sharded_pca_exact_equals_one_gpu(ctx, G, dtype):
+    """Row-sharded pca_init: the data mean, every covariance
+    apply's column chains and the layout's column mean / spread carried rank
+    to rank -> the one-GPU (= reference, test_fit_gpu.py) layout bit for bit."""
+    import torch
+    import paper_2505_15511_b200 as nb
+    n, d = 5000, 24
+    x = nb.generate_mixture(n, d, 6, 10.0, 5, ctx=ctx, dtype=dtype)
+    one = nb.pca_init(x, seed=3, ctx=ctx)
+    grp = nb.Group([0] * G)
+    sl = _slices(n, G, np.random.default_rng(10 + G))
+    rows = [x[a:a + m] for a, m in sl]
+    parts = nb.group_pca_init_sharded(grp, rows, [a for a, _ in sl], n, seed=3)
+    assert np.array_equal(np.concatenate(parts), one)
+    torch.cuda.synchronize()
+
+
+def test_sharded_pca_rank_deficient_jitter(ctx):
+    """Rank-1 data: the second component is the reference's uniform jitter
+    (pca.hpp:189-195), drawn in row order — every rank skips the draws of
+    the rows before its slice."""
+    import torch
+    import paper_2505_15511_b200 as nb
+    rng = np.random.default_rng(4)
+    n, d = 3000, 16
+    x = np.outer(rng.normal(size=n), rng.normal(size=d)).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    one = nb.pca_init(xt, seed=9, ctx=ctx)
+    grp = nb.Group([0] * 3)
+    sl = [(0, 1000), (1000, 700), (1700, 1300)]
+    parts = nb.group_pca_init_sharded(grp, [xt[a:a + m] for a, m in sl], [a for a, _ in sl], n,
+                                      seed=9)
+    assert np.array_equal(np.concatenate(parts), one)
+
+
+def test_sharded_pca_fast_same_plane(ctx):
+    """fast=True: the ranks' covariance sums added in rank order give the
+    one-GPU fast form's principal plane (orientation inside the plane is
+    rounding-level, pca.cu)."""
+    import paper_2505_15511_b200 as nb
+    n, d = 8000, 32
+    x = nb.generate_mixture(n, d, 8, 10.0, 6, ctx=ctx)
+    one = nb.pca_init(x, seed=1, ctx=ctx, fast=True)
+    grp = nb.Group([0] * 2)
+    parts = nb.group_pca_init_sharded(grp, [x[:3000], x[3000:]], [0, 3000], n, seed=1, fast=True)
+    two = np.concatenate(parts)
+    # both standardised: the same plane <=> Y1^T Y2 / n is orthogonal
+    m = one.T @ two / n
+    sv = np.linalg.svd(m, compute_uv=False)
+    np.testing.assert_allclose(sv, [1.0, 1.0], atol=1e-6)
