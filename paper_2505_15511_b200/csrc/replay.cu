@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(256) k_replay_touch(ReplayDev R, SgdParams P, 
   for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) {
     R.tkey[base + e] = sk[e];
     R.tval[base + e] = (uint32_t)(base + e);  // draw * T + slot
-    R.pred[base + e] = 0xFFFFFFFFu;
-    if (R.succ) R.succ[base + e] = 0xFFFFFFFFu;
+    if (R.link) R.link[base + e] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    else R.pred[base + e] = 0xFFFFFFFFu;
   }
 }
 
@@ -228,11 +228,15 @@ __global__ void k_replay_pred(ReplayDev R, uint64_t items) {
   if (e >= items) return;
   const uint32_t v = R.tkey[e];
   if (v == R.n_loc) return;
-  if (e > 0 && R.tkey[e - 1] == v) {
-    const uint32_t prev_draw = R.tval[e - 1] / R.T;  // global draw index
-    R.pred[R.tval[e]] = prev_draw - R.pt_base[v];     // the worker's draw t
+  uint32_t pd = 0xFFFFFFFFu;
+  if (e > 0 && R.tkey[e - 1] == v)
+    pd = R.tval[e - 1] / R.T - R.pt_base[v];  // the worker's draw t of the previous touch
+  if (R.link) {  // one record per touch: predecessor and successor together
+    const uint32_t nx = (e + 1 < items && R.tkey[e + 1] == v) ? R.tval[e + 1] : 0xFFFFFFFFu;
+    if (pd != 0xFFFFFFFFu || nx != 0xFFFFFFFFu) R.link[R.tval[e]] = make_uint2(pd, nx);
+  } else if (pd != 0xFFFFFFFFu) {
+    R.pred[R.tval[e]] = pd;
   }
-  if (R.succ && e + 1 < items && R.tkey[e + 1] == v) R.succ[R.tval[e]] = R.tval[e + 1];
 }
 
 // ------------------------------------------------------ dataflow SGD
@@ -257,6 +261,14 @@ __device__ __forceinline__ bool mbox_take(const double2* mb, double2& v) {
   if (x == kMboxEmpty || y == kMboxEmpty) return false;
   v = make_double2(__longlong_as_double((long long)x), __longlong_as_double((long long)y));
   return true;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void mbox_put(double2* mb, double2 v) {
   asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(mb),
@@ -497,9 +509,52 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
   // (resident: cooperative launch) warp — no claim counter, and a waiting
   // draw holds up only its own warp.
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw < R.followers) {
+    // Loss follower: worker w's per-draw losses summed in draw order
+    // (optimizer.hpp:289-290) as the draws complete, 32 slots at a time; a
+    // slot holds all-ones bits until its draw writes it, and is emptied again
+    // here for the next epoch. Off every dependency chain: draws never wait
+    // for a follower.
+    for (uint32_t w = gw; w < R.nwl; w += R.followers) {
+      const uint32_t D = P.workers[w].draws;
+      double* ls = P.loss_slot + R.draw_base[w];
+      double acc = 0.0;
+      for (uint32_t t0 = 0; t0 < D; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        double v = 0.0;
+        bool ok = t >= D;
+        uint32_t spins = 0, nap = min(64u, R.nap_cap);
+        for (;;) {
+          if (!ok) {
+            const unsigned long long b = ld_relaxed_u64(ls + t);
+            if (b != kMboxEmpty) {
+              v = __longlong_as_double((long long)b);
+              ok = true;
+            }
+          }
+          if (__all_sync(FULL, ok)) break;
+          if ((++spins & 63) == 0 &&
+              (*reinterpret_cast<volatile uint32_t*>(R.stall) || spins > (1u << 24)))
+            break;  // a stalled epoch: the trainer reports it
+          __nanosleep(nap);
+          nap = min(nap * 2, R.nap_cap);
+        }
+        if (t < D) st_relaxed_u64(ls + t, kMboxEmpty);
+        sa[lane] = v;
+        __syncwarp();
+        double a[1] = {acc};
+        const double* const vv[1] = {sa};
+        df_chains<1, false>(a, vv, 0, min(32u, D - t0), FULL);
+        acc = a[0];
+        __syncwarp();
+      }
+      if (lane == 0) R.wloss[w] = acc;
+    }
+    return;
+  }
   const uint64_t total = (uint64_t)R.nwl * R.max_draws;
-  for (uint64_t c = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < total;
-       c += nwarps) {
+  for (uint64_t c = gw - R.followers; c < total; c += nwarps - R.followers) {
     const uint32_t w = (uint32_t)(c % R.nwl);
     const WorkerDev W = P.workers[w];
     const uint32_t t = (uint32_t)(c / R.nwl);
@@ -518,8 +573,9 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     // predecessor-layout lane j (touch slot j): has an earlier touch this
     // epoch (its position arrives in mailbox i*T + j), and the touch to
     // forward the new position to (none: the epoch's last touch -> pos)
-    const bool has_pred = lane < T && R.pred[(size_t)i * T + lane] != 0xFFFFFFFFu;
-    const uint32_t succ = lane < T ? R.succ[(size_t)i * T + lane] : 0xFFFFFFFFu;
+    const uint2 lk = lane < T ? R.link[(size_t)i * T + lane] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    const bool has_pred = lk.x != 0xFFFFFFFFu;
+    const uint32_t succ = lk.y;
     double2* const mb = R.mbox + (size_t)i * T;
     uint32_t own = 0;
     double lm = W.local_mass;

@@ -50,9 +50,11 @@ struct ReplayDev {
   uint32_t* tval;              // per draw and slot: its flat index i * T + slot
   uint32_t* tkey2;             // radix-sort buffers
   uint32_t* tval2;
-  uint32_t* pred;              // per draw and slot: latest earlier draw touching it (none: ~0)
-  uint32_t* succ;              // per draw and slot: the next touch of its point, as a flat
-                               // touch index (none: ~0); warp form only (else nullptr)
+  uint32_t* pred;              // per draw and slot: latest earlier draw touching it (none: ~0);
+                               // per-thread form only (else nullptr)
+  uint2* link;                 // warp form: per draw and slot {latest earlier draw touching
+                               // it, the next touch of its point as a flat touch index}
+                               // (none: ~0), one 8-byte record (else nullptr)
   double2* mbox;               // per touch: the point's position forwarded by its
                                // predecessor (all-ones bits: not yet); warp form only
   uint32_t n_loc;              // local points (the "none" key)
@@ -65,6 +67,9 @@ struct ReplayDev {
   uint32_t total_chunks;       // warps' chunks of draws, worker-interleaved
   uint32_t max_draws, total_draws;
   uint32_t nap_cap;            // longest back-off sleep of a waiting draw (ns)
+  uint32_t followers;          // warp form: warps that sum the workers' losses in draw order
+                               // while the draws run (0: k_loss_seq afterwards)
+  double* wloss;               // per worker: the epoch's loss sum (followers)
 };
 
 void launch_mt_words(const ReplayDev& R, const uint64_t* counts, cudaStream_t st);

@@ -96,7 +96,7 @@ struct RankTrainer {
   DBuf<uint64_t> wcount, wbase;
   DBuf<unsigned long long> words, redges;
   DBuf<double2> rmbox;
-  DBuf<uint32_t> rsucc;
+  DBuf<uint2> rlink;
   DBuf<uint32_t> pool_d, pool_off_d, rheads, rtails, tkey, tval, tkey2, tval2, rpred, reject,
       ticket, pt_base, stall;
   DBuf<uint8_t> rdone, sort_tmp;
@@ -437,15 +437,19 @@ struct RankTrainer {
     tval.alloc(D * T);
     tkey2.alloc(D * T);
     tval2.alloc(D * T);
-    rpred.alloc(D * T);
     if (dataflow_warp_form((uint32_t)k, (uint32_t)s)) {  // position mailboxes (replay.cu)
-      rsucc.alloc(D * T);
+      rlink.alloc(D * T);
       rmbox.alloc(D * T);
       // all empty; every mailbox is emptied again by its reader, so one fill lasts
       NB_CUDA(cudaMemsetAsync(rmbox.p, 0xFF, rmbox.bytes(), S));
+    } else {
+      rpred.alloc(D * T);
     }
     rdone.alloc(D);
     loss_slot.alloc(D);
+    // (warp form: all-ones = not yet written; the loss followers empty each
+    // slot again after reading it, so one fill lasts)
+    NB_CUDA(cudaMemsetAsync(loss_slot.p, 0xFF, loss_slot.bytes(), S));
     reject.alloc(std::max<uint32_t>(nwl, 1));
     redges.alloc(std::max<uint32_t>(nwl, 1));
     ticket.alloc(1);
@@ -472,7 +476,7 @@ struct RankTrainer {
     R.tkey2 = tkey2.p;
     R.tval2 = tval2.p;
     R.pred = rpred.p;
-    R.succ = rsucc.p;
+    R.link = rlink.p;
     R.mbox = rmbox.p;
     R.n_loc = (uint32_t)orig_of.size();
     R.reject = reject.p;
@@ -480,6 +484,13 @@ struct RankTrainer {
     R.done = rdone.p;
     R.ticket = ticket.p;
     R.stall = stall.p;
+    R.wloss = wloss.p;
+    // loss followers (warp form), when the grid leaves room for them
+    R.followers = 0;
+    if (rlink.p && df_blocks) {
+      const uint32_t f = std::min<uint32_t>(std::max<uint32_t>(nwl, 1), 32u);
+      if ((uint64_t)df_blocks * 8 >= 8ull * f) R.followers = f;  // at most 1/8 of the warps
+    }
     R.pt_base = pt_base.p;
     const uint32_t per = dataflow_draws_per_chunk((uint32_t)k, (uint32_t)s);
     R.total_chunks = nwl * ((max_draws + per - 1) / per);
@@ -527,6 +538,8 @@ struct RankTrainer {
   // dataflow SGD -> per-worker losses in draw order.
   void launch_replay_epoch(SgdParams& P) {
     cudaStream_t S = st();
+    if (!df_blocks)
+      df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
     ReplayDev R = replay_dev();
     NB_CUDA(cudaMemsetAsync(reject.p, 0, reject.bytes(), S));
     NB_CUDA(cudaMemsetAsync(redges.p, 0, redges.bytes(), S));
@@ -556,8 +569,10 @@ struct RankTrainer {
     if (nwl && total_draws) {
       launch_sgd_dataflow(P, R, df_blocks, smem_replay, S);
       launched("k_sgd_dataflow");
-      launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
-      launched("k_loss_seq");
+      if (!R.followers) {  // (warp form: the dataflow kernel's followers summed them)
+        launch_loss_seq(loss_slot.p, wk_draw_base.p, wk_d.p, nwl, wloss.p, S);
+        launched("k_loss_seq");
+      }
     }
     NB_CUDA(cudaEventRecord(ev[1], S));
     std::swap(mt_a, mt_b);  // this epoch's end state starts the next
@@ -934,6 +949,7 @@ struct RankTrainer {
         // leave the mailboxes empty for any later epoch (a stalled epoch
         // may have left values in them)
         if (rmbox.p) NB_CUDA(cudaMemsetAsync(rmbox.p, 0xFF, rmbox.bytes(), st()));
+        if (rlink.p) NB_CUDA(cudaMemsetAsync(loss_slot.p, 0xFF, loss_slot.bytes(), st()));
         fail(kInternal, "replay dataflow stalled (schedule watchdog)");
       }
     }
