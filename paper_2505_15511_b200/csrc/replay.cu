@@ -744,6 +744,21 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       ax = __dmul_rn(-pull, dx);
       ay = __dmul_rn(-pull, dy);
     }
+    // A neighbour slot whose point no other slot of this draw holds is final
+    // now (its update needs neither bgs nor the head's sums): forward it at
+    // once — the long chains of the kNN graph run through neighbour slots.
+    const bool solo = is_nb && grp == (1u << lane);
+    if (solo) {
+      double2 v = pv;
+      if (slot) {
+        v.x = __dsub_rn(v.x, __dmul_rn(st, ax));
+        v.y = __dsub_rn(v.y, __dmul_rn(st, ay));
+        if (diverged(v.x, v.y))
+          atomicMin(P.diverge + w, ((unsigned long long)t * stride + lane) << 32 | pt);
+      }
+      if (fwd != 0xFFFFFFFFu) mbox_put(R.mbox + fwd, v);
+      else __stcg(P.pos + pt, v);
+    }
     double bgs, gx, gy;
     {
       sb[lane] = tb;
@@ -829,7 +844,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     sb[lane] = ay;
     __syncwarp();
     DF_MARK(6);
-    if (lane < nsl && lane == fl) {
+    if (lane < nsl && lane == fl && !solo) {
       double2 v = pv;
       if (slot)
         for (uint32_t m = same; m; m &= m - 1) {
