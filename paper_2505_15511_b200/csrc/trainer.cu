@@ -93,6 +93,16 @@ struct RankTrainer {
   // (double-buffered epoch start / end states); host copies only for seek and
   // the rejection fallback
   DBuf<MtState> mt_a, mt_b;
+  // the next epoch's words, formed on a side stream while this epoch's
+  // dependency pass runs: words2 + the state after them (mt_c), valid for
+  // epoch pre_epoch (prefetch off for ranks sharing a device: the dataflow
+  // kernel needs every SM to itself)
+  DBuf<MtState> mt_c;
+  DBuf<unsigned long long> words2;
+  bool prefetch = true, pre_ok = false;
+  uint64_t pre_epoch = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t pre_ev = nullptr, map_ev = nullptr;
   DBuf<uint64_t> wcount, wbase;
   DBuf<unsigned long long> words, redges;
   DBuf<double2> rmbox;
@@ -134,6 +144,12 @@ struct RankTrainer {
   void bind() { bind_device(ctx); }
   void launched(const char* name) { note_launch(ctx, name); }
   ~RankTrainer() {
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+    }
+    if (pre_ev) cudaEventDestroy(pre_ev);
+    if (map_ev) cudaEventDestroy(map_ev);
     if (comm && own_comm) ncclCommDestroy(comm);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -543,9 +559,19 @@ struct RankTrainer {
     ReplayDev R = replay_dev();
     NB_CUDA(cudaMemsetAsync(reject.p, 0, reject.bytes(), S));
     NB_CUDA(cudaMemsetAsync(redges.p, 0, redges.bytes(), S));
-    if (nwl) {
+    if (pre_ok && pre_epoch == epochs_done) {
+      // this epoch's words and end state were formed during the last epoch
+      std::swap(words, words2);
+      std::swap(mt_b, mt_c);
+      R.words = words.p;
+      R.st_out = mt_b.p;
+      NB_CUDA(cudaStreamWaitEvent(S, pre_ev, 0));
+    } else if (nwl) {
       launch_mt_words(R, wcount.p, S);
       launched("k_mt_words");
+    }
+    pre_ok = false;
+    if (nwl) {
       launch_replay_map(R, P, pool_d.p, pool_off_d.p, S);
       launched("k_replay_map");
     }
@@ -557,8 +583,33 @@ struct RankTrainer {
     const bool force = std::getenv("NOMAD_B200_REPLAY_HOST_DRAWS") != nullptr;
     for (uint32_t wl = 0; wl < nwl; ++wl)
       if (rj[wl] || force) host_draws(wl);
+    // the next epoch's MT words on the side stream (its start state, mt_b, is
+    // final now), overlapping this epoch's dependency pass
+    const bool pf = prefetch && nwl && epochs_done + 1 < cfg.epochs;
+    if (pf) {
+      if (!side) {
+        NB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        NB_CUDA(cudaEventCreateWithFlags(&pre_ev, cudaEventDisableTiming));
+        NB_CUDA(cudaEventCreateWithFlags(&map_ev, cudaEventDisableTiming));
+      }
+      if (!words2.p) words2.alloc(words.n);
+      if (!mt_c.p) mt_c.alloc(mt_b.n);
+      ReplayDev Rn = R;
+      Rn.st_in = mt_b.p;
+      Rn.st_out = mt_c.p;
+      Rn.words = words2.p;
+      NB_CUDA(cudaEventRecord(map_ev, S));  // this epoch's map read its words
+      NB_CUDA(cudaStreamWaitEvent(side, map_ev, 0));
+      launch_mt_words(Rn, wcount.p, side);
+      launched("k_mt_words");
+      NB_CUDA(cudaEventRecord(pre_ev, side));
+      pre_ok = true;
+      pre_epoch = epochs_done + 1;
+    }
     launch_replay_deps(R, P, sort_tmp.p, sort_bytes, S);
     launched("k_replay_deps");
+    // the cooperative dataflow kernel needs every SM: the side stream's work first
+    if (pf) NB_CUDA(cudaStreamWaitEvent(S, pre_ev, 0));
     if (!df_blocks)
       df_blocks = dataflow_resident_blocks(smem_replay, ctx->sm_count, (uint32_t)k, (uint32_t)s);
     NB_CUDA(cudaMemsetAsync(rdone.p, 0, rdone.bytes(), S));
@@ -783,6 +834,7 @@ struct RankTrainer {
         }
       for (uint32_t wl = 0; wl < nwl; ++wl)
         NB_CUDA(cudaMemcpy(mt_a.p + wl, &m[wl].s, sizeof(MtState), cudaMemcpyHostToDevice));
+      pre_ok = false;  // a prefetched epoch is no longer the next one
     }
     epochs_done = e;
   }
@@ -1295,6 +1347,7 @@ int32_t nomad_b200_group_trainer_create(nomad_b200_group* grp, const nomad_b200_
       t->rank = rk;
       t->world = G;
       t->grouped = true;
+      t->prefetch = !grp->loopback;  // ranks on one device: no concurrent side-stream work
       t->comm = grp->comm.empty() ? nullptr : static_cast<ncclComm_t>(grp->comm[rk]);
       t->bind();
       t->setup(g, c, in, in_loc, nullptr);
