@@ -456,25 +456,30 @@ __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) 
 constexpr uint32_t kDfBatch = 8;  // R.total_chunks granularity reported for the warp form
 
 // Chains of the warp form: acc[c] = acc[c] (+|-) v[c][j] for j in [j0, j1)
-// whose bit in `mask` is set, in ascending j — the reference's summation
-// order. Terms sit in the warp's 32-entry shared scratch (broadcast reads);
-// each batch issues its 8 loads together (indices clamped to the scratch,
-// adds predicated), so one shared-memory latency covers 8 dependent adds.
+// in ascending j — the reference's summation order. Terms sit in the warp's
+// shared scratch (broadcast reads), 32 entries per array followed by 8
+// entries that stay zero; terms the reference skips are staged as +0.0.
+// Batches of 8 issue their loads together (one shared-memory latency covers
+// 8 dependent adds) and run unpredicated past j1 into zeros: adding or
+// subtracting +0.0 leaves every value unchanged except an accumulator of
+// -0.0 under addition, and an accumulator that starts at +0.0 never becomes
+// -0.0 (in round-to-nearest a sum is -0.0 only if both operands are), so the
+// padded chains give the reference's bits.
+constexpr uint32_t kDfScr = 40;  // doubles per scratch array
 template <int NC, bool SUB>
 __device__ __forceinline__ void df_chains(double (&acc)[NC], const double* const (&v)[NC],
-                                          uint32_t j0, uint32_t j1, uint32_t mask) {
+                                          uint32_t j0, uint32_t j1) {
   for (uint32_t j = j0; j < j1; j += 8) {
     double x[NC][8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
 #pragma unroll
-      for (int c = 0; c < NC; ++c) x[c][e] = v[c][min(j + e, 31u)];
+      for (int c = 0; c < NC; ++c) x[c][e] = v[c][j + e];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      if (j + e < j1 && ((mask >> ((j + e) & 31)) & 1u))
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
-          acc[c] = SUB ? __dsub_rn(acc[c], x[c][e]) : __dadd_rn(acc[c], x[c][e]);
+      for (int c = 0; c < NC; ++c)
+        acc[c] = SUB ? __dsub_rn(acc[c], x[c][e]) : __dadd_rn(acc[c], x[c][e]);
   }
 }
 
@@ -487,8 +492,10 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
   double* wt = sm;
   double* cms = sm + (k + 1) * k;
   const size_t tab = (size_t)(k + 1) * k + (P.gcells ? 0 : 3 * (size_t)C);
-  double* scr = sm + ((tab + 1) & ~(size_t)1) + (threadIdx.x >> 5) * 4 * 32;
-  double *sa = scr, *sb = scr + 32, *sc = scr + 64, *sd = scr + 96;
+  double* scr = sm + ((tab + 1) & ~(size_t)1) + (threadIdx.x >> 5) * 4 * kDfScr;
+  double *sa = scr, *sb = scr + kDfScr, *sc = scr + 2 * kDfScr, *sd = scr + 3 * kDfScr;
+  if ((threadIdx.x & 31) < 8)  // the zero tails of the four arrays (never written again)
+    for (int a = 0; a < 4; ++a) scr[a * kDfScr + 32 + (threadIdx.x & 31)] = 0.0;
   for (uint32_t i = threadIdx.x; i < (k + 1) * k; i += blockDim.x) wt[i] = P.wtab[i];
   if (!P.gcells)
     for (uint32_t r = threadIdx.x; r < C; r += blockDim.x) {
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
         __syncwarp();
         double a[1] = {acc};
         const double* const vv[1] = {sa};
-        df_chains<1, false>(a, vv, 0, min(32u, D - t0), FULL);
+        df_chains<1, false>(a, vv, 0, 32);
         acc = a[0];
         __syncwarp();
       }
@@ -698,7 +705,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       __syncwarp();
       double acc[1] = {remote_sum};
       const double* const v[1] = {sa};
-      df_chains<1, false>(acc, v, 0, min(32u, nr - q0), um);
+      df_chains<1, false>(acc, v, 0, min(32u, nr - q0));  // skipped cells staged as 0
       remote_sum = acc[0];
       __syncwarp();
     }
@@ -710,7 +717,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       __syncwarp();
       double acc[1] = {0.0};
       const double* const v[1] = {sa};
-      df_chains<1, false>(acc, v, cnt + 1, nsl, FULL);
+      df_chains<1, false>(acc, v, cnt + 1, nsl);
       qsum = acc[0];
       __syncwarp();
     }
@@ -767,7 +774,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       __syncwarp();
       double acc[3] = {0.0, 0.0, 0.0};  // three independent chains, list order
       const double* const v[3] = {sb, sc, sd};
-      df_chains<3, false>(acc, v, 1, cnt + 1, FULL);
+      df_chains<3, false>(acc, v, 1, cnt + 1);
       bgs = acc[0];
       gx = acc[1];
       gy = acc[2];
@@ -787,7 +794,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       __syncwarp();
       double acc[2] = {gx, gy};
       const double* const v[2] = {sa, sb};
-      df_chains<2, true>(acc, v, cnt + 1, nsl, FULL);
+      df_chains<2, true>(acc, v, cnt + 1, nsl);
       gx = acc[0];
       gy = acc[1];
       __syncwarp();
@@ -827,7 +834,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       __syncwarp();
       double acc[2] = {gx, gy};
       const double* const v[2] = {sa, sb};
-      df_chains<2, true>(acc, v, 0, min(32u, nr - q0), um);
+      df_chains<2, true>(acc, v, 0, min(32u, nr - q0));
       gx = acc[0];
       gy = acc[1];
       __syncwarp();
@@ -869,7 +876,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       __syncwarp();
       double acc[1] = {0.0};
       const double* const v[1] = {sa};
-      df_chains<1, false>(acc, v, 1, cnt + 1, FULL);
+      df_chains<1, false>(acc, v, 1, cnt + 1);
       if (lane == 0) P.loss_slot[i] = acc[0];
       __syncwarp();
     }
@@ -938,9 +945,10 @@ bool dataflow_warp_form(uint32_t k, uint32_t s) {
 uint32_t dataflow_draws_per_chunk(uint32_t k, uint32_t s) {
   return dataflow_warp_form(k, s) ? kDfBatch : 32;
 }
-// per-warp scratch of the warp form: 4 x 32 doubles (8 warps per block)
+// per-warp scratch of the warp form: 4 x kDfScr doubles (8 warps per block)
 static size_t df_smem(size_t smem, uint32_t k, uint32_t s) {
-  return dataflow_warp_form(k, s) ? ((smem + 15) & ~(size_t)15) + 8 * 4 * 32 * sizeof(double) : smem;
+  return dataflow_warp_form(k, s) ? ((smem + 15) & ~(size_t)15) + 8 * 4 * kDfScr * sizeof(double)
+                                   : smem;
 }
 
 void launch_sgd_dataflow(const SgdParams& P, const ReplayDev& R, uint32_t nblocks, size_t smem,
