@@ -514,7 +514,7 @@ struct RankTrainer {
     R.total_draws = total_draws;
     static const uint32_t nap = [] {
       const char* e = std::getenv("NOMAD_B200_DF_NAP");
-      return e ? (uint32_t)std::max(1, std::atoi(e)) : 256u;
+      return e ? (uint32_t)std::max(1, std::atoi(e)) : 64u;
     }();
     R.nap_cap = nap;
     return R;
