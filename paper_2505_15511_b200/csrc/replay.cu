@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     const uint2 lk = lane < T ? R.link[(size_t)i * T + lane] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
     const bool has_pred = lk.x != 0xFFFFFFFFu;
     const uint32_t succ = lk.y;
-    double2* const mb = R.mbox + (size_t)i * T;
+    double2* const myb = R.mbox + ((size_t)i * T + lane);  // this lane's mailbox
     uint32_t own = 0;
     double lm = W.local_mass;
     if (P.all_but_own) {
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       uint32_t spins = 0, nap = min(64u, R.nap_cap);
       bool abort = false, ok = !mine || !has_pred;
       for (;;) {
-        if (!ok) ok = mbox_take(mb + lane, got);
+        if (!ok) ok = mbox_take(myb, got);
         if (__all_sync(FULL, ok)) break;
         if ((++spins & 63) == 0 &&
             (*reinterpret_cast<volatile uint32_t*>(R.stall) || spins > (1u << 22))) {
@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
     // every mailbox is read once: empty it again for the next epoch (no
     // per-epoch fill), off the dependency chain
     if (has_pred)
-      mbox_put(mb + lane, make_double2(__longlong_as_double((long long)kMboxEmpty),
+      mbox_put(myb, make_double2(__longlong_as_double((long long)kMboxEmpty),
                                        __longlong_as_double((long long)kMboxEmpty)));
     __syncwarp();  // the updates read from the scratch before it is reused
     // the draw's loss (objective.hpp:197-213): sum over the list in order
