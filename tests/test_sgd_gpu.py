@@ -126,6 +126,38 @@ def test_replay_ablation_modes(port, ctx, mode):
     np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
 
 
+@pytest.mark.parametrize("head_only", [False, True])
+def test_replay_star_graph_chains(port, ctx, head_only):
+    """Every row of a cluster lists the cluster's first point (a star), so
+    each worker's epoch is one long dependency chain through that point —
+    the case the early neighbour forward and the position mailboxes exist
+    for — plus repeats of the centre inside some lists: bit-identical."""
+    import paper_2505_15511_b200 as nb
+    x, c, g, pca = index_case(3000, 32, 10, 8, 15)
+    a = np.asarray(c.assignment)
+    off = np.asarray(g.offsets).astype(np.int64)
+    nbr = np.asarray(g.neighbors).copy()
+    first = {int(r): int(np.flatnonzero(a == r)[0]) for r in np.unique(a)}
+    for i in range(len(a)):
+        ctr = first[int(a[i])]
+        if ctr != i and off[i + 1] > off[i]:
+            nbr[off[i]] = ctr                       # the centre leads every list
+            if i % 7 == 0 and off[i + 1] - off[i] > 3:
+                nbr[off[i] + 2] = ctr               # and repeats in some
+    g2 = nb.KnnGraph(len(a), g.k, g.offsets, nbr, np.zeros(0))
+    kw = dict(epochs=10, workers=4, seed=13, head_only=head_only)
+    okw = dict(epochs=10, workers=4, seed=13, head_only=int(head_only))
+    cfg = nb.TrainConfig(**kw)
+    tr = nb.Trainer(g2, nb.ClusterAssignment(c.assignment, c.n_clusters, c.dims, c.centroids,
+                                             c.sizes), pca, cfg, ctx=ctx)
+    loss = tr.run(4)
+    from oracle import train_config
+    rl, rloss, _, _ = port.train_epochs(c.assignment, c.n_clusters, g.offsets, nbr, g.k,
+                                        train_config(**okw), pca, 0, 4)
+    assert np.array_equal(tr.layout(), rl)
+    np.testing.assert_allclose(loss, rloss, rtol=1e-13, atol=0)
+
+
 def test_replay_ragged_neighbor_lists(port, ctx):
     """Clusters smaller than k+1 give short lists (knn.hpp:77-83)."""
     import paper_2505_15511_b200 as nb
