@@ -89,3 +89,28 @@ def test_kmeans_last_step_matches_reference(scale, ctx):
         assert np.array_equal(ref, cl.centroids[r * d:(r + 1) * d]), f"{name}: centroid {r}"
     print(f"config {name}: {iters} Lloyd iterations; last assignment step and centroids "
           f"identical to the reference ({orc.which})")
+
+
+def test_replay_epochs_match_reference(scale, ctx):
+    """The deterministic epoch loop at the BASELINE scale: two replay epochs
+    (W = 8, the real kNN graph with its hub points) from a fixed layout give
+    the reference's epoch loop (optimizer.hpp:342-452, run by the oracle on
+    the same index) bit for bit — positions, per-epoch losses within the log
+    ulp, cluster means."""
+    import paper_2505_15511_b200 as nb
+    from oracle import train_config
+    name, x, c0, cl, iters, g = scale
+    orc = _checker()
+    n = len(cl.assignment)
+    init = np.random.default_rng(1234).standard_normal((n, 2))
+    kw = dict(epochs=200, workers=8, seed=7)
+    tr = nb.Trainer(g, cl, init, nb.TrainConfig(sgd_mode="replay", **kw), ctx=ctx)
+    loss = tr.run(2)
+    rl, rloss, rmeans, secs = orc.train_epochs(cl.assignment, cl.n_clusters, g.offsets,
+                                               g.neighbors, 15, train_config(**kw), init, 0, 2)
+    assert np.array_equal(tr.layout(), rl), f"config {name}: layouts differ"
+    np.testing.assert_allclose(loss, rloss[:2], rtol=1e-13, atol=0)
+    m, _ = tr.means()
+    assert np.array_equal(m, rmeans)
+    print(f"config {name}: 2 replay epochs identical to the reference ({orc.which}, "
+          f"{secs:.1f} s on the CPU)")
