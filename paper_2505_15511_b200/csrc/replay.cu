@@ -276,6 +276,15 @@ __device__ __forceinline__ void mbox_put(double2* mb, double2 v) {
                "l"((unsigned long long)__double_as_longlong(v.y))
                : "memory");
 }
+// A forwarded position whose bits happen to be the empty pattern (only an
+// all-ones NaN, e.g. one passed in unchanged by a caller's layout) is sent as
+// another NaN so the reader is never left waiting.
+__device__ __forceinline__ void mbox_forward(double2* mb, double2 v) {
+  const long long nan = 0x7FFFFFFFFFFFFFFFll;
+  if (__double_as_longlong(v.x) == (long long)kMboxEmpty) v.x = __longlong_as_double(nan);
+  if (__double_as_longlong(v.y) == (long long)kMboxEmpty) v.y = __longlong_as_double(nan);
+  mbox_put(mb, v);
+}
 
 __global__ void __launch_bounds__(256) k_sgd_dataflow(SgdParams P, ReplayDev R) {
   extern __shared__ __align__(16) double sm[];
@@ -763,7 +772,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
         if (diverged(v.x, v.y))
           atomicMin(P.diverge + w, ((unsigned long long)t * stride + lane) << 32 | pt);
       }
-      if (fwd != 0xFFFFFFFFu) mbox_put(R.mbox + fwd, v);
+      if (fwd != 0xFFFFFFFFu) mbox_forward(R.mbox + fwd, v);
       else __stcg(P.pos + pt, v);
     }
     double bgs, gx, gy;
@@ -861,7 +870,7 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
           if (diverged(v.x, v.y))
             atomicMin(P.diverge + w, ((unsigned long long)t * stride + u) << 32 | pt);
         }
-      if (fwd != 0xFFFFFFFFu) mbox_put(R.mbox + fwd, v);
+      if (fwd != 0xFFFFFFFFu) mbox_forward(R.mbox + fwd, v);
       else __stcg(P.pos + pt, v);
     }
     // every mailbox is read once: empty it again for the next epoch (no
