@@ -886,7 +886,10 @@ __global__ void __launch_bounds__(256, DF_MINB) k_sgd_dataflow_warp(SgdParams P,
       double acc[1] = {0.0};
       const double* const v[1] = {sa};
       df_chains<1, false>(acc, v, 1, cnt + 1);
-      if (lane == 0) P.loss_slot[i] = acc[0];
+      if (lane == 0)  // (never the all-ones pattern the loss followers wait on)
+        P.loss_slot[i] = __double_as_longlong(acc[0]) == (long long)kMboxEmpty
+                             ? __longlong_as_double(0x7FFFFFFFFFFFFFFFll)
+                             : acc[0];
       __syncwarp();
     }
 #ifdef DF_TRACE
