@@ -650,7 +650,8 @@ __global__ void k_sizes2(const uint32_t* a, uint64_t n, uint32_t* sizes) {
 void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
                        DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
-                       const std::vector<uint8_t>* own, int kp16);
+                       const std::vector<uint8_t>* own, int kp16, uint32_t max_qtiles = 0,
+                       bool keep = false);
 
 // Builds the graph into device buffers (offsets n+1, nb/dist offsets[n]).
 struct KnnResult {
@@ -1262,8 +1263,57 @@ void build_knn_exact(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
       return e && std::atoi(e) == 64;
     }();
     const int kp_main = (k <= 24 && !force64) ? 32 : 64;
-    knn_tc_candidates(ctx, x, n, d, assign_d, C, mode == NOMAD_B200_KNN_EXACT, cid, clb, ccnt,
-                      &KP, own, kp_main);
+    if (mode == NOMAD_B200_KNN_EXACT && C > 1) {
+      // Probe: the first query tile (128 rows) of every cluster through the
+      // certified filter + re-rank. A large cluster where most probe rows
+      // stay uncertified spans several blobs (its centred norms dwarf its
+      // neighbour distances): the main pass skips it and its rows go straight
+      // to the sub-cluster stage, which the main pass could not spare them.
+      // A wrong guess only moves rows between exact stages.
+      knn_tc_candidates(ctx, x, n, d, assign_d, C, true, cid, clb, ccnt, &KP, own, kp_main, 1);
+      std::vector<uint32_t> probe;
+      std::vector<uint64_t> pcount(C, 0);
+      {
+        std::vector<uint32_t> mh(n);
+        NB_CUDA(cudaMemcpy(mh.data(), mem.p, n * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t r = 0; r < C; ++r) {
+          const uint64_t sz = off[r + 1] - off[r];
+          if (sz < 2 || (own && !(*own)[r])) continue;
+          const uint64_t m = std::min<uint64_t>(sz, 128);
+          pcount[r] = m;
+          probe.insert(probe.end(), mh.begin() + off[r], mh.begin() + off[r] + m);
+        }
+      }
+      std::vector<uint32_t> failed;
+      if (!probe.empty()) {
+        DBuf<uint32_t> pd;
+        upload_rows(probe, pd);
+        failed = rerank_rows(pd.p, probe.size());
+      }
+      std::vector<uint64_t> pfail(C, 0);
+      {
+        std::vector<uint32_t> ah0(n);
+        NB_CUDA(cudaMemcpy(ah0.data(), assign_d, n * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t q : failed) ++pfail[ah0[q]];
+      }
+      std::vector<uint8_t> own2(C, 1);
+      uint32_t skipped = 0;
+      for (uint32_t r = 0; r < C; ++r) {
+        if (own && !(*own)[r]) own2[r] = 0;
+        const uint64_t sz = off[r + 1] - off[r];
+        if (sz >= 1024 && pcount[r] && pfail[r] * 2 >= pcount[r]) {
+          own2[r] = 0;
+          ++skipped;
+        }
+      }
+      stage_done("probe");
+      if (dbg) std::fprintf(stderr, "knn probe: %u multi-blob clusters skip the main pass\n", skipped);
+      knn_tc_candidates(ctx, x, n, d, assign_d, C, true, cid, clb, ccnt, &KP, &own2, kp_main, 0,
+                        true);
+    } else {
+      knn_tc_candidates(ctx, x, n, d, assign_d, C, mode == NOMAD_B200_KNN_EXACT, cid, clb, ccnt,
+                        &KP, own, kp_main);
+    }
     stage_done("tensor-core candidates");
     open = rerank_rows(std::getenv("NOMAD_B200_KNN_IDORDER") ? nullptr : mem.p, n);
     R.tc_uncertified = open.size();

@@ -484,7 +484,8 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
                      uint32_t C,
                      const std::vector<uint64_t>& off, const uint32_t* mem_d,
                      const std::vector<uint32_t>& grp, const double* means_p,
-                     DBuf<uint32_t>& cand_ids, DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt) {
+                     DBuf<uint32_t>& cand_ids, DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt,
+                     uint32_t max_qtiles) {
   cudaStream_t S = ctx->stream;
   const uint32_t G = (uint32_t)grp.size();
   std::vector<uint64_t> pstart(G + 1, 0);
@@ -501,7 +502,7 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
     gl[3 * g] = pstart[g];
     gl[3 * g + 1] = off[r];
     gl[3 * g + 2] = sz;
-    for (uint64_t q = 0; q < sz; q += TM)
+    for (uint64_t q = 0; q < sz && (max_qtiles == 0 || q < (uint64_t)max_qtiles * TM); q += TM)
       tiles.push_back(TcTile{(uint32_t)(pstart[g] + q), (uint32_t)pstart[g], (uint32_t)sz,
                              (uint32_t)q, r});
   }
@@ -579,7 +580,8 @@ static void tc_group(nomad_b200_ctx* ctx, XPtr x, uint64_t d, uint64_t dpad, boo
 void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
                        const uint32_t* assign_d, uint32_t C, bool fp16, DBuf<uint32_t>& cand_ids,
                        DBuf<float>& cand_lb, DBuf<uint32_t>& cand_cnt, int* kp_out,
-                       const std::vector<uint8_t>* own, int kp16) {
+                       const std::vector<uint8_t>* own, int kp16, uint32_t max_qtiles,
+                       bool keep) {
   cudaStream_t S = ctx->stream;
   const int KP = fp16 ? (kp16 == 32 ? 32 : 64) : 32;
   *kp_out = KP;
@@ -602,10 +604,14 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
     fast_column_means(ctx, x, d, mem.p, beg, cnt, rows, means.p);
   }
   tc_lap(S, "grouping + means");
-  cand_ids.alloc(n * (uint64_t)KP);
-  cand_lb.alloc(n);
-  cand_cnt.alloc(n);
-  NB_CUDA(cudaMemsetAsync(cand_cnt.p, 0, n * 4, S));
+  if (!keep) {  // (keep: a second pass over other clusters into the same lists)
+    cand_ids.alloc(n * (uint64_t)KP);
+    cand_lb.alloc(n);
+    cand_cnt.alloc(n);
+    NB_CUDA(cudaMemsetAsync(cand_cnt.p, 0, n * 4, S));
+    // rows no pass reaches keep an empty list with bound 0: never certified
+    NB_CUDA(cudaMemsetAsync(cand_lb.p, 0, n * 4, S));
+  }
   const uint64_t dpad = (d + KC - 1) / KC * KC;
   // Clusters are processed in groups whose padded 16-bit copy fits half of
   // the free device memory (one group unless the dataset is very large, e.g.
@@ -636,7 +642,8 @@ void knn_tc_candidates(nomad_b200_ctx* ctx, XPtr x, uint64_t n, uint64_t d,
       acc += pr;
       ++gi;
     }
-    tc_group(ctx, x, d, dpad, fp16, KP, C, off, mem.p, grp, means.p, cand_ids, cand_lb, cand_cnt);
+    tc_group(ctx, x, d, dpad, fp16, KP, C, off, mem.p, grp, means.p, cand_ids, cand_lb, cand_cnt,
+             max_qtiles);
   }
 }
 
