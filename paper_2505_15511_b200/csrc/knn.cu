@@ -851,6 +851,8 @@ void ffma_filter(nomad_b200_ctx* ctx, const float* x, uint64_t d, const uint32_t
 }
 
 // Stage 1b for one cluster (members[0..m)): returns the rows it certified.
+constexpr uint64_t kBisectSample = 16384;  // rows that shape a bisection (knn subcluster_stage)
+
 uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_t* members,
                           uint64_t m, uint32_t k, int KP, DBuf<uint32_t>& cid, DBuf<float>& clb,
                           DBuf<uint32_t>& ccnt, std::vector<uint32_t>& cert_out) {
@@ -885,7 +887,7 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
   // degenerate.
   // bisection scratch, sized for the whole cluster once (cudaMalloc / cudaFree
   // per bisection would dominate the stage)
-  DBuf<uint32_t> ix(m);
+  DBuf<uint32_t> ix(m), ixs(std::min<uint64_t>(m, kBisectSample));
   DBuf<uint8_t> blab(m);
   DBuf<double> cen(2 * d), sums(2 * d), sse(4), vd(d), yd(d), td(m);
   DBuf<unsigned long long> cnts(2);
@@ -895,17 +897,32 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
     NB_CUDA(cudaMemcpyAsync(ix.p, seg.data(), c * 4, cudaMemcpyHostToDevice, S));
     const unsigned gb = (unsigned)((c + 127) / 128);
     const dim3 gs((unsigned)((d + 127) / 128), 64);
-    auto label_means = [&](const uint8_t* l) {
+    auto label_means = [&](const uint32_t* idx, uint64_t cnt, const uint8_t* l) {
       NB_CUDA(cudaMemsetAsync(sums.p, 0, 2 * d * 8, S));
       NB_CUDA(cudaMemsetAsync(cnts.p, 0, 16, S));
-      k_label_sums<<<gs, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, l, sums.p, cnts.p);
+      k_label_sums<<<gs, 128, 0, S>>>(xr.p, idx, cnt, (uint32_t)d, l, sums.p, cnts.p);
       k_means_from_sums<<<8, 256, 0, S>>>(sums.p, cnts.p, (uint32_t)d, cen.p);
     };
     // mean (cen[0]) and the parent error about it (sse[2..3], labels all 0)
-    label_means(nullptr);
+    label_means(ix.p, c, nullptr);
     NB_CUDA(cudaMemcpyAsync(cen.p + d, cen.p, d * 8, cudaMemcpyDeviceToDevice, S));
     NB_CUDA(cudaMemsetAsync(sse.p, 0, 32, S));
     k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, blab.p, sse.p + 2);
+    // The split direction and centroids come from an evenly strided sample of
+    // at most kBisectSample rows (they shape the partition, never the
+    // certificate); the split itself labels every row.
+    uint64_t cs = c;
+    const uint32_t* is = ix.p;
+    if (c > 2 * kBisectSample) {
+      const uint64_t stride = c / kBisectSample;
+      std::vector<uint32_t> sm;
+      sm.reserve(kBisectSample);
+      for (uint64_t i = 0; i < c && sm.size() < kBisectSample; i += stride) sm.push_back(seg[i]);
+      cs = sm.size();
+      NB_CUDA(cudaMemcpyAsync(ixs.p, sm.data(), cs * 4, cudaMemcpyHostToDevice, S));
+      is = ixs.p;
+    }
+    const unsigned gbs = (unsigned)((cs + 127) / 128);
     // principal direction (5 power steps from a fixed start), cut across it at
     // the middle of the projected range (separates a far fragment at one end
     // as well as two groups of blobs), then two Lloyd steps
@@ -916,14 +933,18 @@ uint64_t subcluster_stage(nomad_b200_ctx* ctx, XPtr x, uint64_t d, const uint32_
       NB_CUDA(cudaMemcpyAsync(yd.p, vh.data(), d * 8, cudaMemcpyHostToDevice, S));
       for (int it = 0; it < 5; ++it) {
         k_normalize<<<1, 256, 0, S>>>(yd.p, (uint32_t)d, vd.p);
-        k_proj_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, vd.p, td.p);
+        k_proj_idx<<<gbs, 128, 0, S>>>(xr.p, is, cs, (uint32_t)d, cen.p, vd.p, td.p);
         NB_CUDA(cudaMemsetAsync(yd.p, 0, d * 8, S));
-        k_backproj_idx<<<gs, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, td.p, yd.p);
+        k_backproj_idx<<<gs, 128, 0, S>>>(xr.p, is, cs, (uint32_t)d, cen.p, td.p, yd.p);
       }
-      k_label_by_midcut<<<1, 1024, 0, S>>>(td.p, c, blab.p);
+      k_label_by_midcut<<<1, 1024, 0, S>>>(td.p, cs, blab.p);
     }
     for (int it = 0; it < 2; ++it) {
-      label_means(blab.p);
+      label_means(is, cs, blab.p);
+      NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
+      k_assign2_idx<<<gbs, 128, 0, S>>>(xr.p, is, cs, (uint32_t)d, cen.p, blab.p, sse.p);
+    }
+    if (is != ix.p) {  // every row against the sample's two centroids
       NB_CUDA(cudaMemsetAsync(sse.p, 0, 16, S));
       k_assign2_idx<<<gb, 128, 0, S>>>(xr.p, ix.p, c, (uint32_t)d, cen.p, blab.p, sse.p);
     }
